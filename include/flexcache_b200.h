@@ -1,0 +1,276 @@
+/*
+ * flexcache_b200.h — C-ABI of the B200-native FlexCache hot path.
+ *
+ * Drop-in boundary for the reference C++ library `lcache`
+ * (/root/reference/proj/include/lcache/*.hpp). The reference exposes only a
+ * C++ API; every entry point below replaces one of its functions (cited as
+ * file:line into /root/reference/proj) and keeps its argument meaning, result
+ * and error behaviour. C++ exceptions become lc_status codes (1:1 with the
+ * reference exception types, errors.hpp:11-42) plus a thread-local message
+ * (lc_last_error). A C++ wrapper with the reference class/function names is
+ * include/lcache_b200/lcache.hpp; the Python mirror is paper_2501_04012_b200.
+ *
+ * Memory: unless stated otherwise, data pointers may be HOST or DEVICE
+ * (cuda pointer attributes are queried); *_dev arguments must be device
+ * memory resident on the context's GPU. All work is issued on the context's
+ * stream; calls returning host-visible results synchronise that stream.
+ *
+ * Layouts (identical to the reference):
+ *   embedding: fp32[dim], unit norm (Embedding, core.hpp:80-102)
+ *   frame:     fp32[H*W*C], channel-minor, index (h*W+w)*C+c (core.hpp:37)
+ *   latent:    [F][H*W*C] (LatentState, core.hpp:62-74); a batch is
+ *              [n][S][F][H*W*C]
+ *   masks:     [F][ceil(H*W/8)] LSB-first packed bits (Bitmap, core.hpp:104-124)
+ *   entry wire bytes: serialize_entry (codec.cpp:358-392)
+ */
+#ifndef FLEXCACHE_B200_H
+#define FLEXCACHE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---------------------------------------------------------------------------
+ * Status codes: one per reference exception type (errors.hpp:11-42).
+ * ------------------------------------------------------------------------- */
+typedef enum lc_status {
+  LC_OK = 0,
+  LC_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument                      */
+  LC_ERR_DEGENERATE_BASE = 2,  /* DegenerateBase   errors.hpp:13             */
+  LC_ERR_STEP_NOT_CACHED = 3,  /* StepNotCached    errors.hpp:17             */
+  LC_ERR_OVERSIZED_ENTRY = 4,  /* OversizedEntry   errors.hpp:22 (see lc_last_oversize) */
+  LC_ERR_SNAPSHOT = 5,         /* SnapshotError    errors.hpp:30             */
+  LC_ERR_LOGIC = 6,            /* std::logic_error (evict_one on empty store, store.cpp:148) */
+  LC_ERR_CUDA = 7,             /* CUDA runtime/driver failure                */
+  LC_ERR_NCCL = 8,             /* reserved: collective failure               */
+  LC_ERR_OOM = 9,              /* device allocation failure                  */
+  LC_ERR_INTERNAL = 10
+} lc_status;
+
+/* Thread-local message of the last failing call on this thread. */
+const char* lc_last_error(void);
+/* OversizedEntry{needed_bytes, capacity_limit} of the last LC_ERR_OVERSIZED_ENTRY. */
+void lc_last_oversize(uint64_t* needed_bytes, uint64_t* capacity_limit);
+const char* lc_version(void);
+
+/* Policy (store.hpp:23). */
+enum { LC_POLICY_FIFO = 0, LC_POLICY_LRU = 1, LC_POLICY_LCBFU = 2, LC_POLICY_LRBU = 3 };
+/* EmbeddingKind (core.hpp:77). */
+enum { LC_KIND_WHOLE = 0, LC_KIND_OBJECT = 1, LC_KIND_BACKGROUND = 2 };
+/* Decision kinds. */
+enum { LC_MISS = 0, LC_WHOLE_HIT = 1, LC_DECOUPLED_HIT = 2 };
+
+/* StepEntry (store.hpp:28-36), flattened; layout shared with the oracle. */
+typedef struct lc_step_entry {
+  uint64_t prompt;
+  int32_t step;
+  int32_t _pad;
+  uint64_t f;
+  uint64_t last_access;
+  uint64_t inserted_at;
+  uint64_t inserted_seq;
+  uint64_t capacity;
+} lc_step_entry;
+
+/* Result of the fused lookup + decide + similarity_to_step path
+ * (no reference code). */
+typedef struct lc_decision {
+  int32_t kind;       /* LC_MISS / LC_WHOLE_HIT / LC_DECOUPLED_HIT          */
+  int32_t step;       /* similarity_to_step(score) for hits, 0 for a miss   */
+  uint64_t whole_id;  /* top-1 of each table (valid if the table is non-empty) */
+  uint64_t object_id;
+  uint64_t background_id;
+  double score;       /* decided score: w (whole) / min(o,b) (decoupled) / max(w, min(o,b)) (miss) */
+  double whole_score, object_score, background_score;
+} lc_decision;
+
+/* ---------------------------------------------------------------------------
+ * Context: one GPU, one stream, scratch arenas.
+ * ------------------------------------------------------------------------- */
+typedef struct lc_ctx lc_ctx;
+lc_status lc_ctx_create(int device, lc_ctx** out);
+lc_status lc_ctx_destroy(lc_ctx* ctx);
+/* Use an external cudaStream_t (e.g. torch's current stream). NULL = own stream. */
+lc_status lc_ctx_set_stream(lc_ctx* ctx, void* cuda_stream);
+void* lc_ctx_stream(lc_ctx* ctx);
+lc_status lc_ctx_synchronize(lc_ctx* ctx);
+/* Number of product kernels launched through this context (instrumentation). */
+uint64_t lc_ctx_launches(lc_ctx* ctx);
+
+/* ---------------------------------------------------------------------------
+ * Core primitives (core.cpp:50-119).
+ * ------------------------------------------------------------------------- */
+/* Embedding ctor normalisation (core.cpp:50-59) of n rows of dim floats:
+ * fp64 sequential sum of squares, (float)(v * (1/sqrt(sq))). Bit-exact. */
+lc_status lc_embedding_normalize(lc_ctx* ctx, const float* v, int64_t n, int dim, float* out);
+/* cosine_similarity (core.cpp:101-114) for n pairs of length len. Bit-exact. */
+lc_status lc_cosine_batch(lc_ctx* ctx, const float* a, const float* b, int64_t n, int64_t len,
+                          double* out);
+
+/* ---------------------------------------------------------------------------
+ * SimilarityIndex (vindex.hpp:23-62): three tables (whole/object/background),
+ * device-resident fp32 master rows + bf16 GEMM copies.
+ * ------------------------------------------------------------------------- */
+typedef struct lc_index lc_index;
+/* dim 0 = fixed by the first insert (vindex.hpp:59). capacity_rows = initial
+ * reservation (grows on demand). */
+lc_status lc_index_create(lc_ctx* ctx, int dim, int64_t capacity_rows, lc_index** out);
+lc_status lc_index_destroy(lc_index* ix);
+/* insert (vindex.cpp:29-48): whole/object/background fp32[dim] unit vectors
+ * (from_unit rule, core.cpp:61-69); duplicate id or dim mismatch =>
+ * LC_ERR_INVALID_ARGUMENT, nothing inserted. */
+lc_status lc_index_insert(lc_index* ix, uint64_t prompt, const float* whole, const float* object,
+                          const float* background, int dim);
+/* Atomic batch insert of n prompts: w/o/b are [n][dim]; all-or-nothing. */
+lc_status lc_index_insert_batch(lc_index* ix, const uint64_t* prompts, const float* whole,
+                                const float* object, const float* background, int64_t n, int dim);
+/* remove (vindex.cpp:76-87): unknown id => LC_ERR_INVALID_ARGUMENT. */
+lc_status lc_index_remove(lc_index* ix, uint64_t prompt);
+lc_status lc_index_contains(lc_index* ix, uint64_t prompt, int32_t* out);
+int64_t lc_index_size(lc_index* ix);
+int lc_index_dim(lc_index* ix);
+/* entries(kind) (vindex.cpp:101-114): ids ascending, rows fp32 (host buffers). */
+lc_status lc_index_export(lc_index* ix, int kind, uint64_t* ids, float* rows, int64_t cap);
+
+/* Top-k by (score desc, id asc) where score = sequential fp64 dot of the
+ * fp32 query with the stored fp32 row (vindex.cpp:58-72); k = 1 is exactly
+ * query_top1 (vindex.cpp:50-74). q is [n][dim]; outputs [n][k] and [n]
+ * (count = min(k, size)). Empty table => counts 0. Results are EXACT:
+ * bf16 tensor-core candidates + fp64 rescore + certified margin, with an
+ * exact fp64 scan for any query the margin cannot certify. */
+lc_status lc_index_query_topk(lc_index* ix, int kind, const float* q, int64_t n, int k,
+                              uint64_t* out_ids, double* out_scores, int32_t* out_counts);
+/* Fused lookup over the three tables + decide + similarity_to_step
+ * (hit threshold defaults.hpp:13, bins defaults.hpp:27).
+ * edges4 = NULL -> defaults. */
+lc_status lc_lookup_decide(lc_index* ix, const float* q_whole, const float* q_object,
+                           const float* q_background, int64_t n, double hit_threshold,
+                           const double* edges4, lc_decision* out);
+/* Tuning / instrumentation of the lookup path. */
+typedef struct lc_lookup_stats {
+  uint64_t queries;       /* (query, table) lookups served               */
+  uint64_t certified;     /* certified by the bf16 margin test            */
+  uint64_t fallback;      /* re-run through the exact fp64 scan           */
+  uint64_t exact_scans;   /* lookups served by the exact scan directly    */
+  double max_abs_err;     /* max |bf16 approx - fp64 exact| seen in rescores */
+} lc_lookup_stats;
+lc_status lc_index_stats(lc_index* ix, lc_lookup_stats* out, int reset);
+/* mode: 0 auto (tensor-core path when size >= 8192), 1 force exact scan,
+ * 2 force tensor-core path. kprime: shortlist length (multiple of 32, <= 128).
+ * eps: certified |bf16 - fp64| score bound (<= 0 -> default 2^-8 + 2^-12). */
+lc_status lc_index_set_lookup(lc_index* ix, int mode, int kprime, double eps);
+/* Shard merge for entry-sharded multi-GPU lookup (a23): merge G per-shard
+ * exact top-k lists [G][n][k] (+counts [G][n]) into the global top-k
+ * by (score desc, id asc). Device or host buffers. */
+lc_status lc_topk_merge(lc_ctx* ctx, const uint64_t* ids, const double* scores,
+                        const int32_t* counts, int G, int64_t n, int k, uint64_t* out_ids,
+                        double* out_scores, int32_t* out_counts);
+/* decide + similarity_to_step on already-computed top-1 triples (used after
+ * the multi-GPU merge). found* may be NULL (all found). */
+lc_status lc_decide_batch(lc_ctx* ctx, const uint64_t* w_ids, const double* w_scores,
+                          const uint64_t* o_ids, const double* o_scores, const uint64_t* b_ids,
+                          const double* b_scores, int64_t n, double hit_threshold,
+                          const double* edges4, lc_decision* out);
+
+/* ---------------------------------------------------------------------------
+ * Latent codec (codec.hpp:69-118) with device-resident entries.
+ * ------------------------------------------------------------------------- */
+typedef struct lc_entry lc_entry;  /* one CompressedEntry living in HBM */
+
+/* select_keyframes (codec.cpp:138-165) for n latents [n][F][E]; map [n][F]. */
+lc_status lc_select_keyframes(lc_ctx* ctx, const float* latents, int64_t n, int F, int H, int W,
+                              int C, double threshold, int32_t* map);
+/* solve_alpha (codec.cpp:181-191) for n pairs of length len; out fp32[n]. */
+lc_status lc_solve_alpha_batch(lc_ctx* ctx, const float* diff_s, const float* diff_base,
+                               int64_t n, int64_t len, float* out);
+/* intra_compress x S + inter_compress (codec.cpp:167-261) for n prompts.
+ * latents [n][S][F][E], steps[S] (host, any order, distinct), masks
+ * [n][F][mb] object + background, prompts[n] (host). On success out[i] owns
+ * a device-resident entry and sizes[i] = compressed_size (codec.cpp:334-338).
+ * On failure no entry is returned. */
+lc_status lc_compress_batch(lc_ctx* ctx, const float* latents, const int32_t* steps, int S,
+                            int F, int H, int W, int C, const uint8_t* obj_masks,
+                            const uint8_t* bg_masks, double threshold, const uint64_t* prompts,
+                            int64_t n, lc_entry** out, uint64_t* sizes);
+/* inter_compress with caller-provided key-frame maps (the IntraCompressed
+ * inputs of codec.hpp:81-82): latents hold at least the key frames. */
+lc_status lc_inter_compress(lc_ctx* ctx, const float* latents, const int32_t* maps,
+                            const int32_t* steps, int S, int F, int H, int W, int C,
+                            const uint8_t* obj_masks, const uint8_t* bg_masks, uint64_t prompt,
+                            lc_entry** out);
+lc_status lc_entry_release(lc_entry* e);
+/* Reference wire bytes (serialize_entry, codec.cpp:358-392); bytes may be
+ * NULL to query the length (== compressed_size). */
+lc_status lc_entry_export(lc_entry* e, uint8_t* bytes, uint64_t cap, uint64_t* len);
+/* deserialize_entry (codec.cpp:394-473) into a device-resident entry. */
+lc_status lc_entry_import(lc_ctx* ctx, const uint8_t* bytes, uint64_t len, lc_entry** out);
+typedef struct lc_entry_info {
+  uint64_t prompt;
+  int32_t base_step, n_steps, F, H, W, C, n_diff;
+  int32_t steps[8];
+  int32_t n_extra[8];
+  uint64_t shared_bytes;        /* entry_shared_bytes  codec.cpp:317-321 */
+  uint64_t private_bytes[8];    /* step_private_bytes  codec.cpp:323-332 */
+  uint64_t compressed_size;     /* codec.cpp:334-338                     */
+} lc_entry_info;
+lc_status lc_entry_get_info(lc_entry* e, lc_entry_info* out);
+/* decompress_step (codec.cpp:263-301) for n (entry, step) pairs into
+ * out_dev [n][F][E] (device). Bit-exact. Unknown step => LC_ERR_STEP_NOT_CACHED. */
+lc_status lc_decompress_batch(lc_ctx* ctx, lc_entry* const* entries, const int32_t* steps,
+                              int64_t n, float* out_dev);
+/* Decoupled hit: decompress the object source and the background source at
+ * the same step and stitch them (stitcher.cpp:7-39) in one pass: each output
+ * pixel is reconstructed only from the source the masks select. */
+lc_status lc_decompress_stitch_batch(lc_ctx* ctx, lc_entry* const* obj_entries,
+                                     lc_entry* const* bg_entries, const int32_t* steps,
+                                     int64_t n, float* out_dev);
+/* stitch (stitcher.cpp:7-39) of n latent pairs already in memory; masks are
+ * the object-source's object masks and the background-source's object masks
+ * (background masks are never read by the reference). */
+lc_status lc_stitch_batch(lc_ctx* ctx, const float* obj, const uint8_t* obj_src_obj_masks,
+                          const float* bg, const uint8_t* bg_src_obj_masks, int64_t n, int F,
+                          int H, int W, int C, float* out);
+
+/* ---------------------------------------------------------------------------
+ * CacheStore (store.hpp:48-120): capacity in compressed_size bytes,
+ * (prompt, step) eviction unit, shared diff blob per prompt.
+ * ------------------------------------------------------------------------- */
+typedef struct lc_store lc_store;
+lc_status lc_store_create(lc_ctx* ctx, uint64_t capacity_limit, int policy, lc_store** out);
+lc_status lc_store_destroy(lc_store* s);
+/* insert_steps (store.cpp:53-91). The store takes its own reference to the
+ * entry (the caller may release its handle). evicted receives up to cap
+ * StepEntry records (n_evicted = total). */
+lc_status lc_store_insert(lc_store* s, uint64_t prompt, lc_entry* entry, const int32_t* steps,
+                          int n_steps, uint64_t now, lc_step_entry* evicted, int cap,
+                          int* n_evicted);
+/* get_step (store.cpp:93-111): actual = served step or 0 (miss); out_dev
+ * (device, [F][E]) may be NULL to only bump f/last_access. */
+lc_status lc_store_get_step(lc_store* s, uint64_t prompt, int desired, uint64_t now,
+                            int32_t* actual, float* out_dev);
+lc_status lc_store_evict_one(lc_store* s, uint64_t now, lc_step_entry* out);
+lc_status lc_store_evict_step(lc_store* s, uint64_t prompt, int step, int32_t* removed);
+uint64_t lc_store_used(lc_store* s);
+uint64_t lc_store_recompute_used(lc_store* s);
+uint64_t lc_store_capacity(lc_store* s);
+int lc_store_policy(lc_store* s);
+int64_t lc_store_step_count(lc_store* s);
+int64_t lc_store_prompt_count(lc_store* s);
+lc_status lc_store_contains(lc_store* s, uint64_t prompt, int32_t* out);
+/* cached_steps (store.cpp:178-184): ascending, up to 5. */
+lc_status lc_store_cached_steps(lc_store* s, uint64_t prompt, int32_t* steps, int* n);
+/* entry_data (store.cpp:192-195): borrowed handle, invalidated by mutation. */
+lc_status lc_store_entry(lc_store* s, uint64_t prompt, lc_entry** out);
+/* entries_snapshot (store.cpp:197-207): (prompt, step) order. */
+lc_status lc_store_entries(lc_store* s, lc_step_entry* out, int64_t cap, int64_t* n);
+/* lrbu_priority / lcbfu_priority (store.cpp:32-42) for n entries. */
+lc_status lc_priority_batch(lc_ctx* ctx, int policy, const lc_step_entry* e, int64_t n,
+                            uint64_t now, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FLEXCACHE_B200_H */

@@ -1,0 +1,196 @@
+// common.cuh — shared host/device plumbing for the FlexCache B200 library:
+// error mapping (reference exception types -> lc_status), the per-GPU
+// context, stream-ordered scratch buffers and host<->device staging for the
+// C-ABI's "host or device pointer" arguments.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "flexcache_b200.h"
+
+namespace fc {
+
+// One exception type carrying the lc_status; thrown inside the library and
+// converted at the C boundary (LC_API_BEGIN/END).
+struct Error : std::runtime_error {
+  lc_status code;
+  Error(lc_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void raise(lc_status c, const std::string& m) { throw Error(c, m); }
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+  if (e != cudaSuccess) {
+    char buf[512];
+    snprintf(buf, sizeof buf, "%s failed at %s:%d: %s", what, file, line, cudaGetErrorString(e));
+    throw Error(e == cudaErrorMemoryAllocation ? LC_ERR_OOM : LC_ERR_CUDA, buf);
+  }
+}
+#define FC_CUDA(x) ::fc::cuda_check((x), #x, __FILE__, __LINE__)
+#define FC_LAUNCH_CHECK() ::fc::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
+
+void set_last_error(const std::string& m);
+void set_last_oversize(uint64_t needed, uint64_t limit);
+
+#define LC_API_BEGIN try {
+#define LC_API_END                                   \
+  }                                                  \
+  catch (const ::fc::Error& e) {                     \
+    ::fc::set_last_error(e.what());                  \
+    return e.code;                                   \
+  }                                                  \
+  catch (const std::bad_alloc& e) {                  \
+    ::fc::set_last_error("host allocation failed");  \
+    return LC_ERR_OOM;                               \
+  }                                                  \
+  catch (const std::exception& e) {                  \
+    ::fc::set_last_error(e.what());                  \
+    return LC_ERR_INTERNAL;                          \
+  }                                                  \
+  return LC_OK;
+
+#define FC_REQUIRE(cond, msg) \
+  do {                        \
+    if (!(cond)) ::fc::raise(LC_ERR_INVALID_ARGUMENT, (msg)); \
+  } while (0)
+
+}  // namespace fc
+
+struct lc_ctx {
+  int device = 0;
+  int sm_count = 148;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::atomic<uint64_t> launches{0};
+};
+
+namespace fc {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) FC_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+inline void count_launch(lc_ctx* ctx, uint64_t n = 1) { ctx->launches.fetch_add(n, std::memory_order_relaxed); }
+
+// Stream-ordered device buffer (cudaMallocAsync / cudaFreeAsync).
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaStream_t s = nullptr;
+  DevBuf() = default;
+  DevBuf(size_t n, cudaStream_t st) : bytes(n), s(st) {
+    if (n) FC_CUDA(cudaMallocAsync(&p, n, st));
+  }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes), s(o.s) { o.p = nullptr; o.bytes = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p; bytes = o.bytes; s = o.s;
+      o.p = nullptr; o.bytes = 0;
+    }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+inline bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// Read-only argument that may live on host or device.
+template <class T>
+struct InArg {
+  const T* dev = nullptr;
+  DevBuf tmp;
+  InArg(lc_ctx* ctx, const T* p, size_t count) {
+    if (!p || count == 0) return;
+    if (is_device_ptr(p)) {
+      dev = p;
+    } else {
+      tmp = DevBuf(count * sizeof(T), ctx->stream);
+      FC_CUDA(cudaMemcpyAsync(tmp.p, p, count * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
+      dev = tmp.as<T>();
+    }
+  }
+};
+
+// Output argument that may live on host or device; finish() copies back.
+template <class T>
+struct OutArg {
+  T* user = nullptr;
+  T* dev = nullptr;
+  size_t count = 0;
+  bool host = false;
+  DevBuf tmp;
+  OutArg(lc_ctx* ctx, T* p, size_t n) : user(p), count(n) {
+    if (!p || n == 0) return;
+    if (is_device_ptr(p)) {
+      dev = p;
+    } else {
+      host = true;
+      tmp = DevBuf(n * sizeof(T), ctx->stream);
+      dev = tmp.as<T>();
+    }
+  }
+  void finish(lc_ctx* ctx) {
+    if (host && count) FC_CUDA(cudaMemcpyAsync(user, dev, count * sizeof(T), cudaMemcpyDeviceToHost, ctx->stream));
+  }
+};
+
+inline unsigned grid_for(int64_t n, int block, int64_t cap = 1 << 30) {
+  int64_t g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return static_cast<unsigned>(g);
+}
+
+inline void sync(lc_ctx* ctx) { FC_CUDA(cudaStreamSynchronize(ctx->stream)); }
+
+}  // namespace fc
+
+// ---------------------------------------------------------------------------
+// Device helpers
+// ---------------------------------------------------------------------------
+namespace fc {
+
+// (score desc, id asc) ordering used by every top-k in the library: the
+// generalisation of query_top1's strict '>' over ascending ids
+// (vindex.cpp:58-72).
+__device__ __forceinline__ bool better(double s1, uint64_t i1, double s2, uint64_t i2) {
+  return s1 > s2 || (s1 == s2 && i1 < i2);
+}
+
+__device__ __forceinline__ double warp_shfl_d(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+
+}  // namespace fc

@@ -1,0 +1,642 @@
+// index.cu — SimilarityIndex (vindex.hpp:23-62) on the GPU.
+//
+// Layout in HBM (per table: whole / object / background):
+//   rows  fp32 [cap][dim]   master copy, bit-identical to the reference rows
+//                           (the exact fp64 scores are computed from these)
+//   rowsb bf16 [cap][dim]   tensor-core operand for the candidate GEMM
+//   ids   u64  [cap]        prompt id of each slot
+// Slots are dense [0, n); remove moves the last slot into the hole (O(dim)
+// instead of the reference's O(n*dim) erase, vindex.cpp:76-87). Row order is
+// irrelevant to results because every top-k orders by (score desc, id asc).
+//
+// Query path (lc_index_query_topk):
+//   size < 8192 or mode 1: exact scan (k_scan_partial + k_scan_merge) — the
+//     reference's sequential fp64 dot (vindex.cpp:66-67) for every row.
+//   otherwise: tcgen05 bf16 GEMM with a fused per-query top-K' shortlist
+//     (lookup_sm100.cu) -> shortlist merge -> exact fp64 rescore of the
+//     K' candidates (k_rescore) -> certification: every row outside the
+//     shortlist has bf16 score <= m (the K'-th shortlisted bf16 score), so its
+//     exact score is <= m + eps; if m + eps < T_k (the k-th exact score) the
+//     answer is provably the exact top-k. Queries that fail the test are
+//     re-run through the exact scan. Results are therefore always identical
+//     to the reference's.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <shared_mutex>
+#include <unordered_map>
+
+#include "common.cuh"
+#include "lookup.cuh"
+#include "topk.cuh"
+
+using namespace fc;
+
+struct lc_index {
+  lc_ctx* ctx = nullptr;
+  int dim = 0;
+  int64_t n = 0, cap = 0;
+  float* rows[3] = {nullptr, nullptr, nullptr};
+  __nv_bfloat16* rowsb[3] = {nullptr, nullptr, nullptr};
+  uint64_t* ids_dev = nullptr;
+  std::vector<uint64_t> ids;
+  std::unordered_map<uint64_t, int64_t> slot;
+  int mode = 0;
+  int kprime = 64;
+  double eps = 0.00390625 + 0.000244140625;  // 2^-8 + 2^-12, see lookup.cuh
+  lc_lookup_stats stats{};
+  ApproxPlan plan[3];
+  mutable std::shared_mutex mu;  // readers: queries; writer: insert/remove (vindex.hpp:61)
+};
+
+namespace fc {
+
+// from_unit rule (core.cpp:61-69) on device rows: finite and
+// |sqrt(sum v^2) - 1| <= 1e-6 with a sequential fp64 sum.
+__global__ void k_check_unit(const float* __restrict__ v, int64_t n, int dim, int* __restrict__ bad) {
+  int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const float* x = v + r * dim;
+  double sq = 0.0;
+  bool ok = true;
+  for (int i = 0; i < dim; ++i) {
+    ok &= isfinite(x[i]);
+    const double t = x[i];
+    sq = fma(t, t, sq);
+  }
+  if (!ok || fabs(sqrt(sq) - 1.0) > 1e-6) atomicExch(bad, 1);
+}
+
+__global__ void k_to_bf16(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst, int64_t count) {
+  int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4;
+  if (i + 3 < count) {
+    float4 v = *reinterpret_cast<const float4*>(src + i);
+    __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+    *reinterpret_cast<__nv_bfloat162*>(dst + i) = a;
+    *reinterpret_cast<__nv_bfloat162*>(dst + i + 2) = b;
+  } else {
+    for (; i < count; ++i) dst[i] = __float2bfloat16_rn(src[i]);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Exact scan: one thread per table row, QB queries per block (in smem); each
+// (query,row) score is the reference's sequential fp64 dot, d = 0..dim-1.
+// Per block and query the top-k of its 128 rows goes to a partial list.
+// ---------------------------------------------------------------------------
+constexpr int SCAN_T = 128;
+constexpr int SCAN_QB = 8;
+
+__global__ void __launch_bounds__(SCAN_T) k_scan_partial(const float* __restrict__ Q, const int32_t* __restrict__ qlist,
+                                                         int nq, const float* __restrict__ rows,
+                                                         const uint64_t* __restrict__ ids, int64_t n_rows, int dim,
+                                                         int k, Cand* __restrict__ partial, int32_t* __restrict__ pcount) {
+  extern __shared__ float s_q[];  // [SCAN_QB][dim]
+  __shared__ Cand s_c[SCAN_T / 32];
+  __shared__ int s_o[SCAN_T / 32];
+  __shared__ Cand s_out[64];
+  const int q0 = blockIdx.y * SCAN_QB;
+  const int qn = min(SCAN_QB, nq - q0);
+  for (int i = threadIdx.x; i < qn * dim; i += SCAN_T) {
+    const int qq = i / dim, d = i - qq * dim;
+    const int qi = qlist ? qlist[q0 + qq] : q0 + qq;
+    s_q[qq * dim + d] = Q[(int64_t)qi * dim + d];
+  }
+  __syncthreads();
+  const int64_t r = blockIdx.x * (int64_t)SCAN_T + threadIdx.x;
+  double acc[SCAN_QB];
+#pragma unroll
+  for (int j = 0; j < SCAN_QB; ++j) acc[j] = 0.0;
+  if (r < n_rows) {
+    const float* x = rows + r * dim;
+    if ((dim & 3) == 0) {
+      for (int d = 0; d < dim; d += 4) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(x + d));
+#pragma unroll
+        for (int j = 0; j < SCAN_QB; ++j) {
+          if (j < qn) {
+            const float* qq = s_q + j * dim + d;
+            acc[j] = fma((double)qq[0], (double)v.x, acc[j]);
+            acc[j] = fma((double)qq[1], (double)v.y, acc[j]);
+            acc[j] = fma((double)qq[2], (double)v.z, acc[j]);
+            acc[j] = fma((double)qq[3], (double)v.w, acc[j]);
+          }
+        }
+      }
+    } else {
+      for (int d = 0; d < dim; ++d) {
+        const double v = x[d];
+#pragma unroll
+        for (int j = 0; j < SCAN_QB; ++j)
+          if (j < qn) acc[j] = fma((double)s_q[j * dim + d], v, acc[j]);
+      }
+    }
+  }
+  const uint64_t myid = r < n_rows ? ids[r] : 0;
+  for (int j = 0; j < qn; ++j) {
+    Cand L[1];
+    int ln = 0;
+    if (r < n_rows) {
+      L[0].s = acc[j];
+      L[0].id = myid;
+      L[0].slot = r;
+      ln = 1;
+    }
+    const int got = block_merge_lists<1>(L, ln, k, s_out, s_c, s_o);
+    const int64_t base = ((int64_t)(q0 + j) * gridDim.x + blockIdx.x);
+    for (int t = threadIdx.x; t < got; t += SCAN_T) partial[base * k + t] = s_out[t];
+    if (threadIdx.x == 0) pcount[base] = got;
+    __syncthreads();
+  }
+}
+
+template <int KMAX>
+__global__ void __launch_bounds__(256) k_scan_merge(const Cand* __restrict__ partial, const int32_t* __restrict__ pcount,
+                                                    int nblk, int k, const int32_t* __restrict__ qlist,
+                                                    uint64_t* __restrict__ out_ids, double* __restrict__ out_sc,
+                                                    int32_t* __restrict__ out_cnt) {
+  __shared__ Cand s_c[8];
+  __shared__ int s_o[8];
+  __shared__ Cand s_out[KMAX];
+  const int q = blockIdx.x;
+  Cand L[KMAX];
+  int ln = 0;
+  for (int b = threadIdx.x; b < nblk; b += blockDim.x) {
+    const int64_t base = (int64_t)q * nblk + b;
+    const int c = pcount[base];
+    for (int t = 0; t < c; ++t) local_insert<KMAX>(L, ln, k, partial[base * k + t]);
+  }
+  const int got = block_merge_lists<KMAX>(L, ln, k, s_out, s_c, s_o);
+  const int qo = qlist ? qlist[q] : q;
+  for (int t = threadIdx.x; t < k; t += blockDim.x) {
+    out_ids[(int64_t)qo * k + t] = t < got ? s_out[t].id : 0;
+    out_sc[(int64_t)qo * k + t] = t < got ? s_out[t].s : 0.0;
+  }
+  if (threadIdx.x == 0) out_cnt[qo] = got;
+}
+
+// ---------------------------------------------------------------------------
+// Exact rescore of the bf16 shortlist + certification (one warp per query).
+// ---------------------------------------------------------------------------
+constexpr int RS_WARPS = 8;
+
+template <int PER_LANE>
+__global__ void __launch_bounds__(RS_WARPS * 32)
+    k_rescore(const float* __restrict__ Q, int nq, int dim, const float* __restrict__ rows,
+              const uint64_t* __restrict__ ids, const float* __restrict__ cand_s, const uint32_t* __restrict__ cand_r,
+              const int32_t* __restrict__ cand_n, int kp, int k, double eps, uint64_t* __restrict__ out_ids,
+              double* __restrict__ out_sc, int32_t* __restrict__ out_cnt, int32_t* __restrict__ fail_list,
+              int32_t* __restrict__ fail_n, unsigned long long* __restrict__ max_err_bits) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q = blockIdx.x * RS_WARPS + warp;
+  if (q >= nq) return;
+  const float* qv = Q + (int64_t)q * dim;
+  const int cn = cand_n[q];
+  Cand mine[PER_LANE];
+  int mn = 0;
+  float min_approx = INFINITY;
+  double local_err = 0.0;
+#pragma unroll
+  for (int t = 0; t < PER_LANE; ++t) {
+    const int c = lane + 32 * t;
+    if (c < cn) {
+      const uint32_t r = cand_r[(int64_t)q * kp + c];
+      const float a = cand_s[(int64_t)q * kp + c];
+      min_approx = fminf(min_approx, a);
+      const float* x = rows + (int64_t)r * dim;
+      double acc = 0.0;
+      for (int d = 0; d < dim; ++d) acc = fma((double)__ldg(qv + d), (double)__ldg(x + d), acc);
+      local_err = fmax(local_err, fabs(acc - (double)a));
+      Cand cc;
+      cc.s = acc;
+      cc.id = ids[r];
+      cc.slot = r;
+      local_insert<PER_LANE>(mine, mn, PER_LANE, cc);
+    }
+  }
+  // warp-wide min of the shortlisted approx scores (the K'-th best approx)
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    min_approx = fminf(min_approx, __shfl_xor_sync(0xffffffffu, min_approx, off));
+    local_err = fmax(local_err, __shfl_xor_sync(0xffffffffu, local_err, off));
+  }
+  if (lane == 0 && local_err > 0) atomicMax(max_err_bits, (unsigned long long)__double_as_longlong(local_err));
+  // k rounds of warp argmax over the per-lane sorted lists
+  int ptr = 0, got = 0;
+  double tk = 0.0;
+  for (int rnd = 0; rnd < k; ++rnd) {
+    Cand c;
+    int owner;
+    if (ptr < mn) {
+      c = mine[ptr];
+      owner = lane;
+    } else {
+      c.s = 0; c.id = 0; c.slot = -1;
+      owner = -1;
+    }
+    warp_argbest(c, owner);
+    if (owner < 0) break;
+    if (lane == owner) ++ptr;
+    if (lane == 0) {
+      out_ids[(int64_t)q * k + rnd] = c.id;
+      out_sc[(int64_t)q * k + rnd] = c.s;
+    }
+    tk = c.s;
+    ++got;
+  }
+  if (lane == 0) {
+    for (int j = got; j < k; ++j) {
+      out_ids[(int64_t)q * k + j] = 0;
+      out_sc[(int64_t)q * k + j] = 0.0;
+    }
+    out_cnt[q] = got;
+    // Certification: rows outside the shortlist have approx <= min_approx.
+    // A shortlist shorter than K' holds every row of the table.
+    const bool full = cn >= kp;
+    const bool ok = !full || (got >= k && (double)min_approx + eps < tk);
+    if (!ok) fail_list[atomicAdd(fail_n, 1)] = q;
+  }
+}
+
+}  // namespace fc
+
+// ---------------------------------------------------------------------------
+// host helpers
+// ---------------------------------------------------------------------------
+namespace {
+
+void ensure_capacity(lc_index* ix, int64_t need) {
+  if (need <= ix->cap) return;
+  int64_t nc = std::max<int64_t>(need, std::max<int64_t>(1024, ix->cap * 2));
+  lc_ctx* ctx = ix->ctx;
+  for (int t = 0; t < 3; ++t) {
+    float* nr = nullptr;
+    __nv_bfloat16* nb = nullptr;
+    FC_CUDA(cudaMalloc(&nr, (size_t)nc * ix->dim * sizeof(float)));
+    FC_CUDA(cudaMalloc(&nb, (size_t)nc * ix->dim * sizeof(__nv_bfloat16)));
+    if (ix->n) {
+      FC_CUDA(cudaMemcpyAsync(nr, ix->rows[t], (size_t)ix->n * ix->dim * sizeof(float), cudaMemcpyDeviceToDevice, ctx->stream));
+      FC_CUDA(cudaMemcpyAsync(nb, ix->rowsb[t], (size_t)ix->n * ix->dim * sizeof(__nv_bfloat16), cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    FC_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (ix->rows[t]) cudaFree(ix->rows[t]);
+    if (ix->rowsb[t]) cudaFree(ix->rowsb[t]);
+    ix->rows[t] = nr;
+    ix->rowsb[t] = nb;
+    ix->plan[t].valid = false;
+  }
+  uint64_t* ni = nullptr;
+  FC_CUDA(cudaMalloc(&ni, (size_t)nc * sizeof(uint64_t)));
+  if (ix->n) FC_CUDA(cudaMemcpyAsync(ni, ix->ids_dev, (size_t)ix->n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, ctx->stream));
+  FC_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (ix->ids_dev) cudaFree(ix->ids_dev);
+  ix->ids_dev = ni;
+  ix->cap = nc;
+}
+
+void check_units_device(lc_ctx* ctx, const float* dev, int64_t n, int dim) {
+  DevBuf bad(sizeof(int), ctx->stream);
+  FC_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), ctx->stream));
+  k_check_unit<<<grid_for(n, 128), 128, 0, ctx->stream>>>(dev, n, dim, bad.as<int>());
+  FC_LAUNCH_CHECK();
+  count_launch(ctx);
+  int hb = 0;
+  FC_CUDA(cudaMemcpyAsync(&hb, bad.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  sync(ctx);
+  if (hb) raise(LC_ERR_INVALID_ARGUMENT, "Embedding: vector is not unit norm");
+}
+
+// Exact top-k of queries (all, or the subset qlist) by full fp64 scan.
+void exact_scan(lc_index* ix, int kind, const float* Qdev, const int32_t* qlist_dev, int nq, int k, uint64_t* oid,
+                double* osc, int32_t* ocnt) {
+  lc_ctx* ctx = ix->ctx;
+  if (nq <= 0) return;
+  const int dim = ix->dim;
+  const int nblk = (int)((ix->n + SCAN_T - 1) / SCAN_T);
+  // bound the partial-list scratch to ~256 MB per pass
+  const int64_t per_q = (int64_t)nblk * k * sizeof(Cand);
+  const int chunk = (int)std::max<int64_t>(SCAN_QB, std::min<int64_t>(nq, ((256ll << 20) / per_q) / SCAN_QB * SCAN_QB));
+  if (chunk < nq) {
+    for (int q0 = 0; q0 < nq; q0 += chunk) {
+      const int cn = std::min(chunk, nq - q0);
+      if (qlist_dev) {
+        exact_scan(ix, kind, Qdev, qlist_dev + q0, cn, k, oid, osc, ocnt);
+      } else {
+        DevBuf ql((size_t)cn * sizeof(int32_t), ctx->stream);
+        std::vector<int32_t> h(cn);
+        for (int i = 0; i < cn; ++i) h[i] = q0 + i;
+        FC_CUDA(cudaMemcpyAsync(ql.p, h.data(), cn * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
+        exact_scan(ix, kind, Qdev, ql.as<int32_t>(), cn, k, oid, osc, ocnt);
+        sync(ctx);
+      }
+    }
+    return;
+  }
+  DevBuf partial((size_t)nq * nblk * k * sizeof(Cand), ctx->stream);
+  DevBuf pcount((size_t)nq * nblk * sizeof(int32_t), ctx->stream);
+  const size_t smem = (size_t)SCAN_QB * dim * sizeof(float);
+  if (smem > 48 * 1024) FC_CUDA(cudaFuncSetAttribute(k_scan_partial, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  dim3 grid(nblk, (nq + SCAN_QB - 1) / SCAN_QB);
+  k_scan_partial<<<grid, SCAN_T, smem, ctx->stream>>>(Qdev, qlist_dev, nq, ix->rows[kind], ix->ids_dev, ix->n, dim, k,
+                                                      partial.as<Cand>(), pcount.as<int32_t>());
+  FC_LAUNCH_CHECK();
+  if (k <= 8)
+    k_scan_merge<8><<<nq, 256, 0, ctx->stream>>>(partial.as<Cand>(), pcount.as<int32_t>(), nblk, k, qlist_dev, oid, osc, ocnt);
+  else
+    k_scan_merge<64><<<nq, 256, 0, ctx->stream>>>(partial.as<Cand>(), pcount.as<int32_t>(), nblk, k, qlist_dev, oid, osc, ocnt);
+  FC_LAUNCH_CHECK();
+  count_launch(ctx, 2);
+}
+
+// Device-resident top-k (no host sync unless a fallback is needed).
+void query_dev(lc_index* ix, int kind, const float* Qdev, int nq, int k, uint64_t* oid, double* osc, int32_t* ocnt) {
+  lc_ctx* ctx = ix->ctx;
+  ix->stats.queries += nq;
+  const bool approx_ok = approx_available() && ix->dim % 64 == 0 && ix->dim <= 1024 && k <= ix->kprime;
+  const bool use_approx = approx_ok && (ix->mode == 2 || (ix->mode == 0 && ix->n >= 8192));
+  if (!use_approx) {
+    FC_REQUIRE(ix->mode != 2 || approx_ok, "lc_index_query_topk: tensor-core path unavailable for this shape");
+    exact_scan(ix, kind, Qdev, nullptr, nq, k, oid, osc, ocnt);
+    ix->stats.exact_scans += nq;
+    return;
+  }
+  const int kp = ix->kprime;
+  DevBuf cs((size_t)nq * kp * sizeof(float), ctx->stream);
+  DevBuf cr((size_t)nq * kp * sizeof(uint32_t), ctx->stream);
+  DevBuf cn((size_t)nq * sizeof(int32_t), ctx->stream);
+  if (!ix->plan[kind].valid || ix->plan[kind].n_rows != ix->n)
+    approx_plan(ix->plan[kind], ix->rowsb[kind], ix->n, ix->dim, ctx->sm_count);
+  approx_shortlist(ctx, ix->plan[kind], Qdev, nq, kp, cs.as<float>(), cr.as<uint32_t>(), cn.as<int32_t>());
+  DevBuf fl((size_t)nq * sizeof(int32_t), ctx->stream);
+  DevBuf fn(16, ctx->stream);  // [0,4) fail count, [8,16) max |err| bits
+  int32_t* fail_n = fn.as<int32_t>();
+  auto* err_bits = reinterpret_cast<unsigned long long*>(fn.as<char>() + 8);
+  FC_CUDA(cudaMemsetAsync(fn.p, 0, 16, ctx->stream));
+  const unsigned g = (unsigned)((nq + RS_WARPS - 1) / RS_WARPS);
+  if (kp <= 32)
+    k_rescore<1><<<g, RS_WARPS * 32, 0, ctx->stream>>>(Qdev, nq, ix->dim, ix->rows[kind], ix->ids_dev, cs.as<float>(),
+                                                       cr.as<uint32_t>(), cn.as<int32_t>(), kp, k, ix->eps, oid, osc, ocnt,
+                                                       fl.as<int32_t>(), fail_n, err_bits);
+  else if (kp <= 64)
+    k_rescore<2><<<g, RS_WARPS * 32, 0, ctx->stream>>>(Qdev, nq, ix->dim, ix->rows[kind], ix->ids_dev, cs.as<float>(),
+                                                       cr.as<uint32_t>(), cn.as<int32_t>(), kp, k, ix->eps, oid, osc, ocnt,
+                                                       fl.as<int32_t>(), fail_n, err_bits);
+  else
+    k_rescore<4><<<g, RS_WARPS * 32, 0, ctx->stream>>>(Qdev, nq, ix->dim, ix->rows[kind], ix->ids_dev, cs.as<float>(),
+                                                       cr.as<uint32_t>(), cn.as<int32_t>(), kp, k, ix->eps, oid, osc, ocnt,
+                                                       fl.as<int32_t>(), fail_n, err_bits);
+  FC_LAUNCH_CHECK();
+  count_launch(ctx);
+  int32_t hf[4] = {0, 0, 0, 0};
+  FC_CUDA(cudaMemcpyAsync(hf, fn.p, 16, cudaMemcpyDeviceToHost, ctx->stream));
+  sync(ctx);
+  double err = 0.0;
+  uint64_t eb = (uint64_t)(uint32_t)hf[2] | ((uint64_t)(uint32_t)hf[3] << 32);
+  memcpy(&err, &eb, 8);
+  ix->stats.max_abs_err = std::max(ix->stats.max_abs_err, err);
+  const int nf = hf[0];
+  ix->stats.certified += nq - nf;
+  ix->stats.fallback += nf;
+  if (nf > 0) exact_scan(ix, kind, Qdev, fl.as<int32_t>(), nf, k, oid, osc, ocnt);
+}
+
+}  // namespace
+
+extern "C" {
+
+lc_status lc_index_create(lc_ctx* ctx, int dim, int64_t capacity_rows, lc_index** out) {
+  LC_API_BEGIN
+  FC_REQUIRE(ctx && out, "lc_index_create: null argument");
+  FC_REQUIRE(dim >= 0, "lc_index_create: negative dim");
+  DeviceGuard g(ctx->device);
+  auto* ix = new lc_index();
+  ix->ctx = ctx;
+  ix->dim = dim;
+  if (dim > 0 && capacity_rows > 0) {
+    try {
+      ensure_capacity(ix, capacity_rows);
+    } catch (...) {
+      delete ix;
+      throw;
+    }
+  }
+  *out = ix;
+  LC_API_END
+}
+
+lc_status lc_index_destroy(lc_index* ix) {
+  LC_API_BEGIN
+  if (!ix) return LC_OK;
+  DeviceGuard g(ix->ctx->device);
+  cudaStreamSynchronize(ix->ctx->stream);
+  for (int t = 0; t < 3; ++t) {
+    if (ix->rows[t]) cudaFree(ix->rows[t]);
+    if (ix->rowsb[t]) cudaFree(ix->rowsb[t]);
+  }
+  if (ix->ids_dev) cudaFree(ix->ids_dev);
+  delete ix;
+  LC_API_END
+}
+
+lc_status lc_index_insert_batch(lc_index* ix, const uint64_t* prompts, const float* w, const float* o, const float* b,
+                                int64_t n, int dim) {
+  LC_API_BEGIN
+  FC_REQUIRE(ix && prompts && w && o && b, "lc_index_insert_batch: null argument");
+  if (n <= 0) return LC_OK;
+  std::unique_lock lock(ix->mu);
+  lc_ctx* ctx = ix->ctx;
+  DeviceGuard g(ctx->device);
+  FC_REQUIRE(dim > 0, "Embedding: empty vector");
+  if (ix->dim != 0 && dim != ix->dim) raise(LC_ERR_INVALID_ARGUMENT, "SimilarityIndex: embedding dimension mismatch");
+  std::vector<uint64_t> pid(n);
+  if (is_device_ptr(prompts)) {
+    FC_CUDA(cudaMemcpy(pid.data(), prompts, n * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  } else {
+    memcpy(pid.data(), prompts, n * sizeof(uint64_t));
+  }
+  {
+    std::vector<uint64_t> sorted(pid);
+    std::sort(sorted.begin(), sorted.end());
+    for (int64_t i = 0; i < n; ++i) {
+      if ((i > 0 && sorted[i] == sorted[i - 1]) || ix->slot.count(sorted[i]))
+        raise(LC_ERR_INVALID_ARGUMENT, "SimilarityIndex: duplicate prompt id");
+    }
+  }
+  const float* src[3] = {w, o, b};
+  InArg<float> a0(ctx, w, (size_t)n * dim), a1(ctx, o, (size_t)n * dim), a2(ctx, b, (size_t)n * dim);
+  const float* dsrc[3] = {a0.dev, a1.dev, a2.dev};
+  (void)src;
+  for (int t = 0; t < 3; ++t) check_units_device(ctx, dsrc[t], n, dim);
+  if (ix->dim == 0) ix->dim = dim;
+  ensure_capacity(ix, ix->n + n);
+  for (int t = 0; t < 3; ++t) {
+    float* dst = ix->rows[t] + (size_t)ix->n * dim;
+    FC_CUDA(cudaMemcpyAsync(dst, dsrc[t], (size_t)n * dim * sizeof(float), cudaMemcpyDeviceToDevice, ctx->stream));
+    const int64_t cnt = (int64_t)n * dim;
+    k_to_bf16<<<grid_for((cnt + 3) / 4, 256), 256, 0, ctx->stream>>>(dst, ix->rowsb[t] + (size_t)ix->n * dim, cnt);
+    FC_LAUNCH_CHECK();
+    count_launch(ctx);
+    ix->plan[t].valid = false;
+  }
+  FC_CUDA(cudaMemcpyAsync(ix->ids_dev + ix->n, pid.data(), n * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
+  for (int64_t i = 0; i < n; ++i) {
+    ix->slot[pid[i]] = ix->n + i;
+    ix->ids.push_back(pid[i]);
+  }
+  ix->n += n;
+  sync(ctx);
+  LC_API_END
+}
+
+lc_status lc_index_insert(lc_index* ix, uint64_t prompt, const float* w, const float* o, const float* b, int dim) {
+  return lc_index_insert_batch(ix, &prompt, w, o, b, 1, dim);
+}
+
+lc_status lc_index_remove(lc_index* ix, uint64_t prompt) {
+  LC_API_BEGIN
+  std::unique_lock lock(ix->mu);
+  lc_ctx* ctx = ix->ctx;
+  DeviceGuard g(ctx->device);
+  auto it = ix->slot.find(prompt);
+  if (it == ix->slot.end()) raise(LC_ERR_INVALID_ARGUMENT, "SimilarityIndex: unknown prompt id");
+  const int64_t s = it->second, last = ix->n - 1;
+  const int dim = ix->dim;
+  if (s != last) {
+    for (int t = 0; t < 3; ++t) {
+      FC_CUDA(cudaMemcpyAsync(ix->rows[t] + (size_t)s * dim, ix->rows[t] + (size_t)last * dim, dim * sizeof(float),
+                              cudaMemcpyDeviceToDevice, ctx->stream));
+      FC_CUDA(cudaMemcpyAsync(ix->rowsb[t] + (size_t)s * dim, ix->rowsb[t] + (size_t)last * dim,
+                              dim * sizeof(__nv_bfloat16), cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    FC_CUDA(cudaMemcpyAsync(ix->ids_dev + s, ix->ids_dev + last, sizeof(uint64_t), cudaMemcpyDeviceToDevice, ctx->stream));
+    const uint64_t moved = ix->ids[last];
+    ix->ids[s] = moved;
+    ix->slot[moved] = s;
+  }
+  ix->ids.pop_back();
+  ix->slot.erase(it);
+  ix->n -= 1;
+  for (int t = 0; t < 3; ++t) ix->plan[t].valid = false;
+  sync(ctx);
+  LC_API_END
+}
+
+lc_status lc_index_contains(lc_index* ix, uint64_t prompt, int32_t* out) {
+  LC_API_BEGIN
+  std::shared_lock lock(ix->mu);
+  *out = ix->slot.count(prompt) ? 1 : 0;
+  LC_API_END
+}
+
+int64_t lc_index_size(lc_index* ix) {
+  std::shared_lock lock(ix->mu);
+  return ix->n;
+}
+
+int lc_index_dim(lc_index* ix) { return ix->dim; }
+
+lc_status lc_index_export(lc_index* ix, int kind, uint64_t* ids, float* rows, int64_t cap) {
+  LC_API_BEGIN
+  FC_REQUIRE(kind >= 0 && kind <= 2, "bad embedding kind");
+  std::shared_lock lock(ix->mu);
+  lc_ctx* ctx = ix->ctx;
+  DeviceGuard g(ctx->device);
+  FC_REQUIRE(cap >= ix->n, "lc_index_export: buffer too small");
+  std::vector<int64_t> order(ix->n);
+  for (int64_t i = 0; i < ix->n; ++i) order[i] = i;
+  std::sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return ix->ids[a] < ix->ids[b]; });
+  std::vector<float> all((size_t)ix->n * ix->dim);
+  if (ix->n) FC_CUDA(cudaMemcpy(all.data(), ix->rows[kind], all.size() * sizeof(float), cudaMemcpyDeviceToHost));
+  for (int64_t i = 0; i < ix->n; ++i) {
+    if (ids) ids[i] = ix->ids[order[i]];
+    if (rows) memcpy(rows + (size_t)i * ix->dim, all.data() + (size_t)order[i] * ix->dim, ix->dim * sizeof(float));
+  }
+  LC_API_END
+}
+
+lc_status lc_index_set_lookup(lc_index* ix, int mode, int kprime, double eps) {
+  LC_API_BEGIN
+  FC_REQUIRE(mode >= 0 && mode <= 2, "mode must be 0, 1 or 2");
+  FC_REQUIRE(kprime == 0 || (kprime >= 32 && kprime <= 128 && kprime % 32 == 0), "kprime: multiple of 32 in [32,128]");
+  std::unique_lock lock(ix->mu);
+  ix->mode = mode;
+  if (kprime) ix->kprime = kprime;
+  if (eps > 0) ix->eps = eps;
+  LC_API_END
+}
+
+lc_status lc_index_stats(lc_index* ix, lc_lookup_stats* out, int reset) {
+  LC_API_BEGIN
+  std::unique_lock lock(ix->mu);
+  if (out) *out = ix->stats;
+  if (reset) ix->stats = lc_lookup_stats{};
+  LC_API_END
+}
+
+lc_status lc_index_query_topk(lc_index* ix, int kind, const float* q, int64_t n, int k, uint64_t* out_ids,
+                              double* out_scores, int32_t* out_counts) {
+  LC_API_BEGIN
+  FC_REQUIRE(kind >= 0 && kind <= 2, "bad embedding kind");
+  FC_REQUIRE(k >= 1 && k <= 64, "k must be in [1, 64]");
+  FC_REQUIRE(n >= 0 && n < (1ll << 31), "bad query count");
+  std::shared_lock lock(ix->mu);
+  lc_ctx* ctx = ix->ctx;
+  DeviceGuard g(ctx->device);
+  if (n == 0) return LC_OK;
+  OutArg<uint64_t> oi(ctx, out_ids, (size_t)n * k);
+  OutArg<double> os(ctx, out_scores, (size_t)n * k);
+  OutArg<int32_t> oc(ctx, out_counts, (size_t)n);
+  if (ix->n == 0) {  // empty table => nullopt (vindex.cpp:54)
+    FC_CUDA(cudaMemsetAsync(oi.dev, 0, (size_t)n * k * sizeof(uint64_t), ctx->stream));
+    FC_CUDA(cudaMemsetAsync(os.dev, 0, (size_t)n * k * sizeof(double), ctx->stream));
+    FC_CUDA(cudaMemsetAsync(oc.dev, 0, (size_t)n * sizeof(int32_t), ctx->stream));
+  } else {
+    InArg<float> qa(ctx, q, (size_t)n * ix->dim);
+    query_dev(ix, kind, qa.dev, (int)n, k, oi.dev, os.dev, oc.dev);
+  }
+  oi.finish(ctx);
+  os.finish(ctx);
+  oc.finish(ctx);
+  sync(ctx);
+  LC_API_END
+}
+
+lc_status lc_lookup_decide(lc_index* ix, const float* qw, const float* qo, const float* qb, int64_t n, double thr,
+                           const double* edges4, lc_decision* out) {
+  LC_API_BEGIN
+  FC_REQUIRE(n >= 0 && n < (1ll << 31), "bad query count");
+  if (n == 0) return LC_OK;
+  lc_ctx* ctx = ix->ctx;
+  DeviceGuard g(ctx->device);
+  std::shared_lock lock(ix->mu);
+  const double def[4] = {0.72, 0.79, 0.86, 0.93};
+  const double* e = edges4 ? edges4 : def;
+  DevBuf ids(3 * (size_t)n * sizeof(uint64_t), ctx->stream), sc(3 * (size_t)n * sizeof(double), ctx->stream),
+      cnt(3 * (size_t)n * sizeof(int32_t), ctx->stream);
+  OutArg<lc_decision> o(ctx, out, (size_t)n);
+  if (ix->n == 0) {
+    FC_CUDA(cudaMemsetAsync(ids.p, 0, ids.bytes, ctx->stream));
+    FC_CUDA(cudaMemsetAsync(sc.p, 0, sc.bytes, ctx->stream));
+    FC_CUDA(cudaMemsetAsync(cnt.p, 0, cnt.bytes, ctx->stream));
+  } else {
+    const float* qs[3] = {qw, qo, qb};
+    for (int t = 0; t < 3; ++t) {
+      InArg<float> qa(ctx, qs[t], (size_t)n * ix->dim);
+      query_dev(ix, t, qa.dev, (int)n, 1, ids.as<uint64_t>() + t * n, sc.as<double>() + t * n, cnt.as<int32_t>() + t * n);
+    }
+  }
+  k_decide<<<grid_for(n, 128), 128, 0, ctx->stream>>>(ids.as<uint64_t>(), sc.as<double>(), ids.as<uint64_t>() + n,
+                                                      sc.as<double>() + n, ids.as<uint64_t>() + 2 * n,
+                                                      sc.as<double>() + 2 * n, cnt.as<int32_t>(), n, thr, e[0], e[1],
+                                                      e[2], e[3], o.dev);
+  FC_LAUNCH_CHECK();
+  count_launch(ctx);
+  o.finish(ctx);
+  sync(ctx);
+  LC_API_END
+}
+
+}  // extern "C"

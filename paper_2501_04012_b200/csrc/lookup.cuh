@@ -1,0 +1,39 @@
+// lookup.cuh — interface of the tcgen05 candidate stage (lookup_sm100.cu).
+//
+// Error model behind the certification in index.cu: queries and rows are
+// unit vectors (from_unit, core.cpp:61-69). Rounding each operand to bf16
+// (unit roundoff 2^-9) perturbs each product q_i*x_i by at most
+// |q_i x_i|(2^-8 + 2^-18), i.e. the dot by <= (2^-8 + 2^-18) * sum|q_i x_i|
+// <= 2^-8 + 2^-18 (Cauchy-Schwarz). fp32 accumulation of dim <= 1024 terms
+// adds <= 1024 * 2^-23 * sum|q_i x_i| ~ 1.2e-4. The default certified bound
+// eps = 2^-8 + 2^-12 = 0.0041 covers both; the measured maximum is reported
+// in lc_lookup_stats.max_abs_err.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+
+namespace fc {
+
+struct ApproxPlan {
+  bool valid = false;
+  int64_t n_rows = 0;
+  int dim = 0;
+  int bn = 64;
+  const __nv_bfloat16* rows = nullptr;
+  alignas(64) CUtensorMap tmap;
+};
+
+bool approx_available();
+void approx_plan(ApproxPlan& p, const __nv_bfloat16* rows_bf16, int64_t n_rows, int dim, int sm_count);
+// Shortlist: for each query the kp rows with the largest bf16 scores
+// (cand_s approx score, cand_r row slot, cand_n count <= kp).
+void approx_shortlist(lc_ctx* ctx, const ApproxPlan& p, const float* Qdev, int nq, int kp, float* cand_s,
+                      uint32_t* cand_r, int32_t* cand_n);
+
+__global__ void k_decide(const uint64_t* wi, const double* ws, const uint64_t* oi, const double* os,
+                         const uint64_t* bi, const double* bs, const int32_t* wc, int64_t n, double thr, double e0,
+                         double e1, double e2, double e3, lc_decision* out);
+
+}  // namespace fc

@@ -1,0 +1,529 @@
+// lookup_sm100.cu — tcgen05 candidate stage of the prompt-similarity lookup.
+//
+// Replaces the scan loop of SimilarityIndex::query_top1 (vindex.cpp:64-72)
+// with S = Q · Xᵀ on the 5th-gen tensor cores, fused with a per-query
+// top-K' shortlist so the [queries x rows] score matrix never leaves the SM.
+//
+// Per CTA (persistent, one per SM, 6 warps):
+//   warp 0      TMA producer: streams bf16 table tiles [BN rows][64 K]
+//               (SWIZZLE_128B) into an NSTAGE smem ring.
+//   warp 1      TMEM owner + single-thread MMA issuer:
+//               tcgen05.mma.cta_group::1.kind::f16, A = 128 queries held
+//               RESIDENT IN TMEM (dim/2 columns, loaded once per work unit),
+//               B = table tile from smem, D = fp32 accumulator in TMEM
+//               (two BN-column buffers, so MMA of tile t+1 overlaps the
+//               epilogue of tile t).
+//   warps 2..5  epilogue: tcgen05.ld of the accumulator (thread = query
+//               row = TMEM lane), threshold filter against the running
+//               K'-th best, replace-min insert into a per-query shortlist in
+//               smem; at the end of the work unit the shortlist is written out.
+// Work unit = (128-query tile, contiguous row range). Units are ordered
+// split-major so that concurrently running CTAs stream the same table
+// region and every 128-query tile after the first reads it from L2.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cudaTypedefs.h>
+
+#include <cstring>
+
+#include "lookup.cuh"
+
+namespace fc {
+
+namespace sm100 {
+
+constexpr int BM = 128;     // queries per tile (TMEM lanes)
+constexpr int BK = 64;      // bf16 per 128-byte swizzle row
+constexpr int NTHREADS = 192;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(phase)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+
+// D[tmem] (+)= A[tmem] * B[smem desc]
+__device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+// K-major operand tile written by TMA with SWIZZLE_128B: rows of 128 B,
+// 8-row atoms of 1024 B (SBO), LBO unused (1), descriptor version 1 (sm100).
+__device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;            // LBO (16 B units)
+  d |= (uint64_t)(1024 >> 4) << 32;  // SBO
+  d |= (uint64_t)1 << 46;            // version
+  d |= (uint64_t)2 << 61;            // SWIZZLE_128B
+  return d;
+}
+
+__device__ __forceinline__ void tmem_ld64(uint32_t taddr, float* v) {
+  uint32_t r[64];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x64.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,"
+      "%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,"
+      "%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]),
+        "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]),
+        "=r"(r[40]), "=r"(r[41]), "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]),
+        "=r"(r[48]), "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]),
+        "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 64; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+
+// Replace-min insert into the thread's (query's) shortlist; rare after the
+// first few tiles, so it is kept out of line to keep the filter loop tight.
+__device__ __noinline__ void list_insert(float* ls, uint32_t* lr, int t, int kp, float v, uint32_t row, int& cnt,
+                                         int& minpos, float& tau) {
+  int at;
+  if (cnt < kp) {
+    at = cnt++;
+  } else {
+    at = minpos;
+  }
+  ls[at * BM + t] = v;
+  lr[at * BM + t] = row;
+  if (cnt == kp) {
+    float m = ls[t];
+    int mp = 0;
+    for (int i = 1; i < kp; ++i) {
+      const float x = ls[i * BM + t];
+      if (x < m) { m = x; mp = i; }
+    }
+    tau = m;
+    minpos = mp;
+  }
+}
+
+struct Params {
+  const __nv_bfloat16* Qb;  // [nq_pad][dim]
+  int nq;                    // real queries
+  int n_qtiles;
+  int dim;
+  int64_t n_rows;
+  int rows_per_split;        // multiple of BN
+  int n_splits;
+  int n_units;
+  int kp;
+  float* part_s;             // [nq][n_splits][kp]
+  uint32_t* part_r;
+  int32_t* part_n;           // [nq][n_splits]
+};
+
+template <int BN, int NSTAGE>
+struct Smem {
+  static constexpr int STAGE_BYTES = BN * 128;
+};
+
+template <int BN, int NSTAGE>
+__global__ void __launch_bounds__(NTHREADS, 1) k_shortlist(const __grid_constant__ CUtensorMap tmap, Params p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // carve: [stages][BN*128] | list scores [kp][128] | list rows [kp][128] | barriers | tmem addr
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr int STAGE_BYTES = BN * 128;
+  uint8_t* stages = base;
+  float* ls = reinterpret_cast<float*>(base + NSTAGE * STAGE_BYTES);
+  uint32_t* lr = reinterpret_cast<uint32_t*>(ls + p.kp * BM);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(lr + p.kp * BM);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + NSTAGE;
+  uint64_t* accf = bars + 2 * NSTAGE;
+  uint64_t* acce = accf + 2;
+  uint64_t* aready = acce + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aready + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nkb = p.dim / BK;
+  const int a_cols = p.dim / 2;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NSTAGE; ++s) {
+      mbar_init(smem_u32(&full[s]), 1);
+      mbar_init(smem_u32(&empty[s]), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(smem_u32(&accf[b]), 1);
+      mbar_init(smem_u32(&acce[b]), 128);
+    }
+    mbar_init(smem_u32(aready), 128);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+        const int split = u / p.n_qtiles;
+        const int64_t r0 = (int64_t)split * p.rows_per_split;
+        const int64_t r1 = min((int64_t)p.n_rows, r0 + p.rows_per_split);
+        for (int64_t row = r0; row < r1; row += BN) {
+          for (int kb = 0; kb < nkb; ++kb) {
+            mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+            mbar_expect_tx(smem_u32(&full[stage]), STAGE_BYTES);
+            tma_load_2d(smem_u32(stages + stage * STAGE_BYTES), &tmap, smem_u32(&full[stage]), kb * BK, (int)row);
+            if (++stage == NSTAGE) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    // instruction descriptor: D f32, A/B bf16, both K-major, M=128, N=BN
+    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+    int stage = 0;
+    uint32_t phase = 0;
+    uint32_t tile = 0;
+    uint32_t unit_i = 0;
+    for (int u = blockIdx.x; u < p.n_units; u += gridDim.x, ++unit_i) {
+      const int split = u / p.n_qtiles;
+      const int64_t r0 = (int64_t)split * p.rows_per_split;
+      const int64_t r1 = min((int64_t)p.n_rows, r0 + p.rows_per_split);
+      mbar_wait(smem_u32(aready), unit_i & 1);
+      tc_fence_after();
+      for (int64_t row = r0; row < r1; row += BN, ++tile) {
+        const uint32_t b = tile & 1;
+        const uint32_t use = tile >> 1;
+        mbar_wait(smem_u32(&acce[b]), (use & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem + a_cols + b * BN;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(smem_u32(&full[stage]), phase);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t sa = smem_u32(stages + stage * STAGE_BYTES);
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k) {
+              const uint64_t bdesc = smem_desc_sw128(sa + k * 32);
+              mma_ts(d_tmem, tmem + (kb * (BK / 16) + k) * 8, bdesc, idesc, (kb | k) != 0);
+            }
+            tc_commit(smem_u32(&empty[stage]));
+          }
+          __syncwarp();
+          if (++stage == NSTAGE) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        if (lane == 0) tc_commit(smem_u32(&accf[b]));
+        __syncwarp();
+      }
+    }
+  } else {
+    // ---------------- epilogue: warps 2..5 ----------------
+    const int quarter = warp & 3;        // TMEM lane quarter this warp may access
+    const int t = quarter * 32 + lane;   // query row within the tile
+    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+    uint32_t tile = 0;
+    uint32_t unit_i = 0;
+    for (int u = blockIdx.x; u < p.n_units; u += gridDim.x, ++unit_i) {
+      const int split = u / p.n_qtiles;
+      const int qtile = u - split * p.n_qtiles;
+      const int64_t r0 = (int64_t)split * p.rows_per_split;
+      const int64_t r1 = min((int64_t)p.n_rows, r0 + p.rows_per_split);
+      // (1) load this unit's 128 queries into TMEM columns [0, dim/2)
+      {
+        const uint4* src = reinterpret_cast<const uint4*>(p.Qb + (size_t)(qtile * BM + t) * p.dim);
+        for (int kb = 0; kb < nkb; ++kb) {
+          uint32_t r[32];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const uint4 v = __ldg(src + kb * 8 + i);
+            r[4 * i + 0] = v.x;
+            r[4 * i + 1] = v.y;
+            r[4 * i + 2] = v.z;
+            r[4 * i + 3] = v.w;
+          }
+          tmem_st32(tmem + lane_base + kb * 32, r);
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        mbar_arrive(smem_u32(aready));
+      }
+      // (2) stream the accumulator tiles, keep the per-query top-kp
+      int cnt = 0, minpos = 0;
+      float tau = -INFINITY;
+      for (int64_t row = r0; row < r1; row += BN, ++tile) {
+        const uint32_t b = tile & 1;
+        const uint32_t use = tile >> 1;
+        mbar_wait(smem_u32(&accf[b]), use & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int h = 0; h < BN / 64; ++h) {
+          float v[64];
+          tmem_ld64(tmem + lane_base + a_cols + b * BN + h * 64, v);
+          if (h == BN / 64 - 1) {
+            tc_fence_before();
+            mbar_arrive(smem_u32(&acce[b]));
+          }
+          const int64_t rbase = row + h * 64;
+          const int lim = (int)min((int64_t)64, r1 - rbase);
+#pragma unroll
+          for (int j = 0; j < 64; ++j)
+            if (j < lim && v[j] > tau) list_insert(ls, lr, t, p.kp, v[j], (uint32_t)(rbase + j), cnt, minpos, tau);
+        }
+      }
+      // (3) write the shortlist of this (query, split)
+      const int q = qtile * BM + t;
+      if (q < p.nq) {
+        const size_t o = ((size_t)q * p.n_splits + split) * p.kp;
+        for (int i = 0; i < cnt; ++i) {
+          p.part_s[o + i] = ls[i * BM + t];
+          p.part_r[o + i] = lr[i * BM + t];
+        }
+        p.part_n[(size_t)q * p.n_splits + split] = cnt;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+__global__ void k_q_to_bf16(const float* __restrict__ Q, int nq, int dim, __nv_bfloat16* __restrict__ Qb, int nq_pad) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t total = (int64_t)nq_pad * dim;
+  if (i >= total) return;
+  const int64_t q = i / dim;
+  Qb[i] = q < nq ? __float2bfloat16_rn(Q[i]) : __float2bfloat16_rn(0.f);
+}
+
+__device__ __forceinline__ uint32_t fkey(float f) {
+  const uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+// Per query: top-kp of the n_splits partial shortlists by bf16 score.
+__global__ void __launch_bounds__(256) k_shortlist_merge(const float* __restrict__ ps, const uint32_t* __restrict__ pr,
+                                                         const int32_t* __restrict__ pn, int n_splits, int kp,
+                                                         float* __restrict__ cs, uint32_t* __restrict__ cr,
+                                                         int32_t* __restrict__ cn) {
+  extern __shared__ uint32_t s_key[];  // [n_splits * kp]
+  __shared__ int s_cnt, s_gt, s_eq, s_pos;
+  const int q = blockIdx.x;
+  const size_t base = (size_t)q * n_splits * kp;
+  const int total = n_splits * kp;
+  for (int i = threadIdx.x; i < total; i += blockDim.x) {
+    const int sp = i / kp, j = i - sp * kp;
+    s_key[i] = j < pn[(size_t)q * n_splits + sp] ? fkey(ps[base + i]) : 0u;  // 0 = empty slot
+  }
+  if (threadIdx.x == 0) s_cnt = 0;
+  __syncthreads();
+  int mine = 0;
+  for (int i = threadIdx.x; i < total; i += blockDim.x) mine += s_key[i] != 0u;
+  atomicAdd(&s_cnt, mine);
+  __syncthreads();
+  const int n_items = s_cnt;
+  uint32_t T = 1;  // keep everything non-empty
+  if (n_items > kp) {
+    uint32_t lo = 1, hi = 0xFFFFFFFFu;
+    while (lo < hi) {
+      const uint32_t mid = lo + (uint32_t)(((uint64_t)hi - lo + 1) >> 1);
+      __syncthreads();
+      if (threadIdx.x == 0) s_gt = 0;
+      __syncthreads();
+      int c = 0;
+      for (int i = threadIdx.x; i < total; i += blockDim.x) c += s_key[i] >= mid;
+      atomicAdd(&s_gt, c);
+      __syncthreads();
+      if (s_gt >= kp) lo = mid; else hi = mid - 1;
+    }
+    T = lo;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    s_pos = 0;
+    s_eq = 0;
+  }
+  __syncthreads();
+  // strictly above T first, then fill with == T
+  for (int i = threadIdx.x; i < total; i += blockDim.x) {
+    if (s_key[i] > T) {
+      const int at = atomicAdd(&s_pos, 1);
+      cs[(size_t)q * kp + at] = ps[base + i];
+      cr[(size_t)q * kp + at] = pr[base + i];
+    }
+  }
+  __syncthreads();
+  const int above = s_pos;
+  for (int i = threadIdx.x; i < total; i += blockDim.x) {
+    if (s_key[i] == T && s_key[i] != 0u) {
+      const int e = atomicAdd(&s_eq, 1);
+      if (above + e < kp) {
+        cs[(size_t)q * kp + above + e] = ps[base + i];
+        cr[(size_t)q * kp + above + e] = pr[base + i];
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) cn[q] = min(kp, above + s_eq);
+}
+
+}  // namespace sm100
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    FC_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !p) raise(LC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+bool approx_available() { return true; }
+
+void approx_plan(ApproxPlan& p, const __nv_bfloat16* rows, int64_t n_rows, int dim, int sm_count) {
+  (void)sm_count;
+  p.n_rows = n_rows;
+  p.dim = dim;
+  p.rows = rows;
+  p.bn = dim <= 512 ? 128 : 64;
+  cuuint64_t gdim[2] = {(cuuint64_t)dim, (cuuint64_t)n_rows};
+  cuuint64_t gstride[1] = {(cuuint64_t)dim * sizeof(__nv_bfloat16)};
+  cuuint32_t box[2] = {(cuuint32_t)sm100::BK, (cuuint32_t)p.bn};
+  cuuint32_t estride[2] = {1, 1};
+  CUresult r = encode_fn()(&p.tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<__nv_bfloat16*>(rows), gdim, gstride,
+                           box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) raise(LC_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  p.valid = true;
+}
+
+template <int BN, int NSTAGE>
+static void launch_shortlist(lc_ctx* ctx, const ApproxPlan& plan, sm100::Params prm) {
+  const size_t smem = 1024 + (size_t)NSTAGE * BN * 128 + (size_t)prm.kp * sm100::BM * 8 + (2 * NSTAGE + 5) * 8 + 16;
+  auto kern = sm100::k_shortlist<BN, NSTAGE>;
+  FC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int grid = std::min(prm.n_units, ctx->sm_count);
+  kern<<<grid, sm100::NTHREADS, smem, ctx->stream>>>(plan.tmap, prm);
+  FC_LAUNCH_CHECK();
+}
+
+void approx_shortlist(lc_ctx* ctx, const ApproxPlan& plan, const float* Qdev, int nq, int kp, float* cand_s,
+                      uint32_t* cand_r, int32_t* cand_n) {
+  using namespace sm100;
+  const int dim = plan.dim;
+  const int n_qtiles = (nq + BM - 1) / BM;
+  const int nq_pad = n_qtiles * BM;
+  DevBuf qb((size_t)nq_pad * dim * sizeof(__nv_bfloat16), ctx->stream);
+  k_q_to_bf16<<<grid_for((int64_t)nq_pad * dim, 256), 256, 0, ctx->stream>>>(Qdev, nq, dim, qb.as<__nv_bfloat16>(), nq_pad);
+  FC_LAUNCH_CHECK();
+  const int bn = plan.bn;
+  const int64_t total_tiles = (plan.n_rows + bn - 1) / bn;
+  int64_t splits = std::max<int64_t>(1, ((int64_t)ctx->sm_count * 8 + n_qtiles - 1) / n_qtiles);
+  splits = std::min<int64_t>(splits, std::max<int64_t>(1, total_tiles / 16));
+  const int64_t tiles_per_split = (total_tiles + splits - 1) / splits;
+  splits = (total_tiles + tiles_per_split - 1) / tiles_per_split;
+  Params prm;
+  prm.Qb = qb.as<__nv_bfloat16>();
+  prm.nq = nq;
+  prm.n_qtiles = n_qtiles;
+  prm.dim = dim;
+  prm.n_rows = plan.n_rows;
+  prm.rows_per_split = (int)(tiles_per_split * bn);
+  prm.n_splits = (int)splits;
+  prm.n_units = (int)(splits * n_qtiles);
+  prm.kp = kp;
+  DevBuf ps((size_t)nq * splits * kp * sizeof(float), ctx->stream);
+  DevBuf pr((size_t)nq * splits * kp * sizeof(uint32_t), ctx->stream);
+  DevBuf pn((size_t)nq * splits * sizeof(int32_t), ctx->stream);
+  prm.part_s = ps.as<float>();
+  prm.part_r = pr.as<uint32_t>();
+  prm.part_n = pn.as<int32_t>();
+  if (bn == 64)
+    launch_shortlist<64, 8>(ctx, plan, prm);
+  else
+    launch_shortlist<128, 6>(ctx, plan, prm);
+  const size_t msmem = (size_t)splits * kp * sizeof(uint32_t);
+  if (msmem > 48 * 1024) FC_CUDA(cudaFuncSetAttribute(k_shortlist_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msmem));
+  k_shortlist_merge<<<nq, 256, msmem, ctx->stream>>>(ps.as<float>(), pr.as<uint32_t>(), pn.as<int32_t>(), (int)splits, kp,
+                                                      cand_s, cand_r, cand_n);
+  FC_LAUNCH_CHECK();
+  count_launch(ctx, 3);
+}
+
+}  // namespace fc

@@ -1,0 +1,597 @@
+// store.cu — CacheStore (store.hpp:48-120) with GPU replacement scoring.
+//
+// Host keeps the per-prompt records (validation, hole fallback, byte
+// accounting; store.cpp:53-217) and a mirror of the per-(prompt, step)
+// bookkeeping. The device holds the live-step table as SoA-ish records
+// (40 B per live step + 16 B per prompt) that the scoring kernels read:
+//   K11 k_policy_head   per live step: attributed capacity
+//                       cap = private + shared / live (integer, store.cpp:122),
+//                       policy key (store.cpp:125-131; fp64 IEEE mul/div), then a
+//                       block-level selection of the H smallest (key, seq).
+//   K12 k_head_merge    merge of the per-block heads -> global sorted head.
+// Eviction (store.cpp:80, repeated evict_one) then walks the head on the
+// host. For LRBU, evicting a step re-attributes the prompt's shared bytes to
+// its surviving siblings, which lowers their keys; those siblings are re-keyed
+// exactly on the host and kept in a small heap, so the victim sequence equals
+// k repeated argmins without k full scans. When the head
+// is exhausted the table is re-scored.
+#include <algorithm>
+#include <cmath>
+#include <map>
+#include <queue>
+#include <unordered_map>
+#include <unordered_set>
+
+#include "entry.hpp"
+#include "topk.cuh"
+
+namespace fc {
+
+struct DevLive {
+  uint64_t f, last, seq, priv;
+  int32_t step;   // 0 = dead slot
+  int32_t pslot;
+};
+struct DevPrompt {
+  uint64_t shared;
+  int32_t live;
+  int32_t pad;
+};
+
+constexpr int HEAD = 64;
+constexpr int POL_T = 256;
+constexpr int POL_PER = 4;
+
+__device__ __forceinline__ double pkey(int policy, const DevLive& l, const DevPrompt& p, uint64_t now, uint64_t* cap_out,
+                                       int* bad) {
+  const uint64_t cap = l.priv + p.shared / (uint64_t)p.live;
+  *cap_out = cap;
+  switch (policy) {
+    case LC_POLICY_FIFO: return (double)l.seq;
+    case LC_POLICY_LRU: return (double)l.last;
+    case LC_POLICY_LCBFU: return __dmul_rn((double)(l.f + 1), (double)l.step);
+    default: {
+      if (now < l.last || cap == 0) {
+        *bad = 1;
+        return 0.0;
+      }
+      const uint64_t dd = now - l.last;
+      const double duration = (double)(dd > 1 ? dd : 1);
+      return __ddiv_rn(__dmul_rn((double)(l.f + 1), (double)l.step), __dmul_rn((double)cap, duration));
+    }
+  }
+}
+
+// Smallest (key, seq) first: encoded as Cand{s = -key, id = seq} so that the
+// shared (score desc, id asc) selection applies unchanged (negation is exact).
+__global__ void __launch_bounds__(POL_T) k_policy_head(const DevLive* __restrict__ live, int64_t n_slots,
+                                                       const DevPrompt* __restrict__ prompts, int policy, uint64_t now,
+                                                       Cand* __restrict__ partial, int32_t* __restrict__ pcount,
+                                                       int* __restrict__ bad) {
+  __shared__ Cand s_c[POL_T / 32];
+  __shared__ int s_o[POL_T / 32];
+  __shared__ Cand s_out[HEAD];
+  Cand L[POL_PER];
+  int ln = 0;
+  int b = 0;
+  const int64_t base = (int64_t)blockIdx.x * POL_T * POL_PER;
+  for (int t = 0; t < POL_PER; ++t) {
+    const int64_t i = base + (int64_t)t * POL_T + threadIdx.x;
+    if (i >= n_slots) break;
+    const DevLive l = live[i];
+    if (l.step == 0) continue;
+    uint64_t cap;
+    const double key = pkey(policy, l, prompts[l.pslot], now, &cap, &b);
+    Cand c;
+    c.s = -key;
+    c.id = l.seq;
+    c.slot = i;
+    local_insert<POL_PER>(L, ln, POL_PER, c);
+  }
+  if (b) atomicExch(bad, 1);
+  const int got = block_merge_lists<POL_PER>(L, ln, HEAD, s_out, s_c, s_o);
+  for (int t = threadIdx.x; t < got; t += POL_T) partial[(int64_t)blockIdx.x * HEAD + t] = s_out[t];
+  if (threadIdx.x == 0) pcount[blockIdx.x] = got;
+}
+
+__global__ void __launch_bounds__(256) k_head_merge(const Cand* __restrict__ partial, const int32_t* __restrict__ pcount,
+                                                    int nblk, Cand* __restrict__ head, int32_t* __restrict__ head_n) {
+  __shared__ Cand s_c[8];
+  __shared__ int s_o[8];
+  __shared__ Cand s_out[HEAD];
+  Cand L[HEAD];
+  int ln = 0;
+  for (int bi = threadIdx.x; bi < nblk; bi += blockDim.x) {
+    const int c = pcount[bi];
+    for (int t = 0; t < c; ++t) local_insert<HEAD>(L, ln, HEAD, partial[(int64_t)bi * HEAD + t]);
+  }
+  const int got = block_merge_lists<HEAD>(L, ln, HEAD, s_out, s_c, s_o);
+  for (int t = threadIdx.x; t < got; t += blockDim.x) head[t] = s_out[t];
+  if (threadIdx.x == 0) *head_n = got;
+}
+
+struct ScatterLive {
+  int64_t slot;
+  DevLive v;
+};
+struct ScatterPrompt {
+  int64_t slot;
+  DevPrompt v;
+};
+__global__ void k_scatter(const ScatterLive* __restrict__ ul, int nl, DevLive* __restrict__ live,
+                          const ScatterPrompt* __restrict__ up, int np, DevPrompt* __restrict__ prompts) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nl) live[ul[i].slot] = ul[i].v;
+  if (i < np) prompts[up[i].slot] = up[i].v;
+}
+
+// Host copy of the policy key: identical IEEE operations to pkey().
+static double host_key(int policy, uint64_t f, int step, uint64_t last, uint64_t seq, uint64_t cap, uint64_t now) {
+  switch (policy) {
+    case LC_POLICY_FIFO: return (double)seq;
+    case LC_POLICY_LRU: return (double)last;
+    case LC_POLICY_LCBFU: return (double)(f + 1) * (double)step;
+    default: {
+      if (now < last) raise(LC_ERR_INVALID_ARGUMENT, "lrbu_priority: now precedes last access");
+      if (cap == 0) raise(LC_ERR_INVALID_ARGUMENT, "lrbu_priority: zero capacity");
+      const uint64_t dd = now - last;
+      const double duration = (double)(dd > 1 ? dd : 1);
+      volatile double num = (double)(f + 1) * (double)step;
+      volatile double den = (double)cap * duration;
+      return num / den;
+    }
+  }
+}
+
+}  // namespace fc
+
+using namespace fc;
+
+struct lc_store {
+  struct Live {
+    int step;
+    int si;  // index into entry data steps
+    uint64_t f, last, inserted_at, seq, priv;
+    int64_t slot;
+  };
+  struct Rec {
+    lc_entry* view = nullptr;
+    uint64_t shared = 0;
+    std::vector<Live> live;  // ascending step
+    int32_t pslot = -1;
+  };
+  lc_ctx* ctx;
+  uint64_t capacity, used = 0, next_seq = 0;
+  int policy;
+  std::map<uint64_t, Rec> prompts;
+  // device table + host mirror
+  std::vector<DevLive> hl;
+  std::vector<DevPrompt> hp;
+  std::vector<int64_t> free_l;
+  std::vector<int32_t> free_p;
+  std::unordered_set<int64_t> dirty_l;
+  std::unordered_set<int32_t> dirty_p;
+  DevLive* dl = nullptr;
+  DevPrompt* dp = nullptr;
+  int64_t cap_l = 0, cap_p = 0;
+  int64_t live_count = 0;
+  uint64_t scorings = 0;
+
+  ~lc_store() {
+    for (auto& kv : prompts) delete kv.second.view;
+    if (dl) cudaFree(dl);
+    if (dp) cudaFree(dp);
+  }
+
+  int64_t alloc_live() {
+    if (!free_l.empty()) {
+      int64_t s = free_l.back();
+      free_l.pop_back();
+      return s;
+    }
+    hl.push_back(DevLive{});
+    return (int64_t)hl.size() - 1;
+  }
+  int32_t alloc_prompt() {
+    if (!free_p.empty()) {
+      int32_t s = free_p.back();
+      free_p.pop_back();
+      return s;
+    }
+    hp.push_back(DevPrompt{});
+    return (int32_t)hp.size() - 1;
+  }
+  void write_live(const Rec& r, const Live& l) {
+    hl[l.slot] = DevLive{l.f, l.last, l.seq, l.priv, l.step, r.pslot};
+    dirty_l.insert(l.slot);
+  }
+  void write_prompt(const Rec& r) {
+    hp[r.pslot] = DevPrompt{r.shared, (int32_t)r.live.size(), 0};
+    dirty_p.insert(r.pslot);
+  }
+
+  void sync_device() {
+    const int64_t nl = (int64_t)hl.size(), np = (int64_t)hp.size();
+    auto grow = [&](auto*& ptr, int64_t& cap, int64_t need, size_t elem, size_t used_elems) {
+      if (need <= cap) return false;
+      const int64_t nc = std::max<int64_t>(need, std::max<int64_t>(1024, cap * 2));
+      void* p = nullptr;
+      FC_CUDA(cudaMalloc(&p, nc * elem));
+      FC_CUDA(cudaMemsetAsync(p, 0, nc * elem, ctx->stream));
+      (void)used_elems;
+      if (ptr) {
+        FC_CUDA(cudaStreamSynchronize(ctx->stream));
+        cudaFree(ptr);
+      }
+      ptr = static_cast<std::remove_reference_t<decltype(ptr)>>(p);
+      cap = nc;
+      return true;
+    };
+    const bool rl = grow(dl, cap_l, nl, sizeof(DevLive), nl);
+    const bool rp = grow(dp, cap_p, np, sizeof(DevPrompt), np);
+    if (rl) {
+      if (nl) FC_CUDA(cudaMemcpyAsync(dl, hl.data(), nl * sizeof(DevLive), cudaMemcpyHostToDevice, ctx->stream));
+      dirty_l.clear();
+    }
+    if (rp) {
+      if (np) FC_CUDA(cudaMemcpyAsync(dp, hp.data(), np * sizeof(DevPrompt), cudaMemcpyHostToDevice, ctx->stream));
+      dirty_p.clear();
+    }
+    if (dirty_l.empty() && dirty_p.empty()) return;
+    std::vector<ScatterLive> ul;
+    std::vector<ScatterPrompt> up;
+    for (int64_t s : dirty_l) ul.push_back(ScatterLive{s, hl[s]});
+    for (int32_t s : dirty_p) up.push_back(ScatterPrompt{s, hp[s]});
+    dirty_l.clear();
+    dirty_p.clear();
+    DevBuf bl(ul.size() * sizeof(ScatterLive) + 16, ctx->stream), bp(up.size() * sizeof(ScatterPrompt) + 16, ctx->stream);
+    if (!ul.empty()) FC_CUDA(cudaMemcpyAsync(bl.p, ul.data(), ul.size() * sizeof(ScatterLive), cudaMemcpyHostToDevice, ctx->stream));
+    if (!up.empty()) FC_CUDA(cudaMemcpyAsync(bp.p, up.data(), up.size() * sizeof(ScatterPrompt), cudaMemcpyHostToDevice, ctx->stream));
+    const int n = (int)std::max(ul.size(), up.size());
+    k_scatter<<<grid_for(n, 256), 256, 0, ctx->stream>>>(bl.as<ScatterLive>(), (int)ul.size(), dl, bp.as<ScatterPrompt>(),
+                                                        (int)up.size(), dp);
+    FC_LAUNCH_CHECK();
+    count_launch(ctx);
+  }
+
+  // GPU scoring: the HEAD smallest (key, seq) live steps at time `now`.
+  std::vector<Cand> score_head(uint64_t now) {
+    sync_device();
+    ++scorings;
+    const int64_t n_slots = (int64_t)hl.size();
+    const int nblk = (int)std::max<int64_t>(1, (n_slots + POL_T * POL_PER - 1) / (POL_T * POL_PER));
+    DevBuf partial((size_t)nblk * HEAD * sizeof(Cand), ctx->stream), pc((size_t)nblk * sizeof(int32_t), ctx->stream);
+    DevBuf head(HEAD * sizeof(Cand) + 16, ctx->stream);
+    DevBuf bad(sizeof(int), ctx->stream);
+    FC_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), ctx->stream));
+    k_policy_head<<<nblk, POL_T, 0, ctx->stream>>>(dl, n_slots, dp, policy, now, partial.as<Cand>(), pc.as<int32_t>(),
+                                                   bad.as<int>());
+    FC_LAUNCH_CHECK();
+    k_head_merge<<<1, 256, 0, ctx->stream>>>(partial.as<Cand>(), pc.as<int32_t>(), nblk, head.as<Cand>(),
+                                             reinterpret_cast<int32_t*>(head.as<Cand>() + HEAD));
+    FC_LAUNCH_CHECK();
+    count_launch(ctx, 2);
+    std::vector<Cand> h(HEAD);
+    int32_t hn = 0, hb = 0;
+    FC_CUDA(cudaMemcpyAsync(h.data(), head.p, HEAD * sizeof(Cand), cudaMemcpyDeviceToHost, ctx->stream));
+    FC_CUDA(cudaMemcpyAsync(&hn, head.as<Cand>() + HEAD, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
+    FC_CUDA(cudaMemcpyAsync(&hb, bad.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    sync(ctx);
+    if (hb) raise(LC_ERR_INVALID_ARGUMENT, "lrbu_priority: now precedes last access");
+    h.resize(hn);
+    return h;
+  }
+
+  // slot -> (prompt record, live index)
+  std::unordered_map<int64_t, uint64_t> slot_prompt;
+
+  lc_step_entry remove_step(std::map<uint64_t, Rec>::iterator it, int li, uint64_t attributed) {
+    Rec& r = it->second;
+    Live l = r.live[li];
+    lc_step_entry out{it->first, l.step, 0, l.f, l.last, l.inserted_at, l.seq, attributed};
+    used -= l.priv;
+    hl[l.slot] = DevLive{};
+    dirty_l.insert(l.slot);
+    free_l.push_back(l.slot);
+    slot_prompt.erase(l.slot);
+    --live_count;
+    r.live.erase(r.live.begin() + li);
+    // the entry view drops the evicted step record (store.cpp:169-170)
+    auto& sel = r.view->sel;
+    sel.erase(std::remove(sel.begin(), sel.end(), l.si), sel.end());
+    if (r.live.empty()) {
+      used -= r.shared;
+      hp[r.pslot] = DevPrompt{};
+      dirty_p.insert(r.pslot);
+      free_p.push_back(r.pslot);
+      delete r.view;
+      prompts.erase(it);
+    } else {
+      write_prompt(r);
+    }
+    return out;
+  }
+
+  // k evictions at a fixed `now` (one insert_steps call, or one evict_one).
+  struct Evictor {
+    lc_store* s;
+    uint64_t now;
+    std::vector<Cand> head;
+    size_t pos = 0;
+    bool have = false;
+    std::unordered_map<int64_t, double> rekeyed;  // slot -> current key (LRBU siblings)
+    struct HE {
+      double key;
+      uint64_t seq;
+      int64_t slot;
+      bool operator>(const HE& o) const { return key > o.key || (key == o.key && seq > o.seq); }
+    };
+    std::priority_queue<HE, std::vector<HE>, std::greater<HE>> heap;
+
+    lc_step_entry next() {
+      if (s->prompts.empty()) raise(LC_ERR_LOGIC, "evict_one: store is empty");
+      for (;;) {
+        if (!have) {
+          head = s->score_head(now);
+          pos = 0;
+          have = true;
+          rekeyed.clear();
+          heap = decltype(heap)();
+        }
+        // first head entry that is still live and was not re-keyed
+        while (pos < head.size() &&
+               (!s->slot_prompt.count(head[pos].slot) || rekeyed.count(head[pos].slot)))
+          ++pos;
+        // drop stale heap tops
+        while (!heap.empty()) {
+          const HE& t = heap.top();
+          auto it = rekeyed.find(t.slot);
+          if (!s->slot_prompt.count(t.slot) || it == rekeyed.end() || it->second != t.key) heap.pop();
+          else break;
+        }
+        if (pos >= head.size()) {
+          have = false;  // head exhausted: re-score the live table
+          continue;
+        }
+        int64_t victim = head[pos].slot;
+        double vkey = -head[pos].s;
+        uint64_t vseq = head[pos].id;
+        if (!heap.empty()) {
+          const HE& t = heap.top();
+          if (t.key < vkey || (t.key == vkey && t.seq < vseq)) {
+            victim = t.slot;
+            vkey = t.key;
+            vseq = t.seq;
+          }
+        }
+        return evict_slot(victim);
+      }
+    }
+
+    lc_step_entry evict_slot(int64_t slot) {
+      auto it = s->prompts.find(s->slot_prompt.at(slot));
+      Rec& r = it->second;
+      int li = -1;
+      for (size_t i = 0; i < r.live.size(); ++i)
+        if (r.live[i].slot == slot) li = (int)i;
+      const uint64_t attributed = r.live[li].priv + r.shared / r.live.size();
+      const bool siblings_rekey = s->policy == LC_POLICY_LRBU && r.live.size() > 1;
+      const uint64_t pid = it->first;
+      lc_step_entry out = s->remove_step(it, li, attributed);
+      if (siblings_rekey) {
+        Rec& rr = s->prompts.at(pid);
+        for (const Live& l : rr.live) {
+          const uint64_t cap = l.priv + rr.shared / rr.live.size();
+          const double k = host_key(s->policy, l.f, l.step, l.last, l.seq, cap, now);
+          rekeyed[l.slot] = k;
+          heap.push(HE{k, l.seq, l.slot});
+        }
+      }
+      return out;
+    }
+  };
+};
+
+extern "C" {
+
+lc_status lc_store_create(lc_ctx* ctx, uint64_t capacity, int policy, lc_store** out) {
+  LC_API_BEGIN
+  FC_REQUIRE(ctx && out, "null argument");
+  if (policy < 0 || policy > 3) raise(LC_ERR_INVALID_ARGUMENT, "invalid policy value");
+  auto* s = new lc_store();
+  s->ctx = ctx;
+  s->capacity = capacity;
+  s->policy = policy;
+  *out = s;
+  LC_API_END
+}
+
+lc_status lc_store_destroy(lc_store* s) {
+  LC_API_BEGIN
+  if (!s) return LC_OK;
+  DeviceGuard g(s->ctx->device);
+  cudaStreamSynchronize(s->ctx->stream);
+  delete s;
+  LC_API_END
+}
+
+lc_status lc_store_insert(lc_store* s, uint64_t prompt, lc_entry* entry, const int32_t* steps, int n_steps, uint64_t now,
+                          lc_step_entry* evicted, int cap, int* n_evicted) {
+  LC_API_BEGIN
+  FC_REQUIRE(s && entry, "null argument");
+  DeviceGuard g(s->ctx->device);
+  if (n_evicted) *n_evicted = 0;
+  for (int i = 0; i < n_steps; ++i)
+    if (steps[i] < 1 || steps[i] > 50) raise(LC_ERR_INVALID_ARGUMENT, "StepId: value out of range 1..50");
+  if (n_steps <= 0) raise(LC_ERR_INVALID_ARGUMENT, "insert_steps: empty step list");
+  const EntryData& d = *entry->d;
+  if (d.prompt != prompt) raise(LC_ERR_INVALID_ARGUMENT, "insert_steps: prompt does not match entry");
+  if (s->prompts.count(prompt)) raise(LC_ERR_INVALID_ARGUMENT, "insert_steps: prompt already cached");
+  auto has = [&](int st) {
+    for (int k : entry->sel)
+      if (d.steps[k] == st) return true;
+    return false;
+  };
+  for (int i = 0; i < n_steps; ++i) {
+    const int st = steps[i];
+    if (!(st == 5 || st == 10 || st == 15 || st == 20 || st == 25))
+      raise(LC_ERR_INVALID_ARGUMENT, "insert_steps: step not cacheable");
+    if (!has(st)) raise(LC_ERR_INVALID_ARGUMENT, "insert_steps: step missing from entry");
+  }
+  // keep only the requested records (store.cpp:68-71)
+  std::vector<int> sel;
+  for (int k : entry->sel)
+    if (std::find(steps, steps + n_steps, d.steps[k]) != steps + n_steps) sel.push_back(k);
+  lc_store::Rec rec;
+  rec.view = make_entry_view(entry->d, sel);
+  rec.shared = d.shared_bytes();
+  uint64_t standalone = rec.shared;
+  for (int k : sel) standalone += d.private_bytes(k);
+  if (standalone > s->capacity) {
+    delete rec.view;
+    set_last_oversize(standalone, s->capacity);
+    raise(LC_ERR_OVERSIZED_ENTRY, "entry of " + std::to_string(standalone) + " bytes exceeds capacity limit of " +
+                                      std::to_string(s->capacity) + " bytes");
+  }
+  int ne = 0;
+  try {
+    if (s->used + standalone > s->capacity) {
+      lc_store::Evictor ev{s, now};
+      while (s->used + standalone > s->capacity) {
+        lc_step_entry v = ev.next();
+        if (evicted && ne < cap) evicted[ne] = v;
+        ++ne;
+      }
+    }
+  } catch (...) {
+    delete rec.view;
+    if (n_evicted) *n_evicted = ne;
+    throw;
+  }
+  rec.pslot = s->alloc_prompt();
+  for (int k : sel) {
+    lc_store::Live l;
+    l.step = d.steps[k];
+    l.si = k;
+    l.f = 0;
+    l.last = now;
+    l.inserted_at = now;
+    l.seq = s->next_seq++;
+    l.priv = d.private_bytes(k);
+    l.slot = s->alloc_live();
+    rec.live.push_back(l);
+  }
+  s->used += standalone;
+  auto it = s->prompts.emplace(prompt, std::move(rec)).first;
+  for (auto& l : it->second.live) {
+    s->write_live(it->second, l);
+    s->slot_prompt[l.slot] = prompt;
+    ++s->live_count;
+  }
+  s->write_prompt(it->second);
+  if (n_evicted) *n_evicted = ne;
+  LC_API_END
+}
+
+lc_status lc_store_get_step(lc_store* s, uint64_t prompt, int desired, uint64_t now, int32_t* actual, float* out_dev) {
+  LC_API_BEGIN
+  DeviceGuard g(s->ctx->device);
+  if (desired < 1 || desired > 50) raise(LC_ERR_INVALID_ARGUMENT, "StepId: value out of range 1..50");
+  if (!(desired == 5 || desired == 10 || desired == 15 || desired == 20 || desired == 25))
+    raise(LC_ERR_INVALID_ARGUMENT, "get_step: desired step not cacheable");
+  *actual = 0;
+  auto it = s->prompts.find(prompt);
+  if (it == s->prompts.end()) return LC_OK;
+  auto& rec = it->second;
+  int li = -1;
+  for (size_t i = 0; i < rec.live.size(); ++i)
+    if (rec.live[i].step <= desired) li = (int)i;
+  if (li < 0) return LC_OK;
+  auto& l = rec.live[li];
+  if (out_dev) {
+    FC_REQUIRE(is_device_ptr(out_dev), "lc_store_get_step: out_dev must be device memory");
+    launch_decompress(s->ctx, {rec.view->d.get()}, {l.si}, out_dev);
+    sync(s->ctx);
+  }
+  l.f += 1;
+  l.last = now;
+  s->write_live(rec, l);
+  *actual = l.step;
+  LC_API_END
+}
+
+lc_status lc_store_evict_one(lc_store* s, uint64_t now, lc_step_entry* out) {
+  LC_API_BEGIN
+  DeviceGuard g(s->ctx->device);
+  lc_store::Evictor ev{s, now};
+  lc_step_entry v = ev.next();
+  if (out) *out = v;
+  LC_API_END
+}
+
+lc_status lc_store_evict_step(lc_store* s, uint64_t prompt, int step, int32_t* removed) {
+  LC_API_BEGIN
+  if (step < 1 || step > 50) raise(LC_ERR_INVALID_ARGUMENT, "StepId: value out of range 1..50");
+  *removed = 0;
+  auto it = s->prompts.find(prompt);
+  if (it == s->prompts.end()) return LC_OK;
+  for (size_t i = 0; i < it->second.live.size(); ++i)
+    if (it->second.live[i].step == step) {
+      auto& r = it->second;
+      s->remove_step(it, (int)i, r.live[i].priv + r.shared / r.live.size());
+      *removed = 1;
+      break;
+    }
+  LC_API_END
+}
+
+uint64_t lc_store_used(lc_store* s) { return s->used; }
+uint64_t lc_store_capacity(lc_store* s) { return s->capacity; }
+int lc_store_policy(lc_store* s) { return s->policy; }
+int64_t lc_store_step_count(lc_store* s) { return s->live_count; }
+int64_t lc_store_prompt_count(lc_store* s) { return (int64_t)s->prompts.size(); }
+
+uint64_t lc_store_recompute_used(lc_store* s) {
+  uint64_t n = 0;
+  for (auto& kv : s->prompts) n += entry_compressed_size(kv.second.view);
+  return n;
+}
+
+lc_status lc_store_contains(lc_store* s, uint64_t prompt, int32_t* out) {
+  LC_API_BEGIN
+  *out = s->prompts.count(prompt) ? 1 : 0;
+  LC_API_END
+}
+
+lc_status lc_store_cached_steps(lc_store* s, uint64_t prompt, int32_t* steps, int* n) {
+  LC_API_BEGIN
+  *n = 0;
+  auto it = s->prompts.find(prompt);
+  if (it == s->prompts.end()) return LC_OK;
+  for (auto& l : it->second.live) steps[(*n)++] = l.step;
+  LC_API_END
+}
+
+lc_status lc_store_entry(lc_store* s, uint64_t prompt, lc_entry** out) {
+  LC_API_BEGIN
+  auto it = s->prompts.find(prompt);
+  *out = it == s->prompts.end() ? nullptr : it->second.view;
+  LC_API_END
+}
+
+lc_status lc_store_entries(lc_store* s, lc_step_entry* out, int64_t cap, int64_t* n) {
+  LC_API_BEGIN
+  int64_t k = 0;
+  for (auto& kv : s->prompts) {
+    const auto& r = kv.second;
+    for (auto& l : r.live) {
+      if (out && k < cap)
+        out[k] = lc_step_entry{kv.first, l.step, 0, l.f, l.last, l.inserted_at, l.seq, l.priv + r.shared / r.live.size()};
+      ++k;
+    }
+  }
+  *n = k;
+  LC_API_END
+}
+
+}  // extern "C"

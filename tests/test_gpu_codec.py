@@ -1,0 +1,170 @@
+"""GPU parity: latent codec (select_keyframes, solve_alpha, compress =
+intra x S + inter, wire format, decompress, stitch, fused decompress+stitch)
+against the reference golden fixtures and the restatement oracle.
+Integer/byte outputs and decompressed floats are compared bit-for-bit."""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+DIMS = (8, 8, 4)
+E = 256
+
+
+def bits(a):
+    a = np.ascontiguousarray(a)
+    return a.view(np.uint32)
+
+
+def test_golden_entries(fc):
+    z = np.load(os.path.join(GOLD, "codec_small.npz"))
+    ci = 0
+    while f"c{ci}_lat" in z:
+        ent = fc.compress(z[f"c{ci}_lat"], z[f"c{ci}_steps"], z[f"c{ci}_om"], z[f"c{ci}_bm"], DIMS, 1000 + ci)
+        wire = ent.serialize()
+        assert wire == bytes(z[f"c{ci}_entry"]), f"case {ci}"
+        assert fc.compressed_size(ent) == len(wire)
+        for s in (5, 10, 15, 20, 25):
+            assert (bits(fc.decompress_step(ent, s)) == bits(z[f"c{ci}_dec{s}"])).all()
+        maps = fc.select_keyframes(z[f"c{ci}_lat"], DIMS)
+        assert (maps == z[f"c{ci}_maps"]).all()
+        ci += 1
+
+
+@pytest.mark.parametrize("F,dims,seed", [(16, (40, 64, 4), 0), (64, (40, 64, 4), 1), (13, (7, 9, 3), 2)])
+def test_compress_batch_vs_oracle(fc, orc, synth, F, dims, seed):
+    n = 3
+    lat = np.stack([synth.latents(seed * 10 + i, F=F, dims=dims) for i in range(n)])
+    masks = [synth.rect_masks(F, dims[0], dims[1], seed * 10 + i) for i in range(n)]
+    om = np.stack([m[0] for m in masks])
+    bm = np.stack([m[1] for m in masks])
+    prompts = [500 + i for i in range(n)]
+    ents, sizes = fc.compress_batch(lat, synth.CACHED_STEPS, om, bm, dims, prompts)
+    E_ = dims[0] * dims[1] * dims[2]
+    for i in range(n):
+        ref_bytes = orc.compress(lat[i], synth.CACHED_STEPS, om[i], bm[i], dims, prompts[i])
+        assert ents[i].serialize() == ref_bytes
+        assert int(sizes[i]) == len(ref_bytes)
+        for s in synth.CACHED_STEPS:
+            assert (bits(fc.decompress_step(ents[i], s)) == bits(orc.decompress(ref_bytes, s, F, E_))).all()
+
+
+def test_edge_latents(fc, orc, synth):
+    dims = (40, 64, 4)
+    for lat in (synth.zero_motion(3, F=64), synth.latents(4, F=16, redundancy=(0, 0, 0, 0, 0)),
+                synth.latents(5, F=16, redundancy=(1, 1, 1, 1, 1))):
+        F = lat.shape[1]
+        om, bm = synth.rect_masks(F, 40, 64, 1)
+        ent = fc.compress(lat, synth.CACHED_STEPS, om, bm, dims, 9)
+        assert ent.serialize() == orc.compress(lat, synth.CACHED_STEPS, om, bm, dims, 9)
+    z = synth.zero_motion(1, F=64)
+    om, bm = synth.rect_masks(64, 40, 64, 1)
+    ent = fc.compress(z, synth.CACHED_STEPS, om, bm, dims, 7)
+    assert fc.compressed_size(ent) == 246435  # SPEC.md:202 zero-motion ratio 53.19
+    for s in synth.CACHED_STEPS:  # every frame bit-exact
+        dec = fc.decompress_step(ent, s)
+        assert (bits(dec) == bits(z[synth.CACHED_STEPS.index(s)])).all()
+
+
+def test_subset_and_single_step(fc, orc, synth):
+    dims = (16, 16, 4)
+    lat = synth.latents(8, F=12, dims=dims)
+    om, bm = synth.rect_masks(12, 16, 16, 8)
+    for steps, rows in (([10], [1]), ([25, 5, 15], [4, 0, 2])):
+        ent = fc.compress(lat[rows], steps, om, bm, dims, 3)
+        assert ent.serialize() == orc.compress(lat[rows], steps, om, bm, dims, 3)
+
+
+def test_errors(fc, synth):
+    dims = (8, 8, 4)
+    lat = synth.latents(3, F=4, dims=dims)
+    om, bm = synth.rect_masks(4, 8, 8, 3)
+    bad = lat.copy()
+    bad[1, 2, 5] = np.inf
+    with pytest.raises(fc.InvalidArgument):
+        fc.compress(bad, synth.CACHED_STEPS, om, bm, dims, 1)
+    zero = lat.copy()
+    zero[2, 1] = 0
+    with pytest.raises(fc.InvalidArgument):
+        fc.compress(zero, synth.CACHED_STEPS, om, bm, dims, 1)
+    with pytest.raises(fc.InvalidArgument):
+        fc.compress(lat, (5, 5, 10, 15, 20), om, bm, dims, 1)
+    with pytest.raises(fc.InvalidArgument):
+        fc.select_keyframes(lat[0], dims, threshold=0.0)
+    ent = fc.compress(lat, synth.CACHED_STEPS, om, bm, dims, 1)
+    with pytest.raises(fc.StepNotCached):
+        fc.decompress_step(ent, 7)
+    wire = ent.serialize()
+    for cut in (5, 40, len(wire) - 1):
+        with pytest.raises(fc.SnapshotError):
+            fc.deserialize_entry(wire[:cut])
+    with pytest.raises(fc.DegenerateBase):
+        fc.solve_alpha(np.ones(10, np.float32), np.zeros(10, np.float32))
+
+
+def test_wire_roundtrip(fc, synth):
+    dims = (40, 64, 4)
+    lat = synth.latents(12, F=16)
+    om, bm = synth.rect_masks(16, 40, 64, 12)
+    ent = fc.compress(lat, synth.CACHED_STEPS, om, bm, dims, 42)
+    wire = ent.serialize()
+    back = fc.deserialize_entry(wire)
+    assert back.serialize() == wire
+    for s in synth.CACHED_STEPS:
+        assert (bits(fc.decompress_step(back, s)) == bits(fc.decompress_step(ent, s))).all()
+
+
+def test_solve_alpha_and_cosine(fc, orc):
+    rng = np.random.default_rng(1)
+    ds = rng.standard_normal((20, 5000)).astype(np.float32)
+    db = rng.standard_normal((20, 5000)).astype(np.float32)
+    ga = fc.solve_alpha(ds, db)
+    oa = np.array([orc.solve_alpha(ds[i], db[i]) for i in range(20)], np.float32)
+    assert (bits(ga) == bits(oa)).all()
+    gc = fc.cosine_similarity(ds, db)
+    oc = np.array([orc.cosine(ds[i], db[i]) for i in range(20)])
+    assert (gc.view(np.uint64) == oc.view(np.uint64)).all()
+    v = rng.standard_normal((50, 768)).astype(np.float32)
+    assert (bits(fc.embedding_normalize(v)) == bits(orc.normalize_rows(v))).all()
+
+
+def test_stitch_golden_and_random(fc, orc, synth):
+    z = np.load(os.path.join(GOLD, "codec_small.npz"))
+    out = fc.stitch(z["stitch_obj"], z["stitch_om"], z["stitch_bg"], z["stitch_sm"], (4, 4, 1))
+    assert (bits(out) == bits(z["stitch_out"])).all()
+    dims = (40, 64, 4)
+    a = synth.latents(1, F=16)[2]
+    b = synth.latents(2, F=16)[2]
+    oo, ob = synth.rect_masks(16, 40, 64, 1)
+    bo, bb = synth.rect_masks(16, 40, 64, 2)
+    g = fc.stitch(a, oo, b, bo, dims)
+    o = orc.stitch(a, oo, ob, b, bo, bb, dims)
+    assert (bits(g) == bits(o)).all()
+    assert (bits(fc.stitch(a, oo, a, oo, dims)) == bits(a)).all()  # idempotence
+
+
+def test_decompress_stitch_fused(fc, orc, synth):
+    dims = (40, 64, 4)
+    F = 16
+    la, lb = synth.latents(21, F=F), synth.latents(22, F=F)
+    ma, mb = synth.rect_masks(F, 40, 64, 21), synth.rect_masks(F, 40, 64, 22)
+    ea = fc.compress(la, synth.CACHED_STEPS, ma[0], ma[1], dims, 1)
+    eb = fc.compress(lb, synth.CACHED_STEPS, mb[0], mb[1], dims, 2)
+    wa, wb = ea.serialize(), eb.serialize()
+    E_ = 40 * 64 * 4
+    for s in (5, 15, 25):
+        fused = fc.decompress_stitch([ea], [eb], [s])[0].cpu().numpy()
+        da, db = orc.decompress(wa, s, F, E_), orc.decompress(wb, s, F, E_)
+        ref = orc.stitch(da, ma[0], ma[1], db, mb[0], mb[1], dims)
+        assert (bits(fused) == bits(ref)).all()
+
+
+def test_inter_compress_with_maps(fc, orc, synth):
+    dims = (40, 64, 4)
+    lat = synth.latents(30, F=16)
+    om, bm = synth.rect_masks(16, 40, 64, 30)
+    maps = fc.select_keyframes(lat, dims)
+    ent = fc.inter_compress(lat, maps, synth.CACHED_STEPS, om, bm, dims, 99)
+    assert ent.serialize() == orc.compress(lat, synth.CACHED_STEPS, om, bm, dims, 99)

@@ -1,0 +1,144 @@
+"""GPU parity: CacheStore (GPU policy scoring + incremental eviction) against
+the reference-generated golden sequence and the restatement oracle: eviction
+order, evicted StepEntry records, used() bytes, hole fallback and served
+latents must be identical."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+DIMS = (8, 8, 4)
+
+
+def tup(e):
+    return list(e.as_tuple())
+
+
+def test_golden_sequences(fc):
+    z = np.load(os.path.join(GOLD, "codec_small.npz"))
+    entries = {}
+    ci = 0
+    while f"c{ci}_entry" in z:
+        entries[1000 + ci] = fc.deserialize_entry(bytes(z[f"c{ci}_entry"]))
+        ci += 1
+    for case in json.load(open(os.path.join(GOLD, "store_seq.json"))):
+        st = fc.CacheStore(case["capacity"], fc.Policy(case["policy"]))
+        for op in case["seq"]:
+            if op["op"] == "insert":
+                try:
+                    ev = st.insert_steps(op["prompt"], entries[op["prompt"]], op["steps"], op["now"])
+                    assert "error" not in op
+                    assert [tup(e) for e in ev] == op["evicted"]
+                except fc.LcacheError as e:
+                    assert op.get("error") == e.code, (op, e)
+            elif op["op"] == "get":
+                r = st.get_step(op["prompt"], op["desired"], op["now"], want_latent=False)
+                assert (r[1] if r else 0) == op["actual"]
+            elif op["op"] == "evict":
+                try:
+                    assert tup(st.evict_one(op["now"])) == op["victim"]
+                except fc.LcacheError as e:
+                    assert op.get("error") == e.code
+            else:
+                assert [tup(e) for e in st.entries_snapshot()] == op["entries"]
+                continue
+            assert st.used() == op["used"] == st.recompute_used()
+
+
+def _tiny_entries(fc, synth, n, seed):
+    """n small entries with varied sizes (F=4, 4x4x2)."""
+    dims = (4, 4, 2)
+    out = {}
+    rng = np.random.default_rng(seed)
+    for i in range(n):
+        r = tuple(float(x) for x in rng.uniform(0, 1, 5))
+        lat = synth.latents(seed * 1000 + i, F=4, dims=dims, redundancy=r)
+        om, bm = synth.rect_masks(4, 4, 4, i)
+        e = fc.compress(lat, synth.CACHED_STEPS, om, bm, dims, 10 + i)
+        out[10 + i] = (e, e.serialize())
+    return out
+
+
+@pytest.mark.parametrize("policy", [0, 1, 2, 3])
+def test_random_trace_vs_oracle(fc, orc, synth, policy):
+    ents = _tiny_entries(fc, synth, 300, policy)
+    sizes = sorted(len(w) for _, w in ents.values())
+    cap = sizes[len(sizes) // 2] * 60   # holds ~60 prompts: inserts evict, bursts exceed the 64-entry head
+    st = fc.CacheStore(cap, fc.Policy(policy))
+    ot = orc.store(cap, policy)
+    rng = np.random.default_rng(policy)
+    keys = list(ents)
+    now = 0
+    for it in range(1500):
+        now += int(rng.integers(0, 3))
+        p = int(rng.choice(keys))
+        op = rng.random()
+        if op < 0.45:
+            steps = sorted(int(x) for x in rng.choice(synth.CACHED_STEPS, size=int(rng.integers(1, 6)), replace=False))
+            try:
+                ev = [tup(e) for e in st.insert_steps(p, ents[p][0], steps, now)]
+                err = None
+            except fc.LcacheError as e:
+                ev, err = None, e.code
+            try:
+                oev = [list(e) for e in ot.insert(p, ents[p][1], steps, now)]
+                oerr = None
+            except Exception as e:
+                oev, oerr = None, e.code
+            assert (ev, err) == (oev, oerr), it
+        elif op < 0.85:
+            d = int(rng.choice(synth.CACHED_STEPS))
+            r = st.get_step(p, d, now)
+            oact, olat = ot.get_step(p, d, now, 4, 32)
+            assert (r[1] if r else 0) == oact
+            if r:
+                assert (r[0].cpu().numpy().view(np.uint32) == olat.view(np.uint32)).all()
+        elif op < 0.95:
+            if st.step_count():
+                assert tup(st.evict_one(now)) == list(ot.evict_one(now))
+            else:
+                with pytest.raises(fc.LogicError):
+                    st.evict_one(now)
+        else:
+            s = int(rng.choice(synth.CACHED_STEPS))
+            assert st.evict_step(p, s) == ot.evict_step(p, s)
+        assert st.used() == ot.used() == st.recompute_used()
+        assert st.used() <= cap
+    assert [tup(e) for e in st.entries_snapshot()] == [list(e) for e in ot.entries()]
+
+
+def test_hole_fallback_and_oversize(fc, synth):
+    ents = _tiny_entries(fc, synth, 2, 99)
+    e, w = ents[10]
+    st = fc.CacheStore(10 ** 9, fc.Policy.Lrbu)
+    st.insert_steps(10, e, [5, 10, 15, 20, 25], 1)
+    assert st.evict_step(10, 10)
+    r = st.get_step(10, 10, 2)
+    assert r[1] == 5  # SPEC.md:363 hole rule
+    assert st.cached_steps(10) == [5, 15, 20, 25]
+    with pytest.raises(fc.InvalidArgument):
+        st.get_step(10, 7, 3)
+    small = fc.CacheStore(100, fc.Policy.Lrbu)
+    with pytest.raises(fc.OversizedEntry) as ei:
+        small.insert_steps(10, e, [5], 1)
+    assert ei.value.capacity_limit == 100 and ei.value.needed_bytes > 100
+    gone = []
+    st2 = fc.CacheStore(len(w), fc.Policy.Fifo)
+    st2.set_eviction_callback(gone.append)
+    st2.insert_steps(10, e, [5, 10, 15, 20, 25], 1)
+    st2.insert_steps(11, ents[11][0], [5], 2)
+    assert 10 in gone
+
+
+def test_priority_functions(fc):
+    e = fc.StepEntry(prompt=1, step=5, f=0, last_access=0, inserted_at=0, inserted_seq=0, capacity=1)
+    assert fc.lrbu_priority(e, 1) == 5.0
+    e.capacity = 2
+    assert fc.lrbu_priority(e, 1) == 2.5
+    assert fc.lcbfu_priority(fc.StepEntry(step=25, f=0, capacity=1)) == 25
+    assert fc.lcbfu_priority(fc.StepEntry(step=5, f=9, capacity=1)) == 50
+    with pytest.raises(fc.InvalidArgument):
+        fc.lrbu_priority(fc.StepEntry(step=5, f=0, last_access=10, capacity=1), 5)
