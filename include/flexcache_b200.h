@@ -99,6 +99,11 @@ void* lc_ctx_stream(lc_ctx* ctx);
 lc_status lc_ctx_synchronize(lc_ctx* ctx);
 /* Number of product kernels launched through this context (instrumentation). */
 uint64_t lc_ctx_launches(lc_ctx* ctx);
+/* Per-kernel CUDA-event timing on the context stream (bench/roofline):
+ * names "shortlist" (tcgen05 lookup GEMM), "rescore", "scan", "decompress",
+ * "decompress_stitch", "gram", "inter", "pack", "policy". */
+lc_status lc_ctx_profile(lc_ctx* ctx, int enable);
+lc_status lc_ctx_kernel_time(lc_ctx* ctx, const char* name, uint64_t* launches, double* total_ms, int reset);
 
 /* ---------------------------------------------------------------------------
  * Core primitives (core.cpp:50-119).

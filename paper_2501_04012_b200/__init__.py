@@ -149,11 +149,24 @@ def _is_dev(a):
 class Context:
     """One GPU + stream (lc_ctx)."""
 
-    def __init__(self, device: int = 0):
+    def __init__(self, device: int = 0, stream: int | None = None):
+        """stream: a cudaStream_t value to issue on; default = torch's current
+        stream on `device` (so library work is stream-ordered with torch ops on
+        the tensors it reads/writes); 1 = cudaStreamLegacy."""
         h = C.c_void_p()
         _check(lib.lc_ctx_create(device, C.byref(h)))
         self.h = h
         self.device = device
+        if stream is None:
+            try:
+                import torch
+                if torch.cuda.is_available():
+                    s = torch.cuda.current_stream(device).cuda_stream
+                    stream = s if s else 1
+            except ImportError:
+                stream = None
+        if stream:
+            self.set_stream(stream)
 
     def set_stream(self, stream_ptr: int | None):
         _check(lib.lc_ctx_set_stream(self.h, C.c_void_p(stream_ptr) if stream_ptr else None))

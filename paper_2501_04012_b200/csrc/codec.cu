@@ -167,6 +167,13 @@ __global__ void k_select(const double* __restrict__ G, int n_items, int F, doubl
   }
 }
 
+__global__ void k_diag(const double* __restrict__ G, int64_t n_items, int F, double* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n_items * F) return;
+  const int64_t item = i / F, j = i - item * F;
+  out[i] = G[item * F * F + j * F + j];
+}
+
 constexpr int MAXS = 8;
 struct InterRes {
   double sim[MAXS][MAXS];    // [s][b]: safe_similarity(recon_s under base b, key_s)
@@ -436,7 +443,9 @@ void gram(lc_ctx* ctx, const float* lat, int n_items, const Geo& g, double* G) {
   const int FP = (g.F + 7) & ~7;
   const size_t smem = (size_t)(4096 / FP) * (FP + 2) * sizeof(double);
   FC_CUDA(cudaFuncSetAttribute(k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  KTimer kt(ctx, "gram");
   k_gram<<<n_items, 64, smem, ctx->stream>>>(lat, g.F, g.E, G);
+  kt.stop();
   FC_LAUNCH_CHECK();
   count_launch(ctx);
 }
@@ -477,9 +486,9 @@ void assemble(lc_ctx* ctx, const float* lat, const uint8_t* om, const uint8_t* b
   std::vector<double> diag((size_t)n * S * F);
   {
     DevBuf d((size_t)n * S * F * sizeof(double), ctx->stream);
-    // strided copy of the diagonals
-    FC_CUDA(cudaMemcpy2DAsync(d.p, sizeof(double), G_dev, (size_t)(F + 1) * sizeof(double), sizeof(double),
-                              (size_t)n * S * F, cudaMemcpyDeviceToDevice, ctx->stream));
+    k_diag<<<grid_for((int64_t)n * S * F, 256), 256, 0, ctx->stream>>>(G_dev, (int64_t)n * S, F, d.as<double>());
+    FC_LAUNCH_CHECK();
+    count_launch(ctx);
     FC_CUDA(cudaMemcpyAsync(diag.data(), d.p, diag.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     sync(ctx);
   }
@@ -490,6 +499,7 @@ void assemble(lc_ctx* ctx, const float* lat, const uint8_t* om, const uint8_t* b
         dp(S * sizeof(int), ctx->stream);
     FC_CUDA(cudaMemcpyAsync(di.p, items.data(), di.bytes, cudaMemcpyHostToDevice, ctx->stream));
     FC_CUDA(cudaMemcpyAsync(dp.p, perm.data(), dp.bytes, cudaMemcpyHostToDevice, ctx->stream));
+    KTimer kt(ctx, "inter");
     k_inter<<<(unsigned)items.size(), INTER_T, 0, ctx->stream>>>(lat, di.as<InterItem>(), S, dp.as<int>(), F, E, G_dev,
                                                                   dr.as<InterRes>());
     FC_LAUNCH_CHECK();
@@ -661,6 +671,7 @@ void assemble(lc_ctx* ctx, const float* lat, const uint8_t* om, const uint8_t* b
   DevBuf dfj(fjobs.size() * sizeof(FrameJob), ctx->stream), dbj(bjobs.size() * sizeof(ByteJob), ctx->stream);
   FC_CUDA(cudaMemcpyAsync(dfj.p, fjobs.data(), dfj.bytes, cudaMemcpyHostToDevice, ctx->stream));
   FC_CUDA(cudaMemcpyAsync(dbj.p, bjobs.data(), dbj.bytes, cudaMemcpyHostToDevice, ctx->stream));
+  KTimer ktp(ctx, "pack");
   for (size_t j0 = 0; j0 < fjobs.size(); j0 += 65535) {
     const unsigned cnt = (unsigned)std::min<size_t>(65535, fjobs.size() - j0);
     k_pack_frames<<<dim3(grid_for(E, 256, 64), cnt), 256, 0, ctx->stream>>>(dfj.as<FrameJob>() + j0, E);
@@ -671,6 +682,7 @@ void assemble(lc_ctx* ctx, const float* lat, const uint8_t* om, const uint8_t* b
     k_pack_bytes<<<dim3(8, cnt), 256, 0, ctx->stream>>>(dbj.as<ByteJob>() + j0);
     FC_LAUNCH_CHECK();
   }
+  ktp.stop();
   count_launch(ctx, 2);
   sync(ctx);
   for (int64_t e = 0; e < n; ++e) {
@@ -712,7 +724,9 @@ void launch_decompress(lc_ctx* ctx, const std::vector<const EntryData*>& ents, c
   DevBuf di(items.size() * sizeof(DecItem), ctx->stream);
   FC_CUDA(cudaMemcpyAsync(di.p, items.data(), di.bytes, cudaMemcpyHostToDevice, ctx->stream));
   const unsigned gy = (unsigned)((E + 1023) / 1024);
+  KTimer kt(ctx, "decompress");
   k_decompress<<<dim3((unsigned)(items.size() * F), gy), 256, 0, ctx->stream>>>(di.as<DecItem>(), F, E);
+  kt.stop();
   FC_LAUNCH_CHECK();
   count_launch(ctx);
 }
@@ -1145,6 +1159,7 @@ lc_status lc_decompress_stitch_batch(lc_ctx* ctx, lc_entry* const* oe, lc_entry*
   DevBuf di(items.size() * sizeof(StitchItem), ctx->stream);
   FC_CUDA(cudaMemcpyAsync(di.p, items.data(), di.bytes, cudaMemcpyHostToDevice, ctx->stream));
   const unsigned gy = (unsigned)((d0->E + 1023) / 1024);
+  KTimer kt(ctx, "decompress_stitch");
   k_decompress_stitch<<<dim3((unsigned)(n * d0->F), gy), 256, 0, ctx->stream>>>(di.as<StitchItem>(), d0->F, d0->E, d0->C,
                                                                                 d0->mb);
   FC_LAUNCH_CHECK();

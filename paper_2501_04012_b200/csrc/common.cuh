@@ -9,6 +9,8 @@
 
 #include <atomic>
 #include <cstdio>
+#include <map>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -69,7 +71,35 @@ struct lc_ctx {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   std::atomic<uint64_t> launches{0};
+  // per-kernel CUDA-event timing (lc_ctx_profile / lc_ctx_kernel_time)
+  bool profile = false;
+  std::mutex prof_mu;
+  std::map<std::string, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>> prof;
 };
+
+namespace fc {
+// Records a CUDA event pair around the launches in its scope (on the
+// context stream) when profiling is enabled.
+struct KTimer {
+  lc_ctx* ctx;
+  const char* name;
+  cudaEvent_t a = nullptr, b = nullptr;
+  KTimer(lc_ctx* c, const char* n) : ctx(c), name(n) {
+    if (!ctx->profile) return;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, ctx->stream);
+  }
+  void stop() {
+    if (!a) return;
+    cudaEventRecord(b, ctx->stream);
+    std::lock_guard<std::mutex> g(ctx->prof_mu);
+    ctx->prof[name].emplace_back(a, b);
+    a = nullptr;
+  }
+  ~KTimer() { stop(); }
+};
+}  // namespace fc
 
 namespace fc {
 

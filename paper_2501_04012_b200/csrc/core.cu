@@ -248,6 +248,40 @@ lc_status lc_ctx_synchronize(lc_ctx* ctx) {
 
 uint64_t lc_ctx_launches(lc_ctx* ctx) { return ctx ? ctx->launches.load() : 0; }
 
+lc_status lc_ctx_profile(lc_ctx* ctx, int enable) {
+  LC_API_BEGIN
+  ctx->profile = enable != 0;
+  LC_API_END
+}
+
+lc_status lc_ctx_kernel_time(lc_ctx* ctx, const char* name, uint64_t* launches, double* total_ms, int reset) {
+  LC_API_BEGIN
+  DeviceGuard g(ctx->device);
+  sync(ctx);
+  std::lock_guard<std::mutex> lk(ctx->prof_mu);
+  uint64_t n = 0;
+  double ms = 0.0;
+  auto it = ctx->prof.find(name ? name : "");
+  if (it != ctx->prof.end()) {
+    for (auto& pr : it->second) {
+      float t = 0.f;
+      FC_CUDA(cudaEventElapsedTime(&t, pr.first, pr.second));
+      ms += t;
+      ++n;
+    }
+    if (reset) {
+      for (auto& pr : it->second) {
+        cudaEventDestroy(pr.first);
+        cudaEventDestroy(pr.second);
+      }
+      ctx->prof.erase(it);
+    }
+  }
+  if (launches) *launches = n;
+  if (total_ms) *total_ms = ms;
+  LC_API_END
+}
+
 lc_status lc_embedding_normalize(lc_ctx* ctx, const float* v, int64_t n, int dim, float* out) {
   LC_API_BEGIN
   FC_REQUIRE(dim > 0, "Embedding: empty vector");

@@ -340,6 +340,7 @@ void exact_scan(lc_index* ix, int kind, const float* Qdev, const int32_t* qlist_
   const size_t smem = (size_t)SCAN_QB * dim * sizeof(float);
   if (smem > 48 * 1024) FC_CUDA(cudaFuncSetAttribute(k_scan_partial, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   dim3 grid(nblk, (nq + SCAN_QB - 1) / SCAN_QB);
+  KTimer kt(ctx, "scan");
   k_scan_partial<<<grid, SCAN_T, smem, ctx->stream>>>(Qdev, qlist_dev, nq, ix->rows[kind], ix->ids_dev, ix->n, dim, k,
                                                       partial.as<Cand>(), pcount.as<int32_t>());
   FC_LAUNCH_CHECK();
@@ -347,6 +348,7 @@ void exact_scan(lc_index* ix, int kind, const float* Qdev, const int32_t* qlist_
     k_scan_merge<8><<<nq, 256, 0, ctx->stream>>>(partial.as<Cand>(), pcount.as<int32_t>(), nblk, k, qlist_dev, oid, osc, ocnt);
   else
     k_scan_merge<64><<<nq, 256, 0, ctx->stream>>>(partial.as<Cand>(), pcount.as<int32_t>(), nblk, k, qlist_dev, oid, osc, ocnt);
+  kt.stop();
   FC_LAUNCH_CHECK();
   count_launch(ctx, 2);
 }
@@ -376,6 +378,7 @@ void query_dev(lc_index* ix, int kind, const float* Qdev, int nq, int k, uint64_
   auto* err_bits = reinterpret_cast<unsigned long long*>(fn.as<char>() + 8);
   FC_CUDA(cudaMemsetAsync(fn.p, 0, 16, ctx->stream));
   const unsigned g = (unsigned)((nq + RS_WARPS - 1) / RS_WARPS);
+  KTimer kt(ctx, "rescore");
   if (kp <= 32)
     k_rescore<1><<<g, RS_WARPS * 32, 0, ctx->stream>>>(Qdev, nq, ix->dim, ix->rows[kind], ix->ids_dev, cs.as<float>(),
                                                        cr.as<uint32_t>(), cn.as<int32_t>(), kp, k, ix->eps, oid, osc, ocnt,
@@ -388,6 +391,7 @@ void query_dev(lc_index* ix, int kind, const float* Qdev, int nq, int k, uint64_
     k_rescore<4><<<g, RS_WARPS * 32, 0, ctx->stream>>>(Qdev, nq, ix->dim, ix->rows[kind], ix->ids_dev, cs.as<float>(),
                                                        cr.as<uint32_t>(), cn.as<int32_t>(), kp, k, ix->eps, oid, osc, ocnt,
                                                        fl.as<int32_t>(), fail_n, err_bits);
+  kt.stop();
   FC_LAUNCH_CHECK();
   count_launch(ctx);
   int32_t hf[4] = {0, 0, 0, 0};

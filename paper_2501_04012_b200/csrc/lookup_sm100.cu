@@ -479,7 +479,9 @@ static void launch_shortlist(lc_ctx* ctx, const ApproxPlan& plan, sm100::Params 
   auto kern = sm100::k_shortlist<BN, NSTAGE>;
   FC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = std::min(prm.n_units, ctx->sm_count);
+  KTimer kt(ctx, "shortlist");
   kern<<<grid, sm100::NTHREADS, smem, ctx->stream>>>(plan.tmap, prm);
+  kt.stop();
   FC_LAUNCH_CHECK();
 }
 

@@ -264,11 +264,13 @@ struct lc_store {
     DevBuf head(HEAD * sizeof(Cand) + 16, ctx->stream);
     DevBuf bad(sizeof(int), ctx->stream);
     FC_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), ctx->stream));
+    KTimer kt(ctx, "policy");
     k_policy_head<<<nblk, POL_T, 0, ctx->stream>>>(dl, n_slots, dp, policy, now, partial.as<Cand>(), pc.as<int32_t>(),
                                                    bad.as<int>());
     FC_LAUNCH_CHECK();
     k_head_merge<<<1, 256, 0, ctx->stream>>>(partial.as<Cand>(), pc.as<int32_t>(), nblk, head.as<Cand>(),
                                              reinterpret_cast<int32_t*>(head.as<Cand>() + HEAD));
+    kt.stop();
     FC_LAUNCH_CHECK();
     count_launch(ctx, 2);
     std::vector<Cand> h(HEAD);

@@ -126,11 +126,11 @@ def test_hole_fallback_and_oversize(fc, synth):
         small.insert_steps(10, e, [5], 1)
     assert ei.value.capacity_limit == 100 and ei.value.needed_bytes > 100
     gone = []
-    st2 = fc.CacheStore(len(w), fc.Policy.Fifo)
+    st2 = fc.CacheStore(len(ents[11][1]), fc.Policy.Fifo)  # exactly prompt 11's full entry
     st2.set_eviction_callback(gone.append)
-    st2.insert_steps(10, e, [5, 10, 15, 20, 25], 1)
-    st2.insert_steps(11, ents[11][0], [5], 2)
-    assert 10 in gone
+    st2.insert_steps(10, e, [5], 1)
+    st2.insert_steps(11, ents[11][0], [5, 10, 15, 20, 25], 2)  # must evict all of prompt 10
+    assert gone == [10] and not st2.contains(10) and st2.used() == st2.capacity_limit()
 
 
 def test_priority_functions(fc):
