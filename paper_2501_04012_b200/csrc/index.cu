@@ -45,7 +45,7 @@ struct lc_index {
   std::vector<uint64_t> ids;
   std::unordered_map<uint64_t, int64_t> slot;
   int mode = 0;
-  int kprime = 64;
+  int kprime = 32;
   double eps = 0.00390625 + 0.000244140625;  // 2^-8 + 2^-12, see lookup.cuh
   lc_lookup_stats stats{};
   ApproxPlan plan[3];
@@ -187,7 +187,7 @@ template <int PER_LANE>
 __global__ void __launch_bounds__(RS_WARPS * 32)
     k_rescore(const float* __restrict__ Q, int nq, int dim, const float* __restrict__ rows,
               const uint64_t* __restrict__ ids, const float* __restrict__ cand_s, const uint32_t* __restrict__ cand_r,
-              const int32_t* __restrict__ cand_n, int kp, int k, double eps, uint64_t* __restrict__ out_ids,
+              const int32_t* __restrict__ cand_n, int kp, int64_t n_rows, int k, double eps, uint64_t* __restrict__ out_ids,
               double* __restrict__ out_sc, int32_t* __restrict__ out_cnt, int32_t* __restrict__ fail_list,
               int32_t* __restrict__ fail_n, unsigned long long* __restrict__ max_err_bits) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -254,9 +254,12 @@ __global__ void __launch_bounds__(RS_WARPS * 32)
     }
     out_cnt[q] = got;
     // Certification: rows outside the shortlist have approx <= min_approx.
-    // A shortlist shorter than K' holds every row of the table.
-    const bool full = cn >= kp;
-    const bool ok = !full || (got >= k && (double)min_approx + eps < tk);
+    // A shortlist holding every row needs no margin; one shorter than
+    // min(K', rows) can only come from a fault and is never trusted.
+    bool ok;
+    if (cn < (kp < n_rows ? kp : n_rows)) ok = false;
+    else if (cn >= n_rows) ok = true;
+    else ok = got >= k && (double)min_approx + eps < tk;
     if (!ok) fail_list[atomicAdd(fail_n, 1)] = q;
   }
 }
@@ -381,15 +384,15 @@ void query_dev(lc_index* ix, int kind, const float* Qdev, int nq, int k, uint64_
   KTimer kt(ctx, "rescore");
   if (kp <= 32)
     k_rescore<1><<<g, RS_WARPS * 32, 0, ctx->stream>>>(Qdev, nq, ix->dim, ix->rows[kind], ix->ids_dev, cs.as<float>(),
-                                                       cr.as<uint32_t>(), cn.as<int32_t>(), kp, k, ix->eps, oid, osc, ocnt,
+                                                       cr.as<uint32_t>(), cn.as<int32_t>(), kp, ix->n, k, ix->eps, oid, osc, ocnt,
                                                        fl.as<int32_t>(), fail_n, err_bits);
   else if (kp <= 64)
     k_rescore<2><<<g, RS_WARPS * 32, 0, ctx->stream>>>(Qdev, nq, ix->dim, ix->rows[kind], ix->ids_dev, cs.as<float>(),
-                                                       cr.as<uint32_t>(), cn.as<int32_t>(), kp, k, ix->eps, oid, osc, ocnt,
+                                                       cr.as<uint32_t>(), cn.as<int32_t>(), kp, ix->n, k, ix->eps, oid, osc, ocnt,
                                                        fl.as<int32_t>(), fail_n, err_bits);
   else
     k_rescore<4><<<g, RS_WARPS * 32, 0, ctx->stream>>>(Qdev, nq, ix->dim, ix->rows[kind], ix->ids_dev, cs.as<float>(),
-                                                       cr.as<uint32_t>(), cn.as<int32_t>(), kp, k, ix->eps, oid, osc, ocnt,
+                                                       cr.as<uint32_t>(), cn.as<int32_t>(), kp, ix->n, k, ix->eps, oid, osc, ocnt,
                                                        fl.as<int32_t>(), fail_n, err_bits);
   kt.stop();
   FC_LAUNCH_CHECK();

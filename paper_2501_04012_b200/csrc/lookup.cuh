@@ -22,7 +22,8 @@ struct ApproxPlan {
   int dim = 0;
   int bn = 64;
   const __nv_bfloat16* rows = nullptr;
-  alignas(64) CUtensorMap tmap;
+  alignas(64) CUtensorMap tmap;   // box [bn rows][64]   (single-CTA kernel)
+  alignas(64) CUtensorMap tmap2;  // box [bn/2 rows][64] (CTA-pair kernel: each CTA loads half a tile)
 };
 
 bool approx_available();

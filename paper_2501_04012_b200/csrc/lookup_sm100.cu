@@ -90,6 +90,99 @@ __device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_
       : "memory");
 }
 
+// Four K=16 MMAs over one 64-wide K box in a single asm block: ptxas moves
+// the three base operands into uniform registers once instead of once per
+// MMA. A advances 8 TMEM columns (16 bf16) and B 32 bytes (desc += 2) per MMA.
+__device__ __forceinline__ void mma_box4(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                         uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p, t;\n"
+      ".reg .b64 d1, d2, d3;\n"
+      ".reg .b32 a1, a2, a3;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "setp.eq.b32 t, 0, 0;\n"
+      "add.s64 d1, %2, 2;\n"
+      "add.s64 d2, %2, 4;\n"
+      "add.s64 d3, %2, 6;\n"
+      "add.u32 a1, %1, 8;\n"
+      "add.u32 a2, %1, 16;\n"
+      "add.u32 a3, %1, 24;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], d1, %3, t;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], d2, %3, t;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], d3, %3, t;\n"
+      "}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+// ---- CTA-pair (cta_group::2) primitives ----
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// arrive on the barrier at the same smem offset in CTA `cta` of the cluster
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t bar, uint32_t cta) {
+  asm volatile(
+      "{\n.reg .b32 ra;\nmapa.shared::cluster.u32 ra, %0, %1;\n"
+      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n}" ::"r"(bar),
+      "r"(cta)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAITC_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAITC_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(phase)
+      : "memory");
+}
+// TMA into this CTA's smem, completion bytes counted on the LEADER's barrier
+// (peer bit cleared), as the pair's MMA consumes both halves at once.
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, uint32_t bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar & 0xFEFFFFFFu)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_pair(uint32_t bar) {
+  asm volatile(
+      "{\n.reg .b16 m;\nmov.b16 m, 3;\n"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n}" ::"r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void mma_box4_pair(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                              uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p, t;\n"
+      ".reg .b64 d1, d2, d3;\n"
+      ".reg .b32 a1, a2, a3;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "setp.eq.b32 t, 0, 0;\n"
+      "add.s64 d1, %2, 2;\n"
+      "add.s64 d2, %2, 4;\n"
+      "add.s64 d3, %2, 6;\n"
+      "add.u32 a1, %1, 8;\n"
+      "add.u32 a2, %1, 16;\n"
+      "add.u32 a3, %1, 24;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [a1], d1, %3, t;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [a2], d2, %3, t;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [a3], d3, %3, t;\n"
+      "}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
 // K-major operand tile written by TMA with SWIZZLE_128B: rows of 128 B,
 // 8-row atoms of 1024 B (SBO), LBO unused (1), descriptor version 1 (sm100).
 __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t addr) {
@@ -136,28 +229,64 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* r) {
       : "memory");
 }
 
-// Replace-min insert into the thread's (query's) shortlist; rare after the
-// first few tiles, so it is kept out of line to keep the filter loop tight.
-__device__ __noinline__ void list_insert(float* ls, uint32_t* lr, int t, int kp, float v, uint32_t row, int& cnt,
-                                         int& minpos, float& tau) {
-  int at;
-  if (cnt < kp) {
-    at = cnt++;
-  } else {
-    at = minpos;
+__device__ __forceinline__ uint32_t okey(float f) {
+  const uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+// Shrink the thread's (query's) candidate buffer to its kp best entries and
+// raise the acceptance threshold tau to the kp-th best score. Exact: T is
+// found by a binary search on the order-preserving key; entries > T are kept,
+// ties at T fill up to kp. Called warp-uniformly and rarely (the buffer only
+// fills after ~64 accepted scores), so the per-score filter stays branch-free.
+__device__ __noinline__ void compact(float* ls, uint32_t* lr, int t, int& cnt, int kp, float& tau) {
+  if (cnt <= kp) return;
+  uint32_t lo = 0, hi = 0xFFFFFFFFu;
+  while (lo < hi) {  // max T with count(key >= T) >= kp
+    const uint32_t mid = lo + (uint32_t)(((uint64_t)hi - lo + 1) >> 1);
+    int c = 0;
+    for (int i = 0; i < cnt; ++i) c += okey(ls[i * BM + t]) >= mid;
+    if (c >= kp) lo = mid; else hi = mid - 1;
   }
-  ls[at * BM + t] = v;
-  lr[at * BM + t] = row;
-  if (cnt == kp) {
-    float m = ls[t];
-    int mp = 0;
-    for (int i = 1; i < kp; ++i) {
-      const float x = ls[i * BM + t];
-      if (x < m) { m = x; mp = i; }
+  const uint32_t T = lo;
+  int above = 0;
+  for (int i = 0; i < cnt; ++i) above += okey(ls[i * BM + t]) > T;
+  int need_eq = kp - above, w = 0;
+  for (int i = 0; i < cnt; ++i) {
+    const float v = ls[i * BM + t];
+    const uint32_t k = okey(v);
+    const bool keep = k > T || (k == T && need_eq > 0);
+    need_eq -= (k == T && keep);
+    if (keep) {
+      ls[w * BM + t] = v;
+      lr[w * BM + t] = lr[i * BM + t];
+      ++w;
     }
-    tau = m;
-    minpos = mp;
   }
+  cnt = w;
+  const float tnew = __uint_as_float((T & 0x80000000u) ? (T & 0x7FFFFFFFu) : ~T);
+  if (tnew > tau) tau = tnew;  // never lower a (possibly shared) threshold
+}
+
+__device__ __forceinline__ float key_float(uint32_t k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k);
+}
+
+// Shared per-query threshold (order-preserving key, 0 = unset): the K'-th
+// best bf16 score of ANY completed work unit is a lower bound on the K'-th
+// best over the whole table, so every unit of that query may drop scores
+// <= it. Later units then accept only a handful of candidates.
+__device__ __forceinline__ void refresh_tau(const uint32_t* gkey, int q, float& tau) {
+  uint32_t k;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(k) : "l"(gkey + q));
+  if (k && key_float(k) > tau) tau = key_float(k);
+}
+
+__device__ __forceinline__ void publish_tau(uint32_t* gkey, int q, const float* ls, int t, int cnt, int kp) {
+  if (cnt < kp) return;
+  float m = ls[t];
+  for (int i = 1; i < cnt; ++i) m = fminf(m, ls[i * BM + t]);
+  atomicMax(gkey + q, okey(m));
 }
 
 struct Params {
@@ -170,26 +299,32 @@ struct Params {
   int n_splits;
   int n_units;
   int kp;
+  int cap;     // candidate buffer slots per query (>= kp + 16)
+  int bps;     // TMA boxes per pipeline stage
+  uint32_t* gkey;  // [nq_pad] shared per-query thresholds (order keys, 0 = unset)
+  int debug;   // diagnostics (FC_SHORTLIST_DEBUG): 1 = skip MMA, 2 = skip TMA, 4 = skip epilogue filter
+  int nstage;
   float* part_s;             // [nq][n_splits][kp]
   uint32_t* part_r;
   int32_t* part_n;           // [nq][n_splits]
 };
 
-template <int BN, int NSTAGE>
-struct Smem {
-  static constexpr int STAGE_BYTES = BN * 128;
-};
+constexpr int MAX_STAGE = 24;
 
-template <int BN, int NSTAGE>
+template <int BN>
 __global__ void __launch_bounds__(NTHREADS, 1) k_shortlist(const __grid_constant__ CUtensorMap tmap, Params p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  // carve: [stages][BN*128] | list scores [kp][128] | list rows [kp][128] | barriers | tmem addr
+  // carve: [stages][BN*128] | cand scores [cap][128] | cand rows [cap][128] | barriers | tmem addr
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  constexpr int STAGE_BYTES = BN * 128;
+  constexpr int BOX_BYTES = BN * 128;  // one TMA box: BN rows x 64 bf16
+  const int BPS = p.bps;               // boxes per pipeline stage (one barrier per stage)
+  const int STAGE_BYTES = BPS * BOX_BYTES;
+  const int NSTAGE = p.nstage;
+  const int cap = p.cap;
   uint8_t* stages = base;
   float* ls = reinterpret_cast<float*>(base + NSTAGE * STAGE_BYTES);
-  uint32_t* lr = reinterpret_cast<uint32_t*>(ls + p.kp * BM);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(lr + p.kp * BM);
+  uint32_t* lr = reinterpret_cast<uint32_t*>(ls + cap * BM);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(lr + cap * BM);
   uint64_t* full = bars;
   uint64_t* empty = bars + NSTAGE;
   uint64_t* accf = bars + 2 * NSTAGE;
@@ -199,6 +334,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_shortlist(const __grid_constant
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nkb = p.dim / BK;
+  const int nsg = nkb / BPS;  // pipeline stages per tile
   const int a_cols = p.dim / 2;
 
   if (threadIdx.x == 0) {
@@ -233,10 +369,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_shortlist(const __grid_constant
         const int64_t r0 = (int64_t)split * p.rows_per_split;
         const int64_t r1 = min((int64_t)p.n_rows, r0 + p.rows_per_split);
         for (int64_t row = r0; row < r1; row += BN) {
-          for (int kb = 0; kb < nkb; ++kb) {
+          for (int sg = 0; sg < nsg; ++sg) {
             mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
-            mbar_expect_tx(smem_u32(&full[stage]), STAGE_BYTES);
-            tma_load_2d(smem_u32(stages + stage * STAGE_BYTES), &tmap, smem_u32(&full[stage]), kb * BK, (int)row);
+            if (p.debug & 2) {  // diagnostic: no table traffic
+              mbar_arrive(smem_u32(&full[stage]));
+            } else {
+              mbar_expect_tx(smem_u32(&full[stage]), STAGE_BYTES);
+              for (int bx = 0; bx < BPS; ++bx)
+                tma_load_2d(smem_u32(stages + stage * STAGE_BYTES + bx * BOX_BYTES), &tmap, smem_u32(&full[stage]),
+                            (sg * BPS + bx) * BK, (int)row);
+            }
             if (++stage == NSTAGE) {
               stage = 0;
               phase ^= 1;
@@ -265,15 +407,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_shortlist(const __grid_constant
         mbar_wait(smem_u32(&acce[b]), (use & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem + a_cols + b * BN;
-        for (int kb = 0; kb < nkb; ++kb) {
+        for (int sg = 0; sg < nsg; ++sg) {
           mbar_wait(smem_u32(&full[stage]), phase);
           tc_fence_after();
           if (lane == 0) {
             const uint32_t sa = smem_u32(stages + stage * STAGE_BYTES);
-#pragma unroll
-            for (int k = 0; k < BK / 16; ++k) {
-              const uint64_t bdesc = smem_desc_sw128(sa + k * 32);
-              mma_ts(d_tmem, tmem + (kb * (BK / 16) + k) * 8, bdesc, idesc, (kb | k) != 0);
+            if (!(p.debug & 1)) {  // debug bit 0: diagnostic run without MMAs
+              for (int bx = 0; bx < BPS; ++bx) {
+                const int kb = sg * BPS + bx;
+                mma_box4(d_tmem, tmem + kb * (BK / 16) * 8, smem_desc_sw128(sa + bx * BOX_BYTES), idesc, kb != 0);
+              }
             }
             tc_commit(smem_u32(&empty[stage]));
           }
@@ -299,6 +442,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_shortlist(const __grid_constant
       const int qtile = u - split * p.n_qtiles;
       const int64_t r0 = (int64_t)split * p.rows_per_split;
       const int64_t r1 = min((int64_t)p.n_rows, r0 + p.rows_per_split);
+      const int q = qtile * BM + t;
       // (1) load this unit's 128 queries into TMEM columns [0, dim/2)
       {
         const uint4* src = reinterpret_cast<const uint4*>(p.Qb + (size_t)(qtile * BM + t) * p.dim);
@@ -318,12 +462,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_shortlist(const __grid_constant
         tc_fence_before();
         mbar_arrive(smem_u32(aready));
       }
-      // (2) stream the accumulator tiles, keep the per-query top-kp
-      int cnt = 0, minpos = 0;
+      // (2) stream the accumulator tiles; branch-free append of every score
+      //     above the running threshold, warp-uniform compaction when full
+      int cnt = 0;
       float tau = -INFINITY;
+      refresh_tau(p.gkey, q, tau);
       for (int64_t row = r0; row < r1; row += BN, ++tile) {
         const uint32_t b = tile & 1;
         const uint32_t use = tile >> 1;
+        if ((tile & 15) == 0) refresh_tau(p.gkey, q, tau);
         mbar_wait(smem_u32(&accf[b]), use & 1);
         tc_fence_after();
 #pragma unroll
@@ -336,13 +483,26 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_shortlist(const __grid_constant
           }
           const int64_t rbase = row + h * 64;
           const int lim = (int)min((int64_t)64, r1 - rbase);
+          const uint32_t r32 = (uint32_t)rbase;
 #pragma unroll
-          for (int j = 0; j < 64; ++j)
-            if (j < lim && v[j] > tau) list_insert(ls, lr, t, p.kp, v[j], (uint32_t)(rbase + j), cnt, minpos, tau);
+          for (int c = 0; c < ((p.debug & 4) ? 0 : 4); ++c) {
+            if (__any_sync(0xffffffffu, cnt + 16 > cap)) compact(ls, lr, t, cnt, p.kp, tau);
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj) {
+              const int j = c * 16 + jj;
+              const bool acc = (j < lim) & (v[j] > tau);
+              if (acc) {
+                ls[cnt * BM + t] = v[j];
+                lr[cnt * BM + t] = r32 + j;
+              }
+              cnt += acc;
+            }
+          }
         }
       }
+      compact(ls, lr, t, cnt, p.kp, tau);
+      publish_tau(p.gkey, q, ls, t, cnt, p.kp);
       // (3) write the shortlist of this (query, split)
-      const int q = qtile * BM + t;
       if (q < p.nq) {
         const size_t o = ((size_t)q * p.n_splits + split) * p.kp;
         for (int i = 0; i < cnt; ++i) {
@@ -358,6 +518,219 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_shortlist(const __grid_constant
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// CTA-pair version (cta_group::2). A work unit covers 256 queries: CTA rank r
+// holds queries [256*qtile + 128*r, +128) resident in its own TMEM. The
+// leader (rank 0) issues tcgen05.mma.cta_group::2 with M=256, N=BN; each CTA
+// TMA-loads only BN/2 of the BN table rows of every tile, so per SM the smem
+// write + MMA read traffic for the table halves, and L2->SM traffic halves.
+// Both CTAs' epilogues read their own 128 x BN accumulator from TMEM.
+template <int BN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
+    k_shortlist2(const __grid_constant__ CUtensorMap tmap, Params p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr int HB = BN / 2;                 // table rows loaded by each CTA per tile
+  constexpr int BOX_BYTES = HB * 128;
+  const int BPS = p.bps;
+  const int STAGE_BYTES = BPS * BOX_BYTES;
+  const int NSTAGE = p.nstage;
+  const int cap = p.cap;
+  uint8_t* stages = base;
+  float* ls = reinterpret_cast<float*>(base + NSTAGE * STAGE_BYTES);
+  uint32_t* lr = reinterpret_cast<uint32_t*>(ls + cap * BM);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(lr + cap * BM);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + NSTAGE;
+  uint64_t* accf = bars + 2 * NSTAGE;
+  uint64_t* acce = accf + 2;
+  uint64_t* aready = acce + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aready + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int nkb = p.dim / BK;
+  const int nsg = nkb / BPS;
+  const int a_cols = p.dim / 2;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NSTAGE; ++s) {
+      mbar_init(smem_u32(&full[s]), 1);
+      mbar_init(smem_u32(&empty[s]), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(smem_u32(&accf[b]), 1);
+      mbar_init(smem_u32(&acce[b]), 8);  // 4 epilogue warps x 2 CTAs
+    }
+    mbar_init(smem_u32(aready), 8);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer (both CTAs, own half of each tile) ----------------
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = pair; u < p.n_units; u += npairs) {
+        const int split = u / p.n_qtiles;
+        const int64_t r0 = (int64_t)split * p.rows_per_split;
+        const int64_t r1 = min((int64_t)p.n_rows, r0 + p.rows_per_split);
+        for (int64_t row = r0; row < r1; row += BN) {
+          for (int sg = 0; sg < nsg; ++sg) {
+            mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+            if (leader) mbar_expect_tx(smem_u32(&full[stage]), 2 * STAGE_BYTES);
+            for (int bx = 0; bx < BPS; ++bx)
+              tma_load_2d_pair(smem_u32(stages + stage * STAGE_BYTES + bx * BOX_BYTES), &tmap, smem_u32(&full[stage]),
+                               (sg * BPS + bx) * BK, (int)(row + rank * HB));
+            if (++stage == NSTAGE) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (leader CTA only) ----------------
+    if (leader) {
+      const uint32_t idesc =
+          (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t tile = 0;
+      uint32_t unit_i = 0;
+      for (int u = pair; u < p.n_units; u += npairs, ++unit_i) {
+        const int split = u / p.n_qtiles;
+        const int64_t r0 = (int64_t)split * p.rows_per_split;
+        const int64_t r1 = min((int64_t)p.n_rows, r0 + p.rows_per_split);
+        mbar_wait_cluster(smem_u32(aready), unit_i & 1);
+        tc_fence_after();
+        for (int64_t row = r0; row < r1; row += BN, ++tile) {
+          const uint32_t b = tile & 1;
+          const uint32_t use = tile >> 1;
+          mbar_wait_cluster(smem_u32(&acce[b]), (use & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t d_tmem = tmem + a_cols + b * BN;
+          for (int sg = 0; sg < nsg; ++sg) {
+            mbar_wait(smem_u32(&full[stage]), phase);
+            tc_fence_after();
+            if (lane == 0) {
+              const uint32_t sa = smem_u32(stages + stage * STAGE_BYTES);
+              for (int bx = 0; bx < BPS; ++bx) {
+                const int kb = sg * BPS + bx;
+                mma_box4_pair(d_tmem, tmem + kb * (BK / 16) * 8, smem_desc_sw128(sa + bx * BOX_BYTES), idesc, kb != 0);
+              }
+              tc_commit_pair(smem_u32(&empty[stage]));
+            }
+            __syncwarp();
+            if (++stage == NSTAGE) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+          if (lane == 0) tc_commit_pair(smem_u32(&accf[b]));
+          __syncwarp();
+        }
+      }
+    }
+  } else {
+    // ---------------- epilogue: warps 2..5 of both CTAs ----------------
+    const int quarter = warp & 3;
+    const int t = quarter * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+    uint32_t tile = 0;
+    for (int u = pair; u < p.n_units; u += npairs) {
+      const int split = u / p.n_qtiles;
+      const int qtile = u - split * p.n_qtiles;
+      const int64_t r0 = (int64_t)split * p.rows_per_split;
+      const int64_t r1 = min((int64_t)p.n_rows, r0 + p.rows_per_split);
+      const int q = qtile * 256 + (int)rank * BM + t;
+      {
+        const uint4* src = reinterpret_cast<const uint4*>(p.Qb + (size_t)q * p.dim);
+        for (int kb = 0; kb < nkb; ++kb) {
+          uint32_t r[32];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const uint4 v = __ldg(src + kb * 8 + i);
+            r[4 * i + 0] = v.x;
+            r[4 * i + 1] = v.y;
+            r[4 * i + 2] = v.z;
+            r[4 * i + 3] = v.w;
+          }
+          tmem_st32(tmem + lane_base + kb * 32, r);
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_remote(smem_u32(aready), 0);
+      }
+      int cnt = 0;
+      float tau = -INFINITY;
+      refresh_tau(p.gkey, q, tau);
+      for (int64_t row = r0; row < r1; row += BN, ++tile) {
+        const uint32_t b = tile & 1;
+        const uint32_t use = tile >> 1;
+        if ((tile & 15) == 0) refresh_tau(p.gkey, q, tau);
+        mbar_wait(smem_u32(&accf[b]), use & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int h = 0; h < BN / 64; ++h) {
+          float v[64];
+          tmem_ld64(tmem + lane_base + a_cols + b * BN + h * 64, v);
+          if (h == BN / 64 - 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_remote(smem_u32(&acce[b]), 0);
+          }
+          const int64_t rbase = row + h * 64;
+          const int lim = (int)min((int64_t)64, r1 - rbase);
+          const uint32_t r32 = (uint32_t)rbase;
+#pragma unroll
+          for (int c = 0; c < ((p.debug & 4) ? 0 : 4); ++c) {
+            if (__any_sync(0xffffffffu, cnt + 16 > cap)) compact(ls, lr, t, cnt, p.kp, tau);
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj) {
+              const int j = c * 16 + jj;
+              const bool acc = (j < lim) & (v[j] > tau);
+              if (acc) {
+                ls[cnt * BM + t] = v[j];
+                lr[cnt * BM + t] = r32 + j;
+              }
+              cnt += acc;
+            }
+          }
+        }
+      }
+      compact(ls, lr, t, cnt, p.kp, tau);
+      publish_tau(p.gkey, q, ls, t, cnt, p.kp);
+      if (q < p.nq) {
+        const size_t o = ((size_t)q * p.n_splits + split) * p.kp;
+        for (int i = 0; i < cnt; ++i) {
+          p.part_s[o + i] = ls[i * BM + t];
+          p.part_r[o + i] = lr[i * BM + t];
+        }
+        p.part_n[(size_t)q * p.n_splits + split] = cnt;
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
 }
 
@@ -470,18 +843,54 @@ void approx_plan(ApproxPlan& p, const __nv_bfloat16* rows, int64_t n_rows, int d
                            box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) raise(LC_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  cuuint32_t box2[2] = {(cuuint32_t)sm100::BK, (cuuint32_t)(p.bn / 2)};
+  r = encode_fn()(&p.tmap2, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<__nv_bfloat16*>(rows), gdim, gstride, box2,
+                  estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) raise(LC_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
   p.valid = true;
 }
 
-template <int BN, int NSTAGE>
+// 1 = single-CTA kernel, 2 = CTA-pair kernel (default)
+static int cta_mode() {
+  const char* e = getenv("FC_SHORTLIST_CTA");
+  return e && atoi(e) == 1 ? 1 : 2;
+}
+
+template <int BN>
 static void launch_shortlist(lc_ctx* ctx, const ApproxPlan& plan, sm100::Params prm) {
-  const size_t smem = 1024 + (size_t)NSTAGE * BN * 128 + (size_t)prm.kp * sm100::BM * 8 + (2 * NSTAGE + 5) * 8 + 16;
-  auto kern = sm100::k_shortlist<BN, NSTAGE>;
-  FC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int grid = std::min(prm.n_units, ctx->sm_count);
-  KTimer kt(ctx, "shortlist");
-  kern<<<grid, sm100::NTHREADS, smem, ctx->stream>>>(plan.tmap, prm);
-  kt.stop();
+  // smem: NSTAGE table tiles + a candidate buffer of `cap` (score,row) slots
+  // per query; a deep buffer makes the warp-uniform compactions rare.
+  // several TMA boxes per stage so the single MMA-issuing thread pays one
+  // barrier wait per 8-16 MMAs instead of per 4
+  const int nkb = prm.dim / sm100::BK;
+  prm.bps = nkb % 4 == 0 ? 4 : nkb % 3 == 0 ? 3 : nkb % 2 == 0 ? 2 : 1;
+  if (BN == 128 && prm.bps > 2) prm.bps = nkb % 2 == 0 ? 2 : 1;
+  const bool pair = cta_mode() == 2;
+  const size_t stage_bytes = (size_t)(pair ? BN / 2 : BN) * 128 * prm.bps;
+  const size_t budget = 227 * 1024 - 1024 - 256;
+  const size_t slot_bytes = (size_t)sm100::BM * 8;
+  const int64_t want = (int64_t)(prm.kp + 64) * slot_bytes;  // candidate buffer depth
+  prm.nstage = (int)std::max<int64_t>(2, std::min<int64_t>(sm100::MAX_STAGE,((int64_t)budget - want) / (int64_t)stage_bytes));
+  const int64_t slots = (int64_t)((budget - prm.nstage * stage_bytes) / slot_bytes);
+  prm.cap = (int)std::min<int64_t>(slots, prm.kp + 128);
+  if (prm.cap < prm.kp + 16) raise(LC_ERR_INVALID_ARGUMENT, "lookup: shortlist too long for shared memory");
+  const size_t smem = 1024 + 256 + prm.nstage * stage_bytes + (size_t)prm.cap * slot_bytes;
+  if (pair) {
+    auto kern = sm100::k_shortlist2<BN>;
+    FC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int grid = 2 * std::min(prm.n_units, ctx->sm_count / 2);
+    KTimer kt(ctx, "shortlist");
+    kern<<<grid, sm100::NTHREADS, smem, ctx->stream>>>(plan.tmap2, prm);
+    kt.stop();
+  } else {
+    auto kern = sm100::k_shortlist<BN>;
+    FC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int grid = std::min(prm.n_units, ctx->sm_count);
+    KTimer kt(ctx, "shortlist");
+    kern<<<grid, sm100::NTHREADS, smem, ctx->stream>>>(plan.tmap, prm);
+    kt.stop();
+  }
   FC_LAUNCH_CHECK();
 }
 
@@ -489,14 +898,16 @@ void approx_shortlist(lc_ctx* ctx, const ApproxPlan& plan, const float* Qdev, in
                       uint32_t* cand_r, int32_t* cand_n) {
   using namespace sm100;
   const int dim = plan.dim;
-  const int n_qtiles = (nq + BM - 1) / BM;
-  const int nq_pad = n_qtiles * BM;
+  const int qt = cta_mode() == 2 ? 2 * BM : BM;  // queries per work unit
+  const int n_qtiles = (nq + qt - 1) / qt;
+  const int nq_pad = n_qtiles * qt;
   DevBuf qb((size_t)nq_pad * dim * sizeof(__nv_bfloat16), ctx->stream);
   k_q_to_bf16<<<grid_for((int64_t)nq_pad * dim, 256), 256, 0, ctx->stream>>>(Qdev, nq, dim, qb.as<__nv_bfloat16>(), nq_pad);
   FC_LAUNCH_CHECK();
   const int bn = plan.bn;
   const int64_t total_tiles = (plan.n_rows + bn - 1) / bn;
-  int64_t splits = std::max<int64_t>(1, ((int64_t)ctx->sm_count * 8 + n_qtiles - 1) / n_qtiles);
+  const int64_t workers = cta_mode() == 2 ? ctx->sm_count / 2 : ctx->sm_count;  // persistent CTAs / CTA pairs
+  int64_t splits = std::max<int64_t>(1, (workers * 8 + n_qtiles - 1) / n_qtiles);
   splits = std::min<int64_t>(splits, std::max<int64_t>(1, total_tiles / 16));
   const int64_t tiles_per_split = (total_tiles + splits - 1) / splits;
   splits = (total_tiles + tiles_per_split - 1) / tiles_per_split;
@@ -510,16 +921,23 @@ void approx_shortlist(lc_ctx* ctx, const ApproxPlan& plan, const float* Qdev, in
   prm.n_splits = (int)splits;
   prm.n_units = (int)(splits * n_qtiles);
   prm.kp = kp;
+  {
+    const char* dbg = getenv("FC_SHORTLIST_DEBUG");
+    prm.debug = dbg ? atoi(dbg) : 0;
+  }
   DevBuf ps((size_t)nq * splits * kp * sizeof(float), ctx->stream);
   DevBuf pr((size_t)nq * splits * kp * sizeof(uint32_t), ctx->stream);
   DevBuf pn((size_t)nq * splits * sizeof(int32_t), ctx->stream);
+  DevBuf gk((size_t)nq_pad * sizeof(uint32_t), ctx->stream);
+  FC_CUDA(cudaMemsetAsync(gk.p, 0, gk.bytes, ctx->stream));
+  prm.gkey = gk.as<uint32_t>();
   prm.part_s = ps.as<float>();
   prm.part_r = pr.as<uint32_t>();
   prm.part_n = pn.as<int32_t>();
   if (bn == 64)
-    launch_shortlist<64, 8>(ctx, plan, prm);
+    launch_shortlist<64>(ctx, plan, prm);
   else
-    launch_shortlist<128, 6>(ctx, plan, prm);
+    launch_shortlist<128>(ctx, plan, prm);
   const size_t msmem = (size_t)splits * kp * sizeof(uint32_t);
   if (msmem > 48 * 1024) FC_CUDA(cudaFuncSetAttribute(k_shortlist_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msmem));
   k_shortlist_merge<<<nq, 256, msmem, ctx->stream>>>(ps.as<float>(), pr.as<uint32_t>(), pn.as<int32_t>(), (int)splits, kp,
