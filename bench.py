@@ -323,24 +323,17 @@ def main():
     o_ids = torch.empty((B, k), dtype=torch.int64, device=dev)
     o_sc = torch.empty((B, k), dtype=torch.float64, device=dev)
     o_cnt = torch.empty((B,), dtype=torch.int32, device=dev)
+    last = {}
     if world > 1:
-        g_ids = torch.empty((world, B, k), dtype=torch.int64, device=dev)
-        g_sc = torch.empty((world, B, k), dtype=torch.float64, device=dev)
-        g_cnt = torch.empty((world, B), dtype=torch.int32, device=dev)
-        m_ids = torch.empty_like(o_ids)
-        m_sc = torch.empty_like(o_sc)
-        m_cnt = torch.empty_like(o_cnt)
+        from paper_2501_04012_b200.sharded import ShardedIndex
+        shard = ShardedIndex(ix)  # one NCCL all-gather of packed (ids, scores, counts) + lc_topk_merge
 
     def step(q):
-        ix.query_topk(fc.EmbeddingKind.Whole, q, k, out=(o_ids, o_sc, o_cnt))
         if world > 1:
-            with torch.cuda.stream(stream):
-                dist.all_gather_into_tensor(g_ids, o_ids)
-                dist.all_gather_into_tensor(g_sc, o_sc)
-                dist.all_gather_into_tensor(g_cnt, o_cnt)
-            fc._check(fc.lib.lc_topk_merge(ctx.h, C.c_void_p(g_ids.data_ptr()), C.c_void_p(g_sc.data_ptr()),
-                                           C.c_void_p(g_cnt.data_ptr()), world, B, k, C.c_void_p(m_ids.data_ptr()),
-                                           C.c_void_p(m_sc.data_ptr()), C.c_void_p(m_cnt.data_ptr())))
+            last["res"] = shard.query_topk(fc.EmbeddingKind.Whole, q, k)
+        else:
+            ix.query_topk(fc.EmbeddingKind.Whole, q, k, out=(o_ids, o_sc, o_cnt))
+            last["res"] = (o_ids, o_sc, o_cnt)
 
     for s in range(args.warmup):
         step(qs[s])
@@ -429,14 +422,14 @@ def main():
                 dq.copy_(hq, non_blocking=True)
             step(dq)
             with torch.cuda.stream(stream):
-                hres.copy_(m_ids, non_blocking=True)
+                hres.copy_(last["res"][0], non_blocking=True)
             stream.synchronize()
         e2e_s = time.perf_counter() - t0
         tt = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e = {"value": args.steps * B / float(tt.item()), "unit": "lookups/s",
                "h2d_bytes_per_step": B * args.dim * 4, "d2h_bytes_per_step": B * k * 8,
-               "api": "lc_index_query_topk (device) + NCCL all-gather + lc_topk_merge, pinned host queries"}
+               "api": "ShardedIndex.query_topk: lc_index_query_topk + one NCCL all-gather + lc_topk_merge, pinned host queries"}
 
     # ---- codec (config[2]) ----
     codec = None

@@ -338,9 +338,14 @@ def lookup_decide(index: SimilarityIndex, qw, qo, qb, hit_threshold=HIT_THRESHOL
 
 
 def decide_batch(w_ids, w_sc, o_ids, o_sc, b_ids, b_sc, hit_threshold=HIT_THRESHOLD, edges=STEP_BIN_EDGES, ctx=None):
-    arrs = [np.ascontiguousarray(a, t) for a, t in ((w_ids, np.uint64), (w_sc, np.float64), (o_ids, np.uint64),
-                                                     (o_sc, np.float64), (b_ids, np.uint64), (b_sc, np.float64))]
-    n = arrs[0].size
+    """decide + similarity_to_step on top-1 triples (host
+    arrays or device tensors); returns a host array of Decision records."""
+    if _is_dev(w_ids):
+        arrs = [a.contiguous() for a in (w_ids, w_sc, o_ids, o_sc, b_ids, b_sc)]
+    else:
+        arrs = [np.ascontiguousarray(a, t) for a, t in ((w_ids, np.uint64), (w_sc, np.float64), (o_ids, np.uint64),
+                                                         (o_sc, np.float64), (b_ids, np.uint64), (b_sc, np.float64))]
+    n = int(arrs[0].numel() if _is_dev(arrs[0]) else arrs[0].size)
     out = (Decision * n)()
     e = np.ascontiguousarray(edges, np.float64)
     _check(lib.lc_decide_batch(_ctx(ctx), *[_ptr(a) for a in arrs], n, hit_threshold, _ptr(e),
@@ -348,18 +353,27 @@ def decide_batch(w_ids, w_sc, o_ids, o_sc, b_ids, b_sc, hit_threshold=HIT_THRESH
     return out
 
 
-def topk_merge(ids, scores, counts, k, ctx=None):
-    """Merge G shard top-k lists ([G][n][k]) into the global top-k."""
-    ids = np.ascontiguousarray(ids, np.uint64)
-    scores = np.ascontiguousarray(scores, np.float64)
-    counts = np.ascontiguousarray(counts, np.int32)
-    G, n = counts.shape
-    oi = np.zeros((n, k), np.uint64)
-    os_ = np.zeros((n, k), np.float64)
-    oc = np.zeros(n, np.int32)
-    _check(lib.lc_topk_merge(_ctx(ctx), _ptr(ids), _ptr(scores), _ptr(counts), G, n, k, _ptr(oi), _ptr(os_),
-                             _ptr(oc)))
-    return oi, os_, oc
+def topk_merge(ids, scores, counts, k, ctx=None, out=None):
+    """Merge G shard top-k lists ([G][n][k], counts [G][n]) into the global
+    top-k by (score desc, id asc). Device tensors in -> device tensors out."""
+    if _is_dev(ids):
+        import torch
+        ids, scores, counts = ids.contiguous(), scores.contiguous(), counts.contiguous()
+        G, n = counts.shape
+        if out is None:
+            out = (torch.empty((n, k), dtype=torch.int64, device=ids.device),
+                   torch.empty((n, k), dtype=torch.float64, device=ids.device),
+                   torch.empty((n,), dtype=torch.int32, device=ids.device))
+    else:
+        ids = np.ascontiguousarray(ids, np.uint64)
+        scores = np.ascontiguousarray(scores, np.float64)
+        counts = np.ascontiguousarray(counts, np.int32)
+        G, n = counts.shape
+        if out is None:
+            out = (np.zeros((n, k), np.uint64), np.zeros((n, k), np.float64), np.zeros(n, np.int32))
+    _check(lib.lc_topk_merge(_ctx(ctx), _ptr(ids), _ptr(scores), _ptr(counts), G, n, k, _ptr(out[0]), _ptr(out[1]),
+                             _ptr(out[2])))
+    return out
 
 
 # ---------------------------------------------------------------------------

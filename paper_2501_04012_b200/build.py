@@ -52,6 +52,36 @@ def build(verbose: bool = False, jobs: int = 8) -> str:
     return LIB
 
 
+CPP_TESTS = os.path.join(ROOT, "tests", "cpp")
+
+
+def build_cpp_tests() -> list:
+    """Compile the C++ host-API programs under tests/cpp against the library
+    (g++ -std=c++20, rpath to _lib). Returns the built executables."""
+    lib = build()
+    out_dir = os.path.join(CPP_TESTS, "_build")
+    os.makedirs(out_dir, exist_ok=True)
+    cuda_inc = os.path.join(os.path.dirname(os.path.dirname(NVCC)), "include")
+    cuda_lib = os.path.join(os.path.dirname(os.path.dirname(NVCC)), "lib64")
+    hdrs = [os.path.join(ROOT, "include", "flexcache_b200.h"),
+            os.path.join(ROOT, "include", "lcache_b200", "lcache.hpp")]
+    exes = []
+    for f in sorted(os.listdir(CPP_TESTS)):
+        if not f.endswith(".cpp"):
+            continue
+        src = os.path.join(CPP_TESTS, f)
+        exe = os.path.join(out_dir, f[:-4])
+        if _stale(exe, [src, lib] + hdrs):
+            cmd = [os.environ.get("CXX", "g++"), "-std=c++20", "-O2", "-Wall", "-Wextra", "-I" + os.path.join(ROOT, "include"),
+                   "-I" + cuda_inc, src, "-o", exe, "-L" + OUT_DIR, "-lflexcache_b200", "-Wl,-rpath," + OUT_DIR,
+                   "-L" + cuda_lib, "-lcudart"]
+            r = subprocess.run(cmd, capture_output=True, text=True)
+            if r.returncode != 0:
+                raise RuntimeError("g++ failed:\n" + r.stdout + r.stderr)
+        exes.append(exe)
+    return exes
+
+
 def _drain(procs, verbose):
     errs = []
     while procs:

@@ -407,7 +407,10 @@ void query_dev(lc_index* ix, int kind, const float* Qdev, int nq, int k, uint64_
   const int nf = hf[0];
   ix->stats.certified += nq - nf;
   ix->stats.fallback += nf;
-  if (nf > 0) exact_scan(ix, kind, Qdev, fl.as<int32_t>(), nf, k, oid, osc, ocnt);
+  // FC_LOOKUP_DIAG=1 (kernel-timing diagnostics with FC_SHORTLIST_DEBUG only): skip the
+  // exact re-scan, so results are NOT exact in that mode.
+  static const bool diag = getenv("FC_LOOKUP_DIAG") && atoi(getenv("FC_LOOKUP_DIAG")) == 1;
+  if (nf > 0 && !diag) exact_scan(ix, kind, Qdev, fl.as<int32_t>(), nf, k, oid, osc, ocnt);
 }
 
 }  // namespace

@@ -117,6 +117,14 @@ __device__ __forceinline__ void mma_box4(uint32_t d_tmem, uint32_t a_tmem, uint6
       : "memory");
 }
 
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.u32 %0, 1, 0, P;\n}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 // ---- CTA-pair (cta_group::2) primitives ----
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -126,11 +134,14 @@ __device__ __forceinline__ uint32_t cluster_rank() {
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
-// arrive on the barrier at the same smem offset in CTA `cta` of the cluster
+// arrive on the barrier at the same smem offset in CTA `cta` of the cluster.
+// Default (.release.cta) semantics: the tcgen05 ordering is carried by
+// tcgen05.fence::before_thread_sync; a .cluster-scope release here compiles
+// to MEMBAR.ALL.GPU per tile and was ~25% of the epilogue warps' time (ncu).
 __device__ __forceinline__ void mbar_arrive_remote(uint32_t bar, uint32_t cta) {
   asm volatile(
       "{\n.reg .b32 ra;\nmapa.shared::cluster.u32 ra, %0, %1;\n"
-      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n}" ::"r"(bar),
+      "mbarrier.arrive.shared::cluster.b64 _, [ra];\n}" ::"r"(bar),
       "r"(cta)
       : "memory");
 }
@@ -139,7 +150,7 @@ __device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t phase) 
       "{\n"
       ".reg .pred P1;\n"
       "WAITC_%=:\n"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
       "@!P1 bra WAITC_%=;\n"
       "}\n" ::"r"(bar),
       "r"(phase)
@@ -217,6 +228,22 @@ __device__ __forceinline__ void tmem_ld64(uint32_t taddr, float* v) {
   for (int i = 0; i < 64; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* r) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
@@ -272,6 +299,64 @@ __device__ __forceinline__ float key_float(uint32_t k) {
   return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k);
 }
 
+// Cheaper compaction for the pair kernel: bisection on the order key with an
+// early stop as soon as the kept set is within [kp, kp + 8] (~5 passes over
+// the buffer instead of 32). Keeping a few more than kp is harmless: the new
+// threshold T is <= the kp-th best kept score, so every later rejection
+// (score <= T) stays below the final K'-th shortlisted score.
+__device__ __noinline__ void compact2(float* ls, uint32_t* lr, int t, int& cnt, int kp, float& tau) {
+  if (cnt <= kp + 8) return;
+  uint32_t lo = 0xFFFFFFFFu, hi = 0;
+  for (int i = 0; i < cnt; ++i) {
+    const uint32_t k = okey(ls[i * BM + t]);
+    lo = min(lo, k);
+    hi = max(hi, k);
+  }
+  int cge = cnt;  // count(key >= lo)
+  while (lo < hi) {
+    const uint32_t mid = lo + (uint32_t)(((uint64_t)hi - lo + 1) >> 1);
+    int c = 0;
+    for (int i = 0; i < cnt; ++i) c += okey(ls[i * BM + t]) >= mid;
+    if (c >= kp) {
+      lo = mid;
+      cge = c;
+      if (c <= kp + 8) break;
+    } else {
+      hi = mid - 1;
+    }
+  }
+  const uint32_t T = lo;
+  int w = 0;
+  if (cge <= kp + 8) {
+    for (int i = 0; i < cnt; ++i) {
+      const float v = ls[i * BM + t];
+      if (okey(v) >= T) {
+        ls[w * BM + t] = v;
+        lr[w * BM + t] = lr[i * BM + t];
+        ++w;
+      }
+    }
+  } else {  // many ties at T: everything above T, then == T up to kp
+    int above = 0;
+    for (int i = 0; i < cnt; ++i) above += okey(ls[i * BM + t]) > T;
+    int need_eq = kp - above;
+    for (int i = 0; i < cnt; ++i) {
+      const float v = ls[i * BM + t];
+      const uint32_t k = okey(v);
+      const bool keep = k > T || (k == T && need_eq > 0);
+      need_eq -= (k == T && keep);
+      if (keep) {
+        ls[w * BM + t] = v;
+        lr[w * BM + t] = lr[i * BM + t];
+        ++w;
+      }
+    }
+  }
+  cnt = w;
+  const float tnew = key_float(T);
+  if (tnew > tau) tau = tnew;
+}
+
 // Shared per-query threshold (order-preserving key, 0 = unset): the K'-th
 // best bf16 score of ANY completed work unit is a lower bound on the K'-th
 // best over the whole table, so every unit of that query may drop scores
@@ -302,6 +387,7 @@ struct Params {
   int cap;     // candidate buffer slots per query (>= kp + 16)
   int bps;     // TMA boxes per pipeline stage
   uint32_t* gkey;  // [nq_pad] shared per-query thresholds (order keys, 0 = unset)
+  uint32_t* stats;  // FC_SHORTLIST_DEBUG & 16: [slow chunks, compactions, warp-tiles]
   int debug;   // diagnostics (FC_SHORTLIST_DEBUG): 1 = skip MMA, 2 = skip TMA, 4 = skip epilogue filter
   int nstage;
   float* part_s;             // [nq][n_splits][kp]
@@ -521,25 +607,70 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_shortlist(const __grid_constant
   }
 }
 
-// CTA-pair version (cta_group::2). A work unit covers 256 queries: CTA rank r
-// holds queries [256*qtile + 128*r, +128) resident in its own TMEM. The
-// leader (rank 0) issues tcgen05.mma.cta_group::2 with M=256, N=BN; each CTA
-// TMA-loads only BN/2 of the BN table rows of every tile, so per SM the smem
-// write + MMA read traffic for the table halves, and L2->SM traffic halves.
-// Both CTAs' epilogues read their own 128 x BN accumulator from TMEM.
-template <int BN>
+// CTA-pair kernel (cta_group::2), the default path for dim <= 768.
+//
+// Why this shape (measured on B200 with scripts/mma_bench.cu): a
+// tcgen05.mma instruction costs >= ~50 issue cycles however small N is, so
+// N=64 tiles cap at ~1.0-1.45 PFLOP/s while N=128 reaches ~2.2 PFLOP/s (the
+// N=256 pipe rate). Holding all 768 query dims in TMEM (384 columns) left
+// room only for two N=64 accumulators; here the first KT <= 8 K-boxes of the
+// 128 queries of each CTA live in TMEM (<= 256 columns) and the remaining
+// KS boxes in shared memory (TMA-loaded, SWIZZLE_128B), which frees 256
+// columns for two N=128 accumulators (MMA of tile t+1 overlaps the epilogue
+// of tile t).
+//
+// Work unit = (256-query tile, row range). CTA rank r holds queries
+// [256*qtile + 128*r, +128) and TMA-loads table rows [row + 64*r, +64) of
+// each 128-row tile; the leader issues M=256 x N=128 x K=16 MMAs reading A
+// from both CTAs' TMEM (first KT boxes) or smem (last KS boxes) and B from
+// both CTAs' smem, so each SM streams 64 table rows per 256x128 tile
+// (~30 B/cycle/SM of L2 traffic at full MMA rate). Each CTA's epilogue owns
+// its 128 accumulator lanes (one query per thread).
+constexpr int PN = 128;               // table rows per tile (MMA N)
+constexpr int PHB = PN / 2;           // table rows per CTA per tile
+constexpr int PBOX = PHB * 128;       // one B box: 64 rows x 64 bf16 = 8 KB
+constexpr int ABOX = BM * 128;        // one A box: 128 queries x 64 bf16 = 16 KB
+constexpr int ACC_COL = 256;          // accumulators at TMEM columns [256, 512)
+constexpr int PMAX_STAGE = 24;
+
+__device__ __forceinline__ void mma_box4_pair_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                                 uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p, t;\n"
+      ".reg .b64 a1, a2, a3, d1, d2, d3;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "setp.eq.b32 t, 0, 0;\n"
+      "add.s64 a1, %1, 2;\n"
+      "add.s64 a2, %1, 4;\n"
+      "add.s64 a3, %1, 6;\n"
+      "add.s64 d1, %2, 2;\n"
+      "add.s64 d2, %2, 4;\n"
+      "add.s64 d3, %2, 6;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], a1, d1, %3, t;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], a2, d2, %3, t;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], a3, d3, %3, t;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
-    k_shortlist2(const __grid_constant__ CUtensorMap tmap, Params p) {
+    k_shortlist_pair(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmQ, Params p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  constexpr int HB = BN / 2;                 // table rows loaded by each CTA per tile
-  constexpr int BOX_BYTES = HB * 128;
-  const int BPS = p.bps;
-  const int STAGE_BYTES = BPS * BOX_BYTES;
   const int NSTAGE = p.nstage;
   const int cap = p.cap;
+  const int nkb = p.dim / BK;
+  const int KT = nkb < 8 ? nkb : 8;  // A boxes resident in TMEM
+  const int KS = nkb - KT;           // A boxes resident in smem
+  const int BPS = p.bps;             // B boxes per pipeline stage (one barrier round trip per 4*BPS MMAs)
+  const int STAGE_BYTES = BPS * PBOX;
+  const int nsg = nkb / BPS;
   uint8_t* stages = base;
-  float* ls = reinterpret_cast<float*>(base + NSTAGE * STAGE_BYTES);
+  uint8_t* asmem = base + NSTAGE * STAGE_BYTES;
+  float* ls = reinterpret_cast<float*>(asmem + KS * ABOX);
   uint32_t* lr = reinterpret_cast<uint32_t*>(ls + cap * BM);
   uint64_t* bars = reinterpret_cast<uint64_t*>(lr + cap * BM);
   uint64_t* full = bars;
@@ -547,15 +678,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   uint64_t* accf = bars + 2 * NSTAGE;
   uint64_t* acce = accf + 2;
   uint64_t* aready = acce + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aready + 1);
+  uint64_t* afree = aready + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(afree + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
-  const int nkb = p.dim / BK;
-  const int nsg = nkb / BPS;
-  const int a_cols = p.dim / 2;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NSTAGE; ++s) {
@@ -566,7 +695,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       mbar_init(smem_u32(&accf[b]), 1);
       mbar_init(smem_u32(&acce[b]), 8);  // 4 epilogue warps x 2 CTAs
     }
-    mbar_init(smem_u32(aready), 8);
+    mbar_init(smem_u32(aready), 8 + (KS > 0 ? 1 : 0));  // + the leader producer's expect_tx
+    mbar_init(smem_u32(afree), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -581,20 +711,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   if (warp == 0) {
     // ---------------- TMA producer (both CTAs, own half of each tile) ----------------
     if (lane == 0) {
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+      if (KS > 0) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmQ)) : "memory");
       int stage = 0;
-      uint32_t phase = 0;
-      for (int u = pair; u < p.n_units; u += npairs) {
+      uint32_t phase = 0, unit_i = 0;
+      for (int u = pair; u < p.n_units; u += npairs, ++unit_i) {
         const int split = u / p.n_qtiles;
+        const int qtile = u - split * p.n_qtiles;
         const int64_t r0 = (int64_t)split * p.rows_per_split;
         const int64_t r1 = min((int64_t)p.n_rows, r0 + p.rows_per_split);
-        for (int64_t row = r0; row < r1; row += BN) {
+        const bool no_tma = p.debug & 2;  // diagnostic: no table / query traffic
+        if (KS > 0) {  // this unit's smem-resident query boxes, once the previous unit's MMAs are done
+          mbar_wait(smem_u32(afree), (unit_i & 1) ^ 1);
+          if (no_tma) {
+            if (leader) mbar_arrive(smem_u32(aready));
+          } else {
+            if (leader) mbar_expect_tx(smem_u32(aready), 2 * KS * ABOX);
+            for (int j = 0; j < KS; ++j)
+              tma_load_2d_pair(smem_u32(asmem + j * ABOX), &tmQ, smem_u32(aready), (KT + j) * BK,
+                               qtile * 2 * BM + (int)rank * BM);
+          }
+        }
+        for (int64_t row = r0; row < r1; row += PN) {
           for (int sg = 0; sg < nsg; ++sg) {
             mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
-            if (leader) mbar_expect_tx(smem_u32(&full[stage]), 2 * STAGE_BYTES);
-            for (int bx = 0; bx < BPS; ++bx)
-              tma_load_2d_pair(smem_u32(stages + stage * STAGE_BYTES + bx * BOX_BYTES), &tmap, smem_u32(&full[stage]),
-                               (sg * BPS + bx) * BK, (int)(row + rank * HB));
+            if (no_tma) {
+              if (leader) mbar_arrive(smem_u32(&full[stage]));
+            } else {
+              if (leader) mbar_expect_tx(smem_u32(&full[stage]), 2 * STAGE_BYTES);
+              for (int bx = 0; bx < BPS; ++bx)
+                tma_load_2d_pair(smem_u32(stages + stage * STAGE_BYTES + bx * PBOX), &tmB, smem_u32(&full[stage]),
+                                 (sg * BPS + bx) * BK, (int)(row + rank * PHB));
+            }
             if (++stage == NSTAGE) {
               stage = 0;
               phase ^= 1;
@@ -603,35 +751,42 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         }
       }
     }
+    __syncwarp();
   } else if (warp == 1) {
     // ---------------- MMA issuer (leader CTA only) ----------------
+    // The whole warp runs the loop (warp-uniform state stays in uniform
+    // registers); one elected lane issues the MMAs and commits.
     if (leader) {
       const uint32_t idesc =
-          (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+          (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(PN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+      const bool issuer = elect_one();
       int stage = 0;
-      uint32_t phase = 0;
-      uint32_t tile = 0;
-      uint32_t unit_i = 0;
+      uint32_t phase = 0, tile = 0, unit_i = 0;
       for (int u = pair; u < p.n_units; u += npairs, ++unit_i) {
         const int split = u / p.n_qtiles;
         const int64_t r0 = (int64_t)split * p.rows_per_split;
         const int64_t r1 = min((int64_t)p.n_rows, r0 + p.rows_per_split);
-        mbar_wait_cluster(smem_u32(aready), unit_i & 1);
+        mbar_wait(smem_u32(aready), unit_i & 1);
         tc_fence_after();
-        for (int64_t row = r0; row < r1; row += BN, ++tile) {
+        for (int64_t row = r0; row < r1; row += PN, ++tile) {
           const uint32_t b = tile & 1;
           const uint32_t use = tile >> 1;
-          mbar_wait_cluster(smem_u32(&acce[b]), (use & 1) ^ 1);
+          mbar_wait(smem_u32(&acce[b]), (use & 1) ^ 1);
           tc_fence_after();
-          const uint32_t d_tmem = tmem + a_cols + b * BN;
+          const uint32_t d_tmem = tmem + ACC_COL + b * PN;
           for (int sg = 0; sg < nsg; ++sg) {
             mbar_wait(smem_u32(&full[stage]), phase);
             tc_fence_after();
-            if (lane == 0) {
-              const uint32_t sa = smem_u32(stages + stage * STAGE_BYTES);
+            if (issuer) {
+#pragma unroll 1
               for (int bx = 0; bx < BPS; ++bx) {
                 const int kb = sg * BPS + bx;
-                mma_box4_pair(d_tmem, tmem + kb * (BK / 16) * 8, smem_desc_sw128(sa + bx * BOX_BYTES), idesc, kb != 0);
+                const uint64_t bdesc = smem_desc_sw128(smem_u32(stages + stage * STAGE_BYTES + bx * PBOX));
+                if (p.debug & 1) continue;
+                if (kb < KT)
+                  mma_box4_pair(d_tmem, tmem + kb * (BK / 16) * 8, bdesc, idesc, kb != 0);
+                else
+                  mma_box4_pair_ss(d_tmem, smem_desc_sw128(smem_u32(asmem + (kb - KT) * ABOX)), bdesc, idesc, 1);
               }
               tc_commit_pair(smem_u32(&empty[stage]));
             }
@@ -641,26 +796,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
               phase ^= 1;
             }
           }
-          if (lane == 0) tc_commit_pair(smem_u32(&accf[b]));
+          if (issuer) tc_commit_pair(smem_u32(&accf[b]));
           __syncwarp();
         }
+        if (issuer) tc_commit_pair(smem_u32(afree));  // A (TMEM + smem parts) may be overwritten
+        __syncwarp();
       }
     }
+    __syncwarp();
   } else {
     // ---------------- epilogue: warps 2..5 of both CTAs ----------------
     const int quarter = warp & 3;
     const int t = quarter * 32 + lane;
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
-    uint32_t tile = 0;
-    for (int u = pair; u < p.n_units; u += npairs) {
+    uint32_t tile = 0, unit_i = 0;
+    for (int u = pair; u < p.n_units; u += npairs, ++unit_i) {
       const int split = u / p.n_qtiles;
       const int qtile = u - split * p.n_qtiles;
       const int64_t r0 = (int64_t)split * p.rows_per_split;
       const int64_t r1 = min((int64_t)p.n_rows, r0 + p.rows_per_split);
-      const int q = qtile * 256 + (int)rank * BM + t;
-      {
+      const int q = qtile * 2 * BM + (int)rank * BM + t;
+      {  // (1) this unit's query row -> TMEM columns [0, 32*KT), once the previous unit's MMAs are done
+        mbar_wait(smem_u32(afree), (unit_i & 1) ^ 1);
+        tc_fence_after();
         const uint4* src = reinterpret_cast<const uint4*>(p.Qb + (size_t)q * p.dim);
-        for (int kb = 0; kb < nkb; ++kb) {
+        for (int kb = 0; kb < KT; ++kb) {
           uint32_t r[32];
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
@@ -677,44 +837,64 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive_remote(smem_u32(aready), 0);
       }
+      // (2) stream the accumulator tiles through the running-threshold filter
       int cnt = 0;
       float tau = -INFINITY;
       refresh_tau(p.gkey, q, tau);
-      for (int64_t row = r0; row < r1; row += BN, ++tile) {
+      for (int64_t row = r0; row < r1; row += PN, ++tile) {
         const uint32_t b = tile & 1;
         const uint32_t use = tile >> 1;
-        if ((tile & 15) == 0) refresh_tau(p.gkey, q, tau);
+        if ((tile & 3) == 0) refresh_tau(p.gkey, q, tau);
         mbar_wait(smem_u32(&accf[b]), use & 1);
         tc_fence_after();
-#pragma unroll
-        for (int h = 0; h < BN / 64; ++h) {
-          float v[64];
-          tmem_ld64(tmem + lane_base + a_cols + b * BN + h * 64, v);
-          if (h == BN / 64 - 1) {
+        if ((p.debug & 16) && lane == 0) atomicAdd(p.stats + 2, 1u);
+        const int lim_all = (int)min((int64_t)PN, r1 - row);
+        // 32 accumulator columns per step (a rolled loop: the unrolled
+        // 128-column body overflowed the instruction cache, ncu "no_inst").
+        // Per 16-score chunk a max tree and a warp vote skip the append code
+        // unless some query of the warp has a score above its threshold.
+#pragma unroll 1
+        for (int cc = 0; cc < PN / 32; ++cc) {
+          float v[32];
+          tmem_ld32(tmem + lane_base + ACC_COL + b * PN + cc * 32, v);
+          if (cc == PN / 32 - 1) {
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_remote(smem_u32(&acce[b]), 0);
           }
-          const int64_t rbase = row + h * 64;
-          const int lim = (int)min((int64_t)64, r1 - rbase);
-          const uint32_t r32 = (uint32_t)rbase;
+          if (p.debug & 4) continue;
 #pragma unroll
-          for (int c = 0; c < ((p.debug & 4) ? 0 : 4); ++c) {
-            if (__any_sync(0xffffffffu, cnt + 16 > cap)) compact(ls, lr, t, cnt, p.kp, tau);
+          for (int hh = 0; hh < 2; ++hh) {
+            const float* vc = v + hh * 16;
+            const int c0 = cc * 32 + hh * 16;
+            float a0 = fmaxf(vc[0], vc[1]), a1 = fmaxf(vc[2], vc[3]), a2 = fmaxf(vc[4], vc[5]), a3 = fmaxf(vc[6], vc[7]);
+            a0 = fmaxf(a0, fmaxf(vc[8], vc[9]));
+            a1 = fmaxf(a1, fmaxf(vc[10], vc[11]));
+            a2 = fmaxf(a2, fmaxf(vc[12], vc[13]));
+            a3 = fmaxf(a3, fmaxf(vc[14], vc[15]));
+            const float mx = fmaxf(fmaxf(a0, a1), fmaxf(a2, a3));
+            if (!__any_sync(0xffffffffu, (mx > tau) | (lim_all < PN))) continue;
+            if ((p.debug & 16) && lane == 0) atomicAdd(p.stats + 0, 1u);
+            if (__any_sync(0xffffffffu, cnt + 16 > cap)) {
+              if ((p.debug & 16) && lane == 0) atomicAdd(p.stats + 1, 1u);
+              const float old_tau = tau;
+              compact2(ls, lr, t, cnt, p.kp, tau);
+              if (tau > old_tau) atomicMax(p.gkey + q, okey(tau));  // share the raised threshold at once
+            }
+            const uint32_t r32 = (uint32_t)(row + c0);
 #pragma unroll
             for (int jj = 0; jj < 16; ++jj) {
-              const int j = c * 16 + jj;
-              const bool acc = (j < lim) & (v[j] > tau);
+              const bool acc = (c0 + jj < lim_all) & (vc[jj] > tau);
               if (acc) {
-                ls[cnt * BM + t] = v[j];
-                lr[cnt * BM + t] = r32 + j;
+                ls[cnt * BM + t] = vc[jj];
+                lr[cnt * BM + t] = r32 + jj;
               }
               cnt += acc;
             }
           }
         }
       }
-      compact(ls, lr, t, cnt, p.kp, tau);
+      compact(ls, lr, t, cnt, p.kp, tau);  // exact: the unit's list holds at most kp entries
       publish_tau(p.gkey, q, ls, t, cnt, p.kp);
       if (q < p.nq) {
         const size_t o = ((size_t)q * p.n_splits + split) * p.kp;
@@ -829,68 +1009,90 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 bool approx_available() { return true; }
 
+static void encode_2d(CUtensorMap* m, const __nv_bfloat16* base, int64_t rows, int cols, int box_rows) {
+  cuuint64_t gdim[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t gstride[1] = {(cuuint64_t)cols * sizeof(__nv_bfloat16)};
+  cuuint32_t box[2] = {(cuuint32_t)sm100::BK, (cuuint32_t)box_rows};
+  cuuint32_t estride[2] = {1, 1};
+  CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<__nv_bfloat16*>(base), gdim, gstride, box,
+                           estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) raise(LC_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+}
+
 void approx_plan(ApproxPlan& p, const __nv_bfloat16* rows, int64_t n_rows, int dim, int sm_count) {
   (void)sm_count;
   p.n_rows = n_rows;
   p.dim = dim;
   p.rows = rows;
   p.bn = dim <= 512 ? 128 : 64;
-  cuuint64_t gdim[2] = {(cuuint64_t)dim, (cuuint64_t)n_rows};
-  cuuint64_t gstride[1] = {(cuuint64_t)dim * sizeof(__nv_bfloat16)};
-  cuuint32_t box[2] = {(cuuint32_t)sm100::BK, (cuuint32_t)p.bn};
-  cuuint32_t estride[2] = {1, 1};
-  CUresult r = encode_fn()(&p.tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<__nv_bfloat16*>(rows), gdim, gstride,
-                           box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) raise(LC_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
-  cuuint32_t box2[2] = {(cuuint32_t)sm100::BK, (cuuint32_t)(p.bn / 2)};
-  r = encode_fn()(&p.tmap2, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<__nv_bfloat16*>(rows), gdim, gstride, box2,
-                  estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) raise(LC_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  encode_2d(&p.tmap, rows, n_rows, dim, p.bn);   // single-CTA kernel: [bn rows][64]
+  encode_2d(&p.tmap2, rows, n_rows, dim, sm100::PHB);  // pair kernel: each CTA's [64 rows][64]
   p.valid = true;
 }
 
-// 1 = single-CTA kernel, 2 = CTA-pair kernel (default)
-static int cta_mode() {
+// 1 = single-CTA kernel (N=64/128, all query dims in TMEM; any dim <= 1024),
+// 2 = CTA-pair kernel (N=128, dim <= 768; default)
+static bool use_pair(int dim) {
   const char* e = getenv("FC_SHORTLIST_CTA");
-  return e && atoi(e) == 1 ? 1 : 2;
+  return !(e && atoi(e) == 1) && dim <= 768;
 }
 
 template <int BN>
-static void launch_shortlist(lc_ctx* ctx, const ApproxPlan& plan, sm100::Params prm) {
+static void launch_single(lc_ctx* ctx, const ApproxPlan& plan, sm100::Params prm) {
   // smem: NSTAGE table tiles + a candidate buffer of `cap` (score,row) slots
-  // per query; a deep buffer makes the warp-uniform compactions rare.
-  // several TMA boxes per stage so the single MMA-issuing thread pays one
-  // barrier wait per 8-16 MMAs instead of per 4
+  // per query; several TMA boxes per stage so the single MMA-issuing thread
+  // pays one barrier wait per 8-16 MMAs instead of per 4
   const int nkb = prm.dim / sm100::BK;
   prm.bps = nkb % 4 == 0 ? 4 : nkb % 3 == 0 ? 3 : nkb % 2 == 0 ? 2 : 1;
   if (BN == 128 && prm.bps > 2) prm.bps = nkb % 2 == 0 ? 2 : 1;
-  const bool pair = cta_mode() == 2;
-  const size_t stage_bytes = (size_t)(pair ? BN / 2 : BN) * 128 * prm.bps;
+  const size_t stage_bytes = (size_t)BN * 128 * prm.bps;
   const size_t budget = 227 * 1024 - 1024 - 256;
   const size_t slot_bytes = (size_t)sm100::BM * 8;
   const int64_t want = (int64_t)(prm.kp + 64) * slot_bytes;  // candidate buffer depth
-  prm.nstage = (int)std::max<int64_t>(2, std::min<int64_t>(sm100::MAX_STAGE,((int64_t)budget - want) / (int64_t)stage_bytes));
+  prm.nstage = (int)std::max<int64_t>(2, std::min<int64_t>(sm100::MAX_STAGE, ((int64_t)budget - want) / (int64_t)stage_bytes));
   const int64_t slots = (int64_t)((budget - prm.nstage * stage_bytes) / slot_bytes);
   prm.cap = (int)std::min<int64_t>(slots, prm.kp + 128);
   if (prm.cap < prm.kp + 16) raise(LC_ERR_INVALID_ARGUMENT, "lookup: shortlist too long for shared memory");
   const size_t smem = 1024 + 256 + prm.nstage * stage_bytes + (size_t)prm.cap * slot_bytes;
-  if (pair) {
-    auto kern = sm100::k_shortlist2<BN>;
-    FC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const int grid = 2 * std::min(prm.n_units, ctx->sm_count / 2);
-    KTimer kt(ctx, "shortlist");
-    kern<<<grid, sm100::NTHREADS, smem, ctx->stream>>>(plan.tmap2, prm);
-    kt.stop();
-  } else {
-    auto kern = sm100::k_shortlist<BN>;
-    FC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const int grid = std::min(prm.n_units, ctx->sm_count);
-    KTimer kt(ctx, "shortlist");
-    kern<<<grid, sm100::NTHREADS, smem, ctx->stream>>>(plan.tmap, prm);
-    kt.stop();
+  auto kern = sm100::k_shortlist<BN>;
+  FC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int grid = std::min(prm.n_units, ctx->sm_count);
+  KTimer kt(ctx, "shortlist");
+  kern<<<grid, sm100::NTHREADS, smem, ctx->stream>>>(plan.tmap, prm);
+  kt.stop();
+  FC_LAUNCH_CHECK();
+}
+
+static void launch_pair(lc_ctx* ctx, const ApproxPlan& plan, const CUtensorMap& tmQ, sm100::Params& prm) {
+  using namespace sm100;
+  const int nkb = prm.dim / BK;
+  const int KS = nkb > 8 ? nkb - 8 : 0;
+  const size_t budget = 227 * 1024 - 1024 - 512;
+  const size_t slot_bytes = (size_t)BM * 8;
+  const size_t fixed = (size_t)KS * ABOX;
+  // candidate buffer: kp + 32 slots minimum (compactions stay rare once the
+  // shared threshold is warm); the rest of smem goes to the table ring
+  const int64_t min_cap = prm.kp + 32;
+  {
+    const char* e = getenv("FC_SHORTLIST_BPS");
+    int want = e ? atoi(e) : 2;
+    while (want > 1 && nkb % want) --want;
+    prm.bps = std::max(1, want);
   }
+  const int64_t stage_bytes = (int64_t)prm.bps * PBOX;
+  int64_t nstage = ((int64_t)budget - (int64_t)fixed - min_cap * (int64_t)slot_bytes) / stage_bytes;
+  nstage = std::min<int64_t>(nstage, PMAX_STAGE);
+  if (const char* e = getenv("FC_SHORTLIST_NSTAGE")) nstage = std::min<int64_t>(nstage, atoi(e));
+  if (nstage < 2) raise(LC_ERR_INVALID_ARGUMENT, "lookup: shortlist too long for shared memory");
+  prm.nstage = (int)nstage;
+  prm.cap = (int)std::min<int64_t>((budget - fixed - nstage * stage_bytes) / slot_bytes, prm.kp + 96);
+  const size_t smem = 1024 + 512 + nstage * stage_bytes + fixed + (size_t)prm.cap * slot_bytes;
+  FC_CUDA(cudaFuncSetAttribute(k_shortlist_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int grid = 2 * std::min(prm.n_units, ctx->sm_count / 2);
+  KTimer kt(ctx, "shortlist");
+  k_shortlist_pair<<<grid, NTHREADS, smem, ctx->stream>>>(plan.tmap2, tmQ, prm);
+  kt.stop();
   FC_LAUNCH_CHECK();
 }
 
@@ -898,15 +1100,16 @@ void approx_shortlist(lc_ctx* ctx, const ApproxPlan& plan, const float* Qdev, in
                       uint32_t* cand_r, int32_t* cand_n) {
   using namespace sm100;
   const int dim = plan.dim;
-  const int qt = cta_mode() == 2 ? 2 * BM : BM;  // queries per work unit
+  const bool pair = use_pair(dim);
+  const int qt = pair ? 2 * BM : BM;  // queries per work unit
   const int n_qtiles = (nq + qt - 1) / qt;
   const int nq_pad = n_qtiles * qt;
   DevBuf qb((size_t)nq_pad * dim * sizeof(__nv_bfloat16), ctx->stream);
   k_q_to_bf16<<<grid_for((int64_t)nq_pad * dim, 256), 256, 0, ctx->stream>>>(Qdev, nq, dim, qb.as<__nv_bfloat16>(), nq_pad);
   FC_LAUNCH_CHECK();
-  const int bn = plan.bn;
+  const int bn = pair ? PN : plan.bn;
   const int64_t total_tiles = (plan.n_rows + bn - 1) / bn;
-  const int64_t workers = cta_mode() == 2 ? ctx->sm_count / 2 : ctx->sm_count;  // persistent CTAs / CTA pairs
+  const int64_t workers = pair ? ctx->sm_count / 2 : ctx->sm_count;  // persistent CTAs / CTA pairs
   int64_t splits = std::max<int64_t>(1, (workers * 8 + n_qtiles - 1) / n_qtiles);
   splits = std::min<int64_t>(splits, std::max<int64_t>(1, total_tiles / 16));
   const int64_t tiles_per_split = (total_tiles + splits - 1) / splits;
@@ -930,14 +1133,30 @@ void approx_shortlist(lc_ctx* ctx, const ApproxPlan& plan, const float* Qdev, in
   DevBuf pn((size_t)nq * splits * sizeof(int32_t), ctx->stream);
   DevBuf gk((size_t)nq_pad * sizeof(uint32_t), ctx->stream);
   FC_CUDA(cudaMemsetAsync(gk.p, 0, gk.bytes, ctx->stream));
+  DevBuf st(16, ctx->stream);
+  FC_CUDA(cudaMemsetAsync(st.p, 0, 16, ctx->stream));
+  prm.stats = st.as<uint32_t>();
   prm.gkey = gk.as<uint32_t>();
   prm.part_s = ps.as<float>();
   prm.part_r = pr.as<uint32_t>();
   prm.part_n = pn.as<int32_t>();
-  if (bn == 64)
-    launch_shortlist<64>(ctx, plan, prm);
-  else
-    launch_shortlist<128>(ctx, plan, prm);
+  if (pair) {
+    alignas(64) CUtensorMap tmQ;
+    encode_2d(&tmQ, qb.as<__nv_bfloat16>(), nq_pad, dim, BM);  // smem-resident query boxes [128 q][64]
+    launch_pair(ctx, plan, tmQ, prm);
+  } else if (bn == 64) {
+    launch_single<64>(ctx, plan, prm);
+  } else {
+    launch_single<128>(ctx, plan, prm);
+  }
+  if (prm.debug & 16) {
+    uint32_t h[4];
+    FC_CUDA(cudaMemcpyAsync(h, st.p, 16, cudaMemcpyDeviceToHost, ctx->stream));
+    sync(ctx);
+    fprintf(stderr, "shortlist stats: warp-tiles %u slow-chunks %u (%.3f/tile) compactions %u (%.4f/tile) nstage %d bps %d cap %d splits %d\n",
+            h[2], h[0], h[0] / (double)std::max(1u, h[2]), h[1], h[1] / (double)std::max(1u, h[2]), prm.nstage, prm.bps,
+            prm.cap, prm.n_splits);
+  }
   const size_t msmem = (size_t)splits * kp * sizeof(uint32_t);
   if (msmem > 48 * 1024) FC_CUDA(cudaFuncSetAttribute(k_shortlist_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msmem));
   k_shortlist_merge<<<nq, 256, msmem, ctx->stream>>>(ps.as<float>(), pr.as<uint32_t>(), pn.as<int32_t>(), (int)splits, kp,

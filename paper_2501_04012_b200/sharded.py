@@ -1,0 +1,140 @@
+"""Entry-sharded lookup over one process per GPU (north_star (4)).
+
+The reference has no distribution at all (single process); this
+module adds the one exchange the sharded cache needs. Prompt p lives on rank
+``p mod G`` (all three tables, its compressed entry and its store records), so
+inserts, removes, codec and eviction bookkeeping are rank-local with no
+collective. A lookup batch runs the exact local top-k on every rank
+(tcgen05 shortlist + fp64 rescore, ``lc_index_query_topk``), then ONE
+all-gather of the per-shard candidates — packed as a single int64 tensor
+[tables][n][2k+1] = (ids, fp64 score bits, count) — and every rank merges the
+G lists by (score desc, id asc) with ``lc_topk_merge``. Because that order is
+a total order independent of the partition, the merged result is the
+reference's global top-k (vindex.cpp:58-72) bit for bit; decide and
+similarity_to_step then run on the merged top-1 triple.
+
+``local_topk`` / ``merge`` / ``decide`` are injectable so the host-side logic
+(partition, packing, gather layout, merge order) is covered by world-size-2
+gloo tests on CPU, with the CPU oracle standing in for the GPU kernels there.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+__all__ = ["owner_of", "ShardedIndex", "pack_candidates", "unpack_candidates"]
+
+
+def owner_of(prompt_ids, world: int):
+    """Rank owning each prompt id: id mod G."""
+    return np.asarray(prompt_ids, dtype=np.uint64) % np.uint64(world)
+
+
+def pack_candidates(torch, ids, scores, counts):
+    """(ids i64 [T][n][k], scores f64 [T][n][k], counts i32 [T][n]) -> one i64
+    tensor [T][n][2k+1] so the exchange is a single collective."""
+    T, n, k = ids.shape
+    out = torch.empty((T, n, 2 * k + 1), dtype=torch.int64, device=ids.device)
+    out[:, :, :k] = ids
+    out[:, :, k:2 * k] = scores.contiguous().view(torch.int64)
+    out[:, :, 2 * k] = counts.to(torch.int64)
+    return out
+
+
+def unpack_candidates(torch, g, k):
+    """[G][T][n][2k+1] -> per table (ids [G][n][k], scores [G][n][k], counts [G][n])."""
+    G, T, n, _ = g.shape
+    res = []
+    for t in range(T):
+        ids = g[:, t, :, :k].contiguous()
+        sc = g[:, t, :, k:2 * k].contiguous().view(torch.float64)
+        cnt = g[:, t, :, 2 * k].to(torch.int32).contiguous()
+        res.append((ids, sc, cnt))
+    return res
+
+
+class ShardedIndex:
+    """A rank's shard of the three-table SimilarityIndex plus the collective merge.
+
+    index      this rank's ``SimilarityIndex`` (device) — or None when
+               ``local_topk`` is supplied (CPU tests)
+    group      torch.distributed process group (None = default group)
+    """
+
+    def __init__(self, index=None, group=None, local_topk=None, merge=None, decide=None):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist = torch, dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.index = index
+        self._local_topk = local_topk
+        self._merge = merge
+        self._decide = decide
+        self._nccl = dist.get_backend(group) == "nccl"
+
+    # ---- partition -------------------------------------------------------
+    def mine(self, prompt_ids):
+        return owner_of(prompt_ids, self.world) == np.uint64(self.rank)
+
+    def insert_batch(self, prompt_ids, whole, obj, background):
+        """Insert the rows this rank owns (id mod G == rank); returns how many."""
+        m = self.mine(prompt_ids)
+        if self._local_topk is not None:
+            raise RuntimeError("insert_batch needs a device index")
+        sel = np.nonzero(m)[0]
+        if len(sel) == 0:
+            return 0
+        self.index.insert_batch(np.asarray(prompt_ids, dtype=np.uint64)[sel], whole[sel], obj[sel], background[sel])
+        return len(sel)
+
+    # ---- lookup ----------------------------------------------------------
+    def _topk_local(self, kind, q, k):
+        if self._local_topk is not None:
+            return self._local_topk(kind, q, k)
+        return self.index.query_topk(kind, q, k)
+
+    def _gather(self, packed):
+        torch, dist = self.torch, self.dist
+        G = self.world
+        if self._nccl:
+            g = torch.empty((G,) + tuple(packed.shape), dtype=packed.dtype, device=packed.device)
+            dist.all_gather_into_tensor(g, packed.contiguous(), group=self.group)
+            return g
+        parts = [torch.empty_like(packed) for _ in range(G)]
+        dist.all_gather(parts, packed.contiguous(), group=self.group)
+        return torch.stack(parts)
+
+    def _merge_lists(self, ids, sc, cnt, k):
+        if self._merge is not None:
+            return self._merge(ids, sc, cnt, k)
+        from . import topk_merge
+        return topk_merge(ids, sc, cnt, k, ctx=self.index.ctx)
+
+    def query_topk(self, kind, q, k):
+        """Global exact top-k of a query batch over all shards: (ids, scores, counts)."""
+        torch = self.torch
+        ids, sc, cnt = self._topk_local(kind, q, k)
+        ids, sc, cnt = (torch.as_tensor(np.asarray(x) if not torch.is_tensor(x) else x) for x in (ids, sc, cnt))
+        packed = pack_candidates(torch, ids.view(torch.int64)[None] if ids.dtype == torch.int64 else
+                                 ids.to(torch.int64)[None], sc[None], cnt[None])
+        g = self._gather(packed)
+        gi, gs, gc = unpack_candidates(torch, g, k)[0]
+        return self._merge_lists(gi, gs, gc, k)
+
+    def lookup_decide(self, qw, qo, qb, hit_threshold=0.65, edges=(0.72, 0.79, 0.86, 0.93)):
+        """Fused 3-table sharded lookup + decide + similarity_to_step; one
+        all-gather for the three tables."""
+        torch = self.torch
+        loc = [self._topk_local(t, q, 1) for t, q in enumerate((qw, qo, qb))]
+        ids = torch.stack([torch.as_tensor(x[0]).to(torch.int64) for x in loc])
+        sc = torch.stack([torch.as_tensor(x[1]) for x in loc])
+        cnt = torch.stack([torch.as_tensor(x[2]) for x in loc])
+        g = self._gather(pack_candidates(torch, ids, sc, cnt))
+        top = [self._merge_lists(gi, gs, gc, 1) for gi, gs, gc in unpack_candidates(torch, g, 1)]
+        if self._decide is not None:
+            return self._decide(top, hit_threshold, edges)
+        from . import decide_batch
+        (wi, ws, _), (oi, os_, _), (bi, bs, _) = top
+        return decide_batch(wi[:, 0], ws[:, 0], oi[:, 0], os_[:, 0], bi[:, 0], bs[:, 0], hit_threshold, edges,
+                            ctx=self.index.ctx)

@@ -61,3 +61,29 @@ def test_no_gpu_is_a_loud_error():
     import paper_2501_04012_b200 as fc
     with pytest.raises(fc.LcacheError):
         fc.Context(0)
+
+
+def _cpp_exes():
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("_fc_build", os.path.join(ROOT, "paper_2501_04012_b200", "build.py"))
+    b = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(b)
+    return b.build_cpp_tests()
+
+
+def test_cpp_host_api_compiles_and_links():
+    """include/lcache_b200/lcache.hpp (the reference-named C++ API) builds with
+    -Wall -Wextra against the library; the program resolves every symbol."""
+    exes = _cpp_exes()
+    assert any(e.endswith("wrapper_kat") for e in exes)
+    out = subprocess.run(["ldd", exes[0]], capture_output=True, text=True).stdout
+    assert "libflexcache_b200.so" in out and "not found" not in out.split("libflexcache_b200.so")[1].split("\n")[0]
+
+
+@pytest.mark.gpu
+def test_cpp_host_api_known_answers():
+    """SPEC known answers through the C++ host API on the GPU."""
+    exe = [e for e in _cpp_exes() if e.endswith("wrapper_kat")][0]
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert " 0 failed" in r.stdout

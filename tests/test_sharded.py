@@ -1,0 +1,141 @@
+"""CPU, world size 2 over gloo: the entry-sharded lookup's host-side logic
+(paper_2501_04012_b200/sharded.py) — partition by id mod G, packing of the
+per-shard candidates into one collective, gather layout, merge order and the
+decide step — against the unsharded CPU oracle. The GPU kernels are replaced
+by the oracle here (local top-k) and by a test-side merge; the same module
+drives NCCL + lc_topk_merge on the GPU (bench.py, test_gpu_lookup)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _merge_checker(ids, sc, cnt, k):
+    """Test-side merge of G lists by (score desc, id asc) — the order of
+    vindex.cpp:58-60 generalised to top-k."""
+    import torch
+    ids, sc, cnt = ids.numpy().view(np.uint64), sc.numpy(), cnt.numpy()
+    G, n, _ = ids.shape
+    oi = np.zeros((n, k), np.uint64)
+    os_ = np.zeros((n, k), np.float64)
+    oc = np.zeros(n, np.int32)
+    for q in range(n):
+        c = [(-sc[g, q, j], int(ids[g, q, j])) for g in range(G) for j in range(cnt[g, q])]
+        c.sort()
+        c = c[:k]
+        oc[q] = len(c)
+        for j, (s, i) in enumerate(c):
+            oi[q, j] = i
+            os_[q, j] = -s
+    return torch.from_numpy(oi.view(np.int64)), torch.from_numpy(os_), torch.from_numpy(oc)
+
+
+def _worker(rank, world, port, n, d, nq, k, seed, out_dir):
+    import sys
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import torch
+    import torch.distributed as dist
+    from oracle import Checker
+    from paper_2501_04012_b200 import sharded
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    orc = Checker("orc")
+    rng = np.random.default_rng(seed)
+    ids = rng.permutation(np.arange(n, dtype=np.uint64) * 3 + 5)
+    tabs = [orc.normalize_rows(rng.standard_normal((n, d)).astype(np.float32)) for _ in range(3)]
+    if n > 8:
+        tabs[0][7] = tabs[0][3]  # exact duplicate rows across shards: ties -> smaller id
+        tabs[0][8] = tabs[0][3]
+    q = [np.ascontiguousarray(t[rng.integers(0, n, nq)] + 0.05 * rng.standard_normal((nq, d)).astype(np.float32))
+         for t in tabs]
+    q = [orc.normalize_rows(x) for x in q]
+    q[0][0] = tabs[0][min(3, n - 1)]  # query that hits the duplicated rows exactly
+    owner = sharded.owner_of(ids, world)
+    mine = owner == np.uint64(rank)
+    shard_ids = ids[mine]
+    shard_tabs = [np.ascontiguousarray(t[mine]) for t in tabs]
+
+    def local_topk(kind, qq, kk):
+        i, s, c = orc.topk_flat(shard_tabs[kind], shard_ids, np.ascontiguousarray(qq), kk)
+        return torch.from_numpy(i.view(np.int64)), torch.from_numpy(s), torch.from_numpy(c)
+
+    def decide(top, thr, edges):
+        (wi, ws, _), (oi, os_, _), (bi, bs, _) = top
+        res = []
+        for j in range(wi.shape[0]):
+            kind, score = orc.decide(float(ws[j, 0]), float(os_[j, 0]), float(bs[j, 0]), thr)
+            res.append((kind, score, orc.similarity_to_step(score, thr, edges) if kind else 0))
+        return res
+
+    sh = sharded.ShardedIndex(local_topk=local_topk, merge=_merge_checker, decide=decide)
+    assert sh.world == world and sh.rank == rank
+    gi, gs, gc = sh.query_topk(0, q[0], k)
+    dec = sh.lookup_decide(q[0], q[1], q[2])
+    np.savez(os.path.join(out_dir, f"r{rank}.npz"), ids=gi.numpy(), sc=gs.numpy(), cnt=gc.numpy(),
+             dec=np.array(dec, dtype=np.float64), n_local=int(mine.sum()))
+    if rank == 0:
+        ri, rs, rc = orc.topk_flat(tabs[0], ids, q[0], k)
+        top1 = [orc.topk_flat(tabs[t], ids, q[t], 1) for t in range(3)]
+        np.savez(os.path.join(out_dir, "ref.npz"), ids=ri.view(np.int64), sc=rs, cnt=rc,
+                 top1=np.stack([np.stack([x[1][:, 0] for x in top1])]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n,k", [(600, 8), (5, 8)])
+def test_sharded_topk_and_decide_match_unsharded_oracle(tmp_path, n, k):
+    import torch.multiprocessing as mp
+    world, d, nq = 2, 64, 40
+    mp.spawn(_worker, args=(world, _free_port(), n, d, nq, k, 17, str(tmp_path)), nprocs=world, join=True)
+    ref = np.load(tmp_path / "ref.npz")
+    r0, r1 = np.load(tmp_path / "r0.npz"), np.load(tmp_path / "r1.npz")
+    assert r0["n_local"] + r1["n_local"] == n and r0["n_local"] > 0 and r1["n_local"] > 0
+    for r in (r0, r1):  # every rank holds the same, exact global answer
+        assert (r["cnt"] == ref["cnt"]).all()
+        for q in range(nq):
+            c = ref["cnt"][q]
+            assert (r["ids"][q, :c] == ref["ids"][q, :c]).all()
+            assert (r["sc"][q, :c].view(np.uint64) == ref["sc"][q, :c].view(np.uint64)).all()
+    assert (r0["dec"] == r1["dec"]).all()
+    if n > 8:
+        # the three identical rows tie: the merged list orders them by ascending id
+        top = r0["ids"][0, :3]
+        assert (np.diff(top) > 0).all() and (r0["sc"][0, :3] == r0["sc"][0, 0]).all()
+
+
+def test_owner_partition_is_id_mod_world():
+    from paper_2501_04012_b200 import sharded
+    ids = np.arange(20, dtype=np.uint64) * 7
+    for G in (1, 2, 4, 8):
+        o = sharded.owner_of(ids, G)
+        assert (o == ids % G).all()
+        assert sum((o == g).sum() for g in range(G)) == len(ids)
+
+
+def test_pack_unpack_roundtrip():
+    import torch
+    from paper_2501_04012_b200 import sharded
+    T, n, k = 3, 5, 4
+    ids = torch.randint(0, 1 << 62, (T, n, k), dtype=torch.int64)
+    sc = torch.randn(T, n, k, dtype=torch.float64)
+    cnt = torch.randint(0, k + 1, (T, n), dtype=torch.int32)
+    p = sharded.pack_candidates(torch, ids, sc, cnt)
+    assert p.shape == (T, n, 2 * k + 1) and p.dtype == torch.int64
+    back = sharded.unpack_candidates(torch, p[None].expand(2, T, n, 2 * k + 1).contiguous(), k)
+    for t in range(T):
+        bi, bs, bc = back[t]
+        assert (bi[1] == ids[t]).all() and (bs[0].view(torch.int64) == sc[t].view(torch.int64)).all()
+        assert (bc[1] == cnt[t]).all()
