@@ -374,6 +374,85 @@ __device__ __forceinline__ void publish_tau(uint32_t* gkey, int q, const float* 
   atomicMax(gkey + q, okey(m));
 }
 
+
+// ---- per-query acceptance histogram (pair kernel) ----
+// hist[q][b] counts, over ALL work units of query q, the accepted bf16
+// scores falling in bucket b (32 buckets per octave on [2^-8, 1), bucket 0
+// = below 2^-8, bucket HB-1 = >= 1). If the buckets >= B hold >= kp counts,
+// the final merged shortlist of q holds >= kp entries >= edge(B): every unit
+// keeps its top min(kp, accepted) entries and the entries >= edge(B) are its
+// largest, so sum_i min(kp, a_i) >= min(kp, sum_i a_i) = kp. Any unit may
+// therefore reject scores <= edge(B) at once; the units of one query, which
+// run concurrently on different row ranges, pool their evidence instead of
+// each warming its own threshold.
+constexpr int HB = 264;         // fine buckets (HB-8 .. HB-1 unused padding)
+constexpr int HC = 272;         // coarse counters at [HC, HC+16): octave o = (b-1)/32 (0..7), 8 = >= 1.0
+constexpr int HSTRIDE = 288;    // per-query words
+__device__ __forceinline__ int hbucket(float s) {
+  const uint32_t u = __float_as_uint(s);
+  if ((int32_t)u < 0) return 0;  // negative
+  const int e = (int)(u >> 23);
+  if (e < 119) return 0;
+  if (e >= 127) return 257;
+  return 1 + (e - 119) * 32 + (int)((u >> 18) & 31);
+}
+__device__ __forceinline__ float hedge(int b) {  // smallest score of bucket b >= 1
+  if (b >= 257) return 1.0f;
+  const int e = 119 + (b - 1) / 32, m = (b - 1) % 32;
+  return __uint_as_float(((uint32_t)e << 23) | ((uint32_t)m << 18));
+}
+__device__ __forceinline__ void hist_publish(uint32_t* h, const float* ls, int t, int from, int to) {
+  for (int i = from; i < to; ++i) {
+    const int bk = hbucket(ls[i * BM + t]);
+    if (bk == 0) continue;  // never used to raise a threshold
+    atomicAdd(h + bk, 1u);
+    atomicAdd(h + HC + (bk - 1) / 32, 1u);
+  }
+}
+// Raise tau to the lower edge of the highest bucket B with sum_{b>=B} h[b] >= kp.
+// Two rounds of independent loads: the 9 octave counters, then the 32 fine
+// buckets of the octave where the running count from the top reaches kp.
+__device__ __forceinline__ void hist_refresh(const uint32_t* h, int kp, float& tau) {
+  const uint4* hc = reinterpret_cast<const uint4*>(h + HC);
+  const uint4 c0 = __ldcg(hc), c1 = __ldcg(hc + 1), c2 = __ldcg(hc + 2);
+  const uint32_t oc[9] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w, c2.x};
+  int sum = (int)oc[8];
+  if (sum >= kp) {
+    if (1.0f > tau) tau = 1.0f;
+    return;
+  }
+  int o = 7;
+  for (; o >= 0; --o) {
+    if (sum + (int)oc[o] >= kp) break;
+    sum += (int)oc[o];
+  }
+  if (o < 0) return;
+  if (hedge(1 + o * 32 + 31) <= tau) return;  // nothing in reach above tau
+  const uint4* hv = reinterpret_cast<const uint4*>(h + 1 + o * 32 - 1);  // 16-byte aligned block [o*32, o*32+32)
+  uint32_t f[33];
+  // fine buckets 1+o*32 .. 32+o*32 live at words o*32+1 .. o*32+32: load words o*32 .. o*32+35
+  uint4 x[9];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) x[i] = __ldcg(hv + i);
+#pragma unroll
+  for (int i = 0; i < 9; ++i) {
+    if (4 * i + 0 <= 32) f[4 * i + 0] = x[i].x;
+    if (4 * i + 1 <= 32) f[4 * i + 1] = x[i].y;
+    if (4 * i + 2 <= 32) f[4 * i + 2] = x[i].z;
+    if (4 * i + 3 <= 32) f[4 * i + 3] = x[i].w;
+  }
+  // f[j] = word o*32 + j; fine bucket 1 + o*32 + jj is word o*32 + 1 + jj = f[1 + jj]
+#pragma unroll
+  for (int jj = 31; jj >= 0; --jj) {
+    sum += (int)f[1 + jj];
+    if (sum >= kp) {
+      const float e = hedge(1 + o * 32 + jj);
+      if (e > tau) tau = e;
+      return;
+    }
+  }
+}
+
 struct Params {
   const __nv_bfloat16* Qb;  // [nq_pad][dim]
   int nq;                    // real queries
@@ -387,6 +466,7 @@ struct Params {
   int cap;     // candidate buffer slots per query (>= kp + 16)
   int bps;     // TMA boxes per pipeline stage
   uint32_t* gkey;  // [nq_pad] shared per-query thresholds (order keys, 0 = unset)
+  uint32_t* hist;   // [nq_pad][HB] acceptance histogram (pair kernel)
   uint32_t* stats;  // FC_SHORTLIST_DEBUG & 16: [slow chunks, compactions, warp-tiles]
   int debug;   // diagnostics (FC_SHORTLIST_DEBUG): 1 = skip MMA, 2 = skip TMA, 4 = skip epilogue filter
   int nstage;
@@ -838,13 +918,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         if (lane == 0) mbar_arrive_remote(smem_u32(aready), 0);
       }
       // (2) stream the accumulator tiles through the running-threshold filter
-      int cnt = 0;
+      int cnt = 0, pub = 0;  // entries [pub, cnt) not yet counted in the histogram
       float tau = -INFINITY;
-      refresh_tau(p.gkey, q, tau);
+      uint32_t* hq = p.hist + (size_t)q * HSTRIDE;
+      hist_refresh(hq, p.kp, tau);
       for (int64_t row = r0; row < r1; row += PN, ++tile) {
         const uint32_t b = tile & 1;
         const uint32_t use = tile >> 1;
-        if ((tile & 3) == 0) refresh_tau(p.gkey, q, tau);
+        if ((tile & 15) == 0) {
+          hist_publish(hq, ls, t, pub, cnt);
+          pub = cnt;
+          hist_refresh(hq, p.kp, tau);
+        }
         mbar_wait(smem_u32(&accf[b]), use & 1);
         tc_fence_after();
         if ((p.debug & 16) && lane == 0) atomicAdd(p.stats + 2, 1u);
@@ -877,9 +962,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             if ((p.debug & 16) && lane == 0) atomicAdd(p.stats + 0, 1u);
             if (__any_sync(0xffffffffu, cnt + 16 > cap)) {
               if ((p.debug & 16) && lane == 0) atomicAdd(p.stats + 1, 1u);
-              const float old_tau = tau;
+              hist_publish(hq, ls, t, pub, cnt);  // count before compaction may drop entries
               compact2(ls, lr, t, cnt, p.kp, tau);
-              if (tau > old_tau) atomicMax(p.gkey + q, okey(tau));  // share the raised threshold at once
+              pub = cnt;
             }
             const uint32_t r32 = (uint32_t)(row + c0);
 #pragma unroll
@@ -894,8 +979,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
           }
         }
       }
+      hist_publish(hq, ls, t, pub, cnt);
       compact(ls, lr, t, cnt, p.kp, tau);  // exact: the unit's list holds at most kp entries
-      publish_tau(p.gkey, q, ls, t, cnt, p.kp);
       if (q < p.nq) {
         const size_t o = ((size_t)q * p.n_splits + split) * p.kp;
         for (int i = 0; i < cnt; ++i) {
@@ -1135,6 +1220,9 @@ void approx_shortlist(lc_ctx* ctx, const ApproxPlan& plan, const float* Qdev, in
   FC_CUDA(cudaMemsetAsync(gk.p, 0, gk.bytes, ctx->stream));
   DevBuf st(16, ctx->stream);
   FC_CUDA(cudaMemsetAsync(st.p, 0, 16, ctx->stream));
+  DevBuf hist(pair ? (size_t)nq_pad * HSTRIDE * sizeof(uint32_t) : 16, ctx->stream);
+  if (pair) FC_CUDA(cudaMemsetAsync(hist.p, 0, hist.bytes, ctx->stream));
+  prm.hist = hist.as<uint32_t>();
   prm.stats = st.as<uint32_t>();
   prm.gkey = gk.as<uint32_t>();
   prm.part_s = ps.as<float>();
