@@ -339,17 +339,59 @@ __device__ __forceinline__ float4 recon4(const float* base, const Recipe& r, int
                      (float)fma(al, (double)b.z, (double)a.z), (float)fma(al, (double)b.w, (double)a.w));
 }
 
-// grid.x = item * F + frame, grid.y = chunks of 4*blockDim floats
-__global__ void __launch_bounds__(256) k_decompress(const DecItem* __restrict__ items, int F, int64_t E) {
+// One block per output frame (grid.x = item * F + frame): the recipe is
+// block-uniform, so the kind branch is hoisted out of the streaming loop and
+// each thread keeps DEC_U float4 loads (x2 for two-source kinds) in flight.
+// Loads use the read-only path; stores are streaming (.cs): the output is
+// written once and not re-read by this kernel.
+constexpr int DEC_T = 256, DEC_U = 4;
+template <int KIND>
+__device__ __forceinline__ void dec_frame(const float* __restrict__ a, const float* __restrict__ b, float alpha,
+                                          float* __restrict__ out, int64_t n4) {
+  const float4* a4 = reinterpret_cast<const float4*>(a);
+  const float4* b4 = reinterpret_cast<const float4*>(b);
+  float4* o4 = reinterpret_cast<float4*>(out);
+  const double al = alpha;
+  for (int64_t i0 = threadIdx.x; i0 < n4; i0 += (int64_t)DEC_T * DEC_U) {
+    float4 va[DEC_U], vb[DEC_U];
+#pragma unroll
+    for (int u = 0; u < DEC_U; ++u) {
+      const int64_t i = i0 + (int64_t)u * DEC_T;
+      if (i < n4) {
+        va[u] = __ldg(a4 + i);
+        if (KIND != 0) vb[u] = __ldg(b4 + i);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < DEC_U; ++u) {
+      const int64_t i = i0 + (int64_t)u * DEC_T;
+      if (i >= n4) break;
+      float4 r = va[u];
+      if (KIND == 1) {
+        r = make_float4(va[u].x + vb[u].x, va[u].y + vb[u].y, va[u].z + vb[u].z, va[u].w + vb[u].w);
+      } else if (KIND == 2) {
+        r = make_float4((float)fma(al, (double)vb[u].x, (double)va[u].x), (float)fma(al, (double)vb[u].y, (double)va[u].y),
+                        (float)fma(al, (double)vb[u].z, (double)va[u].z), (float)fma(al, (double)vb[u].w, (double)va[u].w));
+      }
+      __stcs(o4 + i, r);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(DEC_T) k_decompress(const DecItem* __restrict__ items, int F, int64_t E) {
   const int item = blockIdx.x / F, j = blockIdx.x - item * F;
   const DecItem it = items[item];
   const Recipe r = it.rec[j];
   float* out = it.out + (int64_t)j * E;
-  const int64_t i = ((int64_t)blockIdx.y * blockDim.x + threadIdx.x) * 4;
   if ((E & 3) == 0) {
-    if (i < E) __stcs(reinterpret_cast<float4*>(out + i), recon4(it.base, r, i));
+    const int64_t n4 = E >> 2;
+    const float* a = it.base + r.a;
+    const float* b = it.base + r.b;
+    if (r.kind == 0) dec_frame<0>(a, b, r.alpha, out, n4);
+    else if (r.kind == 1) dec_frame<1>(a, b, r.alpha, out, n4);
+    else dec_frame<2>(a, b, r.alpha, out, n4);
   } else {
-    for (int64_t x = i; x < min(E, i + 4); ++x) out[x] = recon(it.base, r, x);
+    for (int64_t x = threadIdx.x; x < E; x += DEC_T) out[x] = recon(it.base, r, x);
   }
 }
 
@@ -367,25 +409,43 @@ __device__ __forceinline__ bool mask_bit(const uint8_t* m, int64_t p) { return (
 
 // Fused decompress(obj) / decompress(bg) / stitch: pixel p of frame j is the
 // object source's iff objsrc.object_mask | bgsrc.object_mask (stitcher.cpp:25-37).
-__global__ void __launch_bounds__(256) k_decompress_stitch(const StitchItem* __restrict__ items, int F, int64_t E,
-                                                           int C, int64_t mb) {
+// One block per output frame; the frame's two mask planes are OR-ed into
+// shared memory once, then each float4 (one pixel when C == 4) reads only the
+// source its bit selects.
+__global__ void __launch_bounds__(DEC_T) k_decompress_stitch(const StitchItem* __restrict__ items, int F, int64_t E,
+                                                             int C, int64_t mb) {
+  extern __shared__ uint8_t s_m[];  // [mb] OR of the two object masks
   const int item = blockIdx.x / F, j = blockIdx.x - item * F;
   const StitchItem it = items[item];
   const Recipe ro = it.orec[j], rb = it.brec[j];
   const uint8_t* om = it.om + (int64_t)j * mb;
   const uint8_t* sm = it.sm + (int64_t)j * mb;
+  for (int64_t x = threadIdx.x; x < mb; x += DEC_T) s_m[x] = om[x] | sm[x];
+  __syncthreads();
   float* out = it.out + (int64_t)j * E;
-  const int64_t i = ((int64_t)blockIdx.y * blockDim.x + threadIdx.x) * 4;
   if (C == 4) {
-    if (i < E) {
-      const int64_t p = i >> 2;
-      const bool obj = mask_bit(om, p) | mask_bit(sm, p);
-      __stcs(reinterpret_cast<float4*>(out + i), obj ? recon4(it.obase, ro, i) : recon4(it.bbase, rb, i));
+    float4* o4 = reinterpret_cast<float4*>(out);
+    const int64_t n4 = E >> 2;
+    for (int64_t i0 = threadIdx.x; i0 < n4; i0 += (int64_t)DEC_T * DEC_U) {
+      float4 r[DEC_U];
+#pragma unroll
+      for (int u = 0; u < DEC_U; ++u) {
+        const int64_t i = i0 + (int64_t)u * DEC_T;
+        if (i < n4) {
+          const bool obj = (s_m[i >> 3] >> (i & 7)) & 1;
+          r[u] = obj ? recon4(it.obase, ro, i * 4) : recon4(it.bbase, rb, i * 4);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < DEC_U; ++u) {
+        const int64_t i = i0 + (int64_t)u * DEC_T;
+        if (i < n4) __stcs(o4 + i, r[u]);
+      }
     }
   } else {
-    for (int64_t x = i; x < min(E, i + 4); ++x) {
+    for (int64_t x = threadIdx.x; x < E; x += DEC_T) {
       const int64_t p = x / C;
-      const bool obj = mask_bit(om, p) | mask_bit(sm, p);
+      const bool obj = (s_m[p >> 3] >> (p & 7)) & 1;
       out[x] = obj ? recon(it.obase, ro, x) : recon(it.bbase, rb, x);
     }
   }
@@ -723,9 +783,8 @@ void launch_decompress(lc_ctx* ctx, const std::vector<const EntryData*>& ents, c
     items[i] = DecItem{ents[i]->fbase(), ents[i]->recipes(sidx[i]), out + (int64_t)i * F * E};
   DevBuf di(items.size() * sizeof(DecItem), ctx->stream);
   FC_CUDA(cudaMemcpyAsync(di.p, items.data(), di.bytes, cudaMemcpyHostToDevice, ctx->stream));
-  const unsigned gy = (unsigned)((E + 1023) / 1024);
   KTimer kt(ctx, "decompress");
-  k_decompress<<<dim3((unsigned)(items.size() * F), gy), 256, 0, ctx->stream>>>(di.as<DecItem>(), F, E);
+  k_decompress<<<(unsigned)(items.size() * F), DEC_T, 0, ctx->stream>>>(di.as<DecItem>(), F, E);
   kt.stop();
   FC_LAUNCH_CHECK();
   count_launch(ctx);
@@ -1158,10 +1217,9 @@ lc_status lc_decompress_stitch_batch(lc_ctx* ctx, lc_entry* const* oe, lc_entry*
   }
   DevBuf di(items.size() * sizeof(StitchItem), ctx->stream);
   FC_CUDA(cudaMemcpyAsync(di.p, items.data(), di.bytes, cudaMemcpyHostToDevice, ctx->stream));
-  const unsigned gy = (unsigned)((d0->E + 1023) / 1024);
   KTimer kt(ctx, "decompress_stitch");
-  k_decompress_stitch<<<dim3((unsigned)(n * d0->F), gy), 256, 0, ctx->stream>>>(di.as<StitchItem>(), d0->F, d0->E, d0->C,
-                                                                                d0->mb);
+  k_decompress_stitch<<<(unsigned)(n * d0->F), DEC_T, (size_t)d0->mb, ctx->stream>>>(di.as<StitchItem>(), d0->F, d0->E,
+                                                                                     d0->C, d0->mb);
   FC_LAUNCH_CHECK();
   count_launch(ctx);
   sync(ctx);

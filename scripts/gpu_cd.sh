@@ -1,0 +1,3 @@
+export CUDA_MODULE_LOADING=EAGER
+timeout -s KILL 600 python -m pytest tests/test_gpu_codec.py tests/test_gpu_store.py -q -x -m gpu 2>&1 | tail -3
+timeout -s KILL 300 python scripts/time_codec.py
