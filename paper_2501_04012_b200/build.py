@@ -13,7 +13,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(OUT_DIR, "libflexcache_b200.so")
-SOURCES = ["core.cu", "index.cu", "lookup_sm100.cu", "codec.cu", "store.cu"]
+SOURCES = ["core.cu", "index.cu", "lookup_sm100.cu", "gram_sm100.cu", "codec.cu", "store.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off", "-Xptxas", "-v",
@@ -27,10 +27,26 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def _digest(paths):
+    import hashlib
+    h = hashlib.sha1(" ".join(ARCH + FLAGS).encode())
+    for p in sorted(paths):
+        with open(p, "rb") as f:
+            h.update(p.encode() + b"\0" + f.read())
+    return h.hexdigest()
+
+
 def build(verbose: bool = False, jobs: int = 8) -> str:
     os.makedirs(OUT_DIR, exist_ok=True)
-    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
+    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h", ".hpp"))]
     headers.append(os.path.join(ROOT, "include", "flexcache_b200.h"))
+    # content stamp: a repo snapshot copied to another machine (gpurun) gets new
+    # mtimes in arbitrary order; an unchanged source tree must not recompile
+    stamp = os.path.join(OUT_DIR, "build.stamp")
+    srcs = [os.path.join(CSRC, f) for f in SOURCES if os.path.exists(os.path.join(CSRC, f))]
+    dig = _digest(srcs + headers)
+    if os.path.exists(LIB) and os.path.exists(stamp) and open(stamp).read().strip() == dig:
+        return LIB
     objs, procs = [], []
     for src in SOURCES:
         s = os.path.join(CSRC, src)
@@ -49,6 +65,8 @@ def build(verbose: bool = False, jobs: int = 8) -> str:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError("link failed:\n" + r.stdout + r.stderr)
+    with open(stamp, "w") as f:
+        f.write(dig)
     return LIB
 
 

@@ -22,16 +22,30 @@
 // recipes; the decoupled-hit variant fuses the mask select of stitch() so
 // each output pixel is reconstructed only from the source it is taken from.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <numeric>
+#include <thread>
+#include <mutex>
 
 #include "entry.hpp"
 
 namespace fc {
 
+// gram_sm100.cu
+bool gram_tc_supported(int F, int64_t E, const float* lat);
+void gram_tc(lc_ctx* ctx, const float* lat, int n_items, int F, int64_t E, double* G, double* nrm, int* bad);
+
+DevArena::~DevArena() {
+  if (p) {
+    DeviceGuard g(ctx->device);
+    cudaFreeAsync(p, ctx->stream);
+  }
+}
+
 EntryData::~EntryData() {
-  if (dev) {
+  if (dev && !arena) {
     DeviceGuard g(ctx->device);
     cudaFreeAsync(dev, ctx->stream);
   }
@@ -53,6 +67,8 @@ uint64_t entry_compressed_size(const lc_entry* e) {
 // ---------------------------------------------------------------------------
 // kernels
 // ---------------------------------------------------------------------------
+constexpr int DEC_T = 256, DEC_U = 4;  // streaming kernels: threads per block, float4 loads in flight
+
 __global__ void k_nonfinite(const float* __restrict__ v, int64_t n, int* __restrict__ bad) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     if (!isfinite(v[i])) {
@@ -127,43 +143,155 @@ __global__ void __launch_bounds__(64) k_gram(const float* __restrict__ lat, int 
     }
 }
 
-// Greedy forward key-frame selection (codec.cpp:146-163) on the Gram matrix:
-// sim(j,k) = G[j][k] / (sqrt(G[j][j]) * sqrt(G[k][k])) (core.cpp:113).
-__global__ void k_select(const double* __restrict__ G, int n_items, int F, double thr, int32_t* __restrict__ maps,
-                         int* __restrict__ bad) {
-  const int item = blockIdx.x * blockDim.x + threadIdx.x;
+// Sequential fp64 dot in element order (core.cpp:104-110); float4 loads run
+// ahead of the dependent FMA chain.
+__device__ __forceinline__ double exact_dot(const float* __restrict__ a, const float* __restrict__ b, int64_t E) {
+  double dot = 0.0;
+  int64_t i = 0;
+  if ((E & 3) == 0 && ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15) == 0) {
+    const float4* a4 = reinterpret_cast<const float4*>(a);
+    const float4* b4 = reinterpret_cast<const float4*>(b);
+    const int64_t n4 = E >> 2;
+    for (int64_t q = 0; q < n4; q += 4) {
+      float4 va[4], vb[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (q + u < n4) {
+          va[u] = __ldg(a4 + q + u);
+          vb[u] = __ldg(b4 + q + u);
+        }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (q + u < n4) {
+          dot = fma((double)va[u].x, (double)vb[u].x, dot);
+          dot = fma((double)va[u].y, (double)vb[u].y, dot);
+          dot = fma((double)va[u].z, (double)vb[u].z, dot);
+          dot = fma((double)va[u].w, (double)vb[u].w, dot);
+        }
+    }
+    return dot;
+  }
+  for (; i < E; ++i) dot = fma((double)a[i], (double)b[i], dot);
+  return dot;
+}
+
+// select_keyframes (codec.cpp:138-165) from an APPROXIMATE Gram with a
+// certified bound (gram_sm100.cu): a(j,k) = G~(j,k) / (sqrt(n_j) sqrt(n_k))
+// with exact norms satisfies |a - s| <= delta, s = the reference's
+// frame_similarity. For frame j and the current keys: if no key has
+// a >= thr - delta, j is certainly a key; if one key has a >= thr + delta
+// and every other candidate a < a_best - 2 delta, it is certainly the
+// strict-'>' argmax. Otherwise the warp computes the exact sequential fp64
+// dot (core.cpp:104-110 order) of every candidate pair, one lane per pair,
+// and applies the reference rule to the exact values. delta = 0 (exact
+// Gram) takes the exact values directly. One warp per (prompt, step) item.
+__global__ void __launch_bounds__(128) k_select_cert(const double* __restrict__ G, const double* __restrict__ nrm,
+                                                     const float* __restrict__ lat, int n_items, int F, int64_t E,
+                                                     double thr, double delta, int32_t* __restrict__ maps,
+                                                     int* __restrict__ bad, unsigned* __restrict__ n_exact) {
+  __shared__ int s_keys[4][256];
+  __shared__ double s_sim[4][256];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int item = blockIdx.x * 4 + w;
   if (item >= n_items) return;
   const double* g = G + (int64_t)item * F * F;
+  const double* nr = nrm + (int64_t)item * F;
+  const float* X = lat + (int64_t)item * F * E;
   int32_t* map = maps + (int64_t)item * F;
-  int keys[256];
-  int nk = 0;
-  map[0] = 0;
-  keys[nk++] = 0;
+  int* keys = s_keys[w];
+  double* sim = s_sim[w];
   if (F >= 2) {
-    for (int j = 0; j < F; ++j)
-      if (g[(int64_t)j * F + j] == 0.0) {  // cosine_similarity throws (core.cpp:111-112)
-        atomicExch(bad, 1);
-        return;
-      }
+    bool z = false;
+    for (int j = lane; j < F; j += 32) z |= nr[j] == 0.0;
+    if (__any_sync(0xffffffffu, z)) {  // cosine_similarity throws on a zero-norm operand (core.cpp:111-112)
+      if (lane == 0) atomicExch(bad, 1);
+      return;
+    }
   }
+  int nk = 1;
+  if (lane == 0) {
+    keys[0] = 0;
+    map[0] = 0;
+  }
+  __syncwarp();
   for (int j = 1; j < F; ++j) {
-    int best = -1;
-    double best_sim = 0.0;
-    const double sj = sqrt(g[(int64_t)j * F + j]);
-    for (int t = 0; t < nk; ++t) {
+    const double sj = sqrt(nr[j]);
+    // approximate similarity to every current key; candidates: a >= thr - delta
+    double amax = -1e300;
+    int kmax = 1 << 30;
+    int ncand = 0;
+    for (int t = lane; t < nk; t += 32) {
       const int k = keys[t];
-      const double sim = g[(int64_t)j * F + k] / (sj * sqrt(g[(int64_t)k * F + k]));
-      if (sim >= thr && (best < 0 || sim > best_sim)) {
-        best = k;
-        best_sim = sim;
+      const double a = g[(int64_t)j * F + k] / (sj * sqrt(nr[k]));
+      sim[t] = a;
+      if (a >= thr - delta) {
+        ++ncand;
+        if (a > amax || (a == amax && t < kmax)) {
+          amax = a;
+          kmax = t;
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      ncand += __shfl_xor_sync(0xffffffffu, ncand, o);
+      const double am = __shfl_xor_sync(0xffffffffu, amax, o);
+      const int km = __shfl_xor_sync(0xffffffffu, kmax, o);
+      if (am > amax || (am == amax && km < kmax)) {
+        amax = am;
+        kmax = km;
+      }
+    }
+    __syncwarp();
+    int best = -1;  // index into keys
+    if (ncand > 0) {
+      bool certain = delta == 0.0;
+      if (!certain && amax >= thr + delta) {
+        bool close = false;
+        for (int t = lane; t < nk; t += 32)
+          close |= t != kmax && sim[t] >= thr - delta && sim[t] >= amax - 2.0 * delta;
+        certain = !__any_sync(0xffffffffu, close);
+      }
+      if (certain) {
+        // exact Gram: the reference rule on exact values (first max wins);
+        // certified: the approximate argmax is the exact one
+        if (amax >= thr) best = kmax;
+      } else {
+        // exact sequential fp64 dot for every candidate, one lane per pair
+        for (int t0 = 0; t0 < nk; t0 += 32) {
+          const int t = t0 + lane;
+          const bool mine = t < nk && sim[t] >= thr - delta;
+          if (mine) {
+            const int k = keys[t];
+            sim[t] = exact_dot(X + (int64_t)j * E, X + (int64_t)k * E, E) / (sj * sqrt(nr[k]));
+          }
+          if (mine) atomicAdd(n_exact, 1u);
+        }
+        __syncwarp();
+        // strict '>' over ascending key order (codec.cpp:152-156)
+        double bs = 0.0;
+        if (lane == 0) {
+          for (int t = 0; t < nk; ++t) {
+            const double a = sim[t];
+            if (a >= thr - delta && a >= thr && (best < 0 || a > bs)) {
+              best = t;
+              bs = a;
+            }
+          }
+        }
+        best = __shfl_sync(0xffffffffu, best, 0);
       }
     }
     if (best < 0) {
-      map[j] = j;
-      keys[nk++] = j;
-    } else {
-      map[j] = best;
+      if (lane == 0) {
+        keys[nk] = j;
+        map[j] = j;
+      }
+      ++nk;
+    } else if (lane == 0) {
+      map[j] = keys[best];
     }
+    __syncwarp();
   }
 }
 
@@ -190,103 +318,141 @@ struct InterItem {
 
 // One block per (prompt, common key m > 0). Steps are in ascending order
 // through perm (sorted index -> input index).
-constexpr int INTER_T = 64;
-constexpr int INTER_CH = 256;
-__global__ void __launch_bounds__(INTER_T) k_inter(const float* __restrict__ lat, const InterItem* __restrict__ items,
-                                                   int S, const int* __restrict__ perm, int F, int64_t E,
-                                                   const double* __restrict__ G, InterRes* __restrict__ out) {
-  __shared__ float s_key[MAXS][INTER_CH];
-  __shared__ float s_first[MAXS][INTER_CH];
-  __shared__ double s_num[MAXS][MAXS];
-  __shared__ float s_alpha[MAXS][MAXS];
-  __shared__ int s_nz[MAXS], s_exact[MAXS];
-  const InterItem it = items[blockIdx.x];
+// Streams four frames in element order through `step` with the float4 loads
+// of the next 16 elements issued before the current 16 are consumed, so the
+// dependent fp64 chain does not wait on memory latency every iteration.
+template <class Step>
+__device__ __forceinline__ void stream4(const float* __restrict__ p0, const float* __restrict__ p1,
+                                        const float* __restrict__ p2, const float* __restrict__ p3, int64_t E, Step step) {
+  constexpr int U = 4;
+  const float4 *a = reinterpret_cast<const float4*>(p0), *b = reinterpret_cast<const float4*>(p1),
+               *c = reinterpret_cast<const float4*>(p2), *d = reinterpret_cast<const float4*>(p3);
+  const int64_t n4 = E >> 2;
+  float4 A[U], B[U], C[U], D[U];
+  auto load = [&](int64_t q0) {  // n4 % U == 0 (callers require E % 16 == 0)
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      A[u] = __ldg(a + q0 + u);
+      B[u] = __ldg(b + q0 + u);
+      C[u] = __ldg(c + q0 + u);
+      D[u] = __ldg(d + q0 + u);
+    }
+  };
+  load(0);
+  for (int64_t q0 = 0; q0 < n4; q0 += U) {
+    float4 A2[U], B2[U], C2[U], D2[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      A2[u] = A[u];
+      B2[u] = B[u];
+      C2[u] = C[u];
+      D2[u] = D[u];
+    }
+    if (q0 + U < n4) load(q0 + U);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      step(A2[u].x, B2[u].x, C2[u].x, D2[u].x);
+      step(A2[u].y, B2[u].y, C2[u].y, D2[u].y);
+      step(A2[u].z, B2[u].z, C2[u].z, D2[u].z);
+      step(A2[u].w, B2[u].w, C2[u].w, D2[u].w);
+    }
+  }
+}
+
+// One WARP per (prompt, common key m > 0); lanes = (step s, base b) pairs.
+// Each pair's sums are sequential fp64 chains over E (the reference's order),
+// streamed straight from global memory with prefetched float4 loads.
+// Phase A needs only s <= b (num[s][b] = sum d_s*d_b is the same sequence of
+// products as num[b][s], so it is bitwise symmetric); phase B needs s != b.
+constexpr int INTER_W = 4;  // items (warps) per block
+__global__ void __launch_bounds__(INTER_W * 32) k_inter(const float* __restrict__ lat,
+                                                        const InterItem* __restrict__ items, int n_items, int S,
+                                                        const int* __restrict__ perm, int F, int64_t E,
+                                                        const double* __restrict__ nrm, InterRes* __restrict__ out) {
+  __shared__ double s_num[INTER_W][MAXS][MAXS];
+  __shared__ float s_alpha[INTER_W][MAXS][MAXS];
+  __shared__ int s_nz[INTER_W][MAXS], s_exact[INTER_W][MAXS];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int idx = blockIdx.x * INTER_W + w;
+  if (idx >= n_items) return;
+  const InterItem it = items[idx];
   const int m = it.m;
   const float* base = lat + (int64_t)it.entry * S * F * E;
-  const int tid = threadIdx.x;
-  const int s = tid / MAXS, b = tid % MAXS;  // (s, b) pair of this thread
-  const bool pa = s < S && b < S;
-  double acc = 0.0;
-  bool nz = false, exact = true;
-  // ---- phase A: num[s][b] = sum d_s * d_b (den = num[b][b]) ----
-  for (int64_t c0 = 0; c0 < E; c0 += INTER_CH) {
-    const int cn = (int)min((int64_t)INTER_CH, E - c0);
-    __syncthreads();
-    for (int idx = tid; idx < S * INTER_CH; idx += INTER_T) {
-      const int ss = idx / INTER_CH, i = idx - ss * INTER_CH;
-      if (i < cn) {
-        const float* st = base + (int64_t)perm[ss] * F * E;
-        s_key[ss][i] = st[(int64_t)m * E + c0 + i];
-        s_first[ss][i] = st[c0 + i];
-      }
+  const bool vec = (E & 15) == 0 && (reinterpret_cast<uintptr_t>(base) & 15) == 0;
+  auto key = [&](int st) { return base + ((int64_t)perm[st] * F + m) * E; };
+  auto first = [&](int st) { return base + (int64_t)perm[st] * F * E; };
+  // ---- phase A: num[s][b] = sum d_s * d_b, codec.cpp:181-191 (diagonal: nz / exact flags, codec.cpp:41-46) ----
+  const int nA = S * (S + 1) / 2;
+  for (int pr = lane; pr < nA; pr += 32) {
+    int s = 0, r = pr;
+    while (r >= S - s) {
+      r -= S - s;
+      ++s;
     }
-    __syncthreads();
-    if (pa) {
-      for (int i = 0; i < cn; ++i) {
-        const float ds = s_key[s][i] - s_first[s][i];
-        const float db = s_key[b][i] - s_first[b][i];
-        acc = fma((double)ds, (double)db, acc);
-        if (s == b) {
-          nz |= ds != 0.0f;
-          exact &= (s_first[s][i] + ds) == s_key[s][i];
-        }
-      }
+    const int b = s + r;
+    const bool diag = s == b;
+    double acc = 0.0;
+    bool nz = false, exact = true;
+    auto stepA = [&](float k_s, float f_s, float k_b, float f_b) {
+      const float ds = k_s - f_s;
+      const float db = k_b - f_b;
+      acc = fma((double)ds, (double)db, acc);
+      nz |= ds != 0.0f;
+      exact &= (f_s + ds) == k_s;
+    };
+    const float *ks = key(s), *fs = first(s), *kb = key(b), *fb = first(b);
+    if (vec) stream4(ks, fs, kb, fb, E, stepA);
+    else
+      for (int64_t i = 0; i < E; ++i) stepA(ks[i], fs[i], kb[i], fb[i]);
+    s_num[w][s][b] = acc;
+    s_num[w][b][s] = acc;
+    if (diag) {
+      s_nz[w][s] = nz;
+      s_exact[w][s] = exact;
     }
   }
-  if (pa) s_num[s][b] = acc;
-  if (pa && s == b) {
-    s_nz[s] = nz;
-    s_exact[s] = exact;
-  }
-  __syncthreads();
-  if (pa) {
+  __syncwarp();
+  for (int pr = lane; pr < S * S; pr += 32) {
+    const int s = pr / S, b = pr % S;
     float a = 0.0f;
-    if (s_nz[b]) a = (float)(s_num[s][b] / s_num[b][b]);
-    s_alpha[s][b] = a;
+    if (s_nz[w][b]) a = (float)(s_num[w][s][b] / s_num[w][b][b]);
+    s_alpha[w][s][b] = a;
   }
-  __syncthreads();
-  // ---- phase B: trial reconstruction of key m of step s under base b ----
-  const bool pb = pa && s != b && s_nz[b] && isfinite(s_alpha[s][b]);
-  const double alpha = pa ? (double)s_alpha[s][b] : 0.0;
-  double dot = 0.0, na = 0.0;
-  bool nonfin = false;
-  for (int64_t c0 = 0; c0 < E; c0 += INTER_CH) {
-    const int cn = (int)min((int64_t)INTER_CH, E - c0);
-    __syncthreads();
-    for (int idx = tid; idx < S * INTER_CH; idx += INTER_T) {
-      const int ss = idx / INTER_CH, i = idx - ss * INTER_CH;
-      if (i < cn) {
-        const float* st = base + (int64_t)perm[ss] * F * E;
-        s_key[ss][i] = st[(int64_t)m * E + c0 + i];
-        s_first[ss][i] = st[c0 + i];
-      }
-    }
-    __syncthreads();
+  __syncwarp();
+  // ---- phase B: trial reconstruction of key m of step s under base b (codec.cpp:243-252) ----
+  InterRes* o = out + idx;
+  for (int pr = lane; pr < S * S; pr += 32) {
+    const int s = pr / S, b = pr % S;
+    const bool pb = s != b && s_nz[w][b] && isfinite(s_alpha[w][s][b]);
+    const double alpha = (double)s_alpha[w][s][b];
+    double dot = 0.0, na = 0.0;
+    bool nonfin = false;
     if (pb) {
-      for (int i = 0; i < cn; ++i) {
-        const float db = s_key[b][i] - s_first[b][i];
-        const float r = (float)fma(alpha, (double)db, (double)s_first[s][i]);
+      auto stepB = [&](float k_s, float f_s, float k_b, float f_b) {
+        const float db = k_b - f_b;
+        const float r = (float)fma(alpha, (double)db, (double)f_s);
         nonfin |= !isfinite(r);
-        dot = fma((double)r, (double)s_key[s][i], dot);
+        dot = fma((double)r, (double)k_s, dot);
         na = fma((double)r, (double)r, na);
-      }
+      };
+      const float *ks = key(s), *fs = first(s), *kb = key(b), *fb = first(b);
+      if (vec) stream4(ks, fs, kb, fb, E, stepB);
+      else
+        for (int64_t i = 0; i < E; ++i) stepB(ks[i], fs[i], kb[i], fb[i]);
     }
-  }
-  InterRes* o = out + blockIdx.x;
-  if (pa) {
-    o->alpha[s][b] = s_alpha[s][b];
+    o->alpha[s][b] = s_alpha[w][s][b];
     o->nonfinite[s][b] = nonfin;
     double sim = 0.0;
     if (pb) {
-      const double nb = G[((int64_t)it.entry * S + perm[s]) * F * F + (int64_t)m * F + m];
+      const double nb = nrm[((int64_t)it.entry * S + perm[s]) * F + m];
       if (na == 0.0 && nb == 0.0) sim = 1.0;
       else if (na == 0.0 || nb == 0.0) sim = 0.0;
       else sim = dot / (sqrt(na) * sqrt(nb));
     }
     o->sim[s][b] = sim;
     if (s == b) {
-      o->nz[s] = s_nz[s];
-      o->exact[s] = s_exact[s];
+      o->nz[s] = s_nz[w][s];
+      o->exact[s] = s_exact[w][s];
     }
   }
 }
@@ -302,10 +468,38 @@ struct ByteJob {
   int64_t n;
 };
 
-__global__ void k_pack_frames(const FrameJob* __restrict__ jobs, int64_t E) {
-  const FrameJob j = jobs[blockIdx.y];
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < E; i += (int64_t)gridDim.x * blockDim.x)
-    j.dst[i] = j.sub ? j.src[i] - j.sub[i] : j.src[i];
+// One block per job (an E-float frame copy or diff); float4 streaming with
+// several loads in flight (all frame offsets are multiples of E floats).
+__global__ void __launch_bounds__(DEC_T) k_pack_frames(const FrameJob* __restrict__ jobs, int64_t E) {
+  const FrameJob j = jobs[blockIdx.x];
+  if ((E & 3) == 0 && ((reinterpret_cast<uintptr_t>(j.dst) | reinterpret_cast<uintptr_t>(j.src) |
+                        reinterpret_cast<uintptr_t>(j.sub)) & 15) == 0) {
+    const int64_t n4 = E >> 2;
+    const float4* s4 = reinterpret_cast<const float4*>(j.src);
+    const float4* b4 = reinterpret_cast<const float4*>(j.sub);
+    float4* d4 = reinterpret_cast<float4*>(j.dst);
+    for (int64_t i0 = threadIdx.x; i0 < n4; i0 += (int64_t)DEC_T * DEC_U) {
+      float4 v[DEC_U], w[DEC_U];
+#pragma unroll
+      for (int u = 0; u < DEC_U; ++u) {
+        const int64_t i = i0 + (int64_t)u * DEC_T;
+        if (i < n4) {
+          v[u] = __ldg(s4 + i);
+          if (j.sub) w[u] = __ldg(b4 + i);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < DEC_U; ++u) {
+        const int64_t i = i0 + (int64_t)u * DEC_T;
+        if (i < n4) {
+          if (j.sub) v[u] = make_float4(v[u].x - w[u].x, v[u].y - w[u].y, v[u].z - w[u].z, v[u].w - w[u].w);
+          d4[i] = v[u];
+        }
+      }
+    }
+  } else {
+    for (int64_t i = threadIdx.x; i < E; i += DEC_T) j.dst[i] = j.sub ? j.src[i] - j.sub[i] : j.src[i];
+  }
 }
 
 __global__ void k_pack_bytes(const ByteJob* __restrict__ jobs) {
@@ -344,7 +538,6 @@ __device__ __forceinline__ float4 recon4(const float* base, const Recipe& r, int
 // each thread keeps DEC_U float4 loads (x2 for two-source kinds) in flight.
 // Loads use the read-only path; stores are streaming (.cs): the output is
 // written once and not re-read by this kernel.
-constexpr int DEC_T = 256, DEC_U = 4;
 template <int KIND>
 __device__ __forceinline__ void dec_frame(const float* __restrict__ a, const float* __restrict__ b, float alpha,
                                           float* __restrict__ out, int64_t n4) {
@@ -487,6 +680,19 @@ __global__ void k_solve_alpha(const float* __restrict__ ds, const float* __restr
 // ---------------------------------------------------------------------------
 namespace {
 
+// FC_TRACE=1: host-side phase times of the compress orchestration (stderr)
+struct Trace {
+  bool on;
+  std::chrono::steady_clock::time_point t0;
+  Trace() : on(getenv("FC_TRACE") && atoi(getenv("FC_TRACE")) == 1), t0(std::chrono::steady_clock::now()) {}
+  void mark(const char* what) {
+    if (!on) return;
+    const auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "[compress] %-28s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(t - t0).count());
+    t0 = t;
+  }
+};
+
 struct Geo {
   int F, H, W, C;
   int64_t E, mb;
@@ -510,14 +716,82 @@ void gram(lc_ctx* ctx, const float* lat, int n_items, const Geo& g, double* G) {
   count_launch(ctx);
 }
 
+// Frame Gram matrices + exact squared norms of n_items latents. Tensor-core
+// path (gram_sm100.cu) when the shape allows; returns the certified
+// similarity error bound delta for k_select_cert (0 = exact Gram).
+constexpr double GRAM_DELTA = 1e-4;
+// Also raises *bad if any element is non-finite (fused into the tensor-core
+// pass; a separate check pass otherwise).
+double grams_and_norms(lc_ctx* ctx, const float* lat, int n_items, const Geo& g, double* G, double* nrm, int* bad) {
+  if (gram_tc_supported(g.F, g.E, lat)) {
+    gram_tc(ctx, lat, n_items, g.F, g.E, G, nrm, bad);
+    return GRAM_DELTA;
+  }
+  const int64_t total = (int64_t)n_items * g.F * g.E;
+  k_nonfinite<<<grid_for(total, 256, 8192), 256, 0, ctx->stream>>>(lat, total, bad);
+  FC_LAUNCH_CHECK();
+  count_launch(ctx);
+  gram(ctx, lat, n_items, g, G);
+  k_diag<<<grid_for((int64_t)n_items * g.F, 256), 256, 0, ctx->stream>>>(G, n_items, g.F, nrm);
+  FC_LAUNCH_CHECK();
+  count_launch(ctx);
+  return 0.0;
+}
+
+void select_cert(lc_ctx* ctx, const double* G, const double* nrm, const float* lat, int n_items, const Geo& g, double thr,
+                 double delta, int32_t* maps, int* bad) {
+  DevBuf ne(sizeof(unsigned), ctx->stream);
+  FC_CUDA(cudaMemsetAsync(ne.p, 0, sizeof(unsigned), ctx->stream));
+  {
+    KTimer kt(ctx, "select");
+    k_select_cert<<<(unsigned)((n_items + 3) / 4), 128, 0, ctx->stream>>>(G, nrm, lat, n_items, g.F, g.E, thr, delta,
+                                                                          maps, bad, ne.as<unsigned>());
+  }
+  FC_LAUNCH_CHECK();
+  count_launch(ctx);
+  if (getenv("FC_TRACE") && atoi(getenv("FC_TRACE")) == 1) {
+    unsigned h = 0;
+    FC_CUDA(cudaMemcpyAsync(&h, ne.p, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream));
+    sync(ctx);
+    fprintf(stderr, "[compress] select: %u exact pair recomputes over %d items (delta %g)\n", h, n_items, delta);
+  }
+}
+
+// Runs body(e) for e in [0, n) on up to 16 host threads (independent
+// per-entry work); the first exception is rethrown on the caller's thread.
+template <class Body>
+void parallel_for(int64_t n, Body body) {
+  const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+  const int nt = (int)std::min<int64_t>(std::min(hw, 16), std::max<int64_t>(1, n / 8));
+  if (nt <= 1) {
+    for (int64_t e = 0; e < n; ++e) body(e);
+    return;
+  }
+  std::exception_ptr err = nullptr;
+  std::mutex mu;
+  std::vector<std::thread> th;
+  for (int t = 0; t < nt; ++t)
+    th.emplace_back([&, t] {
+      try {
+        for (int64_t e = t; e < n; e += nt) body(e);
+      } catch (...) {
+        std::lock_guard<std::mutex> lk(mu);
+        if (!err) err = std::current_exception();
+      }
+    });
+  for (auto& x : th) x.join();
+  if (err) std::rethrow_exception(err);
+}
+
 // Builds entries for n prompts given maps (host, [n][S][F] in input step
 // order) and the device Gram diagonals. Writes out[i], sizes[i].
 void assemble(lc_ctx* ctx, const float* lat, const uint8_t* om, const uint8_t* bm, const std::vector<int32_t>& steps_in,
-              const Geo& g, const std::vector<int32_t>& maps_h, const double* G_dev, const uint64_t* prompts, int64_t n,
+              const Geo& g, const std::vector<int32_t>& maps_h, const double* nrm_dev, const uint64_t* prompts, int64_t n,
               lc_entry** out, uint64_t* sizes) {
   const int S = (int)steps_in.size();
   const int F = g.F;
   const int64_t E = g.E;
+  Trace tr;
   // sorted step order (codec.cpp:197-199)
   std::vector<int> perm(S);
   std::iota(perm.begin(), perm.end(), 0);
@@ -544,14 +818,9 @@ void assemble(lc_ctx* ctx, const float* lat, const uint8_t* om, const uint8_t* b
   item_begin[n] = (int)items.size();
   // Gram diagonals (norms^2 of every frame) to the host
   std::vector<double> diag((size_t)n * S * F);
-  {
-    DevBuf d((size_t)n * S * F * sizeof(double), ctx->stream);
-    k_diag<<<grid_for((int64_t)n * S * F, 256), 256, 0, ctx->stream>>>(G_dev, (int64_t)n * S, F, d.as<double>());
-    FC_LAUNCH_CHECK();
-    count_launch(ctx);
-    FC_CUDA(cudaMemcpyAsync(diag.data(), d.p, diag.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-    sync(ctx);
-  }
+  FC_CUDA(cudaMemcpyAsync(diag.data(), nrm_dev, diag.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  sync(ctx);
+  tr.mark("common keys + diag D2H");
   // K7 over all (entry, common key) items
   std::vector<InterRes> res(items.size());
   if (!items.empty()) {
@@ -560,13 +829,15 @@ void assemble(lc_ctx* ctx, const float* lat, const uint8_t* om, const uint8_t* b
     FC_CUDA(cudaMemcpyAsync(di.p, items.data(), di.bytes, cudaMemcpyHostToDevice, ctx->stream));
     FC_CUDA(cudaMemcpyAsync(dp.p, perm.data(), dp.bytes, cudaMemcpyHostToDevice, ctx->stream));
     KTimer kt(ctx, "inter");
-    k_inter<<<(unsigned)items.size(), INTER_T, 0, ctx->stream>>>(lat, di.as<InterItem>(), S, dp.as<int>(), F, E, G_dev,
+    k_inter<<<(unsigned)((items.size() + INTER_W - 1) / INTER_W), INTER_W * 32, 0, ctx->stream>>>(
+        lat, di.as<InterItem>(), (int)items.size(), S, dp.as<int>(), F, E, nrm_dev,
                                                                   dr.as<InterRes>());
     FC_LAUNCH_CHECK();
     count_launch(ctx);
     FC_CUDA(cudaMemcpyAsync(res.data(), dr.p, dr.bytes, cudaMemcpyDeviceToHost, ctx->stream));
     sync(ctx);
   }
+  tr.mark("k_inter + D2H");
   auto identical_sim = [](double ss) { return ss == 0.0 ? 1.0 : ss / (std::sqrt(ss) * std::sqrt(ss)); };
   // ---- per entry: base selection + assembly metadata ----
   std::vector<std::shared_ptr<EntryData>> ents(n);
@@ -574,40 +845,48 @@ void assemble(lc_ctx* ctx, const float* lat, const uint8_t* om, const uint8_t* b
   std::vector<ByteJob> bjobs;
   std::vector<Recipe> all_recipes;
   std::vector<std::pair<size_t, size_t>> recipe_span(n);
-  for (int64_t e = 0; e < n; ++e) {
+  std::vector<int> best_base(n, 0);
+  parallel_for(n, [&](int64_t e) {
     const auto& cm = common[e];
     const int i0 = item_begin[e];
-    auto in_common = [&](int m) { return std::binary_search(cm.begin(), cm.end(), m); };
-    auto item_of = [&](int m) -> const InterRes* {
-      // items for this entry are in ascending m (skipping 0)
-      int lo = i0, hi = item_begin[e + 1];
-      while (lo < hi) {
-        int mid = (lo + hi) / 2;
-        if (items[mid].m < m) lo = mid + 1; else hi = mid;
-      }
-      return (lo < item_begin[e + 1] && items[lo].m == m) ? &res[lo] : nullptr;
-    };
+    // direct (m -> K7 item) index; identical-frame similarity per (step, key)
+    // computed once instead of per (base, frame) (this loop was ~13 ms of host
+    // time for 256 entries)
+    std::vector<int> idx(F, -1);
+    for (int c = i0; c < item_begin[e + 1]; ++c) idx[items[c].m] = c;
+    std::vector<char> is_common(F, 0);
+    for (int m : cm) is_common[m] = 1;
+    auto in_common = [&](int m) { return is_common[m] != 0; };
+    auto item_of = [&](int m) -> const InterRes* { return idx[m] >= 0 ? &res[idx[m]] : nullptr; };
     auto mapv = [&](int si, int j) { return maps_h[((size_t)e * S + perm[si]) * F + j]; };
     auto dg = [&](int si, int m) { return diag[((size_t)e * S + perm[si]) * F + m]; };
     // choose base (codec.cpp:240-259); a single step is its own base
     int best_b = 0;
     if (S > 1) {
+      // a non-finite trial reconstruction makes decompress_step throw
+      for (int c = i0; c < item_begin[e + 1]; ++c)
+        for (int b = 0; b < S; ++b)
+          for (int si = 0; si < S; ++si)
+            if (si != b && res[c].nz[b] && std::isfinite(res[c].alpha[si][b]) && res[c].nonfinite[si][b])
+              raise(LC_ERR_INVALID_ARGUMENT, "Frame: non-finite element");
+      std::vector<double> isim((size_t)S * F, 0.0);
+      for (int si = 0; si < S; ++si)
+        for (int j = 0; j < F; ++j) {
+          const int m = mapv(si, j);
+          if (m == j) isim[(size_t)si * F + m] = identical_sim(dg(si, m));
+        }
       double best_score = -2.0;
       for (int b = 0; b < S; ++b) {
-        // a non-finite trial reconstruction makes decompress_step throw
-        for (int c = i0; c < item_begin[e + 1]; ++c)
-          for (int s = 0; s < S; ++s)
-            if (s != b && res[c].nz[b] && std::isfinite(res[c].alpha[s][b]) && res[c].nonfinite[s][b])
-              raise(LC_ERR_INVALID_ARGUMENT, "Frame: non-finite element");
+        // mean per-frame similarity, summed in the reference's (step, frame) order
         double sum = 0.0;
         uint64_t count = 0;
         for (int si = 0; si < S; ++si) {
           for (int j = 0; j < F; ++j) {
             const int m = mapv(si, j);
+            const InterRes* r = m > 0 ? item_of(m) : nullptr;
             double sim;
-            const InterRes* r = (m > 0 && in_common(m)) ? item_of(m) : nullptr;
             if (r && r->nz[b] && si != b && std::isfinite(r->alpha[si][b])) sim = r->sim[si][b];
-            else sim = identical_sim(dg(si, m));
+            else sim = isim[(size_t)si * F + m];
             sum += sim;
             ++count;
           }
@@ -677,21 +956,53 @@ void assemble(lc_ctx* ctx, const float* lat, const uint8_t* om, const uint8_t* b
     d->recipe_off = bytes;
     bytes += (int64_t)S * F * sizeof(Recipe);
     d->dev_bytes = (size_t)bytes;
-    FC_CUDA(cudaMallocAsync((void**)&d->dev, d->dev_bytes, ctx->stream));
+    best_base[e] = best_b;
+    ents[e] = d;
+  });
+  tr.mark("host: base + metadata");
+  // one device allocation for the whole batch (per-entry cudaMallocAsync was
+  // ~13 ms of host time for 256 entries); entries share it by reference
+  size_t total = 0;
+  std::vector<size_t> at(n);
+  for (int64_t e = 0; e < n; ++e) {
+    at[e] = total;
+    total += (ents[e]->dev_bytes + 255) & ~size_t(255);
+  }
+  auto arena = std::make_shared<DevArena>();
+  arena->ctx = ctx;
+  FC_CUDA(cudaMallocAsync((void**)&arena->p, std::max<size_t>(total, 256), ctx->stream));
+  tr.mark("host: arena alloc");
+  // per-entry job / recipe spans (fixed offsets, so entries fill them in parallel)
+  std::vector<size_t> fj_off(n + 1, 0);
+  for (int64_t e = 0; e < n; ++e) {
+    size_t c = S + ents[e]->diff_idx.size();
+    for (int si = 0; si < S; ++si) c += ents[e]->extra_idx[si].size();
+    fj_off[e + 1] = fj_off[e] + c;
+  }
+  fjobs.resize(fj_off[n]);
+  bjobs.resize(2 * n);
+  all_recipes.resize((size_t)n * S * F);
+  parallel_for(n, [&](int64_t e) {
+    const std::shared_ptr<EntryData>& d = ents[e];
+    d->arena = arena;
+    d->dev = arena->p + at[e];
+    const int best_b = best_base[e];
+    const int nd = (int)d->diff_idx.size();
     float* fb = reinterpret_cast<float*>(d->dev);
     const float* latE = lat + (int64_t)e * S * F * E;
     auto frame_ptr = [&](int si, int m) { return latE + ((int64_t)perm[si] * F + m) * E; };
-    for (int si = 0; si < S; ++si) fjobs.push_back(FrameJob{fb + d->first_off[si], frame_ptr(si, 0), nullptr});
+    FrameJob* fj = fjobs.data() + fj_off[e];
+    for (int si = 0; si < S; ++si) *fj++ = FrameJob{fb + d->first_off[si], frame_ptr(si, 0), nullptr};
     const int bsi = best_b;
-    for (int t = 0; t < nd; ++t)
-      fjobs.push_back(FrameJob{fb + d->diff_off[t], frame_ptr(bsi, d->diff_idx[t]), frame_ptr(bsi, 0)});
+    for (int t = 0; t < nd; ++t) *fj++ = FrameJob{fb + d->diff_off[t], frame_ptr(bsi, d->diff_idx[t]), frame_ptr(bsi, 0)};
     for (int si = 0; si < S; ++si)
       for (size_t x = 0; x < d->extra_idx[si].size(); ++x)
-        fjobs.push_back(FrameJob{fb + d->extra_off[si][x], frame_ptr(si, d->extra_idx[si][x]), nullptr});
-    bjobs.push_back(ByteJob{d->dev + d->mask_off, om + (int64_t)e * F * g.mb, (int64_t)F * g.mb});
-    bjobs.push_back(ByteJob{d->dev + d->mask_off + F * g.mb, bm + (int64_t)e * F * g.mb, (int64_t)F * g.mb});
+        *fj++ = FrameJob{fb + d->extra_off[si][x], frame_ptr(si, d->extra_idx[si][x]), nullptr};
+    bjobs[2 * e] = ByteJob{d->dev + d->mask_off, om + (int64_t)e * F * g.mb, (int64_t)F * g.mb};
+    bjobs[2 * e + 1] = ByteJob{d->dev + d->mask_off + F * g.mb, bm + (int64_t)e * F * g.mb, (int64_t)F * g.mb};
     // recipes: decompress_step (codec.cpp:271-299) resolved per frame
-    recipe_span[e].first = all_recipes.size();
+    recipe_span[e].first = (size_t)e * S * F;
+    Recipe* rout = all_recipes.data() + recipe_span[e].first;
     for (int si = 0; si < S; ++si) {
       std::vector<Recipe> key_rec(F);
       for (int m = 0; m < F; ++m) {
@@ -716,11 +1027,11 @@ void assemble(lc_ctx* ctx, const float* lat, const uint8_t* om, const uint8_t* b
         }
         key_rec[m] = r;
       }
-      for (int j = 0; j < F; ++j) all_recipes.push_back(key_rec[d->maps[si][j]]);
+      for (int j = 0; j < F; ++j) *rout++ = key_rec[d->maps[si][j]];
     }
-    recipe_span[e].second = all_recipes.size();
-    ents[e] = d;
-  }
+    recipe_span[e].second = (size_t)(e + 1) * S * F;
+  });
+  tr.mark("host: jobs + recipes");
   // ---- K8: pack frames, masks, recipes ----
   DevBuf rstage(all_recipes.size() * sizeof(Recipe), ctx->stream);
   if (!all_recipes.empty())
@@ -732,9 +1043,8 @@ void assemble(lc_ctx* ctx, const float* lat, const uint8_t* om, const uint8_t* b
   FC_CUDA(cudaMemcpyAsync(dfj.p, fjobs.data(), dfj.bytes, cudaMemcpyHostToDevice, ctx->stream));
   FC_CUDA(cudaMemcpyAsync(dbj.p, bjobs.data(), dbj.bytes, cudaMemcpyHostToDevice, ctx->stream));
   KTimer ktp(ctx, "pack");
-  for (size_t j0 = 0; j0 < fjobs.size(); j0 += 65535) {
-    const unsigned cnt = (unsigned)std::min<size_t>(65535, fjobs.size() - j0);
-    k_pack_frames<<<dim3(grid_for(E, 256, 64), cnt), 256, 0, ctx->stream>>>(dfj.as<FrameJob>() + j0, E);
+  if (!fjobs.empty()) {
+    k_pack_frames<<<(unsigned)fjobs.size(), DEC_T, 0, ctx->stream>>>(dfj.as<FrameJob>(), E);
     FC_LAUNCH_CHECK();
   }
   for (size_t j0 = 0; j0 < bjobs.size(); j0 += 65535) {
@@ -744,7 +1054,9 @@ void assemble(lc_ctx* ctx, const float* lat, const uint8_t* om, const uint8_t* b
   }
   ktp.stop();
   count_launch(ctx, 2);
+  tr.mark("pack launches");
   sync(ctx);
+  tr.mark("pack sync");
   for (int64_t e = 0; e < n; ++e) {
     std::vector<int> sel(S);
     std::iota(sel.begin(), sel.end(), 0);
@@ -861,15 +1173,11 @@ lc_status lc_select_keyframes(lc_ctx* ctx, const float* latents, int64_t n, int 
   OutArg<int32_t> om(ctx, map, (size_t)n * F);
   DevBuf bad(sizeof(int), ctx->stream);
   FC_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), ctx->stream));
-  k_nonfinite<<<grid_for(n * F * E, 256, 4096), 256, 0, ctx->stream>>>(lat.dev, n * F * E, bad.as<int>());
-  FC_LAUNCH_CHECK();
-  DevBuf G((size_t)n * F * F * sizeof(double), ctx->stream);
+  DevBuf G((size_t)n * F * F * sizeof(double), ctx->stream), NR((size_t)n * F * sizeof(double), ctx->stream);
   Geo g{F, H, W, C, E, ((int64_t)H * W + 7) / 8};
-  gram(ctx, lat.dev, (int)n, g, G.as<double>());
+  const double delta = grams_and_norms(ctx, lat.dev, (int)n, g, G.as<double>(), NR.as<double>(), bad.as<int>());
   if (check_flag(ctx, bad)) raise(LC_ERR_INVALID_ARGUMENT, "Frame: non-finite element");
-  k_select<<<grid_for(n, 64), 64, 0, ctx->stream>>>(G.as<double>(), (int)n, F, thr, om.dev, bad.as<int>());
-  FC_LAUNCH_CHECK();
-  count_launch(ctx, 2);
+  select_cert(ctx, G.as<double>(), NR.as<double>(), lat.dev, (int)n, g, thr, delta, om.dev, bad.as<int>());
   om.finish(ctx);
   if (check_flag(ctx, bad)) raise(LC_ERR_INVALID_ARGUMENT, "cosine_similarity: zero-norm operand");
   LC_API_END
@@ -902,28 +1210,28 @@ lc_status lc_compress_batch(lc_ctx* ctx, const float* latents, const int32_t* st
   DeviceGuard dg(ctx->device);
   const int64_t E = (int64_t)H * W * C;
   Geo g{F, H, W, C, E, ((int64_t)H * W + 7) / 8};
+  Trace tr;
   InArg<float> lat(ctx, latents, (size_t)n * S * F * E);
   InArg<uint8_t> om(ctx, obj_masks, (size_t)n * F * g.mb), bm(ctx, bg_masks, (size_t)n * F * g.mb);
   DevBuf bad(sizeof(int), ctx->stream);
   FC_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), ctx->stream));
-  k_nonfinite<<<grid_for(n * S * F * E, 256, 8192), 256, 0, ctx->stream>>>(lat.dev, n * S * F * E, bad.as<int>());
-  FC_LAUNCH_CHECK();
-  count_launch(ctx);
   // K5 + K6: key frames of every (prompt, step)
-  DevBuf G((size_t)n * S * F * F * sizeof(double), ctx->stream);
-  gram(ctx, lat.dev, (int)(n * S), g, G.as<double>());
+  DevBuf G((size_t)n * S * F * F * sizeof(double), ctx->stream), NR((size_t)n * S * F * sizeof(double), ctx->stream);
+  const double delta =
+      grams_and_norms(ctx, lat.dev, (int)(n * S), g, G.as<double>(), NR.as<double>(), bad.as<int>());
   if (check_flag(ctx, bad)) raise(LC_ERR_INVALID_ARGUMENT, "Frame: non-finite element");
+  tr.mark("nonfinite + gram (sync)");
   DevBuf maps((size_t)n * S * F * sizeof(int32_t), ctx->stream);
-  k_select<<<grid_for(n * S, 64), 64, 0, ctx->stream>>>(G.as<double>(), (int)(n * S), F, thr, maps.as<int32_t>(),
-                                                        bad.as<int>());
-  FC_LAUNCH_CHECK();
-  count_launch(ctx);
+  select_cert(ctx, G.as<double>(), NR.as<double>(), lat.dev, (int)(n * S), g, thr, delta, maps.as<int32_t>(),
+              bad.as<int>());
   std::vector<int32_t> maps_h((size_t)n * S * F);
   FC_CUDA(cudaMemcpyAsync(maps_h.data(), maps.p, maps.bytes, cudaMemcpyDeviceToHost, ctx->stream));
   if (check_flag(ctx, bad)) raise(LC_ERR_INVALID_ARGUMENT, "cosine_similarity: zero-norm operand");
   check_distinct_steps(S, steps);
+  tr.mark("select + maps D2H");
   std::vector<int32_t> st(steps, steps + S);
-  assemble(ctx, lat.dev, om.dev, bm.dev, st, g, maps_h, G.as<double>(), prompts, n, out, sizes);
+  assemble(ctx, lat.dev, om.dev, bm.dev, st, g, maps_h, NR.as<double>(), prompts, n, out, sizes);
+  tr.mark("assemble");
   LC_API_END
 }
 
@@ -948,10 +1256,12 @@ lc_status lc_inter_compress(lc_ctx* ctx, const float* latents, const int32_t* ma
     }
   InArg<float> lat(ctx, latents, (size_t)S * F * E);
   InArg<uint8_t> om(ctx, obj_masks, (size_t)F * g.mb), bm(ctx, bg_masks, (size_t)F * g.mb);
-  DevBuf G((size_t)S * F * F * sizeof(double), ctx->stream);
-  gram(ctx, lat.dev, S, g, G.as<double>());
+  DevBuf G((size_t)S * F * F * sizeof(double), ctx->stream), NR((size_t)S * F * sizeof(double), ctx->stream);
+  DevBuf bad(sizeof(int), ctx->stream);
+  FC_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), ctx->stream));
+  grams_and_norms(ctx, lat.dev, S, g, G.as<double>(), NR.as<double>(), bad.as<int>());
   std::vector<int32_t> st(steps, steps + S);
-  assemble(ctx, lat.dev, om.dev, bm.dev, st, g, maps_h, G.as<double>(), &prompt, 1, out, nullptr);
+  assemble(ctx, lat.dev, om.dev, bm.dev, st, g, maps_h, NR.as<double>(), &prompt, 1, out, nullptr);
   LC_API_END
 }
 

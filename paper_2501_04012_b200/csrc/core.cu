@@ -208,6 +208,14 @@ lc_status lc_ctx_create(int device, lc_ctx** out) {
   c->sm_count = prop.multiProcessorCount;
   FC_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   c->own_stream = true;
+  // stream-ordered scratch and entry storage come from the device's default
+  // pool; keep freed blocks cached instead of unmapping them at every sync
+  // (re-mapping ~1 GB of entries per compress batch cost ~10 ms of host time)
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
   *out = c;
   LC_API_END
 }

@@ -29,6 +29,13 @@ struct Recipe {
   int64_t b;
 };
 
+// Device memory shared by the entries of one compress batch (freed with the last).
+struct DevArena {
+  lc_ctx* ctx = nullptr;
+  uint8_t* p = nullptr;
+  ~DevArena();
+};
+
 struct EntryData {
   lc_ctx* ctx = nullptr;
   uint64_t prompt = 0;
@@ -46,6 +53,7 @@ struct EntryData {
   int64_t recipe_off = 0;  // byte offset of Recipe[n_steps][F]
   uint8_t* dev = nullptr;
   size_t dev_bytes = 0;
+  std::shared_ptr<DevArena> arena;  // set when dev lives in a batch allocation
   ~EntryData();
 
   const float* fbase() const { return reinterpret_cast<const float*>(dev); }

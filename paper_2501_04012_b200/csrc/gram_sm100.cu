@@ -1,0 +1,320 @@
+// gram_sm100.cu — K5 on the tensor cores: per (prompt, step) item the F x F
+// frame Gram matrix that select_keyframes needs (codec.cpp:146-163 via
+// frame_similarity, core.cpp:101-119), plus the EXACT squared norms.
+//
+// The reference's similarities are sequential fp64 sums over E = H*W*C
+// elements; reproducing them for all F^2/2 pairs costs F^2/2 * E fp64 FMAs
+// (14.8 ms for config[2] with the exact kernel). Here the Gram is computed
+// APPROXIMATELY on tcgen05 with a rigorous error bound, and select_keyframes
+// (k_select_cert, codec.cu) uses the exact sequential fp64 value for the few
+// pairs whose decision the bound cannot settle. Outputs:
+//   G~[item][F][F]  fp64, |G~(j,k) - dot(j,k)| <= GRAM_REL * sum_i |x_ji x_ki|
+//                   <= GRAM_REL * ||x_j|| ||x_k||  (Cauchy-Schwarz)
+//   nrm[item][F]    fp64, sequential sum_i x_ji^2 in element order — bit-
+//                   identical to cosine_similarity's na/nb (core.cpp:104-110)
+//
+// Error model (bf16x3): x = hi + lo + r with hi = RN_bf16(x), lo =
+// RN_bf16(x - hi), |r| <= 2^-16 |x|; the MMAs form hi*hi' + hi*lo' + lo*hi'
+// (each product exact in fp32), dropping lo*lo' and the r terms:
+// <= 3.1 * 2^-16 |x x'|. Accumulation: fp32 in TMEM over chunks of 256
+// elements (<= 256 * 2^-23 relative to the chunk's sum |x x'|, truncating
+// adders assumed), chunk totals added in fp64. GRAM_REL = 1e-4 covers both
+// (7.8e-5).
+//
+// Tiles: two items (2 x F <= 128 frames) form the M = N = 128 operand; the
+// cross-item blocks of the 128x128 product are unused (tensor throughput is
+// not the limit: the kernel streams each latent once, HBM-bound).
+// Warp roles (320 threads): 0 TMA producer (fp32 boxes of 32 elements),
+// 1 MMA issuer (elected lane), 2-5 converters (thread = frame row: exact
+// norm + hi/lo split into SWIZZLE_128B bf16 tiles), 6-9 epilogue (TMEM ->
+// fp64 chunk accumulation, one row per thread).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+#include "sm100_ptx.cuh"
+
+namespace fc {
+namespace gram {
+
+using namespace sm100;
+
+constexpr int GT = 320;       // threads
+constexpr int KU = 64;        // elements per K unit (one bf16 SW128 row)
+constexpr int XBOX = 128 * 128;  // one fp32 box region: 128 rows x 32 fp32 (128 B)
+constexpr int XSTAGE = 2 * XBOX; // a K unit = two fp32 boxes
+constexpr int BTILE = 128 * 128; // one bf16 tile: 128 rows x 64 bf16
+constexpr int BSTAGE = 2 * BTILE;  // hi + lo
+constexpr int NX = 3, NB = 2;
+constexpr int CHUNK = 4;      // K units per fp32 TMEM accumulation chunk (256 elements)
+
+struct Params {
+  int n_items, F, n_tiles;
+  int64_t E;
+  int n_units;          // E / KU
+  double* G;            // [n_items][F][F]
+  double* nrm;          // [n_items][F]
+  int* bad;             // set to 1 if any element is non-finite (Frame ctor rule, core.cpp:11-25)
+};
+
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int x, int y, int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(bar)
+      : "memory");
+}
+
+// 16-byte chunk c of row r in a 128-B-row SWIZZLE_128B tile
+__device__ __forceinline__ uint32_t sw128(int r, int c) { return (uint32_t)(r * 128 + ((c ^ (r & 7)) << 4)); }
+
+__global__ void __launch_bounds__(GT, 1) k_gram_tc(const __grid_constant__ CUtensorMap tmX, Params p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* xst = base;                    // [NX][2][128 rows][128 B] fp32
+  uint8_t* bst = base + NX * XSTAGE;      // [NB][hi, lo][128 rows][128 B] bf16
+  uint64_t* bars = reinterpret_cast<uint64_t*>(bst + NB * BSTAGE);
+  uint64_t* xfull = bars;
+  uint64_t* xempty = xfull + NX;
+  uint64_t* bfull = xempty + NX;
+  uint64_t* bempty = bfull + NB;
+  uint64_t* afull = bempty + NB;
+  uint64_t* aempty = afull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int F = p.F;
+  const int nu = p.n_units;
+  const int nchunk = (nu + CHUNK - 1) / CHUNK;
+
+  for (int i = threadIdx.x; i < (NX * XSTAGE) / 16; i += GT) reinterpret_cast<uint4*>(xst)[i] = make_uint4(0, 0, 0, 0);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NX; ++s) {
+      mbar_init(smem_u32(&xfull[s]), 1);
+      mbar_init(smem_u32(&xempty[s]), 4);
+    }
+    for (int s = 0; s < NB; ++s) {
+      mbar_init(smem_u32(&bfull[s]), 4);
+      mbar_init(smem_u32(&bempty[s]), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(smem_u32(&afull[b]), 1);
+      mbar_init(smem_u32(&aempty[b]), 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // zero-fill visible to TMA / MMA
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
+      uint32_t u = 0;
+      for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+        const int ia = 2 * tile, ib = 2 * tile + 1;
+        const bool has_b = ib < p.n_items;
+        const uint32_t bytes = (has_b ? 4u : 2u) * (uint32_t)F * 128u;
+        for (int k = 0; k < nu; ++k, ++u) {
+          const int s = u % NX;
+          mbar_wait(smem_u32(&xempty[s]), ((u / NX) & 1) ^ 1);
+          mbar_expect_tx(smem_u32(&xfull[s]), bytes);
+          uint8_t* dst = xst + s * XSTAGE;
+          for (int h = 0; h < 2; ++h) {
+            tma_load_3d(smem_u32(dst + h * XBOX), &tmX, smem_u32(&xfull[s]), k * KU + h * 32, 0, ia);
+            if (has_b) tma_load_3d(smem_u32(dst + h * XBOX + 64 * 128), &tmX, smem_u32(&xfull[s]), k * KU + h * 32, 0, ib);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    const bool issuer = elect_one();
+    uint32_t u = 0, ch = 0;
+    for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+      for (int c = 0; c < nchunk; ++c, ++ch) {
+        const uint32_t ab = ch & 1;
+        mbar_wait(smem_u32(&aempty[ab]), ((ch >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + ab * 128;
+        const int k1 = min(nu, (c + 1) * CHUNK);
+        for (int k = c * CHUNK; k < k1; ++k, ++u) {
+          const int s = u % NB;
+          mbar_wait(smem_u32(&bfull[s]), (u / NB) & 1);
+          tc_fence_after();
+          if (issuer) {
+            const uint64_t dh = smem_desc_sw128(smem_u32(bst + s * BSTAGE));
+            const uint64_t dl = smem_desc_sw128(smem_u32(bst + s * BSTAGE + BTILE));
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {  // K = 16 per MMA; +32 B per step inside the swizzled row
+              const uint64_t o = 2 * t;
+              mma_ss(d, dh + o, dh + o, idesc, (k != c * CHUNK || t != 0) ? 1u : 0u);
+              mma_ss(d, dh + o, dl + o, idesc, 1u);
+              mma_ss(d, dl + o, dh + o, idesc, 1u);
+            }
+            tc_commit(smem_u32(&bempty[s]));
+          }
+          __syncwarp();
+        }
+        if (issuer) tc_commit(smem_u32(&afull[ab]));
+        __syncwarp();
+      }
+    }
+  } else if (warp < 6) {
+    // ---------------- converters: thread = frame row ----------------
+    const int r = threadIdx.x - 64;  // 0..127
+    uint32_t u = 0;
+    for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+      const int item = 2 * tile + (r >> 6);
+      const int row = r & 63;
+      const bool real = row < F && item < p.n_items;
+      double nrm = 0.0;
+      bool finite = true;
+      for (int k = 0; k < nu; ++k, ++u) {
+        const int sx = u % NX, sb = u % NB;
+        mbar_wait(smem_u32(&xfull[sx]), (u / NX) & 1);
+        mbar_wait(smem_u32(&bempty[sb]), ((u / NB) & 1) ^ 1);
+        const uint8_t* xs = xst + sx * XSTAGE;
+        uint8_t* hi = bst + sb * BSTAGE;
+        uint8_t* lo = hi + BTILE;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {  // bf16 chunk c = elements 8c..8c+7 = fp32 box c/4, fp32 chunks 2(c%4), 2(c%4)+1
+          const uint8_t* xb = xs + (c >> 2) * XBOX;
+          const float4 v0 = *reinterpret_cast<const float4*>(xb + sw128(r, 2 * (c & 3)));
+          const float4 v1 = *reinterpret_cast<const float4*>(xb + sw128(r, 2 * (c & 3) + 1));
+          const float x[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+          uint32_t h2[4], l2[4];
+#pragma unroll
+          for (int e = 0; e < 8; e += 2) {
+            finite &= isfinite(x[e]) & isfinite(x[e + 1]);
+            nrm = fma((double)x[e], (double)x[e], nrm);
+            nrm = fma((double)x[e + 1], (double)x[e + 1], nrm);
+            const __nv_bfloat162 h = __floats2bfloat162_rn(x[e], x[e + 1]);
+            const float2 hf = __bfloat1622float2(h);
+            const __nv_bfloat162 l = __floats2bfloat162_rn(x[e] - hf.x, x[e + 1] - hf.y);
+            h2[e / 2] = *reinterpret_cast<const uint32_t*>(&h);
+            l2[e / 2] = *reinterpret_cast<const uint32_t*>(&l);
+          }
+          *reinterpret_cast<uint4*>(hi + sw128(r, c)) = make_uint4(h2[0], h2[1], h2[2], h2[3]);
+          *reinterpret_cast<uint4*>(lo + sw128(r, c)) = make_uint4(l2[0], l2[1], l2[2], l2[3]);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> tensor-core reads
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(smem_u32(&xempty[sx]));
+          mbar_arrive(smem_u32(&bfull[sb]));
+        }
+      }
+      if (real) {
+        p.nrm[(int64_t)item * F + row] = nrm;
+        if (!finite) atomicExch(p.bad, 1);
+      }
+    }
+  } else {
+    // ---------------- epilogue: TMEM -> fp64 chunk sums ----------------
+    const int quarter = warp & 3;
+    const int r = quarter * 32 + lane;  // TMEM lane = frame row of the 128-row operand
+    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+    const int colb = (r >> 6) * 64;     // this row's item occupies columns [colb, colb + 64)
+    uint32_t ch = 0;
+    for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+      double acc[64];
+#pragma unroll
+      for (int i = 0; i < 64; ++i) acc[i] = 0.0;
+      for (int c = 0; c < nchunk; ++c, ++ch) {
+        const uint32_t ab = ch & 1;
+        mbar_wait(smem_u32(&afull[ab]), (ch >> 1) & 1);
+        tc_fence_after();
+        float v[32];
+        tmem_ld32(tmem + lane_base + ab * 128 + colb, v);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) acc[i] += (double)v[i];
+        tmem_ld32(tmem + lane_base + ab * 128 + colb + 32, v);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&aempty[ab]));
+#pragma unroll
+        for (int i = 0; i < 32; ++i) acc[32 + i] += (double)v[i];
+      }
+      const int item = 2 * tile + (r >> 6);
+      const int row = r & 63;
+      if (row < F && item < p.n_items) {
+        double* g = p.G + ((int64_t)item * F + row) * F;
+#pragma unroll
+        for (int i = 0; i < 64; ++i)
+          if (i < F) g[i] = acc[i];
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+  }
+}
+
+}  // namespace gram
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn_gram() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    FC_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !p) raise(LC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// true when the tensor-core Gram applies: F <= 64 (two items per 128-row
+// tile), F % 8 == 0, E % 64 == 0 and 16-byte aligned latents.
+bool gram_tc_supported(int F, int64_t E, const float* lat) {
+  const char* e = getenv("FC_GRAM_EXACT");
+  if (e && atoi(e) == 1) return false;
+  return F >= 8 && F <= 64 && F % 8 == 0 && E % 64 == 0 && E <= (int64_t)1 << 30 &&
+         (reinterpret_cast<uintptr_t>(lat) & 15) == 0;
+}
+
+void gram_tc(lc_ctx* ctx, const float* lat, int n_items, int F, int64_t E, double* G, double* nrm, int* bad) {
+  using namespace gram;
+  alignas(64) CUtensorMap tm;
+  cuuint64_t gdim[3] = {(cuuint64_t)E, (cuuint64_t)F, (cuuint64_t)n_items};
+  cuuint64_t gstride[2] = {(cuuint64_t)E * 4, (cuuint64_t)F * E * 4};
+  cuuint32_t box[3] = {32, (cuuint32_t)F, 1};
+  cuuint32_t estride[3] = {1, 1, 1};
+  CUresult r = encode_fn_gram()(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(lat), gdim, gstride, box,
+                                estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) raise(LC_ERR_CUDA, "cuTensorMapEncodeTiled (gram) failed: " + std::to_string((int)r));
+  Params p;
+  p.n_items = n_items;
+  p.F = F;
+  p.n_tiles = (n_items + 1) / 2;
+  p.E = E;
+  p.n_units = (int)(E / KU);
+  p.G = G;
+  p.nrm = nrm;
+  p.bad = bad;
+  const size_t smem = 1024 + NX * XSTAGE + NB * BSTAGE + 256;
+  FC_CUDA(cudaFuncSetAttribute(k_gram_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int grid = std::min(p.n_tiles, ctx->sm_count);
+  KTimer kt(ctx, "gram");
+  k_gram_tc<<<grid, GT, smem, ctx->stream>>>(tm, p);
+  kt.stop();
+  FC_LAUNCH_CHECK();
+  count_launch(ctx);
+}
+
+}  // namespace fc
