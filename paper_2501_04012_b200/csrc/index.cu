@@ -194,6 +194,10 @@ __global__ void __launch_bounds__(RS_WARPS * 32)
   const int q = blockIdx.x * RS_WARPS + warp;
   if (q >= nq) return;
   const float* qv = Q + (int64_t)q * dim;
+  extern __shared__ float s_rq[];  // [RS_WARPS][dim] this warp's query
+  float* sq = s_rq + (size_t)warp * dim;
+  for (int d = lane; d < dim; d += 32) sq[d] = qv[d];
+  __syncwarp();
   const int cn = cand_n[q];
   Cand mine[PER_LANE];
   int mn = 0;
@@ -208,7 +212,34 @@ __global__ void __launch_bounds__(RS_WARPS * 32)
       min_approx = fminf(min_approx, a);
       const float* x = rows + (int64_t)r * dim;
       double acc = 0.0;
-      for (int d = 0; d < dim; ++d) acc = fma((double)__ldg(qv + d), (double)__ldg(x + d), acc);
+      if ((dim & 15) == 0) {
+        // sequential fp64 in d order (vindex.cpp:67); the row streams as
+        // float4 loads issued 16 elements ahead, the query comes from smem
+        const float4* x4 = reinterpret_cast<const float4*>(x);
+        const float4* q4 = reinterpret_cast<const float4*>(sq);
+        float4 nx[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) nx[u] = __ldg(x4 + u);
+        for (int d4 = 0; d4 < dim / 4; d4 += 4) {
+          float4 cx[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) cx[u] = nx[u];
+          if (d4 + 4 < dim / 4) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) nx[u] = __ldg(x4 + d4 + 4 + u);
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const float4 qq = q4[d4 + u];
+            acc = fma((double)qq.x, (double)cx[u].x, acc);
+            acc = fma((double)qq.y, (double)cx[u].y, acc);
+            acc = fma((double)qq.z, (double)cx[u].z, acc);
+            acc = fma((double)qq.w, (double)cx[u].w, acc);
+          }
+        }
+      } else {
+        for (int d = 0; d < dim; ++d) acc = fma((double)sq[d], (double)__ldg(x + d), acc);
+      }
       local_err = fmax(local_err, fabs(acc - (double)a));
       Cand cc;
       cc.s = acc;
@@ -381,17 +412,23 @@ void query_dev(lc_index* ix, int kind, const float* Qdev, int nq, int k, uint64_
   auto* err_bits = reinterpret_cast<unsigned long long*>(fn.as<char>() + 8);
   FC_CUDA(cudaMemsetAsync(fn.p, 0, 16, ctx->stream));
   const unsigned g = (unsigned)((nq + RS_WARPS - 1) / RS_WARPS);
+  const size_t rs_smem = (size_t)RS_WARPS * ix->dim * sizeof(float);
+  if (rs_smem > 48 * 1024) {
+    FC_CUDA(cudaFuncSetAttribute(k_rescore<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs_smem));
+    FC_CUDA(cudaFuncSetAttribute(k_rescore<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs_smem));
+    FC_CUDA(cudaFuncSetAttribute(k_rescore<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs_smem));
+  }
   KTimer kt(ctx, "rescore");
   if (kp <= 32)
-    k_rescore<1><<<g, RS_WARPS * 32, 0, ctx->stream>>>(Qdev, nq, ix->dim, ix->rows[kind], ix->ids_dev, cs.as<float>(),
+    k_rescore<1><<<g, RS_WARPS * 32, rs_smem, ctx->stream>>>(Qdev, nq, ix->dim, ix->rows[kind], ix->ids_dev, cs.as<float>(),
                                                        cr.as<uint32_t>(), cn.as<int32_t>(), kp, ix->n, k, ix->eps, oid, osc, ocnt,
                                                        fl.as<int32_t>(), fail_n, err_bits);
   else if (kp <= 64)
-    k_rescore<2><<<g, RS_WARPS * 32, 0, ctx->stream>>>(Qdev, nq, ix->dim, ix->rows[kind], ix->ids_dev, cs.as<float>(),
+    k_rescore<2><<<g, RS_WARPS * 32, rs_smem, ctx->stream>>>(Qdev, nq, ix->dim, ix->rows[kind], ix->ids_dev, cs.as<float>(),
                                                        cr.as<uint32_t>(), cn.as<int32_t>(), kp, ix->n, k, ix->eps, oid, osc, ocnt,
                                                        fl.as<int32_t>(), fail_n, err_bits);
   else
-    k_rescore<4><<<g, RS_WARPS * 32, 0, ctx->stream>>>(Qdev, nq, ix->dim, ix->rows[kind], ix->ids_dev, cs.as<float>(),
+    k_rescore<4><<<g, RS_WARPS * 32, rs_smem, ctx->stream>>>(Qdev, nq, ix->dim, ix->rows[kind], ix->ids_dev, cs.as<float>(),
                                                        cr.as<uint32_t>(), cn.as<int32_t>(), kp, ix->n, k, ix->eps, oid, osc, ocnt,
                                                        fl.as<int32_t>(), fail_n, err_bits);
   kt.stop();

@@ -741,6 +741,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             a3 = fmaxf(a3, fmaxf(vc[14], vc[15]));
             const float mx = fmaxf(fmaxf(a0, a1), fmaxf(a2, a3));
             if (!__any_sync(0xffffffffu, (mx > tau) | (lim_all < PN))) continue;
+            if (p.debug & 32) continue;  // diagnostic: fast path only
             if ((p.debug & 16) && lane == 0) atomicAdd(p.stats + 0, 1u);
             if (__any_sync(0xffffffffu, cnt + 16 > cap)) {
               if ((p.debug & 16) && lane == 0) atomicAdd(p.stats + 1, 1u);
