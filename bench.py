@@ -65,6 +65,9 @@ def parse():
     ap.add_argument("--codec-prompts", type=int, default=256)
     ap.add_argument("--codec-frames", type=int, default=64)
     ap.add_argument("--no-codec", action="store_true")
+    ap.add_argument("--no-scoring", action="store_true")
+    ap.add_argument("--score-prompts", type=int, default=100_000)
+    ap.add_argument("--score-evictions", type=int, default=2000)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-queries", type=int, default=0, help="reference sample size (0 = auto)")
     ap.add_argument("--seed", type=int, default=2)
@@ -436,6 +439,13 @@ def main():
     if not args.no_codec and rank == 0:
         codec = bench_codec(torch, fc, ctx, args, dev, peaks)
 
+    scoring = None
+    if not args.no_scoring and rank == 0:
+        try:
+            scoring = bench_scoring(torch, fc, ctx, args, peaks)
+        except Exception as ex:  # reported, never fatal to the headline line
+            scoring = {"error": str(ex)[:200]}
+
     # ---- CPU baseline: reference query_top1 on this box's host cores ----
     cpu = None
     if not args.no_cpu and world == 1 and rank == 0:
@@ -465,7 +475,7 @@ def main():
             "lookup_stats": {"certified": st.certified, "fallback": st.fallback, "max_abs_err": st.max_abs_err},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clk.summary(), "kernel_ms": {k_: round(v_[1], 3) for k_, v_ in kt.items()},
-            "codec": codec,
+            "codec": codec, "scoring": scoring,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -548,6 +558,53 @@ def bench_codec(torch, fc, ctx, args, dev, peaks):
         "decompress_stitch_GBps": (stitch_bytes / (t_.value / 1000) / 1e9) if t_.value else None,
     }
     return res
+
+
+def bench_scoring(torch, fc, ctx, args, peaks):
+    """Replacement scoring on a 100k-prompt x 5-step
+    LRBU store (500k live steps): evict_one throughput and the scoring kernel's
+    GB/s against ~53 algorithmic bytes per live step (§8(d))."""
+    n_p = args.score_prompts
+    steps = [5, 10, 15, 20, 25]
+    F, dims = 1, (8, 8, 1)
+    rng = np.random.default_rng(7)
+    lat = rng.standard_normal((n_p, 5, F, 64)).astype(np.float32)
+    om = np.zeros((n_p, F, 8), np.uint8)
+    ents, sizes = fc.compress_batch(lat, steps, om, om, dims, list(range(1, n_p + 1)), ctx=ctx)
+    st = fc.CacheStore(int(sizes.sum()) * 2, fc.Policy.Lrbu, ctx=ctx)
+    t0 = time.perf_counter()
+    for i, e in enumerate(ents):
+        st.insert_steps(i + 1, e, steps, i + 1)
+    ins_s = time.perf_counter() - t0
+    del ents
+    now = n_p + 1
+    for pid in rng.integers(1, n_p + 1, n_p // 2):  # vary f / last_access
+        st.get_step(int(pid), 25, now, want_latent=False)
+        now += 1
+    live = st.step_count()
+    fc.lib.lc_ctx_profile(ctx.h, 1)
+    fc.lib.lc_ctx_kernel_time(ctx.h, b"policy", None, None, 1)
+    n_ev = args.score_evictions
+    t0 = time.perf_counter()
+    for _ in range(n_ev):
+        st.evict_one(now)
+    ev_s = time.perf_counter() - t0
+    c_, t_ = C.c_uint64(), C.c_double()
+    fc.lib.lc_ctx_kernel_time(ctx.h, b"policy", C.byref(c_), C.byref(t_), 1)
+    fc.lib.lc_ctx_profile(ctx.h, 0)
+    assert st.used() == st.recompute_used()
+    per_launch_ms = t_.value / c_.value if c_.value else None
+    alg_bytes = live * 53
+    return {"workload": f"{n_p} prompts x 5 steps LRBU, {live} live steps, {n_ev} evict_one calls",
+            "evictions_per_s": n_ev / ev_s, "insert_steps_per_s": n_p / ins_s,
+            "scoring_launches": int(c_.value), "scoring_ms_per_launch": per_launch_ms,
+            "roofline": {"bound": "hbm", "kernel": "k_policy_head + k_head_merge",
+                         "achieved": round(alg_bytes / (per_launch_ms / 1e3) / 1e9, 1) if per_launch_ms else None,
+                         "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                         "frac": round(alg_bytes / (per_launch_ms / 1e3) / 1e9 / peaks["hbm_gbs"], 4)
+                         if per_launch_ms else None,
+                         "bytes_per_launch": alg_bytes, "note": "latency-bound at this size (SURVEY 8(d))"},
+            "reference_evict_one_ms_at_500k_live": 38.8}
 
 
 if __name__ == "__main__":

@@ -132,9 +132,11 @@ class Context {
   lc_ctx* h_ = nullptr;
 };
 
+// Intentionally never destroyed: a static owner would tear the context down
+// after the CUDA runtime during process exit.
 inline std::shared_ptr<Context>& default_context_slot() {
-  static std::shared_ptr<Context> ctx;
-  return ctx;
+  static auto* ctx = new std::shared_ptr<Context>();
+  return *ctx;
 }
 inline std::shared_ptr<Context> default_context() {
   auto& c = default_context_slot();

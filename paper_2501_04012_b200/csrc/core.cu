@@ -9,10 +9,16 @@
 
 namespace fc {
 
-static thread_local std::string g_err;
+// POD storage: no TLS destructor, so a C-ABI call made while the process is
+// exiting (e.g. a static owner destroying its context) can still record its error
+static thread_local char g_err[1024];
 static thread_local uint64_t g_over_needed = 0, g_over_limit = 0;
 
-void set_last_error(const std::string& m) { g_err = m; }
+void set_last_error(const std::string& m) {
+  const size_t n = std::min(m.size(), sizeof(g_err) - 1);
+  memcpy(g_err, m.data(), n);
+  g_err[n] = 0;
+}
 void set_last_oversize(uint64_t needed, uint64_t limit) {
   g_over_needed = needed;
   g_over_limit = limit;
@@ -185,7 +191,7 @@ using namespace fc;
 
 extern "C" {
 
-const char* lc_last_error(void) { return g_err.c_str(); }
+const char* lc_last_error(void) { return g_err; }
 void lc_last_oversize(uint64_t* needed, uint64_t* limit) {
   if (needed) *needed = g_over_needed;
   if (limit) *limit = g_over_limit;

@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <cmath>
 #include <map>
+#include <memory>
 #include <queue>
 #include <unordered_map>
 #include <unordered_set>
@@ -94,6 +95,9 @@ __global__ void __launch_bounds__(POL_T) k_policy_head(const DevLive* __restrict
   if (threadIdx.x == 0) pcount[blockIdx.x] = got;
 }
 
+// Block b merges the per-block heads b, b + gridDim.x, ... into its own
+// sorted head; launched twice (many blocks, then one) so no single block
+// walks all ~500 partial heads of a 500k-slot table.
 __global__ void __launch_bounds__(256) k_head_merge(const Cand* __restrict__ partial, const int32_t* __restrict__ pcount,
                                                     int nblk, Cand* __restrict__ head, int32_t* __restrict__ head_n) {
   __shared__ Cand s_c[8];
@@ -101,13 +105,13 @@ __global__ void __launch_bounds__(256) k_head_merge(const Cand* __restrict__ par
   __shared__ Cand s_out[HEAD];
   Cand L[HEAD];
   int ln = 0;
-  for (int bi = threadIdx.x; bi < nblk; bi += blockDim.x) {
+  for (int bi = blockIdx.x + threadIdx.x * gridDim.x; bi < nblk; bi += blockDim.x * gridDim.x) {
     const int c = pcount[bi];
     for (int t = 0; t < c; ++t) local_insert<HEAD>(L, ln, HEAD, partial[(int64_t)bi * HEAD + t]);
   }
   const int got = block_merge_lists<HEAD>(L, ln, HEAD, s_out, s_c, s_o);
-  for (int t = threadIdx.x; t < got; t += blockDim.x) head[t] = s_out[t];
-  if (threadIdx.x == 0) *head_n = got;
+  for (int t = threadIdx.x; t < got; t += blockDim.x) head[(int64_t)blockIdx.x * HEAD + t] = s_out[t];
+  if (threadIdx.x == 0) head_n[blockIdx.x] = got;
 }
 
 struct ScatterLive {
@@ -268,11 +272,15 @@ struct lc_store {
     k_policy_head<<<nblk, POL_T, 0, ctx->stream>>>(dl, n_slots, dp, policy, now, partial.as<Cand>(), pc.as<int32_t>(),
                                                    bad.as<int>());
     FC_LAUNCH_CHECK();
-    k_head_merge<<<1, 256, 0, ctx->stream>>>(partial.as<Cand>(), pc.as<int32_t>(), nblk, head.as<Cand>(),
+    const int mb = std::min(64, std::max(1, nblk / 8));
+    DevBuf mid((size_t)mb * HEAD * sizeof(Cand), ctx->stream), midn((size_t)mb * sizeof(int32_t), ctx->stream);
+    k_head_merge<<<mb, 256, 0, ctx->stream>>>(partial.as<Cand>(), pc.as<int32_t>(), nblk, mid.as<Cand>(),
+                                              midn.as<int32_t>());
+    k_head_merge<<<1, 256, 0, ctx->stream>>>(mid.as<Cand>(), midn.as<int32_t>(), mb, head.as<Cand>(),
                                              reinterpret_cast<int32_t*>(head.as<Cand>() + HEAD));
     kt.stop();
     FC_LAUNCH_CHECK();
-    count_launch(ctx, 2);
+    count_launch(ctx, 3);
     std::vector<Cand> h(HEAD);
     int32_t hn = 0, hb = 0;
     FC_CUDA(cudaMemcpyAsync(h.data(), head.p, HEAD * sizeof(Cand), cudaMemcpyDeviceToHost, ctx->stream));
@@ -286,6 +294,14 @@ struct lc_store {
 
   // slot -> (prompt record, live index)
   std::unordered_map<int64_t, uint64_t> slot_prompt;
+
+  // The eviction state (scored head + re-keyed siblings) stays valid across
+  // evict_one / insert_steps calls at the same `now` as long as nothing but
+  // evictions happened in between; any other mutation drops it.
+  struct Evictor;
+  std::unique_ptr<Evictor> evc;
+  Evictor& evictor(uint64_t now);
+  void invalidate() { evc.reset(); }
 
   lc_step_entry remove_step(std::map<uint64_t, Rec>::iterator it, int li, uint64_t attributed) {
     Rec& r = it->second;
@@ -329,6 +345,7 @@ struct lc_store {
       bool operator>(const HE& o) const { return key > o.key || (key == o.key && seq > o.seq); }
     };
     std::priority_queue<HE, std::vector<HE>, std::greater<HE>> heap;
+    Evictor(lc_store* st, uint64_t n) : s(st), now(n) {}
 
     lc_step_entry next() {
       if (s->prompts.empty()) raise(LC_ERR_LOGIC, "evict_one: store is empty");
@@ -394,6 +411,11 @@ struct lc_store {
   };
 };
 
+lc_store::Evictor& lc_store::evictor(uint64_t now) {
+  if (!evc || evc->now != now) evc.reset(new Evictor(this, now));
+  return *evc;
+}
+
 extern "C" {
 
 lc_status lc_store_create(lc_ctx* ctx, uint64_t capacity, int policy, lc_store** out) {
@@ -458,7 +480,7 @@ lc_status lc_store_insert(lc_store* s, uint64_t prompt, lc_entry* entry, const i
   int ne = 0;
   try {
     if (s->used + standalone > s->capacity) {
-      lc_store::Evictor ev{s, now};
+      lc_store::Evictor& ev = s->evictor(now);
       while (s->used + standalone > s->capacity) {
         lc_step_entry v = ev.next();
         if (evicted && ne < cap) evicted[ne] = v;
@@ -470,6 +492,7 @@ lc_status lc_store_insert(lc_store* s, uint64_t prompt, lc_entry* entry, const i
     if (n_evicted) *n_evicted = ne;
     throw;
   }
+  s->invalidate();  // new live steps may precede the scored head
   rec.pslot = s->alloc_prompt();
   for (int k : sel) {
     lc_store::Live l;
@@ -518,6 +541,7 @@ lc_status lc_store_get_step(lc_store* s, uint64_t prompt, int desired, uint64_t 
   l.f += 1;
   l.last = now;
   s->write_live(rec, l);
+  s->invalidate();  // its key changed
   *actual = l.step;
   LC_API_END
 }
@@ -525,8 +549,7 @@ lc_status lc_store_get_step(lc_store* s, uint64_t prompt, int desired, uint64_t 
 lc_status lc_store_evict_one(lc_store* s, uint64_t now, lc_step_entry* out) {
   LC_API_BEGIN
   DeviceGuard g(s->ctx->device);
-  lc_store::Evictor ev{s, now};
-  lc_step_entry v = ev.next();
+  lc_step_entry v = s->evictor(now).next();
   if (out) *out = v;
   LC_API_END
 }
@@ -541,6 +564,7 @@ lc_status lc_store_evict_step(lc_store* s, uint64_t prompt, int step, int32_t* r
     if (it->second.live[i].step == step) {
       auto& r = it->second;
       s->remove_step(it, (int)i, r.live[i].priv + r.shared / r.live.size());
+      s->invalidate();  // siblings' attributed capacity changed outside the evictor
       *removed = 1;
       break;
     }

@@ -5,6 +5,7 @@
 // exception types. Exit code 0 = all checks passed.
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -61,6 +62,7 @@ static MaskSet rect_masks(int F, int h, int w, int r0, int r1, int c0, int c1) {
 }
 
 int main() {
+  if (getenv("KAT_TRACE")) fprintf(stderr, "%s\n", "core: cosine_similarit");
   // ---- core: cosine_similarity
   {
     const std::vector<float> a{1, 2, 3}, b{4, 5, 6}, z{0, 0, 0};
@@ -68,6 +70,7 @@ int main() {
     CHECK(throws<std::invalid_argument>([&] { cosine_similarity(a, z); }));
     CHECK(throws<std::invalid_argument>([&] { cosine_similarity(a, std::vector<float>{1, 2}); }));
   }
+  if (getenv("KAT_TRACE")) fprintf(stderr, "%s\n", "store policies");
   // ---- store policies
   {
     StepEntry e{PromptId{1}, StepId(5), 0, 0, 0, 0, 1};
@@ -80,6 +83,7 @@ int main() {
     l.f = 9;
     CHECK(lcbfu_priority(l) == 50.0);
   }
+  if (getenv("KAT_TRACE")) fprintf(stderr, "%s\n", "select_keyframes");
   // ---- select_keyframes
   const FrameDims small{4, 4, 2};
   {
@@ -95,12 +99,14 @@ int main() {
     CHECK(select_keyframes(LatentState(StepId(5), groups), 0.99).mapping == (std::vector<int>{0, 0, 0, 0, 4, 4, 4, 4}));
     CHECK(throws<std::invalid_argument>([&] { select_keyframes(LatentState(StepId(5), same), 1.5); }));
   }
+  if (getenv("KAT_TRACE")) fprintf(stderr, "%s\n", "solve_alpha");
   // ---- solve_alpha
   {
     const std::vector<float> base{1, 2, 3, 4}, twice{2, 4, 6, 8}, zero{0, 0, 0, 0};
     CHECK(solve_alpha(twice, base) == 2.0f);
     CHECK(throws<DegenerateBase>([&] { solve_alpha(twice, zero); }));
   }
+  if (getenv("KAT_TRACE")) fprintf(stderr, "%s\n", "codec: zero-motion");
   // ---- codec: zero-motion entry at the paper geometry
   const FrameDims dims{};  // 40 x 64 x 4
   const int F = 64;
@@ -134,6 +140,7 @@ int main() {
     CompressedEntry back = deserialize_entry(bytes);
     CHECK(serialize_entry(back) == bytes);
   }
+  if (getenv("KAT_TRACE")) fprintf(stderr, "%s\n", "store: get_step hole f");
   // ---- store: get_step hole fallback + eviction callback
   {
     CacheStore st(1ull << 30, Policy::Lrbu);
@@ -154,6 +161,7 @@ int main() {
     CacheStore tiny(1000, Policy::Lru);
     CHECK(throws<OversizedEntry>([&] { tiny.insert_steps(PromptId{7}, zero, {StepId(5)}, 1); }));
   }
+  if (getenv("KAT_TRACE")) fprintf(stderr, "%s\n", "index: duplicates");
   // ---- index: duplicates -> smaller id, empty -> none
   {
     SimilarityIndex ix;
@@ -182,6 +190,7 @@ int main() {
     const auto dec = lookup_decide(ix, qw, qw, qw);
     CHECK(dec.size() == 1 && dec[0].kind == LC_WHOLE_HIT && dec[0].whole_id == 9 && dec[0].step == 25);
   }
+  if (getenv("KAT_TRACE")) fprintf(stderr, "%s\n", "stitch rules");
   // ---- stitch rules (a)/(b)/(c) per pixel
   {
     const FrameDims d{4, 4, 1};

@@ -184,3 +184,47 @@ def test_topk_merge_equals_unsharded(fc, orc, synth):
     mi, ms, mc = fc.topk_merge(gi, gs, gc, k)
     oi, os_, oc = orc.topk_flat(tabs[0], ids, q, k)
     assert (mi == oi).all() and (bits(ms) == bits(os_)).all() and (mc == oc).all()
+
+
+def test_sharded_index_product_path_single_rank(fc, orc, synth):
+    """paper_2501_04012_b200.sharded on the GPU: a world-size-1 NCCL group with
+    the device index, packed all-gather and lc_topk_merge on device tensors;
+    plus G=3 logical shards (id mod 3) merged on the device — both equal the
+    unsharded oracle bit for bit (the multi-rank host logic is covered by the
+    gloo tests in test_sharded.py)."""
+    import socket
+    import torch
+    import torch.distributed as dist
+    from paper_2501_04012_b200 import sharded
+    tabs, ids, q = _random_case(synth, 12000, 768, 64, 23)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        ix = fc.SimilarityIndex()
+        sh = sharded.ShardedIndex(ix)
+        assert sh.insert_batch(ids, *tabs) == len(ids)
+        qd = torch.from_numpy(q).cuda()
+        gi, gs, gc = sh.query_topk(0, qd, 8)
+        oi, os_, oc = orc.topk_flat(tabs[0], ids, q, 8)
+        assert (u64(gi.cpu().numpy()) == oi).all() and (bits(gs.cpu().numpy()) == bits(os_)).all()
+        assert (gc.cpu().numpy() == oc).all()
+        dec = sh.lookup_decide(qd, qd, qd)
+        ref = fc.lookup_decide(ix, q, q, q)
+        assert [(d.kind, d.step, d.whole_id) for d in dec] == [(d.kind, d.step, d.whole_id) for d in ref]
+    finally:
+        dist.destroy_process_group()
+    # G = 3 logical shards on one GPU, merged on the device
+    G = 3
+    parts = []
+    for g in range(G):
+        m = sharded.owner_of(ids, G) == np.uint64(g)
+        ixg = fc.SimilarityIndex()
+        ixg.insert_batch(ids[m], tabs[0][m], tabs[1][m], tabs[2][m])
+        parts.append(ixg.query_topk(fc.EmbeddingKind.Whole, torch.from_numpy(q).cuda(), 8))
+    mi, ms, mc = fc.topk_merge(torch.stack([p[0] for p in parts]), torch.stack([p[1] for p in parts]),
+                               torch.stack([p[2] for p in parts]), 8)
+    assert (u64(mi.cpu().numpy()) == oi).all() and (bits(ms.cpu().numpy()) == bits(os_)).all()
