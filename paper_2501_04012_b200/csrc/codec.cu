@@ -786,7 +786,7 @@ void parallel_for(int64_t n, Body body) {
 // Builds entries for n prompts given maps (host, [n][S][F] in input step
 // order) and the device Gram diagonals. Writes out[i], sizes[i].
 void assemble(lc_ctx* ctx, const float* lat, const uint8_t* om, const uint8_t* bm, const std::vector<int32_t>& steps_in,
-              const Geo& g, const std::vector<int32_t>& maps_h, const double* nrm_dev, const uint64_t* prompts, int64_t n,
+              const Geo& g, const int32_t* maps_h, const double* nrm_dev, const uint64_t* prompts, int64_t n,
               lc_entry** out, uint64_t* sizes) {
   const int S = (int)steps_in.size();
   const int F = g.F;
@@ -817,16 +817,18 @@ void assemble(lc_ctx* ctx, const float* lat, const uint8_t* om, const uint8_t* b
   }
   item_begin[n] = (int)items.size();
   // Gram diagonals (norms^2 of every frame) to the host
-  std::vector<double> diag((size_t)n * S * F);
+  PinnedBuf<double> diag((size_t)n * S * F);
   FC_CUDA(cudaMemcpyAsync(diag.data(), nrm_dev, diag.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   sync(ctx);
   tr.mark("common keys + diag D2H");
   // K7 over all (entry, common key) items
-  std::vector<InterRes> res(items.size());
+  PinnedBuf<InterRes> res(items.size());
   if (!items.empty()) {
     DevBuf di(items.size() * sizeof(InterItem), ctx->stream), dr(items.size() * sizeof(InterRes), ctx->stream),
         dp(S * sizeof(int), ctx->stream);
-    FC_CUDA(cudaMemcpyAsync(di.p, items.data(), di.bytes, cudaMemcpyHostToDevice, ctx->stream));
+    PinnedBuf<InterItem> items_h(items.size());
+    memcpy(items_h.data(), items.data(), items.size() * sizeof(InterItem));
+    FC_CUDA(cudaMemcpyAsync(di.p, items_h.data(), di.bytes, cudaMemcpyHostToDevice, ctx->stream));
     FC_CUDA(cudaMemcpyAsync(dp.p, perm.data(), dp.bytes, cudaMemcpyHostToDevice, ctx->stream));
     KTimer kt(ctx, "inter");
     k_inter<<<(unsigned)((items.size() + INTER_W - 1) / INTER_W), INTER_W * 32, 0, ctx->stream>>>(
@@ -841,9 +843,9 @@ void assemble(lc_ctx* ctx, const float* lat, const uint8_t* om, const uint8_t* b
   auto identical_sim = [](double ss) { return ss == 0.0 ? 1.0 : ss / (std::sqrt(ss) * std::sqrt(ss)); };
   // ---- per entry: base selection + assembly metadata ----
   std::vector<std::shared_ptr<EntryData>> ents(n);
-  std::vector<FrameJob> fjobs;
-  std::vector<ByteJob> bjobs;
-  std::vector<Recipe> all_recipes;
+  PinnedBuf<FrameJob> fjobs;
+  PinnedBuf<ByteJob> bjobs;
+  PinnedBuf<Recipe> all_recipes;
   std::vector<std::pair<size_t, size_t>> recipe_span(n);
   std::vector<int> best_base(n, 0);
   parallel_for(n, [&](int64_t e) {
@@ -979,9 +981,12 @@ void assemble(lc_ctx* ctx, const float* lat, const uint8_t* om, const uint8_t* b
     for (int si = 0; si < S; ++si) c += ents[e]->extra_idx[si].size();
     fj_off[e + 1] = fj_off[e] + c;
   }
-  fjobs.resize(fj_off[n]);
-  bjobs.resize(2 * n);
-  all_recipes.resize((size_t)n * S * F);
+  PinnedBuf<FrameJob> fj_buf(fj_off[n]);
+  PinnedBuf<ByteJob> bj_buf(3 * n);  // object masks, background masks, recipes
+  PinnedBuf<Recipe> rc_buf((size_t)n * S * F);
+  std::swap(fjobs.p, fj_buf.p), std::swap(fjobs.n, fj_buf.n);
+  std::swap(bjobs.p, bj_buf.p), std::swap(bjobs.n, bj_buf.n);
+  std::swap(all_recipes.p, rc_buf.p), std::swap(all_recipes.n, rc_buf.n);
   parallel_for(n, [&](int64_t e) {
     const std::shared_ptr<EntryData>& d = ents[e];
     d->arena = arena;
@@ -1037,8 +1042,8 @@ void assemble(lc_ctx* ctx, const float* lat, const uint8_t* om, const uint8_t* b
   if (!all_recipes.empty())
     FC_CUDA(cudaMemcpyAsync(rstage.p, all_recipes.data(), rstage.bytes, cudaMemcpyHostToDevice, ctx->stream));
   for (int64_t e = 0; e < n; ++e)
-    bjobs.push_back(ByteJob{ents[e]->dev + ents[e]->recipe_off, rstage.as<uint8_t>() + recipe_span[e].first * sizeof(Recipe),
-                            (int64_t)((recipe_span[e].second - recipe_span[e].first) * sizeof(Recipe))});
+    bjobs[2 * n + e] = ByteJob{ents[e]->dev + ents[e]->recipe_off, rstage.as<uint8_t>() + recipe_span[e].first * sizeof(Recipe),
+                               (int64_t)((recipe_span[e].second - recipe_span[e].first) * sizeof(Recipe))};
   DevBuf dfj(fjobs.size() * sizeof(FrameJob), ctx->stream), dbj(bjobs.size() * sizeof(ByteJob), ctx->stream);
   FC_CUDA(cudaMemcpyAsync(dfj.p, fjobs.data(), dfj.bytes, cudaMemcpyHostToDevice, ctx->stream));
   FC_CUDA(cudaMemcpyAsync(dbj.p, bjobs.data(), dbj.bytes, cudaMemcpyHostToDevice, ctx->stream));
@@ -1224,13 +1229,13 @@ lc_status lc_compress_batch(lc_ctx* ctx, const float* latents, const int32_t* st
   DevBuf maps((size_t)n * S * F * sizeof(int32_t), ctx->stream);
   select_cert(ctx, G.as<double>(), NR.as<double>(), lat.dev, (int)(n * S), g, thr, delta, maps.as<int32_t>(),
               bad.as<int>());
-  std::vector<int32_t> maps_h((size_t)n * S * F);
+  PinnedBuf<int32_t> maps_h((size_t)n * S * F);
   FC_CUDA(cudaMemcpyAsync(maps_h.data(), maps.p, maps.bytes, cudaMemcpyDeviceToHost, ctx->stream));
   if (check_flag(ctx, bad)) raise(LC_ERR_INVALID_ARGUMENT, "cosine_similarity: zero-norm operand");
   check_distinct_steps(S, steps);
   tr.mark("select + maps D2H");
   std::vector<int32_t> st(steps, steps + S);
-  assemble(ctx, lat.dev, om.dev, bm.dev, st, g, maps_h, NR.as<double>(), prompts, n, out, sizes);
+  assemble(ctx, lat.dev, om.dev, bm.dev, st, g, maps_h.data(), NR.as<double>(), prompts, n, out, sizes);
   tr.mark("assemble");
   LC_API_END
 }
@@ -1261,7 +1266,7 @@ lc_status lc_inter_compress(lc_ctx* ctx, const float* latents, const int32_t* ma
   FC_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), ctx->stream));
   grams_and_norms(ctx, lat.dev, S, g, G.as<double>(), NR.as<double>(), bad.as<int>());
   std::vector<int32_t> st(steps, steps + S);
-  assemble(ctx, lat.dev, om.dev, bm.dev, st, g, maps_h, NR.as<double>(), &prompt, 1, out, nullptr);
+  assemble(ctx, lat.dev, om.dev, bm.dev, st, g, maps_h.data(), NR.as<double>(), &prompt, 1, out, nullptr);
   LC_API_END
 }
 

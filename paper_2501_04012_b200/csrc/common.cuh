@@ -224,3 +224,32 @@ __device__ __forceinline__ bool better(double s1, uint64_t i1, double s2, uint64
 __device__ __forceinline__ double warp_shfl_d(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
 
 }  // namespace fc
+
+namespace fc {
+// Page-locked host staging with a process-wide cache of blocks: D2H / H2D of
+// the compress orchestration's small arrays (maps, norms, per-key results,
+// copy jobs, recipes) run at PCIe/NVLink-C2C speed instead of through the
+// driver's pageable bounce buffers, without a cudaHostAlloc per call.
+void* pinned_acquire(size_t bytes);
+void pinned_release(void* p);
+template <class T>
+struct PinnedBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  PinnedBuf() = default;
+  explicit PinnedBuf(size_t count) : n(count) {
+    if (count) p = static_cast<T*>(pinned_acquire(count * sizeof(T)));
+  }
+  PinnedBuf(const PinnedBuf&) = delete;
+  PinnedBuf& operator=(const PinnedBuf&) = delete;
+  ~PinnedBuf() {
+    if (p) pinned_release(p);
+  }
+  T* data() { return p; }
+  const T* data() const { return p; }
+  size_t size() const { return n; }
+  T& operator[](size_t i) { return p[i]; }
+  const T& operator[](size_t i) const { return p[i]; }
+  bool empty() const { return n == 0; }
+};
+}  // namespace fc

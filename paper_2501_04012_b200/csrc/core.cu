@@ -3,6 +3,7 @@
 // decide/similarity_to_step rule and the shard merge.
 #include <cmath>
 #include <cstring>
+#include <map>
 #include <mutex>
 
 #include "common.cuh"
@@ -13,6 +14,34 @@ namespace fc {
 // exiting (e.g. a static owner destroying its context) can still record its error
 static thread_local char g_err[1024];
 static thread_local uint64_t g_over_needed = 0, g_over_limit = 0;
+
+// ---- pinned host staging cache ----
+namespace {
+std::mutex g_pin_mu;
+std::multimap<size_t, void*> g_pin_free;   // size -> block
+std::map<void*, size_t> g_pin_size;        // block -> size
+}  // namespace
+
+void* pinned_acquire(size_t bytes) {
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  auto it = g_pin_free.lower_bound(bytes);
+  if (it != g_pin_free.end() && it->first <= 4 * bytes + (1 << 20)) {
+    void* p = it->second;
+    g_pin_free.erase(it);
+    return p;
+  }
+  size_t sz = 1 << 16;
+  while (sz < bytes) sz <<= 1;
+  void* p = nullptr;
+  FC_CUDA(cudaHostAlloc(&p, sz, cudaHostAllocPortable));
+  g_pin_size[p] = sz;
+  return p;
+}
+
+void pinned_release(void* p) {
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  g_pin_free.emplace(g_pin_size.at(p), p);
+}
 
 void set_last_error(const std::string& m) {
   const size_t n = std::min(m.size(), sizeof(g_err) - 1);
