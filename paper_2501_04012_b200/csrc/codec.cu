@@ -457,6 +457,166 @@ __global__ void __launch_bounds__(INTER_W * 32) k_inter(const float* __restrict_
   }
 }
 
+// k_inter with the frames staged in shared memory by 1-D bulk copies
+// (cp.async.bulk, mbarrier-completed, double-buffered per warp): the 2S
+// frames an item needs (S keys + S first frames) arrive as contiguous chunks
+// of ICH floats and every lane reads them from smem (lanes share frames, so
+// most reads broadcast). Same arithmetic and element order as k_inter.
+constexpr int ICH = 256;
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ uint32_t s_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void s_mbar_wait(uint32_t bar, uint32_t phase) {
+  asm volatile(
+      "{\n.reg .pred P1;\nWAIT_%=:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n@!P1 bra WAIT_%=;\n}" ::"r"(bar),
+      "r"(phase)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(INTER_W * 32) k_inter_bulk(const float* __restrict__ lat,
+                                                             const InterItem* __restrict__ items, int n_items, int S,
+                                                             const int* __restrict__ perm, int F, int64_t E,
+                                                             const double* __restrict__ nrm,
+                                                             InterRes* __restrict__ out) {
+  extern __shared__ __align__(128) float s_fr[];  // [INTER_W][2 buf][2S frames][ICH]
+  __shared__ __align__(8) uint64_t s_bar[INTER_W][2];
+  __shared__ double s_num[INTER_W][MAXS][MAXS];
+  __shared__ float s_alpha[INTER_W][MAXS][MAXS];
+  __shared__ int s_nz[INTER_W][MAXS], s_exact[INTER_W][MAXS];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int idx = blockIdx.x * INTER_W + w;
+  const bool live = idx < n_items;
+  const int nfr = 2 * S;
+  float* buf = s_fr + (size_t)w * 2 * nfr * ICH;
+  if (lane == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s_u32(&s_bar[w][0])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s_u32(&s_bar[w][1])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  if (!live) return;
+  const InterItem it = items[idx];
+  const int m = it.m;
+  const float* base = lat + (int64_t)it.entry * S * F * E;
+  const int nch = (int)((E + ICH - 1) / ICH);
+  uint32_t use[2] = {0, 0};  // completed phases per buffer (for the parity wait)
+  // frame f of the item: f < S -> key m of sorted step f, else first frame of sorted step f - S
+  auto issue = [&](int c, int bsel) {
+    if (lane == 0) {
+      // the buffer was last read through the generic proxy (after __syncwarp)
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      const int64_t e0 = (int64_t)c * ICH;
+      const uint32_t cnt = (uint32_t)min((int64_t)ICH, E - e0);
+      const uint32_t bar = s_u32(&s_bar[w][bsel]);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(cnt * 4u * nfr) : "memory");
+      for (int f = 0; f < nfr; ++f) {
+        const int st = f < S ? f : f - S;
+        const float* src = base + ((int64_t)perm[st] * F + (f < S ? m : 0)) * E + e0;
+        bulk_g2s(s_u32(buf + ((size_t)bsel * nfr + f) * ICH), src, cnt * 4u, bar);
+      }
+    }
+  };
+  // one streaming pass over E; body(c, frames of buffer) per chunk
+  auto pass = [&](auto&& body) {
+    issue(0, 0);
+    for (int c = 0; c < nch; ++c) {
+      const int bsel = c & 1;
+      if (c + 1 < nch) issue(c + 1, bsel ^ 1);
+      s_mbar_wait(s_u32(&s_bar[w][bsel]), use[bsel] & 1);
+      ++use[bsel];
+      const int cnt = (int)min((int64_t)ICH, E - (int64_t)c * ICH);
+      body(buf + (size_t)bsel * nfr * ICH, cnt);
+      __syncwarp();  // everyone done with this buffer before it is refilled (issue at c + 2)
+    }
+  };
+  // ---- phase A: num[s][b] (s <= b), nz / exact on the diagonal ----
+  const int nA = S * (S + 1) / 2;
+  int sA = 0, bA = 0;
+  {
+    int r = lane;
+    while (sA < S && r >= S - sA) {
+      r -= S - sA;
+      ++sA;
+    }
+    bA = sA + r;
+  }
+  const bool laneA = lane < nA;
+  double acc = 0.0;
+  bool nz = false, exact = true;
+  pass([&](const float* fr, int cnt) {
+    if (!laneA) return;
+    const float* ks = fr + sA * ICH;
+    const float* fs = fr + (S + sA) * ICH;
+    const float* kb = fr + bA * ICH;
+    const float* fb = fr + (S + bA) * ICH;
+    for (int i = 0; i < cnt; ++i) {
+      const float ds = ks[i] - fs[i];
+      const float db = kb[i] - fb[i];
+      acc = fma((double)ds, (double)db, acc);
+      nz |= ds != 0.0f;
+      exact &= (fs[i] + ds) == ks[i];
+    }
+  });
+  if (laneA) {
+    s_num[w][sA][bA] = acc;
+    s_num[w][bA][sA] = acc;
+    if (sA == bA) {
+      s_nz[w][sA] = nz;
+      s_exact[w][sA] = exact;
+    }
+  }
+  __syncwarp();
+  for (int pr = lane; pr < S * S; pr += 32) {
+    const int s = pr / S, b = pr % S;
+    float a = 0.0f;
+    if (s_nz[w][b]) a = (float)(s_num[w][s][b] / s_num[w][b][b]);
+    s_alpha[w][s][b] = a;
+  }
+  __syncwarp();
+  // ---- phase B: trial reconstructions (s != b) ----
+  const int sB = lane / S, bB = lane % S;
+  const bool laneB = lane < S * S;
+  const bool pb = laneB && sB != bB && s_nz[w][bB] && isfinite(s_alpha[w][sB][bB]);
+  const double alpha = laneB ? (double)s_alpha[w][sB][bB] : 0.0;
+  double dot = 0.0, na = 0.0;
+  bool nonfin = false;
+  pass([&](const float* fr, int cnt) {
+    if (!pb) return;
+    const float* ks = fr + sB * ICH;
+    const float* fs = fr + (S + sB) * ICH;
+    const float* kb = fr + bB * ICH;
+    const float* fb = fr + (S + bB) * ICH;
+    for (int i = 0; i < cnt; ++i) {
+      const float db = kb[i] - fb[i];
+      const float r = (float)fma(alpha, (double)db, (double)fs[i]);
+      nonfin |= !isfinite(r);
+      dot = fma((double)r, (double)ks[i], dot);
+      na = fma((double)r, (double)r, na);
+    }
+  });
+  InterRes* o = out + idx;
+  if (laneB) {
+    const int s = sB, b = bB;
+    o->alpha[s][b] = s_alpha[w][s][b];
+    o->nonfinite[s][b] = nonfin;
+    double sim = 0.0;
+    if (pb) {
+      const double nb = nrm[((int64_t)it.entry * S + perm[s]) * F + m];
+      if (na == 0.0 && nb == 0.0) sim = 1.0;
+      else if (na == 0.0 || nb == 0.0) sim = 0.0;
+      else sim = dot / (sqrt(na) * sqrt(nb));
+    }
+    o->sim[s][b] = sim;
+    if (s == b) {
+      o->nz[s] = s_nz[w][s];
+      o->exact[s] = s_exact[w][s];
+    }
+  }
+}
+
 struct FrameJob {
   float* dst;
   const float* src;
@@ -831,9 +991,18 @@ void assemble(lc_ctx* ctx, const float* lat, const uint8_t* om, const uint8_t* b
     FC_CUDA(cudaMemcpyAsync(di.p, items_h.data(), di.bytes, cudaMemcpyHostToDevice, ctx->stream));
     FC_CUDA(cudaMemcpyAsync(dp.p, perm.data(), dp.bytes, cudaMemcpyHostToDevice, ctx->stream));
     KTimer kt(ctx, "inter");
-    k_inter<<<(unsigned)((items.size() + INTER_W - 1) / INTER_W), INTER_W * 32, 0, ctx->stream>>>(
-        lat, di.as<InterItem>(), (int)items.size(), S, dp.as<int>(), F, E, nrm_dev,
-                                                                  dr.as<InterRes>());
+    const unsigned nblk = (unsigned)((items.size() + INTER_W - 1) / INTER_W);
+    const size_t ism = (size_t)INTER_W * 2 * 2 * S * ICH * sizeof(float);
+    const bool bulk = S <= 5 && (E & 3) == 0 && (reinterpret_cast<uintptr_t>(lat) & 15) == 0 &&
+                      !(getenv("FC_INTER_LEGACY") && atoi(getenv("FC_INTER_LEGACY")) == 1);
+    if (bulk) {
+      FC_CUDA(cudaFuncSetAttribute(k_inter_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ism));
+      k_inter_bulk<<<nblk, INTER_W * 32, ism, ctx->stream>>>(lat, di.as<InterItem>(), (int)items.size(), S, dp.as<int>(),
+                                                            F, E, nrm_dev, dr.as<InterRes>());
+    } else {
+      k_inter<<<nblk, INTER_W * 32, 0, ctx->stream>>>(lat, di.as<InterItem>(), (int)items.size(), S, dp.as<int>(), F, E,
+                                                      nrm_dev, dr.as<InterRes>());
+    }
     FC_LAUNCH_CHECK();
     count_launch(ctx);
     FC_CUDA(cudaMemcpyAsync(res.data(), dr.p, dr.bytes, cudaMemcpyDeviceToHost, ctx->stream));

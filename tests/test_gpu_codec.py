@@ -168,3 +168,71 @@ def test_inter_compress_with_maps(fc, orc, synth):
     maps = fc.select_keyframes(lat, dims)
     ent = fc.inter_compress(lat, maps, synth.CACHED_STEPS, om, bm, dims, 99)
     assert ent.serialize() == orc.compress(lat, synth.CACHED_STEPS, om, bm, dims, 99)
+
+
+def _near_threshold_latent(rng, F, E, thr=0.99):
+    """Frames whose cosine to an earlier key sits within the tensor-core Gram's
+    certified bound (1e-4) of the threshold, and frames equally similar to two
+    keys (argmax ties broken by the reference's fp64 rounding), so
+    k_select_cert must fall back to exact sequential fp64 dots."""
+    unit = lambda v: v / np.linalg.norm(v)
+    x = np.zeros((F, E), np.float32)
+    k0 = unit(rng.standard_normal(E))
+    x[0] = k0 * 3.0
+    offs = [-3e-5, -1e-5, -2e-6, 0.0, 2e-6, 1e-5, 3e-5, 9e-5]
+    j = 1
+    for d in offs:  # sim(j, 0) = thr + d (up to fp32 rounding of the frame)
+        c = thr + d
+        u = unit(rng.standard_normal(E) - (rng.standard_normal(E) @ k0) * k0)
+        u = unit(u - (u @ k0) * k0)
+        x[j] = (c * k0 + np.sqrt(1 - c * c) * u) * (1.0 + 0.1 * j)
+        j += 1
+    # two keys 0.985 apart and their bisector (sim ~0.9962 to both)
+    a = unit(rng.standard_normal(E))
+    b = unit(0.985 * a + np.sqrt(1 - 0.985 ** 2) * unit(rng.standard_normal(E)))
+    x[j] = a; j += 1
+    x[j] = b; j += 1
+    x[j] = unit(a + b) * 2.0; j += 1
+    while j < F:
+        x[j] = unit(rng.standard_normal(E)) * 0.5
+        j += 1
+    return x
+
+
+def test_certified_select_near_threshold_and_ties(fc, orc):
+    """tcgen05 Gram + certified select against the oracle on adversarial
+    latents, and the tensor-core path against the exact-Gram path."""
+    dims = (40, 64, 4)
+    E_ = 40 * 64 * 4
+    rng = np.random.default_rng(123)
+    F = 16
+    lats = np.stack([_near_threshold_latent(rng, F, E_) for _ in range(6)])
+    got = fc.select_keyframes(lats, dims)
+    for i in range(lats.shape[0]):
+        ref = orc.select_keyframes(lats[i], dims)
+        assert (got[i] == ref).all(), (i, got[i], ref)
+    # the same through compress (5 steps = perturbations of the same frames)
+    steps = [5, 10, 15, 20, 25]
+    lat5 = np.stack([np.stack([lats[i] * np.float32(1 + 0.01 * s) for s in range(5)]) for i in range(2)])
+    om = np.zeros((2, F, 40 * 64 // 8), np.uint8)
+    ents, sizes = fc.compress_batch(lat5, steps, om, om, dims, [31, 32])
+    for i in range(2):
+        assert ents[i].serialize() == orc.compress(lat5[i], steps, om[i], om[i], dims, 31 + i)
+
+
+def test_tensor_core_gram_equals_exact_gram_path(fc, synth):
+    """FC_GRAM_EXACT=1 forces the sequential-fp64 Gram kernel; maps and wire
+    bytes must not depend on which Gram produced them."""
+    dims = (40, 64, 4)
+    lat = np.stack([synth.latents(70 + i, F=64, dims=dims) for i in range(2)])
+    masks = [synth.rect_masks(64, 40, 64, 70 + i) for i in range(2)]
+    om = np.stack([m[0] for m in masks])
+    bm = np.stack([m[1] for m in masks])
+    a, _ = fc.compress_batch(lat, synth.CACHED_STEPS, om, bm, dims, [1, 2])
+    os.environ["FC_GRAM_EXACT"] = "1"
+    try:
+        b, _ = fc.compress_batch(lat, synth.CACHED_STEPS, om, bm, dims, [1, 2])
+    finally:
+        del os.environ["FC_GRAM_EXACT"]
+    for x, y in zip(a, b):
+        assert x.serialize() == y.serialize()
