@@ -458,11 +458,13 @@ __global__ void __launch_bounds__(INTER_W * 32) k_inter(const float* __restrict_
 }
 
 // k_inter with the frames staged in shared memory by 1-D bulk copies
-// (cp.async.bulk, mbarrier-completed, double-buffered per warp): the 2S
-// frames an item needs (S keys + S first frames) arrive as contiguous chunks
-// of ICH floats and every lane reads them from smem (lanes share frames, so
-// most reads broadcast). Same arithmetic and element order as k_inter.
-constexpr int ICH = 256;
+// (cp.async.bulk, mbarrier-completed, double-buffered per warp). The fp32 ->
+// fp64 conversions run on the quarter-rate XU pipe (ncu: XU-bound), so each
+// chunk's values are converted ONCE per (frame, element) into fp64 staging
+// arrays shared by all (s, b) lanes, instead of once per lane: phase A reads
+// D[s] = (double)(key_s - first_s), phase B reads D[b], (double)first_s and
+// (double)key_s. Same arithmetic and element order as k_inter.
+constexpr int ICH = 128;
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
                "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(bar)
@@ -476,12 +478,17 @@ __device__ __forceinline__ void s_mbar_wait(uint32_t bar, uint32_t phase) {
       : "memory");
 }
 
+// dynamic smem per warp: fp32 frames [2 buf][2S][ICH] + fp64 [3][S][ICH]
+__host__ __device__ constexpr size_t inter_warp_smem(int S) {
+  return (size_t)2 * 2 * S * ICH * sizeof(float) + (size_t)3 * S * ICH * sizeof(double);
+}
+
 __global__ void __launch_bounds__(INTER_W * 32) k_inter_bulk(const float* __restrict__ lat,
                                                              const InterItem* __restrict__ items, int n_items, int S,
                                                              const int* __restrict__ perm, int F, int64_t E,
                                                              const double* __restrict__ nrm,
                                                              InterRes* __restrict__ out) {
-  extern __shared__ __align__(128) float s_fr[];  // [INTER_W][2 buf][2S frames][ICH]
+  extern __shared__ __align__(128) uint8_t s_raw[];
   __shared__ __align__(8) uint64_t s_bar[INTER_W][2];
   __shared__ double s_num[INTER_W][MAXS][MAXS];
   __shared__ float s_alpha[INTER_W][MAXS][MAXS];
@@ -490,7 +497,10 @@ __global__ void __launch_bounds__(INTER_W * 32) k_inter_bulk(const float* __rest
   const int idx = blockIdx.x * INTER_W + w;
   const bool live = idx < n_items;
   const int nfr = 2 * S;
-  float* buf = s_fr + (size_t)w * 2 * nfr * ICH;
+  float* buf = reinterpret_cast<float*>(s_raw + (size_t)w * inter_warp_smem(S));
+  double* dD = reinterpret_cast<double*>(buf + 2 * nfr * ICH);  // [S][ICH] diffs
+  double* dF = dD + S * ICH;                                      // [S][ICH] first frames
+  double* dK = dF + S * ICH;                                      // [S][ICH] keys
   if (lane == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s_u32(&s_bar[w][0])));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s_u32(&s_bar[w][1])));
@@ -502,8 +512,7 @@ __global__ void __launch_bounds__(INTER_W * 32) k_inter_bulk(const float* __rest
   const int m = it.m;
   const float* base = lat + (int64_t)it.entry * S * F * E;
   const int nch = (int)((E + ICH - 1) / ICH);
-  uint32_t use[2] = {0, 0};  // completed phases per buffer (for the parity wait)
-  // frame f of the item: f < S -> key m of sorted step f, else first frame of sorted step f - S
+  uint32_t use[2] = {0, 0};
   auto issue = [&](int c, int bsel) {
     if (lane == 0) {
       // the buffer was last read through the generic proxy (after __syncwarp)
@@ -512,15 +521,15 @@ __global__ void __launch_bounds__(INTER_W * 32) k_inter_bulk(const float* __rest
       const uint32_t cnt = (uint32_t)min((int64_t)ICH, E - e0);
       const uint32_t bar = s_u32(&s_bar[w][bsel]);
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(cnt * 4u * nfr) : "memory");
-      for (int f = 0; f < nfr; ++f) {
+      for (int f = 0; f < nfr; ++f) {  // f < S: key m of sorted step f; else first frame of sorted step f - S
         const int st = f < S ? f : f - S;
         const float* src = base + ((int64_t)perm[st] * F + (f < S ? m : 0)) * E + e0;
         bulk_g2s(s_u32(buf + ((size_t)bsel * nfr + f) * ICH), src, cnt * 4u, bar);
       }
     }
   };
-  // one streaming pass over E; body(c, frames of buffer) per chunk
-  auto pass = [&](auto&& body) {
+  // one streaming pass over E; per chunk: convert (shared by lanes), then body
+  auto pass = [&](bool phaseB, auto&& body) {
     issue(0, 0);
     for (int c = 0; c < nch; ++c) {
       const int bsel = c & 1;
@@ -528,11 +537,22 @@ __global__ void __launch_bounds__(INTER_W * 32) k_inter_bulk(const float* __rest
       s_mbar_wait(s_u32(&s_bar[w][bsel]), use[bsel] & 1);
       ++use[bsel];
       const int cnt = (int)min((int64_t)ICH, E - (int64_t)c * ICH);
-      body(buf + (size_t)bsel * nfr * ICH, cnt);
+      const float* fr = buf + (size_t)bsel * nfr * ICH;
+      for (int x = lane; x < S * cnt; x += 32) {
+        const int st = x / cnt, i = x - st * cnt;
+        const float k = fr[st * ICH + i], f0 = fr[(S + st) * ICH + i];
+        dD[st * ICH + i] = (double)(k - f0);
+        if (phaseB) {
+          dF[st * ICH + i] = (double)f0;
+          dK[st * ICH + i] = (double)k;
+        }
+      }
+      __syncwarp();
+      body(fr, cnt);
       __syncwarp();  // everyone done with this buffer before it is refilled (issue at c + 2)
     }
   };
-  // ---- phase A: num[s][b] (s <= b), nz / exact on the diagonal ----
+  // ---- phase A: num[s][b] (s <= b); nz / exact on the diagonal ----
   const int nA = S * (S + 1) / 2;
   int sA = 0, bA = 0;
   {
@@ -544,26 +564,28 @@ __global__ void __launch_bounds__(INTER_W * 32) k_inter_bulk(const float* __rest
     bA = sA + r;
   }
   const bool laneA = lane < nA;
+  const bool diagA = laneA && sA == bA;
   double acc = 0.0;
   bool nz = false, exact = true;
-  pass([&](const float* fr, int cnt) {
+  pass(false, [&](const float* fr, int cnt) {
     if (!laneA) return;
-    const float* ks = fr + sA * ICH;
-    const float* fs = fr + (S + sA) * ICH;
-    const float* kb = fr + bA * ICH;
-    const float* fb = fr + (S + bA) * ICH;
-    for (int i = 0; i < cnt; ++i) {
-      const float ds = ks[i] - fs[i];
-      const float db = kb[i] - fb[i];
-      acc = fma((double)ds, (double)db, acc);
-      nz |= ds != 0.0f;
-      exact &= (fs[i] + ds) == ks[i];
+    const double* ds = dD + sA * ICH;
+    const double* db = dD + bA * ICH;
+    for (int i = 0; i < cnt; ++i) acc = fma(ds[i], db[i], acc);
+    if (diagA) {  // codec.cpp:41-46 / 222-224 on this step's key
+      const float* ks = fr + sA * ICH;
+      const float* fs = fr + (S + sA) * ICH;
+      for (int i = 0; i < cnt; ++i) {
+        const float d = ks[i] - fs[i];
+        nz |= d != 0.0f;
+        exact &= (fs[i] + d) == ks[i];
+      }
     }
   });
   if (laneA) {
     s_num[w][sA][bA] = acc;
     s_num[w][bA][sA] = acc;
-    if (sA == bA) {
+    if (diagA) {
       s_nz[w][sA] = nz;
       s_exact[w][sA] = exact;
     }
@@ -583,18 +605,17 @@ __global__ void __launch_bounds__(INTER_W * 32) k_inter_bulk(const float* __rest
   const double alpha = laneB ? (double)s_alpha[w][sB][bB] : 0.0;
   double dot = 0.0, na = 0.0;
   bool nonfin = false;
-  pass([&](const float* fr, int cnt) {
+  pass(true, [&](const float*, int cnt) {
     if (!pb) return;
-    const float* ks = fr + sB * ICH;
-    const float* fs = fr + (S + sB) * ICH;
-    const float* kb = fr + bB * ICH;
-    const float* fb = fr + (S + bB) * ICH;
+    const double* db = dD + bB * ICH;
+    const double* fs = dF + sB * ICH;
+    const double* ks = dK + sB * ICH;
     for (int i = 0; i < cnt; ++i) {
-      const float db = kb[i] - fb[i];
-      const float r = (float)fma(alpha, (double)db, (double)fs[i]);
+      const float r = (float)fma(alpha, db[i], fs[i]);
       nonfin |= !isfinite(r);
-      dot = fma((double)r, (double)ks[i], dot);
-      na = fma((double)r, (double)r, na);
+      const double rd = (double)r;
+      dot = fma(rd, ks[i], dot);
+      na = fma(rd, rd, na);
     }
   });
   InterRes* o = out + idx;
@@ -992,7 +1013,7 @@ void assemble(lc_ctx* ctx, const float* lat, const uint8_t* om, const uint8_t* b
     FC_CUDA(cudaMemcpyAsync(dp.p, perm.data(), dp.bytes, cudaMemcpyHostToDevice, ctx->stream));
     KTimer kt(ctx, "inter");
     const unsigned nblk = (unsigned)((items.size() + INTER_W - 1) / INTER_W);
-    const size_t ism = (size_t)INTER_W * 2 * 2 * S * ICH * sizeof(float);
+    const size_t ism = (size_t)INTER_W * inter_warp_smem(S);
     const bool bulk = S <= 5 && (E & 3) == 0 && (reinterpret_cast<uintptr_t>(lat) & 15) == 0 &&
                       !(getenv("FC_INTER_LEGACY") && atoi(getenv("FC_INTER_LEGACY")) == 1);
     if (bulk) {
