@@ -457,187 +457,6 @@ __global__ void __launch_bounds__(INTER_W * 32) k_inter(const float* __restrict_
   }
 }
 
-// k_inter with the frames staged in shared memory by 1-D bulk copies
-// (cp.async.bulk, mbarrier-completed, double-buffered per warp). The fp32 ->
-// fp64 conversions run on the quarter-rate XU pipe (ncu: XU-bound), so each
-// chunk's values are converted ONCE per (frame, element) into fp64 staging
-// arrays shared by all (s, b) lanes, instead of once per lane: phase A reads
-// D[s] = (double)(key_s - first_s), phase B reads D[b], (double)first_s and
-// (double)key_s. Same arithmetic and element order as k_inter.
-constexpr int ICH = 128;
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-               "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(bar)
-               : "memory");
-}
-__device__ __forceinline__ uint32_t s_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void s_mbar_wait(uint32_t bar, uint32_t phase) {
-  asm volatile(
-      "{\n.reg .pred P1;\nWAIT_%=:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n@!P1 bra WAIT_%=;\n}" ::"r"(bar),
-      "r"(phase)
-      : "memory");
-}
-
-// dynamic smem per warp: fp32 frames [2 buf][2S][ICH] + fp64 [3][S][ICH]
-__host__ __device__ constexpr size_t inter_warp_smem(int S) {
-  return (size_t)2 * 2 * S * ICH * sizeof(float) + (size_t)3 * S * ICH * sizeof(double);
-}
-
-__global__ void __launch_bounds__(INTER_W * 32) k_inter_bulk(const float* __restrict__ lat,
-                                                             const InterItem* __restrict__ items, int n_items, int S,
-                                                             const int* __restrict__ perm, int F, int64_t E,
-                                                             const double* __restrict__ nrm,
-                                                             InterRes* __restrict__ out) {
-  extern __shared__ __align__(128) uint8_t s_raw[];
-  __shared__ __align__(8) uint64_t s_bar[INTER_W][2];
-  __shared__ double s_num[INTER_W][MAXS][MAXS];
-  __shared__ float s_alpha[INTER_W][MAXS][MAXS];
-  __shared__ int s_nz[INTER_W][MAXS], s_exact[INTER_W][MAXS];
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int idx = blockIdx.x * INTER_W + w;
-  const bool live = idx < n_items;
-  const int nfr = 2 * S;
-  float* buf = reinterpret_cast<float*>(s_raw + (size_t)w * inter_warp_smem(S));
-  double* dD = reinterpret_cast<double*>(buf + 2 * nfr * ICH);  // [S][ICH] diffs
-  double* dF = dD + S * ICH;                                      // [S][ICH] first frames
-  double* dK = dF + S * ICH;                                      // [S][ICH] keys
-  if (lane == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s_u32(&s_bar[w][0])));
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s_u32(&s_bar[w][1])));
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncwarp();
-  if (!live) return;
-  const InterItem it = items[idx];
-  const int m = it.m;
-  const float* base = lat + (int64_t)it.entry * S * F * E;
-  const int nch = (int)((E + ICH - 1) / ICH);
-  uint32_t use[2] = {0, 0};
-  auto issue = [&](int c, int bsel) {
-    if (lane == 0) {
-      // the buffer was last read through the generic proxy (after __syncwarp)
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      const int64_t e0 = (int64_t)c * ICH;
-      const uint32_t cnt = (uint32_t)min((int64_t)ICH, E - e0);
-      const uint32_t bar = s_u32(&s_bar[w][bsel]);
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(cnt * 4u * nfr) : "memory");
-      for (int f = 0; f < nfr; ++f) {  // f < S: key m of sorted step f; else first frame of sorted step f - S
-        const int st = f < S ? f : f - S;
-        const float* src = base + ((int64_t)perm[st] * F + (f < S ? m : 0)) * E + e0;
-        bulk_g2s(s_u32(buf + ((size_t)bsel * nfr + f) * ICH), src, cnt * 4u, bar);
-      }
-    }
-  };
-  // one streaming pass over E; per chunk: convert (shared by lanes), then body
-  auto pass = [&](bool phaseB, auto&& body) {
-    issue(0, 0);
-    for (int c = 0; c < nch; ++c) {
-      const int bsel = c & 1;
-      if (c + 1 < nch) issue(c + 1, bsel ^ 1);
-      s_mbar_wait(s_u32(&s_bar[w][bsel]), use[bsel] & 1);
-      ++use[bsel];
-      const int cnt = (int)min((int64_t)ICH, E - (int64_t)c * ICH);
-      const float* fr = buf + (size_t)bsel * nfr * ICH;
-      for (int x = lane; x < S * cnt; x += 32) {
-        const int st = x / cnt, i = x - st * cnt;
-        const float k = fr[st * ICH + i], f0 = fr[(S + st) * ICH + i];
-        dD[st * ICH + i] = (double)(k - f0);
-        if (phaseB) {
-          dF[st * ICH + i] = (double)f0;
-          dK[st * ICH + i] = (double)k;
-        }
-      }
-      __syncwarp();
-      body(fr, cnt);
-      __syncwarp();  // everyone done with this buffer before it is refilled (issue at c + 2)
-    }
-  };
-  // ---- phase A: num[s][b] (s <= b); nz / exact on the diagonal ----
-  const int nA = S * (S + 1) / 2;
-  int sA = 0, bA = 0;
-  {
-    int r = lane;
-    while (sA < S && r >= S - sA) {
-      r -= S - sA;
-      ++sA;
-    }
-    bA = sA + r;
-  }
-  const bool laneA = lane < nA;
-  const bool diagA = laneA && sA == bA;
-  double acc = 0.0;
-  bool nz = false, exact = true;
-  pass(false, [&](const float* fr, int cnt) {
-    if (!laneA) return;
-    const double* ds = dD + sA * ICH;
-    const double* db = dD + bA * ICH;
-    for (int i = 0; i < cnt; ++i) acc = fma(ds[i], db[i], acc);
-    if (diagA) {  // codec.cpp:41-46 / 222-224 on this step's key
-      const float* ks = fr + sA * ICH;
-      const float* fs = fr + (S + sA) * ICH;
-      for (int i = 0; i < cnt; ++i) {
-        const float d = ks[i] - fs[i];
-        nz |= d != 0.0f;
-        exact &= (fs[i] + d) == ks[i];
-      }
-    }
-  });
-  if (laneA) {
-    s_num[w][sA][bA] = acc;
-    s_num[w][bA][sA] = acc;
-    if (diagA) {
-      s_nz[w][sA] = nz;
-      s_exact[w][sA] = exact;
-    }
-  }
-  __syncwarp();
-  for (int pr = lane; pr < S * S; pr += 32) {
-    const int s = pr / S, b = pr % S;
-    float a = 0.0f;
-    if (s_nz[w][b]) a = (float)(s_num[w][s][b] / s_num[w][b][b]);
-    s_alpha[w][s][b] = a;
-  }
-  __syncwarp();
-  // ---- phase B: trial reconstructions (s != b) ----
-  const int sB = lane / S, bB = lane % S;
-  const bool laneB = lane < S * S;
-  const bool pb = laneB && sB != bB && s_nz[w][bB] && isfinite(s_alpha[w][sB][bB]);
-  const double alpha = laneB ? (double)s_alpha[w][sB][bB] : 0.0;
-  double dot = 0.0, na = 0.0;
-  bool nonfin = false;
-  pass(true, [&](const float*, int cnt) {
-    if (!pb) return;
-    const double* db = dD + bB * ICH;
-    const double* fs = dF + sB * ICH;
-    const double* ks = dK + sB * ICH;
-    for (int i = 0; i < cnt; ++i) {
-      const float r = (float)fma(alpha, db[i], fs[i]);
-      nonfin |= !isfinite(r);
-      const double rd = (double)r;
-      dot = fma(rd, ks[i], dot);
-      na = fma(rd, rd, na);
-    }
-  });
-  InterRes* o = out + idx;
-  if (laneB) {
-    const int s = sB, b = bB;
-    o->alpha[s][b] = s_alpha[w][s][b];
-    o->nonfinite[s][b] = nonfin;
-    double sim = 0.0;
-    if (pb) {
-      const double nb = nrm[((int64_t)it.entry * S + perm[s]) * F + m];
-      if (na == 0.0 && nb == 0.0) sim = 1.0;
-      else if (na == 0.0 || nb == 0.0) sim = 0.0;
-      else sim = dot / (sqrt(na) * sqrt(nb));
-    }
-    o->sim[s][b] = sim;
-    if (s == b) {
-      o->nz[s] = s_nz[w][s];
-      o->exact[s] = s_exact[w][s];
-    }
-  }
-}
-
 struct FrameJob {
   float* dst;
   const float* src;
@@ -1013,17 +832,8 @@ void assemble(lc_ctx* ctx, const float* lat, const uint8_t* om, const uint8_t* b
     FC_CUDA(cudaMemcpyAsync(dp.p, perm.data(), dp.bytes, cudaMemcpyHostToDevice, ctx->stream));
     KTimer kt(ctx, "inter");
     const unsigned nblk = (unsigned)((items.size() + INTER_W - 1) / INTER_W);
-    const size_t ism = (size_t)INTER_W * inter_warp_smem(S);
-    const bool bulk = S <= 5 && (E & 3) == 0 && (reinterpret_cast<uintptr_t>(lat) & 15) == 0 &&
-                      !(getenv("FC_INTER_LEGACY") && atoi(getenv("FC_INTER_LEGACY")) == 1);
-    if (bulk) {
-      FC_CUDA(cudaFuncSetAttribute(k_inter_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ism));
-      k_inter_bulk<<<nblk, INTER_W * 32, ism, ctx->stream>>>(lat, di.as<InterItem>(), (int)items.size(), S, dp.as<int>(),
-                                                            F, E, nrm_dev, dr.as<InterRes>());
-    } else {
-      k_inter<<<nblk, INTER_W * 32, 0, ctx->stream>>>(lat, di.as<InterItem>(), (int)items.size(), S, dp.as<int>(), F, E,
-                                                      nrm_dev, dr.as<InterRes>());
-    }
+    k_inter<<<nblk, INTER_W * 32, 0, ctx->stream>>>(lat, di.as<InterItem>(), (int)items.size(), S, dp.as<int>(), F, E,
+                                                    nrm_dev, dr.as<InterRes>());
     FC_LAUNCH_CHECK();
     count_launch(ctx);
     FC_CUDA(cudaMemcpyAsync(res.data(), dr.p, dr.bytes, cudaMemcpyDeviceToHost, ctx->stream));
