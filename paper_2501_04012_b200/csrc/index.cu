@@ -199,6 +199,35 @@ __global__ void __launch_bounds__(RS_WARPS * 32)
   for (int d = lane; d < dim; d += 32) sq[d] = qv[d];
   __syncwarp();
   const int cn = cand_n[q];
+  // Only candidates whose bf16 score is within 2*eps of the k-th best bf16
+  // score can reach the exact top-k: the k candidates ranked first by bf16
+  // all have exact >= a_k - eps, and a skipped row has exact <= a + eps <
+  // a_k - eps. Skipping the rest avoids most of the random 3 KB row gathers.
+  float ak = -INFINITY;
+  if (cn > k) {
+    float mine_a[PER_LANE];
+#pragma unroll
+    for (int t = 0; t < PER_LANE; ++t) {
+      const int c = lane + 32 * t;
+      mine_a[t] = c < cn ? cand_s[(int64_t)q * kp + c] : -INFINITY;
+    }
+    // k-th largest by rank counting over the warp's candidates
+#pragma unroll
+    for (int t = 0; t < PER_LANE; ++t) {
+      const int c = lane + 32 * t;
+      int rank = 0;
+      for (int u = 0; u < PER_LANE; ++u)
+        for (int j = 0; j < 32; ++j) {
+          const float o = __shfl_sync(0xffffffffu, mine_a[u], j);
+          const int oc = j + 32 * u;
+          rank += (o > mine_a[t]) | ((o == mine_a[t]) & (oc < c));
+        }
+      const bool is_k = c < cn && rank == k - 1;
+      const unsigned bal = __ballot_sync(0xffffffffu, is_k);
+      if (bal) ak = __shfl_sync(0xffffffffu, mine_a[t], __ffs(bal) - 1);
+    }
+  }
+  const float skip_below = ak - (float)(2.0 * eps) - 1e-6f;  // slack for the float subtraction
   Cand mine[PER_LANE];
   int mn = 0;
   float min_approx = INFINITY;
@@ -210,6 +239,7 @@ __global__ void __launch_bounds__(RS_WARPS * 32)
       const uint32_t r = cand_r[(int64_t)q * kp + c];
       const float a = cand_s[(int64_t)q * kp + c];
       min_approx = fminf(min_approx, a);
+      if (a < skip_below) continue;
       const float* x = rows + (int64_t)r * dim;
       double acc = 0.0;
       if ((dim & 15) == 0) {

@@ -167,32 +167,36 @@ __device__ __forceinline__ void publish_tau(uint32_t* gkey, int q, const float* 
 // therefore reject scores <= edge(B) at once; the units of one query, which
 // run concurrently on different row ranges, pool their evidence instead of
 // each warming its own threshold.
-constexpr int HB = 264;         // fine buckets (HB-8 .. HB-1 unused padding)
-constexpr int HC = 272;         // coarse counters at [HC, HC+16): octave o = (b-1)/32 (0..7), 8 = >= 1.0
-constexpr int HSTRIDE = 288;    // per-query words
+constexpr int BPO = 32;                  // fine buckets per octave (2.2% wide; 64 cut slow chunks 6% but cost more in refresh loads)
+constexpr int BPO_SHIFT = 23 - (BPO == 64 ? 6 : BPO == 32 ? 5 : BPO == 16 ? 4 : -100);  // top log2(BPO) mantissa bits
+static_assert(BPO_SHIFT > 0 && BPO_SHIFT < 23, "BPO must be 16, 32 or 64");
+constexpr int HB = 8 * BPO + 8;          // bucket 0, 8 octaves, overflow (>= 1.0), padding
+constexpr int HOV = 8 * BPO + 1;         // overflow bucket index
+constexpr int HC = HB + 8;               // coarse counters at [HC, HC+16): octave 0..7, 8 = >= 1.0
+constexpr int HSTRIDE = HC + 16;         // per-query words (multiple of 4: 16-byte aligned rows)
 __device__ __forceinline__ int hbucket(float s) {
   const uint32_t u = __float_as_uint(s);
   if ((int32_t)u < 0) return 0;  // negative
   const int e = (int)(u >> 23);
   if (e < 119) return 0;
-  if (e >= 127) return 257;
-  return 1 + (e - 119) * 32 + (int)((u >> 18) & 31);
+  if (e >= 127) return HOV;
+  return 1 + (e - 119) * BPO + (int)((u >> BPO_SHIFT) & (BPO - 1));
 }
 __device__ __forceinline__ float hedge(int b) {  // smallest score of bucket b >= 1
-  if (b >= 257) return 1.0f;
-  const int e = 119 + (b - 1) / 32, m = (b - 1) % 32;
-  return __uint_as_float(((uint32_t)e << 23) | ((uint32_t)m << 18));
+  if (b >= HOV) return 1.0f;
+  const int e = 119 + (b - 1) / BPO, m = (b - 1) % BPO;
+  return __uint_as_float(((uint32_t)e << 23) | ((uint32_t)m << BPO_SHIFT));
 }
 __device__ __forceinline__ void hist_publish(uint32_t* h, const float* ls, int t, int from, int to) {
   for (int i = from; i < to; ++i) {
     const int bk = hbucket(ls[i * BM + t]);
     if (bk == 0) continue;  // never used to raise a threshold
     atomicAdd(h + bk, 1u);
-    atomicAdd(h + HC + (bk - 1) / 32, 1u);
+    atomicAdd(h + HC + (bk - 1) / BPO, 1u);
   }
 }
 // Raise tau to the lower edge of the highest bucket B with sum_{b>=B} h[b] >= kp.
-// Two rounds of independent loads: the 9 octave counters, then the 32 fine
+// Two rounds of independent loads: the 9 octave counters, then the BPO fine
 // buckets of the octave where the running count from the top reaches kp.
 __device__ __forceinline__ void hist_refresh(const uint32_t* h, int kp, float& tau) {
   const uint4* hc = reinterpret_cast<const uint4*>(h + HC);
@@ -209,26 +213,25 @@ __device__ __forceinline__ void hist_refresh(const uint32_t* h, int kp, float& t
     sum += (int)oc[o];
   }
   if (o < 0) return;
-  if (hedge(1 + o * 32 + 31) <= tau) return;  // nothing in reach above tau
-  const uint4* hv = reinterpret_cast<const uint4*>(h + 1 + o * 32 - 1);  // 16-byte aligned block [o*32, o*32+32)
-  uint32_t f[33];
-  // fine buckets 1+o*32 .. 32+o*32 live at words o*32+1 .. o*32+32: load words o*32 .. o*32+35
-  uint4 x[9];
+  if (hedge(1 + o * BPO + BPO - 1) <= tau) return;  // nothing in reach above tau
+  // fine bucket 1 + o*BPO + jj lives at word o*BPO + 1 + jj; load words o*BPO .. o*BPO + BPO + 3
+  const uint4* hv = reinterpret_cast<const uint4*>(h + o * BPO);
+  uint4 x[BPO / 4 + 1];
 #pragma unroll
-  for (int i = 0; i < 9; ++i) x[i] = __ldcg(hv + i);
+  for (int i = 0; i < BPO / 4 + 1; ++i) x[i] = __ldcg(hv + i);
+  uint32_t f[BPO + 4];
 #pragma unroll
-  for (int i = 0; i < 9; ++i) {
-    if (4 * i + 0 <= 32) f[4 * i + 0] = x[i].x;
-    if (4 * i + 1 <= 32) f[4 * i + 1] = x[i].y;
-    if (4 * i + 2 <= 32) f[4 * i + 2] = x[i].z;
-    if (4 * i + 3 <= 32) f[4 * i + 3] = x[i].w;
+  for (int i = 0; i < BPO / 4 + 1; ++i) {
+    f[4 * i + 0] = x[i].x;
+    f[4 * i + 1] = x[i].y;
+    f[4 * i + 2] = x[i].z;
+    f[4 * i + 3] = x[i].w;
   }
-  // f[j] = word o*32 + j; fine bucket 1 + o*32 + jj is word o*32 + 1 + jj = f[1 + jj]
 #pragma unroll
-  for (int jj = 31; jj >= 0; --jj) {
+  for (int jj = BPO - 1; jj >= 0; --jj) {
     sum += (int)f[1 + jj];
     if (sum >= kp) {
-      const float e = hedge(1 + o * 32 + jj);
+      const float e = hedge(1 + o * BPO + jj);
       if (e > tau) tau = e;
       return;
     }
@@ -795,70 +798,69 @@ __device__ __forceinline__ uint32_t fkey(float f) {
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 
-// Per query: top-kp of the n_splits partial shortlists by bf16 score.
-__global__ void __launch_bounds__(256) k_shortlist_merge(const float* __restrict__ ps, const uint32_t* __restrict__ pr,
-                                                         const int32_t* __restrict__ pn, int n_splits, int kp,
-                                                         float* __restrict__ cs, uint32_t* __restrict__ cr,
-                                                         int32_t* __restrict__ cn) {
-  extern __shared__ uint32_t s_key[];  // [n_splits * kp]
-  __shared__ int s_cnt, s_gt, s_eq, s_pos;
-  const int q = blockIdx.x;
-  const size_t base = (size_t)q * n_splits * kp;
+// Per query: top-kp of the n_splits partial shortlists by bf16 score. One
+// warp per query (keys staged in smem): a 32-step binary search on the
+// order-preserving key with warp-reduced counts, then ballot compaction.
+constexpr int MG_W = 8;
+__global__ void __launch_bounds__(MG_W * 32) k_shortlist_merge(const float* __restrict__ ps, const uint32_t* __restrict__ pr,
+                                                               const int32_t* __restrict__ pn, int n_splits, int kp, int nq,
+                                                               float* __restrict__ cs, uint32_t* __restrict__ cr,
+                                                               int32_t* __restrict__ cn, uint32_t* __restrict__ gkeys) {
+  extern __shared__ uint32_t s_key[];  // [warps][n_splits * kp] (or gkeys [nq][..] when too large)
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q = blockIdx.x * (blockDim.x >> 5) + w;
+  if (q >= nq) return;
   const int total = n_splits * kp;
-  for (int i = threadIdx.x; i < total; i += blockDim.x) {
+  uint32_t* key = gkeys ? gkeys + (size_t)q * total : s_key + (size_t)w * total;
+  const size_t base = (size_t)q * total;
+  int n_items = 0;
+  for (int i = lane; i < total; i += 32) {
     const int sp = i / kp, j = i - sp * kp;
-    s_key[i] = j < pn[(size_t)q * n_splits + sp] ? fkey(ps[base + i]) : 0u;  // 0 = empty slot
+    const uint32_t k = j < pn[(size_t)q * n_splits + sp] ? fkey(ps[base + i]) : 0u;  // 0 = empty slot
+    key[i] = k;
+    n_items += k != 0u;
   }
-  if (threadIdx.x == 0) s_cnt = 0;
-  __syncthreads();
-  int mine = 0;
-  for (int i = threadIdx.x; i < total; i += blockDim.x) mine += s_key[i] != 0u;
-  atomicAdd(&s_cnt, mine);
-  __syncthreads();
-  const int n_items = s_cnt;
+  n_items = __reduce_add_sync(0xffffffffu, n_items);
+  __syncwarp();
   uint32_t T = 1;  // keep everything non-empty
   if (n_items > kp) {
     uint32_t lo = 1, hi = 0xFFFFFFFFu;
     while (lo < hi) {
       const uint32_t mid = lo + (uint32_t)(((uint64_t)hi - lo + 1) >> 1);
-      __syncthreads();
-      if (threadIdx.x == 0) s_gt = 0;
-      __syncthreads();
       int c = 0;
-      for (int i = threadIdx.x; i < total; i += blockDim.x) c += s_key[i] >= mid;
-      atomicAdd(&s_gt, c);
-      __syncthreads();
-      if (s_gt >= kp) lo = mid; else hi = mid - 1;
+      for (int i = lane; i < total; i += 32) c += key[i] >= mid;
+      c = __reduce_add_sync(0xffffffffu, c);
+      if (c >= kp) lo = mid; else hi = mid - 1;
     }
     T = lo;
   }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    s_pos = 0;
-    s_eq = 0;
-  }
-  __syncthreads();
-  // strictly above T first, then fill with == T
-  for (int i = threadIdx.x; i < total; i += blockDim.x) {
-    if (s_key[i] > T) {
-      const int at = atomicAdd(&s_pos, 1);
+  // strictly above T first (in slot order), then == T up to kp
+  int out = 0;
+  for (int i0 = 0; i0 < total; i0 += 32) {
+    const int i = i0 + lane;
+    const bool take = i < total && key[i] > T;
+    const unsigned bal = __ballot_sync(0xffffffffu, take);
+    if (take) {
+      const int at = out + __popc(bal & ((1u << lane) - 1));
       cs[(size_t)q * kp + at] = ps[base + i];
       cr[(size_t)q * kp + at] = pr[base + i];
     }
+    out += __popc(bal);
   }
-  __syncthreads();
-  const int above = s_pos;
-  for (int i = threadIdx.x; i < total; i += blockDim.x) {
-    if (s_key[i] == T && s_key[i] != 0u) {
-      const int e = atomicAdd(&s_eq, 1);
-      if (above + e < kp) {
-        cs[(size_t)q * kp + above + e] = ps[base + i];
-        cr[(size_t)q * kp + above + e] = pr[base + i];
+  for (int i0 = 0; i0 < total && out < kp; i0 += 32) {
+    const int i = i0 + lane;
+    const bool take = i < total && key[i] == T && key[i] != 0u;
+    const unsigned bal = __ballot_sync(0xffffffffu, take);
+    if (take) {
+      const int at = out + __popc(bal & ((1u << lane) - 1));
+      if (at < kp) {
+        cs[(size_t)q * kp + at] = ps[base + i];
+        cr[(size_t)q * kp + at] = pr[base + i];
       }
     }
+    out += __popc(bal);
   }
-  __syncthreads();
-  if (threadIdx.x == 0) cn[q] = min(kp, above + s_eq);
+  if (lane == 0) cn[q] = min(kp, out);
 }
 
 }  // namespace sm100
@@ -1028,10 +1030,15 @@ void approx_shortlist(lc_ctx* ctx, const ApproxPlan& plan, const float* Qdev, in
             h[2], h[0], h[0] / (double)std::max(1u, h[2]), h[1], h[1] / (double)std::max(1u, h[2]), prm.nstage, prm.bps,
             prm.cap, prm.n_splits);
   }
-  const size_t msmem = (size_t)splits * kp * sizeof(uint32_t);
+  const size_t per_warp = (size_t)splits * kp * sizeof(uint32_t);
+  const int mw = (int)std::max<size_t>(1, std::min<size_t>(MG_W, (160 * 1024) / per_warp));
+  const bool in_smem = per_warp <= 160 * 1024;
+  DevBuf gkeys(in_smem ? 16 : (size_t)nq * per_warp, ctx->stream);
+  const size_t msmem = in_smem ? (size_t)mw * per_warp : 0;
   if (msmem > 48 * 1024) FC_CUDA(cudaFuncSetAttribute(k_shortlist_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msmem));
-  k_shortlist_merge<<<nq, 256, msmem, ctx->stream>>>(ps.as<float>(), pr.as<uint32_t>(), pn.as<int32_t>(), (int)splits, kp,
-                                                      cand_s, cand_r, cand_n);
+  k_shortlist_merge<<<(nq + mw - 1) / mw, mw * 32, msmem, ctx->stream>>>(
+      ps.as<float>(), pr.as<uint32_t>(), pn.as<int32_t>(), (int)splits, kp, nq, cand_s, cand_r, cand_n,
+      in_smem ? nullptr : gkeys.as<uint32_t>());
   FC_LAUNCH_CHECK();
   count_launch(ctx, 3);
 }
