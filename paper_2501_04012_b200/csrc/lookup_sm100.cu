@@ -251,7 +251,8 @@ struct Params {
   int cap;     // candidate buffer slots per query (>= kp + 16)
   int bps;     // TMA boxes per pipeline stage
   uint32_t* gkey;  // [nq_pad] shared per-query thresholds (order keys, 0 = unset)
-  uint32_t* hist;   // [nq_pad][HB] acceptance histogram (pair kernel)
+  uint32_t* hist;   // [nq_pad][HSTRIDE] acceptance histogram (pair kernel)
+  int refresh_mask; // histogram publish/refresh every (mask + 1) tiles
   uint32_t* stats;  // FC_SHORTLIST_DEBUG & 16: [slow chunks, compactions, warp-tiles]
   int debug;   // diagnostics (FC_SHORTLIST_DEBUG): 1 = skip MMA, 2 = skip TMA, 4 = skip epilogue filter
   int nstage;
@@ -710,7 +711,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       for (int64_t row = r0; row < r1; row += PN, ++tile) {
         const uint32_t b = tile & 1;
         const uint32_t use = tile >> 1;
-        if ((tile & 15) == 0) {
+        if ((tile & p.refresh_mask) == 0) {
           hist_publish(hq, ls, t, pub, cnt);
           pub = cnt;
           hist_refresh(hq, p.kp, tau);
@@ -1008,6 +1009,10 @@ void approx_shortlist(lc_ctx* ctx, const ApproxPlan& plan, const float* Qdev, in
   DevBuf hist(pair ? (size_t)nq_pad * HSTRIDE * sizeof(uint32_t) : 16, ctx->stream);
   if (pair) FC_CUDA(cudaMemsetAsync(hist.p, 0, hist.bytes, ctx->stream));
   prm.hist = hist.as<uint32_t>();
+  {
+    const char* e = getenv("FC_SHORTLIST_REFRESH");
+    prm.refresh_mask = (e ? atoi(e) : 16) - 1;
+  }
   prm.stats = st.as<uint32_t>();
   prm.gkey = gk.as<uint32_t>();
   prm.part_s = ps.as<float>();
