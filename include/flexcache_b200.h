@@ -185,6 +185,13 @@ lc_status lc_decide_batch(lc_ctx* ctx, const uint64_t* w_ids, const double* w_sc
  * ------------------------------------------------------------------------- */
 typedef struct lc_entry lc_entry;  /* one CompressedEntry living in HBM */
 
+/* Codec instrumentation: K7 (inter_compress trial) items computed, and how
+ * many of them the certified kernel could not settle (re-run exactly). */
+typedef struct lc_codec_stats {
+  uint64_t inter_items;
+  uint64_t inter_exact_items;
+} lc_codec_stats;
+lc_status lc_codec_stats_get(lc_ctx* ctx, lc_codec_stats* out, int reset);
 /* select_keyframes (codec.cpp:138-165) for n latents [n][F][E]; map [n][F]. */
 lc_status lc_select_keyframes(lc_ctx* ctx, const float* latents, int64_t n, int F, int H, int W,
                               int C, double threshold, int32_t* map);

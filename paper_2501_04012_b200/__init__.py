@@ -489,6 +489,14 @@ def compress_batch(latents, steps, obj_masks, bg_masks, dims, prompts, threshold
     return [CompressedEntry(C.c_void_p(handles[i]), ctx) for i in range(n)], sizes
 
 
+def codec_stats(reset: bool = False, ctx=None) -> dict:
+    """K7 instrumentation: items computed and items the certified kernel
+    handed to the exact sequential kernel."""
+    st_ = _capi.CodecStats()
+    _check(lib.lc_codec_stats_get(_ctx(ctx), C.byref(st_), int(reset)))
+    return {"inter_items": int(st_.inter_items), "inter_exact_items": int(st_.inter_exact_items)}
+
+
 def compress(latent_steps, steps, obj_masks, bg_masks, dims, prompt, threshold=COMPRESS_THRESHOLD, ctx=None):
     """One prompt: latent_steps [S][F][E], masks [F][mb]."""
     lat = _host(latent_steps, np.float32)

@@ -45,6 +45,10 @@ class LookupStats(C.Structure):
                 ("max_abs_err", f64)]
 
 
+class CodecStats(C.Structure):
+    _fields_ = [("inter_items", u64), ("inter_exact_items", u64)]
+
+
 class EntryInfo(C.Structure):
     _fields_ = [("prompt", u64), ("base_step", i32), ("n_steps", i32), ("F", i32), ("H", i32), ("W", i32),
                 ("C", i32), ("n_diff", i32), ("steps", i32 * 8), ("n_extra", i32 * 8),
@@ -82,6 +86,7 @@ _sig("lc_index_export", st, vp, C.c_int, vp, vp, i64)
 _sig("lc_index_query_topk", st, vp, C.c_int, vp, i64, C.c_int, vp, vp, vp)
 _sig("lc_lookup_decide", st, vp, vp, vp, vp, i64, f64, vp, vp)
 _sig("lc_index_stats", st, vp, C.POINTER(LookupStats), C.c_int)
+_sig("lc_codec_stats_get", st, vp, C.POINTER(CodecStats), C.c_int)
 _sig("lc_index_set_lookup", st, vp, C.c_int, C.c_int, f64)
 _sig("lc_topk_merge", st, vp, vp, vp, vp, C.c_int, i64, C.c_int, vp, vp, vp)
 _sig("lc_decide_batch", st, vp, vp, vp, vp, vp, vp, vp, i64, f64, vp, vp)

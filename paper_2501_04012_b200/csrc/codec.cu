@@ -457,6 +457,309 @@ __global__ void __launch_bounds__(INTER_W * 32) k_inter(const float* __restrict_
   }
 }
 
+// ---------------------------------------------------------------------------
+// Certified K7 (k_inter_cert). The reference's sums are sequential fp64
+// chains; only two things derived from them are observable: the fp32 alphas
+// (stored in the entry) and the choice of base (argmax of the mean trial
+// similarity). Both are robust to a tiny perturbation of the sums except
+// near a rounding boundary / a near-tie, so this kernel computes every sum
+// reassociated (one block per item, all (step, base) pairs from ONE pass
+// over the 2S frames, 15 conversions + 4S^2-ish fp64 FMAs per element
+// instead of ~130 conversions) together with rigorous error bounds:
+//
+//  * alpha[s][b] = (float)(num/den) (codec.cpp:181-191). Each product of two
+//    floats is exact in fp64, so |ours - sequential| <= 2 gamma_E sum|t|
+//    (gamma_n = n u / (1 - n u), u = 2^-53), with sum|d_s d_b| <=
+//    |d_s||d_b| (Cauchy-Schwarz). The quotient interval is evaluated with
+//    directed rounding; if both ends round to the same float (bitwise), that
+//    float is the reference's alpha.
+//  * trial similarity of key m of step s under base b (codec.cpp:243-252):
+//    r = fp32(f_s + alpha d_b) differs from the exact rhat = f_s + alpha d_b by
+//    <= (2^-24 + 2^-52)|rhat_i| per element, and <rhat,k_s>, |rhat|^2 expand
+//    into sums this pass already has (<f_s,k_s>, <d_b,k_s>, <f_s,d_b>,
+//    |d_b|^2, plus the exact norms from the Gram pass). The kernel returns
+//    the approximate similarity and a bound on its distance to the
+//    reference's sequential value.
+// The host certifies the base choice from these (a base whose trial has no
+// approximate term is summed exactly); any item or prompt that cannot be
+// certified is recomputed by the exact k_inter, so results are always the
+// reference's. FC_INTER_EXACT=1 forces the exact kernel.
+struct InterCert {
+  double bound[MAXS][MAXS];  // |sim_reference - sim| <= bound (s != b, nz[b], finite alpha)
+  uint8_t cert;              // 1: every alpha certified, every needed sim bounded
+  uint8_t why;               // diagnostics: 3 overflow guard, 4 |r|^2 bound
+};
+
+constexpr int ICT = 128;         // threads per item
+constexpr int ICT_CHUNK = 1024;  // products staged per step of an exact chain replay
+
+__device__ __forceinline__ float f4c(const float4& v, int c) { return c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w; }
+
+template <int S>
+__global__ void __launch_bounds__(ICT, 2) k_inter_cert(const float* __restrict__ lat, const InterItem* __restrict__ items,
+                                                      const int* __restrict__ perm, int F, int64_t E,
+                                                      const double* __restrict__ nrm, InterRes* __restrict__ out,
+                                                      InterCert* __restrict__ cert, int force_replay) {
+  constexpr int NA = S * (S + 1) / 2;  // A[s<=b] = sum d_s d_b
+  constexpr int NP = S * (S - 1);      // P[s!=b] = sum d_b k_s ; Q[s!=b] = sum f_s d_b
+  constexpr int NV = NA + 2 * NP + S;  // + FK[s] = sum f_s k_s
+  constexpr int NW = ICT / 32;
+  __shared__ double s_red[NW][NV];
+  __shared__ float s_max[NW][2 * S];
+  __shared__ unsigned s_flag[NW][2];
+  __shared__ int s_cert, s_why;
+  __shared__ float s_alpha[S * S];
+  __shared__ int s_amb[S * S];
+  __shared__ double s_pn[ICT_CHUNK], s_pd[ICT_CHUNK], s_chain;
+  const InterItem it = items[blockIdx.x];
+  const int m = it.m;
+  const float* base = lat + (int64_t)it.entry * S * F * E;
+  const float4* kp[S];
+  const float4* fp[S];
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    kp[s] = reinterpret_cast<const float4*>(base + ((int64_t)perm[s] * F + m) * E);
+    fp[s] = reinterpret_cast<const float4*>(base + (int64_t)perm[s] * F * E);
+  }
+  double acc[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) acc[v] = 0.0;
+  unsigned nzm = 0, exm = (1u << S) - 1;
+  float mxf[S], mxd[S];
+#pragma unroll
+  for (int s = 0; s < S; ++s) mxf[s] = mxd[s] = 0.f;
+  const int64_t n4 = E >> 2;
+  for (int64_t v = threadIdx.x; v < n4; v += ICT) {
+    float4 k4[S], f4[S];
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      k4[s] = __ldg(kp[s] + v);
+      f4[s] = __ldg(fp[s] + v);
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      double dd[S], kd[S], fd[S];
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        const float k = f4c(k4[s], c), f = f4c(f4[s], c);
+        const float d = k - f;  // frame_diff (codec.cpp:33-37), fp32
+        nzm |= (d != 0.0f ? 1u : 0u) << s;
+        if (f + d != k) exm &= ~(1u << s);
+        mxf[s] = fmaxf(mxf[s], fabsf(f));
+        mxd[s] = fmaxf(mxd[s], fabsf(d));
+        dd[s] = d;
+        kd[s] = k;
+        fd[s] = f;
+      }
+      int a = 0;
+#pragma unroll
+      for (int s = 0; s < S; ++s)
+#pragma unroll
+        for (int b = s; b < S; ++b, ++a) acc[a] = fma(dd[s], dd[b], acc[a]);
+#pragma unroll
+      for (int s = 0; s < S; ++s)
+#pragma unroll
+        for (int b = 0; b < S; ++b)
+          if (b != s) {
+            acc[a] = fma(dd[b], kd[s], acc[a]);
+            ++a;
+          }
+#pragma unroll
+      for (int s = 0; s < S; ++s)
+#pragma unroll
+        for (int b = 0; b < S; ++b)
+          if (b != s) {
+            acc[a] = fma(fd[s], dd[b], acc[a]);
+            ++a;
+          }
+#pragma unroll
+      for (int s = 0; s < S; ++s, ++a) acc[a] = fma(fd[s], kd[s], acc[a]);
+    }
+  }
+  // block reduction (fixed order)
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    double x = acc[v];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0) s_red[w][v] = x;
+  }
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    float a = mxf[s], b = mxd[s];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, o));
+      b = fmaxf(b, __shfl_xor_sync(0xffffffffu, b, o));
+    }
+    if (lane == 0) {
+      s_max[w][s] = a;
+      s_max[w][S + s] = b;
+    }
+  }
+  nzm = __reduce_or_sync(0xffffffffu, nzm);
+  exm = __reduce_and_sync(0xffffffffu, exm);
+  if (lane == 0) {
+    s_flag[w][0] = nzm;
+    s_flag[w][1] = exm;
+  }
+  if (threadIdx.x == 0) s_cert = 1, s_why = 0;
+  __syncthreads();
+  if (threadIdx.x < NV) {
+    double x = 0.0;
+#pragma unroll
+    for (int q = 0; q < NW; ++q) x += s_red[q][threadIdx.x];
+    s_red[0][threadIdx.x] = x;
+  }
+  if (threadIdx.x < 2 * S) {
+    float x = 0.f;
+#pragma unroll
+    for (int q = 0; q < NW; ++q) x = fmaxf(x, s_max[q][threadIdx.x]);
+    s_max[0][threadIdx.x] = x;
+  }
+  if (threadIdx.x == 0) {
+    unsigned o = 0, e = (1u << S) - 1;
+#pragma unroll
+    for (int q = 0; q < NW; ++q) {
+      o |= s_flag[q][0];
+      e &= s_flag[q][1];
+    }
+    s_flag[0][0] = o;
+    s_flag[0][1] = e;
+  }
+  __syncthreads();
+  // ---- per (s, b) pair: certified alpha ----
+  InterRes* o = out + blockIdx.x;
+  InterCert* oc = cert + blockIdx.x;
+  const unsigned NZ = s_flag[0][0], EX = s_flag[0][1];
+  const double* R = s_red[0];
+  auto Aidx = [](int s, int b) { return s * S - s * (s - 1) / 2 + (b - s); };  // s <= b
+  auto Pidx = [](int s, int b) { return NA + s * (S - 1) + (b < s ? b : b - 1); };
+  auto Qidx = [](int s, int b) { return NA + NP + s * (S - 1) + (b < s ? b : b - 1); };
+  const double u = 0x1p-53;
+  const double gam = (double)E * u / (1.0 - (double)E * u);
+  const double eps_r = 0x1p-24 + 0x1p-52;
+  if (threadIdx.x < S * S) {
+    const int s = threadIdx.x / S, b = threadIdx.x % S;
+    float alpha = 0.0f;
+    int amb = 0;
+    if ((NZ >> b) & 1u) {
+      const double den = R[Aidx(b, b)];
+      if (s == b) {
+        alpha = 1.0f;  // num == den bitwise in the reference (same chain); unused
+      } else {
+        const double num = R[s < b ? Aidx(s, b) : Aidx(b, s)];
+        const double dss = R[Aidx(s, s)];
+        const double tn = sqrt(dss) * sqrt(den) * (1.0 + 8.0 * gam) + 0x1p-1000;
+        const double en = 2.0 * gam * tn * (1.0 + 1e-9);
+        const double ed = 2.0 * gam * den * (1.0 + 1e-9);
+        const double nl = __dsub_rd(num, en), nh = __dadd_ru(num, en);
+        const double dl = __dsub_rd(den, ed), dh = __dadd_ru(den, ed);
+        if (!(dl > 0.0)) {
+          amb = 1;
+        } else {
+          const double qlo = fmin(__ddiv_rd(nl, dl), __ddiv_rd(nl, dh));
+          const double qhi = fmax(__ddiv_ru(nh, dl), __ddiv_ru(nh, dh));
+          const float flo = __double2float_rn(qlo), fhi = __double2float_rn(qhi);
+          if (__float_as_uint(flo) != __float_as_uint(fhi) || force_replay) amb = 1;
+          alpha = flo;
+        }
+      }
+    }
+    s_alpha[threadIdx.x] = alpha;
+    s_amb[threadIdx.x] = amb;
+  }
+  __syncthreads();
+  // Ambiguous alphas (the interval straddles a float rounding boundary; ~1
+  // item in 400 on the synthetic latents): replay the reference's sequential
+  // chains num = sum d_s d_b, den = sum d_b^2 (codec.cpp:185-188). All
+  // threads form the exact fp64 products of a chunk in smem; one thread per
+  // chain adds them in element order.
+  for (int pr = 0; pr < S * S; ++pr) {
+    if (!s_amb[pr]) continue;  // block-uniform
+    const int s = pr / S, b = pr % S;
+    const float* ks = base + ((int64_t)perm[s] * F + m) * E;
+    const float* fs = base + (int64_t)perm[s] * F * E;
+    const float* kb = base + ((int64_t)perm[b] * F + m) * E;
+    const float* fb = base + (int64_t)perm[b] * F * E;
+    double cn = 0.0, cd = 0.0;
+    for (int64_t i0 = 0; i0 < E; i0 += ICT_CHUNK) {
+      for (int t = threadIdx.x; t < ICT_CHUNK && i0 + t < E; t += ICT) {
+        const float ds = ks[i0 + t] - fs[i0 + t], db = kb[i0 + t] - fb[i0 + t];
+        s_pn[t] = (double)ds * (double)db;
+        s_pd[t] = (double)db * (double)db;
+      }
+      __syncthreads();
+      const int lim = (int)(E - i0 < ICT_CHUNK ? E - i0 : ICT_CHUNK);
+      if (threadIdx.x == 0)
+        for (int t = 0; t < lim; ++t) cn += s_pn[t];
+      if (threadIdx.x == 32)
+        for (int t = 0; t < lim; ++t) cd += s_pd[t];
+      __syncthreads();
+    }
+    if (threadIdx.x == 32) s_chain = cd;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      s_alpha[pr] = (float)(cn / s_chain);
+      s_amb[pr] = 0;
+    }
+    __syncthreads();
+  }
+  // ---- per (s, b) pair: approximate trial similarity + bound ----
+  if (threadIdx.x < S * S) {
+    const int s = threadIdx.x / S, b = threadIdx.x % S;
+    const bool nzb = (NZ >> b) & 1u;
+    const float alpha = s_alpha[threadIdx.x];
+    double sim = 0.0, bound = 0.0;
+    bool ok = true;
+    int why = 0;
+    if (nzb && s != b && isfinite(alpha)) {
+      const double den = R[Aidx(b, b)];
+      const double a = (double)alpha;
+      // r must stay finite (else the reference throws; the exact path reports it)
+      if ((double)s_max[0][s] + fabs(a) * (double)s_max[0][S + b] >= 1.0e38) ok = false, why = 3;
+      const double ff = nrm[((int64_t)it.entry * S + perm[s]) * F + 0];  // |f_s|^2, exact
+      const double kk = nrm[((int64_t)it.entry * S + perm[s]) * F + m];  // |k_s|^2, exact
+      const double dot = R[NA + 2 * NP + s] + a * R[Pidx(s, b)];
+      const double na = ff + 2.0 * a * R[Qidx(s, b)] + a * a * den;
+      const double K = sqrt(kk);
+      const double Mx = sqrt(ff) + fabs(a) * sqrt(den);
+      const double tiny = 0x1p-140 * sqrt((double)E);
+      const double rh = sqrt(fmax(na, 0.0) + 8.0 * gam * Mx * Mx) + tiny;  // >= |rhat|
+      const double eta_na = 8.0 * gam * Mx * Mx + (2.0 * eps_r + eps_r * eps_r) * rh * rh + 4.0 * tiny * rh;
+      const double eta_dot = 8.0 * gam * Mx * K + (eps_r * rh + tiny) * K;
+      const double nlo = na - eta_na, nhi = na + eta_na;
+      if (!(nlo > 0.0)) {
+        ok = false, why = 4;
+      } else if (kk == 0.0) {
+        sim = 0.0;  // safe_similarity: na != 0, nb == 0
+      } else {
+        sim = dot / (sqrt(na) * K);
+        bound = (eta_dot / sqrt(nlo) + (fabs(dot) + eta_dot) * (1.0 / sqrt(nlo) - 1.0 / sqrt(nhi))) / K;
+        bound = bound * 1.01 + 16.0 * u * (fabs(sim) + 1.0);
+      }
+    }
+    if (!ok) {
+      s_cert = 0;
+      atomicMax(&s_why, why);
+    }
+    o->alpha[s][b] = alpha;
+    o->sim[s][b] = sim;
+    o->nonfinite[s][b] = 0;
+    oc->bound[s][b] = bound;
+    if (s == b) {
+      o->nz[s] = nzb;
+      o->exact[s] = (EX >> s) & 1u;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    oc->cert = (uint8_t)s_cert;
+    oc->why = (uint8_t)s_why;
+  }
+}
+
 struct FrameJob {
   float* dst;
   const float* src;
@@ -821,39 +1124,183 @@ void assemble(lc_ctx* ctx, const float* lat, const uint8_t* om, const uint8_t* b
   FC_CUDA(cudaMemcpyAsync(diag.data(), nrm_dev, diag.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   sync(ctx);
   tr.mark("common keys + diag D2H");
-  // K7 over all (entry, common key) items
+  // K7 over all (entry, common key) items: certified kernel first (S <= 5),
+  // exact sequential kernel for whatever it cannot certify
   PinnedBuf<InterRes> res(items.size());
-  if (!items.empty()) {
+  std::vector<int> best_base(n, -1);
+  auto identical_sim = [](double ss) { return ss == 0.0 ? 1.0 : ss / (std::sqrt(ss) * std::sqrt(ss)); };
+  const bool vec4 = (E & 3) == 0 && (reinterpret_cast<uintptr_t>(lat) & 15) == 0;
+  const bool try_cert = !items.empty() && S >= 1 && S <= 5 && vec4 &&
+                        !(getenv("FC_INTER_EXACT") && atoi(getenv("FC_INTER_EXACT")) == 1);
+  DevBuf dp(S * sizeof(int), ctx->stream);
+  FC_CUDA(cudaMemcpyAsync(dp.p, perm.data(), dp.bytes, cudaMemcpyHostToDevice, ctx->stream));
+  auto run_exact = [&](const std::vector<int>& which) {  // item indices
+    if (which.empty()) return;
+    std::vector<InterItem> sub(which.size());
+    for (size_t t = 0; t < which.size(); ++t) sub[t] = items[which[t]];
+    DevBuf di(sub.size() * sizeof(InterItem), ctx->stream), dr(sub.size() * sizeof(InterRes), ctx->stream);
+    PinnedBuf<InterItem> items_h(sub.size());
+    PinnedBuf<InterRes> rs(sub.size());
+    memcpy(items_h.data(), sub.data(), sub.size() * sizeof(InterItem));
+    FC_CUDA(cudaMemcpyAsync(di.p, items_h.data(), di.bytes, cudaMemcpyHostToDevice, ctx->stream));
+    {
+      KTimer kt(ctx, "inter");
+      const unsigned nblk = (unsigned)((sub.size() + INTER_W - 1) / INTER_W);
+      k_inter<<<nblk, INTER_W * 32, 0, ctx->stream>>>(lat, di.as<InterItem>(), (int)sub.size(), S, dp.as<int>(), F, E,
+                                                      nrm_dev, dr.as<InterRes>());
+    }
+    FC_LAUNCH_CHECK();
+    count_launch(ctx);
+    FC_CUDA(cudaMemcpyAsync(rs.data(), dr.p, dr.bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    sync(ctx);
+    for (size_t t = 0; t < which.size(); ++t) res[which[t]] = rs[t];
+  };
+  PinnedBuf<InterCert> cres(try_cert ? items.size() : 0);
+  if (try_cert) {
     DevBuf di(items.size() * sizeof(InterItem), ctx->stream), dr(items.size() * sizeof(InterRes), ctx->stream),
-        dp(S * sizeof(int), ctx->stream);
+        dc(items.size() * sizeof(InterCert), ctx->stream);
     PinnedBuf<InterItem> items_h(items.size());
     memcpy(items_h.data(), items.data(), items.size() * sizeof(InterItem));
     FC_CUDA(cudaMemcpyAsync(di.p, items_h.data(), di.bytes, cudaMemcpyHostToDevice, ctx->stream));
-    FC_CUDA(cudaMemcpyAsync(dp.p, perm.data(), dp.bytes, cudaMemcpyHostToDevice, ctx->stream));
-    KTimer kt(ctx, "inter");
-    const unsigned nblk = (unsigned)((items.size() + INTER_W - 1) / INTER_W);
-    k_inter<<<nblk, INTER_W * 32, 0, ctx->stream>>>(lat, di.as<InterItem>(), (int)items.size(), S, dp.as<int>(), F, E,
-                                                    nrm_dev, dr.as<InterRes>());
+    // FC_INTER_REPLAY=1 (tests): treat every alpha as ambiguous -> exact chain replay
+    const int force_replay = getenv("FC_INTER_REPLAY") && atoi(getenv("FC_INTER_REPLAY")) == 1;
+    {
+      KTimer kt(ctx, "inter");
+      const unsigned nb = (unsigned)items.size();
+      auto args = [&](auto kern) {
+        kern<<<nb, ICT, 0, ctx->stream>>>(lat, di.as<InterItem>(), dp.as<int>(), F, E, nrm_dev, dr.as<InterRes>(),
+                                          dc.as<InterCert>(), force_replay);
+      };
+      switch (S) {
+        case 1: args(k_inter_cert<1>); break;
+        case 2: args(k_inter_cert<2>); break;
+        case 3: args(k_inter_cert<3>); break;
+        case 4: args(k_inter_cert<4>); break;
+        default: args(k_inter_cert<5>); break;
+      }
+    }
     FC_LAUNCH_CHECK();
     count_launch(ctx);
     FC_CUDA(cudaMemcpyAsync(res.data(), dr.p, dr.bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    FC_CUDA(cudaMemcpyAsync(cres.data(), dc.p, dc.bytes, cudaMemcpyDeviceToHost, ctx->stream));
     sync(ctx);
+  } else {
+    std::vector<int> all(items.size());
+    std::iota(all.begin(), all.end(), 0);
+    run_exact(all);
+    ctx->inter_exact_items += items.size();
   }
+  ctx->inter_items += items.size();
   tr.mark("k_inter + D2H");
-  auto identical_sim = [](double ss) { return ss == 0.0 ? 1.0 : ss / (std::sqrt(ss) * std::sqrt(ss)); };
-  // ---- per entry: base selection + assembly metadata ----
+  // Base choice (codec.cpp:240-259): mean per-frame similarity summed in the
+  // reference's (step, frame) order, strict '>' over ascending steps. With
+  // certified results each approximate term carries a bound; the choice is
+  // accepted only if it cannot change within the bounds (returns -1 then).
+  auto choose_base = [&](int64_t e, bool with_bounds) -> int {
+    if (S == 1) return 0;
+    const int i0 = item_begin[e], i1 = item_begin[e + 1];
+    std::vector<int> idx(F, -1);
+    for (int c = i0; c < i1; ++c) idx[items[c].m] = c;
+    auto mapv = [&](int si, int j) { return maps_h[((size_t)e * S + perm[si]) * F + j]; };
+    auto dg = [&](int si, int m) { return diag[((size_t)e * S + perm[si]) * F + m]; };
+    if (with_bounds)
+      for (int c = i0; c < i1; ++c)
+        if (!cres[c].cert) return -1;
+    // a non-finite trial reconstruction makes decompress_step throw
+    for (int c = i0; c < i1; ++c)
+      for (int b = 0; b < S; ++b)
+        for (int si = 0; si < S; ++si)
+          if (si != b && res[c].nz[b] && std::isfinite(res[c].alpha[si][b]) && res[c].nonfinite[si][b])
+            raise(LC_ERR_INVALID_ARGUMENT, "Frame: non-finite element");
+    std::vector<double> isim((size_t)S * F, 0.0);
+    for (int si = 0; si < S; ++si)
+      for (int j = 0; j < F; ++j) {
+        const int m = mapv(si, j);
+        if (m == j) isim[(size_t)si * F + m] = identical_sim(dg(si, m));
+      }
+    const double u = 0x1p-53;
+    const double cnt = (double)S * F;
+    const double gam = cnt * u / (1.0 - cnt * u);
+    double score[MAXS], bnd[MAXS];
+    int best_b = 0;
+    double best_score = -2.0;
+    for (int b = 0; b < S; ++b) {
+      double sum = 0.0, bsum = 0.0, asum = 0.0;
+      int napprox = 0;
+      for (int si = 0; si < S; ++si) {
+        for (int j = 0; j < F; ++j) {
+          const int m = mapv(si, j);
+          const int c = m > 0 ? idx[m] : -1;
+          const InterRes* r = c >= 0 ? &res[c] : nullptr;
+          double sim;
+          if (r && r->nz[b] && si != b && std::isfinite(r->alpha[si][b])) {
+            sim = r->sim[si][b];
+            if (with_bounds) {
+              bsum += cres[c].bound[si][b];
+              ++napprox;
+            }
+          } else {
+            sim = isim[(size_t)si * F + m];
+          }
+          sum += sim;
+          asum += std::fabs(sim);
+        }
+      }
+      score[b] = sum / cnt;
+      bnd[b] = napprox == 0 ? 0.0
+                            : ((bsum + 2.0 * gam * (asum + bsum)) / cnt) * (1.0 + 8.0 * u) + 8.0 * u * (std::fabs(score[b]) + 1.0);
+      if (score[b] > best_score) {
+        best_score = score[b];
+        best_b = b;
+      }
+    }
+    if (with_bounds) {
+      const double lo = score[best_b] - bnd[best_b];
+      for (int b = 0; b < S; ++b) {
+        if (b == best_b) continue;
+        const double hi = score[b] + bnd[b];
+        if (b < best_b ? !(hi < lo) : !(hi <= lo)) return -1;
+      }
+    }
+    return best_b;
+  };
+  if (try_cert) {
+    std::vector<char> need(n, 0);
+    parallel_for(n, [&](int64_t e) {
+      best_base[e] = choose_base(e, true);
+      need[e] = best_base[e] < 0;
+    });
+    std::vector<int> redo;
+    for (int64_t e = 0; e < n; ++e)
+      if (need[e])
+        for (int c = item_begin[e]; c < item_begin[e + 1]; ++c) redo.push_back(c);
+    ctx->inter_exact_items += redo.size();
+    if (tr.on) {
+      int nwhy[5] = {0, 0, 0, 0, 0}, ncert = 0, nprompt = 0;
+      for (size_t c = 0; c < items.size(); ++c) {
+        ncert += cres[c].cert;
+        nwhy[std::min<int>(cres[c].why, 4)]++;
+      }
+      for (int64_t e = 0; e < n; ++e) nprompt += need[e];
+      fprintf(stderr, "[compress] K7 cert: %d/%zu items certified (why: ovf %d nr %d), %d/%lld prompts exact\n",
+              ncert, items.size(), nwhy[3], nwhy[4], nprompt, (long long)n);
+    }
+    run_exact(redo);
+    for (int64_t e = 0; e < n; ++e)
+      if (need[e]) best_base[e] = choose_base(e, false);
+  } else {
+    parallel_for(n, [&](int64_t e) { best_base[e] = choose_base(e, false); });
+  }
+  tr.mark("base choice");
+  // ---- per entry: assembly metadata ----
   std::vector<std::shared_ptr<EntryData>> ents(n);
   PinnedBuf<FrameJob> fjobs;
   PinnedBuf<ByteJob> bjobs;
   PinnedBuf<Recipe> all_recipes;
   std::vector<std::pair<size_t, size_t>> recipe_span(n);
-  std::vector<int> best_base(n, 0);
   parallel_for(n, [&](int64_t e) {
     const auto& cm = common[e];
     const int i0 = item_begin[e];
-    // direct (m -> K7 item) index; identical-frame similarity per (step, key)
-    // computed once instead of per (base, frame) (this loop was ~13 ms of host
-    // time for 256 entries)
     std::vector<int> idx(F, -1);
     for (int c = i0; c < item_begin[e + 1]; ++c) idx[items[c].m] = c;
     std::vector<char> is_common(F, 0);
@@ -861,45 +1308,7 @@ void assemble(lc_ctx* ctx, const float* lat, const uint8_t* om, const uint8_t* b
     auto in_common = [&](int m) { return is_common[m] != 0; };
     auto item_of = [&](int m) -> const InterRes* { return idx[m] >= 0 ? &res[idx[m]] : nullptr; };
     auto mapv = [&](int si, int j) { return maps_h[((size_t)e * S + perm[si]) * F + j]; };
-    auto dg = [&](int si, int m) { return diag[((size_t)e * S + perm[si]) * F + m]; };
-    // choose base (codec.cpp:240-259); a single step is its own base
-    int best_b = 0;
-    if (S > 1) {
-      // a non-finite trial reconstruction makes decompress_step throw
-      for (int c = i0; c < item_begin[e + 1]; ++c)
-        for (int b = 0; b < S; ++b)
-          for (int si = 0; si < S; ++si)
-            if (si != b && res[c].nz[b] && std::isfinite(res[c].alpha[si][b]) && res[c].nonfinite[si][b])
-              raise(LC_ERR_INVALID_ARGUMENT, "Frame: non-finite element");
-      std::vector<double> isim((size_t)S * F, 0.0);
-      for (int si = 0; si < S; ++si)
-        for (int j = 0; j < F; ++j) {
-          const int m = mapv(si, j);
-          if (m == j) isim[(size_t)si * F + m] = identical_sim(dg(si, m));
-        }
-      double best_score = -2.0;
-      for (int b = 0; b < S; ++b) {
-        // mean per-frame similarity, summed in the reference's (step, frame) order
-        double sum = 0.0;
-        uint64_t count = 0;
-        for (int si = 0; si < S; ++si) {
-          for (int j = 0; j < F; ++j) {
-            const int m = mapv(si, j);
-            const InterRes* r = m > 0 ? item_of(m) : nullptr;
-            double sim;
-            if (r && r->nz[b] && si != b && std::isfinite(r->alpha[si][b])) sim = r->sim[si][b];
-            else sim = isim[(size_t)si * F + m];
-            sum += sim;
-            ++count;
-          }
-        }
-        const double score = sum / (double)count;
-        if (score > best_score) {
-          best_score = score;
-          best_b = b;
-        }
-      }
-    }
+    const int best_b = best_base[e];
     auto d = std::make_shared<EntryData>();
     d->ctx = ctx;
     d->prompt = prompts[e];
@@ -958,7 +1367,6 @@ void assemble(lc_ctx* ctx, const float* lat, const uint8_t* om, const uint8_t* b
     d->recipe_off = bytes;
     bytes += (int64_t)S * F * sizeof(Recipe);
     d->dev_bytes = (size_t)bytes;
-    best_base[e] = best_b;
     ents[e] = d;
   });
   tr.mark("host: base + metadata");
@@ -1185,6 +1593,20 @@ lc_status lc_select_keyframes(lc_ctx* ctx, const float* latents, int64_t n, int 
   select_cert(ctx, G.as<double>(), NR.as<double>(), lat.dev, (int)n, g, thr, delta, om.dev, bad.as<int>());
   om.finish(ctx);
   if (check_flag(ctx, bad)) raise(LC_ERR_INVALID_ARGUMENT, "cosine_similarity: zero-norm operand");
+  LC_API_END
+}
+
+lc_status lc_codec_stats_get(lc_ctx* ctx, lc_codec_stats* out, int reset) {
+  LC_API_BEGIN
+  FC_REQUIRE(ctx != nullptr, "null context");
+  if (out) {
+    out->inter_items = ctx->inter_items.load();
+    out->inter_exact_items = ctx->inter_exact_items.load();
+  }
+  if (reset) {
+    ctx->inter_items = 0;
+    ctx->inter_exact_items = 0;
+  }
   LC_API_END
 }
 

@@ -71,6 +71,8 @@ struct lc_ctx {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   std::atomic<uint64_t> launches{0};
+  // codec instrumentation (lc_codec_stats)
+  std::atomic<uint64_t> inter_items{0}, inter_exact_items{0};
   // per-kernel CUDA-event timing (lc_ctx_profile / lc_ctx_kernel_time)
   bool profile = false;
   std::mutex prof_mu;

@@ -236,3 +236,59 @@ def test_tensor_core_gram_equals_exact_gram_path(fc, synth):
         del os.environ["FC_GRAM_EXACT"]
     for x, y in zip(a, b):
         assert x.serialize() == y.serialize()
+
+
+def test_certified_inter_equals_exact_path(fc, orc, synth):
+    """The certified K7 (reassociated sums + bounds) must give the same
+    entries as the sequential-fp64 K7 (FC_INTER_EXACT=1) and the oracle; on
+    the synthetic generator every item is settled without the exact kernel."""
+    dims = (40, 64, 4)
+    n = 6
+    lat = np.stack([synth.latents(90 + i, F=64, dims=dims) for i in range(n)])
+    masks = [synth.rect_masks(64, 40, 64, 90 + i) for i in range(n)]
+    om = np.stack([m[0] for m in masks])
+    bm = np.stack([m[1] for m in masks])
+    fc.codec_stats(reset=True)
+    a, sa = fc.compress_batch(lat, synth.CACHED_STEPS, om, bm, dims, list(range(n)))
+    st = fc.codec_stats(reset=True)
+    assert st["inter_items"] > 0 and st["inter_exact_items"] == 0, st
+    os.environ["FC_INTER_EXACT"] = "1"
+    try:
+        b, sb = fc.compress_batch(lat, synth.CACHED_STEPS, om, bm, dims, list(range(n)))
+    finally:
+        del os.environ["FC_INTER_EXACT"]
+    assert fc.codec_stats()["inter_exact_items"] == st["inter_items"]
+    for i, (x, y) in enumerate(zip(a, b)):
+        assert x.serialize() == y.serialize()
+    # every alpha through the in-kernel sequential chain replay
+    os.environ["FC_INTER_REPLAY"] = "1"
+    try:
+        c, _ = fc.compress_batch(lat, synth.CACHED_STEPS, om, bm, dims, list(range(n)))
+    finally:
+        del os.environ["FC_INTER_REPLAY"]
+    for x, y in zip(a, c):
+        assert x.serialize() == y.serialize()
+    for i in (0, n - 1):
+        assert a[i].serialize() == orc.compress(lat[i], synth.CACHED_STEPS, om[i], bm[i], dims, i)
+
+
+def test_certified_inter_ties_fall_back(fc, orc, synth):
+    """Steps that are exact copies make every trial base score identical (the
+    reference keeps the first by strict '>'); the bounds cannot separate
+    them, so those prompts must go through the exact kernel. Mixed with
+    ordinary prompts in one batch."""
+    dims = (40, 64, 4)
+    F = 16
+    one = synth.latents(7, F=F, dims=dims)
+    tie = np.stack([one[0]] * 5)                     # five identical steps
+    tie2 = np.stack([one[0] * np.float32(1.0 + 2.0 ** -20 * s) for s in range(5)])  # near-identical
+    lat = np.stack([synth.latents(8, F=F, dims=dims), tie, tie2])
+    om, bm = synth.rect_masks(F, 40, 64, 8)
+    om = np.stack([om] * 3)
+    bm = np.stack([bm] * 3)
+    fc.codec_stats(reset=True)
+    ents, _ = fc.compress_batch(lat, synth.CACHED_STEPS, om, bm, dims, [1, 2, 3])
+    st = fc.codec_stats(reset=True)
+    assert st["inter_exact_items"] > 0, st
+    for i in range(3):
+        assert ents[i].serialize() == orc.compress(lat[i], synth.CACHED_STEPS, om[i], bm[i], dims, i + 1), i
