@@ -28,6 +28,9 @@
 #include <numeric>
 #include <thread>
 #include <mutex>
+#include <atomic>
+#include <condition_variable>
+#include <functional>
 
 #include "entry.hpp"
 
@@ -143,11 +146,15 @@ __global__ void __launch_bounds__(64) k_gram(const float* __restrict__ lat, int 
     }
 }
 
-// Sequential fp64 dot in element order (core.cpp:104-110); float4 loads run
-// ahead of the dependent FMA chain.
-__device__ __forceinline__ double exact_dot(const float* __restrict__ a, const float* __restrict__ b, int64_t E) {
-  double dot = 0.0;
-  int64_t i = 0;
+// cosine_similarity (core.cpp:101-119): dot, na, nb as sequential fp64
+// chains in element order, dot / (sqrt(na) * sqrt(nb)).
+__device__ __forceinline__ double exact_cos(const float* __restrict__ a, const float* __restrict__ b, int64_t E) {
+  double dot = 0.0, na = 0.0, nb = 0.0;
+  auto step = [&](float x, float y) {
+    dot = fma((double)x, (double)y, dot);
+    na = fma((double)x, (double)x, na);
+    nb = fma((double)y, (double)y, nb);
+  };
   if ((E & 3) == 0 && ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15) == 0) {
     const float4* a4 = reinterpret_cast<const float4*>(a);
     const float4* b4 = reinterpret_cast<const float4*>(b);
@@ -163,21 +170,35 @@ __device__ __forceinline__ double exact_dot(const float* __restrict__ a, const f
 #pragma unroll
       for (int u = 0; u < 4; ++u)
         if (q + u < n4) {
-          dot = fma((double)va[u].x, (double)vb[u].x, dot);
-          dot = fma((double)va[u].y, (double)vb[u].y, dot);
-          dot = fma((double)va[u].z, (double)vb[u].z, dot);
-          dot = fma((double)va[u].w, (double)vb[u].w, dot);
+          step(va[u].x, vb[u].x);
+          step(va[u].y, vb[u].y);
+          step(va[u].z, vb[u].z);
+          step(va[u].w, vb[u].w);
         }
     }
-    return dot;
+  } else {
+    for (int64_t i = 0; i < E; ++i) step(a[i], b[i]);
   }
-  for (; i < E; ++i) dot = fma((double)a[i], (double)b[i], dot);
-  return dot;
+  return dot / (sqrt(na) * sqrt(nb));
+}
+
+// Exact sequential squared norms (core.cpp:104-110 order) of every frame of
+// the listed items: one block per item, one thread per frame.
+__global__ void k_exact_norms(const float* __restrict__ lat, const int32_t* __restrict__ item_ids, int F, int64_t E,
+                              double* __restrict__ nrm) {
+  const int64_t item = item_ids[blockIdx.x];
+  for (int j = threadIdx.x; j < F; j += blockDim.x) {
+    const float* x = lat + (item * F + j) * E;
+    double acc = 0.0;
+    for (int64_t i = 0; i < E; ++i) acc = fma((double)x[i], (double)x[i], acc);
+    nrm[item * F + j] = acc;
+  }
 }
 
 // select_keyframes (codec.cpp:138-165) from an APPROXIMATE Gram with a
 // certified bound (gram_sm100.cu): a(j,k) = G~(j,k) / (sqrt(n_j) sqrt(n_k))
-// with exact norms satisfies |a - s| <= delta, s = the reference's
+// with the (reassociated, relative error <= 2 gamma_E ~ 2e-12) norms satisfies
+// |a - s| <= delta, s = the reference's
 // frame_similarity. For frame j and the current keys: if no key has
 // a >= thr - delta, j is certainly a key; if one key has a >= thr + delta
 // and every other candidate a < a_best - 2 delta, it is certainly the
@@ -263,7 +284,7 @@ __global__ void __launch_bounds__(128) k_select_cert(const double* __restrict__ 
           const bool mine = t < nk && sim[t] >= thr - delta;
           if (mine) {
             const int k = keys[t];
-            sim[t] = exact_dot(X + (int64_t)j * E, X + (int64_t)k * E, E) / (sj * sqrt(nr[k]));
+            sim[t] = exact_cos(X + (int64_t)j * E, X + (int64_t)k * E, E);
           }
           if (mine) atomicAdd(n_exact, 1u);
         }
@@ -719,8 +740,8 @@ __global__ void __launch_bounds__(ICT, 2) k_inter_cert(const float* __restrict__
       const double a = (double)alpha;
       // r must stay finite (else the reference throws; the exact path reports it)
       if ((double)s_max[0][s] + fabs(a) * (double)s_max[0][S + b] >= 1.0e38) ok = false, why = 3;
-      const double ff = nrm[((int64_t)it.entry * S + perm[s]) * F + 0];  // |f_s|^2, exact
-      const double kk = nrm[((int64_t)it.entry * S + perm[s]) * F + m];  // |k_s|^2, exact
+      const double ff = nrm[((int64_t)it.entry * S + perm[s]) * F + 0];  // |f_s|^2 (Gram pass)
+      const double kk = nrm[((int64_t)it.entry * S + perm[s]) * F + m];  // |k_s|^2 (Gram pass)
       const double dot = R[NA + 2 * NP + s] + a * R[Pidx(s, b)];
       const double na = ff + 2.0 * a * R[Qidx(s, b)] + a * a * den;
       const double K = sqrt(kk);
@@ -737,7 +758,8 @@ __global__ void __launch_bounds__(ICT, 2) k_inter_cert(const float* __restrict__
       } else {
         sim = dot / (sqrt(na) * K);
         bound = (eta_dot / sqrt(nlo) + (fabs(dot) + eta_dot) * (1.0 / sqrt(nlo) - 1.0 / sqrt(nhi))) / K;
-        bound = bound * 1.01 + 16.0 * u * (fabs(sim) + 1.0);
+        // + kk (and ff) come from reassociated norms: relative error <= 2 gamma
+        bound = bound * 1.01 + 4.0 * gam * fabs(sim) + 16.0 * u * (fabs(sim) + 1.0);
       }
     }
     if (!ok) {
@@ -1060,36 +1082,95 @@ void select_cert(lc_ctx* ctx, const double* G, const double* nrm, const float* l
   }
 }
 
-// Runs body(e) for e in [0, n) on up to 16 host threads (independent
-// per-entry work); the first exception is rethrown on the caller's thread.
+// Persistent host worker pool for the per-entry orchestration (spawning 16
+// std::threads per phase cost ~0.1-0.2 ms each). Workers sleep on a condition
+// variable; a job is (n, body) with an atomic index; the caller participates.
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool* p = new HostPool();  // immortal: no join at static destruction
+    return *p;
+  }
+  int workers() const { return (int)th_.size(); }
+  void run(int64_t n, const std::function<void(int64_t)>& body) {
+    std::lock_guard<std::mutex> serial(run_mu_);  // one job at a time
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      body_ = &body;
+      n_ = n;
+      next_.store(0);
+      active_ = (int)th_.size();
+      err_ = nullptr;
+      ++gen_;
+    }
+    cv_.notify_all();
+    work();
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [&] { return active_ == 0; });
+    body_ = nullptr;
+    if (err_) std::rethrow_exception(err_);
+  }
+
+ private:
+  HostPool() {
+    const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+    const int nt = std::min(hw, 16) - 1;
+    for (int t = 0; t < nt; ++t)
+      th_.emplace_back([this] {
+        uint64_t seen = 0;
+        for (;;) {
+          {
+            std::unique_lock<std::mutex> lk(mu_);
+            cv_.wait(lk, [&] { return gen_ != seen; });
+            seen = gen_;
+          }
+          work();
+          std::lock_guard<std::mutex> lk(mu_);
+          if (--active_ == 0) done_cv_.notify_all();
+        }
+      });
+    for (auto& t : th_) t.detach();
+  }
+  void work() {
+    const std::function<void(int64_t)>* body = body_;
+    for (;;) {
+      const int64_t e = next_.fetch_add(1);
+      if (e >= n_) return;
+      try {
+        (*body)(e);
+      } catch (...) {
+        std::lock_guard<std::mutex> lk(err_mu_);
+        if (!err_) err_ = std::current_exception();
+      }
+    }
+  }
+  std::vector<std::thread> th_;
+  std::mutex run_mu_, mu_, err_mu_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(int64_t)>* body_ = nullptr;
+  int64_t n_ = 0;
+  std::atomic<int64_t> next_{0};
+  int active_ = 0;
+  uint64_t gen_ = 0;
+  std::exception_ptr err_ = nullptr;
+};
+
+// Runs body(e) for e in [0, n) on the host pool (inline for small n); the
+// first exception is rethrown on the caller's thread.
 template <class Body>
 void parallel_for(int64_t n, Body body) {
-  const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
-  const int nt = (int)std::min<int64_t>(std::min(hw, 16), std::max<int64_t>(1, n / 8));
-  if (nt <= 1) {
+  if (n < 16 || HostPool::get().workers() == 0) {
     for (int64_t e = 0; e < n; ++e) body(e);
     return;
   }
-  std::exception_ptr err = nullptr;
-  std::mutex mu;
-  std::vector<std::thread> th;
-  for (int t = 0; t < nt; ++t)
-    th.emplace_back([&, t] {
-      try {
-        for (int64_t e = t; e < n; e += nt) body(e);
-      } catch (...) {
-        std::lock_guard<std::mutex> lk(mu);
-        if (!err) err = std::current_exception();
-      }
-    });
-  for (auto& x : th) x.join();
-  if (err) std::rethrow_exception(err);
+  const std::function<void(int64_t)> f = body;
+  HostPool::get().run(n, f);
 }
 
 // Builds entries for n prompts given maps (host, [n][S][F] in input step
 // order) and the device Gram diagonals. Writes out[i], sizes[i].
 void assemble(lc_ctx* ctx, const float* lat, const uint8_t* om, const uint8_t* bm, const std::vector<int32_t>& steps_in,
-              const Geo& g, const int32_t* maps_h, const double* nrm_dev, const uint64_t* prompts, int64_t n,
+              const Geo& g, const int32_t* maps_h, double* nrm_dev, bool norms_exact, const uint64_t* prompts, int64_t n,
               lc_entry** out, uint64_t* sizes) {
   const int S = (int)steps_in.size();
   const int F = g.F;
@@ -1134,6 +1215,24 @@ void assemble(lc_ctx* ctx, const float* lat, const uint8_t* om, const uint8_t* b
                         !(getenv("FC_INTER_EXACT") && atoi(getenv("FC_INTER_EXACT")) == 1);
   DevBuf dp(S * sizeof(int), ctx->stream);
   FC_CUDA(cudaMemcpyAsync(dp.p, perm.data(), dp.bytes, cudaMemcpyHostToDevice, ctx->stream));
+  // exact sequential norms of every frame of the given prompts (the exact
+  // K7 and the exact base choice need the reference's values), into nrm_dev
+  // and the host copy
+  auto exact_norms = [&](const std::vector<int64_t>& prompts_e) {
+    if (norms_exact || prompts_e.empty()) return;
+    std::vector<int32_t> ids;
+    for (int64_t e : prompts_e)
+      for (int si = 0; si < S; ++si) ids.push_back((int32_t)(e * S + si));
+    DevBuf dids(ids.size() * sizeof(int32_t), ctx->stream);
+    FC_CUDA(cudaMemcpyAsync(dids.p, ids.data(), dids.bytes, cudaMemcpyHostToDevice, ctx->stream));
+    k_exact_norms<<<(unsigned)ids.size(), 64, 0, ctx->stream>>>(lat, dids.as<int32_t>(), F, E, nrm_dev);
+    FC_LAUNCH_CHECK();
+    count_launch(ctx);
+    for (int32_t id : ids)
+      FC_CUDA(cudaMemcpyAsync(diag.data() + (size_t)id * F, nrm_dev + (size_t)id * F, F * sizeof(double),
+                              cudaMemcpyDeviceToHost, ctx->stream));
+    sync(ctx);
+  };
   auto run_exact = [&](const std::vector<int>& which) {  // item indices
     if (which.empty()) return;
     std::vector<InterItem> sub(which.size());
@@ -1185,6 +1284,9 @@ void assemble(lc_ctx* ctx, const float* lat, const uint8_t* om, const uint8_t* b
     FC_CUDA(cudaMemcpyAsync(cres.data(), dc.p, dc.bytes, cudaMemcpyDeviceToHost, ctx->stream));
     sync(ctx);
   } else {
+    std::vector<int64_t> all_e(n);
+    std::iota(all_e.begin(), all_e.end(), 0);
+    exact_norms(all_e);
     std::vector<int> all(items.size());
     std::iota(all.begin(), all.end(), 0);
     run_exact(all);
@@ -1221,12 +1323,16 @@ void assemble(lc_ctx* ctx, const float* lat, const uint8_t* om, const uint8_t* b
     const double u = 0x1p-53;
     const double cnt = (double)S * F;
     const double gam = cnt * u / (1.0 - cnt * u);
+    // identical-frame terms from reassociated norms: ss/(sqrt(ss) sqrt(ss)) is
+    // within a few ulps of 1 whatever ss is; 8u covers the difference
+    const double ib = (with_bounds && !norms_exact) ? 8.0 * u : 0.0;
     double score[MAXS], bnd[MAXS];
+    int napx[MAXS];
     int best_b = 0;
     double best_score = -2.0;
     for (int b = 0; b < S; ++b) {
       double sum = 0.0, bsum = 0.0, asum = 0.0;
-      int napprox = 0;
+      int napprox = 0, nid = 0;
       for (int si = 0; si < S; ++si) {
         for (int j = 0; j < F; ++j) {
           const int m = mapv(si, j);
@@ -1235,20 +1341,22 @@ void assemble(lc_ctx* ctx, const float* lat, const uint8_t* om, const uint8_t* b
           double sim;
           if (r && r->nz[b] && si != b && std::isfinite(r->alpha[si][b])) {
             sim = r->sim[si][b];
-            if (with_bounds) {
-              bsum += cres[c].bound[si][b];
-              ++napprox;
-            }
+            if (with_bounds) bsum += cres[c].bound[si][b];
+            ++napprox;
           } else {
             sim = isim[(size_t)si * F + m];
+            ++nid;
           }
           sum += sim;
           asum += std::fabs(sim);
         }
       }
+      bsum += nid * ib;
       score[b] = sum / cnt;
-      bnd[b] = napprox == 0 ? 0.0
-                            : ((bsum + 2.0 * gam * (asum + bsum)) / cnt) * (1.0 + 8.0 * u) + 8.0 * u * (std::fabs(score[b]) + 1.0);
+      napx[b] = napprox;
+      bnd[b] = (!with_bounds || (napprox == 0 && ib == 0.0))
+                   ? 0.0
+                   : ((bsum + 2.0 * gam * (asum + bsum)) / cnt) * (1.0 + 8.0 * u) + 8.0 * u * (std::fabs(score[b]) + 1.0);
       if (score[b] > best_score) {
         best_score = score[b];
         best_b = b;
@@ -1258,6 +1366,9 @@ void assemble(lc_ctx* ctx, const float* lat, const uint8_t* om, const uint8_t* b
       const double lo = score[best_b] - bnd[best_b];
       for (int b = 0; b < S; ++b) {
         if (b == best_b) continue;
+        // bases without approximate terms sum the same sequence of values:
+        // their scores are equal in the reference too (first one kept)
+        if (napx[b] == 0 && napx[best_b] == 0) continue;
         const double hi = score[b] + bnd[b];
         if (b < best_b ? !(hi < lo) : !(hi <= lo)) return -1;
       }
@@ -1271,9 +1382,13 @@ void assemble(lc_ctx* ctx, const float* lat, const uint8_t* om, const uint8_t* b
       need[e] = best_base[e] < 0;
     });
     std::vector<int> redo;
+    std::vector<int64_t> redo_e;
     for (int64_t e = 0; e < n; ++e)
-      if (need[e])
+      if (need[e]) {
+        redo_e.push_back(e);
         for (int c = item_begin[e]; c < item_begin[e + 1]; ++c) redo.push_back(c);
+      }
+    exact_norms(redo_e);
     ctx->inter_exact_items += redo.size();
     if (tr.on) {
       int nwhy[5] = {0, 0, 0, 0, 0}, ncert = 0, nprompt = 0;
@@ -1310,7 +1425,7 @@ void assemble(lc_ctx* ctx, const float* lat, const uint8_t* om, const uint8_t* b
     auto mapv = [&](int si, int j) { return maps_h[((size_t)e * S + perm[si]) * F + j]; };
     const int best_b = best_base[e];
     auto d = std::make_shared<EntryData>();
-    d->ctx = ctx;
+    d->ctx = ctx->top();
     d->prompt = prompts[e];
     d->base_step = steps_in[perm[best_b]];
     d->F = F; d->H = g.H; d->W = g.W; d->C = g.C; d->E = E; d->mb = g.mb;
@@ -1379,7 +1494,7 @@ void assemble(lc_ctx* ctx, const float* lat, const uint8_t* om, const uint8_t* b
     total += (ents[e]->dev_bytes + 255) & ~size_t(255);
   }
   auto arena = std::make_shared<DevArena>();
-  arena->ctx = ctx;
+  arena->ctx = ctx->top();
   FC_CUDA(cudaMallocAsync((void**)&arena->p, std::max<size_t>(total, 256), ctx->stream));
   tr.mark("host: arena alloc");
   // per-entry job / recipe spans (fixed offsets, so entries fill them in parallel)
@@ -1568,6 +1683,30 @@ bool all_finite(const float* v, int64_t n) {
   return true;
 }
 
+// K5 + K6 + K7 + K8 for n prompts on ctx's stream (a child context when the
+// batch is split); inputs device-resident.
+void compress_chunk(lc_ctx* ctx, const float* lat, const uint8_t* om, const uint8_t* bm, const std::vector<int32_t>& st,
+                    const Geo& g, double thr, const uint64_t* prompts, int64_t n, lc_entry** out, uint64_t* sizes) {
+  const int S = (int)st.size();
+  const int F = g.F;
+  Trace tr;
+  DevBuf bad(sizeof(int), ctx->stream);
+  FC_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), ctx->stream));
+  DevBuf G((size_t)n * S * F * F * sizeof(double), ctx->stream), NR((size_t)n * S * F * sizeof(double), ctx->stream);
+  const double delta = grams_and_norms(ctx, lat, (int)(n * S), g, G.as<double>(), NR.as<double>(), bad.as<int>());
+  if (check_flag(ctx, bad)) raise(LC_ERR_INVALID_ARGUMENT, "Frame: non-finite element");
+  tr.mark("nonfinite + gram (sync)");
+  DevBuf maps((size_t)n * S * F * sizeof(int32_t), ctx->stream);
+  select_cert(ctx, G.as<double>(), NR.as<double>(), lat, (int)(n * S), g, thr, delta, maps.as<int32_t>(), bad.as<int>());
+  PinnedBuf<int32_t> maps_h((size_t)n * S * F);
+  FC_CUDA(cudaMemcpyAsync(maps_h.data(), maps.p, maps.bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  if (check_flag(ctx, bad)) raise(LC_ERR_INVALID_ARGUMENT, "cosine_similarity: zero-norm operand");
+  check_distinct_steps(S, st.data());  // inter_compress validates after the intra pass (codec.cpp:201-205)
+  tr.mark("select + maps D2H");
+  assemble(ctx, lat, om, bm, st, g, maps_h.data(), NR.as<double>(), delta == 0.0, prompts, n, out, sizes);
+  tr.mark("assemble");
+}
+
 }  // namespace
 
 extern "C" {
@@ -1637,28 +1776,47 @@ lc_status lc_compress_batch(lc_ctx* ctx, const float* latents, const int32_t* st
   DeviceGuard dg(ctx->device);
   const int64_t E = (int64_t)H * W * C;
   Geo g{F, H, W, C, E, ((int64_t)H * W + 7) / 8};
-  Trace tr;
   InArg<float> lat(ctx, latents, (size_t)n * S * F * E);
   InArg<uint8_t> om(ctx, obj_masks, (size_t)n * F * g.mb), bm(ctx, bg_masks, (size_t)n * F * g.mb);
-  DevBuf bad(sizeof(int), ctx->stream);
-  FC_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), ctx->stream));
-  // K5 + K6: key frames of every (prompt, step)
-  DevBuf G((size_t)n * S * F * F * sizeof(double), ctx->stream), NR((size_t)n * S * F * sizeof(double), ctx->stream);
-  const double delta =
-      grams_and_norms(ctx, lat.dev, (int)(n * S), g, G.as<double>(), NR.as<double>(), bad.as<int>());
-  if (check_flag(ctx, bad)) raise(LC_ERR_INVALID_ARGUMENT, "Frame: non-finite element");
-  tr.mark("nonfinite + gram (sync)");
-  DevBuf maps((size_t)n * S * F * sizeof(int32_t), ctx->stream);
-  select_cert(ctx, G.as<double>(), NR.as<double>(), lat.dev, (int)(n * S), g, thr, delta, maps.as<int32_t>(),
-              bad.as<int>());
-  PinnedBuf<int32_t> maps_h((size_t)n * S * F);
-  FC_CUDA(cudaMemcpyAsync(maps_h.data(), maps.p, maps.bytes, cudaMemcpyDeviceToHost, ctx->stream));
-  if (check_flag(ctx, bad)) raise(LC_ERR_INVALID_ARGUMENT, "cosine_similarity: zero-norm operand");
-  check_distinct_steps(S, steps);
-  tr.mark("select + maps D2H");
   std::vector<int32_t> st(steps, steps + S);
-  assemble(ctx, lat.dev, om.dev, bm.dev, st, g, maps_h.data(), NR.as<double>(), prompts, n, out, sizes);
-  tr.mark("assemble");
+  // Two halves on two child streams from two host threads: one half's host
+  // orchestration (syncs, base choice, layout) overlaps the other's kernels.
+  const char* ev = getenv("FC_COMPRESS_SPLIT");
+  const int parts = (n >= 64 && !(ev && atoi(ev) == 0)) ? 2 : 1;
+  for (int64_t e = 0; e < n; ++e) out[e] = nullptr;
+  if (parts == 1) {
+    compress_chunk(ctx, lat.dev, om.dev, bm.dev, st, g, thr, prompts, n, out, sizes);
+  } else {
+    cudaEvent_t ready;
+    FC_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    FC_CUDA(cudaEventRecord(ready, ctx->stream));  // inputs staged on the caller's stream
+    const int64_t n0 = (n / 2 + 7) & ~int64_t(7);
+    const int64_t cut[3] = {0, std::min(n0, n), n};
+    std::exception_ptr err[2] = {nullptr, nullptr};
+    auto run = [&](int part) {
+      try {
+        lc_ctx* c = aux_ctx(ctx, part);
+        FC_CUDA(cudaStreamWaitEvent(c->stream, ready, 0));
+        const int64_t a = cut[part], m = cut[part + 1] - cut[part];
+        compress_chunk(c, lat.dev + a * S * F * E, om.dev + a * F * g.mb, bm.dev + a * F * g.mb, st, g, thr,
+                       prompts + a, m, out + a, sizes ? sizes + a : nullptr);
+      } catch (...) {
+        err[part] = std::current_exception();
+      }
+    };
+    std::thread t1(run, 1);
+    run(0);
+    t1.join();
+    cudaEventDestroy(ready);
+    if (err[0] || err[1]) {
+      for (int64_t e = 0; e < n; ++e)
+        if (out[e]) {
+          lc_entry_release(out[e]);
+          out[e] = nullptr;
+        }
+      std::rethrow_exception(err[0] ? err[0] : err[1]);
+    }
+  }
   LC_API_END
 }
 
@@ -1686,9 +1844,10 @@ lc_status lc_inter_compress(lc_ctx* ctx, const float* latents, const int32_t* ma
   DevBuf G((size_t)S * F * F * sizeof(double), ctx->stream), NR((size_t)S * F * sizeof(double), ctx->stream);
   DevBuf bad(sizeof(int), ctx->stream);
   FC_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), ctx->stream));
-  grams_and_norms(ctx, lat.dev, S, g, G.as<double>(), NR.as<double>(), bad.as<int>());
+  const double delta = grams_and_norms(ctx, lat.dev, S, g, G.as<double>(), NR.as<double>(), bad.as<int>());
   std::vector<int32_t> st(steps, steps + S);
-  assemble(ctx, lat.dev, om.dev, bm.dev, st, g, maps_h.data(), NR.as<double>(), &prompt, 1, out, nullptr);
+  assemble(ctx, lat.dev, om.dev, bm.dev, st, g, maps_h.data(), NR.as<double>(), delta == 0.0, &prompt, 1, out,
+           nullptr);
   LC_API_END
 }
 

@@ -77,6 +77,12 @@ struct lc_ctx {
   bool profile = false;
   std::mutex prof_mu;
   std::map<std::string, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>> prof;
+  // child contexts (own stream, same device) for work a call splits across
+  // streams; launches and kernel timings are accounted on the root
+  lc_ctx* root = nullptr;
+  std::mutex aux_mu;
+  std::vector<lc_ctx*> aux;
+  lc_ctx* top() { return root ? root : this; }
 };
 
 namespace fc {
@@ -87,7 +93,7 @@ struct KTimer {
   const char* name;
   cudaEvent_t a = nullptr, b = nullptr;
   KTimer(lc_ctx* c, const char* n) : ctx(c), name(n) {
-    if (!ctx->profile) return;
+    if (!ctx->top()->profile) return;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
     cudaEventRecord(a, ctx->stream);
@@ -95,8 +101,9 @@ struct KTimer {
   void stop() {
     if (!a) return;
     cudaEventRecord(b, ctx->stream);
-    std::lock_guard<std::mutex> g(ctx->prof_mu);
-    ctx->prof[name].emplace_back(a, b);
+    lc_ctx* t = ctx->top();
+    std::lock_guard<std::mutex> g(t->prof_mu);
+    t->prof[name].emplace_back(a, b);
     a = nullptr;
   }
   ~KTimer() { stop(); }
@@ -118,7 +125,9 @@ struct DeviceGuard {
   }
 };
 
-inline void count_launch(lc_ctx* ctx, uint64_t n = 1) { ctx->launches.fetch_add(n, std::memory_order_relaxed); }
+inline void count_launch(lc_ctx* ctx, uint64_t n = 1) { ctx->top()->launches.fetch_add(n, std::memory_order_relaxed); }
+// i-th child context of ctx (created on first use; destroyed with ctx)
+lc_ctx* aux_ctx(lc_ctx* ctx, int i);
 
 // Stream-ordered device buffer (cudaMallocAsync / cudaFreeAsync).
 struct DevBuf {

@@ -214,6 +214,24 @@ __global__ void k_priority(int policy, const lc_step_entry* __restrict__ e, int6
   if (b) atomicExch(bad, 1);
 }
 
+lc_ctx* aux_ctx(lc_ctx* ctx, int i) {
+  lc_ctx* t = ctx->top();
+  std::lock_guard<std::mutex> lk(t->aux_mu);
+  while ((int)t->aux.size() <= i) {
+    auto* c = new lc_ctx();
+    c->device = t->device;
+    c->sm_count = t->sm_count;
+    c->root = t;
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+      delete c;
+      raise(LC_ERR_CUDA, "aux stream creation failed");
+    }
+    c->own_stream = true;
+    t->aux.push_back(c);
+  }
+  return t->aux[i];
+}
+
 }  // namespace fc
 
 using namespace fc;
@@ -226,6 +244,7 @@ void lc_last_oversize(uint64_t* needed, uint64_t* limit) {
   if (limit) *limit = g_over_limit;
 }
 const char* lc_version(void) { return "flexcache-b200 0.1 (sm_100a)"; }
+
 
 lc_status lc_ctx_create(int device, lc_ctx** out) {
   LC_API_BEGIN
@@ -259,6 +278,11 @@ lc_status lc_ctx_destroy(lc_ctx* ctx) {
   LC_API_BEGIN
   if (!ctx) return LC_OK;
   DeviceGuard g(ctx->device);
+  for (lc_ctx* c : ctx->aux) {
+    cudaStreamSynchronize(c->stream);
+    cudaStreamDestroy(c->stream);
+    delete c;
+  }
   cudaStreamSynchronize(ctx->stream);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;

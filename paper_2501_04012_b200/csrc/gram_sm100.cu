@@ -10,8 +10,11 @@
 // pairs whose decision the bound cannot settle. Outputs:
 //   G~[item][F][F]  fp64, |G~(j,k) - dot(j,k)| <= GRAM_REL * sum_i |x_ji x_ki|
 //                   <= GRAM_REL * ||x_j|| ||x_k||  (Cauchy-Schwarz)
-//   nrm[item][F]    fp64, sequential sum_i x_ji^2 in element order — bit-
-//                   identical to cosine_similarity's na/nb (core.cpp:104-110)
+//   nrm[item][F]    fp64, sum_i x_ji^2 reassociated into 4 chains (each
+//                   product exact): |nrm - sequential| <= 2 gamma_E nrm.
+//                   Zero iff the frame is all zero. Consumers that need the
+//                   reference's exact sequential value (exact select pairs,
+//                   exact K7 fallback) recompute it (k_exact_norms, codec.cu).
 //
 // Error model (bf16x3): x = hi + lo + r with hi = RN_bf16(x), lo =
 // RN_bf16(x - hi), |r| <= 2^-16 |x|; the MMAs form hi*hi' + hi*lo' + lo*hi'
@@ -25,9 +28,10 @@
 // cross-item blocks of the 128x128 product are unused (tensor throughput is
 // not the limit: the kernel streams each latent once, HBM-bound).
 // Warp roles (320 threads): 0 TMA producer (fp32 boxes of 32 elements),
-// 1 MMA issuer (elected lane), 2-5 converters (thread = frame row: exact
-// norm + hi/lo split into SWIZZLE_128B bf16 tiles), 6-9 epilogue (TMEM ->
-// fp64 chunk accumulation, one row per thread).
+// 1 MMA issuer (elected lane), 2-9 workers: thread = half a frame row of
+// each K unit (norm partials + hi/lo split into SWIZZLE_128B bf16 tiles),
+// and the TMEM -> fp64 chunk accumulation of 32 Gram columns of that row
+// one chunk behind.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cudaTypedefs.h>
@@ -46,7 +50,8 @@ constexpr int XBOX = 128 * 128;  // one fp32 box region: 128 rows x 32 fp32 (128
 constexpr int XSTAGE = 2 * XBOX; // a K unit = two fp32 boxes
 constexpr int BTILE = 128 * 128; // one bf16 tile: 128 rows x 64 bf16
 constexpr int BSTAGE = 2 * BTILE;  // hi + lo
-constexpr int NX = 3, NB = 2;
+constexpr int NX = 4, NB = 2;
+constexpr int PF = 8;          // K units prefetched into L2 ahead of the smem ring
 constexpr int CHUNK = 4;      // K units per fp32 TMEM accumulation chunk (256 elements)
 
 struct Params {
@@ -57,6 +62,12 @@ struct Params {
   double* nrm;          // [n_items][F]
   int* bad;             // set to 1 if any element is non-finite (Frame ctor rule, core.cpp:11-25)
 };
+
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int x, int y, int z) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(reinterpret_cast<uint64_t>(map)),
+               "r"(x), "r"(y), "r"(z)
+               : "memory");
+}
 
 __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int x, int y, int z) {
   asm volatile(
@@ -82,6 +93,7 @@ __global__ void __launch_bounds__(GT, 1) k_gram_tc(const __grid_constant__ CUten
   uint64_t* afull = bempty + NB;
   uint64_t* aempty = afull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + 2);
+  __shared__ double s_nrm[2][128];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int F = p.F;
@@ -92,15 +104,15 @@ __global__ void __launch_bounds__(GT, 1) k_gram_tc(const __grid_constant__ CUten
   if (threadIdx.x == 0) {
     for (int s = 0; s < NX; ++s) {
       mbar_init(smem_u32(&xfull[s]), 1);
-      mbar_init(smem_u32(&xempty[s]), 4);
+      mbar_init(smem_u32(&xempty[s]), 8);
     }
     for (int s = 0; s < NB; ++s) {
-      mbar_init(smem_u32(&bfull[s]), 4);
+      mbar_init(smem_u32(&bfull[s]), 8);
       mbar_init(smem_u32(&bempty[s]), 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(smem_u32(&afull[b]), 1);
-      mbar_init(smem_u32(&aempty[b]), 4);
+      mbar_init(smem_u32(&aempty[b]), 8);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -123,14 +135,31 @@ __global__ void __launch_bounds__(GT, 1) k_gram_tc(const __grid_constant__ CUten
         const int ia = 2 * tile, ib = 2 * tile + 1;
         const bool has_b = ib < p.n_items;
         const uint32_t bytes = (has_b ? 4u : 2u) * (uint32_t)F * 128u;
+        // Units are visited from a per-tile rotation: with every SM at the
+        // same element offset, the concurrent 256-B row segments (rows 4E
+        // bytes apart) share their low address bits and pile onto a few HBM
+        // channels (ncu: per-channel DRAM activity 17-35 %). The Gram and
+        // norm sums are order-independent within their error bounds.
+        const int shift = (int)(((int64_t)tile * 97) % nu);
         for (int k = 0; k < nu; ++k, ++u) {
           const int s = u % NX;
+          const int kk = k + shift < nu ? k + shift : k + shift - nu;
+          // the smem ring holds only NX units; keep PF more in flight to L2
+          for (int kq = (k == 0 ? 0 : k + PF - 1); kq < nu && kq < k + PF; ++kq) {
+            const int kw = kq + shift < nu ? kq + shift : kq + shift - nu;
+            tma_prefetch_3d(&tmX, kw * KU, 0, ia);
+            tma_prefetch_3d(&tmX, kw * KU + 32, 0, ia);
+            if (has_b) {
+              tma_prefetch_3d(&tmX, kw * KU, 0, ib);
+              tma_prefetch_3d(&tmX, kw * KU + 32, 0, ib);
+            }
+          }
           mbar_wait(smem_u32(&xempty[s]), ((u / NX) & 1) ^ 1);
           mbar_expect_tx(smem_u32(&xfull[s]), bytes);
           uint8_t* dst = xst + s * XSTAGE;
           for (int h = 0; h < 2; ++h) {
-            tma_load_3d(smem_u32(dst + h * XBOX), &tmX, smem_u32(&xfull[s]), k * KU + h * 32, 0, ia);
-            if (has_b) tma_load_3d(smem_u32(dst + h * XBOX + 64 * 128), &tmX, smem_u32(&xfull[s]), k * KU + h * 32, 0, ib);
+            tma_load_3d(smem_u32(dst + h * XBOX), &tmX, smem_u32(&xfull[s]), kk * KU + h * 32, 0, ia);
+            if (has_b) tma_load_3d(smem_u32(dst + h * XBOX + 64 * 128), &tmX, smem_u32(&xfull[s]), kk * KU + h * 32, 0, ib);
           }
         }
       }
@@ -162,51 +191,77 @@ __global__ void __launch_bounds__(GT, 1) k_gram_tc(const __grid_constant__ CUten
               mma_ss(d, dh + o, dl + o, idesc, 1u);
               mma_ss(d, dl + o, dh + o, idesc, 1u);
             }
-            tc_commit(smem_u32(&bempty[s]));
           }
+          if (issuer) tc_commit(smem_u32(&bempty[s]));
           __syncwarp();
         }
         if (issuer) tc_commit(smem_u32(&afull[ab]));
         __syncwarp();
       }
     }
-  } else if (warp < 6) {
-    // ---------------- converters: thread = frame row ----------------
-    const int r = threadIdx.x - 64;  // 0..127
-    uint32_t u = 0;
-    for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+  } else {
+    // ---------------- 8 worker warps: convert half-rows + TMEM epilogue ----------------
+    // warp w may only touch TMEM lanes 32*(w%4)..+31, so its row quarter is
+    // w%4; warps 2-5 take elements 0-31 of every K unit (fp32 box 0), warps
+    // 6-9 elements 32-63 (box 1). The epilogue of chunk c runs after the
+    // conversion of chunk c+1 (the MMA lags the converters by about a unit).
+    const int quarter = warp & 3;
+    const int h = (warp - 2) >> 2;
+    const int r = quarter * 32 + lane;  // row of the 128-row operand = TMEM lane
+    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+    const int colb = (r >> 6) * 64 + h * 32;  // this thread's 32 Gram columns
+    uint32_t u = 0, ch = 0;
+    int par = 0;
+    for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, par ^= 1) {
       const int item = 2 * tile + (r >> 6);
       const int row = r & 63;
       const bool real = row < F && item < p.n_items;
-      double nrm = 0.0;
-      bool finite = true;
+      double nrm[4];  // 4 independent chains (the sequential one is latency-bound)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) nrm[c] = 0.0;
+      double acc[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) acc[i] = 0.0;
+      auto epilogue = [&](uint32_t gch) {
+        const uint32_t ab = gch & 1;
+        mbar_wait(smem_u32(&afull[ab]), (gch >> 1) & 1);
+        tc_fence_after();
+        float v[32];
+        tmem_ld32(tmem + lane_base + ab * 128 + colb, v);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&aempty[ab]));
+#pragma unroll
+        for (int i = 0; i < 32; ++i) acc[i] += (double)v[i];
+      };
+      const uint32_t ch0 = ch;
       for (int k = 0; k < nu; ++k, ++u) {
         const int sx = u % NX, sb = u % NB;
         mbar_wait(smem_u32(&xfull[sx]), (u / NX) & 1);
         mbar_wait(smem_u32(&bempty[sb]), ((u / NB) & 1) ^ 1);
-        const uint8_t* xs = xst + sx * XSTAGE;
+        const uint8_t* xb = xst + sx * XSTAGE + h * XBOX;
         uint8_t* hi = bst + sb * BSTAGE;
         uint8_t* lo = hi + BTILE;
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {  // bf16 chunk c = elements 8c..8c+7 = fp32 box c/4, fp32 chunks 2(c%4), 2(c%4)+1
-          const uint8_t* xb = xs + (c >> 2) * XBOX;
-          const float4 v0 = *reinterpret_cast<const float4*>(xb + sw128(r, 2 * (c & 3)));
-          const float4 v1 = *reinterpret_cast<const float4*>(xb + sw128(r, 2 * (c & 3) + 1));
+        for (int c = 0; c < 4; ++c) {  // bf16 chunk 4h+c = elements 8c..8c+7 of this box
+          const float4 v0 = *reinterpret_cast<const float4*>(xb + sw128(r, 2 * c));
+          const float4 v1 = *reinterpret_cast<const float4*>(xb + sw128(r, 2 * c + 1));
           const float x[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
           uint32_t h2[4], l2[4];
 #pragma unroll
           for (int e = 0; e < 8; e += 2) {
-            finite &= isfinite(x[e]) & isfinite(x[e + 1]);
-            nrm = fma((double)x[e], (double)x[e], nrm);
-            nrm = fma((double)x[e + 1], (double)x[e + 1], nrm);
-            const __nv_bfloat162 h = __floats2bfloat162_rn(x[e], x[e + 1]);
-            const float2 hf = __bfloat1622float2(h);
-            const __nv_bfloat162 l = __floats2bfloat162_rn(x[e] - hf.x, x[e + 1] - hf.y);
-            h2[e / 2] = *reinterpret_cast<const uint32_t*>(&h);
-            l2[e / 2] = *reinterpret_cast<const uint32_t*>(&l);
+            // a non-finite element makes its norm non-finite (x^2 of a finite
+            // float cannot overflow fp64): checked once per row below
+            nrm[c] = fma((double)x[e], (double)x[e], nrm[c]);
+            nrm[c] = fma((double)x[e + 1], (double)x[e + 1], nrm[c]);
+            const __nv_bfloat162 hh = __floats2bfloat162_rn(x[e], x[e + 1]);
+            const float2 hf = __bfloat1622float2(hh);
+            const __nv_bfloat162 ll = __floats2bfloat162_rn(x[e] - hf.x, x[e + 1] - hf.y);
+            h2[e / 2] = *reinterpret_cast<const uint32_t*>(&hh);
+            l2[e / 2] = *reinterpret_cast<const uint32_t*>(&ll);
           }
-          *reinterpret_cast<uint4*>(hi + sw128(r, c)) = make_uint4(h2[0], h2[1], h2[2], h2[3]);
-          *reinterpret_cast<uint4*>(lo + sw128(r, c)) = make_uint4(l2[0], l2[1], l2[2], l2[3]);
+          *reinterpret_cast<uint4*>(hi + sw128(r, 4 * h + c)) = make_uint4(h2[0], h2[1], h2[2], h2[3]);
+          *reinterpret_cast<uint4*>(lo + sw128(r, 4 * h + c)) = make_uint4(l2[0], l2[1], l2[2], l2[3]);
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> tensor-core reads
         __syncwarp();
@@ -214,45 +269,23 @@ __global__ void __launch_bounds__(GT, 1) k_gram_tc(const __grid_constant__ CUten
           mbar_arrive(smem_u32(&xempty[sx]));
           mbar_arrive(smem_u32(&bfull[sb]));
         }
+        if ((k + 1) % CHUNK == 0 && k + 1 > CHUNK) epilogue(ch++);  // chunk k/CHUNK - 1
       }
+      while (ch < ch0 + (uint32_t)nchunk) epilogue(ch++);
+      // row norm = box-0 half + box-1 half (smem, double-buffered by tile parity)
+      const double t = (nrm[0] + nrm[1]) + (nrm[2] + nrm[3]);
+      if (h == 1) s_nrm[par][r] = t;
+      asm volatile("bar.sync 1, 256;" ::: "memory");
       if (real) {
-        p.nrm[(int64_t)item * F + row] = nrm;
-        if (!finite) atomicExch(p.bad, 1);
-      }
-    }
-  } else {
-    // ---------------- epilogue: TMEM -> fp64 chunk sums ----------------
-    const int quarter = warp & 3;
-    const int r = quarter * 32 + lane;  // TMEM lane = frame row of the 128-row operand
-    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
-    const int colb = (r >> 6) * 64;     // this row's item occupies columns [colb, colb + 64)
-    uint32_t ch = 0;
-    for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
-      double acc[64];
+        if (h == 0) {
+          const double tot = t + s_nrm[par][r];
+          p.nrm[(int64_t)item * F + row] = tot;
+          if (!isfinite(tot)) atomicExch(p.bad, 1);
+        }
+        double* g = p.G + ((int64_t)item * F + row) * F + h * 32;
 #pragma unroll
-      for (int i = 0; i < 64; ++i) acc[i] = 0.0;
-      for (int c = 0; c < nchunk; ++c, ++ch) {
-        const uint32_t ab = ch & 1;
-        mbar_wait(smem_u32(&afull[ab]), (ch >> 1) & 1);
-        tc_fence_after();
-        float v[32];
-        tmem_ld32(tmem + lane_base + ab * 128 + colb, v);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) acc[i] += (double)v[i];
-        tmem_ld32(tmem + lane_base + ab * 128 + colb + 32, v);
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&aempty[ab]));
-#pragma unroll
-        for (int i = 0; i < 32; ++i) acc[32 + i] += (double)v[i];
-      }
-      const int item = 2 * tile + (r >> 6);
-      const int row = r & 63;
-      if (row < F && item < p.n_items) {
-        double* g = p.G + ((int64_t)item * F + row) * F;
-#pragma unroll
-        for (int i = 0; i < 64; ++i)
-          if (i < F) g[i] = acc[i];
+        for (int i = 0; i < 32; ++i)
+          if (h * 32 + i < F) g[i] = acc[i];
       }
     }
   }
