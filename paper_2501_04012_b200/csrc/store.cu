@@ -4,11 +4,13 @@
 // accounting; store.cpp:53-217) and a mirror of the per-(prompt, step)
 // bookkeeping. The device holds the live-step table as SoA-ish records
 // (40 B per live step + 16 B per prompt) that the scoring kernels read:
-//   K11 k_policy_head   per live step: attributed capacity
+//   K11 k_policy_seg    per live step: attributed capacity
 //                       cap = private + shared / live (integer, store.cpp:122),
 //                       policy key (store.cpp:125-131; fp64 IEEE mul/div), then a
-//                       block-level selection of the H smallest (key, seq).
-//   K12 k_head_merge    merge of the per-block heads -> global sorted head.
+//                       bitonic sort of each 4096-slot segment by (key, seq) in
+//                       smem; the first H = 256 are the segment head.
+//   K12 k_head_seg      the same sort over groups of segment heads, repeated
+//                       until one global sorted head remains.
 // Eviction (store.cpp:80, repeated evict_one) then walks the head on the
 // host. For LRBU, evicting a step re-attributes the prompt's shared bytes to
 // its surviving siblings, which lowers their keys; those siblings are re-keyed
@@ -39,9 +41,6 @@ struct DevPrompt {
   int32_t pad;
 };
 
-constexpr int HEAD = 64;
-constexpr int POL_T = 256;
-constexpr int POL_PER = 4;
 
 __device__ __forceinline__ double pkey(int policy, const DevLive& l, const DevPrompt& p, uint64_t now, uint64_t* cap_out,
                                        int* bad) {
@@ -63,55 +62,99 @@ __device__ __forceinline__ double pkey(int policy, const DevLive& l, const DevPr
   }
 }
 
-// Smallest (key, seq) first: encoded as Cand{s = -key, id = seq} so that the
-// shared (score desc, id asc) selection applies unchanged (negation is exact).
-__global__ void __launch_bounds__(POL_T) k_policy_head(const DevLive* __restrict__ live, int64_t n_slots,
-                                                       const DevPrompt* __restrict__ prompts, int policy, uint64_t now,
-                                                       Cand* __restrict__ partial, int32_t* __restrict__ pcount,
-                                                       int* __restrict__ bad) {
-  __shared__ Cand s_c[POL_T / 32];
-  __shared__ int s_o[POL_T / 32];
-  __shared__ Cand s_out[HEAD];
-  Cand L[POL_PER];
-  int ln = 0;
-  int b = 0;
-  const int64_t base = (int64_t)blockIdx.x * POL_T * POL_PER;
-  for (int t = 0; t < POL_PER; ++t) {
-    const int64_t i = base + (int64_t)t * POL_T + threadIdx.x;
-    if (i >= n_slots) break;
-    const DevLive l = live[i];
-    if (l.step == 0) continue;
-    uint64_t cap;
-    const double key = pkey(policy, l, prompts[l.pslot], now, &cap, &b);
-    Cand c;
-    c.s = -key;
-    c.id = l.seq;
-    c.slot = i;
-    local_insert<POL_PER>(L, ln, POL_PER, c);
-  }
-  if (b) atomicExch(bad, 1);
-  const int got = block_merge_lists<POL_PER>(L, ln, HEAD, s_out, s_c, s_o);
-  for (int t = threadIdx.x; t < got; t += POL_T) partial[(int64_t)blockIdx.x * HEAD + t] = s_out[t];
-  if (threadIdx.x == 0) pcount[blockIdx.x] = got;
+// ---------------------------------------------------------------------------
+// K11/K12: the H smallest (key, seq) live steps, as a segmented sort:
+// level 0 computes the key of every slot of a 4096-slot segment in smem and
+// bitonic-sorts the segment by (key, seq); its first H items are the
+// segment's head. Further levels sort groups of 4096/H heads the same way
+// until one head remains. Keys are non-negative doubles (or the FIFO/LRU
+// integers as doubles); the order-preserving bit image makes the comparison
+// a pair of u64 compares. Dead slots sort last.
+constexpr int SEG = 4096;      // items per block
+constexpr int SEG_T = 512;     // threads per block
+constexpr int SCORE_H = 256;   // head length kept per segment / returned
+
+__device__ __forceinline__ uint64_t key_bits(double k) {
+  const uint64_t b = (uint64_t)__double_as_longlong(k);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double bits_key(uint64_t b) {
+  return __longlong_as_double((long long)((b >> 63) ? (b & 0x7fffffffffffffffull) : ~b));
 }
 
-// Block b merges the per-block heads b, b + gridDim.x, ... into its own
-// sorted head; launched twice (many blocks, then one) so no single block
-// walks all ~500 partial heads of a 500k-slot table.
-__global__ void __launch_bounds__(256) k_head_merge(const Cand* __restrict__ partial, const int32_t* __restrict__ pcount,
-                                                    int nblk, Cand* __restrict__ head, int32_t* __restrict__ head_n) {
-  __shared__ Cand s_c[8];
-  __shared__ int s_o[8];
-  __shared__ Cand s_out[HEAD];
-  Cand L[HEAD];
-  int ln = 0;
-  for (int bi = blockIdx.x + threadIdx.x * gridDim.x; bi < nblk; bi += blockDim.x * gridDim.x) {
-    const int c = pcount[bi];
-    for (int t = 0; t < c; ++t) local_insert<HEAD>(L, ln, HEAD, partial[(int64_t)bi * HEAD + t]);
+struct ScoreItem {
+  uint64_t kb, seq;
+  int64_t slot;
+};
+
+__device__ __forceinline__ void seg_sort(uint64_t* kb, uint64_t* sq, int64_t* sl) {
+  for (int size = 2; size <= SEG; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      __syncthreads();
+      for (int t = threadIdx.x; t < SEG / 2; t += SEG_T) {
+        const int i = 2 * t - (t & (stride - 1));
+        const int j = i + stride;
+        const bool up = (i & size) == 0;
+        const bool gt = kb[i] > kb[j] || (kb[i] == kb[j] && sq[i] > sq[j]);
+        if (gt == up) {
+          const uint64_t a = kb[i], c = sq[i];
+          const int64_t e = sl[i];
+          kb[i] = kb[j], sq[i] = sq[j], sl[i] = sl[j];
+          kb[j] = a, sq[j] = c, sl[j] = e;
+        }
+      }
+    }
   }
-  const int got = block_merge_lists<HEAD>(L, ln, HEAD, s_out, s_c, s_o);
-  for (int t = threadIdx.x; t < got; t += blockDim.x) head[(int64_t)blockIdx.x * HEAD + t] = s_out[t];
-  if (threadIdx.x == 0) head_n[blockIdx.x] = got;
+  __syncthreads();
+}
+
+// level 0: keys of slots [blockIdx.x * SEG, +SEG)
+__global__ void __launch_bounds__(SEG_T) k_policy_seg(const DevLive* __restrict__ live, int64_t n_slots,
+                                                      const DevPrompt* __restrict__ prompts, int policy, uint64_t now,
+                                                      ScoreItem* __restrict__ heads, int* __restrict__ bad) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  uint64_t* kb = reinterpret_cast<uint64_t*>(sm);
+  uint64_t* sq = kb + SEG;
+  int64_t* sl = reinterpret_cast<int64_t*>(sq + SEG);
+  int b = 0;
+  for (int t = threadIdx.x; t < SEG; t += SEG_T) {
+    const int64_t i = (int64_t)blockIdx.x * SEG + t;
+    uint64_t k = ~0ull, q = ~0ull;
+    if (i < n_slots) {
+      const DevLive l = live[i];
+      if (l.step != 0) {
+        uint64_t cap;
+        k = key_bits(pkey(policy, l, prompts[l.pslot], now, &cap, &b));
+        q = l.seq;
+      }
+    }
+    kb[t] = k, sq[t] = q, sl[t] = i;
+  }
+  if (b) atomicExch(bad, 1);
+  seg_sort(kb, sq, sl);
+  for (int t = threadIdx.x; t < SCORE_H; t += SEG_T)
+    heads[(int64_t)blockIdx.x * SCORE_H + t] = ScoreItem{kb[t], sq[t], sl[t]};
+}
+
+// level >= 1: block b sorts heads [b * SEG, +SEG) of the previous level
+__global__ void __launch_bounds__(SEG_T) k_head_seg(const ScoreItem* __restrict__ in, int64_t n_in,
+                                                    ScoreItem* __restrict__ out) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  uint64_t* kb = reinterpret_cast<uint64_t*>(sm);
+  uint64_t* sq = kb + SEG;
+  int64_t* sl = reinterpret_cast<int64_t*>(sq + SEG);
+  for (int t = threadIdx.x; t < SEG; t += SEG_T) {
+    const int64_t i = (int64_t)blockIdx.x * SEG + t;
+    if (i < n_in) {
+      const ScoreItem it = in[i];
+      kb[t] = it.kb, sq[t] = it.seq, sl[t] = it.slot;
+    } else {
+      kb[t] = ~0ull, sq[t] = ~0ull, sl[t] = -1;
+    }
+  }
+  seg_sort(kb, sq, sl);
+  for (int t = threadIdx.x; t < SCORE_H; t += SEG_T)
+    out[(int64_t)blockIdx.x * SCORE_H + t] = ScoreItem{kb[t], sq[t], sl[t]};
 }
 
 struct ScatterLive {
@@ -258,37 +301,51 @@ struct lc_store {
     count_launch(ctx);
   }
 
-  // GPU scoring: the HEAD smallest (key, seq) live steps at time `now`.
+  // GPU scoring: the SCORE_H smallest (key, seq) live steps at time `now`.
   std::vector<Cand> score_head(uint64_t now) {
     sync_device();
     ++scorings;
     const int64_t n_slots = (int64_t)hl.size();
-    const int nblk = (int)std::max<int64_t>(1, (n_slots + POL_T * POL_PER - 1) / (POL_T * POL_PER));
-    DevBuf partial((size_t)nblk * HEAD * sizeof(Cand), ctx->stream), pc((size_t)nblk * sizeof(int32_t), ctx->stream);
-    DevBuf head(HEAD * sizeof(Cand) + 16, ctx->stream);
+    const size_t smem = (size_t)SEG * (8 + 8 + 8);
+    FC_CUDA(cudaFuncSetAttribute(k_policy_seg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    FC_CUDA(cudaFuncSetAttribute(k_head_seg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int64_t nblk = std::max<int64_t>(1, (n_slots + SEG - 1) / SEG);
     DevBuf bad(sizeof(int), ctx->stream);
     FC_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), ctx->stream));
+    DevBuf h0((size_t)nblk * SCORE_H * sizeof(ScoreItem), ctx->stream);
     KTimer kt(ctx, "policy");
-    k_policy_head<<<nblk, POL_T, 0, ctx->stream>>>(dl, n_slots, dp, policy, now, partial.as<Cand>(), pc.as<int32_t>(),
-                                                   bad.as<int>());
+    k_policy_seg<<<(unsigned)nblk, SEG_T, smem, ctx->stream>>>(dl, n_slots, dp, policy, now, h0.as<ScoreItem>(),
+                                                                bad.as<int>());
     FC_LAUNCH_CHECK();
-    const int mb = std::min(64, std::max(1, nblk / 8));
-    DevBuf mid((size_t)mb * HEAD * sizeof(Cand), ctx->stream), midn((size_t)mb * sizeof(int32_t), ctx->stream);
-    k_head_merge<<<mb, 256, 0, ctx->stream>>>(partial.as<Cand>(), pc.as<int32_t>(), nblk, mid.as<Cand>(),
-                                              midn.as<int32_t>());
-    k_head_merge<<<1, 256, 0, ctx->stream>>>(mid.as<Cand>(), midn.as<int32_t>(), mb, head.as<Cand>(),
-                                             reinterpret_cast<int32_t*>(head.as<Cand>() + HEAD));
+    count_launch(ctx);
+    DevBuf cur = std::move(h0);
+    int64_t n_in = nblk * SCORE_H;
+    while (n_in > SCORE_H) {
+      const int64_t nb = (n_in + SEG - 1) / SEG;
+      DevBuf nxt((size_t)nb * SCORE_H * sizeof(ScoreItem), ctx->stream);
+      k_head_seg<<<(unsigned)nb, SEG_T, smem, ctx->stream>>>(cur.as<ScoreItem>(), n_in, nxt.as<ScoreItem>());
+      FC_LAUNCH_CHECK();
+      count_launch(ctx);
+      cur = std::move(nxt);
+      n_in = nb * SCORE_H;
+    }
     kt.stop();
-    FC_LAUNCH_CHECK();
-    count_launch(ctx, 3);
-    std::vector<Cand> h(HEAD);
-    int32_t hn = 0, hb = 0;
-    FC_CUDA(cudaMemcpyAsync(h.data(), head.p, HEAD * sizeof(Cand), cudaMemcpyDeviceToHost, ctx->stream));
-    FC_CUDA(cudaMemcpyAsync(&hn, head.as<Cand>() + HEAD, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
+    std::vector<ScoreItem> hi(SCORE_H);
+    int32_t hb = 0;
+    FC_CUDA(cudaMemcpyAsync(hi.data(), cur.p, SCORE_H * sizeof(ScoreItem), cudaMemcpyDeviceToHost, ctx->stream));
     FC_CUDA(cudaMemcpyAsync(&hb, bad.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     sync(ctx);
     if (hb) raise(LC_ERR_INVALID_ARGUMENT, "lrbu_priority: now precedes last access");
-    h.resize(hn);
+    std::vector<Cand> h;
+    h.reserve(SCORE_H);
+    for (const ScoreItem& it : hi) {
+      if (it.kb == ~0ull && it.seq == ~0ull) break;  // dead / padding
+      uint64_t b = it.kb;
+      b = (b >> 63) ? (b & 0x7fffffffffffffffull) : ~b;
+      double key;
+      memcpy(&key, &b, 8);
+      h.push_back(Cand{-key, it.seq, it.slot});
+    }
     return h;
   }
 
