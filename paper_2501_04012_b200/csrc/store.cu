@@ -87,11 +87,12 @@ struct ScoreItem {
   int64_t slot;
 };
 
-__device__ __forceinline__ void seg_sort(uint64_t* kb, uint64_t* sq, int64_t* sl) {
-  for (int size = 2; size <= SEG; size <<= 1) {
+// bitonic sort of kb/sq/sl[0, n2) ascending by (kb, sq); n2 a power of two <= SEG
+__device__ __forceinline__ void seg_sort(uint64_t* kb, uint64_t* sq, int64_t* sl, int n2 = SEG) {
+  for (int size = 2; size <= n2; size <<= 1) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
       __syncthreads();
-      for (int t = threadIdx.x; t < SEG / 2; t += SEG_T) {
+      for (int t = threadIdx.x; t < n2 / 2; t += SEG_T) {
         const int i = 2 * t - (t & (stride - 1));
         const int j = i + stride;
         const bool up = (i & size) == 0;
@@ -155,6 +156,146 @@ __global__ void __launch_bounds__(SEG_T) k_head_seg(const ScoreItem* __restrict_
   seg_sort(kb, sq, sl);
   for (int t = threadIdx.x; t < SCORE_H; t += SEG_T)
     out[(int64_t)blockIdx.x * SCORE_H + t] = ScoreItem{kb[t], sq[t], sl[t]};
+}
+
+
+// ---------------------------------------------------------------------------
+// Fast path (radix threshold select): K11a writes the key image of every
+// slot and its min/max; K11b histograms (kb - min) >> shift over NBIN bins;
+// K11c finds the first bin at which the cumulative count reaches H; K11d
+// compacts every slot at or below that bin; K12 sorts the (<= CAP) survivors
+// by (key, seq). Exact: every slot with a smaller (key, seq) than the H-th
+// survivor is in a bin <= the threshold bin. When ties or a dense bin leave
+// more than CAP survivors, the segmented sort above is used instead.
+constexpr int NBIN = 4096;
+constexpr int CAP = SEG;
+
+__global__ void k_policy_keys(const DevLive* __restrict__ live, int64_t n_slots, const DevPrompt* __restrict__ prompts,
+                              int policy, uint64_t now, uint64_t* __restrict__ K, unsigned long long* __restrict__ mm,
+                              int* __restrict__ bad) {
+  uint64_t lo = ~0ull, hi = 0;
+  int b = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_slots; i += (int64_t)gridDim.x * blockDim.x) {
+    const DevLive l = live[i];
+    uint64_t k = ~0ull;
+    if (l.step != 0) {
+      uint64_t cap;
+      k = key_bits(pkey(policy, l, prompts[l.pslot], now, &cap, &b));
+      lo = k < lo ? k : lo;
+      hi = k > hi ? k : hi;
+    }
+    K[i] = k;
+  }
+  if (b) atomicExch(bad, 1);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const uint64_t a = __shfl_xor_sync(0xffffffffu, lo, o), c = __shfl_xor_sync(0xffffffffu, hi, o);
+    lo = a < lo ? a : lo;
+    hi = c > hi ? c : hi;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&mm[0], (unsigned long long)lo);
+    atomicMax(&mm[1], (unsigned long long)hi);
+  }
+}
+
+__device__ __forceinline__ int bin_shift(uint64_t lo, uint64_t hi) {
+  const uint64_t span = hi > lo ? hi - lo : 0;
+  const int bits = 64 - __clzll((long long)span);  // bits of the span
+  return bits > 12 ? bits - 12 : 0;                // NBIN = 2^12
+}
+
+__global__ void k_policy_hist(const uint64_t* __restrict__ K, int64_t n_slots, const unsigned long long* __restrict__ mm,
+                              unsigned* __restrict__ hist) {
+  __shared__ unsigned h[NBIN];
+  for (int t = threadIdx.x; t < NBIN; t += blockDim.x) h[t] = 0;
+  __syncthreads();
+  const uint64_t lo = mm[0], hi = mm[1];
+  const int sh = bin_shift(lo, hi);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_slots; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = K[i];
+    if (k != ~0ull) atomicAdd(&h[(k - lo) >> sh], 1u);
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < NBIN; t += blockDim.x)
+    if (h[t]) atomicAdd(&hist[t], h[t]);
+}
+
+// one block of 1024: pick[0] = threshold bin, pick[1] = survivors (cum count)
+__global__ void __launch_bounds__(1024) k_policy_pick(const unsigned* __restrict__ hist, int H, int* __restrict__ pick) {
+  __shared__ unsigned c[NBIN];
+  __shared__ int s_bin;
+  constexpr int PER = NBIN / 1024;
+  unsigned loc[PER], run = 0;
+#pragma unroll
+  for (int q = 0; q < PER; ++q) run += (loc[q] = hist[threadIdx.x * PER + q]);
+  // block exclusive scan of the per-thread totals
+  __shared__ unsigned tot[1024];
+  tot[threadIdx.x] = run;
+  if (threadIdx.x == 0) s_bin = NBIN - 1;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    const unsigned v = threadIdx.x >= o ? tot[threadIdx.x - o] : 0;
+    __syncthreads();
+    tot[threadIdx.x] += v;
+    __syncthreads();
+  }
+  unsigned acc = tot[threadIdx.x] - run;
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    acc += loc[q];
+    c[threadIdx.x * PER + q] = acc;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int b = threadIdx.x * PER + q;
+    if (c[b] >= (unsigned)H && (b == 0 || c[b - 1] < (unsigned)H)) s_bin = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    pick[0] = s_bin;
+    pick[1] = (int)c[s_bin];
+  }
+}
+
+__global__ void k_policy_collect(const uint64_t* __restrict__ K, const DevLive* __restrict__ live, int64_t n_slots,
+                                 const unsigned long long* __restrict__ mm, const int* __restrict__ pick,
+                                 ScoreItem* __restrict__ out, int* __restrict__ n_out) {
+  const int c = pick[1];
+  if (c > CAP) return;  // host takes the segmented-sort path
+  const uint64_t lo = mm[0], hi = mm[1];
+  const int sh = bin_shift(lo, hi);
+  const uint64_t tb = (uint64_t)pick[0];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_slots; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = K[i];
+    if (k != ~0ull && ((k - lo) >> sh) <= tb) {
+      const int at = atomicAdd(n_out, 1);
+      if (at < CAP) out[at] = ScoreItem{k, live[i].seq, i};
+    }
+  }
+}
+
+// one block: bitonic sort of the survivors (padded to CAP), first H out
+__global__ void __launch_bounds__(SEG_T) k_policy_final(const ScoreItem* __restrict__ in, const int* __restrict__ n_in,
+                                                        ScoreItem* __restrict__ out) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  uint64_t* kb = reinterpret_cast<uint64_t*>(sm);
+  uint64_t* sq = kb + SEG;
+  int64_t* sl = reinterpret_cast<int64_t*>(sq + SEG);
+  const int n = min(*n_in, CAP);
+  int n2 = SCORE_H;
+  while (n2 < n) n2 <<= 1;  // only the survivors are sorted (usually ~H)
+  for (int t = threadIdx.x; t < n2; t += SEG_T) {
+    if (t < n) {
+      const ScoreItem it = in[t];
+      kb[t] = it.kb, sq[t] = it.seq, sl[t] = it.slot;
+    } else {
+      kb[t] = ~0ull, sq[t] = ~0ull, sl[t] = -1;
+    }
+  }
+  seg_sort(kb, sq, sl, n2);
+  for (int t = threadIdx.x; t < SCORE_H; t += SEG_T) out[t] = ScoreItem{kb[t], sq[t], sl[t]};
 }
 
 struct ScatterLive {
@@ -309,25 +450,71 @@ struct lc_store {
     const size_t smem = (size_t)SEG * (8 + 8 + 8);
     FC_CUDA(cudaFuncSetAttribute(k_policy_seg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     FC_CUDA(cudaFuncSetAttribute(k_head_seg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int64_t nblk = std::max<int64_t>(1, (n_slots + SEG - 1) / SEG);
+    FC_CUDA(cudaFuncSetAttribute(k_policy_final, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     DevBuf bad(sizeof(int), ctx->stream);
     FC_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), ctx->stream));
-    DevBuf h0((size_t)nblk * SCORE_H * sizeof(ScoreItem), ctx->stream);
     KTimer kt(ctx, "policy");
-    k_policy_seg<<<(unsigned)nblk, SEG_T, smem, ctx->stream>>>(dl, n_slots, dp, policy, now, h0.as<ScoreItem>(),
-                                                                bad.as<int>());
-    FC_LAUNCH_CHECK();
-    count_launch(ctx);
-    DevBuf cur = std::move(h0);
-    int64_t n_in = nblk * SCORE_H;
-    while (n_in > SCORE_H) {
-      const int64_t nb = (n_in + SEG - 1) / SEG;
-      DevBuf nxt((size_t)nb * SCORE_H * sizeof(ScoreItem), ctx->stream);
-      k_head_seg<<<(unsigned)nb, SEG_T, smem, ctx->stream>>>(cur.as<ScoreItem>(), n_in, nxt.as<ScoreItem>());
+    // fast path: radix threshold select
+    const char* fe = getenv("FC_SCORE_SORT");
+    const bool fast = !(fe && atoi(fe) == 1) && n_slots > 0;
+    DevBuf cur;
+    if (fast) {
+      // scratch: K[n] | mm[2] | hist[NBIN] | pick[2] | n_out | items[CAP] | head[H]
+      const size_t kbytes = ((size_t)n_slots * 8 + 255) & ~size_t(255);
+      const size_t zoff = kbytes, zbytes = 16 + NBIN * 4 + 16;
+      const size_t ioff = zoff + ((zbytes + 255) & ~size_t(255));
+      const size_t hoff = ioff + CAP * sizeof(ScoreItem);
+      DevBuf scr(hoff + SCORE_H * sizeof(ScoreItem), ctx->stream);
+      uint8_t* base = scr.as<uint8_t>();
+      uint64_t* K = reinterpret_cast<uint64_t*>(base);
+      unsigned long long* mm = reinterpret_cast<unsigned long long*>(base + zoff);
+      unsigned* hist = reinterpret_cast<unsigned*>(base + zoff + 16);
+      int* pick = reinterpret_cast<int*>(base + zoff + 16 + NBIN * 4);
+      int* n_out = pick + 2;
+      FC_CUDA(cudaMemsetAsync(base + zoff, 0, zbytes, ctx->stream));
+      FC_CUDA(cudaMemsetAsync(mm, 0xff, 8, ctx->stream));  // min = ~0
+      const int grid = std::max(1, std::min<int>((int)((n_slots + 255) / 256), ctx->sm_count * 8));
+      k_policy_keys<<<grid, 256, 0, ctx->stream>>>(dl, n_slots, dp, policy, now, K, mm, bad.as<int>());
+      k_policy_hist<<<std::min(grid, ctx->sm_count * 2), 512, 0, ctx->stream>>>(K, n_slots, mm, hist);
+      k_policy_pick<<<1, 1024, 0, ctx->stream>>>(hist, SCORE_H, pick);
+      k_policy_collect<<<grid, 256, 0, ctx->stream>>>(K, dl, n_slots, mm, pick,
+                                                      reinterpret_cast<ScoreItem*>(base + ioff), n_out);
+      k_policy_final<<<1, SEG_T, smem, ctx->stream>>>(reinterpret_cast<ScoreItem*>(base + ioff), n_out,
+                                                      reinterpret_cast<ScoreItem*>(base + hoff));
+      FC_LAUNCH_CHECK();
+      count_launch(ctx, 5);
+      // one sync: head + the survivor count come back together
+      std::vector<ScoreItem> hh(SCORE_H);
+      int hp[3] = {0, 0, 0};
+      int32_t hb0 = 0;
+      FC_CUDA(cudaMemcpyAsync(hh.data(), base + hoff, SCORE_H * sizeof(ScoreItem), cudaMemcpyDeviceToHost, ctx->stream));
+      FC_CUDA(cudaMemcpyAsync(hp, pick, 3 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+      FC_CUDA(cudaMemcpyAsync(&hb0, bad.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+      sync(ctx);
+      if (hb0) raise(LC_ERR_INVALID_ARGUMENT, "lrbu_priority: now precedes last access");
+      if (hp[1] <= CAP) {
+        kt.stop();
+        return decode_head(hh);
+      }
+    }
+    {
+      int64_t nblk = std::max<int64_t>(1, (n_slots + SEG - 1) / SEG);
+      DevBuf h0((size_t)nblk * SCORE_H * sizeof(ScoreItem), ctx->stream);
+      k_policy_seg<<<(unsigned)nblk, SEG_T, smem, ctx->stream>>>(dl, n_slots, dp, policy, now, h0.as<ScoreItem>(),
+                                                                  bad.as<int>());
       FC_LAUNCH_CHECK();
       count_launch(ctx);
-      cur = std::move(nxt);
-      n_in = nb * SCORE_H;
+      cur = std::move(h0);
+      int64_t n_in = nblk * SCORE_H;
+      while (n_in > SCORE_H) {
+        const int64_t nb = (n_in + SEG - 1) / SEG;
+        DevBuf nxt((size_t)nb * SCORE_H * sizeof(ScoreItem), ctx->stream);
+        k_head_seg<<<(unsigned)nb, SEG_T, smem, ctx->stream>>>(cur.as<ScoreItem>(), n_in, nxt.as<ScoreItem>());
+        FC_LAUNCH_CHECK();
+        count_launch(ctx);
+        cur = std::move(nxt);
+        n_in = nb * SCORE_H;
+      }
     }
     kt.stop();
     std::vector<ScoreItem> hi(SCORE_H);
@@ -336,6 +523,10 @@ struct lc_store {
     FC_CUDA(cudaMemcpyAsync(&hb, bad.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     sync(ctx);
     if (hb) raise(LC_ERR_INVALID_ARGUMENT, "lrbu_priority: now precedes last access");
+    return decode_head(hi);
+  }
+
+  static std::vector<Cand> decode_head(const std::vector<ScoreItem>& hi) {
     std::vector<Cand> h;
     h.reserve(SCORE_H);
     for (const ScoreItem& it : hi) {

@@ -66,7 +66,7 @@ def _tiny_entries(fc, synth, n, seed):
 def test_random_trace_vs_oracle(fc, orc, synth, policy):
     ents = _tiny_entries(fc, synth, 300, policy)
     sizes = sorted(len(w) for _, w in ents.values())
-    cap = sizes[len(sizes) // 2] * 60   # holds ~60 prompts: inserts evict, bursts exceed the 64-entry head
+    cap = sizes[len(sizes) // 2] * 60   # holds ~60 prompts: inserts evict
     st = fc.CacheStore(cap, fc.Policy(policy))
     ot = orc.store(cap, policy)
     rng = np.random.default_rng(policy)
@@ -142,3 +142,35 @@ def test_priority_functions(fc):
     assert fc.lcbfu_priority(fc.StepEntry(step=5, f=9, capacity=1)) == 50
     with pytest.raises(fc.InvalidArgument):
         fc.lrbu_priority(fc.StepEntry(step=5, f=0, last_access=10, capacity=1), 5)
+
+
+@pytest.mark.parametrize("policy", [0, 1, 2, 3])
+@pytest.mark.parametrize("sort_path", ["0", "1"])
+def test_eviction_burst_both_scoring_paths(fc, orc, synth, policy, sort_path):
+    """600 evict_one at one `now` over ~1500 live steps: crosses the 256-entry
+    scored head twice (re-scoring), LRBU sibling re-keys, and the radix-select
+    fast path (FC_SCORE_SORT=0) vs the segmented-sort path (=1)."""
+    os.environ["FC_SCORE_SORT"] = sort_path
+    try:
+        ents = _tiny_entries(fc, synth, 300, policy)
+        st = fc.CacheStore(1 << 40, fc.Policy(policy))
+        ot = orc.store(1 << 40, policy)
+        rng = np.random.default_rng(10 + policy)
+        now = 0
+        for p, (e, w) in ents.items():
+            now += int(rng.integers(0, 2))
+            steps = sorted(int(x) for x in rng.choice(synth.CACHED_STEPS, size=int(rng.integers(3, 6)), replace=False))
+            st.insert_steps(p, e, steps, now)
+            ot.insert(p, w, steps, now)
+        for p in rng.choice(list(ents), 400):  # vary f / last_access
+            now += 1
+            d = int(rng.choice(synth.CACHED_STEPS))
+            r = st.get_step(int(p), d, now, want_latent=False)
+            oact, _ = ot.get_step(int(p), d, now, 4, 32)
+            assert (r[1] if r else 0) == oact
+        now += 5
+        for i in range(600):
+            assert tup(st.evict_one(now)) == list(ot.evict_one(now)), i
+        assert st.used() == ot.used() == st.recompute_used()
+    finally:
+        del os.environ["FC_SCORE_SORT"]
