@@ -47,13 +47,17 @@ typedef enum lc_status {
   LC_ERR_CUDA = 7,             /* CUDA runtime/driver failure                */
   LC_ERR_NCCL = 8,             /* reserved: collective failure               */
   LC_ERR_OOM = 9,              /* device allocation failure                  */
-  LC_ERR_INTERNAL = 10
+  LC_ERR_INTERNAL = 10,
+  LC_ERR_IO = 11               /* std::runtime_error: snapshot file I/O (store.cpp:268-276) */
 } lc_status;
 
 /* Thread-local message of the last failing call on this thread. */
 const char* lc_last_error(void);
 /* OversizedEntry{needed_bytes, capacity_limit} of the last LC_ERR_OVERSIZED_ENTRY. */
 void lc_last_oversize(uint64_t* needed_bytes, uint64_t* capacity_limit);
+/* Byte offset carried by the last LC_ERR_SNAPSHOT on this thread
+ * (SnapshotError::byte_offset, errors.hpp:30-35). */
+uint64_t lc_last_snapshot_offset(void);
 const char* lc_version(void);
 
 /* Policy (store.hpp:23). */
@@ -278,6 +282,18 @@ lc_status lc_store_cached_steps(lc_store* s, uint64_t prompt, int32_t* steps, in
 lc_status lc_store_entry(lc_store* s, uint64_t prompt, lc_entry** out);
 /* entries_snapshot (store.cpp:197-207): (prompt, step) order. */
 lc_status lc_store_entries(lc_store* s, lc_step_entry* out, int64_t cap, int64_t* n);
+
+/* ---------------------------------------------------------------------------
+ * Snapshot (save_snapshot / load_snapshot, store.cpp:219-364; store.hpp:122-132):
+ * "FLXC" v1, policy, capacity, next_seq, the three index tables (ids
+ * ascending), then one CRC32-checked record per prompt (serialize_entry bytes
+ * + live step records). Byte-identical to the reference's file for the same
+ * store and index state. Load errors: LC_ERR_SNAPSHOT (+ lc_last_snapshot_offset),
+ * LC_ERR_INVALID_ARGUMENT where the reference's constructors throw, LC_ERR_IO.
+ * ------------------------------------------------------------------------- */
+lc_status lc_snapshot_save(lc_store* store, lc_index* index, const char* path);
+/* On success *store / *index are new objects on ctx (destroy as usual). */
+lc_status lc_snapshot_load(lc_ctx* ctx, const char* path, lc_store** store, lc_index** index);
 /* lrbu_priority / lcbfu_priority (store.cpp:32-42) for n entries. */
 lc_status lc_priority_batch(lc_ctx* ctx, int policy, const lc_step_entry* e, int64_t n,
                             uint64_t now, double* out);

@@ -36,6 +36,7 @@
 #include <cmath>
 #include <compare>
 #include <cstdint>
+#include <filesystem>
 #include <functional>
 #include <map>
 #include <memory>
@@ -109,7 +110,14 @@ inline void check(lc_status s) {
       lc_last_oversize(&need, &lim);
       throw OversizedEntry(need, lim);
     }
-    case LC_ERR_SNAPSHOT: throw SnapshotError(msg, 0);
+    case LC_ERR_SNAPSHOT: {
+      // message is "<what> at byte <offset>"; rebuild the reference's exception
+      const std::uint64_t off = lc_last_snapshot_offset();
+      const std::string tail = " at byte " + std::to_string(off);
+      const bool has = msg.size() >= tail.size() && msg.compare(msg.size() - tail.size(), tail.size(), tail) == 0;
+      throw SnapshotError(has ? msg.substr(0, msg.size() - tail.size()) : msg, (std::size_t)off);
+    }
+    case LC_ERR_IO: throw std::runtime_error(msg);
     case LC_ERR_LOGIC: throw std::logic_error(msg);
     default: throw DeviceError("flexcache_b200: " + msg);
   }
@@ -360,6 +368,10 @@ struct QueryResult {
 class SimilarityIndex {
  public:
   SimilarityIndex() : SimilarityIndex(0) {}
+  // adopts a handle created by the library (load_snapshot)
+  SimilarityIndex(lc_index* adopt, std::shared_ptr<b200::Context> ctx) : ctx_(std::move(ctx)) {
+    h_.reset(adopt, [](lc_index* p) { lc_index_destroy(p); });
+  }
   explicit SimilarityIndex(int dim, std::shared_ptr<b200::Context> ctx = b200::default_context())
       : ctx_(std::move(ctx)) {
     lc_index* h = nullptr;
@@ -729,6 +741,9 @@ inline double lcbfu_priority(const StepEntry& e) {
 
 class CacheStore {
  public:
+  CacheStore(lc_store* adopt, std::shared_ptr<b200::Context> ctx) : ctx_(std::move(ctx)) {
+    h_.reset(adopt, [](lc_store* p) { lc_store_destroy(p); });
+  }
   CacheStore(std::uint64_t capacity_limit, Policy policy,
              std::shared_ptr<b200::Context> ctx = b200::default_context())
       : ctx_(std::move(ctx)) {
@@ -862,6 +877,23 @@ class CacheStore {
   std::shared_ptr<lc_store> h_;
   std::function<void(PromptId)> on_prompt_gone_;
 };
+
+// store.hpp:122-132: versioned binary snapshot of the store plus the three
+// index tables. The eviction callback is not part of it.
+struct SnapshotData {
+  CacheStore store;
+  SimilarityIndex index;
+};
+inline void save_snapshot(const CacheStore& store, const SimilarityIndex& index, const std::filesystem::path& path) {
+  b200::check(lc_snapshot_save(store.handle(), index.handle(), path.string().c_str()));
+}
+inline SnapshotData load_snapshot(const std::filesystem::path& path,
+                                  std::shared_ptr<b200::Context> ctx = b200::default_context()) {
+  lc_store* s = nullptr;
+  lc_index* i = nullptr;
+  b200::check(lc_snapshot_load(ctx->get(), path.string().c_str(), &s, &i));
+  return SnapshotData{CacheStore(s, ctx), SimilarityIndex(i, ctx)};
+}
 
 }  // namespace LCACHE_B200_NS
 

@@ -108,6 +108,14 @@ class Checker:
             fn(n).restype = C.c_uint64
         for n in ("store_step_count", "store_prompt_count"):
             fn(n).argtypes = [C.c_void_p]
+        if kind == "ref":  # snapshots exist only in the reference (store.cpp:219-364)
+            fn("snapshot_save").argtypes = [C.c_void_p, C.c_void_p, C.c_char_p]
+            fn("snapshot_load").argtypes = [C.c_char_p, C.POINTER(C.c_void_p)]
+            for n in ("snapshot_store", "snapshot_index"):
+                fn(n).argtypes = [C.c_void_p]
+                fn(n).restype = C.c_void_p
+            fn("snapshot_free").argtypes = [C.c_void_p]
+            fn("last_snapshot_offset").restype = C.c_uint64
             fn(n).restype = C.c_int64
         fn("store_entries").argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.POINTER(C.c_int)]
         if kind == "orc":
@@ -262,14 +270,50 @@ class Checker:
     def store(self, capacity, policy):
         return _Store(self, capacity, policy)
 
+    def index(self, dim):
+        return _Index(self, dim)
+
+    # ---- snapshots (reference only) -----------------------------------------
+    def snapshot_save(self, store, index, path):
+        self._chk(self._f("snapshot_save")(store.h, index.h, str(path).encode()))
+
+    def snapshot_load(self, path):
+        """-> (store, index); both keep the loaded SnapshotData alive."""
+        h = C.c_void_p()
+        self._chk(self._f("snapshot_load")(str(path).encode(), C.byref(h)))
+        owner = _SnapOwner(self, h)
+        st = _Store.__new__(_Store)
+        st.c, st.h, st._owner = self, self._f("snapshot_store")(h), owner
+        ix = _Index.__new__(_Index)
+        ix.c, ix.h, ix._owner, ix.dim = self, self._f("snapshot_index")(h), owner, None
+        return st, ix
+
+    def last_snapshot_offset(self):
+        return self._f("last_snapshot_offset")()
+
+
+class _SnapOwner:
+    def __init__(self, chk, h):
+        self.c, self.h = chk, h
+
+    def __del__(self):
+        try:
+            self.c._f("snapshot_free")(self.h)
+        except Exception:
+            pass
+
 
 class _Index:
+    _owner = None
+
     def __init__(self, chk: Checker, dim):
         self.c = chk
         self.h = chk._f("index_new")(dim)
         self.dim = dim
 
     def __del__(self):
+        if self._owner is not None:
+            return
         try:
             self.c._f("index_free")(self.h)
         except Exception:
@@ -297,11 +341,15 @@ class _Index:
 
 
 class _Store:
+    _owner = None
+
     def __init__(self, chk: Checker, capacity, policy):
         self.c = chk
         self.h = chk._f("store_new")(capacity, policy)
 
     def __del__(self):
+        if self._owner is not None:
+            return
         try:
             self.c._f("store_free")(self.h)
         except Exception:

@@ -26,6 +26,7 @@ using namespace lcache;
 
 namespace {
 thread_local std::string g_err;
+thread_local uint64_t g_snap_off = 0;
 
 template <class F>
 int guard(F&& f) {
@@ -43,6 +44,7 @@ int guard(F&& f) {
     return ORC_ERR_OVERSIZED_ENTRY;
   } catch (const SnapshotError& e) {
     g_err = e.what();
+    g_snap_off = e.byte_offset;
     return ORC_ERR_SNAPSHOT;
   } catch (const std::invalid_argument& e) {
     g_err = e.what();
@@ -358,5 +360,21 @@ int ref_store_entries(void* h, orc_step_entry* out, int cap, int* n) {
     for (size_t i = 0; i < v.size() && static_cast<int>(i) < cap; ++i) put_step_entry(v[i], out + i);
   });
 }
+
+// Snapshots (store.cpp:219-364): save/load through the reference's own code.
+uint64_t ref_last_snapshot_offset(void) { return g_snap_off; }
+int ref_snapshot_save(void* store, void* index, const char* path) {
+  return guard([&] {
+    save_snapshot(*static_cast<CacheStore*>(store), *static_cast<SimilarityIndex*>(index), path);
+  });
+}
+// On success *out owns a SnapshotData; its store / index are borrowed via
+// ref_snapshot_store / ref_snapshot_index and freed with ref_snapshot_free.
+int ref_snapshot_load(const char* path, void** out) {
+  return guard([&] { *out = new SnapshotData(load_snapshot(path)); });
+}
+void* ref_snapshot_store(void* d) { return &static_cast<SnapshotData*>(d)->store; }
+void* ref_snapshot_index(void* d) { return &static_cast<SnapshotData*>(d)->index; }
+void ref_snapshot_free(void* d) { delete static_cast<SnapshotData*>(d); }
 
 }  // extern "C"

@@ -25,6 +25,7 @@ used in place (no copies), host arrays are staged by the library.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 from enum import IntEnum
 
@@ -74,7 +75,12 @@ class OversizedEntry(LcacheError):
 
 
 class SnapshotError(LcacheError):
+    """SnapshotError (errors.hpp:30-35): byte_offset of the failing record/field."""
     code = 5
+
+    def __init__(self, msg, byte_offset=0):
+        super().__init__(msg)
+        self.byte_offset = byte_offset
 
 
 class LogicError(LcacheError):
@@ -85,8 +91,13 @@ class CudaError(LcacheError):
     code = 7
 
 
+class SnapshotIOError(LcacheError, OSError):
+    """std::runtime_error from snapshot file I/O (store.cpp:268-276)."""
+    code = 11
+
+
 _ERR = {1: InvalidArgument, 2: DegenerateBase, 3: StepNotCached, 4: OversizedEntry, 5: SnapshotError,
-        6: LogicError, 7: CudaError, 9: CudaError}
+        6: LogicError, 7: CudaError, 9: CudaError, 11: SnapshotIOError}
 
 
 def _check(rc):
@@ -98,6 +109,8 @@ def _check(rc):
         a, b = C.c_uint64(), C.c_uint64()
         lib.lc_last_oversize(C.byref(a), C.byref(b))
         raise OversizedEntry(msg, a.value, b.value)
+    if cls is SnapshotError:
+        raise SnapshotError(msg, int(lib.lc_last_snapshot_offset()))
     err = cls(msg)
     err.code = rc
     raise err
@@ -711,3 +724,21 @@ class CacheStore:
         buf = (StepEntry * max(n.value, 1))()
         _check(lib.lc_store_entries(self.h, buf, n.value, C.byref(n)))
         return [StepEntry.from_buffer_copy(buf[i]) for i in range(n.value)]
+
+
+def save_snapshot(store: "CacheStore", index: "SimilarityIndex", path) -> None:
+    """save_snapshot (store.cpp:232-273): byte-identical FLXC v1 file."""
+    _check(lib.lc_snapshot_save(store.h, index.h, os.fspath(path).encode()))
+
+
+def load_snapshot(path, ctx: Context | None = None):
+    """load_snapshot (store.cpp:275-364) -> (CacheStore, SimilarityIndex) in HBM.
+    The eviction callback is not part of the snapshot (store.hpp:123-124)."""
+    ctx = ctx or default_context()
+    hs, hi = C.c_void_p(), C.c_void_p()
+    _check(lib.lc_snapshot_load(ctx.h, os.fspath(path).encode(), C.byref(hs), C.byref(hi)))
+    st = CacheStore.__new__(CacheStore)
+    st.ctx, st.h, st._cb = ctx, hs, None
+    ix = SimilarityIndex.__new__(SimilarityIndex)
+    ix.ctx, ix.h = ctx, hi
+    return st, ix

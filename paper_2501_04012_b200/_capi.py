@@ -65,6 +65,7 @@ def _sig(name, res, *args):
 st = C.c_int  # lc_status
 _sig("lc_last_error", C.c_char_p)
 _sig("lc_last_oversize", None, C.POINTER(u64), C.POINTER(u64))
+_sig("lc_last_snapshot_offset", u64)
 _sig("lc_version", C.c_char_p)
 _sig("lc_ctx_create", st, C.c_int, C.POINTER(vp))
 _sig("lc_ctx_destroy", st, vp)
@@ -104,6 +105,8 @@ _sig("lc_decompress_batch", st, vp, vp, vp, i64, vp)
 _sig("lc_decompress_stitch_batch", st, vp, vp, vp, vp, i64, vp)
 _sig("lc_stitch_batch", st, vp, vp, vp, vp, vp, i64, C.c_int, C.c_int, C.c_int, C.c_int, vp)
 _sig("lc_store_create", st, vp, u64, C.c_int, C.POINTER(vp))
+_sig("lc_snapshot_save", st, vp, vp, C.c_char_p)
+_sig("lc_snapshot_load", st, vp, C.c_char_p, C.POINTER(vp), C.POINTER(vp))
 _sig("lc_store_destroy", st, vp)
 _sig("lc_store_insert", st, vp, u64, vp, vp, C.c_int, u64, vp, C.c_int, C.POINTER(C.c_int))
 _sig("lc_store_get_step", st, vp, u64, C.c_int, u64, C.POINTER(i32), vp)

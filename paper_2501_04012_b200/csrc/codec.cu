@@ -1663,7 +1663,7 @@ struct Reader {
   const uint8_t* p;
   uint64_t n, pos = 0;
   void need(uint64_t k) {
-    if (pos + k > n) raise(LC_ERR_SNAPSHOT, "truncated input at byte " + std::to_string(pos));
+    if (pos + k > n) raise_snap("truncated input", pos);
   }
   uint8_t u8() { need(1); return p[pos++]; }
   uint16_t u16() { need(2); uint16_t v = (uint16_t)(p[pos] | (p[pos + 1] << 8)); pos += 2; return v; }
@@ -1676,6 +1676,15 @@ struct Reader {
   }
   const uint8_t* bytes(uint64_t k) { need(k); const uint8_t* r = p + pos; pos += k; return r; }
 };
+
+bool bytes_finite(const uint8_t* p, int64_t n) {  // n little-endian fp32 values, any alignment
+  for (int64_t i = 0; i < n; ++i) {
+    uint32_t u;
+    memcpy(&u, p + 4 * i, 4);
+    if ((u & 0x7f800000u) == 0x7f800000u) return false;
+  }
+  return true;
+}
 
 bool all_finite(const float* v, int64_t n) {
   for (int64_t i = 0; i < n; ++i)
@@ -1708,6 +1717,148 @@ void compress_chunk(lc_ctx* ctx, const float* lat, const uint8_t* om, const uint
 }
 
 }  // namespace
+
+namespace fc {
+// deserialize_entry (codec.cpp:395-473) from the front of bytes[0, len):
+// parses one entry, reports the bytes it used, uploads it to HBM. Errors as
+// the reference (SnapshotError offsets relative to the entry start).
+lc_entry* import_entry(lc_ctx* ctx, const uint8_t* bytes, uint64_t len, uint64_t* consumed) {
+  Reader r{bytes, len};
+  auto d = std::make_shared<EntryData>();
+  d->ctx = ctx;
+  d->prompt = r.u64();
+  const int base = r.u8();
+  const int ns = r.u8();
+  const int nd = r.u16();
+  d->F = r.u16();
+  d->H = r.u16();
+  d->W = r.u16();
+  d->C = r.u16();
+  if (ns < 1 || d->F < 1 || d->H < 1 || d->W < 1 || d->C < 1) raise_snap("invalid entry header", 0);
+  if (base < 1 || base > 50) raise(LC_ERR_INVALID_ARGUMENT, "StepId: value out of range 1..50");
+  d->base_step = base;
+  d->E = (int64_t)d->H * d->W * d->C;
+  d->mb = ((int64_t)d->H * d->W + 7) / 8;
+  const int64_t E = d->E;
+  std::vector<const uint8_t*> firsts(ns), raw_alpha(ns, nullptr);
+  std::vector<std::vector<const uint8_t*>> extras(ns);
+  d->steps.resize(ns);
+  d->maps.resize(ns);
+  d->extra_idx.resize(ns);
+  d->alphas.resize(ns);
+  for (int s = 0; s < ns; ++s) {
+    const uint64_t step_pos = r.pos;
+    const int step = r.u8();
+    if (step < 1 || step > 50) raise(LC_ERR_INVALID_ARGUMENT, "StepId: value out of range 1..50");
+    d->steps[s] = step;
+    firsts[s] = r.bytes(4ull * E);
+    d->maps[s].resize(d->F);
+    for (int j = 0; j < d->F; ++j) {
+      d->maps[s][j] = r.u16();
+      if (d->maps[s][j] >= d->F) raise_snap("key frame map index out of range", step_pos);
+    }
+    // Frame(dims, first) validates here, before anything later is parsed (core.cpp:19-25)
+    if (!bytes_finite(firsts[s], E)) raise(LC_ERR_INVALID_ARGUMENT, "Frame: non-finite element");
+    if (step != base) raw_alpha[s] = r.bytes(4ull * nd);
+    const int nx = r.u16();
+    std::vector<std::pair<int, const uint8_t*>> xs;
+    for (int x = 0; x < nx; ++x) {
+      const int m = r.u16();
+      if (m >= d->F) raise_snap("extra frame index out of range", step_pos);
+      const uint8_t* fr = r.bytes(4ull * E);
+      if (!bytes_finite(fr, E)) raise(LC_ERR_INVALID_ARGUMENT, "Frame: non-finite element");
+      bool dup = false;
+      for (auto& pr : xs) dup |= pr.first == m;
+      if (!dup) xs.emplace_back(m, fr);  // std::map::emplace keeps the first
+    }
+    std::sort(xs.begin(), xs.end(), [](auto& a, auto& b) { return a.first < b.first; });
+    for (auto& pr : xs) {
+      d->extra_idx[s].push_back(pr.first);
+      extras[s].push_back(pr.second);
+    }
+    if (s > 0 && !(d->steps[s - 1] < step)) raise_snap("steps out of order", step_pos);
+  }
+  std::vector<const uint8_t*> diffs;
+  std::vector<int> all_idx(nd);
+  for (int t = 0; t < nd; ++t) {
+    const uint64_t pos = r.pos;
+    const int m = r.u16();
+    if (m < 1 || m >= d->F) raise_snap("diff index out of range", pos);
+    all_idx[t] = m;
+    const uint8_t* df = r.bytes(4ull * E);
+    // base_diffs.diffs.emplace keeps the first of a repeated index (codec.cpp:443)
+    if (std::find(d->diff_idx.begin(), d->diff_idx.end(), m) == d->diff_idx.end()) {
+      d->diff_idx.push_back(m);
+      diffs.push_back(df);
+    }
+  }
+  if (!std::is_sorted(all_idx.begin(), all_idx.end())) raise_snap("diff indices out of order", r.pos);
+  const int nu = (int)d->diff_idx.size();
+  for (int s = 0; s < ns; ++s) {
+    if (d->steps[s] == base) continue;
+    d->alphas[s].resize(nu);
+    for (int t = 0, u = 0; t < nd; ++t)  // alphas.emplace keeps the first too (codec.cpp:448-451)
+      if (t == 0 || all_idx[t] != all_idx[t - 1]) memcpy(&d->alphas[s][u++], raw_alpha[s] + 4ull * t, 4);
+  }
+  const uint8_t* masks = r.bytes(2ull * d->F * d->mb);
+  *consumed = r.pos;
+  // host image -> device
+  int64_t off = 0;
+  d->first_off.resize(ns);
+  for (int s = 0; s < ns; ++s) { d->first_off[s] = off; off += E; }
+  d->diff_off.resize(nu);
+  for (int t = 0; t < nu; ++t) { d->diff_off[t] = off; off += E; }
+  d->extra_off.resize(ns);
+  for (int s = 0; s < ns; ++s)
+    for (size_t x = 0; x < d->extra_idx[s].size(); ++x) { d->extra_off[s].push_back(off); off += E; }
+  int64_t bytes_n = ((off * 4 + 15) / 16) * 16;
+  d->mask_off = bytes_n;
+  bytes_n += ((2 * d->F * d->mb + 15) / 16) * 16;
+  d->recipe_off = bytes_n;
+  bytes_n += (int64_t)ns * d->F * sizeof(Recipe);
+  d->dev_bytes = (size_t)bytes_n;
+  std::vector<uint8_t> img(d->dev_bytes, 0);
+  for (int s = 0; s < ns; ++s) memcpy(img.data() + 4 * d->first_off[s], firsts[s], 4ull * E);
+  for (int t = 0; t < nu; ++t) memcpy(img.data() + 4 * d->diff_off[t], diffs[t], 4ull * E);
+  for (int s = 0; s < ns; ++s)
+    for (size_t x = 0; x < extras[s].size(); ++x) memcpy(img.data() + 4 * d->extra_off[s][x], extras[s][x], 4ull * E);
+  memcpy(img.data() + d->mask_off, masks, 2ull * d->F * d->mb);
+  Recipe* rec = reinterpret_cast<Recipe*>(img.data() + d->recipe_off);
+  for (int s = 0; s < ns; ++s) {
+    std::vector<Recipe> key_rec(d->F);
+    for (int m = 0; m < d->F; ++m) {
+      Recipe rr{0, 0.f, d->first_off[s], 0};
+      if (m != 0) {
+        auto xi = std::lower_bound(d->extra_idx[s].begin(), d->extra_idx[s].end(), m);
+        if (xi != d->extra_idx[s].end() && *xi == m) {
+          rr.a = d->extra_off[s][xi - d->extra_idx[s].begin()];
+        } else {
+          auto di = std::lower_bound(d->diff_idx.begin(), d->diff_idx.end(), m);
+          if (di != d->diff_idx.end() && *di == m) {
+            const size_t t = di - d->diff_idx.begin();
+            rr.b = d->diff_off[t];
+            if (d->steps[s] == base) rr.kind = 1;
+            else {
+              rr.kind = 2;
+              rr.alpha = d->alphas[s][t];
+            }
+          }
+        }
+      }
+      key_rec[m] = rr;
+    }
+    // a non-key frame maps to a key; decompress copies that key's reconstruction
+    for (int j = 0; j < d->F; ++j) rec[(size_t)s * d->F + j] = key_rec[d->maps[s][j]];
+  }
+  FC_CUDA(cudaMallocAsync((void**)&d->dev, d->dev_bytes, ctx->stream));
+  FC_CUDA(cudaMemcpyAsync(d->dev, img.data(), d->dev_bytes, cudaMemcpyHostToDevice, ctx->stream));
+  sync(ctx);
+  std::vector<int> sel(ns);
+  std::iota(sel.begin(), sel.end(), 0);
+  return make_entry_view(d, std::move(sel));
+}
+
+}  // namespace fc
 
 extern "C" {
 
@@ -1923,141 +2074,13 @@ lc_status lc_entry_import(lc_ctx* ctx, const uint8_t* bytes, uint64_t len, lc_en
   LC_API_BEGIN
   FC_REQUIRE(ctx && bytes && out, "null argument");
   DeviceGuard dg(ctx->device);
-  Reader r{bytes, len};
-  auto d = std::make_shared<EntryData>();
-  d->ctx = ctx;
-  d->prompt = r.u64();
-  const int base = r.u8();
-  const int ns = r.u8();
-  const int nd = r.u16();
-  d->F = r.u16();
-  d->H = r.u16();
-  d->W = r.u16();
-  d->C = r.u16();
-  if (ns < 1 || d->F < 1 || d->H < 1 || d->W < 1 || d->C < 1) raise(LC_ERR_SNAPSHOT, "invalid entry header at byte 0");
-  if (base < 1 || base > 50) raise(LC_ERR_INVALID_ARGUMENT, "StepId: value out of range 1..50");
-  d->base_step = base;
-  d->E = (int64_t)d->H * d->W * d->C;
-  d->mb = ((int64_t)d->H * d->W + 7) / 8;
-  const int64_t E = d->E;
-  std::vector<const uint8_t*> firsts(ns), raw_alpha(ns, nullptr);
-  std::vector<std::vector<const uint8_t*>> extras(ns);
-  d->steps.resize(ns);
-  d->maps.resize(ns);
-  d->extra_idx.resize(ns);
-  d->alphas.resize(ns);
-  for (int s = 0; s < ns; ++s) {
-    const uint64_t step_pos = r.pos;
-    const int step = r.u8();
-    if (step < 1 || step > 50) raise(LC_ERR_INVALID_ARGUMENT, "StepId: value out of range 1..50");
-    d->steps[s] = step;
-    firsts[s] = r.bytes(4ull * E);
-    d->maps[s].resize(d->F);
-    for (int j = 0; j < d->F; ++j) {
-      d->maps[s][j] = r.u16();
-      if (d->maps[s][j] >= d->F) raise(LC_ERR_SNAPSHOT, "key frame map index out of range at byte " + std::to_string(step_pos));
-    }
-    if (step != base) raw_alpha[s] = r.bytes(4ull * nd);
-    const int nx = r.u16();
-    std::vector<std::pair<int, const uint8_t*>> xs;
-    for (int x = 0; x < nx; ++x) {
-      const int m = r.u16();
-      if (m >= d->F) raise(LC_ERR_SNAPSHOT, "extra frame index out of range at byte " + std::to_string(step_pos));
-      const uint8_t* fr = r.bytes(4ull * E);
-      bool dup = false;
-      for (auto& pr : xs) dup |= pr.first == m;
-      if (!dup) xs.emplace_back(m, fr);  // std::map::emplace keeps the first
-    }
-    std::sort(xs.begin(), xs.end(), [](auto& a, auto& b) { return a.first < b.first; });
-    for (auto& pr : xs) {
-      d->extra_idx[s].push_back(pr.first);
-      extras[s].push_back(pr.second);
-    }
-    if (s > 0 && !(d->steps[s - 1] < step)) raise(LC_ERR_SNAPSHOT, "steps out of order at byte " + std::to_string(step_pos));
+  uint64_t used = 0;
+  lc_entry* e = import_entry(ctx, bytes, len, &used);
+  if (used != len) {
+    lc_entry_release(e);
+    raise_snap("trailing bytes", used);
   }
-  std::vector<const uint8_t*> diffs(nd);
-  for (int t = 0; t < nd; ++t) {
-    const uint64_t pos = r.pos;
-    const int m = r.u16();
-    if (m < 1 || m >= d->F) raise(LC_ERR_SNAPSHOT, "diff index out of range at byte " + std::to_string(pos));
-    d->diff_idx.push_back(m);
-    diffs[t] = r.bytes(4ull * E);
-  }
-  for (int t = 1; t < nd; ++t) {
-    if (d->diff_idx[t] < d->diff_idx[t - 1]) raise(LC_ERR_SNAPSHOT, "diff indices out of order at byte " + std::to_string(r.pos));
-    if (d->diff_idx[t] == d->diff_idx[t - 1]) raise(LC_ERR_SNAPSHOT, "duplicate diff index");
-  }
-  for (int s = 0; s < ns; ++s) {
-    if (d->steps[s] == base) continue;
-    d->alphas[s].resize(nd);
-    if (nd) memcpy(d->alphas[s].data(), raw_alpha[s], 4ull * nd);
-  }
-  const uint8_t* masks = r.bytes(2ull * d->F * d->mb);
-  if (r.pos != len) raise(LC_ERR_SNAPSHOT, "trailing bytes at byte " + std::to_string(r.pos));
-  // host image -> device
-  int64_t off = 0;
-  d->first_off.resize(ns);
-  for (int s = 0; s < ns; ++s) { d->first_off[s] = off; off += E; }
-  d->diff_off.resize(nd);
-  for (int t = 0; t < nd; ++t) { d->diff_off[t] = off; off += E; }
-  d->extra_off.resize(ns);
-  for (int s = 0; s < ns; ++s)
-    for (size_t x = 0; x < d->extra_idx[s].size(); ++x) { d->extra_off[s].push_back(off); off += E; }
-  int64_t bytes_n = ((off * 4 + 15) / 16) * 16;
-  d->mask_off = bytes_n;
-  bytes_n += ((2 * d->F * d->mb + 15) / 16) * 16;
-  d->recipe_off = bytes_n;
-  bytes_n += (int64_t)ns * d->F * sizeof(Recipe);
-  d->dev_bytes = (size_t)bytes_n;
-  std::vector<uint8_t> img(d->dev_bytes, 0);
-  for (int s = 0; s < ns; ++s) memcpy(img.data() + 4 * d->first_off[s], firsts[s], 4ull * E);
-  for (int t = 0; t < nd; ++t) memcpy(img.data() + 4 * d->diff_off[t], diffs[t], 4ull * E);
-  for (int s = 0; s < ns; ++s)
-    for (size_t x = 0; x < extras[s].size(); ++x) memcpy(img.data() + 4 * d->extra_off[s][x], extras[s][x], 4ull * E);
-  if (!all_finite(reinterpret_cast<const float*>(img.data()), off)) {
-    // diffs are not Frames (no finite check) in the reference; only firsts/extras are
-    for (int s = 0; s < ns; ++s) {
-      if (!all_finite(reinterpret_cast<const float*>(img.data() + 4 * d->first_off[s]), E))
-        raise(LC_ERR_INVALID_ARGUMENT, "Frame: non-finite element");
-      for (size_t x = 0; x < extras[s].size(); ++x)
-        if (!all_finite(reinterpret_cast<const float*>(img.data() + 4 * d->extra_off[s][x]), E))
-          raise(LC_ERR_INVALID_ARGUMENT, "Frame: non-finite element");
-    }
-  }
-  memcpy(img.data() + d->mask_off, masks, 2ull * d->F * d->mb);
-  Recipe* rec = reinterpret_cast<Recipe*>(img.data() + d->recipe_off);
-  for (int s = 0; s < ns; ++s) {
-    std::vector<Recipe> key_rec(d->F);
-    for (int m = 0; m < d->F; ++m) {
-      Recipe rr{0, 0.f, d->first_off[s], 0};
-      if (m != 0) {
-        auto xi = std::lower_bound(d->extra_idx[s].begin(), d->extra_idx[s].end(), m);
-        if (xi != d->extra_idx[s].end() && *xi == m) {
-          rr.a = d->extra_off[s][xi - d->extra_idx[s].begin()];
-        } else {
-          auto di = std::lower_bound(d->diff_idx.begin(), d->diff_idx.end(), m);
-          if (di != d->diff_idx.end() && *di == m) {
-            const size_t t = di - d->diff_idx.begin();
-            rr.b = d->diff_off[t];
-            if (d->steps[s] == base) rr.kind = 1;
-            else {
-              rr.kind = 2;
-              rr.alpha = d->alphas[s][t];
-            }
-          }
-        }
-      }
-      key_rec[m] = rr;
-    }
-    // a non-key frame maps to a key; decompress copies that key's reconstruction
-    for (int j = 0; j < d->F; ++j) rec[(size_t)s * d->F + j] = key_rec[d->maps[s][j]];
-  }
-  FC_CUDA(cudaMallocAsync((void**)&d->dev, d->dev_bytes, ctx->stream));
-  FC_CUDA(cudaMemcpyAsync(d->dev, img.data(), d->dev_bytes, cudaMemcpyHostToDevice, ctx->stream));
-  sync(ctx);
-  std::vector<int> sel(ns);
-  std::iota(sel.begin(), sel.end(), 0);
-  *out = make_entry_view(d, std::move(sel));
+  *out = e;
   LC_API_END
 }
 

@@ -40,6 +40,8 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
 
 void set_last_error(const std::string& m);
 void set_last_oversize(uint64_t needed, uint64_t limit);
+// SnapshotError(what, offset) (errors.hpp:30-35): message "<what> at byte <offset>"
+[[noreturn]] void raise_snap(const std::string& what, uint64_t offset);
 
 #define LC_API_BEGIN try {
 #define LC_API_END                                   \

@@ -13,7 +13,7 @@ namespace fc {
 // POD storage: no TLS destructor, so a C-ABI call made while the process is
 // exiting (e.g. a static owner destroying its context) can still record its error
 static thread_local char g_err[1024];
-static thread_local uint64_t g_over_needed = 0, g_over_limit = 0;
+static thread_local uint64_t g_over_needed = 0, g_over_limit = 0, g_snap_off = 0;
 
 // ---- pinned host staging cache ----
 namespace {
@@ -48,6 +48,11 @@ void set_last_error(const std::string& m) {
   memcpy(g_err, m.data(), n);
   g_err[n] = 0;
 }
+void raise_snap(const std::string& what, uint64_t offset) {
+  g_snap_off = offset;
+  raise(LC_ERR_SNAPSHOT, what + " at byte " + std::to_string(offset));
+}
+
 void set_last_oversize(uint64_t needed, uint64_t limit) {
   g_over_needed = needed;
   g_over_limit = limit;
@@ -243,6 +248,7 @@ void lc_last_oversize(uint64_t* needed, uint64_t* limit) {
   if (needed) *needed = g_over_needed;
   if (limit) *limit = g_over_limit;
 }
+uint64_t lc_last_snapshot_offset(void) { return g_snap_off; }
 const char* lc_version(void) { return "flexcache-b200 0.1 (sm_100a)"; }
 
 

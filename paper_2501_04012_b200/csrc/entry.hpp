@@ -89,6 +89,8 @@ struct lc_entry {
 namespace fc {
 lc_entry* make_entry_view(const std::shared_ptr<EntryData>& d, std::vector<int> sel);
 uint64_t entry_compressed_size(const lc_entry* e);
+// deserialize_entry from the front of bytes[0, len) (codec.cu); *consumed = bytes used
+lc_entry* import_entry(lc_ctx* ctx, const uint8_t* bytes, uint64_t len, uint64_t* consumed);
 // Decompress n (entry, step-index) pairs into out [n][F][E] on the ctx stream.
 void launch_decompress(lc_ctx* ctx, const std::vector<const EntryData*>& ents, const std::vector<int>& step_idx,
                        float* out, const int32_t* fbits_update = nullptr);

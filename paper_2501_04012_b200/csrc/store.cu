@@ -869,3 +869,243 @@ lc_status lc_store_entries(lc_store* s, lc_step_entry* out, int64_t cap, int64_t
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Snapshots (store.cpp:219-364). Host-side byte stream: the index tables and
+// entries are pulled from HBM (lc_index_export / lc_entry_export), the live
+// records come from the host mirror. Load pushes them back (index batch
+// insert with the from_unit rule; entries via import_entry).
+// ---------------------------------------------------------------------------
+namespace fc {
+namespace {
+
+// CRC-32 (IEEE 802.3, reflected 0xEDB88320) = zlib crc32(0, buf, len)
+uint32_t crc32_of(const uint8_t* p, size_t n) {
+  static uint32_t table[256];
+  static bool init = [] {
+    for (uint32_t i = 0; i < 256; ++i) {
+      uint32_t c = i;
+      for (int k = 0; k < 8; ++k) c = (c & 1) ? 0xEDB88320u ^ (c >> 1) : c >> 1;
+      table[i] = c;
+    }
+    return true;
+  }();
+  (void)init;
+  uint32_t c = 0xFFFFFFFFu;
+  for (size_t i = 0; i < n; ++i) c = table[(c ^ p[i]) & 0xFF] ^ (c >> 8);
+  return c ^ 0xFFFFFFFFu;
+}
+
+struct BW {  // ByteWriter (serialize.hpp:17-52), little-endian
+  std::vector<uint8_t> b;
+  void u8(uint8_t v) { b.push_back(v); }
+  void u16(uint16_t v) { u8((uint8_t)v), u8((uint8_t)(v >> 8)); }
+  void u32(uint32_t v) { for (int i = 0; i < 4; ++i) u8((uint8_t)(v >> (8 * i))); }
+  void u64(uint64_t v) { for (int i = 0; i < 8; ++i) u8((uint8_t)(v >> (8 * i))); }
+  void raw(const void* p, size_t n) { b.insert(b.end(), (const uint8_t*)p, (const uint8_t*)p + n); }
+};
+
+struct BR {  // ByteReader (serialize.hpp:54-106): truncation -> SnapshotError at pos
+  const uint8_t* p;
+  uint64_t n, pos = 0;
+  void need(uint64_t k) const {
+    if (pos + k > n) raise_snap("truncated input", pos);
+  }
+  uint8_t u8() { need(1); return p[pos++]; }
+  uint16_t u16() { need(2); uint16_t v = (uint16_t)(p[pos] | (p[pos + 1] << 8)); pos += 2; return v; }
+  uint32_t u32() {
+    need(4);
+    uint32_t v = 0;
+    for (int i = 0; i < 4; ++i) v |= (uint32_t)p[pos + i] << (8 * i);
+    pos += 4;
+    return v;
+  }
+  uint64_t u64() {
+    need(8);
+    uint64_t v = 0;
+    for (int i = 0; i < 8; ++i) v |= (uint64_t)p[pos + i] << (8 * i);
+    pos += 8;
+    return v;
+  }
+  const uint8_t* bytes(uint64_t k) { need(k); const uint8_t* r = p + pos; pos += k; return r; }
+};
+
+void check_status(lc_status st) {
+  if (st != LC_OK) raise(st, lc_last_error());
+}
+
+}  // namespace
+}  // namespace fc
+
+extern "C" {
+
+lc_status lc_snapshot_save(lc_store* s, lc_index* ix, const char* path) {
+  LC_API_BEGIN
+  FC_REQUIRE(s && ix && path, "lc_snapshot_save: null argument");
+  DeviceGuard g(s->ctx->device);
+  BW w;
+  w.raw("FLXC", 4);
+  w.u16(1);
+  w.u8((uint8_t)s->policy);
+  w.u64(s->capacity);
+  w.u64(s->next_seq);
+  const int dim = lc_index_dim(ix);
+  w.u16((uint16_t)dim);
+  const int64_t n = lc_index_size(ix);
+  std::vector<uint64_t> ids(std::max<int64_t>(n, 1));
+  std::vector<float> rows((size_t)std::max<int64_t>(n, 1) * std::max(dim, 1));
+  for (int kind = 0; kind < 3; ++kind) {  // Whole, Object, Background (store.cpp:241-248)
+    if (n) check_status(lc_index_export(ix, kind, ids.data(), rows.data(), n));
+    w.u32((uint32_t)n);
+    for (int64_t i = 0; i < n; ++i) {
+      w.u64(ids[i]);
+      w.raw(rows.data() + (size_t)i * dim, 4ull * dim);
+    }
+  }
+  w.u32((uint32_t)s->prompts.size());
+  std::vector<uint8_t> body;
+  for (const auto& kv : s->prompts) {  // ascending prompt id (std::map)
+    const lc_store::Rec& r = kv.second;
+    const uint64_t elen = entry_compressed_size(r.view);
+    body.resize(elen);
+    uint64_t got = 0;
+    check_status(lc_entry_export(r.view, body.data(), elen, &got));
+    body.resize(got);
+    BW lb;
+    lb.u8((uint8_t)r.live.size());
+    for (const auto& l : r.live) {  // ascending step
+      lb.u8((uint8_t)l.step);
+      lb.u64(l.f);
+      lb.u64(l.last);
+      lb.u64(l.inserted_at);
+      lb.u64(l.seq);
+    }
+    body.insert(body.end(), lb.b.begin(), lb.b.end());
+    w.u32((uint32_t)body.size());
+    w.raw(body.data(), body.size());
+    w.u32(crc32_of(body.data(), body.size()));
+  }
+  FILE* f = fopen(path, "wb");
+  if (!f) raise(LC_ERR_IO, std::string("cannot open snapshot for writing: ") + path);
+  const size_t wr = fwrite(w.b.data(), 1, w.b.size(), f);
+  const int cl = fclose(f);
+  if (wr != w.b.size() || cl != 0) raise(LC_ERR_IO, std::string("snapshot write failed: ") + path);
+  LC_API_END
+}
+
+lc_status lc_snapshot_load(lc_ctx* ctx, const char* path, lc_store** store_out, lc_index** index_out) {
+  LC_API_BEGIN
+  FC_REQUIRE(ctx && path && store_out && index_out, "lc_snapshot_load: null argument");
+  DeviceGuard g(ctx->device);
+  std::vector<uint8_t> raw;
+  {
+    FILE* f = fopen(path, "rb");
+    if (!f) raise(LC_ERR_IO, std::string("cannot open snapshot: ") + path);
+    uint8_t buf[1 << 16];
+    size_t k;
+    while ((k = fread(buf, 1, sizeof buf, f)) > 0) raw.insert(raw.end(), buf, buf + k);
+    fclose(f);
+  }
+  BR r{raw.data(), raw.size()};
+  const uint8_t* magic = r.bytes(4);
+  if (memcmp(magic, "FLXC", 4) != 0) raise_snap("bad magic", 0);
+  const uint16_t version = r.u16();
+  if (version != 1) raise_snap("unsupported version " + std::to_string(version), r.pos - 2);
+  const int policy = r.u8();
+  if (policy > 3) raise_snap("invalid policy byte", r.pos - 1);
+  const uint64_t capacity = r.u64();
+  const uint64_t next_seq = r.u64();
+  const int dim = r.u16();
+  // three tables, zipped back into atomic inserts (store.cpp:297-320)
+  std::vector<uint64_t> tid[3];
+  std::vector<float> trow[3];
+  for (int t = 0; t < 3; ++t) {
+    const uint32_t count = r.u32();
+    for (uint32_t i = 0; i < count; ++i) {
+      tid[t].push_back(r.u64());
+      const uint8_t* v = r.bytes(4ull * dim);
+      const size_t at = trow[t].size();
+      trow[t].resize(at + dim);
+      if (dim) memcpy(trow[t].data() + at, v, 4ull * dim);
+    }
+  }
+  if (tid[0].size() != tid[1].size() || tid[0].size() != tid[2].size())
+    raise_snap("index tables disagree on entry count", r.pos);
+  for (size_t i = 0; i < tid[0].size(); ++i)
+    if (tid[0][i] != tid[1][i] || tid[0][i] != tid[2][i]) raise_snap("index tables disagree on prompt ids", r.pos);
+  std::unique_ptr<lc_store, lc_status (*)(lc_store*)> st(nullptr, lc_store_destroy);
+  std::unique_ptr<lc_index, lc_status (*)(lc_index*)> ix(nullptr, lc_index_destroy);
+  {
+    lc_index* pi = nullptr;
+    check_status(lc_index_create(ctx, dim, (int64_t)tid[0].size(), &pi));
+    ix.reset(pi);
+    lc_store* ps = nullptr;
+    check_status(lc_store_create(ctx, capacity, policy, &ps));
+    st.reset(ps);
+  }
+  if (!tid[0].empty())
+    check_status(lc_index_insert_batch(ix.get(), tid[0].data(), trow[0].data(), trow[1].data(), trow[2].data(),
+                                       (int64_t)tid[0].size(), dim));
+  lc_store* s = st.get();
+  s->next_seq = next_seq;
+  const uint32_t n_prompts = r.u32();
+  for (uint32_t i = 0; i < n_prompts; ++i) {
+    const uint64_t record_pos = r.pos;
+    const uint32_t body_len = r.u32();
+    const uint8_t* body = r.bytes(body_len);
+    const uint32_t crc = r.u32();
+    if (crc32_of(body, body_len) != crc) raise_snap("checksum mismatch in prompt record", record_pos);
+    uint64_t used_e = 0;
+    lc_entry* view = import_entry(ctx, body, body_len, &used_e);
+    std::unique_ptr<lc_entry, lc_status (*)(lc_entry*)> vh(view, lc_entry_release);
+    const EntryData& d = *view->d;
+    BR br{body, body_len, used_e};
+    lc_store::Rec rec;
+    rec.shared = d.shared_bytes();
+    const int n_live = br.u8();
+    for (int k = 0; k < n_live; ++k) {
+      const int sv = br.u8();
+      if (sv < 1 || sv > 50) raise(LC_ERR_INVALID_ARGUMENT, "StepId: value out of range 1..50");  // StepId(sv)
+      lc_store::Live l;
+      l.f = br.u64();
+      l.last = br.u64();
+      l.inserted_at = br.u64();
+      l.seq = br.u64();
+      int si = -1;
+      for (size_t q = 0; q < d.steps.size(); ++q)
+        if (d.steps[q] == sv) si = (int)q;
+      if (si < 0) raise_snap("live step missing from entry data", record_pos);
+      bool dup = false;  // rec.live.emplace keeps the first record of a step
+      for (const auto& x : rec.live) dup |= x.step == sv;
+      if (dup) continue;
+      l.step = sv;
+      l.si = si;
+      l.priv = d.private_bytes(si);
+      rec.live.push_back(l);
+    }
+    if (br.pos != br.n) raise_snap("trailing bytes in prompt record", record_pos);
+    if (rec.live.empty()) raise_snap("prompt record with no live steps", record_pos);
+    std::sort(rec.live.begin(), rec.live.end(), [](const auto& a, const auto& b) { return a.step < b.step; });
+    uint64_t bytes = rec.shared;
+    for (const auto& l : rec.live) bytes += l.priv;
+    s->used += bytes;  // counted even if the prompt id repeats (store.cpp:356-358)
+    const uint64_t prompt = d.prompt;
+    if (s->prompts.count(prompt)) continue;  // prompts_.emplace keeps the first
+    rec.view = vh.release();
+    rec.pslot = s->alloc_prompt();
+    for (auto& l : rec.live) l.slot = s->alloc_live();
+    auto it = s->prompts.emplace(prompt, std::move(rec)).first;
+    for (auto& l : it->second.live) {
+      s->write_live(it->second, l);
+      s->slot_prompt[l.slot] = prompt;
+      ++s->live_count;
+    }
+    s->write_prompt(it->second);
+  }
+  if (r.pos != r.n) raise_snap("trailing bytes after last record", r.pos);
+  *store_out = st.release();
+  *index_out = ix.release();
+  LC_API_END
+}
+
+}  // extern "C"

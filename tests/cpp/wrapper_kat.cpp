@@ -161,6 +161,43 @@ int main() {
     CacheStore tiny(1000, Policy::Lru);
     CHECK(throws<OversizedEntry>([&] { tiny.insert_steps(PromptId{7}, zero, {StepId(5)}, 1); }));
   }
+  if (getenv("KAT_TRACE")) fprintf(stderr, "%s\n", "snapshot round trip");
+  // ---- snapshot: save -> load -> save is bit-exact; bad magic -> SnapshotError at 0
+  {
+    CacheStore st(1ull << 30, Policy::Lrbu);
+    st.insert_steps(PromptId{7}, zero, {StepId(5), StepId(15)}, 1);
+    SimilarityIndex ix(4);
+    const std::vector<float> u{0.5f, 0.5f, 0.5f, 0.5f};
+    ix.insert(Embedding::from_unit(u, EmbeddingKind::Whole), Embedding::from_unit(u, EmbeddingKind::Object),
+              Embedding::from_unit(u, EmbeddingKind::Background), PromptId{7});
+    const std::string p1 = "/tmp/wrapper_kat_a.flxc", p2 = "/tmp/wrapper_kat_b.flxc";
+    save_snapshot(st, ix, p1);
+    SnapshotData d = load_snapshot(p1);
+    save_snapshot(d.store, d.index, p2);
+    auto slurp = [](const std::string& p) {
+      FILE* f = fopen(p.c_str(), "rb");
+      std::vector<char> v;
+      int c;
+      while (f && (c = fgetc(f)) != EOF) v.push_back((char)c);
+      if (f) fclose(f);
+      return v;
+    };
+    const auto a = slurp(p1), b = slurp(p2);
+    CHECK(!a.empty() && a == b);
+    CHECK(d.store.used() == st.used() && d.index.size() == 1);
+    FILE* f = fopen(p2.c_str(), "r+b");
+    if (f) {
+      fputc('X', f);
+      fclose(f);
+    }
+    bool off0 = false;
+    try {
+      load_snapshot(p2);
+    } catch (const SnapshotError& e) {
+      off0 = e.byte_offset == 0;
+    }
+    CHECK(off0);
+  }
   if (getenv("KAT_TRACE")) fprintf(stderr, "%s\n", "index: duplicates");
   // ---- index: duplicates -> smaller id, empty -> none
   {
