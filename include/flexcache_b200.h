@@ -294,6 +294,82 @@ lc_status lc_store_entries(lc_store* s, lc_step_entry* out, int64_t cap, int64_t
 lc_status lc_snapshot_save(lc_store* store, lc_index* index, const char* path);
 /* On success *store / *index are new objects on ctx (destroy as usual). */
 lc_status lc_snapshot_load(lc_ctx* ctx, const char* path, lc_store** store, lc_index** index);
+/* ---------------------------------------------------------------------------
+ * Engine (the reference ships no engine code): the request
+ * pipeline lookup -> decide -> step selection -> get_step / decompress+stitch
+ * -> simulated generation -> update_after_generation, with the latency and
+ * cost models. Requests are processed in order with results identical to
+ * serial execution; a batch shares one exact top-8 lookup per table and
+ * fixes it up on the host for rows inserted / removed by earlier requests.
+ * Definitions the SPEC leaves open (documented in DESIGN.md):
+ *   - a hit whose source has no live step <= the desired one serves nothing
+ *     (actual 0) and is then handled like a miss for latency and update;
+ *   - a decoupled hit serves the largest step both sources hold <= desired;
+ *   - update_after_generation inserts nothing while the prompt is cached.
+ * ------------------------------------------------------------------------- */
+typedef struct lc_engine lc_engine;
+typedef struct lc_engine_config {
+  double hit_threshold;      /* defaults.hpp:13  0.65 */
+  double compress_threshold; /* defaults.hpp:14  0.99 */
+  double bin_edges[4];       /* defaults.hpp:27  0.72 0.79 0.86 0.93 */
+  double t_per_step;         /* defaults.hpp:21  4.84 s */
+  double t_lookup;           /* defaults.hpp:22  0.14 s */
+  double t_extract;          /* defaults.hpp:23  3.6 s  */
+  double t_stitch;           /* defaults.hpp:24  0 s    */
+  int32_t total_steps;       /* defaults.hpp:17  50     */
+  int32_t policy;            /* LC_POLICY_*             */
+  uint64_t capacity;         /* store capacity, compressed_size bytes */
+  int32_t dim, F, H, W, C;   /* embedding dim, latent geometry */
+} lc_engine_config;
+void lc_engine_config_default(lc_engine_config* cfg);
+typedef struct lc_request {
+  uint64_t prompt;
+  uint64_t arrival; /* logical time, non-decreasing */
+} lc_request;
+typedef struct lc_outcome {
+  lc_decision decision; /* decide + similarity_to_step on the exact top-1s   */
+  int32_t actual_step;  /* served step = skipped steps (0: nothing served)   */
+  int32_t n_inserted;   /* steps inserted by update_after_generation          */
+  int32_t n_evicted;    /* steps evicted by that insert                       */
+  int32_t _pad;
+  double latency;       /* t_extract + t_lookup + t_per_step*(50-actual) (+ t_stitch) */
+} lc_outcome;
+typedef struct lc_engine_metrics {
+  uint64_t requests, whole_hits, decoupled_hits, misses;
+  uint64_t skipped_hist[6]; /* skipped steps 0,5,10,15,20,25 */
+  uint64_t skipped_total;
+  double simulated_time;        /* sum of latencies */
+  double computation_savings;   /* skipped_total / (50 * requests) */
+  double mean_latency;
+  double throughput_vs_nocache; /* 50 * t_per_step / mean_latency */
+} lc_engine_metrics;
+typedef struct lc_pricing {
+  double gpu_rate;             /* $/hour (defaults.hpp:33: 3.67) */
+  double storage_rate;         /* $/GB/month (no default) */
+  double provisioned_storage;  /* GB */
+} lc_pricing;
+typedef struct lc_cost_report {
+  double gpu_cost_per_video, storage_cost_per_video, videos_per_month, throughput_vs_nocache, mean_latency;
+} lc_cost_report;
+lc_status lc_engine_create(lc_ctx* ctx, const lc_engine_config* cfg, lc_engine** out);
+lc_status lc_engine_destroy(lc_engine* e);
+/* process_request + update_after_generation for n requests
+ * in order. q_* [n][dim] unit embeddings; latents [n][5][F][H*W*C] fp32 =
+ * each prompt's own latents at steps 5..25; masks [n][F][ceil(H*W/8)].
+ * Host or device buffers. served_dev (device [n][F][E], may be NULL)
+ * receives the served / stitched latent of every hit. On error, out[0..j)
+ * hold the requests completed before the failing one. */
+lc_status lc_engine_process(lc_engine* e, const lc_request* req, int64_t n, const float* q_whole,
+                            const float* q_object, const float* q_background, const float* latents,
+                            const uint8_t* obj_masks, const uint8_t* bg_masks, float* served_dev,
+                            lc_outcome* out);
+lc_status lc_engine_metrics_get(lc_engine* e, lc_engine_metrics* out);
+/* report; zero requests => LC_ERR_INVALID_ARGUMENT. */
+lc_status lc_engine_report(lc_engine* e, const lc_pricing* pricing, lc_cost_report* out);
+/* The engine's index and store (borrowed; e.g. for lc_snapshot_save). */
+lc_index* lc_engine_index(lc_engine* e);
+lc_store* lc_engine_store(lc_engine* e);
+
 /* lrbu_priority / lcbfu_priority (store.cpp:32-42) for n entries. */
 lc_status lc_priority_batch(lc_ctx* ctx, int policy, const lc_step_entry* e, int64_t n,
                             uint64_t now, double* out);

@@ -270,9 +270,6 @@ class Checker:
     def store(self, capacity, policy):
         return _Store(self, capacity, policy)
 
-    def index(self, dim):
-        return _Index(self, dim)
-
     # ---- snapshots (reference only) -----------------------------------------
     def snapshot_save(self, store, index, path):
         self._chk(self._f("snapshot_save")(store.h, index.h, str(path).encode()))
@@ -358,11 +355,11 @@ class _Store:
     def insert(self, prompt, entry: bytes, steps, now):
         buf = np.frombuffer(entry, np.uint8)
         st = np.ascontiguousarray(steps, np.int32)
-        ev = (StepEntryC * 64)()
+        ev = (StepEntryC * 4096)()
         n = C.c_int()
-        self.c._chk(self.c._f("store_insert")(self.h, prompt, _p(buf), buf.size, _p(st), st.size, now, ev, 64,
+        self.c._chk(self.c._f("store_insert")(self.h, prompt, _p(buf), buf.size, _p(st), st.size, now, ev, 4096,
                                               C.byref(n)))
-        return [ev[i].as_tuple() for i in range(min(n.value, 64))]
+        return [ev[i].as_tuple() for i in range(min(n.value, 4096))]
 
     def get_step(self, prompt, desired, now, F=None, E=None):
         act = C.c_int32()

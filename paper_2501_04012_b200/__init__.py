@@ -263,7 +263,7 @@ class SimilarityIndex:
 
     def __del__(self):
         try:
-            if self.h:
+            if self.h and not getattr(self, "_borrowed", None):
                 lib.lc_index_destroy(self.h)
                 self.h = None
         except Exception:
@@ -628,7 +628,7 @@ class CacheStore:
 
     def __del__(self):
         try:
-            if self.h:
+            if self.h and not getattr(self, "_borrowed", None):
                 lib.lc_store_destroy(self.h)
                 self.h = None
         except Exception:
@@ -742,3 +742,105 @@ def load_snapshot(path, ctx: Context | None = None):
     ix = SimilarityIndex.__new__(SimilarityIndex)
     ix.ctx, ix.h = ctx, hi
     return st, ix
+
+
+# ---------------------------------------------------------------------------
+# Engine: request pipeline + latency / cost models
+# ---------------------------------------------------------------------------
+KIND_NAMES = {0: "miss", 1: "whole", 2: "decoupled"}
+
+
+def engine_config(**kw) -> "_capi.EngineConfig":
+    """defaults.hpp values, overridden by keyword (bin_edges as a 4-sequence)."""
+    c = _capi.EngineConfig()
+    lib.lc_engine_config_default(C.byref(c))
+    for k, v in kw.items():
+        if k == "bin_edges":
+            for i, x in enumerate(v):
+                c.bin_edges[i] = float(x)
+        elif k == "policy":
+            c.policy = int(v)
+        else:
+            setattr(c, k, v)
+    return c
+
+
+class Engine:
+    """process_request / update_after_generation / report over an HBM-resident
+    index + store. Requests of one process() call are
+    served in order with one shared exact lookup (see engine.cu)."""
+
+    def __init__(self, config=None, ctx: Context | None = None, **kw):
+        self.ctx = ctx or default_context()
+        self.config = config if config is not None else engine_config(**kw)
+        h = C.c_void_p()
+        _check(lib.lc_engine_create(self.ctx.h, C.byref(self.config), C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib.lc_engine_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    @property
+    def index(self) -> "SimilarityIndex":
+        ix = SimilarityIndex.__new__(SimilarityIndex)
+        ix.ctx, ix.h, ix._borrowed = self.ctx, C.c_void_p(lib.lc_engine_index(self.h)), self
+        return ix
+
+    @property
+    def store(self) -> "CacheStore":
+        st = CacheStore.__new__(CacheStore)
+        st.ctx, st.h, st._cb, st._borrowed = self.ctx, C.c_void_p(lib.lc_engine_store(self.h)), None, self
+        return st
+
+    def process(self, prompts, arrivals, q_whole, q_object, q_background, latents, obj_masks, bg_masks,
+                served=None):
+        """prompts/arrivals [n]; q_* [n][dim]; latents [n][5][F][E] (steps 5..25);
+        masks [n][F][mb]; served: optional device tensor [n][F][E] for the
+        served / stitched latents. Returns a list of outcome dicts."""
+        n = len(prompts)
+        req = (_capi.Request * max(n, 1))()
+        for i in range(n):
+            req[i].prompt = int(prompts[i])
+            req[i].arrival = int(arrivals[i])
+        outs = (_capi.Outcome * max(n, 1))()
+        qw, qo, qb = (_host(x, np.float32) for x in (q_whole, q_object, q_background))
+        lat = _host(latents, np.float32)
+        om, bm = _host(obj_masks, np.uint8), _host(bg_masks, np.uint8)
+        _check(lib.lc_engine_process(self.h, req, n, _ptr(qw), _ptr(qo), _ptr(qb), _ptr(lat), _ptr(om), _ptr(bm),
+                                     None if served is None else _ptr(served), outs))
+        res = []
+        for i in range(n):
+            o = outs[i]
+            d = o.decision
+            res.append({"prompt": int(prompts[i]), "kind": KIND_NAMES[d.kind], "desired_step": d.step,
+                        "whole_id": d.whole_id, "object_id": d.object_id, "background_id": d.background_id,
+                        "score": d.score, "scores": (d.whole_score, d.object_score, d.background_score),
+                        "actual_step": o.actual_step, "n_inserted": o.n_inserted, "n_evicted": o.n_evicted,
+                        "latency": o.latency})
+        return res
+
+    def metrics(self) -> dict:
+        m = _capi.EngineMetrics()
+        _check(lib.lc_engine_metrics_get(self.h, C.byref(m)))
+        return {"requests": m.requests, "whole_hits": m.whole_hits, "decoupled_hits": m.decoupled_hits,
+                "misses": m.misses, "skipped_hist": {5 * i: int(m.skipped_hist[i]) for i in range(6)},
+                "skipped_total": m.skipped_total, "simulated_time": m.simulated_time,
+                "computation_savings": m.computation_savings, "mean_latency": m.mean_latency,
+                "throughput_vs_nocache": m.throughput_vs_nocache}
+
+    def report(self, gpu_rate=3.67, storage_rate=0.0, provisioned_storage=0.0) -> dict:
+        p = _capi.Pricing(gpu_rate, storage_rate, provisioned_storage)
+        r = _capi.CostReport()
+        _check(lib.lc_engine_report(self.h, C.byref(p), C.byref(r)))
+        return {"gpu_cost_per_video": r.gpu_cost_per_video, "storage_cost_per_video": r.storage_cost_per_video,
+                "videos_per_month": r.videos_per_month, "throughput_vs_nocache": r.throughput_vs_nocache,
+                "mean_latency": r.mean_latency}
+
+    def save_snapshot(self, path):
+        _check(lib.lc_snapshot_save(lib.lc_engine_store(self.h), lib.lc_engine_index(self.h),
+                                    os.fspath(path).encode()))

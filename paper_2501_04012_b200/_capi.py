@@ -40,6 +40,36 @@ class Decision(C.Structure):
                 ("score", f64), ("whole_score", f64), ("object_score", f64), ("background_score", f64)]
 
 
+class EngineConfig(C.Structure):
+    _fields_ = [("hit_threshold", f64), ("compress_threshold", f64), ("bin_edges", f64 * 4), ("t_per_step", f64),
+                ("t_lookup", f64), ("t_extract", f64), ("t_stitch", f64), ("total_steps", i32), ("policy", i32),
+                ("capacity", u64), ("dim", i32), ("F", i32), ("H", i32), ("W", i32), ("C", i32)]
+
+
+class Request(C.Structure):
+    _fields_ = [("prompt", u64), ("arrival", u64)]
+
+
+class Outcome(C.Structure):
+    _fields_ = [("decision", Decision), ("actual_step", i32), ("n_inserted", i32), ("n_evicted", i32),
+                ("_pad", i32), ("latency", f64)]
+
+
+class EngineMetrics(C.Structure):
+    _fields_ = [("requests", u64), ("whole_hits", u64), ("decoupled_hits", u64), ("misses", u64),
+                ("skipped_hist", u64 * 6), ("skipped_total", u64), ("simulated_time", f64),
+                ("computation_savings", f64), ("mean_latency", f64), ("throughput_vs_nocache", f64)]
+
+
+class Pricing(C.Structure):
+    _fields_ = [("gpu_rate", f64), ("storage_rate", f64), ("provisioned_storage", f64)]
+
+
+class CostReport(C.Structure):
+    _fields_ = [("gpu_cost_per_video", f64), ("storage_cost_per_video", f64), ("videos_per_month", f64),
+                ("throughput_vs_nocache", f64), ("mean_latency", f64)]
+
+
 class LookupStats(C.Structure):
     _fields_ = [("queries", u64), ("certified", u64), ("fallback", u64), ("exact_scans", u64),
                 ("max_abs_err", f64)]
@@ -106,6 +136,14 @@ _sig("lc_decompress_stitch_batch", st, vp, vp, vp, vp, i64, vp)
 _sig("lc_stitch_batch", st, vp, vp, vp, vp, vp, i64, C.c_int, C.c_int, C.c_int, C.c_int, vp)
 _sig("lc_store_create", st, vp, u64, C.c_int, C.POINTER(vp))
 _sig("lc_snapshot_save", st, vp, vp, C.c_char_p)
+_sig("lc_engine_config_default", None, C.POINTER(EngineConfig))
+_sig("lc_engine_create", st, vp, C.POINTER(EngineConfig), C.POINTER(vp))
+_sig("lc_engine_destroy", st, vp)
+_sig("lc_engine_process", st, vp, C.POINTER(Request), i64, vp, vp, vp, vp, vp, vp, vp, C.POINTER(Outcome))
+_sig("lc_engine_metrics_get", st, vp, C.POINTER(EngineMetrics))
+_sig("lc_engine_report", st, vp, C.POINTER(Pricing), C.POINTER(CostReport))
+_sig("lc_engine_index", vp, vp)
+_sig("lc_engine_store", vp, vp)
 _sig("lc_snapshot_load", st, vp, C.c_char_p, C.POINTER(vp), C.POINTER(vp))
 _sig("lc_store_destroy", st, vp)
 _sig("lc_store_insert", st, vp, u64, vp, vp, C.c_int, u64, vp, C.c_int, C.POINTER(C.c_int))

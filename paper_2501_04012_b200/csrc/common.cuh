@@ -230,7 +230,7 @@ namespace fc {
 // (score desc, id asc) ordering used by every top-k in the library: the
 // generalisation of query_top1's strict '>' over ascending ids
 // (vindex.cpp:58-72).
-__device__ __forceinline__ bool better(double s1, uint64_t i1, double s2, uint64_t i2) {
+__host__ __device__ __forceinline__ bool better(double s1, uint64_t i1, double s2, uint64_t i2) {
   return s1 > s2 || (s1 == s2 && i1 < i2);
 }
 

@@ -1,0 +1,1 @@
+timeout -s KILL 1200 python -m pytest tests -m gpu -q -x 2>&1 | tail -8
