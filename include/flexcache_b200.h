@@ -269,6 +269,13 @@ lc_status lc_store_get_step(lc_store* s, uint64_t prompt, int desired, uint64_t 
                             int32_t* actual, float* out_dev);
 lc_status lc_store_evict_one(lc_store* s, uint64_t now, lc_step_entry* out);
 lc_status lc_store_evict_step(lc_store* s, uint64_t prompt, int step, int32_t* removed);
+/* The step evict_one(now) would remove next (same StepEntry, with its policy
+ * key), without removing it: the per-shard candidate of a global eviction
+ * across entry-sharded stores. Empty => LC_ERR_LOGIC. */
+lc_status lc_store_peek(lc_store* s, uint64_t now, lc_step_entry* out, double* key);
+/* store.hpp:113 next_seq_: sharded stores keep one global insertion counter. */
+uint64_t lc_store_next_seq(lc_store* s);
+lc_status lc_store_set_next_seq(lc_store* s, uint64_t seq);
 uint64_t lc_store_used(lc_store* s);
 uint64_t lc_store_recompute_used(lc_store* s);
 uint64_t lc_store_capacity(lc_store* s);

@@ -972,8 +972,9 @@ static void put_entry(const OStore* s, const ORec* r, const OLive* l, uint64_t c
   o->inserted_seq = l->inserted_seq; o->capacity = cap;
 }
 
-/* min_priority_step + evict_one, src/store.cpp:113-157. */
-static int evict_one_impl(OStore* s, uint64_t now, orc_step_entry* out) {
+/* min_priority_step + evict_one, src/store.cpp:113-157; peek = 1 reports the
+ * victim (and its key) without removing it (sharded global eviction). */
+static int evict_one_impl2(OStore* s, uint64_t now, orc_step_entry* out, int peek, double* key_out) {
   if (s->n == 0) return fail(ORC_ERR_LOGIC, "evict_one: store is empty");
   int64_t bri = -1; int bli = -1; double bkey = 0.0; uint64_t bcap = 0, bseq = 0;
   for (int64_t ri = 0; ri < s->n; ++ri) {
@@ -994,13 +995,25 @@ static int evict_one_impl(OStore* s, uint64_t now, orc_step_entry* out) {
     }
   }
   put_entry(s, s->recs[bri], &s->recs[bri]->live[bli], bcap, out);
-  remove_step(s, bri, bli);
+  if (key_out) *key_out = bkey;
+  if (!peek) remove_step(s, bri, bli);
   return ORC_OK;
+}
+
+static int evict_one_impl(OStore* s, uint64_t now, orc_step_entry* out) {
+  return evict_one_impl2(s, now, out, 0, NULL);
 }
 
 int orc_store_evict_one(void* h, uint64_t now, orc_step_entry* out) {
   return evict_one_impl((OStore*)h, now, out);
 }
+
+int orc_store_peek(void* h, uint64_t now, orc_step_entry* out, double* key) {
+  return evict_one_impl2((OStore*)h, now, out, 1, key);
+}
+
+uint64_t orc_store_next_seq(void* h) { return ((OStore*)h)->next_seq; }
+void orc_store_set_next_seq(void* h, uint64_t seq) { ((OStore*)h)->next_seq = seq; }
 
 /* insert_steps, src/store.cpp:53-91. */
 int orc_store_insert(void* h, uint64_t prompt, const uint8_t* entry, uint64_t len,

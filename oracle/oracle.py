@@ -102,6 +102,11 @@ class Checker:
         fn("store_get_step").argtypes = [C.c_void_p, C.c_uint64, C.c_int, C.c_uint64, C.POINTER(C.c_int32),
                                          C.c_void_p]
         fn("store_evict_one").argtypes = [C.c_void_p, C.c_uint64, C.POINTER(StepEntryC)]
+        if kind == "orc":
+            fn("store_peek").argtypes = [C.c_void_p, C.c_uint64, C.POINTER(StepEntryC), C.POINTER(C.c_double)]
+            fn("store_next_seq").argtypes = [C.c_void_p]
+            fn("store_next_seq").restype = C.c_uint64
+            fn("store_set_next_seq").argtypes = [C.c_void_p, C.c_uint64]
         fn("store_evict_step").argtypes = [C.c_void_p, C.c_uint64, C.c_int, C.POINTER(C.c_int32)]
         for n in ("store_used", "store_recompute_used"):
             fn(n).argtypes = [C.c_void_p]
@@ -372,6 +377,18 @@ class _Store:
         e = StepEntryC()
         self.c._chk(self.c._f("store_evict_one")(self.h, now, C.byref(e)))
         return e.as_tuple()
+
+    def peek(self, now):
+        """(StepEntry tuple, key) evict_one(now) would take, without evicting."""
+        e, k = StepEntryC(), C.c_double()
+        self.c._chk(self.c._f("store_peek")(self.h, now, C.byref(e), C.byref(k)))
+        return e.as_tuple(), k.value
+
+    def next_seq(self):
+        return self.c._f("store_next_seq")(self.h)
+
+    def set_next_seq(self, seq):
+        self.c._f("store_set_next_seq")(self.h, seq)
 
     def evict_step(self, prompt, step):
         r = C.c_int32()

@@ -111,6 +111,11 @@ int orc_topk_flat(const float* table, const uint64_t* ids, int64_t n_rows, int d
 int orc_decide(double w, double o, double b, double threshold, int32_t* kind, double* score);
 int orc_similarity_to_step(double score, double threshold, const double* edges4,
                            int32_t* step);
+/*  - peek = evict_one without the removal (store.cpp:113-157 argmin) and the
+ *    insertion counter (store.hpp:113), for entry-sharded stores. */
+int orc_store_peek(void* h, uint64_t now, orc_step_entry* out, double* key);
+uint64_t orc_store_next_seq(void* h);
+void orc_store_set_next_seq(void* h, uint64_t seq);
 
 #ifdef __cplusplus
 }

@@ -671,6 +671,19 @@ class CacheStore:
             return None
         return out, act.value
 
+    def peek(self, now: int):
+        """(StepEntry, policy key) that evict_one(now) would remove, without
+        removing it (per-shard candidate of a global eviction)."""
+        e, k = StepEntry(), C.c_double()
+        _check(lib.lc_store_peek(self.h, now, C.byref(e), C.byref(k)))
+        return e, k.value
+
+    def next_seq(self) -> int:
+        return int(lib.lc_store_next_seq(self.h))
+
+    def set_next_seq(self, seq: int):
+        _check(lib.lc_store_set_next_seq(self.h, seq))
+
     def evict_one(self, now: int) -> StepEntry:
         e = StepEntry()
         _check(lib.lc_store_evict_one(self.h, now, C.byref(e)))

@@ -136,6 +136,9 @@ _sig("lc_decompress_stitch_batch", st, vp, vp, vp, vp, i64, vp)
 _sig("lc_stitch_batch", st, vp, vp, vp, vp, vp, i64, C.c_int, C.c_int, C.c_int, C.c_int, vp)
 _sig("lc_store_create", st, vp, u64, C.c_int, C.POINTER(vp))
 _sig("lc_snapshot_save", st, vp, vp, C.c_char_p)
+_sig("lc_store_peek", st, vp, u64, C.POINTER(StepEntry), C.POINTER(f64))
+_sig("lc_store_next_seq", u64, vp)
+_sig("lc_store_set_next_seq", st, vp, u64)
 _sig("lc_engine_config_default", None, C.POINTER(EngineConfig))
 _sig("lc_engine_create", st, vp, C.POINTER(EngineConfig), C.POINTER(vp))
 _sig("lc_engine_destroy", st, vp)

@@ -595,7 +595,9 @@ struct lc_store {
     std::priority_queue<HE, std::vector<HE>, std::greater<HE>> heap;
     Evictor(lc_store* st, uint64_t n) : s(st), now(n) {}
 
-    lc_step_entry next() {
+    // The slot evict_one(now) takes next (exact argmin of (key, seq) over the
+    // live table), with its key; only stale bookkeeping is dropped.
+    int64_t pick(double* key_out, uint64_t* seq_out) {
       if (s->prompts.empty()) raise(LC_ERR_LOGIC, "evict_one: store is empty");
       for (;;) {
         if (!have) {
@@ -631,8 +633,22 @@ struct lc_store {
             vseq = t.seq;
           }
         }
-        return evict_slot(victim);
+        if (key_out) *key_out = vkey;
+        if (seq_out) *seq_out = vseq;
+        return victim;
       }
+    }
+
+    lc_step_entry next() { return evict_slot(pick(nullptr, nullptr)); }
+
+    // the StepEntry evict_slot(slot) would return, without evicting
+    lc_step_entry describe(int64_t slot) const {
+      const auto it = s->prompts.find(s->slot_prompt.at(slot));
+      const Rec& r = it->second;
+      for (const Live& l : r.live)
+        if (l.slot == slot)
+          return lc_step_entry{it->first, l.step, 0, l.f, l.last, l.inserted_at, l.seq, l.priv + r.shared / r.live.size()};
+      raise(LC_ERR_INTERNAL, "evictor: slot not live");
     }
 
     lc_step_entry evict_slot(int64_t slot) {
@@ -799,6 +815,27 @@ lc_status lc_store_evict_one(lc_store* s, uint64_t now, lc_step_entry* out) {
   DeviceGuard g(s->ctx->device);
   lc_step_entry v = s->evictor(now).next();
   if (out) *out = v;
+  LC_API_END
+}
+
+lc_status lc_store_peek(lc_store* s, uint64_t now, lc_step_entry* out, double* key) {
+  LC_API_BEGIN
+  FC_REQUIRE(s, "null store");
+  DeviceGuard g(s->ctx->device);
+  lc_store::Evictor& ev = s->evictor(now);
+  double k = 0.0;
+  const int64_t slot = ev.pick(&k, nullptr);
+  if (out) *out = ev.describe(slot);
+  if (key) *key = k;
+  LC_API_END
+}
+
+uint64_t lc_store_next_seq(lc_store* s) { return s ? s->next_seq : 0; }
+lc_status lc_store_set_next_seq(lc_store* s, uint64_t seq) {
+  LC_API_BEGIN
+  FC_REQUIRE(s, "null store");
+  FC_REQUIRE(seq >= s->next_seq, "lc_store_set_next_seq: sequence numbers only move forward");
+  s->next_seq = seq;
   LC_API_END
 }
 

@@ -21,7 +21,7 @@ from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["owner_of", "ShardedIndex", "pack_candidates", "unpack_candidates"]
+__all__ = ["owner_of", "ShardedIndex", "ShardedStore", "pack_candidates", "unpack_candidates"]
 
 
 def owner_of(prompt_ids, world: int):
@@ -138,3 +138,152 @@ class ShardedIndex:
         (wi, ws, _), (oi, os_, _), (bi, bs, _) = top
         return decide_batch(wi[:, 0], ws[:, 0], oi[:, 0], os_[:, 0], bi[:, 0], bs[:, 0], hit_threshold, edges,
                             ctx=self.index.ctx)
+
+
+# ---------------------------------------------------------------------------
+# Entry-sharded CacheStore under ONE global capacity budget
+# ---------------------------------------------------------------------------
+CACHEABLE = (5, 10, 15, 20, 25)
+
+
+class ShardedStore:
+    """CacheStore (store.hpp:48-120) whose (prompt, step) records live on the
+    owner rank (id mod G) while capacity, eviction order and the insertion
+    counter are global. SPMD: every rank calls every operation in the same
+    order (the engine's request order); the owner passes the entry.
+
+    Exactness: a step's policy key depends only on its own prompt's records
+    (store.cpp:113-136), which all live on the owner, so the global victim of
+    evict_one is the minimum over the ranks' local victims by (key, seq) —
+    one small all-gather of each rank's candidate (lc_store_peek) per
+    eviction. next_seq_ (store.hpp:113) is replayed identically on every rank.
+    The sequence of victims, used() and every StepEntry equal the unsharded
+    store's.
+
+    local      this rank's store with unbounded capacity: the product
+               ``CacheStore`` or (CPU tests) an adapter over the oracle store,
+               exposing insert_steps / get_step / evict_one / peek / used /
+               step_count / contains / set_next_seq
+    entry_info callable(entry) -> (shared_bytes, {step: private_bytes}) (owner only)
+    """
+
+    FIELDS = 10  # present, key bits, seq, prompt, step, f, last, inserted_at, capacity, local used()
+
+    def __init__(self, capacity, local, entry_info, group=None, device=None):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist = torch, dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.capacity = int(capacity)
+        self.local = local
+        self.entry_info = entry_info
+        self.seq = 0
+        self._nccl = dist.get_backend(group) == "nccl"
+        self.device = device if device is not None else ("cuda" if self._nccl else "cpu")
+
+    def owner(self, prompt) -> int:
+        return int(prompt) % self.world
+
+    # ---- collectives -----------------------------------------------------
+    def _all_gather(self, row):
+        torch, dist = self.torch, self.dist
+        t = torch.as_tensor(np.asarray(row, dtype=np.int64), device=self.device)
+        parts = [torch.empty_like(t) for _ in range(self.world)]
+        dist.all_gather(parts, t, group=self.group)
+        return torch.stack(parts).cpu().numpy()
+
+    def _bcast(self, row, src):
+        torch, dist = self.torch, self.dist
+        t = torch.as_tensor(np.asarray(row, dtype=np.int64), device=self.device).clone()
+        dist.broadcast(t, src=dist.get_global_rank(self.group, src) if self.group is not None else src,
+                       group=self.group)
+        return t.cpu().numpy()
+
+    def used(self) -> int:
+        return int(self._all_gather([self.local.used()])[:, 0].sum())
+
+    def step_count(self) -> int:
+        return int(self._all_gather([self.local.step_count()])[:, 0].sum())
+
+    # ---- global eviction -------------------------------------------------
+    def _candidates(self, now):
+        """One all-gather: every rank's local victim (lc_store_peek) and used()."""
+        if self.local.step_count() == 0:
+            row = [0] * (self.FIELDS - 1)
+        else:
+            e, key = self.local.peek(now)  # e = (prompt, step, f, last, inserted_at, seq, capacity)
+            e = e.as_tuple() if hasattr(e, "as_tuple") else tuple(e)
+            kb = int(np.float64(key).view(np.int64))
+            row = [1, kb, e[5], e[0], e[1], e[2], e[3], e[4], e[6]]
+        return self._all_gather(row + [self.local.used()])
+
+    def evict_one(self, now, g=None):
+        """The global (key, seq) minimum; identical StepEntry tuple on every rank."""
+        if g is None:
+            g = self._candidates(now)
+        live = [r for r in range(self.world) if g[r, 0]]
+        if not live:
+            raise LookupError("evict_one: store is empty")  # std::logic_error (store.cpp:148)
+        win = min(live, key=lambda r: (float(np.int64(g[r, 1]).view(np.float64)), int(np.uint64(g[r, 2]))))
+        row = g[win]
+        ent = (int(np.uint64(row[3])), int(row[4]), int(np.uint64(row[5])), int(np.uint64(row[6])),
+               int(np.uint64(row[7])), int(np.uint64(row[2])), int(np.uint64(row[8])))
+        if win == self.rank:
+            got = self.local.evict_one(now)
+            got = got.as_tuple() if hasattr(got, "as_tuple") else tuple(got)
+            assert tuple(int(x) for x in got) == ent, (got, ent)
+        return ent
+
+    def insert_steps(self, prompt, entry, steps, now):
+        """insert_steps (store.cpp:53-91) with the validation, OversizedEntry
+        and eviction loop decided globally; returns the evicted StepEntry
+        tuples (same list on every rank)."""
+        own = self.owner(prompt)
+        steps = [int(s) for s in steps]
+        status, standalone = 0, 0
+        if self.rank == own:
+            try:
+                if not steps:
+                    raise ValueError("insert_steps: empty step list")
+                shared, priv = self.entry_info(entry)
+                for s in steps:
+                    if s not in CACHEABLE:
+                        raise ValueError("insert_steps: step not cacheable")
+                    if s not in priv:
+                        raise ValueError("insert_steps: step missing from entry")
+                if self.local.contains(prompt):
+                    raise ValueError("insert_steps: prompt already cached")
+                standalone = shared + sum(priv[s] for s in set(steps))
+                status = 2 if standalone > self.capacity else 0
+            except ValueError:
+                status = 1
+        st, standalone = (int(x) for x in self._bcast([status, standalone], own))
+        if st == 1:
+            raise ValueError("insert_steps: rejected by the owner shard")
+        if st == 2:
+            raise OverflowError(f"entry of {standalone} bytes exceeds capacity limit of {self.capacity} bytes")
+        evicted = []
+        while True:
+            g = self._candidates(now)
+            if int(g[:, self.FIELDS - 1].sum()) + standalone <= self.capacity:
+                break
+            evicted.append(self.evict_one(now, g))
+        if self.rank == own:
+            self.local.set_next_seq(self.seq)
+            self.local.insert_steps(prompt, entry, steps, now)
+        self.seq += len(set(steps))
+        return evicted
+
+    def get_step(self, prompt, desired, now, **kw):
+        """get_step on the owner (f / last_access bump, decompress there);
+        returns (actual step, owner-local result or None) on every rank."""
+        own = self.owner(prompt)
+        res = None
+        actual = 0
+        if self.rank == own:
+            res = self.local.get_step(prompt, desired, now, **kw)
+            actual = int(res[1]) if res else 0
+        actual = int(self._bcast([actual], own)[0])
+        return actual, res

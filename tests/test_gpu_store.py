@@ -174,3 +174,97 @@ def test_eviction_burst_both_scoring_paths(fc, orc, synth, policy, sort_path):
         assert st.used() == ot.used() == st.recompute_used()
     finally:
         del os.environ["FC_SCORE_SORT"]
+
+
+def _gpu_store_worker(rank, world, port, policy, seed, out_dir):
+    import pickle
+    import socket  # noqa: F401
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    sys.path.insert(0, os.path.join(root, "oracle"))
+    sys.path.insert(0, os.path.join(root, "tests"))
+    import torch.distributed as dist
+    from oracle import Checker
+    import paper_2501_04012_b200 as fc
+    from paper_2501_04012_b200 import sharded, synth
+    from test_sharded import _store_trace
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    orc = Checker("orc")
+    ents, ops, cap = _store_trace(orc, synth, seed)
+    dev_ents = {p: fc.deserialize_entry(b) for p, b in ents.items()}
+
+    def info(e):
+        i = e.info()
+        return i.shared_bytes, {i.steps[k]: i.private_bytes[k] for k in range(i.n_steps)}
+
+    class Local(fc.CacheStore):
+        def get_step(self, p, d, now):
+            return super().get_step(p, d, now, want_latent=False)
+
+    sh = sharded.ShardedStore(cap, Local(1 << 62, fc.Policy(policy)), info)
+    ref = orc.store(cap, policy) if rank == 0 else None
+    log, ref_log = [], []
+    for op, p, x, now in ops:
+        if op == "ins":
+            try:
+                got = [tuple(int(v) for v in e) for e in sh.insert_steps(p, dev_ents[p], x, now)]
+            except (ValueError, OverflowError) as e:
+                got = type(e).__name__
+            log.append(got)
+            if ref is not None:
+                try:
+                    ref_log.append([tuple(int(v) for v in e) for e in ref.insert(p, ents[p], x, now)])
+                except Exception as e:  # noqa: BLE001
+                    ref_log.append("OverflowError" if e.code == 4 else "ValueError")
+        elif op == "get":
+            log.append(sh.get_step(p, x, now)[0])
+            if ref is not None:
+                ref_log.append(ref.get_step(p, x, now)[0])
+        else:
+            try:
+                log.append(sh.evict_one(now))
+            except LookupError:
+                log.append("empty")
+            if ref is not None:
+                try:
+                    ref_log.append(tuple(int(v) for v in ref.evict_one(now)))
+                except Exception:  # noqa: BLE001
+                    ref_log.append("empty")
+        if ref is not None:
+            ref_log.append(ref.used())
+        log.append(sh.used())
+    with open(os.path.join(out_dir, f"g{rank}.pkl"), "wb") as f:
+        pickle.dump({"log": log, "ref": ref_log}, f)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("policy", [0, 3])
+def test_sharded_product_stores_global_budget(tmp_path, policy):
+    """Two ranks (gloo, both on cuda:0), each a product CacheStore shard with
+    lc_store_peek candidates: the global eviction sequence equals the
+    unsharded reference-restatement store's."""
+    import pickle
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    mp.spawn(_gpu_store_worker, args=(2, port, policy, 21 + policy, str(tmp_path)), nprocs=2, join=True)
+    g0 = pickle.load(open(tmp_path / "g0.pkl", "rb"))
+    g1 = pickle.load(open(tmp_path / "g1.pkl", "rb"))
+    assert g0["log"] == g1["log"] == g0["ref"]
+
+
+def test_peek_matches_evict_one(fc, synth):
+    ents = _tiny_entries(fc, synth, 40, 5)
+    st = fc.CacheStore(1 << 40, fc.Policy.Lrbu)
+    for i, (p, (e, _)) in enumerate(ents.items()):
+        st.insert_steps(p, e, [5, 15, 25], i)
+    for _ in range(60):
+        e, k = st.peek(100)
+        assert e.as_tuple() == st.evict_one(100).as_tuple()

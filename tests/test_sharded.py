@@ -139,3 +139,138 @@ def test_pack_unpack_roundtrip():
         bi, bs, bc = back[t]
         assert (bi[1] == ids[t]).all() and (bs[0].view(torch.int64) == sc[t].view(torch.int64)).all()
         assert (bc[1] == cnt[t]).all()
+
+
+# ---------------------------------------------------------------------------
+# entry-sharded store under one global capacity budget
+# ---------------------------------------------------------------------------
+class _OrcLocal:
+    """A rank's local store: the C oracle's CacheStore with unbounded capacity."""
+
+    def __init__(self, orc, policy):
+        self.s = orc.store(1 << 62, policy)
+
+    def insert_steps(self, p, entry, steps, now):
+        return self.s.insert(p, entry, steps, now)
+
+    def get_step(self, p, d, now):
+        a, _ = self.s.get_step(p, d, now)
+        return (None, a) if a else None
+
+    def evict_one(self, now):
+        return self.s.evict_one(now)
+
+    def peek(self, now):
+        return self.s.peek(now)
+
+    def used(self):
+        return self.s.used()
+
+    def step_count(self):
+        return self.s.step_count()
+
+    def contains(self, p):
+        return any(e[0] == p for e in self.s.entries())
+
+    def set_next_seq(self, seq):
+        self.s.set_next_seq(seq)
+
+
+def _store_trace(orc, synth, seed, n_prompts=40, n_ops=400):
+    """Entries (bytes) and a random op list shared by every rank."""
+    dims = (4, 4, 2)
+    rng = np.random.default_rng(seed)
+    ents = {}
+    for i in range(n_prompts):
+        r = tuple(float(x) for x in rng.uniform(0, 1, 5))
+        lat = synth.latents(seed * 1000 + i, F=4, dims=dims, redundancy=r)
+        om, bm = synth.rect_masks(4, 4, 4, i)
+        ents[100 + i] = orc.compress(lat, synth.CACHED_STEPS, om, bm, dims, 100 + i)
+    ops, now = [], 0
+    keys = sorted(ents)
+    for _ in range(n_ops):
+        now += int(rng.integers(0, 3))
+        p = int(rng.choice(keys))
+        u = rng.random()
+        if u < 0.45:
+            st = sorted(int(x) for x in rng.choice(synth.CACHED_STEPS, size=int(rng.integers(1, 6)), replace=False))
+            ops.append(("ins", p, st, now))
+        elif u < 0.85:
+            ops.append(("get", p, int(rng.choice(synth.CACHED_STEPS)), now))
+        else:
+            ops.append(("evict", 0, 0, now))
+    sizes = sorted(len(b) for b in ents.values())
+    return ents, ops, sizes[len(sizes) // 2] * 8
+
+
+def _store_worker(rank, world, port, policy, seed, out_dir):
+    import sys
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import torch.distributed as dist
+    from oracle import Checker
+    from paper_2501_04012_b200 import sharded, synth
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    orc = Checker("orc")
+    ents, ops, cap = _store_trace(orc, synth, seed)
+
+    def info(b):
+        d = orc.entry_info(b)
+        return d["shared"], dict(zip(d["steps"], d["private"]))
+
+    sh = sharded.ShardedStore(cap, _OrcLocal(orc, policy), info)
+    ref = orc.store(cap, policy) if rank == 0 else None
+    log, ref_log = [], []
+    for op, p, x, now in ops:
+        if op == "ins":
+            try:
+                got = [tuple(int(v) for v in e) for e in sh.insert_steps(p, ents[p], x, now)]
+            except (ValueError, OverflowError) as e:
+                got = type(e).__name__
+            log.append(got)
+            if ref is not None:
+                try:
+                    exp = [tuple(int(v) for v in e) for e in ref.insert(p, ents[p], x, now)]
+                except Exception as e:  # noqa: BLE001
+                    exp = "OverflowError" if e.code == 4 else "ValueError"
+                ref_log.append(exp)
+        elif op == "get":
+            a, _ = sh.get_step(p, x, now)
+            log.append(a)
+            if ref is not None:
+                ref_log.append(ref.get_step(p, x, now)[0])
+        else:
+            try:
+                log.append(sh.evict_one(now))
+            except LookupError:
+                log.append("empty")
+            if ref is not None:
+                try:
+                    ref_log.append(tuple(int(v) for v in ref.evict_one(now)))
+                except Exception:  # noqa: BLE001
+                    ref_log.append("empty")
+        if ref is not None:
+            ref_log.append(ref.used())
+        log.append(sh.used())
+    import pickle
+    with open(os.path.join(out_dir, f"s{rank}.pkl"), "wb") as f:
+        pickle.dump({"log": log, "ref": ref_log, "local_steps": sh.local.step_count()}, f)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("policy", [0, 1, 2, 3])
+def test_sharded_store_global_budget_matches_unsharded(tmp_path, policy):
+    import pickle
+    import torch.multiprocessing as mp
+    world = 2
+    mp.spawn(_store_worker, args=(world, _free_port(), policy, 5 + policy, str(tmp_path)), nprocs=world,
+             join=True)
+    r0 = pickle.load(open(tmp_path / "s0.pkl", "rb"))
+    r1 = pickle.load(open(tmp_path / "s1.pkl", "rb"))
+    assert r0["log"] == r1["log"]          # every rank sees the same global outcome
+    assert r0["log"] == r0["ref"]          # ... which is the unsharded store's
+    assert r0["local_steps"] > 0 and r1["local_steps"] > 0
+    assert any(isinstance(x, list) and x for x in r0["log"])  # inserts did evict
