@@ -169,6 +169,7 @@ __global__ void __launch_bounds__(SEG_T) k_head_seg(const ScoreItem* __restrict_
 // more than CAP survivors, the segmented sort above is used instead.
 constexpr int NBIN = 4096;
 constexpr int CAP = SEG;
+constexpr int REFINE = 2 * SCORE_H;  // refine the threshold bin above this many survivors (smaller final sort)
 
 __global__ void k_policy_keys(const DevLive* __restrict__ live, int64_t n_slots, const DevPrompt* __restrict__ prompts,
                               int policy, uint64_t now, uint64_t* __restrict__ K, unsigned long long* __restrict__ mm,
@@ -256,20 +257,68 @@ __global__ void __launch_bounds__(1024) k_policy_pick(const unsigned* __restrict
   if (threadIdx.x == 0) {
     pick[0] = s_bin;
     pick[1] = (int)c[s_bin];
+    pick[2] = s_bin > 0 ? (int)c[s_bin - 1] : 0;  // items in bins below the threshold bin
   }
+}
+
+// Refinement when the first pick leaves more than REFINE survivors (a dense
+// key range near the minimum): histogram the next 12 bits of the keys inside that bin and pick
+// again with the remaining budget H - pick[2]. pick[3] = sub-bin threshold,
+// pick[4] = final survivor count (pick[1] when no refinement is needed).
+__global__ void k_policy_hist2(const uint64_t* __restrict__ K, int64_t n_slots, const unsigned long long* __restrict__ mm,
+                               const int* __restrict__ pick, unsigned* __restrict__ hist2) {
+  if (pick[1] <= REFINE) return;
+  __shared__ unsigned h[NBIN];
+  for (int t = threadIdx.x; t < NBIN; t += blockDim.x) h[t] = 0;
+  __syncthreads();
+  const uint64_t lo = mm[0], hi = mm[1];
+  const int sh = bin_shift(lo, hi);
+  const int sh2 = sh > 12 ? sh - 12 : 0;
+  const uint64_t tb = (uint64_t)pick[0];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_slots; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = K[i];
+    if (k != ~0ull && ((k - lo) >> sh) == tb) atomicAdd(&h[((k - lo) >> sh2) & (NBIN - 1)], 1u);
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < NBIN; t += blockDim.x)
+    if (h[t]) atomicAdd(&hist2[t], h[t]);
+}
+
+__global__ void k_policy_pick2(const unsigned* __restrict__ hist2, int H, int* __restrict__ pick) {
+  if (threadIdx.x != 0) return;
+  if (pick[1] <= REFINE) {
+    pick[3] = NBIN - 1;
+    pick[4] = pick[1];
+    return;
+  }
+  const unsigned need = (unsigned)(H - pick[2]);
+  unsigned acc = 0;
+  int b = NBIN - 1;
+  for (int t = 0; t < NBIN; ++t) {
+    acc += hist2[t];
+    if (acc >= need) {
+      b = t;
+      break;
+    }
+  }
+  pick[3] = b;
+  pick[4] = pick[2] + (int)acc;
 }
 
 __global__ void k_policy_collect(const uint64_t* __restrict__ K, const DevLive* __restrict__ live, int64_t n_slots,
                                  const unsigned long long* __restrict__ mm, const int* __restrict__ pick,
                                  ScoreItem* __restrict__ out, int* __restrict__ n_out) {
-  const int c = pick[1];
+  const int c = pick[4];
   if (c > CAP) return;  // host takes the segmented-sort path
   const uint64_t lo = mm[0], hi = mm[1];
   const int sh = bin_shift(lo, hi);
-  const uint64_t tb = (uint64_t)pick[0];
+  const int sh2 = sh > 12 ? sh - 12 : 0;
+  const uint64_t tb = (uint64_t)pick[0], tb2 = (uint64_t)pick[3];
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_slots; i += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t k = K[i];
-    if (k != ~0ull && ((k - lo) >> sh) <= tb) {
+    if (k == ~0ull) continue;
+    const uint64_t b = (k - lo) >> sh;
+    if (b < tb || (b == tb && (((k - lo) >> sh2) & (NBIN - 1)) <= tb2)) {
       const int at = atomicAdd(n_out, 1);
       if (at < CAP) out[at] = ScoreItem{k, live[i].seq, i};
     }
@@ -448,9 +497,13 @@ struct lc_store {
     ++scorings;
     const int64_t n_slots = (int64_t)hl.size();
     const size_t smem = (size_t)SEG * (8 + 8 + 8);
-    FC_CUDA(cudaFuncSetAttribute(k_policy_seg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    FC_CUDA(cudaFuncSetAttribute(k_head_seg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    FC_CUDA(cudaFuncSetAttribute(k_policy_final, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    static std::atomic<uint64_t> attr_done{0};  // per device, once
+    if (!(attr_done.load() & (1ull << (ctx->device & 63)))) {
+      FC_CUDA(cudaFuncSetAttribute(k_policy_seg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      FC_CUDA(cudaFuncSetAttribute(k_head_seg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      FC_CUDA(cudaFuncSetAttribute(k_policy_final, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr_done.fetch_or(1ull << (ctx->device & 63));
+    }
     DevBuf bad(sizeof(int), ctx->stream);
     FC_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), ctx->stream));
     KTimer kt(ctx, "policy");
@@ -459,9 +512,9 @@ struct lc_store {
     const bool fast = !(fe && atoi(fe) == 1) && n_slots > 0;
     DevBuf cur;
     if (fast) {
-      // scratch: K[n] | mm[2] | hist[NBIN] | pick[2] | n_out | items[CAP] | head[H]
+      // scratch: K[n] | mm[2] | hist[NBIN] | hist2[NBIN] | pick[5] | n_out | items[CAP] | head[H]
       const size_t kbytes = ((size_t)n_slots * 8 + 255) & ~size_t(255);
-      const size_t zoff = kbytes, zbytes = 16 + NBIN * 4 + 16;
+      const size_t zoff = kbytes, zbytes = 16 + 2 * NBIN * 4 + 32;
       const size_t ioff = zoff + ((zbytes + 255) & ~size_t(255));
       const size_t hoff = ioff + CAP * sizeof(ScoreItem);
       DevBuf scr(hoff + SCORE_H * sizeof(ScoreItem), ctx->stream);
@@ -469,33 +522,37 @@ struct lc_store {
       uint64_t* K = reinterpret_cast<uint64_t*>(base);
       unsigned long long* mm = reinterpret_cast<unsigned long long*>(base + zoff);
       unsigned* hist = reinterpret_cast<unsigned*>(base + zoff + 16);
-      int* pick = reinterpret_cast<int*>(base + zoff + 16 + NBIN * 4);
-      int* n_out = pick + 2;
+      unsigned* hist2 = hist + NBIN;
+      int* pick = reinterpret_cast<int*>(base + zoff + 16 + 2 * NBIN * 4);
+      int* n_out = pick + 5;
       FC_CUDA(cudaMemsetAsync(base + zoff, 0, zbytes, ctx->stream));
       FC_CUDA(cudaMemsetAsync(mm, 0xff, 8, ctx->stream));  // min = ~0
       const int grid = std::max(1, std::min<int>((int)((n_slots + 255) / 256), ctx->sm_count * 8));
       k_policy_keys<<<grid, 256, 0, ctx->stream>>>(dl, n_slots, dp, policy, now, K, mm, bad.as<int>());
       k_policy_hist<<<std::min(grid, ctx->sm_count * 2), 512, 0, ctx->stream>>>(K, n_slots, mm, hist);
       k_policy_pick<<<1, 1024, 0, ctx->stream>>>(hist, SCORE_H, pick);
+      k_policy_hist2<<<std::min(grid, ctx->sm_count * 2), 512, 0, ctx->stream>>>(K, n_slots, mm, pick, hist2);
+      k_policy_pick2<<<1, 32, 0, ctx->stream>>>(hist2, SCORE_H, pick);
       k_policy_collect<<<grid, 256, 0, ctx->stream>>>(K, dl, n_slots, mm, pick,
                                                       reinterpret_cast<ScoreItem*>(base + ioff), n_out);
       k_policy_final<<<1, SEG_T, smem, ctx->stream>>>(reinterpret_cast<ScoreItem*>(base + ioff), n_out,
                                                       reinterpret_cast<ScoreItem*>(base + hoff));
       FC_LAUNCH_CHECK();
-      count_launch(ctx, 5);
+      count_launch(ctx, 7);
+      kt.stop();  // GPU span of the scoring launches (not the readback)
       // one sync: head + the survivor count come back together
       std::vector<ScoreItem> hh(SCORE_H);
-      int hp[3] = {0, 0, 0};
+      int hp[6] = {0, 0, 0, 0, 0, 0};
       int32_t hb0 = 0;
       FC_CUDA(cudaMemcpyAsync(hh.data(), base + hoff, SCORE_H * sizeof(ScoreItem), cudaMemcpyDeviceToHost, ctx->stream));
-      FC_CUDA(cudaMemcpyAsync(hp, pick, 3 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+      FC_CUDA(cudaMemcpyAsync(hp, pick, 6 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
       FC_CUDA(cudaMemcpyAsync(&hb0, bad.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
       sync(ctx);
       if (hb0) raise(LC_ERR_INVALID_ARGUMENT, "lrbu_priority: now precedes last access");
-      if (hp[1] <= CAP) {
-        kt.stop();
-        return decode_head(hh);
-      }
+      if (getenv("FC_TRACE") && atoi(getenv("FC_TRACE")) == 1)
+        fprintf(stderr, "[score] slots %lld: bin %d, survivors %d (below %d), sub-bin %d -> %d%s\n", (long long)n_slots,
+                hp[0], hp[1], hp[2], hp[3], hp[4], hp[4] <= CAP ? "" : " => segmented sort");
+      if (hp[4] <= CAP) return decode_head(hh);
     }
     {
       int64_t nblk = std::max<int64_t>(1, (n_slots + SEG - 1) / SEG);

@@ -19,6 +19,10 @@ for i, e in enumerate(ents):
 print(f"insert {n_p}: {time.perf_counter()-t0:.2f} s")
 del ents
 now = n_p + 1
+if len(sys.argv) > 2 and sys.argv[2] == "gets":  # bench.py's access pattern: vary f / last_access
+    for pid in rng.integers(1, n_p + 1, n_p // 2):
+        st.get_step(int(pid), 25, now, want_latent=False)
+        now += 1
 fc.lib.lc_ctx_profile(ctx.h, 1)
 for mode in ("py", "raw"):
     e = fc._capi.StepEntry()
