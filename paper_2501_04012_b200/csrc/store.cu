@@ -222,20 +222,21 @@ __global__ void k_policy_hist(const uint64_t* __restrict__ K, int64_t n_slots, c
     if (h[t]) atomicAdd(&hist[t], h[t]);
 }
 
-// one block of 1024: pick[0] = threshold bin, pick[1] = survivors (cum count)
-__global__ void __launch_bounds__(1024) k_policy_pick(const unsigned* __restrict__ hist, int H, int* __restrict__ pick) {
+// Block of 1024 threads over NBIN bin counts: the first bin whose cumulative
+// count reaches `need` (NBIN - 1 if none), its cumulative count and the count
+// below it.
+__device__ void block_pick(const unsigned* __restrict__ hist, unsigned need, int* bin, unsigned* at, unsigned* below) {
   __shared__ unsigned c[NBIN];
+  __shared__ unsigned tot[1024];
   __shared__ int s_bin;
   constexpr int PER = NBIN / 1024;
   unsigned loc[PER], run = 0;
 #pragma unroll
   for (int q = 0; q < PER; ++q) run += (loc[q] = hist[threadIdx.x * PER + q]);
-  // block exclusive scan of the per-thread totals
-  __shared__ unsigned tot[1024];
   tot[threadIdx.x] = run;
   if (threadIdx.x == 0) s_bin = NBIN - 1;
   __syncthreads();
-  for (int o = 1; o < 1024; o <<= 1) {
+  for (int o = 1; o < 1024; o <<= 1) {  // inclusive scan of the per-thread totals
     const unsigned v = threadIdx.x >= o ? tot[threadIdx.x - o] : 0;
     __syncthreads();
     tot[threadIdx.x] += v;
@@ -251,13 +252,23 @@ __global__ void __launch_bounds__(1024) k_policy_pick(const unsigned* __restrict
 #pragma unroll
   for (int q = 0; q < PER; ++q) {
     const int b = threadIdx.x * PER + q;
-    if (c[b] >= (unsigned)H && (b == 0 || c[b - 1] < (unsigned)H)) s_bin = b;
+    if (c[b] >= need && (b == 0 || c[b - 1] < need)) s_bin = b;
   }
   __syncthreads();
+  *bin = s_bin;
+  *at = c[s_bin];
+  *below = s_bin > 0 ? c[s_bin - 1] : 0;
+}
+
+// pick[0] = threshold bin, pick[1] = survivors (cum count), pick[2] = below it
+__global__ void __launch_bounds__(1024) k_policy_pick(const unsigned* __restrict__ hist, int H, int* __restrict__ pick) {
+  int bin;
+  unsigned at, below;
+  block_pick(hist, (unsigned)H, &bin, &at, &below);
   if (threadIdx.x == 0) {
-    pick[0] = s_bin;
-    pick[1] = (int)c[s_bin];
-    pick[2] = s_bin > 0 ? (int)c[s_bin - 1] : 0;  // items in bins below the threshold bin
+    pick[0] = bin;
+    pick[1] = (int)at;
+    pick[2] = (int)below;
   }
 }
 
@@ -284,25 +295,21 @@ __global__ void k_policy_hist2(const uint64_t* __restrict__ K, int64_t n_slots, 
     if (h[t]) atomicAdd(&hist2[t], h[t]);
 }
 
-__global__ void k_policy_pick2(const unsigned* __restrict__ hist2, int H, int* __restrict__ pick) {
-  if (threadIdx.x != 0) return;
+__global__ void __launch_bounds__(1024) k_policy_pick2(const unsigned* __restrict__ hist2, int H, int* __restrict__ pick) {
   if (pick[1] <= REFINE) {
-    pick[3] = NBIN - 1;
-    pick[4] = pick[1];
+    if (threadIdx.x == 0) {
+      pick[3] = NBIN - 1;
+      pick[4] = pick[1];
+    }
     return;
   }
-  const unsigned need = (unsigned)(H - pick[2]);
-  unsigned acc = 0;
-  int b = NBIN - 1;
-  for (int t = 0; t < NBIN; ++t) {
-    acc += hist2[t];
-    if (acc >= need) {
-      b = t;
-      break;
-    }
+  int bin;
+  unsigned at, below;
+  block_pick(hist2, (unsigned)(H - pick[2]), &bin, &at, &below);
+  if (threadIdx.x == 0) {
+    pick[3] = bin;
+    pick[4] = pick[2] + (int)at;
   }
-  pick[3] = b;
-  pick[4] = pick[2] + (int)acc;
 }
 
 __global__ void k_policy_collect(const uint64_t* __restrict__ K, const DevLive* __restrict__ live, int64_t n_slots,
@@ -532,7 +539,7 @@ struct lc_store {
       k_policy_hist<<<std::min(grid, ctx->sm_count * 2), 512, 0, ctx->stream>>>(K, n_slots, mm, hist);
       k_policy_pick<<<1, 1024, 0, ctx->stream>>>(hist, SCORE_H, pick);
       k_policy_hist2<<<std::min(grid, ctx->sm_count * 2), 512, 0, ctx->stream>>>(K, n_slots, mm, pick, hist2);
-      k_policy_pick2<<<1, 32, 0, ctx->stream>>>(hist2, SCORE_H, pick);
+      k_policy_pick2<<<1, 1024, 0, ctx->stream>>>(hist2, SCORE_H, pick);
       k_policy_collect<<<grid, 256, 0, ctx->stream>>>(K, dl, n_slots, mm, pick,
                                                       reinterpret_cast<ScoreItem*>(base + ioff), n_out);
       k_policy_final<<<1, SEG_T, smem, ctx->stream>>>(reinterpret_cast<ScoreItem*>(base + ioff), n_out,
