@@ -1170,7 +1170,8 @@ void parallel_for(int64_t n, Body body) {
 // Builds entries for n prompts given maps (host, [n][S][F] in input step
 // order) and the device Gram diagonals. Writes out[i], sizes[i].
 void assemble(lc_ctx* ctx, const float* lat, const uint8_t* om, const uint8_t* bm, const std::vector<int32_t>& steps_in,
-              const Geo& g, const int32_t* maps_h, double* nrm_dev, bool norms_exact, const uint64_t* prompts, int64_t n,
+              const Geo& g, const int32_t* maps_h, double* nrm_dev, double* diag, bool norms_exact, const uint64_t* prompts,
+              int64_t n,
               lc_entry** out, uint64_t* sizes) {
   const int S = (int)steps_in.size();
   const int F = g.F;
@@ -1200,11 +1201,7 @@ void assemble(lc_ctx* ctx, const float* lat, const uint8_t* om, const uint8_t* b
     }
   }
   item_begin[n] = (int)items.size();
-  // Gram diagonals (norms^2 of every frame) to the host
-  PinnedBuf<double> diag((size_t)n * S * F);
-  FC_CUDA(cudaMemcpyAsync(diag.data(), nrm_dev, diag.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-  sync(ctx);
-  tr.mark("common keys + diag D2H");
+  tr.mark("common keys");
   // K7 over all (entry, common key) items: certified kernel first (S <= 5),
   // exact sequential kernel for whatever it cannot certify
   PinnedBuf<InterRes> res(items.size());
@@ -1229,7 +1226,7 @@ void assemble(lc_ctx* ctx, const float* lat, const uint8_t* om, const uint8_t* b
     FC_LAUNCH_CHECK();
     count_launch(ctx);
     for (int32_t id : ids)
-      FC_CUDA(cudaMemcpyAsync(diag.data() + (size_t)id * F, nrm_dev + (size_t)id * F, F * sizeof(double),
+      FC_CUDA(cudaMemcpyAsync(diag + (size_t)id * F, nrm_dev + (size_t)id * F, F * sizeof(double),
                               cudaMemcpyDeviceToHost, ctx->stream));
     sync(ctx);
   };
@@ -1699,20 +1696,29 @@ void compress_chunk(lc_ctx* ctx, const float* lat, const uint8_t* om, const uint
   const int S = (int)st.size();
   const int F = g.F;
   Trace tr;
-  DevBuf bad(sizeof(int), ctx->stream);
-  FC_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), ctx->stream));
+  // flags[0]: non-finite element (Gram pass), flags[1]: zero-norm frame (select)
+  DevBuf flags(2 * sizeof(int), ctx->stream);
+  FC_CUDA(cudaMemsetAsync(flags.p, 0, 2 * sizeof(int), ctx->stream));
   DevBuf G((size_t)n * S * F * F * sizeof(double), ctx->stream), NR((size_t)n * S * F * sizeof(double), ctx->stream);
-  const double delta = grams_and_norms(ctx, lat, (int)(n * S), g, G.as<double>(), NR.as<double>(), bad.as<int>());
-  if (check_flag(ctx, bad)) raise(LC_ERR_INVALID_ARGUMENT, "Frame: non-finite element");
-  tr.mark("nonfinite + gram (sync)");
+  const double delta = grams_and_norms(ctx, lat, (int)(n * S), g, G.as<double>(), NR.as<double>(), flags.as<int>());
   DevBuf maps((size_t)n * S * F * sizeof(int32_t), ctx->stream);
-  select_cert(ctx, G.as<double>(), NR.as<double>(), lat, (int)(n * S), g, thr, delta, maps.as<int32_t>(), bad.as<int>());
+  select_cert(ctx, G.as<double>(), NR.as<double>(), lat, (int)(n * S), g, thr, delta, maps.as<int32_t>(),
+              flags.as<int>() + 1);
+  // one round trip: maps, frame norms and both flags
   PinnedBuf<int32_t> maps_h((size_t)n * S * F);
+  PinnedBuf<double> diag((size_t)n * S * F);
+  PinnedBuf<int> fl(2);
   FC_CUDA(cudaMemcpyAsync(maps_h.data(), maps.p, maps.bytes, cudaMemcpyDeviceToHost, ctx->stream));
-  if (check_flag(ctx, bad)) raise(LC_ERR_INVALID_ARGUMENT, "cosine_similarity: zero-norm operand");
+  FC_CUDA(cudaMemcpyAsync(diag.data(), NR.p, NR.bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  FC_CUDA(cudaMemcpyAsync(fl.data(), flags.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  sync(ctx);
+  // the reference validates frames first (Frame ctor), then the cosine's zero norm
+  if (fl[0]) raise(LC_ERR_INVALID_ARGUMENT, "Frame: non-finite element");
+  if (fl[1]) raise(LC_ERR_INVALID_ARGUMENT, "cosine_similarity: zero-norm operand");
   check_distinct_steps(S, st.data());  // inter_compress validates after the intra pass (codec.cpp:201-205)
-  tr.mark("select + maps D2H");
-  assemble(ctx, lat, om, bm, st, g, maps_h.data(), NR.as<double>(), delta == 0.0, prompts, n, out, sizes);
+  tr.mark("gram + select + D2H (one sync)");
+  assemble(ctx, lat, om, bm, st, g, maps_h.data(), NR.as<double>(), diag.data(), delta == 0.0, prompts, n, out,
+           sizes);
   tr.mark("assemble");
 }
 
@@ -1932,8 +1938,12 @@ lc_status lc_compress_batch(lc_ctx* ctx, const float* latents, const int32_t* st
   std::vector<int32_t> st(steps, steps + S);
   // Two halves on two child streams from two host threads: one half's host
   // orchestration (syncs, base choice, layout) overlaps the other's kernels.
+  // The batch is split over child streams driven by host threads: one
+  // part's host orchestration (syncs, base choice, layout) overlaps the
+  // others' kernels. FC_COMPRESS_SPLIT=k overrides the part count (0/1 = off).
   const char* ev = getenv("FC_COMPRESS_SPLIT");
-  const int parts = (n >= 64 && !(ev && atoi(ev) == 0)) ? 2 : 1;
+  int parts = ev ? std::max(1, atoi(ev)) : 2;
+  parts = (int)std::min<int64_t>(parts, std::max<int64_t>(1, n / 32));
   for (int64_t e = 0; e < n; ++e) out[e] = nullptr;
   if (parts == 1) {
     compress_chunk(ctx, lat.dev, om.dev, bm.dev, st, g, thr, prompts, n, out, sizes);
@@ -1941,31 +1951,37 @@ lc_status lc_compress_batch(lc_ctx* ctx, const float* latents, const int32_t* st
     cudaEvent_t ready;
     FC_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
     FC_CUDA(cudaEventRecord(ready, ctx->stream));  // inputs staged on the caller's stream
-    const int64_t n0 = (n / 2 + 7) & ~int64_t(7);
-    const int64_t cut[3] = {0, std::min(n0, n), n};
-    std::exception_ptr err[2] = {nullptr, nullptr};
+    std::vector<int64_t> cut(parts + 1, 0);
+    for (int k = 1; k < parts; ++k) cut[k] = std::min<int64_t>(n, ((n * k / parts) + 7) & ~int64_t(7));
+    cut[parts] = n;
+    std::vector<std::exception_ptr> err(parts, nullptr);
     auto run = [&](int part) {
       try {
         lc_ctx* c = aux_ctx(ctx, part);
         FC_CUDA(cudaStreamWaitEvent(c->stream, ready, 0));
         const int64_t a = cut[part], m = cut[part + 1] - cut[part];
-        compress_chunk(c, lat.dev + a * S * F * E, om.dev + a * F * g.mb, bm.dev + a * F * g.mb, st, g, thr,
-                       prompts + a, m, out + a, sizes ? sizes + a : nullptr);
+        if (m > 0)
+          compress_chunk(c, lat.dev + a * S * F * E, om.dev + a * F * g.mb, bm.dev + a * F * g.mb, st, g, thr,
+                         prompts + a, m, out + a, sizes ? sizes + a : nullptr);
       } catch (...) {
         err[part] = std::current_exception();
       }
     };
-    std::thread t1(run, 1);
+    std::vector<std::thread> th;
+    for (int k = 1; k < parts; ++k) th.emplace_back(run, k);
     run(0);
-    t1.join();
+    for (auto& t : th) t.join();
     cudaEventDestroy(ready);
-    if (err[0] || err[1]) {
+    std::exception_ptr first = nullptr;
+    for (auto& e : err)
+      if (e && !first) first = e;
+    if (first) {
       for (int64_t e = 0; e < n; ++e)
         if (out[e]) {
           lc_entry_release(out[e]);
           out[e] = nullptr;
         }
-      std::rethrow_exception(err[0] ? err[0] : err[1]);
+      std::rethrow_exception(first);
     }
   }
   LC_API_END
@@ -1996,9 +2012,12 @@ lc_status lc_inter_compress(lc_ctx* ctx, const float* latents, const int32_t* ma
   DevBuf bad(sizeof(int), ctx->stream);
   FC_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), ctx->stream));
   const double delta = grams_and_norms(ctx, lat.dev, S, g, G.as<double>(), NR.as<double>(), bad.as<int>());
+  PinnedBuf<double> diag((size_t)S * F);
+  FC_CUDA(cudaMemcpyAsync(diag.data(), NR.p, NR.bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  if (check_flag(ctx, bad)) raise(LC_ERR_INVALID_ARGUMENT, "Frame: non-finite element");
   std::vector<int32_t> st(steps, steps + S);
-  assemble(ctx, lat.dev, om.dev, bm.dev, st, g, maps_h.data(), NR.as<double>(), delta == 0.0, &prompt, 1, out,
-           nullptr);
+  assemble(ctx, lat.dev, om.dev, bm.dev, st, g, maps_h.data(), NR.as<double>(), diag.data(), delta == 0.0, &prompt, 1,
+           out, nullptr);
   LC_API_END
 }
 
