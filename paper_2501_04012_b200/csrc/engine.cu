@@ -23,6 +23,8 @@
 #include <unordered_set>
 #include <vector>
 
+#include <chrono>
+
 #include "common.cuh"
 #include "decide.cuh"
 
@@ -50,6 +52,24 @@ std::vector<float> to_host(const float* p, size_t n) {
   else memcpy(h.data(), p, n * sizeof(float));
   return h;
 }
+
+// FC_TRACE=1: accumulated host time per engine phase, printed per call
+struct PhaseClock {
+  bool on = getenv("FC_TRACE") && atoi(getenv("FC_TRACE")) == 1;
+  double t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  void lap(int k) {
+    if (!on) return;
+    const auto n = std::chrono::steady_clock::now();
+    t[k] += std::chrono::duration<double, std::milli>(n - t0).count();
+    t0 = n;
+  }
+  ~PhaseClock() {
+    if (on)
+      fprintf(stderr, "[engine] lookup %.3f fixup %.3f serve %.3f defer %.3f flush-compress %.3f flush-insert %.3f "
+              "serial-update %.3f index-insert %.3f ms\n", t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[7]);
+  }
+};
 
 }  // namespace
 }  // namespace fc
@@ -147,6 +167,7 @@ lc_status lc_engine_process(lc_engine* e, const lc_request* req, int64_t n, cons
   const int64_t mb = ((int64_t)c.H * c.W + 7) / 8;
   if (served_dev) FC_REQUIRE(is_device_ptr(served_dev), "lc_engine_process: served_dev must be device memory");
   // queries on the host (exact fix-up dots) and as the batch lookup input
+  PhaseClock pc;
   const float* qs[3] = {q_whole, q_object, q_background};
   std::vector<float> qh[3];
   for (int t = 0; t < 3; ++t) qh[t] = to_host(qs[t], (size_t)n * d);
@@ -162,14 +183,129 @@ lc_status lc_engine_process(lc_engine* e, const lc_request* req, int64_t n, cons
     if (size0 > 0)
       ok(lc_index_query_topk(e->ix, t, qh[t].data(), n, KTOP, bid[t].data(), bsc[t].data(), bcnt[t].data()));
   }
+  pc.lap(0);
   // index changes since the batch lookup
   std::unordered_set<uint64_t> removed;                        // present at lookup time, removed since
   std::map<uint64_t, std::array<const float*, 3>> added;       // inserted since (rows in qh)
+  // index inserts are batched too (lookups inside the batch score the added
+  // rows exactly on the host); they reach the device index before any device
+  // query (re-query) and at the end of the batch
+  std::vector<uint64_t> ix_pending;
+  auto index_flush = [&]() {
+    if (ix_pending.empty()) return;
+    const size_t m = ix_pending.size();
+    std::vector<float> rows[3];
+    for (int t = 0; t < 3; ++t) {
+      rows[t].resize(m * d);
+      for (size_t q = 0; q < m; ++q) memcpy(rows[t].data() + q * d, added.at(ix_pending[q])[t], d * sizeof(float));
+    }
+    ok(lc_index_insert_batch(e->ix, ix_pending.data(), rows[0].data(), rows[1].data(), rows[2].data(), (int64_t)m, d));
+    ix_pending.clear();
+  };
+  auto index_has = [&](uint64_t p) {
+    if (std::find(ix_pending.begin(), ix_pending.end(), p) != ix_pending.end()) return true;
+    int32_t inx = 0;
+    ok(lc_index_contains(e->ix, p, &inx));
+    return inx != 0;
+  };
+  auto index_add = [&](uint64_t p, const float* w, const float* ob, const float* bg) {
+    ix_pending.push_back(p);
+    added[p] = {w, ob, bg};
+  };
   auto index_remove = [&](uint64_t p) {
-    ok(lc_index_remove(e->ix, p));
+    auto it = std::find(ix_pending.begin(), ix_pending.end(), p);
+    if (it != ix_pending.end()) ix_pending.erase(it);  // never reached the device
+    else ok(lc_index_remove(e->ix, p));
     removed.insert(p);
     added.erase(p);
   };
+  // ---- deferred cache updates ----
+  // An update whose insert provably evicts nothing (used + an upper bound of
+  // every pending entry's compressed_size fits the capacity) does not depend
+  // on anything that happens to other prompts before it is applied, so the
+  // compressions of such updates are batched (one lc_compress_batch per step
+  // set) and inserted in request order at the next flush: when a later
+  // request needs a pending prompt's store record, when a non-deferrable
+  // update comes, or at the end of the batch. The store/index states equal
+  // serial execution. FC_ENGINE_SERIAL=1 disables it.
+  const bool defer_ok = !(getenv("FC_ENGINE_SERIAL") && atoi(getenv("FC_ENGINE_SERIAL")) == 1);
+  struct Pending {
+    int64_t j;
+    uint64_t prompt, now;
+    int first;
+  };
+  std::vector<Pending> pending;
+  std::unordered_set<uint64_t> pending_ids;
+  uint64_t pending_bound = 0;
+  // compressed_size upper bound for S steps (codec.cpp:305-338 with every
+  // non-first key frame stored twice: as a base diff and as an extra)
+  auto size_bound = [&](int S) {
+    const uint64_t fr = 2 + 4 * (uint64_t)E, F = (uint64_t)c.F;
+    return 20 + (F - 1) * fr + 2 * F * (uint64_t)mb + (uint64_t)S * (1 + 4 * (uint64_t)E + 2 * F + 4 * (F - 1) + 2 + (F - 1) * fr);
+  };
+  const bool lat_dev = is_device_ptr(latents), om_dev = is_device_ptr(obj_masks), bm_dev = is_device_ptr(bg_masks);
+  auto flush = [&]() {
+    if (pending.empty()) return;
+    // one compress per step set; entries in request order
+    std::map<int64_t, lc_entry*> ent_of;
+    for (int first = 0; first < 5; ++first) {
+      std::vector<const Pending*> grp;
+      for (const auto& pd : pending)
+        if (pd.first == first) grp.push_back(&pd);
+      if (grp.empty()) continue;
+      const int S = 5 - first;
+      const size_t m = grp.size(), fe = (size_t)S * c.F * E, fm = (size_t)c.F * mb;
+      DevBuf dl(m * fe * sizeof(float), e->ctx->stream), dom(m * fm, e->ctx->stream), dbm(m * fm, e->ctx->stream);
+      for (size_t q = 0; q < m; ++q) {
+        const int64_t j = grp[q]->j;
+        FC_CUDA(cudaMemcpyAsync(dl.as<float>() + q * fe, latents + ((size_t)j * 5 + first) * c.F * E, fe * sizeof(float),
+                                lat_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, e->ctx->stream));
+        FC_CUDA(cudaMemcpyAsync(dom.as<uint8_t>() + q * fm, obj_masks + (size_t)j * fm, fm,
+                                om_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, e->ctx->stream));
+        FC_CUDA(cudaMemcpyAsync(dbm.as<uint8_t>() + q * fm, bg_masks + (size_t)j * fm, fm,
+                                bm_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, e->ctx->stream));
+      }
+      std::vector<uint64_t> pids(m);
+      for (size_t q = 0; q < m; ++q) pids[q] = grp[q]->prompt;
+      std::vector<lc_entry*> ents(m, nullptr);
+      std::vector<int32_t> steps(kCached + first, kCached + 5);
+      ok(lc_compress_batch(e->ctx, dl.as<float>(), steps.data(), S, c.F, c.H, c.W, c.C, dom.as<uint8_t>(),
+                           dbm.as<uint8_t>(), c.compress_threshold, pids.data(), (int64_t)m, ents.data(), nullptr));
+      for (size_t q = 0; q < m; ++q) ent_of[grp[q]->j] = ents[q];
+    }
+    pc.lap(4);
+    std::exception_ptr err = nullptr;
+    for (const auto& pd : pending) {
+      lc_entry* ent = ent_of[pd.j];
+      if (!err) {
+        const int S = 5 - pd.first;
+        std::vector<int32_t> steps(kCached + pd.first, kCached + 5);
+        int nev = 0;
+        lc_step_entry ev1;
+        const lc_status st1 = lc_store_insert(e->st, pd.prompt, ent, steps.data(), S, pd.now, &ev1, 1, &nev);
+        if (st1 != LC_OK) {
+          try {
+            ok(st1);
+          } catch (...) {
+            err = std::current_exception();
+          }
+        } else if (nev != 0) {
+          try {
+            raise(LC_ERR_INTERNAL, "engine: a deferred insert evicted (size bound violated)");
+          } catch (...) {
+            err = std::current_exception();
+          }
+        }
+      }
+      lc_entry_release(ent);
+    }
+    pending.clear();
+    pending_ids.clear();
+    pending_bound = 0;
+    pc.lap(5);
+    if (err) std::rethrow_exception(err);
+  };
+  try {
   for (int64_t j = 0; j < n; ++j) {
     const lc_request& r = req[j];
     const uint64_t now = r.arrival;
@@ -196,21 +332,39 @@ lc_status lc_engine_process(lc_engine* e, const lc_request* req, int64_t n, cons
         uint64_t i1 = 0;
         double s1 = 0;
         int32_t c1 = 0;
+        index_flush();
         ok(lc_index_query_topk(e->ix, t, q, 1, 1, &i1, &s1, &c1));
         have[t] = c1 > 0;
         tid[t] = i1;
         tsc[t] = s1;
         continue;
       }
-      for (const auto& kv : added) {
-        const double s = row_dot(q, kv.second[t], d);
-        if (!have[t] || better(s, kv.first, tsc[t], tid[t])) {
-          have[t] = true;
-          tid[t] = kv.first;
-          tsc[t] = s;
+      // exact scores of the rows added since the lookup, four independent
+      // sequential chains at a time (each in vindex.cpp:67 element order)
+      auto it = added.begin();
+      while (it != added.end()) {
+        const float* x[4];
+        uint64_t id[4];
+        int m = 0;
+        for (; m < 4 && it != added.end(); ++m, ++it) {
+          x[m] = it->second[t];
+          id[m] = it->first;
         }
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int i = 0; i < d; ++i) {
+          const double qi = (double)q[i];
+          for (int u = 0; u < 4; ++u)
+            if (u < m) acc[u] += qi * (double)x[u][i];
+        }
+        for (int u = 0; u < m; ++u)
+          if (!have[t] || better(acc[u], id[u], tsc[t], tid[t])) {
+            have[t] = true;
+            tid[t] = id[u];
+            tsc[t] = acc[u];
+          }
       }
     }
+    pc.lap(1);
     // ---- (2) decide + similarity_to_step ----
     lc_outcome o{};
     o.decision.whole_id = tid[0];
@@ -218,6 +372,11 @@ lc_status lc_engine_process(lc_engine* e, const lc_request* req, int64_t n, cons
     o.decision.background_id = tid[2];
     decide_one(tsc[0], tsc[1], tsc[2], have[0], c.hit_threshold, c.bin_edges, &o.decision);
     // ---- (3) serve ----
+    if (!pending_ids.empty() &&
+        ((o.decision.kind == LC_WHOLE_HIT && pending_ids.count(o.decision.whole_id)) ||
+         (o.decision.kind == LC_DECOUPLED_HIT &&
+          (pending_ids.count(o.decision.object_id) || pending_ids.count(o.decision.background_id)))))
+      flush();
     int actual = 0;
     float* srv = served_dev ? served_dev + (size_t)j * c.F * E : nullptr;
     if (o.decision.kind == LC_WHOLE_HIT) {
@@ -246,17 +405,30 @@ lc_status lc_engine_process(lc_engine* e, const lc_request* req, int64_t n, cons
       }
     }
     o.actual_step = actual;
+    pc.lap(2);
     // ---- (4) latency model ----
     o.latency = c.t_extract + c.t_lookup + c.t_per_step * (double)(c.total_steps - actual) +
                 ((o.decision.kind == LC_DECOUPLED_HIT && actual > 0) ? c.t_stitch : 0.0);
     // ---- (5) update_after_generation ----
     if (actual < 25) {
-      int32_t cached = 0;
-      ok(lc_store_contains(e->st, r.prompt, &cached));
-      if (!cached) {
-        int first = 0;  // first inserted step index into 5..25
-        while (first < 5 && kCached[first] <= actual) ++first;
-        const int S = 5 - first;
+      int32_t cached = pending_ids.count(r.prompt) ? 1 : 0;
+      if (!cached) ok(lc_store_contains(e->st, r.prompt, &cached));
+      int first = 0;  // first inserted step index into 5..25
+      while (first < 5 && kCached[first] <= actual) ++first;
+      const int S = 5 - first;
+      const uint64_t bound = size_bound(S);
+      if (!cached && defer_ok && lc_store_used(e->st) + pending_bound + bound <= c.capacity &&
+          pending_bound + bound >= pending_bound) {
+        pending.push_back(Pending{j, r.prompt, now, first});
+        pending_ids.insert(r.prompt);
+        pending_bound += bound;
+        o.n_inserted = S;
+        pc.lap(3);
+        if (!index_has(r.prompt))
+          index_add(r.prompt, qh[0].data() + (size_t)j * d, qh[1].data() + (size_t)j * d, qh[2].data() + (size_t)j * d);
+        pc.lap(7);
+      } else if (!cached) {
+        flush();  // in-order state before an insert that may evict
         std::vector<int32_t> steps(kCached + first, kCached + 5);
         const float* lat = latents + ((size_t)j * 5 + first) * c.F * E;
         lc_entry* ent = nullptr;
@@ -271,24 +443,16 @@ lc_status lc_engine_process(lc_engine* e, const lc_request* req, int64_t n, cons
         for (int k = 0; k < std::min<int>(nev, (int)ev.size()); ++k) {
           int32_t still = 0;
           ok(lc_store_contains(e->st, ev[k].prompt, &still));
-          int32_t inx = 0;
-          ok(lc_index_contains(e->ix, ev[k].prompt, &inx));
-          if (!still && inx) index_remove(ev[k].prompt);
+          if (!still && index_has(ev[k].prompt)) index_remove(ev[k].prompt);
         }
         ok(s1);
         o.n_inserted = S;
         o.n_evicted = nev;
-        int32_t inx = 0;
-        ok(lc_index_contains(e->ix, r.prompt, &inx));
-        if (!inx) {
-          const float* w = qh[0].data() + (size_t)j * d;
-          const float* ob = qh[1].data() + (size_t)j * d;
-          const float* bg = qh[2].data() + (size_t)j * d;
-          ok(lc_index_insert(e->ix, r.prompt, w, ob, bg, d));
-          added[r.prompt] = {w, ob, bg};
-        }
+        if (!index_has(r.prompt))
+          index_add(r.prompt, qh[0].data() + (size_t)j * d, qh[1].data() + (size_t)j * d, qh[2].data() + (size_t)j * d);
       }
     }
+    pc.lap(6);
     // ---- (6) metrics ----
     lc_engine_metrics& M = e->m;
     ++M.requests;
@@ -299,6 +463,17 @@ lc_status lc_engine_process(lc_engine* e, const lc_request* req, int64_t n, cons
     M.skipped_total += (uint64_t)actual;
     M.simulated_time += o.latency;
     out[j] = o;
+  }
+  flush();
+  index_flush();
+  } catch (...) {
+    // requests before the failing one are complete: apply their updates
+    try {
+      flush();
+      index_flush();
+    } catch (...) {
+    }
+    throw;
   }
   LC_API_END
 }

@@ -292,3 +292,27 @@ def test_certified_inter_ties_fall_back(fc, orc, synth):
     assert st["inter_exact_items"] > 0, st
     for i in range(3):
         assert ents[i].serialize() == orc.compress(lat[i], synth.CACHED_STEPS, om[i], bm[i], dims, i + 1), i
+
+
+def test_large_latent_shape_config4(fc, orc, synth):
+    """config[4] geometry: 64 frames of 72x128x4 (576x1024 video latents):
+    tensor-core Gram path (E = 36,864), certified K7, decompress and the
+    fused decoupled stitch stay bit-exact with the oracle."""
+    dims = (72, 128, 4)
+    F = 64
+    n = 2
+    lat = np.stack([synth.latents(300 + i, F=F, dims=dims) for i in range(n)])
+    masks = [synth.rect_masks(F, 72, 128, 300 + i) for i in range(n)]
+    om = np.stack([m[0] for m in masks])
+    bm = np.stack([m[1] for m in masks])
+    ents, sizes = fc.compress_batch(lat, synth.CACHED_STEPS, om, bm, dims, [1, 2])
+    E_ = 72 * 128 * 4
+    for i in range(n):
+        ref = orc.compress(lat[i], synth.CACHED_STEPS, om[i], bm[i], dims, i + 1)
+        assert ents[i].serialize() == ref
+        assert (bits(fc.decompress_step(ents[i], 15)) == bits(orc.decompress(ref, 15, F, E_))).all()
+    fused = fc.decompress_stitch([ents[0]], [ents[1]], [20])[0].cpu().numpy()
+    da = orc.decompress(ents[0].serialize(), 20, F, E_)
+    db = orc.decompress(ents[1].serialize(), 20, F, E_)
+    exp = orc.stitch(da, om[0], bm[0], db, om[1], bm[1], dims)
+    assert (bits(fused) == bits(exp)).all()
