@@ -71,6 +71,8 @@ def parse():
     ap.add_argument("--no-engine", action="store_true")
     ap.add_argument("--engine-cached", type=int, default=10_000)
     ap.add_argument("--engine-requests", type=int, default=1000)
+    ap.add_argument("--mixed-requests", type=int, default=4096)
+    ap.add_argument("--mixed-capacity-gb", type=float, default=4.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-queries", type=int, default=0, help="reference sample size (0 = auto)")
     ap.add_argument("--seed", type=int, default=2)
@@ -455,6 +457,7 @@ def main():
     if not args.no_engine and rank == 0:
         try:
             engine = bench_engine(torch, fc, ctx, args, dev)
+            engine["mixed"] = bench_engine_mixed(torch, fc, ctx, args, dev)
         except Exception as ex:  # reported, never fatal to the headline line
             engine = {"error": str(ex)[:200]}
 
@@ -645,6 +648,56 @@ def bench_engine(torch, fc, ctx, args, dev):
             "skipped_hist": m["skipped_hist"], "computation_savings": m["computation_savings"],
             "throughput_vs_nocache_simulated": m["throughput_vs_nocache"],
             "api": "Engine.process (host inputs: embeddings + each prompt's latents, pinned)"}
+
+
+def bench_engine_mixed(torch, fc, ctx, args, dev):
+    """config[3] scaled: a cold engine serving R requests of 64-frame 40x64x4
+    latents (Zipf(1.0) prompt reuse over 20,000 templates, popularity
+    reshuffled every R/4 requests) under a fixed capacity budget,
+    so inserts evict (LRBU) and evicted prompts leave the index. Latents are
+    generated on the device per 256-request batch (generation not timed)."""
+    n_r, F, dims, D = args.mixed_requests, 64, (40, 64, 4), 768
+    cap = int(args.mixed_capacity_gb * (1 << 30))
+    g = torch.Generator(device=dev)
+    g.manual_seed(21)
+    n_t = 20000
+    T = torch.randn(n_t, 3, D, generator=g, device=dev)
+    cfg = fc.engine_config(dim=D, F=F, H=40, W=64, C=4, policy=int(fc.Policy.Lrbu), capacity=cap)
+    eng = fc.Engine(cfg, ctx=ctx)
+    rng = np.random.default_rng(21)
+    w = 1.0 / np.arange(1, n_t + 1)
+    w /= w.sum()
+    perm = rng.permutation(n_t)
+    dt, done, ev = 0.0, 0, 0
+    B = 256
+    for j0 in range(0, n_r, B):
+        if j0 % max(B, n_r // 4) == 0 and j0:
+            perm = rng.permutation(n_t)  # popularity drift
+        m = min(B, n_r - j0)
+        t = torch.as_tensor(perm[rng.choice(n_t, size=m, p=w)], device=dev)
+        qs = []
+        for k in range(3):
+            raw = (T[t, k] + 0.3 * torch.rand(m, 1, generator=g, device=dev) *
+                   torch.randn(m, D, generator=g, device=dev)).contiguous()
+            u = torch.empty_like(raw)
+            fc._check(fc.lib.lc_embedding_normalize(ctx.h, C.c_void_p(raw.data_ptr()), m, D, C.c_void_p(u.data_ptr())))
+            qs.append(u.cpu().numpy())
+        lat, om, bm = make_latents(torch, m, F, dims, 1000 + j0, dev)
+        prompts = list(range(1 + j0, 1 + j0 + m))
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        outs = eng.process(prompts, list(range(1 + j0, 1 + j0 + m)), qs[0], qs[1], qs[2], lat, om, bm)
+        torch.cuda.synchronize()
+        dt += time.perf_counter() - t0
+        done += m
+        ev += sum(o["n_evicted"] for o in outs)
+        del lat
+    m_ = eng.metrics()
+    return {"workload": f"config[3] scaled: {n_r} requests, 64 x 40x64x4 latents (device-resident), Zipf(1.0) over "
+                        f"{n_t} templates with popularity reshuffles, LRBU, capacity {args.mixed_capacity_gb} GiB",
+            "requests_per_s": done / dt, "evicted_steps": ev, "store_used_bytes": eng.store.used(),
+            "whole_hits": m_["whole_hits"], "decoupled_hits": m_["decoupled_hits"], "misses": m_["misses"],
+            "computation_savings": m_["computation_savings"]}
 
 
 def bench_scoring(torch, fc, ctx, args, peaks):
