@@ -38,13 +38,6 @@ void ok(lc_status st) {
   if (st != LC_OK) raise(st, lc_last_error() ? lc_last_error() : "engine: library call failed");
 }
 
-// vindex.cpp:58-72: sequential fp64 dot of the fp32 query with the fp32 row
-double row_dot(const float* q, const float* x, int d) {
-  double acc = 0.0;
-  for (int i = 0; i < d; ++i) acc += (double)q[i] * (double)x[i];
-  return acc;
-}
-
 std::vector<float> to_host(const float* p, size_t n) {
   std::vector<float> h(n);
   if (n == 0) return h;
