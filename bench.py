@@ -239,6 +239,58 @@ def cpu_reference_lookup(table_np, queries_np, nthreads, n_q):
     return kind, n_q / dt, build_s, dt
 
 
+def _safe(fn):
+    try:
+        return fn()
+    except Exception as ex:  # reported, never the target
+        return {"value": None, "kind": "unavailable", "sample": str(ex)[:200]}
+
+
+def cpu_reference_codec(lat_np, om_np, bm_np, nthreads):
+    """The reference's intra_compress x 5 + inter_compress (oracle/_ref) on
+    host cores over a bounded sample of the config[2] prompts."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import Checker, available
+    kind = "reference" if available("ref") else "port"
+    chk = Checker("ref" if kind == "reference" else "orc")
+    n = lat_np.shape[0]
+    t0 = time.perf_counter()
+    sizes = chk.compress_batch_sizes(lat_np, [5, 10, 15, 20, 25], om_np, bm_np, (40, 64, 4), list(range(1, n + 1)),
+                                     nthreads=nthreads)
+    dt = time.perf_counter() - t0
+    byt = lat_np.nbytes + om_np.nbytes + bm_np.nbytes + int(sizes.sum())
+    return {"value": byt / dt / 1e9, "unit": "GB/s (compress)", "cores": nthreads, "kind": kind,
+            "sample": f"{n} config[2] prompts (5 x 64 x 40x64x4), {dt:.1f}s"}
+
+
+def cpu_reference_evict(n_prompts=100_000, n_ev=16):
+    """The reference's evict_one (single writer, store.cpp:113-157) at
+    5 x n_prompts live steps (bench_scoring's state, without get_steps)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import Checker, available
+    kind = "reference" if available("ref") else "port"
+    chk = Checker("ref" if kind == "reference" else "orc")
+    rng = np.random.default_rng(7)
+    lat = rng.standard_normal((1, 5, 1, 64)).astype(np.float32)
+    om = np.zeros((1, 8), np.uint8)
+    st = chk.store(1 << 62, 3)
+    steps = [5, 10, 15, 20, 25]
+    ent = chk.compress(lat[0], steps, om, om, (8, 8, 1), 1)
+    # the same bytes for every prompt id: patch the prompt field (first 8 bytes, LE)
+    t0 = time.perf_counter()
+    for i in range(n_prompts):
+        b = (i + 1).to_bytes(8, "little") + ent[8:]
+        st.insert(i + 1, b, steps, i + 1)
+    build_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    for _ in range(n_ev):
+        st.evict_one(n_prompts + 1)
+    dt = time.perf_counter() - t0
+    return {"value": n_ev / dt, "unit": "evictions/s", "cores": 1, "kind": kind,
+            "ms_per_evict_one": dt / n_ev * 1e3,
+            "sample": f"{n_ev} evict_one at {5 * n_prompts} live steps (LRBU); store build {build_s:.1f}s excluded"}
+
+
 def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -559,7 +611,16 @@ def bench_codec(torch, fc, ctx, args, dev, peaks):
     dk_bytes = dec_bytes / 5 if dk_n else 0
     dk_gbs = (dec_bytes * dec_reps) / (dk_t / 1000) / 1e9 if dk_t else None
     stitch_bytes = half * F * E * 4 * 2 + 2 * half * F * (40 * 64 // 8)  # out + selected source reads + masks
+    cpu = None
+    if not args.no_cpu:
+        try:
+            m = min(n, 32)
+            cpu = cpu_reference_codec(lat[:m].cpu().numpy(), om[:m].cpu().numpy(), bm[:m].cpu().numpy(),
+                                      os.cpu_count() or 1)
+        except Exception as ex:  # reported, never the target
+            cpu = {"value": None, "kind": "unavailable", "sample": str(ex)[:200]}
     res = {
+        "cpu_baseline": cpu,
         "workload": f"config[2]: {n} prompts x 5 steps x {F} frames x 40x64x4 fp32, rect masks, thr 0.99",
         "raw_bytes": raw, "compressed_bytes": int(sizes.sum()), "ratio": raw / float(sizes.sum()),
         "compress_GBps": comp_bytes / comp_s / 1e9, "compress_frac_hbm": comp_bytes / comp_s / 1e9 / hbm,
@@ -745,7 +806,7 @@ def bench_scoring(torch, fc, ctx, args, peaks):
                          "frac": round(alg_bytes / (per_launch_ms / 1e3) / 1e9 / peaks["hbm_gbs"], 4)
                          if per_launch_ms else None,
                          "bytes_per_launch": alg_bytes, "note": "latency-bound at this size (SURVEY 8(d))"},
-            "reference_evict_one_ms_at_500k_live": 38.8}
+            "cpu_baseline": _safe(lambda: cpu_reference_evict(n_p)) if not args.no_cpu else None}
 
 
 if __name__ == "__main__":
