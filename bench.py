@@ -353,10 +353,16 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one process per GPU; FC_DIST_BACKEND=gloo lets several ranks share one GPU (smoke runs)
+    backend = os.environ.get("FC_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     import paper_2501_04012_b200 as fc
     stream = torch.cuda.Stream(device=dev)  # library + collectives + events share this stream
     torch.cuda.set_stream(stream)
@@ -420,7 +426,8 @@ def main():
     fc.lib.lc_ctx_profile(ctx.h, 0)
     launches = ctx.launches - launches0
     ms = ev0.elapsed_time(ev1)
-    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    red_dev = dev if backend == "nccl" else "cpu"
+    t = torch.tensor([ms], device=red_dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
@@ -487,11 +494,12 @@ def main():
                 hres.copy_(last["res"][0], non_blocking=True)
             stream.synchronize()
         e2e_s = time.perf_counter() - t0
-        tt = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+        tt = torch.tensor([e2e_s], device=red_dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e = {"value": args.steps * B / float(tt.item()), "unit": "lookups/s",
                "h2d_bytes_per_step": B * args.dim * 4, "d2h_bytes_per_step": B * k * 8,
-               "api": "ShardedIndex.query_topk: lc_index_query_topk + one NCCL all-gather + lc_topk_merge, pinned host queries"}
+               "api": f"ShardedIndex.query_topk: lc_index_query_topk + one {backend} all-gather + lc_topk_merge, "
+                      "pinned host queries"}
 
     # ---- codec (config[2]) ----
     codec = None
@@ -534,7 +542,8 @@ def main():
             "metric": "cache lookups/s @1M entries", "value": value, "unit": "lookups/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": "config[1] lookup: 1M cached 768-d embeddings, 4096-query batches, top-8",
+            "config": {"workload": f"config[1] lookup: {args.rows:,} cached {args.dim}-d embeddings, {B}-query batches, "
+                                   f"top-{k}",
                        "rows": args.rows, "dim": args.dim, "global_batch": B, "k": k, "kprime": args.kprime,
                        "sharding": f"id mod {world}", "parallelism": f"entry-sharded x{world}",
                        "l2": "inputs larger than L2 (1.5 GB bf16 table streamed per step)",

@@ -101,9 +101,11 @@ class ShardedIndex:
             g = torch.empty((G,) + tuple(packed.shape), dtype=packed.dtype, device=packed.device)
             dist.all_gather_into_tensor(g, packed.contiguous(), group=self.group)
             return g
-        parts = [torch.empty_like(packed) for _ in range(G)]
-        dist.all_gather(parts, packed.contiguous(), group=self.group)
-        return torch.stack(parts)
+        # gloo (CPU tests, or a one-GPU smoke run of several ranks): host tensors
+        src = packed.contiguous().cpu()
+        parts = [torch.empty_like(src) for _ in range(G)]
+        dist.all_gather(parts, src, group=self.group)
+        return torch.stack(parts).to(packed.device)
 
     def _merge_lists(self, ids, sc, cnt, k):
         if self._merge is not None:
