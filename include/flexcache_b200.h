@@ -377,6 +377,29 @@ lc_status lc_engine_report(lc_engine* e, const lc_pricing* pricing, lc_cost_repo
 lc_index* lc_engine_index(lc_engine* e);
 lc_store* lc_engine_store(lc_engine* e);
 
+/* ---------------------------------------------------------------------------
+ * simgen (simgen.hpp declares it, no reference code): the
+ * on-device synthetic generator, defined in csrc/simgen.cu and restated in
+ * oracle/lc_oracle.c (orc_synth_*), bit-identical between the two.
+ * ------------------------------------------------------------------------- */
+/* synth_embedding for n prompts: tokens [n][max_tokens] (first n_tokens[i]
+ * used, 1..16), unit fp32 out [n][dim]; host or device buffers. */
+lc_status lc_synth_embeddings(lc_ctx* ctx, const uint64_t* tokens, const int32_t* n_tokens,
+                              int max_tokens, int64_t n, int dim, uint64_t seed, float* out);
+typedef struct lc_latent_spec {
+  double redundancy[5]; /* redundant-frame fraction per cached step (defaults.hpp:42) */
+  double alpha[5];      /* differential scale per step (defaults.hpp:43)            */
+  double noise_sigma;   /* relative noise on the differentials (defaults.hpp:44)     */
+  double dup_noise;     /* absolute jitter of a redundant frame                      */
+} lc_latent_spec;
+void lc_latent_spec_default(lc_latent_spec* spec);
+/* synth_latents for n prompt seeds: latents [n][5][F][H*W*C] (steps 5..25),
+ * rectangular object / background masks [n][F][ceil(H*W/8)]. spec NULL =
+ * defaults. */
+lc_status lc_synth_latents(lc_ctx* ctx, const uint64_t* prompt_seeds, int64_t n, int F, int H,
+                           int W, int C, const lc_latent_spec* spec, float* latents,
+                           uint8_t* obj_masks, uint8_t* bg_masks);
+
 /* lrbu_priority / lcbfu_priority (store.cpp:32-42) for n entries. */
 lc_status lc_priority_batch(lc_ctx* ctx, int policy, const lc_step_entry* e, int64_t n,
                             uint64_t now, double* out);

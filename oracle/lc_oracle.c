@@ -1150,3 +1150,115 @@ int orc_store_entries(void* h, orc_step_entry* out, int cap, int* n) {
   *n = k;
   return ORC_OK;
 }
+
+/* ---------------------------------------------------------------------------
+ * simgen: no reference code exists; this restates the
+ * generator defined in paper_2501_04012_b200/csrc/simgen.cu line for line
+ * (counter-based hash_combine streams, rng.hpp:25-31; Irwin-Hall normals).
+ * ------------------------------------------------------------------------- */
+static uint64_t sg_hash(uint64_t a, uint64_t b) { /* rng.hpp:25-31 */
+  uint64_t z = a ^ (b + 0x9e3779b97f4a7c15ull + (a << 6) + (a >> 2));
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+static double sg_U(uint64_t s, uint64_t i) { return (double)(sg_hash(s, i) >> 11) * 0x1.0p-53; }
+static double sg_N(uint64_t s, uint64_t i) {
+  const double a = sg_U(s, 4 * i) + sg_U(s, 4 * i + 1);
+  const double b = sg_U(s, 4 * i + 2) + sg_U(s, 4 * i + 3);
+  return ((a + b) - 2.0) * 1.7320508075688772;
+}
+
+int orc_synth_embedding(const uint64_t* tokens, int n_tok, int dim, uint64_t seed, float* out) {
+  if (n_tok < 1 || n_tok > 16 || dim <= 0) return fail(ORC_ERR_INVALID_ARGUMENT, "synth_embedding: 1..16 tokens");
+  double inv[16];
+  uint64_t st[16];
+  for (int t = 0; t < n_tok; ++t) {
+    st[t] = sg_hash(seed, tokens[t]);
+    double sq = 0.0;
+    for (int d = 0; d < dim; ++d) {
+      const float v = (float)sg_N(st[t], (uint64_t)d);
+      sq += (double)v * (double)v;
+    }
+    inv[t] = 1.0 / sqrt(sq);
+  }
+  double sq = 0.0;
+  for (int d = 0; d < dim; ++d) {
+    double acc = 0.0;
+    for (int t = 0; t < n_tok; ++t) {
+      const float v = (float)sg_N(st[t], (uint64_t)d);
+      acc += (double)(float)((double)v * inv[t]);
+    }
+    out[d] = (float)acc;
+    sq += (double)out[d] * (double)out[d];
+  }
+  const double iv = 1.0 / sqrt(sq);
+  for (int d = 0; d < dim; ++d) out[d] = (float)((double)out[d] * iv);
+  return ORC_OK;
+}
+
+static float sg_key(uint64_t s, int i, int j, int64_t e, int64_t E, const double* alpha, double noise) {
+  const double base = sg_N(sg_hash(s, 2), (uint64_t)e);
+  const double first = (double)(float)(base * (1.0 - 0.05 * i) + 0.05 * sg_N(sg_hash(s, 3 + i), (uint64_t)e));
+  if (j == 0) return (float)first;
+  const double dj = sg_N(sg_hash(s, 1), (uint64_t)(j * E + e));
+  const double nz = 1.0 + noise * sg_N(sg_hash(s, 10 + i), (uint64_t)(j * E + e));
+  return (float)(first + (alpha[i] * dj) * nz);
+}
+
+/* one prompt: lat [5][F][E], masks [F][mb] */
+int orc_synth_latents(uint64_t s, int F, int H, int W, int C, const double* red, const double* alpha,
+                      double noise, double dup, float* lat, uint8_t* om, uint8_t* bm) {
+  if (F < 1 || F > 256 || H < 1 || W < 1 || C < 1) return fail(ORC_ERR_INVALID_ARGUMENT, "synth_latents: geometry");
+  const int64_t E = (int64_t)H * W * C, mb = ((int64_t)H * W + 7) / 8;
+  int perm[256];
+  for (int t = 0; t < F - 1; ++t) perm[t] = t + 1;
+  for (int t = F - 2; t >= 1; --t) {
+    const int q = (int)(sg_hash(sg_hash(s, 30), (uint64_t)t) % (uint64_t)(t + 1));
+    const int x = perm[t]; perm[t] = perm[q]; perm[q] = x;
+  }
+  for (int i = 0; i < 5; ++i) {
+    const int n_red = (int)floor(red[i] * (double)(F - 1) + 0.5);
+    char is_red[256] = {0};
+    for (int t = 0; t < n_red && t < F - 1; ++t) is_red[perm[t]] = 1;
+    int keys[256], nk = 1, plan[256];
+    keys[0] = 0; plan[0] = -1;
+    for (int j = 1; j < F; ++j) {
+      if (is_red[j]) plan[j] = keys[sg_hash(sg_hash(s, 40 + i), (uint64_t)j) % (uint64_t)nk];
+      else { plan[j] = -1; keys[nk++] = j; }
+    }
+    for (int j = 0; j < F; ++j) {
+      float* fr = lat + ((int64_t)i * F + j) * E;
+      for (int64_t e = 0; e < E; ++e) {
+        if (plan[j] < 0) fr[e] = sg_key(s, i, j, e, E, alpha, noise);
+        else {
+          const double xk = (double)sg_key(s, i, plan[j], e, E, alpha, noise);
+          fr[e] = (float)(xk + dup * sg_N(sg_hash(s, 20 + i), (uint64_t)(j * E + e)));
+        }
+      }
+    }
+  }
+  const uint64_t m = sg_hash(s, 50);
+  const int h0 = (int)(sg_hash(m, 0) % (uint64_t)(H / 2 > 0 ? H / 2 : 1));
+  const int h1 = h0 + 1 + (int)(sg_hash(m, 1) % (uint64_t)(H - h0));
+  const int w0 = (int)(sg_hash(m, 2) % (uint64_t)(W / 2 > 0 ? W / 2 : 1));
+  const int w1 = w0 + 1 + (int)(sg_hash(m, 3) % (uint64_t)(W - w0));
+  const int span = W - w1 + 1 > 1 ? W - w1 + 1 : 1;
+  for (int j = 0; j < F; ++j) {
+    const int sh = j % span;
+    for (int64_t by = 0; by < mb; ++by) {
+      uint8_t ob = 0, bb = 0;
+      for (int b = 0; b < 8; ++b) {
+        const int64_t px = by * 8 + b;
+        if (px >= (int64_t)H * W) break;
+        const int y = (int)(px / W), x = (int)(px % W);
+        const int in = y >= h0 && y < h1 && x >= w0 + sh && x < (w1 + sh < W ? w1 + sh : W);
+        ob |= (uint8_t)(in ? 1 : 0) << b;
+        bb |= (uint8_t)(in ? 0 : 1) << b;
+      }
+      om[(int64_t)j * mb + by] = ob;
+      bm[(int64_t)j * mb + by] = bb;
+    }
+  }
+  return ORC_OK;
+}

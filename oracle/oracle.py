@@ -103,6 +103,10 @@ class Checker:
                                          C.c_void_p]
         fn("store_evict_one").argtypes = [C.c_void_p, C.c_uint64, C.POINTER(StepEntryC)]
         if kind == "orc":
+            fn("synth_embedding").argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_uint64, C.c_void_p]
+            fn("synth_latents").argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p,
+                                            C.c_void_p, C.c_double, C.c_double, C.c_void_p, C.c_void_p,
+                                            C.c_void_p]
             fn("store_peek").argtypes = [C.c_void_p, C.c_uint64, C.POINTER(StepEntryC), C.POINTER(C.c_double)]
             fn("store_next_seq").argtypes = [C.c_void_p]
             fn("store_next_seq").restype = C.c_uint64
@@ -186,6 +190,25 @@ class Checker:
         st = C.c_int32()
         self._chk(self.lib.orc_similarity_to_step(score, thr, _p(e), C.byref(st)))
         return st.value
+
+    # ---- simgen (restatement of csrc/simgen.cu) -----------------------------
+    def synth_embedding(self, tokens, dim, seed):
+        t = np.ascontiguousarray(tokens, np.uint64)
+        out = np.zeros(dim, np.float32)
+        self._chk(self._f("synth_embedding")(_p(t), t.size, dim, seed, _p(out)))
+        return out
+
+    def synth_latents(self, seed, F, dims, redundancy=(0.9, 0.8, 0.6, 0.4, 0.25),
+                      alpha=(1.0, 0.9, 0.8, 0.7, 0.6), noise=0.01, dup=0.02):
+        H, W, Cc = dims
+        E, mb = H * W * Cc, (H * W + 7) // 8
+        lat = np.zeros((5, F, E), np.float32)
+        om = np.zeros((F, mb), np.uint8)
+        bm = np.zeros((F, mb), np.uint8)
+        r = np.ascontiguousarray(redundancy, np.float64)
+        a = np.ascontiguousarray(alpha, np.float64)
+        self._chk(self._f("synth_latents")(seed, F, H, W, Cc, _p(r), _p(a), noise, dup, _p(lat), _p(om), _p(bm)))
+        return lat, om, bm
 
     # ---- codec ------------------------------------------------------------
     def select_keyframes(self, frames, dims, thr=0.99):

@@ -116,6 +116,12 @@ int orc_similarity_to_step(double score, double threshold, const double* edges4,
 int orc_store_peek(void* h, uint64_t now, orc_step_entry* out, double* key);
 uint64_t orc_store_next_seq(void* h);
 void orc_store_set_next_seq(void* h, uint64_t seq);
+/*  - simgen (no reference code): the generator defined in
+ *    csrc/simgen.cu, restated. */
+int orc_synth_embedding(const uint64_t* tokens, int n_tok, int dim, uint64_t seed, float* out);
+int orc_synth_latents(uint64_t seed, int F, int H, int W, int C, const double* redundancy,
+                      const double* alpha, double noise, double dup, float* lat, uint8_t* om,
+                      uint8_t* bm);
 
 #ifdef __cplusplus
 }

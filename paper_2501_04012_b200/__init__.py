@@ -857,3 +857,54 @@ class Engine:
     def save_snapshot(self, path):
         _check(lib.lc_snapshot_save(lib.lc_engine_store(self.h), lib.lc_engine_index(self.h),
                                     os.fspath(path).encode()))
+
+
+# ---------------------------------------------------------------------------
+# simgen: on-device synthetic embeddings / latents
+# ---------------------------------------------------------------------------
+def synth_embeddings(token_sets, dim, seed, ctx=None, out=None):
+    """synth_embedding for a list of token-id sets (1..16 ids each) -> unit
+    fp32 [n][dim] (device tensor unless `out` is given)."""
+    ctx = ctx or default_context()
+    n = len(token_sets)
+    mt = max(len(t) for t in token_sets)
+    tok = np.zeros((n, mt), np.uint64)
+    nt = np.zeros(n, np.int32)
+    for i, t in enumerate(token_sets):
+        tok[i, :len(t)] = t
+        nt[i] = len(t)
+    if out is None:
+        out = _torch_out((n, dim), ctx)
+    _check(lib.lc_synth_embeddings(ctx.h, _ptr(tok), _ptr(nt), mt, n, dim, seed, _ptr(out)))
+    return out
+
+
+def latent_spec(**kw) -> "_capi.LatentSpec":
+    s = _capi.LatentSpec()
+    lib.lc_latent_spec_default(C.byref(s))
+    for k, v in kw.items():
+        if k in ("redundancy", "alpha"):
+            arr = getattr(s, k)
+            for i, x in enumerate(v):
+                arr[i] = float(x)
+        else:
+            setattr(s, k, float(v))
+    return s
+
+
+def synth_latents(prompt_seeds, F, dims, spec=None, ctx=None):
+    """synth_latents for n prompt seeds -> (latents [n][5][F][E], obj masks,
+    bg masks [n][F][mb]) as device tensors."""
+    import torch
+    ctx = ctx or default_context()
+    ps = np.ascontiguousarray(prompt_seeds, np.uint64)
+    n = ps.size
+    H, W, Cc = dims
+    E, mb = H * W * Cc, (H * W + 7) // 8
+    dev = torch.device("cuda", ctx.device)
+    lat = torch.empty((n, 5, F, E), dtype=torch.float32, device=dev)
+    om = torch.empty((n, F, mb), dtype=torch.uint8, device=dev)
+    bm = torch.empty((n, F, mb), dtype=torch.uint8, device=dev)
+    sp = spec if spec is not None else latent_spec()
+    _check(lib.lc_synth_latents(ctx.h, _ptr(ps), n, F, H, W, Cc, C.byref(sp), _ptr(lat), _ptr(om), _ptr(bm)))
+    return lat, om, bm

@@ -70,6 +70,10 @@ class CostReport(C.Structure):
                 ("throughput_vs_nocache", f64), ("mean_latency", f64)]
 
 
+class LatentSpec(C.Structure):
+    _fields_ = [("redundancy", f64 * 5), ("alpha", f64 * 5), ("noise_sigma", f64), ("dup_noise", f64)]
+
+
 class LookupStats(C.Structure):
     _fields_ = [("queries", u64), ("certified", u64), ("fallback", u64), ("exact_scans", u64),
                 ("max_abs_err", f64)]
@@ -140,6 +144,9 @@ _sig("lc_store_peek", st, vp, u64, C.POINTER(StepEntry), C.POINTER(f64))
 _sig("lc_store_next_seq", u64, vp)
 _sig("lc_store_set_next_seq", st, vp, u64)
 _sig("lc_engine_config_default", None, C.POINTER(EngineConfig))
+_sig("lc_synth_embeddings", st, vp, vp, vp, C.c_int, i64, C.c_int, u64, vp)
+_sig("lc_latent_spec_default", None, C.POINTER(LatentSpec))
+_sig("lc_synth_latents", st, vp, vp, i64, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(LatentSpec), vp, vp, vp)
 _sig("lc_engine_create", st, vp, C.POINTER(EngineConfig), C.POINTER(vp))
 _sig("lc_engine_destroy", st, vp)
 _sig("lc_engine_process", st, vp, C.POINTER(Request), i64, vp, vp, vp, vp, vp, vp, vp, C.POINTER(Outcome))

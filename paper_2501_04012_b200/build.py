@@ -13,7 +13,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(OUT_DIR, "libflexcache_b200.so")
-SOURCES = ["core.cu", "index.cu", "lookup_sm100.cu", "gram_sm100.cu", "codec.cu", "store.cu", "engine.cu"]
+SOURCES = ["core.cu", "index.cu", "lookup_sm100.cu", "gram_sm100.cu", "codec.cu", "store.cu", "engine.cu", "simgen.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off", "-Xptxas", "-v",
