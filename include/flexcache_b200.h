@@ -327,6 +327,8 @@ typedef struct lc_engine_config {
   int32_t policy;            /* LC_POLICY_*             */
   uint64_t capacity;         /* store capacity, compressed_size bytes */
   int32_t dim, F, H, W, C;   /* embedding dim, latent geometry */
+  int32_t skip_oversized;    /* 1: an update whose entry alone exceeds the capacity inserts
+                                nothing (CLI capacity sweeps); 0: OversizedEntry */
 } lc_engine_config;
 void lc_engine_config_default(lc_engine_config* cfg);
 typedef struct lc_request {

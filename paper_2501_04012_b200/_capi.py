@@ -43,7 +43,8 @@ class Decision(C.Structure):
 class EngineConfig(C.Structure):
     _fields_ = [("hit_threshold", f64), ("compress_threshold", f64), ("bin_edges", f64 * 4), ("t_per_step", f64),
                 ("t_lookup", f64), ("t_extract", f64), ("t_stitch", f64), ("total_steps", i32), ("policy", i32),
-                ("capacity", u64), ("dim", i32), ("F", i32), ("H", i32), ("W", i32), ("C", i32)]
+                ("capacity", u64), ("dim", i32), ("F", i32), ("H", i32), ("W", i32), ("C", i32),
+                ("skip_oversized", i32)]
 
 
 class Request(C.Structure):

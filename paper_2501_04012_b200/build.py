@@ -100,6 +100,33 @@ def build_cpp_tests() -> list:
     return exes
 
 
+def build_tools() -> list:
+    """Compile the C++ command-line front-end (tools/*.cpp) against the
+    library into paper_2501_04012_b200/_bin."""
+    lib = build()
+    tools = os.path.join(ROOT, "tools")
+    out_dir = os.path.join(os.path.dirname(OUT_DIR), "_bin")
+    os.makedirs(out_dir, exist_ok=True)
+    cuda_inc = os.path.join(os.path.dirname(os.path.dirname(NVCC)), "include")
+    cuda_lib = os.path.join(os.path.dirname(os.path.dirname(NVCC)), "lib64")
+    hdr = os.path.join(ROOT, "include", "flexcache_b200.h")
+    exes = []
+    for f in sorted(os.listdir(tools)) if os.path.isdir(tools) else []:
+        if not f.endswith(".cpp"):
+            continue
+        src = os.path.join(tools, f)
+        exe = os.path.join(out_dir, "flexcache" if f == "flexcache_cli.cpp" else f[:-4])
+        if _stale(exe, [src, lib, hdr]):
+            cmd = [os.environ.get("CXX", "g++"), "-std=c++20", "-O2", "-Wall", "-Wextra", "-I" + os.path.join(ROOT, "include"),
+                   "-I" + cuda_inc, src, "-o", exe, "-L" + OUT_DIR, "-lflexcache_b200", "-Wl,-rpath," + OUT_DIR,
+                   "-L" + cuda_lib, "-lcudart"]
+            r = subprocess.run(cmd, capture_output=True, text=True)
+            if r.returncode != 0:
+                raise RuntimeError("g++ failed:\n" + r.stdout + r.stderr)
+        exes.append(exe)
+    return exes
+
+
 def _drain(procs, verbose):
     errs = []
     while procs:

@@ -430,8 +430,10 @@ lc_status lc_engine_process(lc_engine* e, const lc_request* req, int64_t n, cons
                              bg_masks + (size_t)j * c.F * mb, c.compress_threshold, &r.prompt, 1, &ent, &sz));
         std::vector<lc_step_entry> ev((size_t)lc_store_step_count(e->st) + 1);
         int nev = 0;
-        const lc_status s1 = lc_store_insert(e->st, r.prompt, ent, steps.data(), S, now, ev.data(), (int)ev.size(), &nev);
+        lc_status s1 = lc_store_insert(e->st, r.prompt, ent, steps.data(), S, now, ev.data(), (int)ev.size(), &nev);
         lc_entry_release(ent);
+        const bool skipped = s1 == LC_ERR_OVERSIZED_ENTRY && c.skip_oversized;
+        if (skipped) s1 = LC_OK;
         // the eviction callback: a prompt whose last step went leaves the index
         for (int k = 0; k < std::min<int>(nev, (int)ev.size()); ++k) {
           int32_t still = 0;
@@ -439,9 +441,9 @@ lc_status lc_engine_process(lc_engine* e, const lc_request* req, int64_t n, cons
           if (!still && index_has(ev[k].prompt)) index_remove(ev[k].prompt);
         }
         ok(s1);
-        o.n_inserted = S;
+        o.n_inserted = skipped ? 0 : S;
         o.n_evicted = nev;
-        if (!index_has(r.prompt))
+        if (!skipped && !index_has(r.prompt))
           index_add(r.prompt, qh[0].data() + (size_t)j * d, qh[1].data() + (size_t)j * d, qh[2].data() + (size_t)j * d);
       }
     }
