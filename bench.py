@@ -571,13 +571,16 @@ def bench_codec(torch, fc, ctx, args, dev, peaks):
     fc.lib.lc_ctx_profile(ctx.h, 1)
     for name in ("gram", "inter", "pack", "decompress", "decompress_stitch"):
         fc.lib.lc_ctx_kernel_time(ctx.h, name.encode(), None, None, 1)
-    reps = 2
-    t0 = time.perf_counter()
+    reps = 5
+    rep_s = []
     for _ in range(reps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
         ents, sizes = fc.compress_batch(lat, steps, om, bm, dims, prompts, ctx=ctx)
+        rep_s.append(time.perf_counter() - t0)
         if _ < reps - 1:
             del ents
-    comp_s = (time.perf_counter() - t0) / reps
+    comp_s = statistics.median(rep_s)  # one call per rep; the median resists a one-off host stall
     raw = n * 5 * F * E * 4
     mask_b = 2 * n * F * (40 * 64 // 8)
     comp_bytes = raw + mask_b + int(sizes.sum())
@@ -633,8 +636,9 @@ def bench_codec(torch, fc, ctx, args, dev, peaks):
         "workload": f"config[2]: {n} prompts x 5 steps x {F} frames x 40x64x4 fp32, rect masks, thr 0.99",
         "raw_bytes": raw, "compressed_bytes": int(sizes.sum()), "ratio": raw / float(sizes.sum()),
         "compress_GBps": comp_bytes / comp_s / 1e9, "compress_frac_hbm": comp_bytes / comp_s / 1e9 / hbm,
-        "compress_s": comp_s,
+        "compress_s": comp_s, "compress_s_reps": [round(x, 5) for x in rep_s],
         "compress_kernel_ms": {k_: round(v_[1] / max(1, reps), 3) for k_, v_ in ker.items() if k_ != "decompress"},
+        "compress_timing": "median of 5 calls, wall clock, inputs device-resident",
         "decompress_GBps_e2e": dec_bytes / dec_s / 1e9, "decompress_frac_hbm_e2e": dec_bytes / dec_s / 1e9 / hbm,
         "roofline": {"bound": "hbm", "achieved": round(dk_gbs, 1) if dk_gbs else None, "peak": hbm, "unit": "GB/s",
                      "frac": round(dk_gbs / hbm, 4) if dk_gbs else None, "traffic": None,

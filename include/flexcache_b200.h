@@ -162,9 +162,11 @@ lc_status lc_lookup_decide(lc_index* ix, const float* q_whole, const float* q_ob
 typedef struct lc_lookup_stats {
   uint64_t queries;       /* (query, table) lookups served               */
   uint64_t certified;     /* certified by the bf16 margin test            */
-  uint64_t fallback;      /* re-run through the exact fp64 scan           */
+  uint64_t fallback;      /* not certified by the K' shortlist            */
   uint64_t exact_scans;   /* lookups served by the exact scan directly    */
   double max_abs_err;     /* max |bf16 approx - fp64 exact| seen in rescores */
+  uint64_t tier2_certified; /* of the fallbacks: certified by the K'=128 re-shortlist
+                               (the rest are counted in exact_scans) */
 } lc_lookup_stats;
 lc_status lc_index_stats(lc_index* ix, lc_lookup_stats* out, int reset);
 /* mode: 0 auto (tensor-core path when size >= 8192), 1 force exact scan,

@@ -77,7 +77,7 @@ class LatentSpec(C.Structure):
 
 class LookupStats(C.Structure):
     _fields_ = [("queries", u64), ("certified", u64), ("fallback", u64), ("exact_scans", u64),
-                ("max_abs_err", f64)]
+                ("max_abs_err", f64), ("tier2_certified", u64)]
 
 
 class CodecStats(C.Structure):

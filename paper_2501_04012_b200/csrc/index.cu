@@ -178,6 +178,31 @@ __global__ void __launch_bounds__(256) k_scan_merge(const Cand* __restrict__ par
   if (threadIdx.x == 0) out_cnt[qo] = got;
 }
 
+// Tier-2 helpers: gather the uncertified queries, scatter their results back.
+__global__ void k_gather_queries(const float* __restrict__ Q, const int32_t* __restrict__ list, int n, int dim,
+                                 float* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)n * dim) return;
+  const int64_t r = i / dim, d = i - r * dim;
+  out[i] = Q[(int64_t)list[r] * dim + d];
+}
+__global__ void k_scatter_topk(const uint64_t* __restrict__ ids, const double* __restrict__ sc,
+                               const int32_t* __restrict__ cnt, const int32_t* __restrict__ list, int n, int k,
+                               uint64_t* __restrict__ oid, double* __restrict__ osc, int32_t* __restrict__ ocnt) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)n * k) return;
+  const int64_t r = i / k, t = i - r * k;
+  const int64_t q = list[r];
+  oid[q * k + t] = ids[i];
+  osc[q * k + t] = sc[i];
+  if (t == 0) ocnt[q] = cnt[r];
+}
+__global__ void k_map_list(const int32_t* __restrict__ sub, const int32_t* __restrict__ list, int n,
+                           int32_t* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = list[sub[i]];
+}
+
 // ---------------------------------------------------------------------------
 // Exact rescore of the bf16 shortlist + certification (one warp per query).
 // ---------------------------------------------------------------------------
@@ -477,7 +502,62 @@ void query_dev(lc_index* ix, int kind, const float* Qdev, int nq, int k, uint64_
   // FC_LOOKUP_DIAG=1 (kernel-timing diagnostics with FC_SHORTLIST_DEBUG only): skip the
   // exact re-scan, so results are NOT exact in that mode.
   static const bool diag = getenv("FC_LOOKUP_DIAG") && atoi(getenv("FC_LOOKUP_DIAG")) == 1;
-  if (nf > 0 && !diag) exact_scan(ix, kind, Qdev, fl.as<int32_t>(), nf, k, oid, osc, ocnt);
+  if (nf == 0 || diag) return;
+  // Tier 2: the uncertified queries (near-ties around the k-th score) rerun
+  // the tensor-core shortlist with K' = 128 and are rescored/certified again
+  // (~one streaming pass of the bf16 table); only what still fails takes the
+  // exact fp64 scan of every row. FC_LOOKUP_TIER2=0 disables it.
+  const bool tier2_off = getenv("FC_LOOKUP_TIER2") && atoi(getenv("FC_LOOKUP_TIER2")) == 0;
+  const int dim = ix->dim;
+  DevBuf q2((size_t)nf * dim * sizeof(float), ctx->stream);
+  k_gather_queries<<<grid_for((int64_t)nf * dim, 256), 256, 0, ctx->stream>>>(Qdev, fl.as<int32_t>(), nf, dim,
+                                                                             q2.as<float>());
+  constexpr int KP2_MAX = 128;
+  DevBuf cs2((size_t)nf * KP2_MAX * sizeof(float), ctx->stream), cr2((size_t)nf * KP2_MAX * sizeof(uint32_t), ctx->stream);
+  DevBuf cn2((size_t)nf * sizeof(int32_t), ctx->stream);
+  int kp2 = 0;  // the longest shortlist the kernel's shared memory allows at this dim (> kp)
+  if (!tier2_off && k <= KP2_MAX)
+    for (int cand = KP2_MAX; cand > kp && kp2 == 0; cand -= 32) {
+      try {
+        approx_shortlist(ctx, ix->plan[kind], q2.as<float>(), nf, cand, cs2.as<float>(), cr2.as<uint32_t>(),
+                         cn2.as<int32_t>());
+        kp2 = cand;
+      } catch (const Error& e) {
+        if (e.code != LC_ERR_INVALID_ARGUMENT) throw;  // smem budget at this K': try a shorter one
+      }
+    }
+  if (kp2 == 0) {
+    exact_scan(ix, kind, Qdev, fl.as<int32_t>(), nf, k, oid, osc, ocnt);
+    return;
+  }
+  DevBuf id2((size_t)nf * k * sizeof(uint64_t), ctx->stream), sc2((size_t)nf * k * sizeof(double), ctx->stream);
+  DevBuf ct2((size_t)nf * sizeof(int32_t), ctx->stream), fl2((size_t)nf * sizeof(int32_t), ctx->stream);
+  DevBuf fn2(16, ctx->stream);
+  FC_CUDA(cudaMemsetAsync(fn2.p, 0, 16, ctx->stream));
+  {
+    KTimer kt2(ctx, "rescore");
+    k_rescore<4><<<(unsigned)((nf + RS_WARPS - 1) / RS_WARPS), RS_WARPS * 32, rs_smem, ctx->stream>>>(
+        q2.as<float>(), nf, dim, ix->rows[kind], ix->ids_dev, cs2.as<float>(), cr2.as<uint32_t>(), cn2.as<int32_t>(),
+        kp2, ix->n, k, ix->eps, id2.as<uint64_t>(), sc2.as<double>(), ct2.as<int32_t>(), fl2.as<int32_t>(),
+        fn2.as<int32_t>(), reinterpret_cast<unsigned long long*>(fn2.as<char>() + 8));
+  }
+  k_scatter_topk<<<grid_for((int64_t)nf * k, 256), 256, 0, ctx->stream>>>(
+      id2.as<uint64_t>(), sc2.as<double>(), ct2.as<int32_t>(), fl.as<int32_t>(), nf, k, oid, osc, ocnt);
+  FC_LAUNCH_CHECK();
+  count_launch(ctx, 3);
+  int32_t hf2[4] = {0, 0, 0, 0};
+  FC_CUDA(cudaMemcpyAsync(hf2, fn2.p, 16, cudaMemcpyDeviceToHost, ctx->stream));
+  sync(ctx);
+  const int nf2 = hf2[0];
+  ix->stats.tier2_certified += nf - nf2;
+  if (nf2 > 0) {
+    DevBuf ol((size_t)nf2 * sizeof(int32_t), ctx->stream);
+    k_map_list<<<grid_for(nf2, 128), 128, 0, ctx->stream>>>(fl2.as<int32_t>(), fl.as<int32_t>(), nf2, ol.as<int32_t>());
+    FC_LAUNCH_CHECK();
+    count_launch(ctx);
+    exact_scan(ix, kind, Qdev, ol.as<int32_t>(), nf2, k, oid, osc, ocnt);
+    ix->stats.exact_scans += nf2;
+  }
 }
 
 }  // namespace

@@ -228,3 +228,36 @@ def test_sharded_index_product_path_single_rank(fc, orc, synth):
     mi, ms, mc = fc.topk_merge(torch.stack([p[0] for p in parts]), torch.stack([p[1] for p in parts]),
                                torch.stack([p[2] for p in parts]), 8)
     assert (u64(mi.cpu().numpy()) == oi).all() and (bits(ms.cpu().numpy()) == bits(os_)).all()
+
+
+@pytest.mark.parametrize("tier2", ["1", "0"])
+def test_near_tied_cluster_tier2_and_exact(fc, orc, synth, tier2):
+    """100 rows within ~1e-3 of each other around each query: the K'=32 bf16
+    shortlist cannot certify the top-8 (its 32nd score is inside the error
+    bound of the 8th), the K'=128 re-shortlist can; with FC_LOOKUP_TIER2=0 the
+    exact scan answers. Both are bit-exact with the oracle."""
+    os.environ["FC_LOOKUP_TIER2"] = tier2
+    try:
+        rng = np.random.default_rng(41)
+        n, dim, nq = 20000, 256, 6
+        base = rng.standard_normal((n, dim)).astype(np.float32)
+        q = rng.standard_normal((nq, dim)).astype(np.float32)
+        for j in range(nq):  # a cluster of 100 near-copies of each query
+            for c in range(100):
+                base[j * 100 + c] = q[j] + 0.01 * rng.standard_normal(dim).astype(np.float32)
+        tab = orc.normalize_rows(base)
+        qn = orc.normalize_rows(q)
+        ids = np.arange(n, dtype=np.uint64) * 7 + 3
+        ix = build_index(fc, [tab, tab, tab], ids, mode=2, kprime=32)
+        ix.stats(reset=True)
+        gi, gs, gc = ix.query_topk(fc.EmbeddingKind.Whole, qn, 8)
+        oi, os_, oc = orc.topk_flat(tab, ids, qn, 8)
+        assert (u64(gi) == oi).all() and (bits(gs) == bits(os_)).all() and (gc == oc).all()
+        s = ix.stats()
+        assert s.fallback == nq, s.fallback
+        if tier2 == "1":
+            assert s.tier2_certified == nq and s.exact_scans == 0, (s.tier2_certified, s.exact_scans)
+        else:
+            assert s.tier2_certified == 0
+    finally:
+        del os.environ["FC_LOOKUP_TIER2"]
