@@ -125,6 +125,9 @@ class Checker:
                 fn(n).restype = C.c_void_p
             fn("snapshot_free").argtypes = [C.c_void_p]
             fn("last_snapshot_offset").restype = C.c_uint64
+            fn("compress_batch_hash").argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
+                                                  C.c_int, C.c_void_p, C.c_void_p, C.c_double, C.c_void_p, C.c_int,
+                                                  C.c_int, C.c_void_p, C.c_void_p]
             fn(n).restype = C.c_int64
         fn("store_entries").argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.POINTER(C.c_int)]
         if kind == "orc":
@@ -254,6 +257,21 @@ class Checker:
         self._chk(self._f("compress_batch")(_p(lat), _p(steps), S, F, H, W, Cc, _p(om), _p(bm), thr,
                                             _p(prompts), n, nthreads, _p(out)))
         return out
+
+    def compress_batch_hash(self, lat, steps, obj_masks, bg_masks, dims, prompts, nthreads=1, thr=0.99):
+        """(sizes, FNV-1a 64 of each entry's wire bytes) — reference only."""
+        lat = np.ascontiguousarray(lat, np.float32)
+        steps = np.ascontiguousarray(steps, np.int32)
+        om = np.ascontiguousarray(obj_masks, np.uint8)
+        bm = np.ascontiguousarray(bg_masks, np.uint8)
+        prompts = np.ascontiguousarray(prompts, np.uint64)
+        n, S, F = lat.shape[0], lat.shape[1], lat.shape[2]
+        H, W, Cc = dims
+        sizes = np.zeros(n, np.uint64)
+        hashes = np.zeros(n, np.uint64)
+        self._chk(self._f("compress_batch_hash")(_p(lat), _p(steps), S, F, H, W, Cc, _p(om), _p(bm), thr,
+                                                 _p(prompts), n, nthreads, _p(sizes), _p(hashes)))
+        return sizes, hashes
 
     def decompress(self, entry: bytes, step, F, E):
         buf = np.frombuffer(entry, np.uint8)

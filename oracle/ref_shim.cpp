@@ -255,6 +255,42 @@ int ref_compress_batch(const float* lat, const int32_t* steps, int S, int F, int
   return ORC_OK;
 }
 
+// As ref_compress_batch, plus a position-weighted checksum of every entry's
+// wire bytes, sum_i b[i] * ((i * 0x9E3779B1 + 1) mod 2^32) mod 2^64 (full-size
+// parity checks compare checksums instead of shipping GBs of bytes).
+int ref_compress_batch_hash(const float* lat, const int32_t* steps, int S, int F, int H, int W,
+                            int C, const uint8_t* obj_masks, const uint8_t* bg_masks, double thr,
+                            const uint64_t* prompts, int n, int nthreads, uint64_t* out_sizes,
+                            uint64_t* out_hash) {
+  const FrameDims d = dims_of(H, W, C);
+  const size_t ent = static_cast<size_t>(S) * F * d.elems();
+  const size_t mb = static_cast<size_t>(F) * ((static_cast<size_t>(H) * W + 7) / 8);
+  if (nthreads < 1) nthreads = 1;
+  std::vector<int> st(nthreads, ORC_OK);
+  auto work = [&](int t) {
+    for (int i = t; i < n; i += nthreads) {
+      int rc = guard([&] {
+        const auto b = compress_one(lat + i * ent, steps, S, F, d, obj_masks + i * mb, bg_masks + i * mb, thr,
+                                    prompts[i]);
+        out_sizes[i] = b.size();
+        uint64_t h = 0;
+        for (size_t x = 0; x < b.size(); ++x) h += (uint64_t)b[x] * (uint64_t)(uint32_t)(x * 0x9E3779B1u + 1u);
+        out_hash[i] = h;
+      });
+      if (rc != ORC_OK) {
+        st[t] = rc;
+        return;
+      }
+    }
+  };
+  std::vector<std::thread> ts;
+  for (int t = 0; t < nthreads; ++t) ts.emplace_back(work, t);
+  for (auto& t : ts) t.join();
+  for (int rc : st)
+    if (rc != ORC_OK) return rc;
+  return ORC_OK;
+}
+
 int ref_decompress(const uint8_t* entry, uint64_t len, int step, float* out) {
   return guard([&] {
     CompressedEntry e = parse_entry(entry, len);
