@@ -913,6 +913,60 @@ __global__ void __launch_bounds__(DEC_T) k_decompress(const DecItem* __restrict_
   }
 }
 
+// Grouped decompress: one block per (item, key frame); the key's
+// reconstruction is computed once per element chunk and stored to every frame
+// that maps to it (intra_decompress copies, codec.cpp:174-179), so each
+// source float is read once per step instead of once per duplicate frame.
+struct DecJob {
+  int32_t item, key;
+  uint64_t mask[4];  // frames (< 256) whose map points at `key`
+};
+
+__global__ void __launch_bounds__(DEC_T) k_decompress_groups(const DecItem* __restrict__ items,
+                                                             const DecJob* __restrict__ jobs, int F, int64_t E) {
+  const DecJob jb = jobs[blockIdx.x];
+  const DecItem it = items[jb.item];
+  const Recipe r = it.rec[jb.key];
+  const int64_t n4 = E >> 2;
+  const float4* a4 = reinterpret_cast<const float4*>(it.base + r.a);
+  const float4* b4 = reinterpret_cast<const float4*>(it.base + r.b);
+  const double al = r.alpha;
+  __shared__ int fr[256];
+  __shared__ int s_nf;
+  if (threadIdx.x == 0) {
+    int nf = 0;
+    for (int w = 0; w < 4; ++w)
+      for (uint64_t m = jb.mask[w]; m; m &= m - 1) fr[nf++] = w * 64 + __ffsll((long long)m) - 1;
+    s_nf = nf;
+  }
+  __syncthreads();
+  const int nf = s_nf;
+  for (int64_t i0 = threadIdx.x; i0 < n4; i0 += (int64_t)DEC_T * DEC_U) {
+    float4 va[DEC_U], vb[DEC_U];
+#pragma unroll
+    for (int u = 0; u < DEC_U; ++u) {
+      const int64_t i = i0 + (int64_t)u * DEC_T;
+      if (i < n4) {
+        va[u] = __ldg(a4 + i);
+        if (r.kind != 0) vb[u] = __ldg(b4 + i);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < DEC_U; ++u) {
+      const int64_t i = i0 + (int64_t)u * DEC_T;
+      if (i >= n4) break;
+      float4 v = va[u];
+      if (r.kind == 1) {
+        v = make_float4(va[u].x + vb[u].x, va[u].y + vb[u].y, va[u].z + vb[u].z, va[u].w + vb[u].w);
+      } else if (r.kind == 2) {
+        v = make_float4((float)fma(al, (double)vb[u].x, (double)va[u].x), (float)fma(al, (double)vb[u].y, (double)va[u].y),
+                        (float)fma(al, (double)vb[u].z, (double)va[u].z), (float)fma(al, (double)vb[u].w, (double)va[u].w));
+      }
+      for (int q = 0; q < nf; ++q) __stcs(reinterpret_cast<float4*>(it.out + (int64_t)fr[q] * E) + i, v);
+    }
+  }
+}
+
 struct StitchItem {
   const float* obase;
   const Recipe* orec;
@@ -1620,6 +1674,30 @@ void launch_decompress(lc_ctx* ctx, const std::vector<const EntryData*>& ents, c
     items[i] = DecItem{ents[i]->fbase(), ents[i]->recipes(sidx[i]), out + (int64_t)i * F * E};
   DevBuf di(items.size() * sizeof(DecItem), ctx->stream);
   FC_CUDA(cudaMemcpyAsync(di.p, items.data(), di.bytes, cudaMemcpyHostToDevice, ctx->stream));
+  const char* ge = getenv("FC_DEC_GROUPS");
+  const bool groups = (E & 3) == 0 && F <= 256 && !(ge && atoi(ge) == 0);
+  if (groups) {
+    std::vector<DecJob> jobs((size_t)ents.size() * F);  // pageable: the async copy stages it before returning
+    size_t nj = 0;
+    for (size_t i = 0; i < ents.size(); ++i) {
+      const std::vector<int32_t>& mp = ents[i]->maps[sidx[i]];
+      for (int m = 0; m < F; ++m) {
+        if (mp[m] != m) continue;
+        DecJob jb{(int32_t)i, m, {0, 0, 0, 0}};
+        for (int j = m; j < F; ++j)
+          if (mp[j] == m) jb.mask[j >> 6] |= 1ull << (j & 63);
+        jobs[nj++] = jb;
+      }
+    }
+    DevBuf dj(nj * sizeof(DecJob), ctx->stream);
+    FC_CUDA(cudaMemcpyAsync(dj.p, jobs.data(), dj.bytes, cudaMemcpyHostToDevice, ctx->stream));
+    KTimer kt(ctx, "decompress");
+    k_decompress_groups<<<(unsigned)nj, DEC_T, 0, ctx->stream>>>(di.as<DecItem>(), dj.as<DecJob>(), F, E);
+    kt.stop();
+    FC_LAUNCH_CHECK();
+    count_launch(ctx);
+    return;
+  }
   KTimer kt(ctx, "decompress");
   k_decompress<<<(unsigned)(items.size() * F), DEC_T, 0, ctx->stream>>>(di.as<DecItem>(), F, E);
   kt.stop();
