@@ -519,6 +519,7 @@ void query_dev(lc_index* ix, int kind, const float* Qdev, int nq, int k, uint64_
   if (!tier2_off && k <= KP2_MAX)
     for (int cand = KP2_MAX; cand > kp && kp2 == 0; cand -= 32) {
       try {
+        ShortlistTimerName tn("shortlist_tier2");
         approx_shortlist(ctx, ix->plan[kind], q2.as<float>(), nf, cand, cs2.as<float>(), cr2.as<uint32_t>(),
                          cn2.as<int32_t>());
         kp2 = cand;
@@ -535,7 +536,7 @@ void query_dev(lc_index* ix, int kind, const float* Qdev, int nq, int k, uint64_
   DevBuf fn2(16, ctx->stream);
   FC_CUDA(cudaMemsetAsync(fn2.p, 0, 16, ctx->stream));
   {
-    KTimer kt2(ctx, "rescore");
+    KTimer kt2(ctx, "rescore_tier2");
     k_rescore<4><<<(unsigned)((nf + RS_WARPS - 1) / RS_WARPS), RS_WARPS * 32, rs_smem, ctx->stream>>>(
         q2.as<float>(), nf, dim, ix->rows[kind], ix->ids_dev, cs2.as<float>(), cr2.as<uint32_t>(), cn2.as<int32_t>(),
         kp2, ix->n, k, ix->eps, id2.as<uint64_t>(), sc2.as<double>(), ct2.as<int32_t>(), fl2.as<int32_t>(),

@@ -32,6 +32,15 @@ void approx_plan(ApproxPlan& p, const __nv_bfloat16* rows_bf16, int64_t n_rows, 
 // (cand_s approx score, cand_r row slot, cand_n count <= kp).
 void approx_shortlist(lc_ctx* ctx, const ApproxPlan& p, const float* Qdev, int nq, int kp, float* cand_s,
                       uint32_t* cand_r, int32_t* cand_n);
+// kernel-timer name of the shortlist launches ("shortlist"; the tier-2
+// re-shortlist of uncertified queries is timed apart so per-launch averages
+// of the main pass stay clean)
+extern thread_local const char* g_shortlist_timer;
+struct ShortlistTimerName {
+  const char* prev;
+  explicit ShortlistTimerName(const char* n) : prev(g_shortlist_timer) { g_shortlist_timer = n; }
+  ~ShortlistTimerName() { g_shortlist_timer = prev; }
+};
 
 __global__ void k_decide(const uint64_t* wi, const double* ws, const uint64_t* oi, const double* os,
                          const uint64_t* bi, const double* bs, const int32_t* wc, int64_t n, double thr, double e0,
