@@ -407,7 +407,7 @@ def main():
         step(qs[s])
     ix.stats(reset=True)
     fc.lib.lc_ctx_profile(ctx.h, 1)
-    for name in ("shortlist", "rescore", "scan"):
+    for name in ("shortlist", "rescore", "scan", "shortlist_tier2", "rescore_tier2", "shortlist_merge"):
         fc.lib.lc_ctx_kernel_time(ctx.h, name.encode(), None, None, 1)
     launches0 = ctx.launches
     if world > 1:
@@ -438,7 +438,7 @@ def main():
     value = args.steps * B / (ms / 1000.0)
     st = ix.stats()
     kt = {}
-    for name in ("shortlist", "rescore", "scan"):
+    for name in ("shortlist", "rescore", "scan", "shortlist_tier2", "rescore_tier2", "shortlist_merge"):
         n_, tot = C.c_uint64(), C.c_double()
         fc.lib.lc_ctx_kernel_time(ctx.h, name.encode(), C.byref(n_), C.byref(tot), 1)
         kt[name] = (n_.value, tot.value)
@@ -545,7 +545,8 @@ def main():
         line = {
             "metric": "cache lookups/s @1M entries", "value": value, "unit": "lookups/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-            "ms_per_step_median": statistics.median(step_ms), "ms_per_step_max": max(step_ms), "higher_is_better": True,
+            "ms_per_step_median": statistics.median(step_ms), "ms_per_step_max": max(step_ms),
+            "ms_per_step_all": [round(x, 3) for x in step_ms], "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": f"config[1] lookup: {args.rows:,} cached {args.dim}-d embeddings, {B}-query batches, "
                                    f"top-{k}",

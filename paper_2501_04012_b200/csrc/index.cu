@@ -267,9 +267,33 @@ __global__ void __launch_bounds__(RS_WARPS * 32)
       if (a < skip_below) continue;
       const float* x = rows + (int64_t)r * dim;
       double acc = 0.0;
-      if ((dim & 15) == 0) {
+      if ((dim & 31) == 0) {
         // sequential fp64 in d order (vindex.cpp:67); the row streams as
-        // float4 loads issued 16 elements ahead, the query comes from smem
+        // float4 loads issued 32 elements (two 128 B lines) ahead -- the
+        // gathers are latency-bound, so the depth in flight sets the speed
+        const float4* x4 = reinterpret_cast<const float4*>(x);
+        const float4* q4 = reinterpret_cast<const float4*>(sq);
+        float4 nx[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) nx[u] = __ldg(x4 + u);
+        for (int d4 = 0; d4 < dim / 4; d4 += 8) {
+          float4 cx[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) cx[u] = nx[u];
+          if (d4 + 8 < dim / 4) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) nx[u] = __ldg(x4 + d4 + 8 + u);
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const float4 qq = q4[d4 + u];
+            acc = fma((double)qq.x, (double)cx[u].x, acc);
+            acc = fma((double)qq.y, (double)cx[u].y, acc);
+            acc = fma((double)qq.z, (double)cx[u].z, acc);
+            acc = fma((double)qq.w, (double)cx[u].w, acc);
+          }
+        }
+      } else if ((dim & 15) == 0) {
         const float4* x4 = reinterpret_cast<const float4*>(x);
         const float4* q4 = reinterpret_cast<const float4*>(sq);
         float4 nx[4];
@@ -504,60 +528,77 @@ void query_dev(lc_index* ix, int kind, const float* Qdev, int nq, int k, uint64_
   static const bool diag = getenv("FC_LOOKUP_DIAG") && atoi(getenv("FC_LOOKUP_DIAG")) == 1;
   if (nf == 0 || diag) return;
   // Tier 2: the uncertified queries (near-ties around the k-th score) rerun
-  // the tensor-core shortlist with K' = 128 and are rescored/certified again
-  // (~one streaming pass of the bf16 table); only what still fails takes the
-  // exact fp64 scan of every row. FC_LOOKUP_TIER2=0 disables it.
+  // the tensor-core shortlist with a longer K' and are rescored/certified
+  // again (~one streaming pass of the bf16 table each), escalating K' = kp + 32
+  // then 128 (K' = kp + 32 certifies the usual near-ties at ~2/3 the cost, as
+  // more pipeline stages fit); only what still fails takes the exact fp64 scan
+  // of every row. FC_LOOKUP_TIER2=0 disables it; FC_LOOKUP_TIER2_KP caps K'.
   const bool tier2_off = getenv("FC_LOOKUP_TIER2") && atoi(getenv("FC_LOOKUP_TIER2")) == 0;
   const int dim = ix->dim;
-  DevBuf q2((size_t)nf * dim * sizeof(float), ctx->stream);
-  k_gather_queries<<<grid_for((int64_t)nf * dim, 256), 256, 0, ctx->stream>>>(Qdev, fl.as<int32_t>(), nf, dim,
-                                                                             q2.as<float>());
   constexpr int KP2_MAX = 128;
-  DevBuf cs2((size_t)nf * KP2_MAX * sizeof(float), ctx->stream), cr2((size_t)nf * KP2_MAX * sizeof(uint32_t), ctx->stream);
-  DevBuf cn2((size_t)nf * sizeof(int32_t), ctx->stream);
-  int kp2 = 0;  // the longest shortlist the kernel's shared memory allows at this dim (> kp)
-  if (!tier2_off && k <= KP2_MAX)
-    for (int cand = KP2_MAX; cand > kp && kp2 == 0; cand -= 32) {
+  int kp2_cap = KP2_MAX;
+  if (const char* e = getenv("FC_LOOKUP_TIER2_KP")) kp2_cap = std::max(kp + 32, std::min(KP2_MAX, atoi(e)));
+  DevBuf list_buf((size_t)nf * sizeof(int32_t), ctx->stream);  // current failures -> original query index
+  FC_CUDA(cudaMemcpyAsync(list_buf.p, fl.p, (size_t)nf * sizeof(int32_t), cudaMemcpyDeviceToDevice, ctx->stream));
+  int n_left = nf;
+  int prev = kp;
+  for (int level = 0; level < 2 && !tier2_off && n_left > 0; ++level) {
+    const int want = std::min(kp2_cap, level == 0 ? kp + 32 : KP2_MAX);
+    if (want <= prev || k > want) break;
+    DevBuf q2((size_t)n_left * dim * sizeof(float), ctx->stream);
+    k_gather_queries<<<grid_for((int64_t)n_left * dim, 256), 256, 0, ctx->stream>>>(Qdev, list_buf.as<int32_t>(), n_left,
+                                                                                   dim, q2.as<float>());
+    FC_LAUNCH_CHECK();
+    count_launch(ctx);
+    DevBuf cs2((size_t)n_left * want * sizeof(float), ctx->stream), cr2((size_t)n_left * want * sizeof(uint32_t), ctx->stream);
+    DevBuf cn2((size_t)n_left * sizeof(int32_t), ctx->stream);
+    int kp2 = 0;  // the longest shortlist <= want that the kernel's shared memory allows at this dim
+    for (int cand = want; cand > prev && kp2 == 0; cand -= 32) {
       try {
         ShortlistTimerName tn("shortlist_tier2");
-        approx_shortlist(ctx, ix->plan[kind], q2.as<float>(), nf, cand, cs2.as<float>(), cr2.as<uint32_t>(),
+        approx_shortlist(ctx, ix->plan[kind], q2.as<float>(), n_left, cand, cs2.as<float>(), cr2.as<uint32_t>(),
                          cn2.as<int32_t>());
         kp2 = cand;
       } catch (const Error& e) {
         if (e.code != LC_ERR_INVALID_ARGUMENT) throw;  // smem budget at this K': try a shorter one
       }
     }
-  if (kp2 == 0) {
-    exact_scan(ix, kind, Qdev, fl.as<int32_t>(), nf, k, oid, osc, ocnt);
-    return;
-  }
-  DevBuf id2((size_t)nf * k * sizeof(uint64_t), ctx->stream), sc2((size_t)nf * k * sizeof(double), ctx->stream);
-  DevBuf ct2((size_t)nf * sizeof(int32_t), ctx->stream), fl2((size_t)nf * sizeof(int32_t), ctx->stream);
-  DevBuf fn2(16, ctx->stream);
-  FC_CUDA(cudaMemsetAsync(fn2.p, 0, 16, ctx->stream));
-  {
-    KTimer kt2(ctx, "rescore_tier2");
-    k_rescore<4><<<(unsigned)((nf + RS_WARPS - 1) / RS_WARPS), RS_WARPS * 32, rs_smem, ctx->stream>>>(
-        q2.as<float>(), nf, dim, ix->rows[kind], ix->ids_dev, cs2.as<float>(), cr2.as<uint32_t>(), cn2.as<int32_t>(),
-        kp2, ix->n, k, ix->eps, id2.as<uint64_t>(), sc2.as<double>(), ct2.as<int32_t>(), fl2.as<int32_t>(),
-        fn2.as<int32_t>(), reinterpret_cast<unsigned long long*>(fn2.as<char>() + 8));
-  }
-  k_scatter_topk<<<grid_for((int64_t)nf * k, 256), 256, 0, ctx->stream>>>(
-      id2.as<uint64_t>(), sc2.as<double>(), ct2.as<int32_t>(), fl.as<int32_t>(), nf, k, oid, osc, ocnt);
-  FC_LAUNCH_CHECK();
-  count_launch(ctx, 3);
-  int32_t hf2[4] = {0, 0, 0, 0};
-  FC_CUDA(cudaMemcpyAsync(hf2, fn2.p, 16, cudaMemcpyDeviceToHost, ctx->stream));
-  sync(ctx);
-  const int nf2 = hf2[0];
-  ix->stats.tier2_certified += nf - nf2;
-  if (nf2 > 0) {
-    DevBuf ol((size_t)nf2 * sizeof(int32_t), ctx->stream);
-    k_map_list<<<grid_for(nf2, 128), 128, 0, ctx->stream>>>(fl2.as<int32_t>(), fl.as<int32_t>(), nf2, ol.as<int32_t>());
+    if (kp2 == 0) break;
+    prev = kp2;
+    DevBuf id2((size_t)n_left * k * sizeof(uint64_t), ctx->stream), sc2((size_t)n_left * k * sizeof(double), ctx->stream);
+    DevBuf ct2((size_t)n_left * sizeof(int32_t), ctx->stream), fl2((size_t)n_left * sizeof(int32_t), ctx->stream);
+    DevBuf fn2(16, ctx->stream);
+    FC_CUDA(cudaMemsetAsync(fn2.p, 0, 16, ctx->stream));
+    {
+      KTimer kt2(ctx, "rescore_tier2");
+      k_rescore<4><<<(unsigned)((n_left + RS_WARPS - 1) / RS_WARPS), RS_WARPS * 32, rs_smem, ctx->stream>>>(
+          q2.as<float>(), n_left, dim, ix->rows[kind], ix->ids_dev, cs2.as<float>(), cr2.as<uint32_t>(),
+          cn2.as<int32_t>(), kp2, ix->n, k, ix->eps, id2.as<uint64_t>(), sc2.as<double>(), ct2.as<int32_t>(),
+          fl2.as<int32_t>(), fn2.as<int32_t>(), reinterpret_cast<unsigned long long*>(fn2.as<char>() + 8));
+    }
+    // every row lands in place; the still-uncertified ones are overwritten below
+    k_scatter_topk<<<grid_for((int64_t)n_left * k, 256), 256, 0, ctx->stream>>>(
+        id2.as<uint64_t>(), sc2.as<double>(), ct2.as<int32_t>(), list_buf.as<int32_t>(), n_left, k, oid, osc, ocnt);
     FC_LAUNCH_CHECK();
-    count_launch(ctx);
-    exact_scan(ix, kind, Qdev, ol.as<int32_t>(), nf2, k, oid, osc, ocnt);
-    ix->stats.exact_scans += nf2;
+    count_launch(ctx, 2);
+    int32_t hf2[4] = {0, 0, 0, 0};
+    FC_CUDA(cudaMemcpyAsync(hf2, fn2.p, 16, cudaMemcpyDeviceToHost, ctx->stream));
+    sync(ctx);
+    const int nf2 = hf2[0];
+    ix->stats.tier2_certified += n_left - nf2;
+    if (nf2 > 0) {
+      DevBuf nl((size_t)nf2 * sizeof(int32_t), ctx->stream);
+      k_map_list<<<grid_for(nf2, 128), 128, 0, ctx->stream>>>(fl2.as<int32_t>(), list_buf.as<int32_t>(), nf2,
+                                                              nl.as<int32_t>());
+      FC_LAUNCH_CHECK();
+      count_launch(ctx);
+      FC_CUDA(cudaMemcpyAsync(list_buf.p, nl.p, (size_t)nf2 * sizeof(int32_t), cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    n_left = nf2;
+  }
+  if (n_left > 0) {
+    exact_scan(ix, kind, Qdev, list_buf.as<int32_t>(), n_left, k, oid, osc, ocnt);
+    ix->stats.exact_scans += n_left;
   }
 }
 

@@ -800,40 +800,54 @@ __device__ __forceinline__ uint32_t fkey(float f) {
 }
 
 // Per query: top-kp of the n_splits partial shortlists by bf16 score. One
-// warp per query: the non-empty slots are compacted (slot order kept) into
-// smem as (order-preserving key, slot); a 32-step binary search on the key
-// over those with warp-reduced counts finds the kp-th largest; ballot
-// compaction writes the result. Most slots are empty (every unit filters by
-// the query's shared acceptance threshold), so the search scans ~10x fewer
-// keys than the n_splits * kp slots.
+// warp per query: the filled prefix of every split's list (pn[] entries) is
+// compacted (slot order kept) as (order-preserving key, slot); a 32-step binary
+// search on the key over those with warp-reduced counts finds the kp-th
+// largest; ballot compaction writes the result. Most slots are empty (every
+// unit filters by the query's shared acceptance threshold), so only ~1/10 of
+// the n_splits * kp slots are read, and a small per-warp shared buffer (MG_CAP
+// items, spilling to gkeys when a query has more) keeps ~24 warps per SM
+// resident to hide the load latency.
 constexpr int MG_W = 8;
+constexpr int MG_CAP = 1024;
 __global__ void __launch_bounds__(MG_W * 32) k_shortlist_merge(const float* __restrict__ ps, const uint32_t* __restrict__ pr,
                                                                const int32_t* __restrict__ pn, int n_splits, int kp, int nq,
                                                                float* __restrict__ cs, uint32_t* __restrict__ cr,
                                                                int32_t* __restrict__ cn, uint32_t* __restrict__ gkeys) {
-  extern __shared__ uint32_t s_key[];  // [warps][2][n_splits * kp] (or gkeys [nq][2][..] when too large)
+  extern __shared__ uint32_t s_key[];  // [warps][2][MG_CAP] (gkeys [nq][2][n_splits * kp] past that)
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = blockIdx.x * (blockDim.x >> 5) + w;
   if (q >= nq) return;
   const int total = n_splits * kp;
-  uint32_t* key = gkeys ? gkeys + (size_t)q * 2 * total : s_key + (size_t)w * 2 * total;
-  uint32_t* slot = key + total;
+  const int32_t* pq = pn + (size_t)q * n_splits;
+  int n_all = 0;
+  for (int s0 = lane; s0 < n_splits; s0 += 32) n_all += min(__ldg(pq + s0), kp);
+  n_all = __reduce_add_sync(0xffffffffu, n_all);
+  const int cap = n_all <= MG_CAP ? MG_CAP : total;
+  uint32_t* key = n_all <= MG_CAP ? s_key + (size_t)w * 2 * MG_CAP : gkeys + (size_t)q * 2 * total;
+  uint32_t* slot = key + cap;
   const size_t base = (size_t)q * total;
-  int n_items = 0;  // dense prefix [0, n_items) of non-empty slots, in slot order
-  for (int i0 = 0; i0 < total; i0 += 32) {
-    const int i = i0 + lane;
-    uint32_t k = 0u;
-    if (i < total) {
-      const int sp = i / kp, j = i - sp * kp;
-      if (j < pn[(size_t)q * n_splits + sp]) k = fkey(ps[base + i]);
+  int n_items = 0;  // dense prefix [0, n_items) of filled slots, in slot order
+  for (int s0 = 0; s0 < n_splits; s0 += 32) {
+    const int c = s0 + lane < n_splits ? min(__ldg(pq + s0 + lane), kp) : 0;
+    int inc = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
     }
-    const unsigned bal = __ballot_sync(0xffffffffu, k != 0u);
-    if (k != 0u) {
-      const int at = n_items + __popc(bal & ((1u << lane) - 1));
-      key[at] = k;
-      slot[at] = (uint32_t)i;
+    const int ns = min(32, n_splits - s0);
+#pragma unroll 8
+    for (int t = 0; t < ns; ++t) {
+      const int ct = __shfl_sync(0xffffffffu, c, t);
+      const int off = n_items + __shfl_sync(0xffffffffu, inc, t) - ct;
+      const int sp = s0 + t;
+      for (int j = lane; j < ct; j += 32) {
+        key[off + j] = fkey(ps[base + (size_t)sp * kp + j]);
+        slot[off + j] = (uint32_t)(sp * kp + j);
+      }
     }
-    n_items += __popc(bal);
+    n_items += __shfl_sync(0xffffffffu, inc, 31);
   }
   __syncwarp();
   uint32_t T = 1;  // keep everything non-empty
@@ -875,6 +889,93 @@ __global__ void __launch_bounds__(MG_W * 32) k_shortlist_merge(const float* __re
     out += __popc(bal);
   }
   if (lane == 0) cn[q] = min(kp, out);
+}
+
+// Same selection as k_shortlist_merge with one CTA per query (MC_T threads):
+// used when there are too few queries to fill the GPU with one warp each (the
+// tier-2 re-shortlist of a handful of near-tie queries), where one warp would
+// walk tens of thousands of keys 32 times. Slot order is kept by a per-chunk
+// block scan, so the chosen candidates are identical.
+constexpr int MC_T = 1024;
+__device__ __forceinline__ int block_sum(int v, int* red) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  v = __reduce_add_sync(0xffffffffu, v);
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  int t = lane < (MC_T / 32) ? red[lane] : 0;
+  return __reduce_add_sync(0xffffffffu, t);
+}
+// Exclusive prefix of `flag` over the CTA in thread order; returns the chunk total.
+__device__ __forceinline__ int block_scan(bool flag, int* red, int* pre) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned bal = __ballot_sync(0xffffffffu, flag);
+  __syncthreads();
+  if (lane == 0) red[w] = __popc(bal);
+  __syncthreads();
+  int x = lane < (MC_T / 32) ? red[lane] : 0, inc = x;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  const int tot = __shfl_sync(0xffffffffu, inc, 31);
+  *pre = __shfl_sync(0xffffffffu, inc - x, w) + __popc(bal & ((1u << lane) - 1));
+  return tot;
+}
+__global__ void __launch_bounds__(MC_T) k_shortlist_merge_cta(const float* __restrict__ ps, const uint32_t* __restrict__ pr,
+                                                              const int32_t* __restrict__ pn, int n_splits, int kp,
+                                                              float* __restrict__ cs, uint32_t* __restrict__ cr,
+                                                              int32_t* __restrict__ cn) {
+  extern __shared__ uint32_t s_key[];  // [2][n_splits * kp]
+  __shared__ int red[MC_T / 32];
+  const int q = blockIdx.x;
+  const int total = n_splits * kp;
+  uint32_t* key = s_key;
+  uint32_t* slot = key + total;
+  const size_t base = (size_t)q * total;
+  int n_items = 0;
+  for (int i0 = 0; i0 < total; i0 += MC_T) {
+    const int i = i0 + threadIdx.x;
+    uint32_t k = 0u;
+    if (i < total) {
+      const int sp = i / kp, j = i - sp * kp;
+      if (j < pn[(size_t)q * n_splits + sp]) k = fkey(ps[base + i]);
+    }
+    int pre;
+    const int tot = block_scan(k != 0u, red, &pre);
+    if (k != 0u) {
+      key[n_items + pre] = k;
+      slot[n_items + pre] = (uint32_t)i;
+    }
+    n_items += tot;
+  }
+  __syncthreads();
+  uint32_t T = 1;
+  if (n_items > kp) {
+    uint32_t lo = 1, hi = 0xFFFFFFFFu;
+    while (lo < hi) {
+      const uint32_t mid = lo + (uint32_t)(((uint64_t)hi - lo + 1) >> 1);
+      int c = 0;
+      for (int i = threadIdx.x; i < n_items; i += MC_T) c += key[i] >= mid;
+      c = block_sum(c, red);
+      if (c >= kp) lo = mid; else hi = mid - 1;
+    }
+    T = lo;
+  }
+  int out = 0;
+  for (int pass = 0; pass < 2; ++pass)
+    for (int i0 = 0; i0 < n_items && out < kp; i0 += MC_T) {
+      const int i = i0 + threadIdx.x;
+      const bool take = i < n_items && (pass == 0 ? key[i] > T : key[i] == T);
+      int pre;
+      const int tot = block_scan(take, red, &pre);
+      if (take && out + pre < kp) {
+        cs[(size_t)q * kp + out + pre] = ps[base + slot[i]];
+        cr[(size_t)q * kp + out + pre] = pr[base + slot[i]];
+      }
+      out += tot;
+    }
+  if (threadIdx.x == 0) cn[q] = min(kp, out);
 }
 
 }  // namespace sm100
@@ -986,7 +1087,9 @@ void approx_shortlist(lc_ctx* ctx, const ApproxPlan& plan, const float* Qdev, in
                       uint32_t* cand_r, int32_t* cand_n) {
   using namespace sm100;
   const int dim = plan.dim;
-  const bool pair = use_pair(dim);
+  // a CTA pair's 256-query tile is mostly padding for a handful of queries
+  // (the tier-2 re-shortlist): the single-CTA kernel does half the MMA work
+  const bool pair = use_pair(dim) && nq > BM;
   const int qt = pair ? 2 * BM : BM;  // queries per work unit
   const int n_qtiles = (nq + qt - 1) / qt;
   const int nq_pad = n_qtiles * qt;
@@ -1002,6 +1105,8 @@ void approx_shortlist(lc_ctx* ctx, const ApproxPlan& plan, const float* Qdev, in
   // 74 splits 2.74 GB and 2.5 % faster; 148 splits cost more in the merge)
   int64_t splits = std::max<int64_t>(1, (workers * 16 + n_qtiles - 1) / n_qtiles);
   splits = std::min<int64_t>(splits, std::max<int64_t>(1, total_tiles / 16));
+  // keep one query's partial lists within the merge's shared memory (few queries)
+  splits = std::min<int64_t>(splits, std::max<int64_t>(workers, (200 * 1024) / ((int64_t)kp * 8)));
   const int64_t tiles_per_split = (total_tiles + splits - 1) / splits;
   splits = (total_tiles + tiles_per_split - 1) / tiles_per_split;
   Params prm;
@@ -1055,14 +1160,31 @@ void approx_shortlist(lc_ctx* ctx, const ApproxPlan& plan, const float* Qdev, in
             prm.cap, prm.n_splits);
   }
   const size_t per_warp = (size_t)splits * kp * 2 * sizeof(uint32_t);  // keys + slots
-  const int mw = (int)std::max<size_t>(1, std::min<size_t>(MG_W, (200 * 1024) / per_warp));
-  const bool in_smem = per_warp <= 200 * 1024;
-  DevBuf gkeys(in_smem ? 16 : (size_t)nq * per_warp, ctx->stream);
-  const size_t msmem = in_smem ? (size_t)mw * per_warp : 0;
-  if (msmem > 48 * 1024) FC_CUDA(cudaFuncSetAttribute(k_shortlist_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msmem));
-  k_shortlist_merge<<<(nq + mw - 1) / mw, mw * 32, msmem, ctx->stream>>>(
+  KTimer kmt(ctx, "shortlist_merge");
+  if (nq < ctx->sm_count && per_warp <= 200 * 1024) {
+    static int attr_dev = -1;
+    if (attr_dev != ctx->device) {
+      FC_CUDA(cudaFuncSetAttribute(k_shortlist_merge_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      attr_dev = ctx->device;
+    }
+    k_shortlist_merge_cta<<<nq, MC_T, per_warp, ctx->stream>>>(ps.as<float>(), pr.as<uint32_t>(), pn.as<int32_t>(),
+                                                               (int)splits, kp, cand_s, cand_r, cand_n);
+    FC_LAUNCH_CHECK();
+    count_launch(ctx, 3);
+    return;
+  }
+  // spill space for queries with more than MG_CAP filled slots (rare: the
+  // acceptance threshold keeps ~1/10 of the slots)
+  DevBuf gkeys(per_warp > (size_t)MG_CAP * 8 ? (size_t)nq * per_warp : 16, ctx->stream);
+  const size_t msmem = (size_t)MG_W * 2 * MG_CAP * sizeof(uint32_t);
+  static int attr_dev2 = -1;
+  if (attr_dev2 != ctx->device) {
+    FC_CUDA(cudaFuncSetAttribute(k_shortlist_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msmem));
+    attr_dev2 = ctx->device;
+  }
+  k_shortlist_merge<<<(nq + MG_W - 1) / MG_W, MG_W * 32, msmem, ctx->stream>>>(
       ps.as<float>(), pr.as<uint32_t>(), pn.as<int32_t>(), (int)splits, kp, nq, cand_s, cand_r, cand_n,
-      in_smem ? nullptr : gkeys.as<uint32_t>());
+      gkeys.as<uint32_t>());
   FC_LAUNCH_CHECK();
   count_launch(ctx, 3);
 }
