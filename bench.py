@@ -720,7 +720,9 @@ def bench_engine(torch, fc, ctx, args, dev):
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     m = eng.metrics()
-    return {"workload": f"config[0]: {n_c} cached prompts (768-d, 16 x 40x64x4 fp32), {n_r}-request Zipf(1.0) trace "
+    ist = ix.stats()
+    istats = {f: getattr(ist, f) for f, _ in ist._fields_}
+    return {"index_stats": istats, "workload": f"config[0]: {n_c} cached prompts (768-d, 16 x 40x64x4 fp32), {n_r}-request Zipf(1.0) trace "
                         f"over a 50x40 template grid (request noise U[0,2] x per-dim sigma), LRBU, unbounded capacity, "
                         "batches of 64",
             "requests_per_s": n_r / dt, "ms_per_request": dt / n_r * 1e3, "prefill_s": fill_s,

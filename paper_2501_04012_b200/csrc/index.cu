@@ -533,7 +533,12 @@ void query_dev(lc_index* ix, int kind, const float* Qdev, int nq, int k, uint64_
   // then 128 (K' = kp + 32 certifies the usual near-ties at ~2/3 the cost, as
   // more pipeline stages fit); only what still fails takes the exact fp64 scan
   // of every row. FC_LOOKUP_TIER2=0 disables it; FC_LOOKUP_TIER2_KP caps K'.
-  const bool tier2_off = getenv("FC_LOOKUP_TIER2") && atoi(getenv("FC_LOOKUP_TIER2")) == 0;
+  // Clustered tables (many near-duplicate rows per query, e.g. shared object
+  // embeddings) fail for most of the batch and a longer K' rarely helps there:
+  // when more than 1/16 of the batch (and > 8 queries) failed, go straight to
+  // the exact scan. Same results either way; this only picks the cheaper path.
+  const bool tier2_off = (getenv("FC_LOOKUP_TIER2") && atoi(getenv("FC_LOOKUP_TIER2")) == 0) ||
+                         (nf > 8 && nf * 16 > nq);
   const int dim = ix->dim;
   constexpr int KP2_MAX = 128;
   int kp2_cap = KP2_MAX;
