@@ -261,3 +261,27 @@ def test_near_tied_cluster_tier2_and_exact(fc, orc, synth, tier2):
             assert s.tier2_certified == 0
     finally:
         del os.environ["FC_LOOKUP_TIER2"]
+
+
+@pytest.mark.parametrize("nq", [40, 300])
+def test_duplicate_heavy_table_merge_paths(fc, orc, nq):
+    """A table of 1,000 distinct rows each stored 100 times (100k rows): every
+    work unit's shortlist fills up with equal scores, so the per-query merge
+    sees more filled slots than its shared-memory buffer (global spill path,
+    nq >= the SM count) or runs one CTA per query (nq < the SM count); ties
+    are broken by id exactly as the oracle does, and the uncertifiable queries
+    take the exact scan. Bit-exact with the oracle either way."""
+    rng = np.random.default_rng(77)
+    dim = 64
+    distinct = orc.normalize_rows(rng.standard_normal((1000, dim)).astype(np.float32))
+    tab = np.repeat(distinct, 100, axis=0)
+    perm = rng.permutation(tab.shape[0])
+    tab = np.ascontiguousarray(tab[perm])
+    ids = (np.arange(tab.shape[0], dtype=np.uint64) * 13 + 5)
+    q = orc.normalize_rows((distinct[rng.integers(0, 1000, nq)] +
+                            0.05 * rng.standard_normal((nq, dim))).astype(np.float32))
+    ix = build_index(fc, [tab, tab, tab], ids, mode=2, kprime=32)
+    gi, gs, gc = ix.query_topk(fc.EmbeddingKind.Whole, q, 8)
+    oi, os_, oc = orc.topk_flat(tab, ids, q, 8)
+    assert (gc == oc).all()
+    assert (u64(gi) == oi).all() and (bits(gs) == bits(os_)).all()
