@@ -711,12 +711,23 @@ def bench_engine(torch, fc, ctx, args, dev):
     del lat
     prompts = list(range(n_c + 1, n_c + n_r + 1))
     arrivals = list(range(1, n_r + 1))
+    # warm-up (untimed): one batch through a throwaway engine on the same
+    # context primes one-time costs (lazy module loads, host pools) that
+    # otherwise land on the first timed call (~0.1 s)
+    warm = fc.Engine(cfg, ctx=ctx)
+    warm.process(prompts[:64], arrivals[:64], qw[:64], qo[:64], qb[:64], lat_h[:64], om_h[:64], bm_h[:64])
+    del warm
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     outs = []
+    call_ms = []
     for j0 in range(0, n_r, 64):
         sl = slice(j0, j0 + 64)
+        tc = time.perf_counter()
         outs += eng.process(prompts[sl], arrivals[sl], qw[sl], qo[sl], qb[sl], lat_h[sl], om_h[sl], bm_h[sl])
+        call_ms.append(round((time.perf_counter() - tc) * 1e3, 2))
+    if os.environ.get("FC_TRACE") == "1":
+        print("[bench] engine process wall ms per call:", call_ms, file=sys.stderr)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     m = eng.metrics()

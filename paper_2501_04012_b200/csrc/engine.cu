@@ -75,9 +75,32 @@ struct lc_engine {
   lc_index* ix = nullptr;
   lc_store* st = nullptr;
   lc_engine_metrics m{};
+  // device staging for the deferred compressions' inputs, kept across calls:
+  // a fresh ~100 MB stream-ordered allocation per flush fragmented the pool
+  // against the store's entries and cost 5-190 ms of pool growth per call
+  void* stage = nullptr;
+  size_t stage_bytes = 0;
+  void* stage_for(size_t bytes) {
+    if (bytes > stage_bytes) {
+      if (stage) {
+        FC_CUDA(cudaStreamSynchronize(ctx->stream));
+        cudaFree(stage);
+        stage = nullptr;
+        stage_bytes = 0;
+      }
+      const size_t want = std::max(bytes, bytes + bytes / 2);
+      FC_CUDA(cudaMalloc(&stage, want));
+      stage_bytes = want;
+    }
+    return stage;
+  }
   ~lc_engine() {
     if (st) lc_store_destroy(st);
     if (ix) lc_index_destroy(ix);
+    if (stage) {
+      cudaStreamSynchronize(ctx->stream);
+      cudaFree(stage);
+    }
   }
 };
 
@@ -133,6 +156,24 @@ lc_status lc_engine_create(lc_ctx* ctx, const lc_engine_config* cfg, lc_engine**
   e->cfg = *cfg;
   ok(lc_index_create(ctx, cfg->dim, 0, &e->ix));
   ok(lc_store_create(ctx, cfg->capacity, cfg->policy, &e->st));
+  {
+    // Pre-grow the device's stream-ordered pool (its release threshold keeps
+    // freed memory cached, core.cu) to about what the store will hold: entry
+    // arenas then carve from mapped memory instead of growing the pool inside
+    // a request batch (4-30 ms per growth step measured on B200).
+    DeviceGuard g(ctx->device);
+    size_t free_b = 0, total_b = 0;
+    FC_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    size_t want = cfg->capacity > 0 ? (size_t)cfg->capacity + (size_t)cfg->capacity / 4 + (1ull << 30) : (8ull << 30);
+    want = std::min(want, free_b / 2);
+    void* p = nullptr;
+    if (want >= (64ull << 20) && cudaMallocAsync(&p, want, ctx->stream) == cudaSuccess) {
+      cudaFreeAsync(p, ctx->stream);
+      FC_CUDA(cudaStreamSynchronize(ctx->stream));
+    } else {
+      cudaGetLastError();  // reservation is best effort
+    }
+  }
   *out = e.release();
   LC_API_END
 }
@@ -248,22 +289,30 @@ lc_status lc_engine_process(lc_engine* e, const lc_request* req, int64_t n, cons
       if (grp.empty()) continue;
       const int S = 5 - first;
       const size_t m = grp.size(), fe = (size_t)S * c.F * E, fm = (size_t)c.F * mb;
-      DevBuf dl(m * fe * sizeof(float), e->ctx->stream), dom(m * fm, e->ctx->stream), dbm(m * fm, e->ctx->stream);
+      // inputs staged in the engine's persistent buffer (latents, then the
+      // two mask sets, 256-byte aligned); the previous group's compress has
+      // returned (it ends with a stream sync), so the buffer is free
+      const size_t lat_b = (m * fe * sizeof(float) + 255) & ~size_t(255), msk_b = (m * fm + 255) & ~size_t(255);
+      auto* sbase = static_cast<uint8_t*>(e->stage_for(lat_b + 2 * msk_b));
+      float* dl = reinterpret_cast<float*>(sbase);
+      uint8_t* dom = sbase + lat_b;
+      uint8_t* dbm = dom + msk_b;
       for (size_t q = 0; q < m; ++q) {
         const int64_t j = grp[q]->j;
-        FC_CUDA(cudaMemcpyAsync(dl.as<float>() + q * fe, latents + ((size_t)j * 5 + first) * c.F * E, fe * sizeof(float),
+        FC_CUDA(cudaMemcpyAsync(dl + q * fe, latents + ((size_t)j * 5 + first) * c.F * E, fe * sizeof(float),
                                 lat_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, e->ctx->stream));
-        FC_CUDA(cudaMemcpyAsync(dom.as<uint8_t>() + q * fm, obj_masks + (size_t)j * fm, fm,
+        FC_CUDA(cudaMemcpyAsync(dom + q * fm, obj_masks + (size_t)j * fm, fm,
                                 om_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, e->ctx->stream));
-        FC_CUDA(cudaMemcpyAsync(dbm.as<uint8_t>() + q * fm, bg_masks + (size_t)j * fm, fm,
+        FC_CUDA(cudaMemcpyAsync(dbm + q * fm, bg_masks + (size_t)j * fm, fm,
                                 bm_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, e->ctx->stream));
       }
       std::vector<uint64_t> pids(m);
       for (size_t q = 0; q < m; ++q) pids[q] = grp[q]->prompt;
       std::vector<lc_entry*> ents(m, nullptr);
       std::vector<int32_t> steps(kCached + first, kCached + 5);
-      ok(lc_compress_batch(e->ctx, dl.as<float>(), steps.data(), S, c.F, c.H, c.W, c.C, dom.as<uint8_t>(),
-                           dbm.as<uint8_t>(), c.compress_threshold, pids.data(), (int64_t)m, ents.data(), nullptr));
+      ok(lc_compress_batch(e->ctx, dl, steps.data(), S, c.F, c.H, c.W, c.C, dom, dbm, c.compress_threshold, pids.data(),
+                           (int64_t)m, ents.data(), nullptr));
+      sync(e->ctx);  // the staging buffer is reused by the next group / call
       for (size_t q = 0; q < m; ++q) ent_of[grp[q]->j] = ents[q];
     }
     pc.lap(4);
