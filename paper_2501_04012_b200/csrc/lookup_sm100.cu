@@ -21,6 +21,7 @@
 // split-major so that concurrently running CTAs stream the same table
 // region and every 128-query tile after the first reads it from L2.
 #include <cuda.h>
+#include <atomic>
 #include <cuda_bf16.h>
 #include <cudaTypedefs.h>
 
@@ -1162,10 +1163,10 @@ void approx_shortlist(lc_ctx* ctx, const ApproxPlan& plan, const float* Qdev, in
   const size_t per_warp = (size_t)splits * kp * 2 * sizeof(uint32_t);  // keys + slots
   KTimer kmt(ctx, "shortlist_merge");
   if (nq < ctx->sm_count && per_warp <= 200 * 1024) {
-    static int attr_dev = -1;
-    if (attr_dev != ctx->device) {
+    static std::atomic<uint64_t> attr_set{0};  // per-device bit: the attribute is per device
+    if (!(attr_set.load() >> (ctx->device & 63) & 1)) {
       FC_CUDA(cudaFuncSetAttribute(k_shortlist_merge_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      attr_dev = ctx->device;
+      attr_set.fetch_or(1ull << (ctx->device & 63));
     }
     k_shortlist_merge_cta<<<nq, MC_T, per_warp, ctx->stream>>>(ps.as<float>(), pr.as<uint32_t>(), pn.as<int32_t>(),
                                                                (int)splits, kp, cand_s, cand_r, cand_n);
@@ -1177,10 +1178,10 @@ void approx_shortlist(lc_ctx* ctx, const ApproxPlan& plan, const float* Qdev, in
   // acceptance threshold keeps ~1/10 of the slots)
   DevBuf gkeys(per_warp > (size_t)MG_CAP * 8 ? (size_t)nq * per_warp : 16, ctx->stream);
   const size_t msmem = (size_t)MG_W * 2 * MG_CAP * sizeof(uint32_t);
-  static int attr_dev2 = -1;
-  if (attr_dev2 != ctx->device) {
+  static std::atomic<uint64_t> attr_set2{0};
+  if (!(attr_set2.load() >> (ctx->device & 63) & 1)) {
     FC_CUDA(cudaFuncSetAttribute(k_shortlist_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msmem));
-    attr_dev2 = ctx->device;
+    attr_set2.fetch_or(1ull << (ctx->device & 63));
   }
   k_shortlist_merge<<<(nq + MG_W - 1) / MG_W, MG_W * 32, msmem, ctx->stream>>>(
       ps.as<float>(), pr.as<uint32_t>(), pn.as<int32_t>(), (int)splits, kp, nq, cand_s, cand_r, cand_n,
