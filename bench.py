@@ -392,13 +392,22 @@ def main():
     o_sc = torch.empty((B, k), dtype=torch.float64, device=dev)
     o_cnt = torch.empty((B,), dtype=torch.int32, device=dev)
     last = {}
+    comm = None
     if world > 1:
-        from paper_2501_04012_b200.sharded import ShardedIndex
-        shard = ShardedIndex(ix)  # one NCCL all-gather of packed (ids, scores, counts) + lc_topk_merge
+        # the communicator lives in the library context (lc_ctx_comm_init:
+        # NCCL over NVLink; host transport through the gloo group for
+        # FC_DIST_BACKEND=gloo smoke runs); each batch = local exact top-k,
+        # one grouped all-gather, k_topk_merge (lc_sharded_query_topk)
+        from paper_2501_04012_b200 import sharded
+        sharded.attach_comm(ctx, transport="nccl" if backend == "nccl" else "host")
+        shard = sharded.CommShardedIndex(ix, args.dim)
+        nr, rk, be, _ = sharded.comm_info(ctx)
+        comm = {"backend": {1: "nccl", 2: "host"}.get(be, "none"), "nranks": nr, "rank": rk,
+                "api": "lc_sharded_query_topk"}
 
     def step(q):
         if world > 1:
-            last["res"] = shard.query_topk(fc.EmbeddingKind.Whole, q, k)
+            last["res"] = shard.query_topk(fc.EmbeddingKind.Whole, q, k, out=(o_ids, o_sc, o_cnt))
         else:
             ix.query_topk(fc.EmbeddingKind.Whole, q, k, out=(o_ids, o_sc, o_cnt))
             last["res"] = (o_ids, o_sc, o_cnt)
@@ -502,7 +511,7 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e = {"value": args.steps * B / float(tt.item()), "unit": "lookups/s",
                "h2d_bytes_per_step": B * args.dim * 4, "d2h_bytes_per_step": B * k * 8,
-               "api": f"ShardedIndex.query_topk: lc_index_query_topk + one {backend} all-gather + lc_topk_merge, "
+               "api": f"lc_sharded_query_topk: local exact top-k + one {backend} all-gather + k_topk_merge, "
                       "pinned host queries"}
 
     # ---- codec (config[2]) ----
@@ -557,7 +566,7 @@ def main():
             "lookup_stats": {"certified": st.certified, "fallback": st.fallback, "max_abs_err": st.max_abs_err},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clk.summary(), "kernel_ms": {k_: round(v_[1], 3) for k_, v_ in kt.items()},
-            "codec": codec, "scoring": scoring, "engine": engine,
+            "codec": codec, "scoring": scoring, "engine": engine, "comm": comm,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -45,7 +45,7 @@ typedef enum lc_status {
   LC_ERR_SNAPSHOT = 5,         /* SnapshotError    errors.hpp:30             */
   LC_ERR_LOGIC = 6,            /* std::logic_error (evict_one on empty store, store.cpp:148) */
   LC_ERR_CUDA = 7,             /* CUDA runtime/driver failure                */
-  LC_ERR_NCCL = 8,             /* reserved: collective failure               */
+  LC_ERR_NCCL = 8,             /* collective failure (NCCL / host all-gather) */
   LC_ERR_OOM = 9,              /* device allocation failure                  */
   LC_ERR_INTERNAL = 10,
   LC_ERR_IO = 11               /* std::runtime_error: snapshot file I/O (store.cpp:268-276) */
@@ -171,7 +171,11 @@ typedef struct lc_lookup_stats {
 lc_status lc_index_stats(lc_index* ix, lc_lookup_stats* out, int reset);
 /* mode: 0 auto (tensor-core path when size >= 8192), 1 force exact scan,
  * 2 force tensor-core path. kprime: shortlist length (multiple of 32, <= 128).
- * eps: certified |bf16 - fp64| score bound (<= 0 -> default 2^-8 + 2^-12). */
+ * eps: certified |bf16 - fp64| score bound for a unit query (<= 0 -> default
+ * 2^-8 + 2^-12; values below that proven bound are clamped up to it). Each
+ * query's bound is scaled by max(1, ||q||), so non-unit queries stay exact;
+ * queries with a non-finite element fail with LC_ERR_INVALID_ARGUMENT
+ * (reference queries are Embeddings, core.cpp:11-15). */
 lc_status lc_index_set_lookup(lc_index* ix, int mode, int kprime, double eps);
 /* Shard merge for entry-sharded multi-GPU lookup (a23): merge G per-shard
  * exact top-k lists [G][n][k] (+counts [G][n]) into the global top-k
@@ -275,6 +279,17 @@ lc_status lc_store_evict_step(lc_store* s, uint64_t prompt, int step, int32_t* r
  * key), without removing it: the per-shard candidate of a global eviction
  * across entry-sharded stores. Empty => LC_ERR_LOGIC. */
 lc_status lc_store_peek(lc_store* s, uint64_t now, lc_step_entry* out, double* key);
+/* The next (up to) m steps repeated evict_one(now) would remove, in order,
+ * each with its policy key and used() after its removal — without removing
+ * them. Stops early with *more = 1 where the store would re-score its table.
+ * One call per shard per eviction burst of an entry-sharded store. */
+lc_status lc_store_peek_many(lc_store* s, uint64_t now, int m, lc_step_entry* out, double* keys,
+                             uint64_t* used_after, int* n_out, int* more);
+/* insert_steps validation only (store.cpp:53-76: step range, non-empty,
+ * prompt match, not cached, cacheable, present in entry); *standalone = the
+ * entry's shared + requested private bytes. No OversizedEntry check. */
+lc_status lc_store_check_insert(lc_store* s, uint64_t prompt, lc_entry* entry, const int32_t* steps,
+                                int n_steps, uint64_t* standalone);
 /* store.hpp:113 next_seq_: sharded stores keep one global insertion counter. */
 uint64_t lc_store_next_seq(lc_store* s);
 lc_status lc_store_set_next_seq(lc_store* s, uint64_t seq);
@@ -407,6 +422,59 @@ lc_status lc_synth_latents(lc_ctx* ctx, const uint64_t* prompt_seeds, int64_t n,
 /* lrbu_priority / lcbfu_priority (store.cpp:32-42) for n entries. */
 lc_status lc_priority_batch(lc_ctx* ctx, int policy, const lc_step_entry* e, int64_t n,
                             uint64_t now, double* out);
+
+/* ---------------------------------------------------------------------------
+ * Entry-sharded multi-GPU cache (the reference is single-node
+ * CPU and has no counterpart). One process or thread per GPU; prompt p lives
+ * on rank lc_shard_owner(p, G) = p mod G (its index rows, entry and live
+ * steps). Every sharded call is COLLECTIVE: all ranks call it in the same
+ * order with the same arguments (queries, prompt, steps, now).
+ * ------------------------------------------------------------------------- */
+/* ncclGetUniqueId: rank 0 creates it and shares the 128 bytes out of band. */
+lc_status lc_comm_unique_id(uint8_t* id128);
+/* NCCL communicator (ncclCommInitRank) on the context's GPU. */
+lc_status lc_ctx_comm_init(lc_ctx* ctx, int nranks, int rank, const uint8_t* id128);
+/* Caller-provided transport: fn all-gathers `bytes` from every rank into
+ * recv[nranks][bytes] (host buffers) and returns 0 on success. */
+typedef int (*lc_allgather_fn)(void* user, const void* send, void* recv, uint64_t bytes);
+lc_status lc_ctx_comm_host(lc_ctx* ctx, int nranks, int rank, lc_allgather_fn fn, void* user);
+/* backend: 0 none, 1 NCCL (nranks from ncclCommCount), 2 host callback. */
+lc_status lc_ctx_comm_info(lc_ctx* ctx, int* nranks, int* rank, int* backend,
+                           uint64_t* collectives);
+uint64_t lc_shard_owner(uint64_t prompt, int nranks);
+/* Global exact top-k over the union of the ranks' shards: local top-k
+ * (lc_index_query_topk path), one grouped all-gather of the [G][n][k] lists,
+ * merge by (score desc, id asc) (vindex.cpp:58-72). Same queries on every
+ * rank; every rank gets the full result. */
+lc_status lc_sharded_query_topk(lc_index* ix, int kind, const float* q, int64_t n, int dim, int k,
+                                uint64_t* out_ids, double* out_scores, int32_t* out_counts);
+lc_status lc_sharded_lookup_decide(lc_index* ix, const float* qw, const float* qo,
+                                   const float* qb, int64_t n, int dim, double hit_threshold,
+                                   const double* edges4, lc_decision* out);
+/* CacheStore (store.hpp:48-120) under ONE global capacity budget. Each rank
+ * owns a local unbounded store (lc_sharded_store_local) holding its prompts.
+ * insert_steps / evict_one produce the same StepEntry sequence, used() and
+ * next_seq as a single store holding every prompt: evictions are the
+ * (key, seq) merge of the shards' lc_store_peek_many lists, `batch` victims
+ * per shard per all-gather round (0 = 64). */
+typedef struct lc_sharded_store lc_sharded_store;
+lc_status lc_sharded_store_create(lc_ctx* ctx, uint64_t capacity, int policy, int batch,
+                                  lc_sharded_store** out);
+lc_status lc_sharded_store_destroy(lc_sharded_store* ss);
+lc_store* lc_sharded_store_local(lc_sharded_store* ss);
+/* entry: the owner rank passes the prompt's entry, the others NULL. Errors
+ * (validation, OversizedEntry) are raised on every rank. */
+lc_status lc_sharded_store_insert(lc_sharded_store* ss, uint64_t prompt, lc_entry* entry,
+                                  const int32_t* steps, int n_steps, uint64_t now,
+                                  lc_step_entry* evicted, int cap, int* n_evicted);
+lc_status lc_sharded_store_evict_one(lc_sharded_store* ss, uint64_t now, lc_step_entry* out);
+/* get_step on the owner (out_dev: owner's device buffer or NULL); every rank
+ * gets the actual step (0 = nothing served). */
+lc_status lc_sharded_store_get_step(lc_sharded_store* ss, uint64_t prompt, int desired, uint64_t now,
+                                    int32_t* actual, float* out_dev);
+lc_status lc_sharded_store_used(lc_sharded_store* ss, uint64_t* out);
+lc_status lc_sharded_store_stats(lc_sharded_store* ss, uint64_t* rounds, uint64_t* local_evictions,
+                                 uint64_t* next_seq);
 
 #ifdef __cplusplus
 }

@@ -895,6 +895,132 @@ inline SnapshotData load_snapshot(const std::filesystem::path& path,
   return SnapshotData{CacheStore(s, ctx), SimilarityIndex(i, ctx)};
 }
 
+// ---------------------------------------------------------------- entry-sharded multi-GPU
+// Not in the reference (single process, CPU). One process (or thread) per
+// GPU; prompt p lives on rank p mod G. Rank 0 makes a communicator id and
+// shares its 128 bytes out of band (MPI_Bcast, a TCP store, a file); every
+// rank attaches it to its context. All Sharded* calls are collective: every
+// rank calls them in the same order with the same arguments.
+namespace b200 {
+using CommId = std::array<std::uint8_t, 128>;
+inline CommId comm_unique_id() {
+  CommId id{};
+  check(lc_comm_unique_id(id.data()));
+  return id;
+}
+inline void attach_nccl(Context& ctx, int nranks, int rank, const CommId& id) {
+  check(lc_ctx_comm_init(ctx.get(), nranks, rank, id.data()));
+}
+// Caller-provided transport (e.g. MPI_Allgather): fn(user, send, recv[nranks][bytes], bytes) -> 0 on success.
+inline void attach_host_transport(Context& ctx, int nranks, int rank, lc_allgather_fn fn, void* user) {
+  check(lc_ctx_comm_host(ctx.get(), nranks, rank, fn, user));
+}
+inline std::uint64_t shard_owner(PromptId p, int nranks) { return lc_shard_owner(p.value, nranks); }
+}  // namespace b200
+
+// This rank's shard of the three tables; queries return the GLOBAL answer
+// (local exact top-k, one all-gather, merge by (score desc, id asc)).
+class ShardedSimilarityIndex {
+ public:
+  explicit ShardedSimilarityIndex(int dim, std::shared_ptr<b200::Context> ctx = b200::default_context())
+      : local_(dim, ctx), ctx_(std::move(ctx)), dim_(dim) {
+    b200::check(lc_ctx_comm_info(ctx_->get(), &nranks_, &rank_, nullptr, nullptr));
+  }
+  bool owns(PromptId p) const { return (int)b200::shard_owner(p, nranks_) == rank_; }
+  // not collective: only the owner stores the rows (others ignore the call)
+  void insert(const Embedding& whole, const Embedding& object, const Embedding& background, PromptId prompt) {
+    if (owns(prompt)) local_.insert(whole, object, background, prompt);
+  }
+  void remove(PromptId prompt) {
+    if (owns(prompt)) local_.remove(prompt);
+  }
+  std::optional<QueryResult> query_top1(EmbeddingKind kind, const Embedding& query) const {
+    std::uint64_t id = 0;
+    double sc = 0.0;
+    int32_t cnt = 0;
+    b200::check(lc_sharded_query_topk(local_.handle(), (int)kind, query.values().data(), 1, dim_, 1, &id, &sc, &cnt));
+    if (cnt == 0) return std::nullopt;
+    return QueryResult{PromptId{id}, sc};
+  }
+  std::vector<std::vector<QueryResult>> query_topk(EmbeddingKind kind, std::span<const float> queries, int k) const {
+    if (queries.size() % (size_t)dim_) throw std::invalid_argument("query_topk: bad query buffer");
+    const int64_t n = (int64_t)(queries.size() / dim_);
+    std::vector<std::uint64_t> ids((size_t)n * k);
+    std::vector<double> sc((size_t)n * k);
+    std::vector<int32_t> cnt((size_t)n);
+    b200::check(lc_sharded_query_topk(local_.handle(), (int)kind, queries.data(), n, dim_, k, ids.data(), sc.data(),
+                                      cnt.data()));
+    std::vector<std::vector<QueryResult>> out((size_t)n);
+    for (int64_t i = 0; i < n; ++i)
+      for (int j = 0; j < cnt[i]; ++j) out[i].push_back({PromptId{ids[i * k + j]}, sc[i * k + j]});
+    return out;
+  }
+  std::vector<lc_decision> lookup_decide(std::span<const float> q_whole, std::span<const float> q_object,
+                                         std::span<const float> q_background,
+                                         double hit_threshold = defaults::kHitThreshold) const {
+    if (q_whole.size() % (size_t)dim_ || q_object.size() != q_whole.size() || q_background.size() != q_whole.size())
+      throw std::invalid_argument("lookup_decide: bad query buffers");
+    const int64_t n = (int64_t)(q_whole.size() / dim_);
+    std::vector<lc_decision> out((size_t)n);
+    b200::check(lc_sharded_lookup_decide(local_.handle(), q_whole.data(), q_object.data(), q_background.data(), n,
+                                         dim_, hit_threshold, defaults::kStepBinEdges.data(), out.data()));
+    return out;
+  }
+  SimilarityIndex& local() { return local_; }
+
+ private:
+  SimilarityIndex local_;
+  std::shared_ptr<b200::Context> ctx_;
+  int dim_, nranks_ = 1, rank_ = 0;
+};
+
+// CacheStore under one global capacity budget: the same StepEntry sequence,
+// used() and sequence numbers as one CacheStore holding every prompt.
+class ShardedCacheStore {
+ public:
+  ShardedCacheStore(std::uint64_t capacity_limit, Policy policy,
+                    std::shared_ptr<b200::Context> ctx = b200::default_context(), int batch = 0)
+      : ctx_(std::move(ctx)) {
+    lc_sharded_store* h = nullptr;
+    b200::check(lc_sharded_store_create(ctx_->get(), capacity_limit, (int)policy, batch, &h));
+    h_.reset(h, [](lc_sharded_store* p) { lc_sharded_store_destroy(p); });
+  }
+  // entry: the owner rank's CompressedEntry, nullptr on the other ranks
+  std::vector<StepEntry> insert_steps(PromptId prompt, const CompressedEntry* entry, const std::vector<StepId>& steps,
+                                      std::uint64_t now) {
+    std::vector<int32_t> st;
+    for (StepId s : steps) st.push_back(s.value());
+    std::vector<lc_step_entry> ev(4096);
+    int n = 0;
+    b200::check(lc_sharded_store_insert(h_.get(), prompt.value, entry ? entry->handle() : nullptr, st.data(),
+                                        (int)st.size(), now, ev.data(), (int)ev.size(), &n));
+    std::vector<StepEntry> out;
+    for (int i = 0; i < std::min<int>(n, (int)ev.size()); ++i) out.push_back(b200::from_c(ev[i]));
+    return out;
+  }
+  StepEntry evict_one(std::uint64_t now) {
+    lc_step_entry e{};
+    b200::check(lc_sharded_store_evict_one(h_.get(), now, &e));
+    return b200::from_c(e);
+  }
+  // the actual step served (0 = nothing); the latent stays on the owner's GPU (out_dev, owner only)
+  int get_step(PromptId prompt, StepId desired, std::uint64_t now, float* out_dev = nullptr) {
+    int32_t a = 0;
+    b200::check(lc_sharded_store_get_step(h_.get(), prompt.value, desired.value(), now, &a, out_dev));
+    return a;
+  }
+  std::uint64_t used() const {
+    std::uint64_t u = 0;
+    b200::check(lc_sharded_store_used(h_.get(), &u));
+    return u;
+  }
+  lc_store* local_handle() const { return lc_sharded_store_local(h_.get()); }
+
+ private:
+  std::shared_ptr<b200::Context> ctx_;
+  std::shared_ptr<lc_sharded_store> h_;
+};
+
 }  // namespace LCACHE_B200_NS
 
 template <>

@@ -113,7 +113,10 @@ def _check(rc):
         raise SnapshotError(msg, int(lib.lc_last_snapshot_offset()))
     err = cls(msg)
     err.code = rc
-    raise err
+    try:
+        raise err
+    finally:  # no frame <-> exception cycle (it would keep library objects alive until a GC pass)
+        del err
 
 
 class EmbeddingKind(IntEnum):
@@ -207,6 +210,14 @@ class Context:
 _default_ctx: Context | None = None
 
 
+def _alive(ctx) -> bool:
+    """False once the context was destroyed: objects found in the same garbage
+    cycle as their context may be finalised after it (PEP 442 order is
+    arbitrary); their device memory then goes with the process instead of
+    being released through a dangling context."""
+    return ctx is None or bool(getattr(ctx, "h", None))
+
+
 def default_context() -> Context:
     global _default_ctx
     if _default_ctx is None:
@@ -263,7 +274,7 @@ class SimilarityIndex:
 
     def __del__(self):
         try:
-            if self.h and not getattr(self, "_borrowed", None):
+            if self.h and not getattr(self, "_borrowed", None) and _alive(self.ctx):
                 lib.lc_index_destroy(self.h)
                 self.h = None
         except Exception:
@@ -402,7 +413,7 @@ class CompressedEntry:
 
     def __del__(self):
         try:
-            if self.owned and self.h:
+            if self.owned and self.h and _alive(self.ctx):
                 lib.lc_entry_release(self.h)
                 self.h = None
         except Exception:
@@ -628,7 +639,7 @@ class CacheStore:
 
     def __del__(self):
         try:
-            if self.h and not getattr(self, "_borrowed", None):
+            if self.h and not getattr(self, "_borrowed", None) and _alive(self.ctx):
                 lib.lc_store_destroy(self.h)
                 self.h = None
         except Exception:
@@ -792,7 +803,7 @@ class Engine:
 
     def __del__(self):
         try:
-            if self.h:
+            if self.h and _alive(self.ctx):
                 lib.lc_engine_destroy(self.h)
                 self.h = None
         except Exception:

@@ -172,6 +172,27 @@ _sig("lc_store_cached_steps", st, vp, u64, vp, C.POINTER(C.c_int))
 _sig("lc_store_entry", st, vp, u64, C.POINTER(vp))
 _sig("lc_store_entries", st, vp, vp, i64, C.POINTER(i64))
 _sig("lc_priority_batch", st, vp, C.c_int, vp, i64, u64, vp)
+_sig("lc_store_peek_many", st, vp, u64, C.c_int, C.POINTER(StepEntry), vp, vp, C.POINTER(C.c_int),
+     C.POINTER(C.c_int))
+_sig("lc_store_check_insert", st, vp, u64, vp, vp, C.c_int, C.POINTER(u64))
+# entry-sharded multi-GPU (shard.cu)
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, vp, vp, vp, u64)
+_sig("lc_comm_unique_id", st, vp)
+_sig("lc_ctx_comm_init", st, vp, C.c_int, C.c_int, vp)
+_sig("lc_ctx_comm_host", st, vp, C.c_int, C.c_int, ALLGATHER_FN, vp)
+_sig("lc_ctx_comm_info", st, vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(u64))
+_sig("lc_shard_owner", u64, u64, C.c_int)
+_sig("lc_sharded_query_topk", st, vp, C.c_int, vp, i64, C.c_int, C.c_int, vp, vp, vp)
+_sig("lc_sharded_lookup_decide", st, vp, vp, vp, vp, i64, C.c_int, f64, vp, vp)
+_sig("lc_sharded_store_create", st, vp, u64, C.c_int, C.c_int, C.POINTER(vp))
+_sig("lc_sharded_store_destroy", st, vp)
+_sig("lc_sharded_store_local", vp, vp)
+_sig("lc_sharded_store_insert", st, vp, u64, vp, vp, C.c_int, u64, C.POINTER(StepEntry), C.c_int,
+     C.POINTER(C.c_int))
+_sig("lc_sharded_store_evict_one", st, vp, u64, C.POINTER(StepEntry))
+_sig("lc_sharded_store_get_step", st, vp, u64, C.c_int, u64, C.POINTER(i32), vp)
+_sig("lc_sharded_store_used", st, vp, C.POINTER(u64))
+_sig("lc_sharded_store_stats", st, vp, C.POINTER(u64), C.POINTER(u64), C.POINTER(u64))
 
 # every symbol declared in include/flexcache_b200.h (checked by the CPU tests)
 EXPORTED = sorted(n for n in dir(lib) if n.startswith("lc_"))

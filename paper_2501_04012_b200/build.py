@@ -13,7 +13,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(OUT_DIR, "libflexcache_b200.so")
-SOURCES = ["core.cu", "index.cu", "lookup_sm100.cu", "gram_sm100.cu", "codec.cu", "store.cu", "engine.cu", "simgen.cu"]
+SOURCES = ["core.cu", "index.cu", "lookup_sm100.cu", "gram_sm100.cu", "codec.cu", "store.cu", "engine.cu", "simgen.cu", "shard.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off", "-Xptxas", "-v",
@@ -61,7 +61,7 @@ def build(verbose: bool = False, jobs: int = 8) -> str:
                 _drain(procs, verbose)
     _drain(procs, verbose)
     if _stale(LIB, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart", "-lcuda"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart", "-lcuda", "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError("link failed:\n" + r.stdout + r.stderr)

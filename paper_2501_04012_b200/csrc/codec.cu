@@ -42,14 +42,14 @@ void gram_tc(lc_ctx* ctx, const float* lat, int n_items, int F, int64_t E, doubl
 
 DevArena::~DevArena() {
   if (p) {
-    DeviceGuard g(ctx->device);
+    QuietDeviceGuard g(ctx->device);
     cudaFreeAsync(p, ctx->stream);
   }
 }
 
 EntryData::~EntryData() {
   if (dev && !arena) {
-    DeviceGuard g(ctx->device);
+    QuietDeviceGuard g(ctx->device);
     cudaFreeAsync(dev, ctx->stream);
   }
 }
@@ -1750,6 +1750,14 @@ struct Reader {
     return v;
   }
   const uint8_t* bytes(uint64_t k) { need(k); const uint8_t* r = p + pos; pos += k; return r; }
+  // `count` items of `each` bytes that the reference reads one at a time
+  // (ByteReader::f32_array per float, in.bytes per mask): a truncation is
+  // reported at the start of the first incomplete item (serialize.hpp:86-105)
+  const uint8_t* items(uint64_t count, uint64_t each) {
+    if (pos + count * each > n) raise_snap("truncated input", pos + each * ((n - pos) / each));
+    return bytes(count * each);
+  }
+  const uint8_t* f32s(uint64_t k) { return items(k, 4); }
 };
 
 bool bytes_finite(const uint8_t* p, int64_t n) {  // n little-endian fp32 values, any alignment
@@ -1835,7 +1843,7 @@ lc_entry* import_entry(lc_ctx* ctx, const uint8_t* bytes, uint64_t len, uint64_t
     const int step = r.u8();
     if (step < 1 || step > 50) raise(LC_ERR_INVALID_ARGUMENT, "StepId: value out of range 1..50");
     d->steps[s] = step;
-    firsts[s] = r.bytes(4ull * E);
+    firsts[s] = r.f32s((uint64_t)E);
     d->maps[s].resize(d->F);
     for (int j = 0; j < d->F; ++j) {
       d->maps[s][j] = r.u16();
@@ -1843,13 +1851,13 @@ lc_entry* import_entry(lc_ctx* ctx, const uint8_t* bytes, uint64_t len, uint64_t
     }
     // Frame(dims, first) validates here, before anything later is parsed (core.cpp:19-25)
     if (!bytes_finite(firsts[s], E)) raise(LC_ERR_INVALID_ARGUMENT, "Frame: non-finite element");
-    if (step != base) raw_alpha[s] = r.bytes(4ull * nd);
+    if (step != base) raw_alpha[s] = r.f32s((uint64_t)nd);
     const int nx = r.u16();
     std::vector<std::pair<int, const uint8_t*>> xs;
     for (int x = 0; x < nx; ++x) {
       const int m = r.u16();
       if (m >= d->F) raise_snap("extra frame index out of range", step_pos);
-      const uint8_t* fr = r.bytes(4ull * E);
+      const uint8_t* fr = r.f32s((uint64_t)E);
       if (!bytes_finite(fr, E)) raise(LC_ERR_INVALID_ARGUMENT, "Frame: non-finite element");
       bool dup = false;
       for (auto& pr : xs) dup |= pr.first == m;
@@ -1869,7 +1877,7 @@ lc_entry* import_entry(lc_ctx* ctx, const uint8_t* bytes, uint64_t len, uint64_t
     const int m = r.u16();
     if (m < 1 || m >= d->F) raise_snap("diff index out of range", pos);
     all_idx[t] = m;
-    const uint8_t* df = r.bytes(4ull * E);
+    const uint8_t* df = r.f32s((uint64_t)E);
     // base_diffs.diffs.emplace keeps the first of a repeated index (codec.cpp:443)
     if (std::find(d->diff_idx.begin(), d->diff_idx.end(), m) == d->diff_idx.end()) {
       d->diff_idx.push_back(m);
@@ -1884,7 +1892,7 @@ lc_entry* import_entry(lc_ctx* ctx, const uint8_t* bytes, uint64_t len, uint64_t
     for (int t = 0, u = 0; t < nd; ++t)  // alphas.emplace keeps the first too (codec.cpp:448-451)
       if (t == 0 || all_idx[t] != all_idx[t - 1]) memcpy(&d->alphas[s][u++], raw_alpha[s] + 4ull * t, 4);
   }
-  const uint8_t* masks = r.bytes(2ull * d->F * d->mb);
+  const uint8_t* masks = r.items(2ull * d->F, (uint64_t)d->mb);
   *consumed = r.pos;
   // host image -> device
   int64_t off = 0;

@@ -67,6 +67,11 @@ void set_last_oversize(uint64_t needed, uint64_t limit);
 
 }  // namespace fc
 
+namespace fc {
+struct Comm;  // shard.cu: NCCL communicator or host all-gather callback
+void comm_free(Comm* c);
+}  // namespace fc
+
 struct lc_ctx {
   int device = 0;
   int sm_count = 148;
@@ -85,6 +90,8 @@ struct lc_ctx {
   std::mutex aux_mu;
   std::vector<lc_ctx*> aux;
   lc_ctx* top() { return root ? root : this; }
+  // entry-sharded multi-GPU (lc_ctx_comm_init / lc_ctx_comm_host)
+  fc::Comm* comm = nullptr;
 };
 
 namespace fc {
@@ -124,6 +131,21 @@ struct DeviceGuard {
     int cur = -1;
     cudaGetDevice(&cur);
     if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// For destructors: switches device like DeviceGuard but never throws (a
+// destructor that throws terminates the process, e.g. during CUDA teardown).
+struct QuietDeviceGuard {
+  int prev = -1;
+  explicit QuietDeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev && cudaSetDevice(dev) != cudaSuccess) cudaGetLastError();
+  }
+  ~QuietDeviceGuard() {
+    int cur = -1;
+    if (cudaGetDevice(&cur) == cudaSuccess && prev >= 0 && cur != prev) cudaSetDevice(prev);
+    cudaGetLastError();
   }
 };
 

@@ -258,6 +258,7 @@ lc_status lc_ctx_destroy(lc_ctx* ctx) {
     delete c;
   }
   cudaStreamSynchronize(ctx->stream);
+  comm_free(ctx->comm);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   LC_API_END

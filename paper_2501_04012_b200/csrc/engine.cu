@@ -267,6 +267,7 @@ lc_status lc_engine_process(lc_engine* e, const lc_request* req, int64_t n, cons
     int64_t j;
     uint64_t prompt, now;
     int first;
+    bool added_ix;  // its embeddings were registered for the index at deferral
   };
   std::vector<Pending> pending;
   std::unordered_set<uint64_t> pending_ids;
@@ -278,10 +279,20 @@ lc_status lc_engine_process(lc_engine* e, const lc_request* req, int64_t n, cons
     return 20 + (F - 1) * fr + 2 * F * (uint64_t)mb + (uint64_t)S * (1 + 4 * (uint64_t)E + 2 * F + 4 * (F - 1) + 2 + (F - 1) * fr);
   };
   const bool lat_dev = is_device_ptr(latents), om_dev = is_device_ptr(obj_masks), bm_dev = is_device_ptr(bg_masks);
+  // A deferred update that cannot be stored (its compress or insert failed)
+  // must not leave its prompt in the index: a later lookup would hit a prompt
+  // with no store record.
+  auto unregister = [&](const Pending& pd) {
+    if (!pd.added_ix) return;
+    int32_t cached = 0;
+    ok(lc_store_contains(e->st, pd.prompt, &cached));
+    if (!cached && index_has(pd.prompt)) index_remove(pd.prompt);
+  };
   auto flush = [&]() {
     if (pending.empty()) return;
     // one compress per step set; entries in request order
     std::map<int64_t, lc_entry*> ent_of;
+    try {
     for (int first = 0; first < 5; ++first) {
       std::vector<const Pending*> grp;
       for (const auto& pd : pending)
@@ -315,6 +326,17 @@ lc_status lc_engine_process(lc_engine* e, const lc_request* req, int64_t n, cons
       sync(e->ctx);  // the staging buffer is reused by the next group / call
       for (size_t q = 0; q < m; ++q) ent_of[grp[q]->j] = ents[q];
     }
+    } catch (...) {
+      // nothing of this flush is stored: release what was compressed and take
+      // the pending prompts back out of the index
+      for (auto& kv : ent_of) lc_entry_release(kv.second);
+      std::vector<Pending> drop;
+      drop.swap(pending);
+      pending_ids.clear();
+      pending_bound = 0;
+      for (const auto& pd : drop) unregister(pd);
+      throw;
+    }
     pc.lap(4);
     std::exception_ptr err = nullptr;
     for (const auto& pd : pending) {
@@ -341,9 +363,12 @@ lc_status lc_engine_process(lc_engine* e, const lc_request* req, int64_t n, cons
       }
       lc_entry_release(ent);
     }
-    pending.clear();
+    std::vector<Pending> done;
+    done.swap(pending);
     pending_ids.clear();
     pending_bound = 0;
+    if (err)
+      for (const auto& pd : done) unregister(pd);  // the failed insert and every later one
     pc.lap(5);
     if (err) std::rethrow_exception(err);
   };
@@ -461,12 +486,13 @@ lc_status lc_engine_process(lc_engine* e, const lc_request* req, int64_t n, cons
       const uint64_t bound = size_bound(S);
       if (!cached && defer_ok && lc_store_used(e->st) + pending_bound + bound <= c.capacity &&
           pending_bound + bound >= pending_bound) {
-        pending.push_back(Pending{j, r.prompt, now, first});
+        const bool add_ix = !index_has(r.prompt);
+        pending.push_back(Pending{j, r.prompt, now, first, add_ix});
         pending_ids.insert(r.prompt);
         pending_bound += bound;
         o.n_inserted = S;
         pc.lap(3);
-        if (!index_has(r.prompt))
+        if (add_ix)
           index_add(r.prompt, qh[0].data() + (size_t)j * d, qh[1].data() + (size_t)j * d, qh[2].data() + (size_t)j * d);
         pc.lap(7);
       } else if (!cached) {

@@ -46,13 +46,28 @@ struct lc_index {
   std::unordered_map<uint64_t, int64_t> slot;
   int mode = 0;
   int kprime = 32;
-  double eps = 0.00390625 + 0.000244140625;  // 2^-8 + 2^-12, see lookup.cuh
+  double eps = kEpsBound;  // certified bound for a unit query; scaled by ||q|| per query (k_rescore)
   lc_lookup_stats stats{};
   ApproxPlan plan[3];
   mutable std::shared_mutex mu;  // readers: queries; writer: insert/remove (vindex.hpp:61)
+  // Concurrent readers (shared lock on mu) still touch two pieces of shared
+  // state: the per-table tensor-map plans (rebuilt lazily after a mutation)
+  // and the counters; each has its own small lock.
+  std::mutex plan_mu, stats_mu;
 };
 
 namespace fc {
+
+// Non-finite query elements (reference queries are Embeddings, which reject
+// them: core.cpp:11-15, 50-53). One thread per query row.
+__global__ void k_check_finite_rows(const float* __restrict__ v, int64_t n, int dim, int* __restrict__ bad) {
+  int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const float* x = v + r * dim;
+  bool ok = true;
+  for (int i = 0; i < dim; ++i) ok &= isfinite(x[i]);
+  if (!ok) atomicExch(bad, 1);
+}
 
 // from_unit rule (core.cpp:61-69) on device rows: finite and
 // |sqrt(sum v^2) - 1| <= 1e-6 with a sequential fp64 sum.
@@ -214,15 +229,37 @@ __global__ void __launch_bounds__(RS_WARPS * 32)
               const uint64_t* __restrict__ ids, const float* __restrict__ cand_s, const uint32_t* __restrict__ cand_r,
               const int32_t* __restrict__ cand_n, int kp, int64_t n_rows, int k, double eps, uint64_t* __restrict__ out_ids,
               double* __restrict__ out_sc, int32_t* __restrict__ out_cnt, int32_t* __restrict__ fail_list,
-              int32_t* __restrict__ fail_n, unsigned long long* __restrict__ max_err_bits) {
+              int32_t* __restrict__ fail_n, unsigned long long* __restrict__ max_err_bits,
+              int32_t* __restrict__ bad_query) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = blockIdx.x * RS_WARPS + warp;
   if (q >= nq) return;
   const float* qv = Q + (int64_t)q * dim;
   extern __shared__ float s_rq[];  // [RS_WARPS][dim] this warp's query
   float* sq = s_rq + (size_t)warp * dim;
-  for (int d = lane; d < dim; d += 32) sq[d] = qv[d];
+  double qsq = 0.0;
+  bool qfin = true;
+  for (int d = lane; d < dim; d += 32) {
+    const float v = qv[d];
+    sq[d] = v;
+    qfin &= isfinite(v);
+    qsq = fma((double)v, (double)v, qsq);
+  }
   __syncwarp();
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) qsq += __shfl_xor_sync(0xffffffffu, qsq, off);
+  qfin = __all_sync(0xffffffffu, qfin);
+  if (!qfin && lane == 0) atomicExch(bad_query, 1);
+  // The error model (lookup.cuh) bounds |bf16 - exact| by eps * ||q|| * ||x||
+  // with ||x|| = 1 (rows pass the from_unit rule on insert). Queries through
+  // the C-ABI are not guaranteed unit, so the bound is scaled by ||q|| (the
+  // (1 + 2^-20) covers the rounding of the norm itself); queries of norm <= 1
+  // keep the unit bound (conservative). A query so large that fp32
+  // accumulation could overflow, or a non-finite one, is never certified.
+  const double qn = sqrt(qsq);
+  // (shortlist scores are stored as fp16: |score| <= ||q|| must stay far below 65504)
+  const bool q_uncertifiable = !qfin || !(qn < 16384.0);
+  eps = eps * fmax(1.0, qn * (1.0 + 0x1p-20));
   const int cn = cand_n[q];
   // Only candidates whose bf16 score is within 2*eps of the k-th best bf16
   // score can reach the exact top-k: the k candidates ranked first by bf16
@@ -252,7 +289,10 @@ __global__ void __launch_bounds__(RS_WARPS * 32)
       if (bal) ak = __shfl_sync(0xffffffffu, mine_a[t], __ffs(bal) - 1);
     }
   }
-  const float skip_below = ak - (float)(2.0 * eps) - 1e-6f;  // slack for the float subtraction
+  // shortlist scores are fp16 values rounded UP from the fp32 accumulator
+  // (lookup_sm100.cu hkey_ru): a candidate's approx lies in [s - ulp, s], with
+  // ulp <= |s| * 2^-10 + 2^-24, which widens the window by that much
+  const float skip_below = ak - (float)(2.0 * eps) - fabsf(ak) * 0x1p-10f - 0x1p-20f;
   Cand mine[PER_LANE];
   int mn = 0;
   float min_approx = INFINITY;
@@ -369,7 +409,7 @@ __global__ void __launch_bounds__(RS_WARPS * 32)
     bool ok;
     if (cn < (kp < n_rows ? kp : n_rows)) ok = false;
     else if (cn >= n_rows) ok = true;
-    else ok = got >= k && (double)min_approx + eps < tk;
+    else ok = !q_uncertifiable && got >= k && (double)min_approx + eps < tk;
     if (!ok) fail_list[atomicAdd(fail_n, 1)] = q;
   }
 }
@@ -469,12 +509,27 @@ void exact_scan(lc_index* ix, int kind, const float* Qdev, const int32_t* qlist_
 // Device-resident top-k (no host sync unless a fallback is needed).
 void query_dev(lc_index* ix, int kind, const float* Qdev, int nq, int k, uint64_t* oid, double* osc, int32_t* ocnt) {
   lc_ctx* ctx = ix->ctx;
-  ix->stats.queries += nq;
+  {
+    std::lock_guard<std::mutex> sl(ix->stats_mu);
+    ix->stats.queries += nq;
+  }
   const bool approx_ok = approx_available() && ix->dim % 64 == 0 && ix->dim <= 1024 && k <= ix->kprime;
   const bool use_approx = approx_ok && (ix->mode == 2 || (ix->mode == 0 && ix->n >= 8192));
   if (!use_approx) {
     FC_REQUIRE(ix->mode != 2 || approx_ok, "lc_index_query_topk: tensor-core path unavailable for this shape");
+    {
+      DevBuf bad(sizeof(int), ctx->stream);
+      FC_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), ctx->stream));
+      k_check_finite_rows<<<grid_for(nq, 128), 128, 0, ctx->stream>>>(Qdev, nq, ix->dim, bad.as<int>());
+      FC_LAUNCH_CHECK();
+      count_launch(ctx);
+      int hb = 0;
+      FC_CUDA(cudaMemcpyAsync(&hb, bad.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+      sync(ctx);
+      if (hb) raise(LC_ERR_INVALID_ARGUMENT, "Embedding: non-finite element");
+    }
     exact_scan(ix, kind, Qdev, nullptr, nq, k, oid, osc, ocnt);
+    std::lock_guard<std::mutex> sl(ix->stats_mu);
     ix->stats.exact_scans += nq;
     return;
   }
@@ -482,12 +537,16 @@ void query_dev(lc_index* ix, int kind, const float* Qdev, int nq, int k, uint64_
   DevBuf cs((size_t)nq * kp * sizeof(float), ctx->stream);
   DevBuf cr((size_t)nq * kp * sizeof(uint32_t), ctx->stream);
   DevBuf cn((size_t)nq * sizeof(int32_t), ctx->stream);
-  if (!ix->plan[kind].valid || ix->plan[kind].n_rows != ix->n)
-    approx_plan(ix->plan[kind], ix->rowsb[kind], ix->n, ix->dim, ctx->sm_count);
+  {
+    std::lock_guard<std::mutex> pl(ix->plan_mu);
+    if (!ix->plan[kind].valid || ix->plan[kind].n_rows != ix->n)
+      approx_plan(ix->plan[kind], ix->rowsb[kind], ix->n, ix->dim, ctx->sm_count);
+  }
   approx_shortlist(ctx, ix->plan[kind], Qdev, nq, kp, cs.as<float>(), cr.as<uint32_t>(), cn.as<int32_t>());
   DevBuf fl((size_t)nq * sizeof(int32_t), ctx->stream);
-  DevBuf fn(16, ctx->stream);  // [0,4) fail count, [8,16) max |err| bits
+  DevBuf fn(16, ctx->stream);  // [0,4) fail count, [4,8) non-finite query flag, [8,16) max |err| bits
   int32_t* fail_n = fn.as<int32_t>();
+  int32_t* bad_q = fn.as<int32_t>() + 1;
   auto* err_bits = reinterpret_cast<unsigned long long*>(fn.as<char>() + 8);
   FC_CUDA(cudaMemsetAsync(fn.p, 0, 16, ctx->stream));
   const unsigned g = (unsigned)((nq + RS_WARPS - 1) / RS_WARPS);
@@ -501,15 +560,15 @@ void query_dev(lc_index* ix, int kind, const float* Qdev, int nq, int k, uint64_
   if (kp <= 32)
     k_rescore<1><<<g, RS_WARPS * 32, rs_smem, ctx->stream>>>(Qdev, nq, ix->dim, ix->rows[kind], ix->ids_dev, cs.as<float>(),
                                                        cr.as<uint32_t>(), cn.as<int32_t>(), kp, ix->n, k, ix->eps, oid, osc, ocnt,
-                                                       fl.as<int32_t>(), fail_n, err_bits);
+                                                       fl.as<int32_t>(), fail_n, err_bits, bad_q);
   else if (kp <= 64)
     k_rescore<2><<<g, RS_WARPS * 32, rs_smem, ctx->stream>>>(Qdev, nq, ix->dim, ix->rows[kind], ix->ids_dev, cs.as<float>(),
                                                        cr.as<uint32_t>(), cn.as<int32_t>(), kp, ix->n, k, ix->eps, oid, osc, ocnt,
-                                                       fl.as<int32_t>(), fail_n, err_bits);
+                                                       fl.as<int32_t>(), fail_n, err_bits, bad_q);
   else
     k_rescore<4><<<g, RS_WARPS * 32, rs_smem, ctx->stream>>>(Qdev, nq, ix->dim, ix->rows[kind], ix->ids_dev, cs.as<float>(),
                                                        cr.as<uint32_t>(), cn.as<int32_t>(), kp, ix->n, k, ix->eps, oid, osc, ocnt,
-                                                       fl.as<int32_t>(), fail_n, err_bits);
+                                                       fl.as<int32_t>(), fail_n, err_bits, bad_q);
   kt.stop();
   FC_LAUNCH_CHECK();
   count_launch(ctx);
@@ -519,10 +578,14 @@ void query_dev(lc_index* ix, int kind, const float* Qdev, int nq, int k, uint64_
   double err = 0.0;
   uint64_t eb = (uint64_t)(uint32_t)hf[2] | ((uint64_t)(uint32_t)hf[3] << 32);
   memcpy(&err, &eb, 8);
-  ix->stats.max_abs_err = std::max(ix->stats.max_abs_err, err);
+  if (hf[1]) raise(LC_ERR_INVALID_ARGUMENT, "Embedding: non-finite element");
   const int nf = hf[0];
-  ix->stats.certified += nq - nf;
-  ix->stats.fallback += nf;
+  {
+    std::lock_guard<std::mutex> sl(ix->stats_mu);
+    ix->stats.max_abs_err = std::max(ix->stats.max_abs_err, err);
+    ix->stats.certified += nq - nf;
+    ix->stats.fallback += nf;
+  }
   // FC_LOOKUP_DIAG=1 (kernel-timing diagnostics with FC_SHORTLIST_DEBUG only): skip the
   // exact re-scan, so results are NOT exact in that mode.
   static const bool diag = getenv("FC_LOOKUP_DIAG") && atoi(getenv("FC_LOOKUP_DIAG")) == 1;
@@ -579,7 +642,8 @@ void query_dev(lc_index* ix, int kind, const float* Qdev, int nq, int k, uint64_
       k_rescore<4><<<(unsigned)((n_left + RS_WARPS - 1) / RS_WARPS), RS_WARPS * 32, rs_smem, ctx->stream>>>(
           q2.as<float>(), n_left, dim, ix->rows[kind], ix->ids_dev, cs2.as<float>(), cr2.as<uint32_t>(),
           cn2.as<int32_t>(), kp2, ix->n, k, ix->eps, id2.as<uint64_t>(), sc2.as<double>(), ct2.as<int32_t>(),
-          fl2.as<int32_t>(), fn2.as<int32_t>(), reinterpret_cast<unsigned long long*>(fn2.as<char>() + 8));
+          fl2.as<int32_t>(), fn2.as<int32_t>(), reinterpret_cast<unsigned long long*>(fn2.as<char>() + 8),
+          fn2.as<int32_t>() + 1);
     }
     // every row lands in place; the still-uncertified ones are overwritten below
     k_scatter_topk<<<grid_for((int64_t)n_left * k, 256), 256, 0, ctx->stream>>>(
@@ -590,7 +654,10 @@ void query_dev(lc_index* ix, int kind, const float* Qdev, int nq, int k, uint64_
     FC_CUDA(cudaMemcpyAsync(hf2, fn2.p, 16, cudaMemcpyDeviceToHost, ctx->stream));
     sync(ctx);
     const int nf2 = hf2[0];
-    ix->stats.tier2_certified += n_left - nf2;
+    {
+      std::lock_guard<std::mutex> sl(ix->stats_mu);
+      ix->stats.tier2_certified += n_left - nf2;
+    }
     if (nf2 > 0) {
       DevBuf nl((size_t)nf2 * sizeof(int32_t), ctx->stream);
       k_map_list<<<grid_for(nf2, 128), 128, 0, ctx->stream>>>(fl2.as<int32_t>(), list_buf.as<int32_t>(), nf2,
@@ -603,11 +670,32 @@ void query_dev(lc_index* ix, int kind, const float* Qdev, int nq, int k, uint64_
   }
   if (n_left > 0) {
     exact_scan(ix, kind, Qdev, list_buf.as<int32_t>(), n_left, k, oid, osc, ocnt);
+    std::lock_guard<std::mutex> sl(ix->stats_mu);
     ix->stats.exact_scans += n_left;
   }
 }
 
 }  // namespace
+
+namespace fc {
+// Device-resident exact top-k for the entry-sharded path (shard.cu): the
+// rank-local lookup whose lists the collective merges. Q/outputs on device;
+// an empty table yields counts 0. Takes the index's reader lock.
+lc_ctx* index_ctx(lc_index* ix) { return ix->ctx; }
+int index_dim(lc_index* ix) { return ix->dim; }
+void index_topk_dev(lc_index* ix, int kind, const float* Qdev, int nq, int k, uint64_t* oid, double* osc, int32_t* ocnt) {
+  std::shared_lock lock(ix->mu);
+  lc_ctx* ctx = ix->ctx;
+  if (nq <= 0) return;
+  if (ix->n == 0) {
+    FC_CUDA(cudaMemsetAsync(oid, 0, (size_t)nq * k * sizeof(uint64_t), ctx->stream));
+    FC_CUDA(cudaMemsetAsync(osc, 0, (size_t)nq * k * sizeof(double), ctx->stream));
+    FC_CUDA(cudaMemsetAsync(ocnt, 0, (size_t)nq * sizeof(int32_t), ctx->stream));
+    return;
+  }
+  query_dev(ix, kind, Qdev, nq, k, oid, osc, ocnt);
+}
+}  // namespace fc
 
 extern "C" {
 
@@ -768,13 +856,16 @@ lc_status lc_index_set_lookup(lc_index* ix, int mode, int kprime, double eps) {
   std::unique_lock lock(ix->mu);
   ix->mode = mode;
   if (kprime) ix->kprime = kprime;
-  if (eps > 0) ix->eps = eps;
+  // the certificate is only sound at or above the proven bound (lookup.cuh):
+  // a larger eps only widens it, a smaller one is clamped
+  if (eps > 0) ix->eps = std::max(eps, kEpsBound);
   LC_API_END
 }
 
 lc_status lc_index_stats(lc_index* ix, lc_lookup_stats* out, int reset) {
   LC_API_BEGIN
   std::unique_lock lock(ix->mu);
+  std::lock_guard<std::mutex> sl(ix->stats_mu);
   if (out) *out = ix->stats;
   if (reset) ix->stats = lc_lookup_stats{};
   LC_API_END

@@ -8,6 +8,9 @@
 // adds <= 1024 * 2^-23 * sum|q_i x_i| ~ 1.2e-4. The default certified bound
 // eps = 2^-8 + 2^-12 = 0.0041 covers both; the measured maximum is reported
 // in lc_lookup_stats.max_abs_err.
+// For a query of norm ||q|| != 1 every term above scales by ||q||, so the
+// rescore uses eps * max(1, ||q||) per query (index.cu k_rescore); the bound
+// cannot be lowered below kEpsBound through lc_index_set_lookup.
 #pragma once
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -15,6 +18,8 @@
 #include "common.cuh"
 
 namespace fc {
+
+constexpr double kEpsBound = 0.00390625 + 0.000244140625;  // 2^-8 + 2^-12
 
 struct ApproxPlan {
   bool valid = false;

@@ -23,6 +23,7 @@
 #include <cuda.h>
 #include <atomic>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cudaTypedefs.h>
 
 #include <cstring>
@@ -82,61 +83,56 @@ __device__ __forceinline__ float key_float(uint32_t k) {
   return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k);
 }
 
-// Cheaper compaction for the pair kernel: bisection on the order key with an
-// early stop as soon as the kept set is within [kp, kp + 8] (~5 passes over
-// the buffer instead of 32). Keeping a few more than kp is harmless: the new
-// threshold T is <= the kp-th best kept score, so every later rejection
-// (score <= T) stays below the final K'-th shortlisted score.
-__device__ __noinline__ void compact2(float* ls, uint32_t* lr, int t, int& cnt, int kp, float& tau) {
-  if (cnt <= kp + 8) return;
+// ---- packed shortlist candidates ----
+// A candidate is ONE u32: (order-preserving key of the score rounded UP to
+// fp16) << 16 | row offset within the work unit's row range (< 65536). The
+// stored score is an upper bound of the fp32 accumulator value, so the
+// certificate "every row outside the shortlist has approx <= m" holds with m =
+// the K'-th best STORED score; larger keys are better, and keys are unique
+// within a unit (distinct offsets). Half the shared memory of (fp32, u32)
+// pairs: the freed bytes deepen the TMA ring.
+__device__ __forceinline__ uint32_t hkey_ru(float v) {
+  const uint32_t h = __half_as_ushort(__float2half_ru(v));
+  return (h & 0x8000u) ? (~h & 0xFFFFu) : (h | 0x8000u);
+}
+__device__ __forceinline__ float hkey_float(uint32_t k16) {
+  const uint32_t h = (k16 & 0x8000u) ? (k16 & 0x7FFFu) : (~k16 & 0xFFFFu);
+  return __half2float(__ushort_as_half((unsigned short)h));
+}
+
+// Keep the kp largest keys of the thread's list (exact) or, while streaming,
+// between kp and kp + 8 of them (bisection with early stop); raise tau to the
+// stored score of the smallest kept key. Every later rejection (score <= tau)
+// then ranks below kp kept entries, so it is below the final K'-th stored
+// score of the query. Called warp-uniformly.
+__device__ __noinline__ void compact_keys(uint32_t* lk, int t, int& cnt, int kp, float& tau, bool exact) {
+  if (cnt <= (exact ? kp : kp + 8)) return;
   uint32_t lo = 0xFFFFFFFFu, hi = 0;
   for (int i = 0; i < cnt; ++i) {
-    const uint32_t k = okey(ls[i * BM + t]);
+    const uint32_t k = lk[i * BM + t];
     lo = min(lo, k);
     hi = max(hi, k);
   }
-  int cge = cnt;  // count(key >= lo)
-  while (lo < hi) {
+  const int slack = exact ? 0 : 8;
+  while (lo < hi) {  // max T with count(key >= T) >= kp
     const uint32_t mid = lo + (uint32_t)(((uint64_t)hi - lo + 1) >> 1);
     int c = 0;
-    for (int i = 0; i < cnt; ++i) c += okey(ls[i * BM + t]) >= mid;
+    for (int i = 0; i < cnt; ++i) c += lk[i * BM + t] >= mid;
     if (c >= kp) {
       lo = mid;
-      cge = c;
-      if (c <= kp + 8) break;
+      if (c <= kp + slack) break;
     } else {
       hi = mid - 1;
     }
   }
   const uint32_t T = lo;
   int w = 0;
-  if (cge <= kp + 8) {
-    for (int i = 0; i < cnt; ++i) {
-      const float v = ls[i * BM + t];
-      if (okey(v) >= T) {
-        ls[w * BM + t] = v;
-        lr[w * BM + t] = lr[i * BM + t];
-        ++w;
-      }
-    }
-  } else {  // many ties at T: everything above T, then == T up to kp
-    int above = 0;
-    for (int i = 0; i < cnt; ++i) above += okey(ls[i * BM + t]) > T;
-    int need_eq = kp - above;
-    for (int i = 0; i < cnt; ++i) {
-      const float v = ls[i * BM + t];
-      const uint32_t k = okey(v);
-      const bool keep = k > T || (k == T && need_eq > 0);
-      need_eq -= (k == T && keep);
-      if (keep) {
-        ls[w * BM + t] = v;
-        lr[w * BM + t] = lr[i * BM + t];
-        ++w;
-      }
-    }
+  for (int i = 0; i < cnt; ++i) {
+    const uint32_t k = lk[i * BM + t];
+    if (k >= T) lk[w++ * BM + t] = k;
   }
   cnt = w;
-  const float tnew = key_float(T);
+  const float tnew = hkey_float(T >> 16);
   if (tnew > tau) tau = tnew;
 }
 
@@ -188,9 +184,9 @@ __device__ __forceinline__ float hedge(int b) {  // smallest score of bucket b >
   const int e = 119 + (b - 1) / BPO, m = (b - 1) % BPO;
   return __uint_as_float(((uint32_t)e << 23) | ((uint32_t)m << BPO_SHIFT));
 }
-__device__ __forceinline__ void hist_publish(uint32_t* h, const float* ls, int t, int from, int to) {
+__device__ __forceinline__ void hist_publish(uint32_t* h, const uint32_t* lk, int t, int from, int to) {
   for (int i = from; i < to; ++i) {
-    const int bk = hbucket(ls[i * BM + t]);
+    const int bk = hbucket(hkey_float(lk[i * BM + t] >> 16));
     if (bk == 0) continue;  // never used to raise a threshold
     atomicAdd(h + bk, 1u);
     atomicAdd(h + HC + (bk - 1) / BPO, 1u);
@@ -257,8 +253,7 @@ struct Params {
   uint32_t* stats;  // FC_SHORTLIST_DEBUG & 16: [slow chunks, compactions, warp-tiles]
   int debug;   // diagnostics (FC_SHORTLIST_DEBUG): 1 = skip MMA, 2 = skip TMA, 4 = skip epilogue filter
   int nstage;
-  float* part_s;             // [nq][n_splits][kp]
-  uint32_t* part_r;
+  uint32_t* part_k;          // [nq][n_splits][kp] packed candidates (hkey_ru(score) << 16 | row - r0)
   int32_t* part_n;           // [nq][n_splits]
 };
 
@@ -458,10 +453,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_shortlist(const __grid_constant
       // (3) write the shortlist of this (query, split)
       if (q < p.nq) {
         const size_t o = ((size_t)q * p.n_splits + split) * p.kp;
-        for (int i = 0; i < cnt; ++i) {
-          p.part_s[o + i] = ls[i * BM + t];
-          p.part_r[o + i] = lr[i * BM + t];
-        }
+        for (int i = 0; i < cnt; ++i) p.part_k[o + i] = (hkey_ru(ls[i * BM + t]) << 16) | (lr[i * BM + t] - (uint32_t)r0);
         p.part_n[(size_t)q * p.n_splits + split] = cnt;
       }
     }
@@ -537,9 +529,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   const int nsg = nkb / BPS;
   uint8_t* stages = base;
   uint8_t* asmem = base + NSTAGE * STAGE_BYTES;
-  float* ls = reinterpret_cast<float*>(asmem + KS * ABOX);
-  uint32_t* lr = reinterpret_cast<uint32_t*>(ls + cap * BM);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(lr + cap * BM);
+  uint32_t* lk = reinterpret_cast<uint32_t*>(asmem + KS * ABOX);  // [cap][BM] packed candidates
+  uint64_t* bars = reinterpret_cast<uint64_t*>(lk + cap * BM);
   uint64_t* full = bars;
   uint64_t* empty = bars + NSTAGE;
   uint64_t* accf = bars + 2 * NSTAGE;
@@ -709,36 +700,50 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       float tau = -INFINITY;
       uint32_t* hq = p.hist + (size_t)q * HSTRIDE;
       hist_refresh(hq, p.kp, tau);
+      // FC_SHORTLIST_DEBUG & 16: per-warp clock64 spans [accumulator wait, histogram, compaction, appends]
+      long long cyc[4] = {0, 0, 0, 0}, c_t0 = 0;
+      const bool prof = p.debug & 16;
       for (int64_t row = r0; row < r1; row += PN, ++tile) {
         const uint32_t b = tile & 1;
         const uint32_t use = tile >> 1;
         if ((tile & p.refresh_mask) == 0) {
-          hist_publish(hq, ls, t, pub, cnt);
+          if (prof) c_t0 = clock64();
+          hist_publish(hq, lk, t, pub, cnt);
           pub = cnt;
           hist_refresh(hq, p.kp, tau);
+          if (prof) cyc[1] += clock64() - c_t0;
         }
+        if (prof) c_t0 = clock64();
         mbar_wait(smem_u32(&accf[b]), use & 1);
         tc_fence_after();
+        if (prof) cyc[0] += clock64() - c_t0;
         if ((p.debug & 16) && lane == 0) atomicAdd(p.stats + 2, 1u);
         const int lim_all = (int)min((int64_t)PN, r1 - row);
-        // 32 accumulator columns per step (a rolled loop: the unrolled
-        // 128-column body overflowed the instruction cache, ncu "no_inst").
-        // Per 16-score chunk a max tree and a warp vote skip the append code
-        // unless some query of the warp has a score above its threshold.
-#pragma unroll 1
-        for (int cc = 0; cc < PN / 32; ++cc) {
-          float v[32];
-          tmem_ld32(tmem + lane_base + ACC_COL + b * PN + cc * 32, v);
-          if (cc == PN / 32 - 1) {
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive_remote(smem_u32(&acce[b]), 0);
+        const uint32_t off_base = (uint32_t)(row - r0);
+        // The tile's 128 accumulator columns in four 32-column loads, software
+        // pipelined over two register sets (the next load is in flight while
+        // the current columns are filtered). Nothing that may call a function
+        // (compaction) runs while a load is in flight: before each 32-column
+        // step the buffers are compacted if 32 more appends might not fit.
+        const uint32_t acc_base = tmem + lane_base + ACC_COL + b * PN;
+        auto make_room = [&]() {
+          if (__any_sync(0xffffffffu, cnt + 32 > cap)) {
+            if ((p.debug & 16) && lane == 0) atomicAdd(p.stats + 1, 1u);
+            if (prof) c_t0 = clock64();
+            hist_publish(hq, lk, t, pub, cnt);  // count before compaction may drop entries
+            compact_keys(lk, t, cnt, p.kp, tau, false);
+            pub = cnt;
+            if (prof) cyc[2] += clock64() - c_t0;
           }
-          if (p.debug & 4) continue;
+        };
+        auto filter = [&](const uint32_t* r, int col0) {
+          if (p.debug & 4) return;
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
-            const float* vc = v + hh * 16;
-            const int c0 = cc * 32 + hh * 16;
+            float vc[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) vc[i] = __uint_as_float(r[hh * 16 + i]);
+            const int c0 = col0 + hh * 16;
             float a0 = fmaxf(vc[0], vc[1]), a1 = fmaxf(vc[2], vc[3]), a2 = fmaxf(vc[4], vc[5]), a3 = fmaxf(vc[6], vc[7]);
             a0 = fmaxf(a0, fmaxf(vc[8], vc[9]));
             a1 = fmaxf(a1, fmaxf(vc[10], vc[11]));
@@ -748,33 +753,56 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             if (!__any_sync(0xffffffffu, (mx > tau) | (lim_all < PN))) continue;
             if (p.debug & 32) continue;  // diagnostic: fast path only
             if ((p.debug & 16) && lane == 0) atomicAdd(p.stats + 0, 1u);
-            if (__any_sync(0xffffffffu, cnt + 16 > cap)) {
-              if ((p.debug & 16) && lane == 0) atomicAdd(p.stats + 1, 1u);
-              hist_publish(hq, ls, t, pub, cnt);  // count before compaction may drop entries
-              compact2(ls, lr, t, cnt, p.kp, tau);
-              pub = cnt;
-            }
-            const uint32_t r32 = (uint32_t)(row + c0);
+            if (prof) c_t0 = clock64();
+            // accepted scores go to independent slots (popc of the accept
+            // mask below each column): no dependent chain through cnt
+            uint32_t m = 0;
 #pragma unroll
-            for (int jj = 0; jj < 16; ++jj) {
-              const bool acc = (c0 + jj < lim_all) & (vc[jj] > tau);
-              if (acc) {
-                ls[cnt * BM + t] = vc[jj];
-                lr[cnt * BM + t] = r32 + jj;
-              }
-              cnt += acc;
-            }
+            for (int jj = 0; jj < 16; ++jj) m |= (uint32_t)((c0 + jj < lim_all) & (vc[jj] > tau)) << jj;
+            const uint32_t off0 = off_base + (uint32_t)c0;
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj)
+              if ((m >> jj) & 1u) lk[(cnt + __popc(m & ((1u << jj) - 1u))) * BM + t] = (hkey_ru(vc[jj]) << 16) | (off0 + jj);
+            cnt += __popc(m);
+            if (prof) cyc[3] += clock64() - c_t0;
+          }
+        };
+        uint32_t ra[32], rb[32];
+        make_room();
+        tmem_ld32_issue(acc_base, ra);
+        tmem_ld32_wait(ra);
+#pragma unroll 1
+        for (int cp = 0; cp < PN / 32; cp += 2) {
+          tmem_ld32_issue(acc_base + (cp + 1) * 32, rb);
+          filter(ra, cp * 32);
+          tmem_ld32_wait(rb);
+          const bool last = cp + 2 >= PN / 32;
+          if (last) {  // every column of this accumulator buffer has been read
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_remote(smem_u32(&acce[b]), 0);
+          }
+          make_room();
+          if (!last) tmem_ld32_issue(acc_base + (cp + 2) * 32, ra);
+          filter(rb, (cp + 1) * 32);
+          if (!last) {
+            tmem_ld32_wait(ra);
+            make_room();
           }
         }
       }
-      hist_publish(hq, ls, t, pub, cnt);
-      compact(ls, lr, t, cnt, p.kp, tau);  // exact: the unit's list holds at most kp entries
+      if (prof) c_t0 = clock64();
+      hist_publish(hq, lk, t, pub, cnt);
+      compact_keys(lk, t, cnt, p.kp, tau, true);  // exact: the unit's list holds at most kp entries
+      if (prof) {
+        cyc[2] += clock64() - c_t0;
+        if (lane == 0)
+          for (int i = 0; i < 4; ++i)
+            atomicAdd(reinterpret_cast<unsigned long long*>(p.stats + 4) + i, (unsigned long long)cyc[i]);
+      }
       if (q < p.nq) {
         const size_t o = ((size_t)q * p.n_splits + split) * p.kp;
-        for (int i = 0; i < cnt; ++i) {
-          p.part_s[o + i] = ls[i * BM + t];
-          p.part_r[o + i] = lr[i * BM + t];
-        }
+        for (int i = 0; i < cnt; ++i) p.part_k[o + i] = lk[i * BM + t];
         p.part_n[(size_t)q * p.n_splits + split] = cnt;
       }
     }
@@ -795,14 +823,11 @@ __global__ void k_q_to_bf16(const float* __restrict__ Q, int nq, int dim, __nv_b
   Qb[i] = q < nq ? __float2bfloat16_rn(Q[i]) : __float2bfloat16_rn(0.f);
 }
 
-__device__ __forceinline__ uint32_t fkey(float f) {
-  const uint32_t u = __float_as_uint(f);
-  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-}
 
-// Per query: top-kp of the n_splits partial shortlists by bf16 score. One
-// warp per query: the filled prefix of every split's list (pn[] entries) is
-// compacted (slot order kept) as (order-preserving key, slot); a 32-step binary
+// Per query: top-kp of the n_splits partial shortlists by packed key (stored
+// fp16 upper-bound score, then row offset). One warp per query: the filled
+// prefix of every split's list (pn[] entries) is
+// compacted (slot order kept) as (key, slot); a 32-step binary
 // search on the key over those with warp-reduced counts finds the kp-th
 // largest; ballot compaction writes the result. Most slots are empty (every
 // unit filters by the query's shared acceptance threshold), so only ~1/10 of
@@ -811,9 +836,16 @@ __device__ __forceinline__ uint32_t fkey(float f) {
 // resident to hide the load latency.
 constexpr int MG_W = 8;
 constexpr int MG_CAP = 1024;
-__global__ void __launch_bounds__(MG_W * 32) k_shortlist_merge(const float* __restrict__ ps, const uint32_t* __restrict__ pr,
-                                                               const int32_t* __restrict__ pn, int n_splits, int kp, int nq,
-                                                               float* __restrict__ cs, uint32_t* __restrict__ cr,
+// One output candidate: stored score (upper bound of the bf16 score) and
+// absolute row slot of a packed key found at `slot` (= split * kp + j).
+__device__ __forceinline__ void emit(uint32_t key, uint32_t slot, int kp, int rps, float* cs, uint32_t* cr, size_t at) {
+  cs[at] = hkey_float(key >> 16);
+  cr[at] = (slot / (uint32_t)kp) * (uint32_t)rps + (key & 0xFFFFu);
+}
+
+__global__ void __launch_bounds__(MG_W * 32) k_shortlist_merge(const uint32_t* __restrict__ pk,
+                                                               const int32_t* __restrict__ pn, int n_splits, int kp, int rps,
+                                                               int nq, float* __restrict__ cs, uint32_t* __restrict__ cr,
                                                                int32_t* __restrict__ cn, uint32_t* __restrict__ gkeys) {
   extern __shared__ uint32_t s_key[];  // [warps][2][MG_CAP] (gkeys [nq][2][n_splits * kp] past that)
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -844,7 +876,7 @@ __global__ void __launch_bounds__(MG_W * 32) k_shortlist_merge(const float* __re
       const int off = n_items + __shfl_sync(0xffffffffu, inc, t) - ct;
       const int sp = s0 + t;
       for (int j = lane; j < ct; j += 32) {
-        key[off + j] = fkey(ps[base + (size_t)sp * kp + j]);
+        key[off + j] = __ldg(pk + base + (size_t)sp * kp + j);
         slot[off + j] = (uint32_t)(sp * kp + j);
       }
     }
@@ -871,8 +903,7 @@ __global__ void __launch_bounds__(MG_W * 32) k_shortlist_merge(const float* __re
     const unsigned bal = __ballot_sync(0xffffffffu, take);
     if (take) {
       const int at = out + __popc(bal & ((1u << lane) - 1));
-      cs[(size_t)q * kp + at] = ps[base + slot[i]];
-      cr[(size_t)q * kp + at] = pr[base + slot[i]];
+      emit(key[i], slot[i], kp, rps, cs, cr, (size_t)q * kp + at);
     }
     out += __popc(bal);
   }
@@ -882,10 +913,7 @@ __global__ void __launch_bounds__(MG_W * 32) k_shortlist_merge(const float* __re
     const unsigned bal = __ballot_sync(0xffffffffu, take);
     if (take) {
       const int at = out + __popc(bal & ((1u << lane) - 1));
-      if (at < kp) {
-        cs[(size_t)q * kp + at] = ps[base + slot[i]];
-        cr[(size_t)q * kp + at] = pr[base + slot[i]];
-      }
+      if (at < kp) emit(key[i], slot[i], kp, rps, cs, cr, (size_t)q * kp + at);
     }
     out += __popc(bal);
   }
@@ -923,8 +951,8 @@ __device__ __forceinline__ int block_scan(bool flag, int* red, int* pre) {
   *pre = __shfl_sync(0xffffffffu, inc - x, w) + __popc(bal & ((1u << lane) - 1));
   return tot;
 }
-__global__ void __launch_bounds__(MC_T) k_shortlist_merge_cta(const float* __restrict__ ps, const uint32_t* __restrict__ pr,
-                                                              const int32_t* __restrict__ pn, int n_splits, int kp,
+__global__ void __launch_bounds__(MC_T) k_shortlist_merge_cta(const uint32_t* __restrict__ pk,
+                                                              const int32_t* __restrict__ pn, int n_splits, int kp, int rps,
                                                               float* __restrict__ cs, uint32_t* __restrict__ cr,
                                                               int32_t* __restrict__ cn) {
   extern __shared__ uint32_t s_key[];  // [2][n_splits * kp]
@@ -940,7 +968,7 @@ __global__ void __launch_bounds__(MC_T) k_shortlist_merge_cta(const float* __res
     uint32_t k = 0u;
     if (i < total) {
       const int sp = i / kp, j = i - sp * kp;
-      if (j < pn[(size_t)q * n_splits + sp]) k = fkey(ps[base + i]);
+      if (j < pn[(size_t)q * n_splits + sp]) k = pk[base + i];  // never 0 (see hkey_ru)
     }
     int pre;
     const int tot = block_scan(k != 0u, red, &pre);
@@ -970,10 +998,7 @@ __global__ void __launch_bounds__(MC_T) k_shortlist_merge_cta(const float* __res
       const bool take = i < n_items && (pass == 0 ? key[i] > T : key[i] == T);
       int pre;
       const int tot = block_scan(take, red, &pre);
-      if (take && out + pre < kp) {
-        cs[(size_t)q * kp + out + pre] = ps[base + slot[i]];
-        cr[(size_t)q * kp + out + pre] = pr[base + slot[i]];
-      }
+      if (take && out + pre < kp) emit(key[i], slot[i], kp, rps, cs, cr, (size_t)q * kp + out + pre);
       out += tot;
     }
   if (threadIdx.x == 0) cn[q] = min(kp, out);
@@ -1055,7 +1080,7 @@ static void launch_pair(lc_ctx* ctx, const ApproxPlan& plan, const CUtensorMap& 
   const int nkb = prm.dim / BK;
   const int KS = nkb > 8 ? nkb - 8 : 0;
   const size_t budget = 227 * 1024 - 1024 - 512;
-  const size_t slot_bytes = (size_t)BM * 8;
+  const size_t slot_bytes = (size_t)BM * 4;  // one packed u32 per candidate
   const size_t fixed = (size_t)KS * ABOX;
   // candidate buffer: kp + 32 slots minimum (compactions stay rare once the
   // shared threshold is warm); the rest of smem goes to the table ring
@@ -1072,7 +1097,9 @@ static void launch_pair(lc_ctx* ctx, const ApproxPlan& plan, const CUtensorMap& 
   if (const char* e = getenv("FC_SHORTLIST_NSTAGE")) nstage = std::min<int64_t>(nstage, atoi(e));
   if (nstage < 2) raise(LC_ERR_INVALID_ARGUMENT, "lookup: shortlist too long for shared memory");
   prm.nstage = (int)nstage;
-  prm.cap = (int)std::min<int64_t>((budget - fixed - nstage * stage_bytes) / slot_bytes, prm.kp + 96);
+  int64_t cap_max = prm.kp + 96;
+  if (const char* e = getenv("FC_SHORTLIST_CAPMAX")) cap_max = std::max<int64_t>(min_cap, atoi(e));
+  prm.cap = (int)std::min<int64_t>((budget - fixed - nstage * stage_bytes) / slot_bytes, cap_max);
   const size_t smem = 1024 + 512 + nstage * stage_bytes + fixed + (size_t)prm.cap * slot_bytes;
   FC_CUDA(cudaFuncSetAttribute(k_shortlist_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = 2 * std::min(prm.n_units, ctx->sm_count / 2);
@@ -1108,7 +1135,9 @@ void approx_shortlist(lc_ctx* ctx, const ApproxPlan& plan, const float* Qdev, in
   splits = std::min<int64_t>(splits, std::max<int64_t>(1, total_tiles / 16));
   // keep one query's partial lists within the merge's shared memory (few queries)
   splits = std::min<int64_t>(splits, std::max<int64_t>(workers, (200 * 1024) / ((int64_t)kp * 8)));
-  const int64_t tiles_per_split = (total_tiles + splits - 1) / splits;
+  // packed candidates carry the row offset in 16 bits
+  splits = std::max<int64_t>(splits, (total_tiles * bn + 65535) / 65536);
+  const int64_t tiles_per_split = std::min<int64_t>((total_tiles + splits - 1) / splits, 65536 / bn);
   splits = (total_tiles + tiles_per_split - 1) / tiles_per_split;
   Params prm;
   prm.Qb = qb.as<__nv_bfloat16>();
@@ -1124,13 +1153,12 @@ void approx_shortlist(lc_ctx* ctx, const ApproxPlan& plan, const float* Qdev, in
     const char* dbg = getenv("FC_SHORTLIST_DEBUG");
     prm.debug = dbg ? atoi(dbg) : 0;
   }
-  DevBuf ps((size_t)nq * splits * kp * sizeof(float), ctx->stream);
-  DevBuf pr((size_t)nq * splits * kp * sizeof(uint32_t), ctx->stream);
+  DevBuf pk((size_t)nq * splits * kp * sizeof(uint32_t), ctx->stream);
   DevBuf pn((size_t)nq * splits * sizeof(int32_t), ctx->stream);
   DevBuf gk((size_t)nq_pad * sizeof(uint32_t), ctx->stream);
   FC_CUDA(cudaMemsetAsync(gk.p, 0, gk.bytes, ctx->stream));
-  DevBuf st(16, ctx->stream);
-  FC_CUDA(cudaMemsetAsync(st.p, 0, 16, ctx->stream));
+  DevBuf st(64, ctx->stream);  // u32 [0,4): counters; u64 [2,6): epilogue cycle spans
+  FC_CUDA(cudaMemsetAsync(st.p, 0, 64, ctx->stream));
   DevBuf hist(pair ? (size_t)nq_pad * HSTRIDE * sizeof(uint32_t) : 16, ctx->stream);
   if (pair) FC_CUDA(cudaMemsetAsync(hist.p, 0, hist.bytes, ctx->stream));
   prm.hist = hist.as<uint32_t>();
@@ -1140,8 +1168,7 @@ void approx_shortlist(lc_ctx* ctx, const ApproxPlan& plan, const float* Qdev, in
   }
   prm.stats = st.as<uint32_t>();
   prm.gkey = gk.as<uint32_t>();
-  prm.part_s = ps.as<float>();
-  prm.part_r = pr.as<uint32_t>();
+  prm.part_k = pk.as<uint32_t>();
   prm.part_n = pn.as<int32_t>();
   if (pair) {
     alignas(64) CUtensorMap tmQ;
@@ -1153,12 +1180,16 @@ void approx_shortlist(lc_ctx* ctx, const ApproxPlan& plan, const float* Qdev, in
     launch_single<128>(ctx, plan, prm);
   }
   if (prm.debug & 16) {
-    uint32_t h[4];
-    FC_CUDA(cudaMemcpyAsync(h, st.p, 16, cudaMemcpyDeviceToHost, ctx->stream));
+    uint32_t h[16];
+    FC_CUDA(cudaMemcpyAsync(h, st.p, 64, cudaMemcpyDeviceToHost, ctx->stream));
     sync(ctx);
-    fprintf(stderr, "shortlist stats: warp-tiles %u slow-chunks %u (%.3f/tile) compactions %u (%.4f/tile) nstage %d bps %d cap %d splits %d\n",
-            h[2], h[0], h[0] / (double)std::max(1u, h[2]), h[1], h[1] / (double)std::max(1u, h[2]), prm.nstage, prm.bps,
-            prm.cap, prm.n_splits);
+    unsigned long long cy[4];
+    memcpy(cy, h + 4, sizeof cy);
+    const double wt = (double)std::max(1u, h[2]);  // warp-tiles
+    fprintf(stderr, "shortlist stats: warp-tiles %u slow-chunks %u (%.3f/tile) compactions %u (%.4f/tile) nstage %d bps %d cap %d splits %d"
+            " | cycles per warp-tile: acc-wait %.0f hist %.0f compact %.0f append %.0f\n",
+            h[2], h[0], h[0] / wt, h[1], h[1] / wt, prm.nstage, prm.bps, prm.cap, prm.n_splits, cy[0] / wt, cy[1] / wt,
+            cy[2] / wt, cy[3] / wt);
   }
   const size_t per_warp = (size_t)splits * kp * 2 * sizeof(uint32_t);  // keys + slots
   KTimer kmt(ctx, "shortlist_merge");
@@ -1168,8 +1199,8 @@ void approx_shortlist(lc_ctx* ctx, const ApproxPlan& plan, const float* Qdev, in
       FC_CUDA(cudaFuncSetAttribute(k_shortlist_merge_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
       attr_set.fetch_or(1ull << (ctx->device & 63));
     }
-    k_shortlist_merge_cta<<<nq, MC_T, per_warp, ctx->stream>>>(ps.as<float>(), pr.as<uint32_t>(), pn.as<int32_t>(),
-                                                               (int)splits, kp, cand_s, cand_r, cand_n);
+    k_shortlist_merge_cta<<<nq, MC_T, per_warp, ctx->stream>>>(pk.as<uint32_t>(), pn.as<int32_t>(), (int)splits, kp,
+                                                               prm.rows_per_split, cand_s, cand_r, cand_n);
     FC_LAUNCH_CHECK();
     count_launch(ctx, 3);
     return;
@@ -1184,7 +1215,7 @@ void approx_shortlist(lc_ctx* ctx, const ApproxPlan& plan, const float* Qdev, in
     attr_set2.fetch_or(1ull << (ctx->device & 63));
   }
   k_shortlist_merge<<<(nq + MG_W - 1) / MG_W, MG_W * 32, msmem, ctx->stream>>>(
-      ps.as<float>(), pr.as<uint32_t>(), pn.as<int32_t>(), (int)splits, kp, nq, cand_s, cand_r, cand_n,
+      pk.as<uint32_t>(), pn.as<int32_t>(), (int)splits, kp, prm.rows_per_split, nq, cand_s, cand_r, cand_n,
       gkeys.as<uint32_t>());
   FC_LAUNCH_CHECK();
   count_launch(ctx, 3);

@@ -705,6 +705,77 @@ struct lc_store {
 
     lc_step_entry next() { return evict_slot(pick(nullptr, nullptr)); }
 
+    // The next (up to) m victims evict_one(now) would take, with their keys and
+    // used() after each removal, WITHOUT evicting: the walk of pick() /
+    // evict_slot() replayed on overlays (removed slots, per-prompt removed
+    // counts, re-keyed siblings). It stops at m or earlier where the real walk
+    // would re-score the table (scored head exhausted); *more = live steps
+    // remain beyond the list. A shard's
+    // sequence depends only on its own records, so the global eviction of an
+    // entry-sharded store is the (key, seq) merge of these per-shard lists.
+    int peek(int m, lc_step_entry* out, double* keys, uint64_t* used_after, bool* more) {
+      *more = false;
+      if (s->prompts.empty() || m <= 0) return 0;
+      pick(nullptr, nullptr);  // a scored head exists (may re-score)
+      size_t p = pos;
+      std::unordered_map<int64_t, double> rk(rekeyed);
+      auto hp = heap;
+      std::unordered_set<int64_t> removed;
+      std::unordered_map<uint64_t, size_t> gone;  // prompt -> live steps removed so far
+      uint64_t u = s->used;
+      int n = 0;
+      auto live = [&](int64_t slot) { return s->slot_prompt.count(slot) && !removed.count(slot); };
+      while (n < m) {
+        while (p < head.size() && (!live(head[p].slot) || rk.count(head[p].slot))) ++p;
+        while (!hp.empty()) {
+          const HE& t = hp.top();
+          auto it = rk.find(t.slot);
+          if (!live(t.slot) || it == rk.end() || it->second != t.key) hp.pop();
+          else break;
+        }
+        if (p >= head.size()) break;  // the real walk would re-score here
+        int64_t victim = head[p].slot;
+        double vkey = -head[p].s;
+        uint64_t vseq = head[p].id;
+        if (!hp.empty()) {
+          const HE& t = hp.top();
+          if (t.key < vkey || (t.key == vkey && t.seq < vseq)) {
+            victim = t.slot;
+            vkey = t.key;
+            vseq = t.seq;
+          }
+        }
+        const uint64_t pid = s->slot_prompt.at(victim);
+        const Rec& r = s->prompts.at(pid);
+        size_t& g = gone[pid];
+        const size_t nlive = r.live.size() - g;
+        const Live* lv = nullptr;
+        for (const Live& l : r.live)
+          if (l.slot == victim) lv = &l;
+        out[n] = lc_step_entry{pid, lv->step, 0, lv->f, lv->last, lv->inserted_at, lv->seq, lv->priv + r.shared / nlive};
+        keys[n] = vkey;
+        removed.insert(victim);
+        ++g;
+        u -= lv->priv;
+        if (nlive == 1) u -= r.shared;
+        used_after[n] = u;
+        ++n;
+        if (s->policy == LC_POLICY_LRBU && nlive > 1) {  // evict_slot's sibling re-key
+          for (const Live& l : r.live) {
+            if (removed.count(l.slot)) continue;
+            const uint64_t cap = l.priv + r.shared / (nlive - 1);
+            const double k = host_key(s->policy, l.f, l.step, l.last, l.seq, cap, now);
+            rk[l.slot] = k;
+            hp.push(HE{k, l.seq, l.slot});
+          }
+        }
+      }
+      // the shard's sequence continues past this list (cut at m, or at a
+      // re-score point) while live steps remain unlisted
+      *more = (int64_t)removed.size() < s->live_count;
+      return n;
+    }
+
     // the StepEntry evict_slot(slot) would return, without evicting
     lc_step_entry describe(int64_t slot) const {
       const auto it = s->prompts.find(s->slot_prompt.at(slot));
@@ -767,12 +838,14 @@ lc_status lc_store_destroy(lc_store* s) {
   LC_API_END
 }
 
-lc_status lc_store_insert(lc_store* s, uint64_t prompt, lc_entry* entry, const int32_t* steps, int n_steps, uint64_t now,
-                          lc_step_entry* evicted, int cap, int* n_evicted) {
-  LC_API_BEGIN
-  FC_REQUIRE(s && entry, "null argument");
-  DeviceGuard g(s->ctx->device);
-  if (n_evicted) *n_evicted = 0;
+}  // extern "C"
+
+namespace {
+// insert_steps validation (store.cpp:53-76) up to, not including, the
+// OversizedEntry check: the records kept (entry->sel indices of the requested
+// steps) and the entry's standalone size (shared + their private bytes).
+std::vector<int> check_insert(lc_store* s, uint64_t prompt, lc_entry* entry, const int32_t* steps, int n_steps,
+                              uint64_t* standalone) {
   for (int i = 0; i < n_steps; ++i)
     if (steps[i] < 1 || steps[i] > 50) raise(LC_ERR_INVALID_ARGUMENT, "StepId: value out of range 1..50");
   if (n_steps <= 0) raise(LC_ERR_INVALID_ARGUMENT, "insert_steps: empty step list");
@@ -794,11 +867,35 @@ lc_status lc_store_insert(lc_store* s, uint64_t prompt, lc_entry* entry, const i
   std::vector<int> sel;
   for (int k : entry->sel)
     if (std::find(steps, steps + n_steps, d.steps[k]) != steps + n_steps) sel.push_back(k);
+  uint64_t sz = d.shared_bytes();
+  for (int k : sel) sz += d.private_bytes(k);
+  *standalone = sz;
+  return sel;
+}
+}  // namespace
+
+extern "C" {
+
+lc_status lc_store_check_insert(lc_store* s, uint64_t prompt, lc_entry* entry, const int32_t* steps, int n_steps,
+                                uint64_t* standalone) {
+  LC_API_BEGIN
+  FC_REQUIRE(s && entry && standalone, "null argument");
+  check_insert(s, prompt, entry, steps, n_steps, standalone);
+  LC_API_END
+}
+
+lc_status lc_store_insert(lc_store* s, uint64_t prompt, lc_entry* entry, const int32_t* steps, int n_steps, uint64_t now,
+                          lc_step_entry* evicted, int cap, int* n_evicted) {
+  LC_API_BEGIN
+  FC_REQUIRE(s && entry, "null argument");
+  DeviceGuard g(s->ctx->device);
+  if (n_evicted) *n_evicted = 0;
+  uint64_t standalone = 0;
+  const std::vector<int> sel = check_insert(s, prompt, entry, steps, n_steps, &standalone);
+  const EntryData& d = *entry->d;
   lc_store::Rec rec;
   rec.view = make_entry_view(entry->d, sel);
   rec.shared = d.shared_bytes();
-  uint64_t standalone = rec.shared;
-  for (int k : sel) standalone += d.private_bytes(k);
   if (standalone > s->capacity) {
     delete rec.view;
     set_last_oversize(standalone, s->capacity);
@@ -891,6 +988,20 @@ lc_status lc_store_peek(lc_store* s, uint64_t now, lc_step_entry* out, double* k
   const int64_t slot = ev.pick(&k, nullptr);
   if (out) *out = ev.describe(slot);
   if (key) *key = k;
+  LC_API_END
+}
+
+lc_status lc_store_peek_many(lc_store* s, uint64_t now, int m, lc_step_entry* out, double* keys, uint64_t* used_after,
+                             int* n_out, int* more) {
+  LC_API_BEGIN
+  FC_REQUIRE(s && out && keys && used_after && n_out, "null argument");
+  DeviceGuard g(s->ctx->device);
+  *n_out = 0;
+  if (more) *more = 0;
+  if (s->prompts.empty()) return LC_OK;
+  bool mo = false;
+  *n_out = s->evictor(now).peek(m, out, keys, used_after, &mo);
+  if (more) *more = mo ? 1 : 0;
   LC_API_END
 }
 
@@ -1029,6 +1140,12 @@ struct BR {  // ByteReader (serialize.hpp:54-106): truncation -> SnapshotError a
     return v;
   }
   const uint8_t* bytes(uint64_t k) { need(k); const uint8_t* r = p + pos; pos += k; return r; }
+  // k fp32 values: the reference reads them one at a time (f32_array), so a
+  // truncation is reported at the start of the first incomplete value
+  const uint8_t* f32s(uint64_t k) {
+    if (pos + 4 * k > n) raise_snap("truncated input", pos + 4 * ((n - pos) / 4));
+    return bytes(4 * k);
+  }
 };
 
 void check_status(lc_status st) {
@@ -1124,7 +1241,7 @@ lc_status lc_snapshot_load(lc_ctx* ctx, const char* path, lc_store** store_out, 
     const uint32_t count = r.u32();
     for (uint32_t i = 0; i < count; ++i) {
       tid[t].push_back(r.u64());
-      const uint8_t* v = r.bytes(4ull * dim);
+      const uint8_t* v = r.f32s((uint64_t)dim);
       const size_t at = trow[t].size();
       trow[t].resize(at + dim);
       if (dim) memcpy(trow[t].data() + at, v, 4ull * dim);

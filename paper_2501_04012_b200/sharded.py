@@ -21,7 +21,8 @@ from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["owner_of", "ShardedIndex", "ShardedStore", "pack_candidates", "unpack_candidates"]
+__all__ = ["owner_of", "ShardedIndex", "ShardedStore", "pack_candidates", "unpack_candidates", "attach_comm",
+           "comm_info", "CommShardedIndex", "CommShardedStore"]
 
 
 def owner_of(prompt_ids, world: int):
@@ -189,16 +190,23 @@ class ShardedStore:
         return int(prompt) % self.world
 
     # ---- collectives -----------------------------------------------------
+    @staticmethod
+    def _pack(row):
+        """u64 fields (prompt ids, seq, f, ...) travel as their int64 bit
+        images: values >= 2^63 wrap instead of raising on one rank (which would
+        leave the other ranks blocked in the collective)."""
+        return np.array([int(v) & 0xFFFFFFFFFFFFFFFF for v in row], dtype=np.uint64).view(np.int64)
+
     def _all_gather(self, row):
         torch, dist = self.torch, self.dist
-        t = torch.as_tensor(np.asarray(row, dtype=np.int64), device=self.device)
+        t = torch.as_tensor(self._pack(row), device=self.device)
         parts = [torch.empty_like(t) for _ in range(self.world)]
         dist.all_gather(parts, t, group=self.group)
         return torch.stack(parts).cpu().numpy()
 
     def _bcast(self, row, src):
         torch, dist = self.torch, self.dist
-        t = torch.as_tensor(np.asarray(row, dtype=np.int64), device=self.device).clone()
+        t = torch.as_tensor(self._pack(row), device=self.device).clone()
         dist.broadcast(t, src=dist.get_global_rank(self.group, src) if self.group is not None else src,
                        group=self.group)
         return t.cpu().numpy()
@@ -289,3 +297,190 @@ class ShardedStore:
             actual = int(res[1]) if res else 0
         actual = int(self._bcast([actual], own)[0])
         return actual, res
+
+
+# ---------------------------------------------------------------------------
+# C-ABI sharding (shard.cu): the communicator lives in the library context,
+# so C++ callers (include/lcache_b200/lcache.hpp) shard without Python. These
+# classes are thin handles over lc_sharded_*; torch.distributed only
+# bootstraps the communicator.
+# ---------------------------------------------------------------------------
+def attach_comm(ctx, group=None, transport: str | None = None):
+    """Give `ctx` the communicator of a torch.distributed group.
+
+    transport "nccl": an NCCL communicator created inside the library
+    (ncclCommInitRank; the unique id is broadcast from rank 0 over the group).
+    transport "host": every collective goes through `group`'s all_gather on
+    host tensors (gloo) via lc_ctx_comm_host — used where NCCL cannot run,
+    e.g. several ranks sharing one GPU in the tests.
+    Default: "nccl" when the group's backend is NCCL, else "host"."""
+    import ctypes as C
+    import torch
+    import torch.distributed as dist
+    from ._capi import ALLGATHER_FN, lib
+    from . import _check
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    if transport is None:
+        transport = "nccl" if dist.get_backend(group) == "nccl" else "host"
+    if transport == "nccl":
+        uid = (C.c_uint8 * 128)()
+        if rank == 0:
+            _check(lib.lc_comm_unique_id(uid))
+        obj = [bytes(uid)]
+        src = dist.get_global_rank(group, 0) if group is not None else 0
+        dist.broadcast_object_list(obj, src=src, group=group)
+        uid = (C.c_uint8 * 128).from_buffer_copy(obj[0])
+        _check(lib.lc_ctx_comm_init(ctx.h, world, rank, uid))
+        return ctx
+
+    def _gather(user, send, recv, nbytes):
+        try:
+            t = torch.frombuffer(bytearray(C.string_at(send, nbytes)), dtype=torch.uint8)
+            parts = [torch.empty(nbytes, dtype=torch.uint8) for _ in range(world)]
+            dist.all_gather(parts, t, group=group)
+            for r, p in enumerate(parts):
+                C.memmove(recv + r * nbytes, p.data_ptr(), nbytes)
+            return 0
+        except Exception:  # noqa: BLE001 — reported as LC_ERR_NCCL by the library
+            return 1
+
+    cb = ALLGATHER_FN(_gather)
+    ctx._comm_cb = cb  # the library holds the raw pointer: keep the thunk alive
+    _check(lib.lc_ctx_comm_host(ctx.h, world, rank, cb, None))
+    return ctx
+
+
+def comm_info(ctx):
+    """(nranks, rank, backend 0 none / 1 nccl / 2 host, collectives issued)."""
+    import ctypes as C
+    from ._capi import lib
+    from . import _check
+    n, r, b, c = C.c_int(), C.c_int(), C.c_int(), C.c_uint64()
+    _check(lib.lc_ctx_comm_info(ctx.h, C.byref(n), C.byref(r), C.byref(b), C.byref(c)))
+    return n.value, r.value, b.value, c.value
+
+
+class CommShardedIndex:
+    """This rank's shard of the index, queried collectively through
+    lc_sharded_query_topk / lc_sharded_lookup_decide (one grouped all-gather
+    per batch inside the library)."""
+
+    def __init__(self, index, dim: int):
+        self.index, self.dim = index, dim
+        self.ctx = index.ctx
+        self.world, self.rank = comm_info(self.ctx)[:2]
+
+    def mine(self, prompt_ids):
+        return owner_of(prompt_ids, self.world) == np.uint64(self.rank)
+
+    def insert_batch(self, prompt_ids, whole, obj, background):
+        sel = np.nonzero(self.mine(prompt_ids))[0]
+        if len(sel):
+            self.index.insert_batch(np.asarray(prompt_ids, dtype=np.uint64)[sel], whole[sel], obj[sel], background[sel])
+        return len(sel)
+
+    def query_topk(self, kind, q, k, out=None):
+        from . import _check, _host, _is_dev, _ptr
+        from ._capi import lib
+        q = _host(q, np.float32)
+        n = q.shape[0]
+        if out is None:
+            if _is_dev(q):
+                import torch
+                out = (torch.empty((n, k), dtype=torch.int64, device=q.device),
+                       torch.empty((n, k), dtype=torch.float64, device=q.device),
+                       torch.empty((n,), dtype=torch.int32, device=q.device))
+            else:
+                out = (np.zeros((n, k), np.uint64), np.zeros((n, k), np.float64), np.zeros(n, np.int32))
+        _check(lib.lc_sharded_query_topk(self.index.h, int(kind), _ptr(q), n, self.dim, k, _ptr(out[0]),
+                                         _ptr(out[1]), _ptr(out[2])))
+        return out
+
+    def lookup_decide(self, qw, qo, qb, hit_threshold=0.65, edges=(0.72, 0.79, 0.86, 0.93)):
+        from . import _check, _host, _ptr
+        from ._capi import Decision, lib
+        qs = [_host(x, np.float32) for x in (qw, qo, qb)]
+        n = qs[0].shape[0]
+        out = (Decision * n)()
+        e = np.asarray(edges, np.float64)
+        _check(lib.lc_sharded_lookup_decide(self.index.h, _ptr(qs[0]), _ptr(qs[1]), _ptr(qs[2]), n, self.dim,
+                                            hit_threshold, _ptr(e), out))
+        return list(out)
+
+
+class CommShardedStore:
+    """CacheStore under one global budget across ranks (lc_sharded_store_*):
+    the same StepEntry sequence, used() and next_seq as one unsharded store.
+    Every method is collective; insert_steps takes the entry on the owner
+    rank (prompt mod G) and None elsewhere."""
+
+    def __init__(self, capacity: int, policy, ctx, batch: int = 0):
+        import ctypes as C
+        from . import CacheStore, _check
+        from ._capi import lib
+        self.ctx = ctx
+        h = C.c_void_p()
+        _check(lib.lc_sharded_store_create(ctx.h, capacity, int(policy), batch, C.byref(h)))
+        self.h = h
+        self.world, self.rank = comm_info(ctx)[:2]
+        loc = CacheStore.__new__(CacheStore)
+        loc.ctx, loc.h, loc._cb, loc._borrowed = ctx, C.c_void_p(lib.lc_sharded_store_local(h)), None, True
+        self.local = loc
+
+    def __del__(self):
+        try:
+            from ._capi import lib
+            from . import _alive
+            if self.h and _alive(self.ctx):
+                lib.lc_sharded_store_destroy(self.h)
+                self.h = None
+        except Exception:  # noqa: BLE001
+            pass
+
+    def owner(self, prompt) -> int:
+        return int(prompt) % self.world
+
+    def insert_steps(self, prompt, entry, steps, now):
+        import ctypes as C
+        from . import _check, _ptr
+        from ._capi import StepEntry, lib
+        st_ = np.ascontiguousarray(steps, np.int32)
+        cap = 4096
+        ev = (StepEntry * cap)()
+        n = C.c_int()
+        _check(lib.lc_sharded_store_insert(self.h, int(prompt), entry.h if entry is not None else None, _ptr(st_),
+                                           st_.size, now, ev, cap, C.byref(n)))
+        return [tuple(int(v) for v in ev[i].as_tuple()) for i in range(min(n.value, cap))]
+
+    def evict_one(self, now):
+        from . import _check
+        from ._capi import StepEntry, lib
+        import ctypes as C
+        e = StepEntry()
+        _check(lib.lc_sharded_store_evict_one(self.h, now, C.byref(e)))
+        return tuple(int(v) for v in e.as_tuple())
+
+    def get_step(self, prompt, desired, now, out=None):
+        import ctypes as C
+        from . import _check, _ptr
+        from ._capi import lib
+        a = C.c_int32()
+        _check(lib.lc_sharded_store_get_step(self.h, int(prompt), desired, now, C.byref(a),
+                                             _ptr(out) if out is not None else None))
+        return a.value
+
+    def used(self) -> int:
+        import ctypes as C
+        from . import _check
+        from ._capi import lib
+        u = C.c_uint64()
+        _check(lib.lc_sharded_store_used(self.h, C.byref(u)))
+        return u.value
+
+    def stats(self):
+        import ctypes as C
+        from . import _check
+        from ._capi import lib
+        r, e, s = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        _check(lib.lc_sharded_store_stats(self.h, C.byref(r), C.byref(e), C.byref(s)))
+        return {"rounds": r.value, "local_evictions": e.value, "next_seq": s.value}

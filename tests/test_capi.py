@@ -87,3 +87,13 @@ def test_cpp_host_api_known_answers():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert " 0 failed" in r.stdout
+
+
+@pytest.mark.gpu
+def test_cpp_sharded_host_api_two_ranks():
+    """lcache.hpp ShardedSimilarityIndex / ShardedCacheStore: two ranks (threads,
+    one GPU, in-process all-gather transport) equal an unsharded index/store."""
+    exe = [e for e in _cpp_exes() if e.endswith("sharded_kat")][0]
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert " 0 failed" in r.stdout

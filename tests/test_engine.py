@@ -190,3 +190,25 @@ def test_random_trace_vs_restatement(fc, orc, synth, policy, cap_prompts, batch)
     assert m["whole_hits"] + m["decoupled_hits"] > 0 and m["misses"] > 0
     assert eng.store.used() == oe.st.used()
     assert [list(e.as_tuple()) for e in eng.store.entries_snapshot()] == [list(e) for e in oe.st.entries()]
+
+
+@pytest.mark.gpu
+def test_deferred_update_compress_error_leaves_no_index_orphan(fc, orc, synth):
+    """A batch whose deferred (non-evicting) update cannot be compressed (a
+    non-finite latent: Frame ctor, core.cpp:19-25) raises, and the prompts of
+    that flush are neither in the store nor left behind in the index (a later
+    lookup would otherwise hit a prompt with no data)."""
+    world = World(orc, synth)
+    eng = _product(fc, 1 << 40, 3)  # roomy budget: every update is deferred
+    reqs = [(world.prompt(i, i % 5), 10 * (i + 1), i, i % 5) for i in range(4)]
+    arr = world.arrays(reqs)
+    arr[3][2, 1, 0, 5] = np.nan  # request 2's step-10 latent
+    with pytest.raises(fc.InvalidArgument):
+        eng.process([r[0] for r in reqs], [r[1] for r in reqs], *arr)
+    ix, st = eng.index, eng.store
+    for p, *_ in reqs:
+        assert ix.contains(p) == st.contains(p), p
+    # the engine keeps working after the failure
+    reqs2 = [(world.prompt(5, 1), 100, 5, 1)]
+    out = eng.process([r[0] for r in reqs2], [r[1] for r in reqs2], *world.arrays(reqs2))
+    assert out[0]["kind"] == "miss" and st.contains(world.prompt(5, 1)) and ix.contains(world.prompt(5, 1))

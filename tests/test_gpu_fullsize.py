@@ -1,5 +1,10 @@
 """Parity at BASELINE.json's full sizes (GPU), through checks that do not need
 the CPU oracle to redo the whole workload:
+  * config[1] lookup against the reference ITSELF: the SURVEY 8(d) table
+    (1M x 768, 5 % exact duplicate rows) and query batch (50 % fresh, 50 %
+    perturbed stored rows) that bench.py times; 64 queries of the 4096-query
+    batch are compared with the unmodified reference query_top1 (oracle/_ref,
+    vindex.cpp:50-74, all host cores) and with the restatement's top-8;
   * config[1] lookup (1M x 768, top-8): the certified tensor-core path equals
     the independent sequential-fp64 exact scan (mode 1) on a query sample, and
     ids / scores are ordered by (score desc, id asc);
@@ -14,6 +19,69 @@ import numpy as np
 import pytest
 
 pytestmark = pytest.mark.gpu
+
+
+def _bench_module():
+    import importlib.util
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("_fc_bench", os.path.join(root, "bench.py"))
+    m = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(m)
+    return m
+
+
+def test_lookup_1m_config1_equals_reference(fc, orc, ref):
+    import concurrent.futures as cf
+    import torch
+    bench = _bench_module()
+    dev = torch.device("cuda", 0)
+    ctx = fc.default_context()
+    n, d, B, k, nq = 1_000_000, 768, 4096, 8, 64
+    tab = bench.make_table(torch, fc, ctx, n, d, 2, dev)
+    q = bench.make_queries(torch, fc, ctx, tab, B, 1000, dev)
+    ids = np.arange(n, dtype=np.uint64)
+    ix = fc.SimilarityIndex(ctx=ctx)
+    ix.insert_batch(ids, tab, tab, tab)
+    ix.set_lookup(0, 32)  # the bench's default path (tensor cores at this size)
+    gi, gs, gc = (x.cpu().numpy() for x in ix.query_topk(fc.EmbeddingKind.Whole, q, k))
+    st = ix.stats()
+    assert st.certified + st.fallback == B
+    tab_h = tab.cpu().numpy()
+    del tab
+    q_h = q.cpu().numpy()
+    # sample: 32 perturbed-row queries (hits) and 32 fresh ones (misses)
+    top = gs[:, 0]
+    hits = np.nonzero(top >= 0.65)[0][:nq // 2]
+    miss = np.nonzero(top < 0.65)[0][:nq - hits.size]
+    sel = np.sort(np.concatenate([hits, miss]))
+    assert sel.size == nq and hits.size == nq // 2
+    qs = np.ascontiguousarray(q_h[sel])
+    nth = os.cpu_count() or 1
+    # restatement top-8, queries split over host threads (ctypes drops the GIL)
+    parts = np.array_split(np.arange(nq), min(nth, nq))
+    with cf.ThreadPoolExecutor(len(parts)) as ex:
+        res = list(ex.map(lambda p: orc.topk_flat(tab_h, ids, qs[p], k), parts))
+    oi = np.concatenate([r[0] for r in res])
+    os_ = np.concatenate([r[1] for r in res])
+    oc = np.concatenate([r[2] for r in res])
+    assert (oc == gc[sel]).all()
+    assert (oi == gi[sel].view(np.uint64)).all()
+    assert (os_.view(np.uint64) == gs[sel].view(np.uint64)).all()
+    # the unmodified reference: insert the 1M rows (ascending ids append), query_top1
+    rix = ref.index(d)
+    fn = getattr(ref.lib, ref.pfx + "index_insert")
+    import ctypes as C
+    base, rowb = tab_h.ctypes.data, d * 4
+    for i in range(n):
+        p = C.c_void_p(base + i * rowb)
+        assert fn(rix.h, i, p, p, p, d) == 0
+    rid, rsc, rfd = rix.query_top1(0, qs, nthreads=nth)
+    assert (rfd == 1).all()
+    assert (rid == gi[sel, 0].view(np.uint64)).all()
+    assert (rsc.view(np.uint64) == gs[sel, 0].view(np.uint64)).all()
+    # the sample covers exact-duplicate ties somewhere in the batch
+    dup_tie = (gs[:, :-1] == gs[:, 1:]).any()
+    assert dup_tie
 
 
 def test_lookup_1m_tensor_path_equals_exact_scan(fc):

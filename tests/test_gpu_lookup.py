@@ -285,3 +285,59 @@ def test_duplicate_heavy_table_merge_paths(fc, orc, nq):
     oi, os_, oc = orc.topk_flat(tab, ids, q, 8)
     assert (gc == oc).all()
     assert (u64(gi) == oi).all() and (bits(gs) == bits(os_)).all()
+
+
+def _cluster_case(orc, seed, n=20000, dim=256, nq=6, spread=0.01):
+    rng = np.random.default_rng(seed)
+    base = rng.standard_normal((n, dim)).astype(np.float32)
+    q = rng.standard_normal((nq, dim)).astype(np.float32)
+    for j in range(nq):  # 100 near-copies of each query: near-tied top-8s
+        for c in range(100):
+            base[j * 100 + c] = q[j] + spread * rng.standard_normal(dim).astype(np.float32)
+    return orc.normalize_rows(base), orc.normalize_rows(q)
+
+
+@pytest.mark.parametrize("scale", [8.0, 100.0, 0.125])
+def test_non_unit_queries_stay_exact(fc, orc, scale):
+    """The C-ABI takes raw floats, so a caller can pass queries that are not
+    unit (the reference cannot: queries are Embeddings, core.cpp:50-69). The
+    certified bound scales with ||q|| (k_rescore), so a query of norm 8 or 100
+    near a cluster of near-ties must still return the exact top-8 of the
+    sequential fp64 dot (vindex.cpp:66-67), bit for bit."""
+    tab, qn = _cluster_case(orc, 91, spread=0.03)
+    ids = np.arange(tab.shape[0], dtype=np.uint64) * 5 + 1
+    q = (qn * np.float32(scale)).astype(np.float32)
+    ix = build_index(fc, [tab, tab, tab], ids, mode=2, kprime=32)
+    gi, gs, gc = ix.query_topk(fc.EmbeddingKind.Whole, q, 8)
+    oi, os_, oc = orc.topk_flat(tab, ids, q, 8)
+    assert (u64(gi) == oi).all() and (bits(gs) == bits(os_)).all() and (gc == oc).all()
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+def test_non_finite_query_rejected(fc, synth, mode):
+    tabs, ids, q = _random_case(synth, 9000, 256, 40, 13)
+    ix = build_index(fc, tabs, ids, mode=mode)
+    q = q.copy()
+    q[17, 3] = np.nan
+    with pytest.raises(fc.InvalidArgument):
+        ix.query_topk(fc.EmbeddingKind.Whole, q, 8)
+    q[17, 3] = np.inf
+    with pytest.raises(fc.InvalidArgument):
+        ix.query_topk(fc.EmbeddingKind.Whole, q, 8)
+    q[17, 3] = 0.0
+    ix.query_topk(fc.EmbeddingKind.Whole, q, 8)  # finite again: accepted
+
+
+def test_eps_below_proven_bound_is_clamped(fc, orc):
+    """lc_index_set_lookup cannot make the certificate unsound: an eps below
+    2^-8 + 2^-12 is raised to it, so near-tied clusters (which the bf16
+    shortlist cannot certify) still end bit-exact."""
+    tab, qn = _cluster_case(orc, 41)
+    ids = np.arange(tab.shape[0], dtype=np.uint64) * 7 + 3
+    ix = build_index(fc, [tab, tab, tab], ids, mode=2, kprime=32)
+    ix.set_lookup(2, 32, 1e-12)
+    ix.stats(reset=True)
+    gi, gs, gc = ix.query_topk(fc.EmbeddingKind.Whole, qn, 8)
+    oi, os_, oc = orc.topk_flat(tab, ids, qn, 8)
+    assert (u64(gi) == oi).all() and (bits(gs) == bits(os_)).all() and (gc == oc).all()
+    assert ix.stats().fallback == qn.shape[0]

@@ -167,3 +167,40 @@ def test_snapshot_record_level_errors(fc, ref, synth, tmp_path):
             assert e1.code == e2.code, (name, e1, e2)
             if e1.code == 5:
                 assert e1.byte_offset == ref.last_snapshot_offset(), (name, e1, e2)
+
+
+def test_entry_truncation_offsets_match_reference(fc, ref, synth):
+    """deserialize_entry (codec.cpp:394-473) of every prefix of a few entries:
+    the same error type and SnapshotError byte offset as the reference, whose
+    ByteReader reads frames / alphas / diffs one float at a time and masks one
+    bitmap at a time (serialize.hpp:86-105) — a cut inside a frame reports the
+    start of the first incomplete float, not the start of the frame."""
+    ents = _tiny(fc, synth, 3, 5)
+    n_checked = 0
+    for pid, (_, wire) in ents.items():
+        for cut in range(len(wire)):
+            b = wire[:cut]
+            e1 = _err(lambda: fc.deserialize_entry(b))
+            e2 = _err(lambda: ref.entry_info(b))
+            assert e1 is not None and e2 is not None, (pid, cut)
+            assert e1.code == e2.code, (pid, cut, e1, e2)
+            if e1.code == 5:
+                assert e1.byte_offset == ref.last_snapshot_offset(), (pid, cut, e1, e2)
+                n_checked += 1
+    assert n_checked > 100
+
+
+def test_snapshot_truncation_inside_index_row(fc, ref, synth, tmp_path):
+    st, rst, ix, rix, _ = _build_pair(fc, ref, synth, 1, n=8, seed=9)
+    good = tmp_path / "good.flxc"
+    ref.snapshot_save(rst, rix, good)
+    raw = good.read_bytes()
+    hdr = 4 + 2 + 1 + 8 + 8 + 2
+    row0 = hdr + 4 + 8  # first fp32 of the first whole-table row
+    for cut in (row0 + 1, row0 + 10, row0 + 4 * DIM - 1, row0 + 4 * DIM + 8 + 6):
+        path = tmp_path / f"t{cut}.flxc"
+        path.write_bytes(raw[:cut])
+        e1 = _err(lambda: fc.load_snapshot(path))
+        e2 = _err(lambda: ref.snapshot_load(path))
+        assert e1.code == e2.code == 5
+        assert e1.byte_offset == ref.last_snapshot_offset(), (cut, e1, e2)

@@ -176,7 +176,7 @@ class _OrcLocal:
         self.s.set_next_seq(seq)
 
 
-def _store_trace(orc, synth, seed, n_prompts=40, n_ops=400):
+def _store_trace(orc, synth, seed, n_prompts=40, n_ops=400, id_base=100):
     """Entries (bytes) and a random op list shared by every rank."""
     dims = (4, 4, 2)
     rng = np.random.default_rng(seed)
@@ -185,7 +185,7 @@ def _store_trace(orc, synth, seed, n_prompts=40, n_ops=400):
         r = tuple(float(x) for x in rng.uniform(0, 1, 5))
         lat = synth.latents(seed * 1000 + i, F=4, dims=dims, redundancy=r)
         om, bm = synth.rect_masks(4, 4, 4, i)
-        ents[100 + i] = orc.compress(lat, synth.CACHED_STEPS, om, bm, dims, 100 + i)
+        ents[id_base + i] = orc.compress(lat, synth.CACHED_STEPS, om, bm, dims, id_base + i)
     ops, now = [], 0
     keys = sorted(ents)
     for _ in range(n_ops):
@@ -203,7 +203,7 @@ def _store_trace(orc, synth, seed, n_prompts=40, n_ops=400):
     return ents, ops, sizes[len(sizes) // 2] * 8
 
 
-def _store_worker(rank, world, port, policy, seed, out_dir):
+def _store_worker(rank, world, port, policy, seed, out_dir, id_base=100):
     import sys
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
@@ -214,7 +214,7 @@ def _store_worker(rank, world, port, policy, seed, out_dir):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     orc = Checker("orc")
-    ents, ops, cap = _store_trace(orc, synth, seed)
+    ents, ops, cap = _store_trace(orc, synth, seed, id_base=id_base)
 
     def info(b):
         d = orc.entry_info(b)
@@ -261,12 +261,15 @@ def _store_worker(rank, world, port, policy, seed, out_dir):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("policy", [0, 1, 2, 3])
-def test_sharded_store_global_budget_matches_unsharded(tmp_path, policy):
+@pytest.mark.parametrize("policy,id_base", [(0, 100), (1, 100), (2, 100), (3, 100), (0, 2 ** 63 + 100),
+                                           (3, 2 ** 64 - 41)])
+def test_sharded_store_global_budget_matches_unsharded(tmp_path, policy, id_base):
+    """Includes prompt ids >= 2^63 (u64 in the reference, store.hpp:28): they
+    cross the collective as int64 bit images."""
     import pickle
     import torch.multiprocessing as mp
     world = 2
-    mp.spawn(_store_worker, args=(world, _free_port(), policy, 5 + policy, str(tmp_path)), nprocs=world,
+    mp.spawn(_store_worker, args=(world, _free_port(), policy, 5 + policy, str(tmp_path), id_base), nprocs=world,
              join=True)
     r0 = pickle.load(open(tmp_path / "s0.pkl", "rb"))
     r1 = pickle.load(open(tmp_path / "s1.pkl", "rb"))
