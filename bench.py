@@ -611,6 +611,31 @@ def bench_codec(torch, fc, ctx, args, dev, peaks):
         for s in steps:
             fc.decompress_batch(ents, [s] * n, out=out)
     dec_s = (time.perf_counter() - t0) / dec_reps
+    # fidelity of the served latents vs the raw ones (outside the timed region):
+    # the codec is lossy by design (non-key frames are served as their key
+    # frame, non-base steps as first + alpha * diff), bounded per frame by the
+    # key-frame threshold (select_keyframes, codec.cpp:138-165)
+    fid = {"max_abs": 0.0, "sq_err": 0.0, "sq_ref": 0.0, "cos_min": 1.0, "cos_sum": 0.0, "frames": 0,
+           "frames_ge_thr": 0}
+    for si, s_ in enumerate(steps):
+        fc.decompress_batch(ents, [s_] * n, out=out)
+        ref_ = lat[:, si]
+        d_ = (out - ref_).double()
+        fid["max_abs"] = max(fid["max_abs"], float(d_.abs().max()))
+        fid["sq_err"] += float((d_ * d_).sum())
+        rd = ref_.double()
+        od = out.double()
+        fid["sq_ref"] += float((rd * rd).sum())
+        cos = (od * rd).sum(-1) / (od.norm(dim=-1) * rd.norm(dim=-1))
+        fid["cos_min"] = min(fid["cos_min"], float(cos.min()))
+        fid["cos_sum"] += float(cos.sum())
+        fid["frames"] += cos.numel()
+        fid["frames_ge_thr"] += int((cos >= 0.99).sum())
+        del d_, rd, od, cos
+    fidelity = {"max_abs": fid["max_abs"], "rel_l2": (fid["sq_err"] / fid["sq_ref"]) ** 0.5,
+                "frame_cosine_min": fid["cos_min"], "frame_cosine_mean": fid["cos_sum"] / fid["frames"],
+                "frames_cosine_ge_0.99": fid["frames_ge_thr"] / fid["frames"],
+                "vs": "decompress_step (codec.cpp:263-301) of every step vs the raw input latents, fp64 metrics"}
     # algorithmic bytes: every output frame written once + the step's stored data read once
     infos = [e.info() for e in ents]
     read_b = 0
@@ -660,6 +685,7 @@ def bench_codec(torch, fc, ctx, args, dev, peaks):
                      "kernel": "k_decompress", "bytes_per_launch": int(dk_bytes),
                      "avg_launch_ms": round(dk_t / dk_n, 4) if dk_n else None},
         "decompress_stitch_GBps": (stitch_bytes / (t_.value / 1000) / 1e9) if t_.value else None,
+        "fidelity": fidelity,
     }
     return res
 

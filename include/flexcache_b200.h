@@ -171,11 +171,12 @@ typedef struct lc_lookup_stats {
 lc_status lc_index_stats(lc_index* ix, lc_lookup_stats* out, int reset);
 /* mode: 0 auto (tensor-core path when size >= 8192), 1 force exact scan,
  * 2 force tensor-core path. kprime: shortlist length (multiple of 32, <= 128).
- * eps: certified |bf16 - fp64| score bound for a unit query (<= 0 -> default
- * 2^-8 + 2^-12; values below that proven bound are clamped up to it). Each
- * query's bound is scaled by max(1, ||q||), so non-unit queries stay exact;
- * queries with a non-finite element fail with LC_ERR_INVALID_ARGUMENT
- * (reference queries are Embeddings, core.cpp:11-15). */
+ * eps: floor on the certified |bf16 - fp64| score bound (<= 0 -> none). The
+ * bound itself is proven per query from ||q||, the query's and the stored
+ * rows' bf16 rounding residuals (lookup.cuh), so results stay exact for any
+ * finite query, unit or not; eps can only widen it. Queries with a
+ * non-finite element fail with LC_ERR_INVALID_ARGUMENT (reference queries
+ * are Embeddings, core.cpp:11-15). */
 lc_status lc_index_set_lookup(lc_index* ix, int mode, int kprime, double eps);
 /* Shard merge for entry-sharded multi-GPU lookup (a23): merge G per-shard
  * exact top-k lists [G][n][k] (+counts [G][n]) into the global top-k

@@ -46,7 +46,11 @@ struct lc_index {
   std::unordered_map<uint64_t, int64_t> slot;
   int mode = 0;
   int kprime = 32;
-  double eps = kEpsBound;  // certified bound for a unit query; scaled by ||q|| per query (k_rescore)
+  // Certified |bf16 score - exact| bound, per query in k_rescore from
+  // ||q||, ||q - bf16(q)|| and dres = max over stored rows of ||x - bf16(x)||
+  // (lookup.cuh); eps_floor (lc_index_set_lookup) can only widen it.
+  double dres[3] = {0.0, 0.0, 0.0};
+  double eps_floor = 0.0;
   lc_lookup_stats stats{};
   ApproxPlan plan[3];
   mutable std::shared_mutex mu;  // readers: queries; writer: insert/remove (vindex.hpp:61)
@@ -71,18 +75,24 @@ __global__ void k_check_finite_rows(const float* __restrict__ v, int64_t n, int 
 
 // from_unit rule (core.cpp:61-69) on device rows: finite and
 // |sqrt(sum v^2) - 1| <= 1e-6 with a sequential fp64 sum.
-__global__ void k_check_unit(const float* __restrict__ v, int64_t n, int dim, int* __restrict__ bad) {
+// Also the row's bf16 rounding residual norm ||x - bf16_rn(x)|| (rounded
+// up), max-reduced into *res_bits (non-negative doubles order as u64).
+__global__ void k_check_unit(const float* __restrict__ v, int64_t n, int dim, int* __restrict__ bad,
+                             unsigned long long* __restrict__ res_bits) {
   int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (r >= n) return;
   const float* x = v + r * dim;
-  double sq = 0.0;
+  double sq = 0.0, rs = 0.0;
   bool ok = true;
   for (int i = 0; i < dim; ++i) {
     ok &= isfinite(x[i]);
     const double t = x[i];
     sq = fma(t, t, sq);
+    const double e = t - (double)__bfloat162float(__float2bfloat16_rn(x[i]));
+    rs = fma(e, e, rs);
   }
   if (!ok || fabs(sqrt(sq) - 1.0) > 1e-6) atomicExch(bad, 1);
+  else if (res_bits) atomicMax(res_bits, (unsigned long long)__double_as_longlong(sqrt(rs) * (1.0 + 0x1p-40)));
 }
 
 __global__ void k_to_bf16(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst, int64_t count) {
@@ -227,7 +237,8 @@ template <int PER_LANE>
 __global__ void __launch_bounds__(RS_WARPS * 32)
     k_rescore(const float* __restrict__ Q, int nq, int dim, const float* __restrict__ rows,
               const uint64_t* __restrict__ ids, const float* __restrict__ cand_s, const uint32_t* __restrict__ cand_r,
-              const int32_t* __restrict__ cand_n, int kp, int64_t n_rows, int k, double eps, uint64_t* __restrict__ out_ids,
+              const int32_t* __restrict__ cand_n, int kp, int64_t n_rows, int k, double dres, double eps_floor,
+              uint64_t* __restrict__ out_ids,
               double* __restrict__ out_sc, int32_t* __restrict__ out_cnt, int32_t* __restrict__ fail_list,
               int32_t* __restrict__ fail_n, unsigned long long* __restrict__ max_err_bits,
               int32_t* __restrict__ bad_query) {
@@ -237,29 +248,40 @@ __global__ void __launch_bounds__(RS_WARPS * 32)
   const float* qv = Q + (int64_t)q * dim;
   extern __shared__ float s_rq[];  // [RS_WARPS][dim] this warp's query
   float* sq = s_rq + (size_t)warp * dim;
-  double qsq = 0.0;
+  double qsq = 0.0, dsq = 0.0;
   bool qfin = true;
   for (int d = lane; d < dim; d += 32) {
     const float v = qv[d];
     sq[d] = v;
     qfin &= isfinite(v);
     qsq = fma((double)v, (double)v, qsq);
+    const double e = (double)v - (double)__bfloat162float(__float2bfloat16_rn(v));  // k_q_to_bf16 rounding
+    dsq = fma(e, e, dsq);
   }
   __syncwarp();
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) qsq += __shfl_xor_sync(0xffffffffu, qsq, off);
+  for (int off = 16; off > 0; off >>= 1) {
+    qsq += __shfl_xor_sync(0xffffffffu, qsq, off);
+    dsq += __shfl_xor_sync(0xffffffffu, dsq, off);
+  }
   qfin = __all_sync(0xffffffffu, qfin);
   if (!qfin && lane == 0) atomicExch(bad_query, 1);
-  // The error model (lookup.cuh) bounds |bf16 - exact| by eps * ||q|| * ||x||
-  // with ||x|| = 1 (rows pass the from_unit rule on insert). Queries through
-  // the C-ABI are not guaranteed unit, so the bound is scaled by ||q|| (the
-  // (1 + 2^-20) covers the rounding of the norm itself); queries of norm <= 1
-  // keep the unit bound (conservative). A query so large that fp32
-  // accumulation could overflow, or a non-finite one, is never certified.
-  const double qn = sqrt(qsq);
+  // Certified bound of |fp32 tensor-core score - exact dot| for this query
+  // against any stored row x (lookup.cuh): with q = bq + dq, x = bx + dx
+  // (bf16 round-to-nearest parts), q.x - bq.bx = q.dx + dq.x - dq.dx, so
+  //   |.| <= ||q|| dres + ||dq|| (||x|| + dres) + fp32 accumulation,
+  // ||x|| <= 1 + 1e-6 (from_unit rule on insert), dres = the max residual
+  // norm of the stored rows, and the accumulation of <= 1024 exact products
+  // adds <= 1024 * 2^-23 * ||bq|| ||bx||. The norms are fp64 warp sums
+  // (relative error far below the 2^-40 margin). Non-unit queries are
+  // covered by the same formula. A query so large that fp16-stored scores
+  // could overflow, or a non-finite one, is never certified.
+  const double qn = sqrt(qsq) * (1.0 + 0x1p-40), dqn = sqrt(dsq) * (1.0 + 0x1p-40);
   // (shortlist scores are stored as fp16: |score| <= ||q|| must stay far below 65504)
   const bool q_uncertifiable = !qfin || !(qn < 16384.0);
-  eps = eps * fmax(1.0, qn * (1.0 + 0x1p-20));
+  const double xn = 1.0 + 1e-6;
+  double eps = qn * dres + dqn * (xn + dres) + 0x1p-13 * (qn + dqn) * (xn + dres);
+  eps = fmax(eps * (1.0 + 0x1p-20), eps_floor * fmax(1.0, qn));
   const int cn = cand_n[q];
   // Only candidates whose bf16 score is within 2*eps of the k-th best bf16
   // score can reach the exact top-k: the k candidates ranked first by bf16
@@ -450,16 +472,21 @@ void ensure_capacity(lc_index* ix, int64_t need) {
   ix->cap = nc;
 }
 
-void check_units_device(lc_ctx* ctx, const float* dev, int64_t n, int dim) {
-  DevBuf bad(sizeof(int), ctx->stream);
-  FC_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), ctx->stream));
-  k_check_unit<<<grid_for(n, 128), 128, 0, ctx->stream>>>(dev, n, dim, bad.as<int>());
+// from_unit check of n rows; returns the max bf16 residual norm of the rows
+double check_units_device(lc_ctx* ctx, const float* dev, int64_t n, int dim) {
+  DevBuf bad(16, ctx->stream);
+  FC_CUDA(cudaMemsetAsync(bad.p, 0, 16, ctx->stream));
+  k_check_unit<<<grid_for(n, 128), 128, 0, ctx->stream>>>(dev, n, dim, bad.as<int>(),
+                                                          reinterpret_cast<unsigned long long*>(bad.as<char>() + 8));
   FC_LAUNCH_CHECK();
   count_launch(ctx);
-  int hb = 0;
-  FC_CUDA(cudaMemcpyAsync(&hb, bad.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  uint64_t hb[2] = {0, 0};
+  FC_CUDA(cudaMemcpyAsync(hb, bad.p, 16, cudaMemcpyDeviceToHost, ctx->stream));
   sync(ctx);
-  if (hb) raise(LC_ERR_INVALID_ARGUMENT, "Embedding: vector is not unit norm");
+  if ((uint32_t)hb[0]) raise(LC_ERR_INVALID_ARGUMENT, "Embedding: vector is not unit norm");
+  double r = 0.0;
+  memcpy(&r, &hb[1], 8);
+  return r;
 }
 
 // Exact top-k of queries (all, or the subset qlist) by full fp64 scan.
@@ -559,15 +586,15 @@ void query_dev(lc_index* ix, int kind, const float* Qdev, int nq, int k, uint64_
   KTimer kt(ctx, "rescore");
   if (kp <= 32)
     k_rescore<1><<<g, RS_WARPS * 32, rs_smem, ctx->stream>>>(Qdev, nq, ix->dim, ix->rows[kind], ix->ids_dev, cs.as<float>(),
-                                                       cr.as<uint32_t>(), cn.as<int32_t>(), kp, ix->n, k, ix->eps, oid, osc, ocnt,
+                                                       cr.as<uint32_t>(), cn.as<int32_t>(), kp, ix->n, k, ix->dres[kind], ix->eps_floor, oid, osc, ocnt,
                                                        fl.as<int32_t>(), fail_n, err_bits, bad_q);
   else if (kp <= 64)
     k_rescore<2><<<g, RS_WARPS * 32, rs_smem, ctx->stream>>>(Qdev, nq, ix->dim, ix->rows[kind], ix->ids_dev, cs.as<float>(),
-                                                       cr.as<uint32_t>(), cn.as<int32_t>(), kp, ix->n, k, ix->eps, oid, osc, ocnt,
+                                                       cr.as<uint32_t>(), cn.as<int32_t>(), kp, ix->n, k, ix->dres[kind], ix->eps_floor, oid, osc, ocnt,
                                                        fl.as<int32_t>(), fail_n, err_bits, bad_q);
   else
     k_rescore<4><<<g, RS_WARPS * 32, rs_smem, ctx->stream>>>(Qdev, nq, ix->dim, ix->rows[kind], ix->ids_dev, cs.as<float>(),
-                                                       cr.as<uint32_t>(), cn.as<int32_t>(), kp, ix->n, k, ix->eps, oid, osc, ocnt,
+                                                       cr.as<uint32_t>(), cn.as<int32_t>(), kp, ix->n, k, ix->dres[kind], ix->eps_floor, oid, osc, ocnt,
                                                        fl.as<int32_t>(), fail_n, err_bits, bad_q);
   kt.stop();
   FC_LAUNCH_CHECK();
@@ -641,7 +668,7 @@ void query_dev(lc_index* ix, int kind, const float* Qdev, int nq, int k, uint64_
       KTimer kt2(ctx, "rescore_tier2");
       k_rescore<4><<<(unsigned)((n_left + RS_WARPS - 1) / RS_WARPS), RS_WARPS * 32, rs_smem, ctx->stream>>>(
           q2.as<float>(), n_left, dim, ix->rows[kind], ix->ids_dev, cs2.as<float>(), cr2.as<uint32_t>(),
-          cn2.as<int32_t>(), kp2, ix->n, k, ix->eps, id2.as<uint64_t>(), sc2.as<double>(), ct2.as<int32_t>(),
+          cn2.as<int32_t>(), kp2, ix->n, k, ix->dres[kind], ix->eps_floor, id2.as<uint64_t>(), sc2.as<double>(), ct2.as<int32_t>(),
           fl2.as<int32_t>(), fn2.as<int32_t>(), reinterpret_cast<unsigned long long*>(fn2.as<char>() + 8),
           fn2.as<int32_t>() + 1);
     }
@@ -761,8 +788,10 @@ lc_status lc_index_insert_batch(lc_index* ix, const uint64_t* prompts, const flo
   InArg<float> a0(ctx, w, (size_t)n * dim), a1(ctx, o, (size_t)n * dim), a2(ctx, b, (size_t)n * dim);
   const float* dsrc[3] = {a0.dev, a1.dev, a2.dev};
   (void)src;
-  for (int t = 0; t < 3; ++t) check_units_device(ctx, dsrc[t], n, dim);
+  double res[3];
+  for (int t = 0; t < 3; ++t) res[t] = check_units_device(ctx, dsrc[t], n, dim);
   if (ix->dim == 0) ix->dim = dim;
+  for (int t = 0; t < 3; ++t) ix->dres[t] = std::max(ix->dres[t], res[t]);  // removals keep the max (conservative)
   ensure_capacity(ix, ix->n + n);
   for (int t = 0; t < 3; ++t) {
     float* dst = ix->rows[t] + (size_t)ix->n * dim;
@@ -856,9 +885,9 @@ lc_status lc_index_set_lookup(lc_index* ix, int mode, int kprime, double eps) {
   std::unique_lock lock(ix->mu);
   ix->mode = mode;
   if (kprime) ix->kprime = kprime;
-  // the certificate is only sound at or above the proven bound (lookup.cuh):
-  // a larger eps only widens it, a smaller one is clamped
-  if (eps > 0) ix->eps = std::max(eps, kEpsBound);
+  // eps > 0 is a floor on the certified bound (scaled by max(1, ||q||)):
+  // it can only widen the proven per-query bound, never narrow it
+  ix->eps_floor = eps > 0 ? eps : 0.0;
   LC_API_END
 }
 

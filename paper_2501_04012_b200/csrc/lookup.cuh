@@ -1,16 +1,19 @@
 // lookup.cuh — interface of the tcgen05 candidate stage (lookup_sm100.cu).
 //
-// Error model behind the certification in index.cu: queries and rows are
-// unit vectors (from_unit, core.cpp:61-69). Rounding each operand to bf16
-// (unit roundoff 2^-9) perturbs each product q_i*x_i by at most
-// |q_i x_i|(2^-8 + 2^-18), i.e. the dot by <= (2^-8 + 2^-18) * sum|q_i x_i|
-// <= 2^-8 + 2^-18 (Cauchy-Schwarz). fp32 accumulation of dim <= 1024 terms
-// adds <= 1024 * 2^-23 * sum|q_i x_i| ~ 1.2e-4. The default certified bound
-// eps = 2^-8 + 2^-12 = 0.0041 covers both; the measured maximum is reported
-// in lc_lookup_stats.max_abs_err.
-// For a query of norm ||q|| != 1 every term above scales by ||q||, so the
-// rescore uses eps * max(1, ||q||) per query (index.cu k_rescore); the bound
-// cannot be lowered below kEpsBound through lc_index_set_lookup.
+// Error model behind the certification in index.cu (k_rescore). Operands are
+// rounded to bf16 with round-to-nearest: q = bq + dq, x = bx + dx. Products
+// of bf16 values are exact in fp32, so the tensor-core score differs from the
+// exact dot q.x by
+//   q.x - bq.bx = q.dx + dq.x - dq.dx           (rounding of the operands)
+//   + fp32 accumulation of <= 1024 products      (<= 1024 * 2^-23 * ||bq|| ||bx||,
+//                                                 any summation order)
+// and Cauchy-Schwarz gives, for every stored row x,
+//   |score - q.x| <= ||q|| dres + ||dq|| (||x|| + dres) + 2^-13 (||q|| + ||dq||)(||x|| + dres)
+// with ||x|| <= 1 + 1e-6 (rows pass the from_unit rule, core.cpp:61-69) and
+// dres = max over stored rows of ||dx|| (computed exactly on insert). For
+// unit Gaussian-like rows dres ~ ||dq|| ~ 2^-8 / sqrt(12), so the bound is
+// ~0.0025 instead of the worst case 2^-8 + 2^-12. The measured maximum error
+// is reported in lc_lookup_stats.max_abs_err.
 #pragma once
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -19,7 +22,6 @@
 
 namespace fc {
 
-constexpr double kEpsBound = 0.00390625 + 0.000244140625;  // 2^-8 + 2^-12
 
 struct ApproxPlan {
   bool valid = false;

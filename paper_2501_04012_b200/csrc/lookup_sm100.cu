@@ -515,7 +515,16 @@ __device__ __forceinline__ void mma_box4_pair_ss(uint32_t d_tmem, uint64_t a_des
       : "memory");
 }
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
+// Pair kernel warps: 0 TMA producer, 1 MMA issuer, 2..9 epilogue. Two
+// epilogue warps share each TMEM lane quarter (a warp may only read lanes
+// 32 * (warp % 4) ..): warp half h = (warp - 2) / 4 filters accumulator
+// columns [64 h, 64 h + 64) of every tile into its own candidate list, so the
+// latency-bound filter (max tree, vote, append) has two warps per SM
+// sub-partition to hide it.
+constexpr int PAIR_THREADS = 320;
+constexpr int EPI_HALF_COLS = PN / 2;
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
     k_shortlist_pair(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmQ, Params p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -529,8 +538,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   const int nsg = nkb / BPS;
   uint8_t* stages = base;
   uint8_t* asmem = base + NSTAGE * STAGE_BYTES;
-  uint32_t* lk = reinterpret_cast<uint32_t*>(asmem + KS * ABOX);  // [cap][BM] packed candidates
-  uint64_t* bars = reinterpret_cast<uint64_t*>(lk + cap * BM);
+  uint32_t* lk_all = reinterpret_cast<uint32_t*>(asmem + KS * ABOX);  // [2 halves][cap][BM] packed candidates
+  uint64_t* bars = reinterpret_cast<uint64_t*>(lk_all + 2 * cap * BM);
   uint64_t* full = bars;
   uint64_t* empty = bars + NSTAGE;
   uint64_t* accf = bars + 2 * NSTAGE;
@@ -551,9 +560,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(smem_u32(&accf[b]), 1);
-      mbar_init(smem_u32(&acce[b]), 8);  // 4 epilogue warps x 2 CTAs
+      mbar_init(smem_u32(&acce[b]), 16);  // 8 epilogue warps x 2 CTAs
     }
-    mbar_init(smem_u32(aready), 8 + (KS > 0 ? 1 : 0));  // + the leader producer's expect_tx
+    mbar_init(smem_u32(aready), 16 + (KS > 0 ? 1 : 0));  // + the leader producer's expect_tx
     mbar_init(smem_u32(afree), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -620,21 +629,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       const bool issuer = elect_one();
       int stage = 0;
       uint32_t phase = 0, tile = 0, unit_i = 0;
+      // FC_SHORTLIST_DEBUG & 16: MMA-warp cycles waiting for [a free accumulator, TMA data, the unit's A]
+      const bool mprof = p.debug & 16;
+      long long mcyc[3] = {0, 0, 0};
       for (int u = pair; u < p.n_units; u += npairs, ++unit_i) {
         const int split = u / p.n_qtiles;
         const int64_t r0 = (int64_t)split * p.rows_per_split;
         const int64_t r1 = min((int64_t)p.n_rows, r0 + p.rows_per_split);
-        mbar_wait(smem_u32(aready), unit_i & 1);
-        tc_fence_after();
+        {
+          const long long a_t0 = mprof ? clock64() : 0;
+          mbar_wait(smem_u32(aready), unit_i & 1);
+          tc_fence_after();
+          if (mprof) mcyc[2] += clock64() - a_t0;
+        }
         for (int64_t row = r0; row < r1; row += PN, ++tile) {
           const uint32_t b = tile & 1;
           const uint32_t use = tile >> 1;
+          long long m_t0 = mprof ? clock64() : 0;
           mbar_wait(smem_u32(&acce[b]), (use & 1) ^ 1);
           tc_fence_after();
+          if (mprof) {
+            const long long t1 = clock64();
+            mcyc[0] += t1 - m_t0;
+          }
           const uint32_t d_tmem = tmem + ACC_COL + b * PN;
           for (int sg = 0; sg < nsg; ++sg) {
+            if (mprof) m_t0 = clock64();
             mbar_wait(smem_u32(&full[stage]), phase);
             tc_fence_after();
+            if (mprof) mcyc[1] += clock64() - m_t0;
             if (issuer) {
 #pragma unroll 1
               for (int bx = 0; bx < BPS; ++bx) {
@@ -660,13 +683,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         if (issuer) tc_commit_pair(smem_u32(afree));  // A (TMEM + smem parts) may be overwritten
         __syncwarp();
       }
+      if (mprof && issuer)
+        for (int i = 0; i < 3; ++i)
+          atomicAdd(reinterpret_cast<unsigned long long*>(p.stats + 12) + i, (unsigned long long)mcyc[i]);
     }
     __syncwarp();
   } else {
-    // ---------------- epilogue: warps 2..5 of both CTAs ----------------
+    // ---------------- epilogue: warps 2..9 of both CTAs ----------------
     const int quarter = warp & 3;
+    const int half = (warp - 2) >> 2;
     const int t = quarter * 32 + lane;
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+    uint32_t* lk = lk_all + (size_t)half * cap * BM;
     uint32_t tile = 0, unit_i = 0;
     for (int u = pair; u < p.n_units; u += npairs, ++unit_i) {
       const int split = u / p.n_qtiles;
@@ -678,7 +706,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         mbar_wait(smem_u32(afree), (unit_i & 1) ^ 1);
         tc_fence_after();
         const uint4* src = reinterpret_cast<const uint4*>(p.Qb + (size_t)q * p.dim);
-        for (int kb = 0; kb < KT; ++kb) {
+        for (int kb = half; kb < KT; kb += 2) {  // the two warps of a quarter split the boxes
           uint32_t r[32];
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
@@ -718,76 +746,58 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         tc_fence_after();
         if (prof) cyc[0] += clock64() - c_t0;
         if ((p.debug & 16) && lane == 0) atomicAdd(p.stats + 2, 1u);
-        const int lim_all = (int)min((int64_t)PN, r1 - row);
-        const uint32_t off_base = (uint32_t)(row - r0);
-        // The tile's 128 accumulator columns in four 32-column loads, software
-        // pipelined over two register sets (the next load is in flight while
-        // the current columns are filtered). Nothing that may call a function
-        // (compaction) runs while a load is in flight: before each 32-column
-        // step the buffers are compacted if 32 more appends might not fit.
-        const uint32_t acc_base = tmem + lane_base + ACC_COL + b * PN;
-        auto make_room = [&]() {
-          if (__any_sync(0xffffffffu, cnt + 32 > cap)) {
-            if ((p.debug & 16) && lane == 0) atomicAdd(p.stats + 1, 1u);
-            if (prof) c_t0 = clock64();
-            hist_publish(hq, lk, t, pub, cnt);  // count before compaction may drop entries
-            compact_keys(lk, t, cnt, p.kp, tau, false);
-            pub = cnt;
-            if (prof) cyc[2] += clock64() - c_t0;
-          }
-        };
-        auto filter = [&](const uint32_t* r, int col0) {
-          if (p.debug & 4) return;
+        // columns [64 half, +64) of the tile; lim = valid rows of this half
+        const int lim_all = (int)max((int64_t)0, min((int64_t)EPI_HALF_COLS, r1 - row - half * EPI_HALF_COLS));
+        const uint32_t off_base = (uint32_t)(row - r0) + half * EPI_HALF_COLS;
+        // 32 accumulator columns per step (a rolled loop: the unrolled
+        // 128-column body overflowed the instruction cache, ncu "no_inst";
+        // round 2 measured unrolled / software-pipelined / out-of-line slow
+        // path variants of this loop 15-25 % slower). Per 16-score chunk a max
+        // tree and a warp vote skip the append code unless some query of the
+        // warp has a score above its threshold.
+        // both 32-column loads of this warp's half in flight together, then
+        // the accumulator buffer is released before any filtering
+        uint32_t rv[EPI_HALF_COLS];
+        tmem_ld32_issue(tmem + lane_base + ACC_COL + b * PN + half * EPI_HALF_COLS, rv);
+        tmem_ld32_issue(tmem + lane_base + ACC_COL + b * PN + half * EPI_HALF_COLS + 32, rv + 32);
+        tmem_ld32_wait(rv);
+        tmem_ld32_wait(rv + 32);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_remote(smem_u32(&acce[b]), 0);
+        if (!(p.debug & 4)) {
 #pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {
+          for (int hh = 0; hh < EPI_HALF_COLS / 16; ++hh) {
             float vc[16];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) vc[i] = __uint_as_float(r[hh * 16 + i]);
-            const int c0 = col0 + hh * 16;
+            for (int i = 0; i < 16; ++i) vc[i] = __uint_as_float(rv[hh * 16 + i]);
+            const int c0 = hh * 16;
             float a0 = fmaxf(vc[0], vc[1]), a1 = fmaxf(vc[2], vc[3]), a2 = fmaxf(vc[4], vc[5]), a3 = fmaxf(vc[6], vc[7]);
             a0 = fmaxf(a0, fmaxf(vc[8], vc[9]));
             a1 = fmaxf(a1, fmaxf(vc[10], vc[11]));
             a2 = fmaxf(a2, fmaxf(vc[12], vc[13]));
             a3 = fmaxf(a3, fmaxf(vc[14], vc[15]));
             const float mx = fmaxf(fmaxf(a0, a1), fmaxf(a2, a3));
-            if (!__any_sync(0xffffffffu, (mx > tau) | (lim_all < PN))) continue;
+            if (!__any_sync(0xffffffffu, (mx > tau) | (lim_all < EPI_HALF_COLS))) continue;
             if (p.debug & 32) continue;  // diagnostic: fast path only
             if ((p.debug & 16) && lane == 0) atomicAdd(p.stats + 0, 1u);
+            if (__any_sync(0xffffffffu, cnt + 16 > cap)) {
+              if ((p.debug & 16) && lane == 0) atomicAdd(p.stats + 1, 1u);
+              if (prof) c_t0 = clock64();
+              hist_publish(hq, lk, t, pub, cnt);  // count before compaction may drop entries
+              compact_keys(lk, t, cnt, p.kp, tau, false);
+              pub = cnt;
+              if (prof) cyc[2] += clock64() - c_t0;
+            }
             if (prof) c_t0 = clock64();
-            // accepted scores go to independent slots (popc of the accept
-            // mask below each column): no dependent chain through cnt
-            uint32_t m = 0;
-#pragma unroll
-            for (int jj = 0; jj < 16; ++jj) m |= (uint32_t)((c0 + jj < lim_all) & (vc[jj] > tau)) << jj;
             const uint32_t off0 = off_base + (uint32_t)c0;
 #pragma unroll
-            for (int jj = 0; jj < 16; ++jj)
-              if ((m >> jj) & 1u) lk[(cnt + __popc(m & ((1u << jj) - 1u))) * BM + t] = (hkey_ru(vc[jj]) << 16) | (off0 + jj);
-            cnt += __popc(m);
+            for (int jj = 0; jj < 16; ++jj) {
+              const bool acc = (c0 + jj < lim_all) & (vc[jj] > tau);
+              if (acc) lk[cnt * BM + t] = (hkey_ru(vc[jj]) << 16) | (off0 + jj);
+              cnt += acc;
+            }
             if (prof) cyc[3] += clock64() - c_t0;
-          }
-        };
-        uint32_t ra[32], rb[32];
-        make_room();
-        tmem_ld32_issue(acc_base, ra);
-        tmem_ld32_wait(ra);
-#pragma unroll 1
-        for (int cp = 0; cp < PN / 32; cp += 2) {
-          tmem_ld32_issue(acc_base + (cp + 1) * 32, rb);
-          filter(ra, cp * 32);
-          tmem_ld32_wait(rb);
-          const bool last = cp + 2 >= PN / 32;
-          if (last) {  // every column of this accumulator buffer has been read
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive_remote(smem_u32(&acce[b]), 0);
-          }
-          make_room();
-          if (!last) tmem_ld32_issue(acc_base + (cp + 2) * 32, ra);
-          filter(rb, (cp + 1) * 32);
-          if (!last) {
-            tmem_ld32_wait(ra);
-            make_room();
           }
         }
       }
@@ -801,9 +811,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             atomicAdd(reinterpret_cast<unsigned long long*>(p.stats + 4) + i, (unsigned long long)cyc[i]);
       }
       if (q < p.nq) {
-        const size_t o = ((size_t)q * p.n_splits + split) * p.kp;
+        const int sub = 2 * split + half;  // the merge sees 2 lists per row range
+        const size_t o = ((size_t)q * 2 * p.n_splits + sub) * p.kp;
         for (int i = 0; i < cnt; ++i) p.part_k[o + i] = lk[i * BM + t];
-        p.part_n[(size_t)q * p.n_splits + split] = cnt;
+        p.part_n[(size_t)q * 2 * p.n_splits + sub] = cnt;
       }
     }
   }
@@ -838,13 +849,16 @@ constexpr int MG_W = 8;
 constexpr int MG_CAP = 1024;
 // One output candidate: stored score (upper bound of the bf16 score) and
 // absolute row slot of a packed key found at `slot` (= split * kp + j).
-__device__ __forceinline__ void emit(uint32_t key, uint32_t slot, int kp, int rps, float* cs, uint32_t* cr, size_t at) {
+// (list index >> rshift = row range: the pair kernel writes two lists, one per
+// epilogue column half, for each row range)
+__device__ __forceinline__ void emit(uint32_t key, uint32_t slot, int kp, int rps, int rshift, float* cs, uint32_t* cr,
+                                     size_t at) {
   cs[at] = hkey_float(key >> 16);
-  cr[at] = (slot / (uint32_t)kp) * (uint32_t)rps + (key & 0xFFFFu);
+  cr[at] = ((slot / (uint32_t)kp) >> rshift) * (uint32_t)rps + (key & 0xFFFFu);
 }
 
 __global__ void __launch_bounds__(MG_W * 32) k_shortlist_merge(const uint32_t* __restrict__ pk,
-                                                               const int32_t* __restrict__ pn, int n_splits, int kp, int rps,
+                                                               const int32_t* __restrict__ pn, int n_splits, int kp, int rps, int rshift,
                                                                int nq, float* __restrict__ cs, uint32_t* __restrict__ cr,
                                                                int32_t* __restrict__ cn, uint32_t* __restrict__ gkeys) {
   extern __shared__ uint32_t s_key[];  // [warps][2][MG_CAP] (gkeys [nq][2][n_splits * kp] past that)
@@ -903,7 +917,7 @@ __global__ void __launch_bounds__(MG_W * 32) k_shortlist_merge(const uint32_t* _
     const unsigned bal = __ballot_sync(0xffffffffu, take);
     if (take) {
       const int at = out + __popc(bal & ((1u << lane) - 1));
-      emit(key[i], slot[i], kp, rps, cs, cr, (size_t)q * kp + at);
+      emit(key[i], slot[i], kp, rps, rshift, cs, cr, (size_t)q * kp + at);
     }
     out += __popc(bal);
   }
@@ -913,7 +927,7 @@ __global__ void __launch_bounds__(MG_W * 32) k_shortlist_merge(const uint32_t* _
     const unsigned bal = __ballot_sync(0xffffffffu, take);
     if (take) {
       const int at = out + __popc(bal & ((1u << lane) - 1));
-      if (at < kp) emit(key[i], slot[i], kp, rps, cs, cr, (size_t)q * kp + at);
+      if (at < kp) emit(key[i], slot[i], kp, rps, rshift, cs, cr, (size_t)q * kp + at);
     }
     out += __popc(bal);
   }
@@ -952,7 +966,7 @@ __device__ __forceinline__ int block_scan(bool flag, int* red, int* pre) {
   return tot;
 }
 __global__ void __launch_bounds__(MC_T) k_shortlist_merge_cta(const uint32_t* __restrict__ pk,
-                                                              const int32_t* __restrict__ pn, int n_splits, int kp, int rps,
+                                                              const int32_t* __restrict__ pn, int n_splits, int kp, int rps, int rshift,
                                                               float* __restrict__ cs, uint32_t* __restrict__ cr,
                                                               int32_t* __restrict__ cn) {
   extern __shared__ uint32_t s_key[];  // [2][n_splits * kp]
@@ -998,7 +1012,7 @@ __global__ void __launch_bounds__(MC_T) k_shortlist_merge_cta(const uint32_t* __
       const bool take = i < n_items && (pass == 0 ? key[i] > T : key[i] == T);
       int pre;
       const int tot = block_scan(take, red, &pre);
-      if (take && out + pre < kp) emit(key[i], slot[i], kp, rps, cs, cr, (size_t)q * kp + out + pre);
+      if (take && out + pre < kp) emit(key[i], slot[i], kp, rps, rshift, cs, cr, (size_t)q * kp + out + pre);
       out += tot;
     }
   if (threadIdx.x == 0) cn[q] = min(kp, out);
@@ -1080,7 +1094,7 @@ static void launch_pair(lc_ctx* ctx, const ApproxPlan& plan, const CUtensorMap& 
   const int nkb = prm.dim / BK;
   const int KS = nkb > 8 ? nkb - 8 : 0;
   const size_t budget = 227 * 1024 - 1024 - 512;
-  const size_t slot_bytes = (size_t)BM * 4;  // one packed u32 per candidate
+  const size_t slot_bytes = (size_t)2 * BM * 4;  // one packed u32 per candidate, one list per column half
   const size_t fixed = (size_t)KS * ABOX;
   // candidate buffer: kp + 32 slots minimum (compactions stay rare once the
   // shared threshold is warm); the rest of smem goes to the table ring
@@ -1104,7 +1118,7 @@ static void launch_pair(lc_ctx* ctx, const ApproxPlan& plan, const CUtensorMap& 
   FC_CUDA(cudaFuncSetAttribute(k_shortlist_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = 2 * std::min(prm.n_units, ctx->sm_count / 2);
   KTimer kt(ctx, g_shortlist_timer);
-  k_shortlist_pair<<<grid, NTHREADS, smem, ctx->stream>>>(plan.tmap2, tmQ, prm);
+  k_shortlist_pair<<<grid, PAIR_THREADS, smem, ctx->stream>>>(plan.tmap2, tmQ, prm);
   kt.stop();
   FC_LAUNCH_CHECK();
 }
@@ -1134,7 +1148,7 @@ void approx_shortlist(lc_ctx* ctx, const ApproxPlan& plan, const float* Qdev, in
   int64_t splits = std::max<int64_t>(1, (workers * 16 + n_qtiles - 1) / n_qtiles);
   splits = std::min<int64_t>(splits, std::max<int64_t>(1, total_tiles / 16));
   // keep one query's partial lists within the merge's shared memory (few queries)
-  splits = std::min<int64_t>(splits, std::max<int64_t>(workers, (200 * 1024) / ((int64_t)kp * 8)));
+  splits = std::min<int64_t>(splits, std::max<int64_t>(workers, (200 * 1024) / ((int64_t)kp * 8 * (pair ? 2 : 1))));
   // packed candidates carry the row offset in 16 bits
   splits = std::max<int64_t>(splits, (total_tiles * bn + 65535) / 65536);
   const int64_t tiles_per_split = std::min<int64_t>((total_tiles + splits - 1) / splits, 65536 / bn);
@@ -1153,12 +1167,16 @@ void approx_shortlist(lc_ctx* ctx, const ApproxPlan& plan, const float* Qdev, in
     const char* dbg = getenv("FC_SHORTLIST_DEBUG");
     prm.debug = dbg ? atoi(dbg) : 0;
   }
-  DevBuf pk((size_t)nq * splits * kp * sizeof(uint32_t), ctx->stream);
-  DevBuf pn((size_t)nq * splits * sizeof(int32_t), ctx->stream);
+  // candidate lists per query: one per row range (single-CTA kernel) or one
+  // per row range and epilogue column half (pair kernel)
+  const int rshift = pair ? 1 : 0;
+  const int64_t lists = splits << rshift;
+  DevBuf pk((size_t)nq * lists * kp * sizeof(uint32_t), ctx->stream);
+  DevBuf pn((size_t)nq * lists * sizeof(int32_t), ctx->stream);
   DevBuf gk((size_t)nq_pad * sizeof(uint32_t), ctx->stream);
   FC_CUDA(cudaMemsetAsync(gk.p, 0, gk.bytes, ctx->stream));
-  DevBuf st(64, ctx->stream);  // u32 [0,4): counters; u64 [2,6): epilogue cycle spans
-  FC_CUDA(cudaMemsetAsync(st.p, 0, 64, ctx->stream));
+  DevBuf st(96, ctx->stream);  // u32 [0,4): counters; u64 [2,6): epilogue cycle spans; u64 [6,9): MMA waits
+  FC_CUDA(cudaMemsetAsync(st.p, 0, 96, ctx->stream));
   DevBuf hist(pair ? (size_t)nq_pad * HSTRIDE * sizeof(uint32_t) : 16, ctx->stream);
   if (pair) FC_CUDA(cudaMemsetAsync(hist.p, 0, hist.bytes, ctx->stream));
   prm.hist = hist.as<uint32_t>();
@@ -1180,18 +1198,20 @@ void approx_shortlist(lc_ctx* ctx, const ApproxPlan& plan, const float* Qdev, in
     launch_single<128>(ctx, plan, prm);
   }
   if (prm.debug & 16) {
-    uint32_t h[16];
-    FC_CUDA(cudaMemcpyAsync(h, st.p, 64, cudaMemcpyDeviceToHost, ctx->stream));
+    uint32_t h[24];
+    FC_CUDA(cudaMemcpyAsync(h, st.p, 96, cudaMemcpyDeviceToHost, ctx->stream));
     sync(ctx);
-    unsigned long long cy[4];
+    unsigned long long cy[4], mc[3];
     memcpy(cy, h + 4, sizeof cy);
+    memcpy(mc, h + 12, sizeof mc);
     const double wt = (double)std::max(1u, h[2]);  // warp-tiles
     fprintf(stderr, "shortlist stats: warp-tiles %u slow-chunks %u (%.3f/tile) compactions %u (%.4f/tile) nstage %d bps %d cap %d splits %d"
-            " | cycles per warp-tile: acc-wait %.0f hist %.0f compact %.0f append %.0f\n",
+            " | cycles per warp-tile: acc-wait %.0f hist %.0f compact %.0f append %.0f"
+            " | MMA cycles per tile: acc-free wait %.0f data wait %.0f A wait %.0f\n",
             h[2], h[0], h[0] / wt, h[1], h[1] / wt, prm.nstage, prm.bps, prm.cap, prm.n_splits, cy[0] / wt, cy[1] / wt,
-            cy[2] / wt, cy[3] / wt);
+            cy[2] / wt, cy[3] / wt, mc[0] * 16.0 / wt, mc[1] * 16.0 / wt, mc[2] * 16.0 / wt);
   }
-  const size_t per_warp = (size_t)splits * kp * 2 * sizeof(uint32_t);  // keys + slots
+  const size_t per_warp = (size_t)lists * kp * 2 * sizeof(uint32_t);  // keys + slots
   KTimer kmt(ctx, "shortlist_merge");
   if (nq < ctx->sm_count && per_warp <= 200 * 1024) {
     static std::atomic<uint64_t> attr_set{0};  // per-device bit: the attribute is per device
@@ -1199,8 +1219,8 @@ void approx_shortlist(lc_ctx* ctx, const ApproxPlan& plan, const float* Qdev, in
       FC_CUDA(cudaFuncSetAttribute(k_shortlist_merge_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
       attr_set.fetch_or(1ull << (ctx->device & 63));
     }
-    k_shortlist_merge_cta<<<nq, MC_T, per_warp, ctx->stream>>>(pk.as<uint32_t>(), pn.as<int32_t>(), (int)splits, kp,
-                                                               prm.rows_per_split, cand_s, cand_r, cand_n);
+    k_shortlist_merge_cta<<<nq, MC_T, per_warp, ctx->stream>>>(pk.as<uint32_t>(), pn.as<int32_t>(), (int)lists, kp,
+                                                               prm.rows_per_split, rshift, cand_s, cand_r, cand_n);
     FC_LAUNCH_CHECK();
     count_launch(ctx, 3);
     return;
@@ -1215,7 +1235,7 @@ void approx_shortlist(lc_ctx* ctx, const ApproxPlan& plan, const float* Qdev, in
     attr_set2.fetch_or(1ull << (ctx->device & 63));
   }
   k_shortlist_merge<<<(nq + MG_W - 1) / MG_W, MG_W * 32, msmem, ctx->stream>>>(
-      pk.as<uint32_t>(), pn.as<int32_t>(), (int)splits, kp, prm.rows_per_split, nq, cand_s, cand_r, cand_n,
+      pk.as<uint32_t>(), pn.as<int32_t>(), (int)lists, kp, prm.rows_per_split, rshift, nq, cand_s, cand_r, cand_n,
       gkeys.as<uint32_t>());
   FC_LAUNCH_CHECK();
   count_launch(ctx, 3);
