@@ -165,8 +165,11 @@ typedef struct lc_lookup_stats {
   uint64_t fallback;      /* not certified by the K' shortlist            */
   uint64_t exact_scans;   /* lookups served by the exact scan directly    */
   double max_abs_err;     /* max |bf16 approx - fp64 exact| seen in rescores */
-  uint64_t tier2_certified; /* of the fallbacks: certified by the K'=128 re-shortlist
+  uint64_t tier2_certified; /* of the fallbacks: certified by a bf16 re-shortlist
                                (the rest are counted in exact_scans) */
+  uint64_t i8_batches;    /* batches whose tier 1 was the int8 tensor-core shortlist */
+  uint64_t i8_rescored;   /* rows exact-scored by the int8 tier's rescore  */
+  uint64_t i8_candidates; /* rows in the int8 tier's merged shortlists     */
 } lc_lookup_stats;
 lc_status lc_index_stats(lc_index* ix, lc_lookup_stats* out, int reset);
 /* mode: 0 auto (tensor-core path when size >= 8192), 1 force exact scan,

@@ -23,6 +23,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -51,6 +52,17 @@ struct lc_index {
   // (lookup.cuh); eps_floor (lc_index_set_lookup) can only widen it.
   double dres[3] = {0.0, 0.0, 0.0};
   double eps_floor = 0.0;
+  // int8 tier-1 copy (dim % 128 == 0): rows quantized per 128-slot tile
+  // (lookup.cuh); dres8 = max residual norm of the quantized rows (kept as a
+  // running max over re-quantizations, so it stays a bound).
+  bool i8 = false;
+  int8_t* rows8[3] = {nullptr, nullptr, nullptr};
+  float* tscale[3] = {nullptr, nullptr, nullptr};
+  float* tres[3] = {nullptr, nullptr, nullptr};  // per-tile max residual norm
+  double dres8[3] = {0.0, 0.0, 0.0};
+  int i8_kout = 256;   // merged candidates per query (FC_LOOKUP_I8_KOUT)
+  int i8_kunit = 32;   // per unit list
+  I8Plan iplan[3];
   lc_lookup_stats stats{};
   ApproxPlan plan[3];
   mutable std::shared_mutex mu;  // readers: queries; writer: insert/remove (vindex.hpp:61)
@@ -436,12 +448,271 @@ __global__ void __launch_bounds__(RS_WARPS * 32)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Exact rescore of the int8 shortlist + certification (one warp per query).
+//
+// The int8 tier hands over up to KI_MAX candidates per query with stored
+// scores U (upper bounds of the exact dot) and cand_m[q] (every row outside
+// the list has exact <= cand_m). Two passes over the list:
+//  1. bf16 pre-score b of every candidate: bf16(q) . bf16(x) in fp32, one
+//     candidate per warp iteration with the row read coalesced (1.5 KB at
+//     dim 768) -- |b - q.x| <= eps_bf, the bound of k_rescore;
+//  2. the reference's sequential fp64 dot (vindex.cpp:67) only for the
+//     candidates with b >= b_k - 2 eps_bf (b_k = k-th best b): the k best by b
+//     all have exact >= b_k - eps_bf, so a skipped one (exact <= b + eps_bf)
+//     cannot reach the top k. Typically ~10-20 of the ~100 candidates.
+// Certified iff cand_m + (fp64 rounding of the reference dot) < T_k, or the
+// list holds every row. k <= 32 (the best 32 exact candidates are kept sorted
+// across the lanes by a bitonic merge per chunk of 32).
+// ---------------------------------------------------------------------------
+constexpr int KI_MAX = 256;
+constexpr int RI_WARPS = 4;
+
+__device__ __forceinline__ Cand shfl_cand(const Cand& c, int src_lane_xor) {
+  Cand o;
+  o.s = __shfl_xor_sync(0xffffffffu, c.s, src_lane_xor);
+  o.id = __shfl_xor_sync(0xffffffffu, c.id, src_lane_xor);
+  o.slot = __shfl_xor_sync(0xffffffffu, c.slot, src_lane_xor);
+  return o;
+}
+// one compare-exchange step of a warp bitonic network in "better first" order
+__device__ __forceinline__ void cx_step(Cand& c, int j, bool best_first) {
+  const int lane = threadIdx.x & 31;
+  const Cand o = shfl_cand(c, j);
+  const bool lower = (lane & j) == 0;
+  const bool take_o = (lower == best_first) ? cand_better(o, c) : cand_better(c, o);
+  if (take_o) c = o;
+}
+// sort 32 candidates (one per lane) best first
+__device__ __forceinline__ void warp_sort32(Cand& c) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) cx_step(c, j, (lane & k) == 0);
+}
+// top-32 of two best-first sorted lists (A, B), best first, into A
+__device__ __forceinline__ void warp_merge32(Cand& a, const Cand& b) {
+  const int lane = threadIdx.x & 31;
+  Cand br;  // B reversed
+  br.s = __shfl_sync(0xffffffffu, b.s, 31 - lane);
+  br.id = __shfl_sync(0xffffffffu, b.id, 31 - lane);
+  br.slot = __shfl_sync(0xffffffffu, b.slot, 31 - lane);
+  if (cand_better(br, a)) a = br;  // bitonic: holds the best 32 of A u B
+#pragma unroll
+  for (int j = 16; j > 0; j >>= 1) cx_step(a, j, true);
+}
+__device__ __forceinline__ uint32_t fkey(float f) {
+  const uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+__global__ void __launch_bounds__(RI_WARPS * 32)
+    k_rescore_i8(const float* __restrict__ Q, int nq, int dim, const float* __restrict__ rows,
+                 const __nv_bfloat16* __restrict__ rowsb, const uint64_t* __restrict__ ids,
+                 const uint32_t* __restrict__ cand_r, const int32_t* __restrict__ cand_n,
+                 const float* __restrict__ cand_m, int kout, int64_t n_rows, int k, double dres, double eps_floor,
+                 uint64_t* __restrict__ out_ids, double* __restrict__ out_sc, int32_t* __restrict__ out_cnt,
+                 int32_t* __restrict__ fail_list, int32_t* __restrict__ fail_n,
+                 unsigned long long* __restrict__ max_err_bits, int32_t* __restrict__ bad_query,
+                 unsigned long long* __restrict__ gathered) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q = blockIdx.x * RI_WARPS + warp;
+  if (q >= nq) return;
+  extern __shared__ uint8_t s_raw[];
+  // per warp: fp32 query [dim] | bf16 query [dim] | sort keys [KI_MAX]
+  const size_t per_warp = (size_t)dim * 6 + KI_MAX * 8;
+  uint8_t* wbase = s_raw + (size_t)warp * per_warp;
+  float* sq = reinterpret_cast<float*>(wbase);
+  __nv_bfloat16* sb = reinterpret_cast<__nv_bfloat16*>(wbase + (size_t)dim * 4);
+  uint64_t* skey = reinterpret_cast<uint64_t*>(wbase + (size_t)dim * 6);
+  const float* qv = Q + (int64_t)q * dim;
+  double qsq = 0.0, dsq = 0.0;
+  bool qfin = true;
+  for (int d = lane; d < dim; d += 32) {
+    const float v = qv[d];
+    sq[d] = v;
+    const __nv_bfloat16 bv = __float2bfloat16_rn(v);
+    sb[d] = bv;
+    qfin &= isfinite(v);
+    qsq = fma((double)v, (double)v, qsq);
+    const double e = (double)v - (double)__bfloat162float(bv);
+    dsq = fma(e, e, dsq);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    qsq += __shfl_xor_sync(0xffffffffu, qsq, off);
+    dsq += __shfl_xor_sync(0xffffffffu, dsq, off);
+  }
+  qfin = __all_sync(0xffffffffu, qfin);
+  if (!qfin && lane == 0) atomicExch(bad_query, 1);
+  const double qn = sqrt(qsq) * (1.0 + 0x1p-40), dqn = sqrt(dsq) * (1.0 + 0x1p-40);
+  const bool q_uncertifiable = !qfin || !(qn < 16384.0);
+  // bf16 score bound (as k_rescore: operand rounding + fp32 accumulation)
+  const double xn = 1.0 + 1e-6;
+  double eps = qn * dres + dqn * (xn + dres) + 0x1p-13 * (qn + dqn) * (xn + dres);
+  eps = fmax(eps * (1.0 + 0x1p-20), eps_floor * fmax(1.0, qn));
+  // the reference's fp64 sequential dot vs the real dot: <= dim 2^-53 ||q|| ||x||
+  const double margin = 1e-12 * (1.0 + qn);
+  const int cn = min(cand_n[q], KI_MAX);
+  // (1) bf16 pre-score, 4 candidates per iteration (loads of all 4 in flight)
+  const uint4* sb4 = reinterpret_cast<const uint4*>(sb);
+  const int n16 = dim / 8;  // 16-byte chunks per bf16 row
+  for (int i0 = 0; i0 < cn; i0 += 4) {
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    uint32_t rr[4];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) rr[g] = i0 + g < cn ? cand_r[(int64_t)q * kout + i0 + g] : 0u;
+    for (int c = lane; c < n16; c += 32) {
+      const uint4 qa = sb4[c];
+      uint4 xa[4];
+#pragma unroll
+      for (int g = 0; g < 4; ++g)
+        xa[g] = i0 + g < cn ? __ldg(reinterpret_cast<const uint4*>(rowsb + (int64_t)rr[g] * dim) + c) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        const __nv_bfloat162* x2 = reinterpret_cast<const __nv_bfloat162*>(&xa[g]);
+        const __nv_bfloat162* q2 = reinterpret_cast<const __nv_bfloat162*>(&qa);
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const float2 xf = __bfloat1622float2(x2[h]), qf = __bfloat1622float2(q2[h]);
+          acc[g] = fmaf(qf.x, xf.x, acc[g]);
+          acc[g] = fmaf(qf.y, xf.y, acc[g]);
+        }
+      }
+    }
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) acc[g] += __shfl_xor_sync(0xffffffffu, acc[g], off);
+    }
+    if (lane < 4 && i0 + lane < cn) {
+      const float bsc = lane == 0 ? acc[0] : lane == 1 ? acc[1] : lane == 2 ? acc[2] : acc[3];
+      skey[i0 + lane] = ((uint64_t)fkey(bsc) << 32) | (uint32_t)(i0 + lane);
+    }
+  }
+  // (2) sort by b, descending
+  int np2 = 32;
+  while (np2 < cn) np2 <<= 1;
+  for (int i = cn + lane; i < np2; i += 32) skey[i] = 0;
+  __syncwarp();
+  for (int kk = 2; kk <= np2; kk <<= 1)
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      for (int i = lane; i < np2; i += 32) {
+        const int p = i ^ j;
+        if (p > i) {
+          const uint64_t a = skey[i], b = skey[p];
+          const bool desc = (i & kk) == 0;
+          if (desc ? a < b : a > b) {
+            skey[i] = b;
+            skey[p] = a;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  auto key_b = [](uint64_t key) {
+    const uint32_t ok = (uint32_t)(key >> 32);
+    return __uint_as_float((ok & 0x80000000u) ? (ok & 0x7FFFFFFFu) : ~ok);
+  };
+  // exact-score the prefix with b >= b_k - 2 eps (the whole list when it
+  // holds <= k candidates)
+  const float bk = cn > k ? key_b(skey[k - 1]) : -INFINITY;
+  const double need_b = (double)bk - 2.0 * eps;
+  Cand best;
+  best.s = -INFINITY;
+  best.id = ~0ull;
+  best.slot = -1;
+  int n_have = 0, n_gath = 0;
+  double local_err = 0.0;
+  for (int base = 0; base < cn; base += 32) {
+    if ((double)key_b(skey[base]) < need_b) break;
+    Cand c;
+    c.s = -INFINITY;
+    c.id = ~0ull;
+    c.slot = -1;
+    const int i = base + lane;
+    if (i < cn && (double)key_b(skey[i]) >= need_b) {
+      const int li = (int)(uint32_t)skey[i];
+      const uint32_t r = cand_r[(int64_t)q * kout + li];
+      const float* x = rows + (int64_t)r * dim;
+      double acc = 0.0;
+      {
+        // sequential fp64 in d order (vindex.cpp:67), 32 elements in flight
+        // (dim % 128 == 0 on the int8 tier)
+        const float4* x4 = reinterpret_cast<const float4*>(x);
+        const float4* q4 = reinterpret_cast<const float4*>(sq);
+        float4 nx[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) nx[u] = __ldg(x4 + u);
+        for (int d4 = 0; d4 < dim / 4; d4 += 8) {
+          float4 cx[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) cx[u] = nx[u];
+          if (d4 + 8 < dim / 4) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) nx[u] = __ldg(x4 + d4 + 8 + u);
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const float4 qq = q4[d4 + u];
+            acc = fma((double)qq.x, (double)cx[u].x, acc);
+            acc = fma((double)qq.y, (double)cx[u].y, acc);
+            acc = fma((double)qq.z, (double)cx[u].z, acc);
+            acc = fma((double)qq.w, (double)cx[u].w, acc);
+          }
+        }
+      }
+      local_err = fmax(local_err, fabs(acc - (double)key_b(skey[i])));
+      c.s = acc;
+      c.id = ids[r];
+      c.slot = r;
+      ++n_gath;
+    }
+    n_have += __popc(__ballot_sync(0xffffffffu, c.slot >= 0));
+    warp_sort32(c);
+    warp_merge32(best, c);
+  }
+  const double tk = __shfl_sync(0xffffffffu, best.s, min(k, 32) - 1);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    local_err = fmax(local_err, __shfl_xor_sync(0xffffffffu, local_err, off));
+    n_gath += __shfl_xor_sync(0xffffffffu, n_gath, off);
+  }
+  if (lane == 0) {
+    if (local_err > 0) atomicMax(max_err_bits, (unsigned long long)__double_as_longlong(local_err));
+    atomicAdd(gathered, (unsigned long long)n_gath);
+    atomicAdd(gathered + 1, (unsigned long long)cn);
+  }
+  const int got = min(n_have, k);
+  if (lane < k) {
+    out_ids[(int64_t)q * k + lane] = lane < got ? best.id : 0;
+    out_sc[(int64_t)q * k + lane] = lane < got ? best.s : 0.0;
+  }
+  if (lane == 0) {
+    out_cnt[q] = got;
+    bool ok;
+    if (q_uncertifiable) ok = false;
+    else if (cn >= n_rows) ok = true;  // every row is in the list
+    else ok = got >= k && (double)cand_m[q] + margin < tk;
+    if (!ok) fail_list[atomicAdd(fail_n, 1)] = q;
+  }
+}
+
 }  // namespace fc
 
 // ---------------------------------------------------------------------------
 // host helpers
 // ---------------------------------------------------------------------------
 namespace {
+
+// int8 tier 1 for shapes the s8 kernel takes (128-byte K boxes, A in TMEM);
+// FC_LOOKUP_I8=0 keeps the bf16 tier only (A/B measurements)
+bool i8_wanted(int dim) {
+  static const bool off = getenv("FC_LOOKUP_I8") && atoi(getenv("FC_LOOKUP_I8")) == 0;
+  return !off && dim % 128 == 0 && dim <= 1024;
+}
 
 void ensure_capacity(lc_index* ix, int64_t need) {
   if (need <= ix->cap) return;
@@ -462,6 +733,29 @@ void ensure_capacity(lc_index* ix, int64_t need) {
     ix->rows[t] = nr;
     ix->rowsb[t] = nb;
     ix->plan[t].valid = false;
+    if (ix->i8) {
+      int8_t* n8 = nullptr;
+      float *ns = nullptr, *nr8 = nullptr;
+      // whole 128-row tiles: the quantizer writes (zeros) up to the tile end
+      const int64_t nc8 = (nc + 127) / 128 * 128;
+      FC_CUDA(cudaMalloc(&n8, (size_t)nc8 * ix->dim));
+      FC_CUDA(cudaMalloc(&ns, (size_t)(nc8 / 128) * sizeof(float)));
+      FC_CUDA(cudaMalloc(&nr8, (size_t)(nc8 / 128) * sizeof(float)));
+      if (ix->n) {
+        const size_t nt = (size_t)((ix->n + 127) / 128);
+        FC_CUDA(cudaMemcpyAsync(n8, ix->rows8[t], nt * 128 * ix->dim, cudaMemcpyDeviceToDevice, ctx->stream));
+        FC_CUDA(cudaMemcpyAsync(ns, ix->tscale[t], nt * sizeof(float), cudaMemcpyDeviceToDevice, ctx->stream));
+        FC_CUDA(cudaMemcpyAsync(nr8, ix->tres[t], nt * sizeof(float), cudaMemcpyDeviceToDevice, ctx->stream));
+      }
+      FC_CUDA(cudaStreamSynchronize(ctx->stream));
+      if (ix->rows8[t]) cudaFree(ix->rows8[t]);
+      if (ix->tscale[t]) cudaFree(ix->tscale[t]);
+      if (ix->tres[t]) cudaFree(ix->tres[t]);
+      ix->rows8[t] = n8;
+      ix->tscale[t] = ns;
+      ix->tres[t] = nr8;
+      ix->iplan[t].valid = false;
+    }
   }
   uint64_t* ni = nullptr;
   FC_CUDA(cudaMalloc(&ni, (size_t)nc * sizeof(uint64_t)));
@@ -470,6 +764,24 @@ void ensure_capacity(lc_index* ix, int64_t need) {
   if (ix->ids_dev) cudaFree(ix->ids_dev);
   ix->ids_dev = ni;
   ix->cap = nc;
+}
+
+// Re-quantize the int8 tiles [t0, t1) of every table (after an insert or a
+// remove changed their rows) and fold their residual norms into dres8.
+void requantize(lc_index* ix, int64_t t0, int64_t t1) {
+  if (!ix->i8 || t1 <= t0 || ix->n == 0) return;
+  lc_ctx* ctx = ix->ctx;
+  DevBuf rb(3 * sizeof(unsigned long long), ctx->stream);
+  FC_CUDA(cudaMemsetAsync(rb.p, 0, rb.bytes, ctx->stream));
+  for (int t = 0; t < 3; ++t) {
+    i8_quantize_tiles(ctx, ix->rows[t], ix->n, ix->dim, t0, t1, ix->rows8[t], ix->tscale[t], ix->tres[t],
+                      rb.as<unsigned long long>() + t);
+    ix->iplan[t].valid = false;
+  }
+  double r[3];
+  FC_CUDA(cudaMemcpyAsync(r, rb.p, sizeof r, cudaMemcpyDeviceToHost, ctx->stream));
+  sync(ctx);
+  for (int t = 0; t < 3; ++t) ix->dres8[t] = std::max(ix->dres8[t], r[t]);
 }
 
 // from_unit check of n rows; returns the max bf16 residual norm of the rows
@@ -540,7 +852,11 @@ void query_dev(lc_index* ix, int kind, const float* Qdev, int nq, int k, uint64_
     std::lock_guard<std::mutex> sl(ix->stats_mu);
     ix->stats.queries += nq;
   }
-  const bool approx_ok = approx_available() && ix->dim % 64 == 0 && ix->dim <= 1024 && k <= ix->kprime;
+  // bf16 tier: the query's K boxes and two accumulators must fit TMEM (dim <= 768);
+  // int8 tier: dim % 128 == 0, <= 1024 (ix->i8), k <= 32, batches that fill CTA pairs
+  const bool bf16_ok = ix->dim % 64 == 0 && ix->dim <= 768 && k <= ix->kprime;
+  const bool i8_ok = ix->i8 && k <= 32 && nq > 128;
+  const bool approx_ok = approx_available() && (bf16_ok || i8_ok);
   const bool use_approx = approx_ok && (ix->mode == 2 || (ix->mode == 0 && ix->n >= 8192));
   if (!use_approx) {
     FC_REQUIRE(ix->mode != 2 || approx_ok, "lc_index_query_topk: tensor-core path unavailable for this shape");
@@ -561,44 +877,91 @@ void query_dev(lc_index* ix, int kind, const float* Qdev, int nq, int k, uint64_
     return;
   }
   const int kp = ix->kprime;
-  DevBuf cs((size_t)nq * kp * sizeof(float), ctx->stream);
-  DevBuf cr((size_t)nq * kp * sizeof(uint32_t), ctx->stream);
-  DevBuf cn((size_t)nq * sizeof(int32_t), ctx->stream);
-  {
-    std::lock_guard<std::mutex> pl(ix->plan_mu);
-    if (!ix->plan[kind].valid || ix->plan[kind].n_rows != ix->n)
-      approx_plan(ix->plan[kind], ix->rowsb[kind], ix->n, ix->dim, ctx->sm_count);
-  }
-  approx_shortlist(ctx, ix->plan[kind], Qdev, nq, kp, cs.as<float>(), cr.as<uint32_t>(), cn.as<int32_t>());
+  const int dim = ix->dim;
   DevBuf fl((size_t)nq * sizeof(int32_t), ctx->stream);
   DevBuf fn(16, ctx->stream);  // [0,4) fail count, [4,8) non-finite query flag, [8,16) max |err| bits
   int32_t* fail_n = fn.as<int32_t>();
   int32_t* bad_q = fn.as<int32_t>() + 1;
   auto* err_bits = reinterpret_cast<unsigned long long*>(fn.as<char>() + 8);
   FC_CUDA(cudaMemsetAsync(fn.p, 0, 16, ctx->stream));
-  const unsigned g = (unsigned)((nq + RS_WARPS - 1) / RS_WARPS);
-  const size_t rs_smem = (size_t)RS_WARPS * ix->dim * sizeof(float);
+  const size_t rs_smem = (size_t)RS_WARPS * dim * sizeof(float);
   if (rs_smem > 48 * 1024) {
     FC_CUDA(cudaFuncSetAttribute(k_rescore<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs_smem));
     FC_CUDA(cudaFuncSetAttribute(k_rescore<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs_smem));
     FC_CUDA(cudaFuncSetAttribute(k_rescore<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs_smem));
   }
-  KTimer kt(ctx, "rescore");
-  if (kp <= 32)
-    k_rescore<1><<<g, RS_WARPS * 32, rs_smem, ctx->stream>>>(Qdev, nq, ix->dim, ix->rows[kind], ix->ids_dev, cs.as<float>(),
-                                                       cr.as<uint32_t>(), cn.as<int32_t>(), kp, ix->n, k, ix->dres[kind], ix->eps_floor, oid, osc, ocnt,
-                                                       fl.as<int32_t>(), fail_n, err_bits, bad_q);
-  else if (kp <= 64)
-    k_rescore<2><<<g, RS_WARPS * 32, rs_smem, ctx->stream>>>(Qdev, nq, ix->dim, ix->rows[kind], ix->ids_dev, cs.as<float>(),
-                                                       cr.as<uint32_t>(), cn.as<int32_t>(), kp, ix->n, k, ix->dres[kind], ix->eps_floor, oid, osc, ocnt,
-                                                       fl.as<int32_t>(), fail_n, err_bits, bad_q);
-  else
-    k_rescore<4><<<g, RS_WARPS * 32, rs_smem, ctx->stream>>>(Qdev, nq, ix->dim, ix->rows[kind], ix->ids_dev, cs.as<float>(),
-                                                       cr.as<uint32_t>(), cn.as<int32_t>(), kp, ix->n, k, ix->dres[kind], ix->eps_floor, oid, osc, ocnt,
-                                                       fl.as<int32_t>(), fail_n, err_bits, bad_q);
-  kt.stop();
-  FC_LAUNCH_CHECK();
-  count_launch(ctx);
+  // Tier 1: the int8 tensor-core shortlist (2x the bf16 tensor rate) for
+  // batches that fill CTA pairs, else the bf16 shortlist with K' = kprime.
+  const bool tier1_i8 = i8_ok;
+  int64_t gathered = -1, cands = -1;
+  if (tier1_i8) {
+    const int kout = ix->i8_kout;
+    DevBuf cs((size_t)nq * kout * sizeof(float), ctx->stream), cr((size_t)nq * kout * sizeof(uint32_t), ctx->stream);
+    DevBuf cn((size_t)nq * sizeof(int32_t), ctx->stream), cm((size_t)nq * sizeof(float), ctx->stream);
+    DevBuf gb(2 * sizeof(unsigned long long), ctx->stream);
+    FC_CUDA(cudaMemsetAsync(gb.p, 0, gb.bytes, ctx->stream));
+    {
+      std::lock_guard<std::mutex> pl(ix->plan_mu);
+      if (!ix->iplan[kind].valid || ix->iplan[kind].n_rows != ix->n) {
+        // median tile residual: the threshold offset of the int8 filter
+        const int64_t nt = (ix->n + 127) / 128;
+        std::vector<float> tr(nt);
+        FC_CUDA(cudaMemcpyAsync(tr.data(), ix->tres[kind], nt * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+        sync(ctx);
+        std::nth_element(tr.begin(), tr.begin() + nt / 2, tr.end());
+        i8_plan(ix->iplan[kind], ix->rows8[kind], ix->tscale[kind], ix->tres[kind], ix->n, dim, tr[nt / 2]);
+      }
+    }
+    i8_shortlist(ctx, ix->iplan[kind], Qdev, nq, k, ix->i8_kunit, kout, cs.as<float>(), cr.as<uint32_t>(),
+                 cn.as<int32_t>(), cm.as<float>());
+    const size_t ri_smem = (size_t)RI_WARPS * ((size_t)dim * 6 + KI_MAX * 8);
+    static std::atomic<uint64_t> attr_set{0};
+    if (!(attr_set.load() >> (ctx->device & 63) & 1)) {
+      FC_CUDA(cudaFuncSetAttribute(k_rescore_i8, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(RI_WARPS * (1024 * 6 + KI_MAX * 8))));
+      attr_set.fetch_or(1ull << (ctx->device & 63));
+    }
+    KTimer kt(ctx, "rescore");
+    k_rescore_i8<<<(unsigned)((nq + RI_WARPS - 1) / RI_WARPS), RI_WARPS * 32, ri_smem, ctx->stream>>>(
+        Qdev, nq, dim, ix->rows[kind], ix->rowsb[kind], ix->ids_dev, cr.as<uint32_t>(), cn.as<int32_t>(),
+        cm.as<float>(), kout, ix->n, k, ix->dres[kind], ix->eps_floor, oid, osc, ocnt, fl.as<int32_t>(), fail_n,
+        err_bits, bad_q, gb.as<unsigned long long>());
+    kt.stop();
+    FC_LAUNCH_CHECK();
+    count_launch(ctx);
+    unsigned long long hg[2] = {0, 0};
+    FC_CUDA(cudaMemcpyAsync(hg, gb.p, sizeof hg, cudaMemcpyDeviceToHost, ctx->stream));
+    sync(ctx);
+    gathered = (int64_t)hg[0];
+    cands = (int64_t)hg[1];
+  } else {
+    DevBuf cs((size_t)nq * kp * sizeof(float), ctx->stream);
+    DevBuf cr((size_t)nq * kp * sizeof(uint32_t), ctx->stream);
+    DevBuf cn((size_t)nq * sizeof(int32_t), ctx->stream);
+    {
+      std::lock_guard<std::mutex> pl(ix->plan_mu);
+      if (!ix->plan[kind].valid || ix->plan[kind].n_rows != ix->n)
+        approx_plan(ix->plan[kind], ix->rowsb[kind], ix->n, dim, ctx->sm_count);
+    }
+    approx_shortlist(ctx, ix->plan[kind], Qdev, nq, kp, cs.as<float>(), cr.as<uint32_t>(), cn.as<int32_t>());
+    const unsigned g = (unsigned)((nq + RS_WARPS - 1) / RS_WARPS);
+    KTimer kt(ctx, "rescore");
+    if (kp <= 32)
+      k_rescore<1><<<g, RS_WARPS * 32, rs_smem, ctx->stream>>>(Qdev, nq, dim, ix->rows[kind], ix->ids_dev, cs.as<float>(),
+                                                         cr.as<uint32_t>(), cn.as<int32_t>(), kp, ix->n, k, ix->dres[kind], ix->eps_floor, oid, osc, ocnt,
+                                                         fl.as<int32_t>(), fail_n, err_bits, bad_q);
+    else if (kp <= 64)
+      k_rescore<2><<<g, RS_WARPS * 32, rs_smem, ctx->stream>>>(Qdev, nq, dim, ix->rows[kind], ix->ids_dev, cs.as<float>(),
+                                                         cr.as<uint32_t>(), cn.as<int32_t>(), kp, ix->n, k, ix->dres[kind], ix->eps_floor, oid, osc, ocnt,
+                                                         fl.as<int32_t>(), fail_n, err_bits, bad_q);
+    else
+      k_rescore<4><<<g, RS_WARPS * 32, rs_smem, ctx->stream>>>(Qdev, nq, dim, ix->rows[kind], ix->ids_dev, cs.as<float>(),
+                                                         cr.as<uint32_t>(), cn.as<int32_t>(), kp, ix->n, k, ix->dres[kind], ix->eps_floor, oid, osc, ocnt,
+                                                         fl.as<int32_t>(), fail_n, err_bits, bad_q);
+    kt.stop();
+    FC_LAUNCH_CHECK();
+    count_launch(ctx);
+  }
   int32_t hf[4] = {0, 0, 0, 0};
   FC_CUDA(cudaMemcpyAsync(hf, fn.p, 16, cudaMemcpyDeviceToHost, ctx->stream));
   sync(ctx);
@@ -612,33 +975,45 @@ void query_dev(lc_index* ix, int kind, const float* Qdev, int nq, int k, uint64_
     ix->stats.max_abs_err = std::max(ix->stats.max_abs_err, err);
     ix->stats.certified += nq - nf;
     ix->stats.fallback += nf;
+    if (tier1_i8) {
+      ix->stats.i8_batches += 1;
+      ix->stats.i8_rescored += gathered;
+      ix->stats.i8_candidates += cands;
+    }
   }
   // FC_LOOKUP_DIAG=1 (kernel-timing diagnostics with FC_SHORTLIST_DEBUG only): skip the
   // exact re-scan, so results are NOT exact in that mode.
   static const bool diag = getenv("FC_LOOKUP_DIAG") && atoi(getenv("FC_LOOKUP_DIAG")) == 1;
   if (nf == 0 || diag) return;
   // Tier 2: the uncertified queries (near-ties around the k-th score) rerun
-  // the tensor-core shortlist with a longer K' and are rescored/certified
-  // again (~one streaming pass of the bf16 table each), escalating K' = kp + 32
-  // then 128 (K' = kp + 32 certifies the usual near-ties at ~2/3 the cost, as
-  // more pipeline stages fit); only what still fails takes the exact fp64 scan
-  // of every row. FC_LOOKUP_TIER2=0 disables it; FC_LOOKUP_TIER2_KP caps K'.
+  // the bf16 tensor-core shortlist (after the int8 tier: first with K' =
+  // kprime, whose ~5x tighter bound certifies almost all of them) with a
+  // longer K' and are rescored/certified again (~one streaming pass of the
+  // bf16 table each), escalating K' = kp + 32 then 128 (K' = kp + 32
+  // certifies the usual near-ties at ~2/3 the cost, as more pipeline stages
+  // fit); only what still fails takes the exact fp64 scan of every row.
+  // FC_LOOKUP_TIER2=0 disables it; FC_LOOKUP_TIER2_KP caps K'.
   // Clustered tables (many near-duplicate rows per query, e.g. shared object
   // embeddings) fail for most of the batch and a longer K' rarely helps there:
-  // when more than 1/16 of the batch (and > 8 queries) failed, go straight to
-  // the exact scan. Same results either way; this only picks the cheaper path.
-  const bool tier2_off = (getenv("FC_LOOKUP_TIER2") && atoi(getenv("FC_LOOKUP_TIER2")) == 0) ||
-                         (nf > 8 && nf * 16 > nq);
-  const int dim = ix->dim;
+  // when more than 1/16 of the batch (and > 8 queries) failed a bf16 pass, go
+  // straight to the exact scan. Same results either way; this only picks the
+  // cheaper path.
+  const bool tier2_env_off = getenv("FC_LOOKUP_TIER2") && atoi(getenv("FC_LOOKUP_TIER2")) == 0;
+  bool tier2_off = tier2_env_off || !bf16_ok || (!tier1_i8 && nf > 8 && nf * 16 > nq);
   constexpr int KP2_MAX = 128;
   int kp2_cap = KP2_MAX;
   if (const char* e = getenv("FC_LOOKUP_TIER2_KP")) kp2_cap = std::max(kp + 32, std::min(KP2_MAX, atoi(e)));
   DevBuf list_buf((size_t)nf * sizeof(int32_t), ctx->stream);  // current failures -> original query index
   FC_CUDA(cudaMemcpyAsync(list_buf.p, fl.p, (size_t)nf * sizeof(int32_t), cudaMemcpyDeviceToDevice, ctx->stream));
   int n_left = nf;
-  int prev = kp;
-  for (int level = 0; level < 2 && !tier2_off && n_left > 0; ++level) {
-    const int want = std::min(kp2_cap, level == 0 ? kp + 32 : KP2_MAX);
+  int prev = tier1_i8 ? 0 : kp;
+  if (tier1_i8 && !tier2_off) {
+    std::lock_guard<std::mutex> pl(ix->plan_mu);
+    if (!ix->plan[kind].valid || ix->plan[kind].n_rows != ix->n)
+      approx_plan(ix->plan[kind], ix->rowsb[kind], ix->n, dim, ctx->sm_count);
+  }
+  for (int level = tier1_i8 ? -1 : 0; level < 2 && !tier2_off && n_left > 0; ++level) {
+    const int want = level < 0 ? kp : std::min(kp2_cap, level == 0 ? kp + 32 : KP2_MAX);
     if (want <= prev || k > want) break;
     DevBuf q2((size_t)n_left * dim * sizeof(float), ctx->stream);
     k_gather_queries<<<grid_for((int64_t)n_left * dim, 256), 256, 0, ctx->stream>>>(Qdev, list_buf.as<int32_t>(), n_left,
@@ -693,6 +1068,8 @@ void query_dev(lc_index* ix, int kind, const float* Qdev, int nq, int k, uint64_
       count_launch(ctx);
       FC_CUDA(cudaMemcpyAsync(list_buf.p, nl.p, (size_t)nf2 * sizeof(int32_t), cudaMemcpyDeviceToDevice, ctx->stream));
     }
+    // a bf16 pass that left most of its queries uncertified: clustered rows
+    if (level < 0 && nf2 > 8 && nf2 * 16 > nq) tier2_off = true;
     n_left = nf2;
   }
   if (n_left > 0) {
@@ -734,6 +1111,9 @@ lc_status lc_index_create(lc_ctx* ctx, int dim, int64_t capacity_rows, lc_index*
   auto* ix = new lc_index();
   ix->ctx = ctx;
   ix->dim = dim;
+  ix->i8 = dim > 0 && i8_wanted(dim);
+  if (const char* e = getenv("FC_LOOKUP_I8_KOUT")) ix->i8_kout = std::max(32, std::min(KI_MAX, atoi(e) / 32 * 32));
+  if (const char* e = getenv("FC_LOOKUP_I8_KUNIT")) ix->i8_kunit = std::max(8, std::min(64, atoi(e)));
   if (dim > 0 && capacity_rows > 0) {
     try {
       ensure_capacity(ix, capacity_rows);
@@ -754,6 +1134,9 @@ lc_status lc_index_destroy(lc_index* ix) {
   for (int t = 0; t < 3; ++t) {
     if (ix->rows[t]) cudaFree(ix->rows[t]);
     if (ix->rowsb[t]) cudaFree(ix->rowsb[t]);
+    if (ix->rows8[t]) cudaFree(ix->rows8[t]);
+    if (ix->tscale[t]) cudaFree(ix->tscale[t]);
+    if (ix->tres[t]) cudaFree(ix->tres[t]);
   }
   if (ix->ids_dev) cudaFree(ix->ids_dev);
   delete ix;
@@ -790,7 +1173,11 @@ lc_status lc_index_insert_batch(lc_index* ix, const uint64_t* prompts, const flo
   (void)src;
   double res[3];
   for (int t = 0; t < 3; ++t) res[t] = check_units_device(ctx, dsrc[t], n, dim);
-  if (ix->dim == 0) ix->dim = dim;
+  if (ix->dim == 0) {
+    ix->dim = dim;
+    // an index created with dim 0 has no storage yet: the int8 copy can start now
+    ix->i8 = i8_wanted(dim);
+  }
   for (int t = 0; t < 3; ++t) ix->dres[t] = std::max(ix->dres[t], res[t]);  // removals keep the max (conservative)
   ensure_capacity(ix, ix->n + n);
   for (int t = 0; t < 3; ++t) {
@@ -807,7 +1194,9 @@ lc_status lc_index_insert_batch(lc_index* ix, const uint64_t* prompts, const flo
     ix->slot[pid[i]] = ix->n + i;
     ix->ids.push_back(pid[i]);
   }
+  const int64_t n0 = ix->n;
   ix->n += n;
+  requantize(ix, n0 / 128, (ix->n + 127) / 128);
   sync(ctx);
   LC_API_END
 }
@@ -841,6 +1230,11 @@ lc_status lc_index_remove(lc_index* ix, uint64_t prompt) {
   ix->slot.erase(it);
   ix->n -= 1;
   for (int t = 0; t < 3; ++t) ix->plan[t].valid = false;
+  // the hole's tile got the last row; the last tile lost it
+  // the hole's slot now holds the last row: re-quantize its tile (the other
+  // rows of the last tile keep their valid quantization)
+  if (s != last) requantize(ix, s / 128, s / 128 + 1);
+  for (int t = 0; t < 3; ++t) ix->iplan[t].valid = false;
   sync(ctx);
   LC_API_END
 }

@@ -33,6 +33,43 @@ struct ApproxPlan {
   alignas(64) CUtensorMap tmap2;  // box [bn/2 rows][64] (CTA-pair kernel: each CTA loads half a tile)
 };
 
+// ---- int8 candidate stage (tier 1 for dim % 128 == 0) ----
+// Table rows are quantized per 128-row tile (the MMA tile): x = s_t * xq + dx
+// with s_t = max|x| over the tile / 127 and xq = rint(x / s_t) in [-127, 127];
+// queries per row: q = s_q * qq + dq. The s8 x s8 -> s32 tensor-core dot is
+// exact, so with a = s_q s_t (qq . xq) (real arithmetic):
+//   |q.x - a| = |dq.x + (s_q qq).dx| <= ||dq|| ||x|| + ||s_q qq|| ||dx||
+//            <= ||dq|| X + ||qhat|| R8
+// with X = max ||x|| <= 1 + 1e-6 (from_unit rule) and R8 = max over stored
+// rows of ||dx|| (computed exactly when a tile is quantized). Typical bound
+// for unit Gaussian-like 768-d rows: ~0.02 (bf16: ~0.004), which widens the
+// shortlist to ~100-200 rows per query (CPU study: scripts/int8_cert_study.py)
+// but runs the GEMM at the s8 tensor rate (2x bf16).
+struct I8Plan {
+  bool valid = false;
+  int64_t n_rows = 0;
+  int dim = 0;
+  const int8_t* rows = nullptr;   // [n][dim] quantized rows
+  const float* tscale = nullptr;  // [ceil(n/128)] tile scales
+  const float* tres = nullptr;    // [ceil(n/128)] max residual norm of the tile's rows (rounded up)
+  float r_typ = 0.f;              // median tile residual (threshold heuristic only)
+  alignas(64) CUtensorMap tmap;   // box [64 rows][128 B] (each CTA of the pair loads half a tile)
+};
+void i8_plan(I8Plan& p, const int8_t* rows, const float* tscale, const float* tres, int64_t n_rows, int dim,
+             float r_typ);
+// Quantize tiles [t0, t1) of an fp32 table of n_rows rows into rows8/tscale
+// (rows >= n_rows of the last tile become zero); each tile's max residual norm
+// ||dx|| (rounded up) goes to tres and is max-reduced into *res_bits.
+void i8_quantize_tiles(lc_ctx* ctx, const float* rows, int64_t n_rows, int dim, int64_t t0, int64_t t1, int8_t* rows8,
+                       float* tscale, float* tres, unsigned long long* res_bits);
+// Candidates of every query for a top-k: stored scores are U = a + eps_t, an
+// upper bound of the exact dot q.x of the row (eps_t = the row's tile bound).
+// Each unit keeps <= kp_unit rows, the merge the kout best U. cand_m[q] = an
+// upper bound of U for EVERY row outside the output list (the max drop level
+// of the units and the merge cut): rows outside have exact <= cand_m[q].
+void i8_shortlist(lc_ctx* ctx, const I8Plan& p, const float* Qdev, int nq, int k, int kp_unit, int kout, float* cand_s,
+                  uint32_t* cand_r, int32_t* cand_n, float* cand_m);
+
 bool approx_available();
 void approx_plan(ApproxPlan& p, const __nv_bfloat16* rows_bf16, int64_t n_rows, int dim, int sm_count);
 // Shortlist: for each query the kp rows with the largest bf16 scores

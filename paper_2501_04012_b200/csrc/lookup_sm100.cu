@@ -192,16 +192,18 @@ __device__ __forceinline__ void hist_publish(uint32_t* h, const uint32_t* lk, in
     atomicAdd(h + HC + (bk - 1) / BPO, 1u);
   }
 }
-// Raise tau to the lower edge of the highest bucket B with sum_{b>=B} h[b] >= kp.
+// Raise tau to (the lower edge of the highest bucket B with sum_{b>=B} h[b] >= kp) - off.
 // Two rounds of independent loads: the 9 octave counters, then the BPO fine
 // buckets of the octave where the running count from the top reaches kp.
-__device__ __forceinline__ void hist_refresh(const uint32_t* h, int kp, float& tau) {
+// (bf16 tier: off = 0, kp = K'; int8 tier: kp = k and off = the query's
+// typical error bound plus a slack, see k_shortlist_pair)
+__device__ __forceinline__ void hist_refresh(const uint32_t* h, int kp, float& tau, float off = 0.f) {
   const uint4* hc = reinterpret_cast<const uint4*>(h + HC);
   const uint4 c0 = __ldcg(hc), c1 = __ldcg(hc + 1), c2 = __ldcg(hc + 2);
   const uint32_t oc[9] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w, c2.x};
   int sum = (int)oc[8];
   if (sum >= kp) {
-    if (1.0f > tau) tau = 1.0f;
+    if (1.0f - off > tau) tau = 1.0f - off;
     return;
   }
   int o = 7;
@@ -210,7 +212,7 @@ __device__ __forceinline__ void hist_refresh(const uint32_t* h, int kp, float& t
     sum += (int)oc[o];
   }
   if (o < 0) return;
-  if (hedge(1 + o * BPO + BPO - 1) <= tau) return;  // nothing in reach above tau
+  if (hedge(1 + o * BPO + BPO - 1) - off <= tau) return;  // nothing in reach above tau
   // fine bucket 1 + o*BPO + jj lives at word o*BPO + 1 + jj; load words o*BPO .. o*BPO + BPO + 3
   const uint4* hv = reinterpret_cast<const uint4*>(h + o * BPO);
   uint4 x[BPO / 4 + 1];
@@ -228,7 +230,7 @@ __device__ __forceinline__ void hist_refresh(const uint32_t* h, int kp, float& t
   for (int jj = BPO - 1; jj >= 0; --jj) {
     sum += (int)f[1 + jj];
     if (sum >= kp) {
-      const float e = hedge(1 + o * BPO + jj);
+      const float e = hedge(1 + o * BPO + jj) - off;
       if (e > tau) tau = e;
       return;
     }
@@ -236,7 +238,7 @@ __device__ __forceinline__ void hist_refresh(const uint32_t* h, int kp, float& t
 }
 
 struct Params {
-  const __nv_bfloat16* Qb;  // [nq_pad][dim]
+  const __nv_bfloat16* Qb;  // [nq_pad][dim] (int8 kernel: const int8_t*)
   int nq;                    // real queries
   int n_qtiles;
   int dim;
@@ -255,6 +257,15 @@ struct Params {
   int nstage;
   uint32_t* part_k;          // [nq][n_splits][kp] packed candidates (hkey_ru(score) << 16 | row - r0)
   int32_t* part_n;           // [nq][n_splits]
+  // int8 kernel only
+  int kh;                    // histogram threshold target (int8: k, the top-k size); bf16: = kp
+  const float* tscale;       // [tiles] per-128-row tile scale s_t
+  const float* tres;         // [tiles] max ||x - s_t xq|| over the tile's rows (rounded up)
+  const float* qscale;       // [nq_pad] per-query scale s_q
+  const float2* qerr;        // [nq_pad] (||dq|| X, ||qhat||) rounded up; padding queries (0, 0)
+  float r_typ;               // typical tile residual (median of tres): threshold offset
+  float slack;               // threshold offset slack (actual vs bounded error, bucket width)
+  float* part_d;             // [nq][lists] drop level: every row the unit rejected or dropped has U <= it
 };
 
 constexpr int MAX_STAGE = 24;
@@ -515,6 +526,27 @@ __device__ __forceinline__ void mma_box4_pair_ss(uint32_t d_tmem, uint64_t a_des
       : "memory");
 }
 
+// int8 kernel: the largest integer dot that is rejected at threshold tau for a
+// (query, tile) with fp32 scale product sqt = fl(s_q * s_t). Rejecting
+// dot <= thr guarantees a = s_q s_t dot <= tau in real arithmetic: the fp32
+// division and the product rounding (<= 2^-24 each) are covered by the 2^-20
+// pull toward -inf. tau = -inf (nothing rejected yet) gives INT_MIN.
+__device__ __forceinline__ int i8_thr(float tau, float sqt) {
+  if (!(tau > -INFINITY)) return INT_MIN;
+  const float t = __fdiv_rn(tau, sqt);
+  const float c = t * (t > 0.f ? (1.f - 0x1p-20f) : (1.f + 0x1p-20f));
+  if (c >= 2147483520.f) return INT_MAX;
+  if (c <= -2147483520.f) return INT_MIN;
+  return (int)floorf(c);
+}
+// stored score of an accepted int8 dot: fp32 value rounded up past the
+// rounding of fl(s_q s_t) * dot (<= 2^-23 relative), so hkey_ru() of it is an
+// upper bound of a
+__device__ __forceinline__ float i8_score_up(int dot, float sqt) {
+  const float a = (float)dot * sqt;
+  return a + fabsf(a) * 0x1p-20f;
+}
+
 // Pair kernel warps: 0 TMA producer, 1 MMA issuer, 2..9 epilogue. Two
 // epilogue warps share each TMEM lane quarter (a warp may only read lanes
 // 32 * (warp % 4) ..): warp half h = (warp - 2) / 4 filters accumulator
@@ -524,13 +556,19 @@ __device__ __forceinline__ void mma_box4_pair_ss(uint32_t d_tmem, uint64_t a_des
 constexpr int PAIR_THREADS = 320;
 constexpr int EPI_HALF_COLS = PN / 2;
 
+// I8: kind::i8 tier (s8 table tile x s8 queries -> s32 accumulators): every
+// query K box (128 int8) lives in TMEM (dim <= 1024), the epilogue filters the
+// exact integer dots against a per-(query, tile) integer threshold and stores
+// rounded-up fp32 scores; each unit reports its drop level (final tau).
+template <bool I8>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
     k_shortlist_pair(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmQ, Params p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int NSTAGE = p.nstage;
   const int cap = p.cap;
-  const int nkb = p.dim / BK;
+  constexpr int BKE = I8 ? 128 : BK;  // K elements per 128-byte box
+  const int nkb = p.dim / BKE;
   const int KT = nkb < 8 ? nkb : 8;  // A boxes resident in TMEM
   const int KS = nkb - KT;           // A boxes resident in smem
   const int BPS = p.bps;             // B boxes per pipeline stage (one barrier round trip per 4*BPS MMAs)
@@ -595,7 +633,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
           } else {
             if (leader) mbar_expect_tx(smem_u32(aready), 2 * KS * ABOX);
             for (int j = 0; j < KS; ++j)
-              tma_load_2d_pair(smem_u32(asmem + j * ABOX), &tmQ, smem_u32(aready), (KT + j) * BK,
+              tma_load_2d_pair(smem_u32(asmem + j * ABOX), &tmQ, smem_u32(aready), (KT + j) * BKE,
                                qtile * 2 * BM + (int)rank * BM);
           }
         }
@@ -608,7 +646,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
               if (leader) mbar_expect_tx(smem_u32(&full[stage]), 2 * STAGE_BYTES);
               for (int bx = 0; bx < BPS; ++bx)
                 tma_load_2d_pair(smem_u32(stages + stage * STAGE_BYTES + bx * PBOX), &tmB, smem_u32(&full[stage]),
-                                 (sg * BPS + bx) * BK, (int)(row + rank * PHB));
+                                 (sg * BPS + bx) * BKE, (int)(row + rank * PHB));
             }
             if (++stage == NSTAGE) {
               stage = 0;
@@ -624,8 +662,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
     // The whole warp runs the loop (warp-uniform state stays in uniform
     // registers); one elected lane issues the MMAs and commits.
     if (leader) {
-      const uint32_t idesc =
-          (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(PN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+      // D f32 (bf16) or s32 (i8: c_format 2, A/B signed 8-bit), K-major, M=256, N=PN
+      const uint32_t idesc = ((I8 ? 2u : 1u) << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(PN >> 3) << 17) |
+                             ((uint32_t)(256 >> 4) << 24);
       const bool issuer = elect_one();
       int stage = 0;
       uint32_t phase = 0, tile = 0, unit_i = 0;
@@ -664,7 +703,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
                 const int kb = sg * BPS + bx;
                 const uint64_t bdesc = smem_desc_sw128(smem_u32(stages + stage * STAGE_BYTES + bx * PBOX));
                 if (p.debug & 1) continue;
-                if (kb < KT)
+                if (I8)
+                  mma_box4_pair_i8(d_tmem, tmem + kb * 32, bdesc, idesc, kb != 0);
+                else if (kb < KT)
                   mma_box4_pair(d_tmem, tmem + kb * (BK / 16) * 8, bdesc, idesc, kb != 0);
                 else
                   mma_box4_pair_ss(d_tmem, smem_desc_sw128(smem_u32(asmem + (kb - KT) * ABOX)), bdesc, idesc, 1);
@@ -705,7 +746,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
       {  // (1) this unit's query row -> TMEM columns [0, 32*KT), once the previous unit's MMAs are done
         mbar_wait(smem_u32(afree), (unit_i & 1) ^ 1);
         tc_fence_after();
-        const uint4* src = reinterpret_cast<const uint4*>(p.Qb + (size_t)q * p.dim);
+        const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(p.Qb) +
+                                                          (size_t)q * p.dim * (I8 ? 1 : 2));
         for (int kb = half; kb < KT; kb += 2) {  // the two warps of a quarter split the boxes
           uint32_t r[32];
 #pragma unroll
@@ -727,7 +769,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
       int cnt = 0, pub = 0;  // entries [pub, cnt) not yet counted in the histogram
       float tau = -INFINITY;
       uint32_t* hq = p.hist + (size_t)q * HSTRIDE;
-      hist_refresh(hq, p.kp, tau);
+      // int8: s_q and the error terms of this thread's query (padding: 1, (0, 0));
+      // the unit filters and stores U = a + eps_t, an upper bound of the exact
+      // score (eps_t = ||dq|| X + ||qhat|| R_t, the tile's bound, lookup.cuh),
+      // and raises tau to (k-th best U seen) - (typical eps + slack): rows
+      // with U below that are almost surely below the k-th exact score (the
+      // certificate, not this heuristic, decides; a too-high tau only sends
+      // the query to the bf16 tier)
+      const float qsc = I8 ? __ldg(p.qscale + q) : 1.f;
+      const float2 qe = I8 ? __ldg(p.qerr + q) : make_float2(0.f, 0.f);
+      const float hoff = I8 ? __fmaf_ru(qe.y, p.r_typ, qe.x) + p.slack : 0.f;
+      hist_refresh(hq, p.kh, tau, hoff);
       // FC_SHORTLIST_DEBUG & 16: per-warp clock64 spans [accumulator wait, histogram, compaction, appends]
       long long cyc[4] = {0, 0, 0, 0}, c_t0 = 0;
       const bool prof = p.debug & 16;
@@ -738,9 +790,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
           if (prof) c_t0 = clock64();
           hist_publish(hq, lk, t, pub, cnt);
           pub = cnt;
-          hist_refresh(hq, p.kp, tau);
+          hist_refresh(hq, p.kh, tau, hoff);
           if (prof) cyc[1] += clock64() - c_t0;
         }
+        // int8: this tile's scale product, error bound and integer threshold
+        // (reject a <= tau - eps_t, i.e. U <= tau)
+        const float sqt = I8 ? qsc * __ldg(p.tscale + (row >> 7)) : 1.f;
+        const float eps_t = I8 ? __fmaf_ru(qe.y, __ldg(p.tres + (row >> 7)), qe.x) : 0.f;
+        int thr = I8 ? i8_thr(__fsub_rd(tau, eps_t), sqt) : 0;
         if (prof) c_t0 = clock64();
         mbar_wait(smem_u32(&accf[b]), use & 1);
         tc_fence_after();
@@ -768,17 +825,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
         if (!(p.debug & 4)) {
 #pragma unroll
           for (int hh = 0; hh < EPI_HALF_COLS / 16; ++hh) {
-            float vc[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i) vc[i] = __uint_as_float(rv[hh * 16 + i]);
             const int c0 = hh * 16;
-            float a0 = fmaxf(vc[0], vc[1]), a1 = fmaxf(vc[2], vc[3]), a2 = fmaxf(vc[4], vc[5]), a3 = fmaxf(vc[6], vc[7]);
-            a0 = fmaxf(a0, fmaxf(vc[8], vc[9]));
-            a1 = fmaxf(a1, fmaxf(vc[10], vc[11]));
-            a2 = fmaxf(a2, fmaxf(vc[12], vc[13]));
-            a3 = fmaxf(a3, fmaxf(vc[14], vc[15]));
-            const float mx = fmaxf(fmaxf(a0, a1), fmaxf(a2, a3));
-            if (!__any_sync(0xffffffffu, (mx > tau) | (lim_all < EPI_HALF_COLS))) continue;
+            bool hot;
+            if constexpr (I8) {  // exact s32 dots: 3-input integer max tree
+              const int* vi = reinterpret_cast<const int*>(rv + c0);
+              int m0 = __vimax3_s32(vi[0], vi[1], vi[2]), m1 = __vimax3_s32(vi[3], vi[4], vi[5]);
+              int m2 = __vimax3_s32(vi[6], vi[7], vi[8]), m3 = __vimax3_s32(vi[9], vi[10], vi[11]);
+              int m4 = __vimax3_s32(vi[12], vi[13], vi[14]);
+              m0 = __vimax3_s32(m0, m1, m2);
+              m3 = __vimax3_s32(m3, m4, vi[15]);
+              hot = max(m0, m3) > thr;
+            } else {
+              float vc[16];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) vc[i] = __uint_as_float(rv[c0 + i]);
+              float a0 = fmaxf(vc[0], vc[1]), a1 = fmaxf(vc[2], vc[3]), a2 = fmaxf(vc[4], vc[5]), a3 = fmaxf(vc[6], vc[7]);
+              a0 = fmaxf(a0, fmaxf(vc[8], vc[9]));
+              a1 = fmaxf(a1, fmaxf(vc[10], vc[11]));
+              a2 = fmaxf(a2, fmaxf(vc[12], vc[13]));
+              a3 = fmaxf(a3, fmaxf(vc[14], vc[15]));
+              hot = fmaxf(fmaxf(a0, a1), fmaxf(a2, a3)) > tau;
+            }
+            if (!__any_sync(0xffffffffu, hot | (lim_all < EPI_HALF_COLS))) continue;
             if (p.debug & 32) continue;  // diagnostic: fast path only
             if ((p.debug & 16) && lane == 0) atomicAdd(p.stats + 0, 1u);
             if (__any_sync(0xffffffffu, cnt + 16 > cap)) {
@@ -787,14 +855,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
               hist_publish(hq, lk, t, pub, cnt);  // count before compaction may drop entries
               compact_keys(lk, t, cnt, p.kp, tau, false);
               pub = cnt;
+              if (I8) thr = i8_thr(__fsub_rd(tau, eps_t), sqt);
               if (prof) cyc[2] += clock64() - c_t0;
             }
             if (prof) c_t0 = clock64();
             const uint32_t off0 = off_base + (uint32_t)c0;
 #pragma unroll
             for (int jj = 0; jj < 16; ++jj) {
-              const bool acc = (c0 + jj < lim_all) & (vc[jj] > tau);
-              if (acc) lk[cnt * BM + t] = (hkey_ru(vc[jj]) << 16) | (off0 + jj);
+              bool acc;
+              float v;
+              if constexpr (I8) {
+                const int d = (int)rv[c0 + jj];
+                acc = (c0 + jj < lim_all) & (d > thr);
+                v = __fadd_ru(i8_score_up(d, sqt), eps_t);
+              } else {
+                v = __uint_as_float(rv[c0 + jj]);
+                acc = (c0 + jj < lim_all) & (v > tau);
+              }
+              if (acc) lk[cnt * BM + t] = (hkey_ru(v) << 16) | (off0 + jj);
               cnt += acc;
             }
             if (prof) cyc[3] += clock64() - c_t0;
@@ -815,6 +893,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
         const size_t o = ((size_t)q * 2 * p.n_splits + sub) * p.kp;
         for (int i = 0; i < cnt; ++i) p.part_k[o + i] = lk[i * BM + t];
         p.part_n[(size_t)q * 2 * p.n_splits + sub] = cnt;
+        // every row this list's unit rejected (a <= tau at the time) or
+        // compacted away (stored score <= the raised tau) has a <= final tau
+        if (I8) p.part_d[(size_t)q * 2 * p.n_splits + sub] = tau;
       }
     }
   }
@@ -857,10 +938,15 @@ __device__ __forceinline__ void emit(uint32_t key, uint32_t slot, int kp, int rp
   cr[at] = ((slot / (uint32_t)kp) >> rshift) * (uint32_t)rps + (key & 0xFFFFu);
 }
 
+// kout = output slots per query (kp for the bf16 tier; the int8 tier merges
+// short unit lists into a longer one). pd (int8 tier, else null): per-list
+// drop levels; cm[q] = max(drop levels, stored score at the merge cut), an
+// upper bound of the approximate score of every row outside q's output.
 __global__ void __launch_bounds__(MG_W * 32) k_shortlist_merge(const uint32_t* __restrict__ pk,
                                                                const int32_t* __restrict__ pn, int n_splits, int kp, int rps, int rshift,
-                                                               int nq, float* __restrict__ cs, uint32_t* __restrict__ cr,
-                                                               int32_t* __restrict__ cn, uint32_t* __restrict__ gkeys) {
+                                                               int nq, int kout, float* __restrict__ cs, uint32_t* __restrict__ cr,
+                                                               int32_t* __restrict__ cn, uint32_t* __restrict__ gkeys,
+                                                               const float* __restrict__ pd, float* __restrict__ cm) {
   extern __shared__ uint32_t s_key[];  // [warps][2][MG_CAP] (gkeys [nq][2][n_splits * kp] past that)
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = blockIdx.x * (blockDim.x >> 5) + w;
@@ -870,6 +956,12 @@ __global__ void __launch_bounds__(MG_W * 32) k_shortlist_merge(const uint32_t* _
   int n_all = 0;
   for (int s0 = lane; s0 < n_splits; s0 += 32) n_all += min(__ldg(pq + s0), kp);
   n_all = __reduce_add_sync(0xffffffffu, n_all);
+  float drop = -INFINITY;
+  if (pd) {
+    for (int s0 = lane; s0 < n_splits; s0 += 32) drop = fmaxf(drop, __ldg(pd + (size_t)q * n_splits + s0));
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) drop = fmaxf(drop, __shfl_xor_sync(0xffffffffu, drop, off));
+  }
   const int cap = n_all <= MG_CAP ? MG_CAP : total;
   uint32_t* key = n_all <= MG_CAP ? s_key + (size_t)w * 2 * MG_CAP : gkeys + (size_t)q * 2 * total;
   uint32_t* slot = key + cap;
@@ -898,17 +990,19 @@ __global__ void __launch_bounds__(MG_W * 32) k_shortlist_merge(const uint32_t* _
   }
   __syncwarp();
   uint32_t T = 1;  // keep everything non-empty
-  if (n_items > kp) {
+  if (n_items > kout) {
     uint32_t lo = 1, hi = 0xFFFFFFFFu;
     while (lo < hi) {
       const uint32_t mid = lo + (uint32_t)(((uint64_t)hi - lo + 1) >> 1);
       int c = 0;
       for (int i = lane; i < n_items; i += 32) c += key[i] >= mid;
       c = __reduce_add_sync(0xffffffffu, c);
-      if (c >= kp) lo = mid; else hi = mid - 1;
+      if (c >= kout) lo = mid; else hi = mid - 1;
     }
     T = lo;
+    drop = fmaxf(drop, hkey_float(T >> 16));  // cut entries have stored score <= that of T
   }
+  if (cm && lane == 0) cm[q] = drop;
   // strictly above T first (in slot order), then == T up to kp
   int out = 0;
   for (int i0 = 0; i0 < n_items; i0 += 32) {
@@ -917,21 +1011,21 @@ __global__ void __launch_bounds__(MG_W * 32) k_shortlist_merge(const uint32_t* _
     const unsigned bal = __ballot_sync(0xffffffffu, take);
     if (take) {
       const int at = out + __popc(bal & ((1u << lane) - 1));
-      emit(key[i], slot[i], kp, rps, rshift, cs, cr, (size_t)q * kp + at);
+      emit(key[i], slot[i], kp, rps, rshift, cs, cr, (size_t)q * kout + at);
     }
     out += __popc(bal);
   }
-  for (int i0 = 0; i0 < n_items && out < kp; i0 += 32) {
+  for (int i0 = 0; i0 < n_items && out < kout; i0 += 32) {
     const int i = i0 + lane;
     const bool take = i < n_items && key[i] == T;
     const unsigned bal = __ballot_sync(0xffffffffu, take);
     if (take) {
       const int at = out + __popc(bal & ((1u << lane) - 1));
-      if (at < kp) emit(key[i], slot[i], kp, rps, rshift, cs, cr, (size_t)q * kp + at);
+      if (at < kout) emit(key[i], slot[i], kp, rps, rshift, cs, cr, (size_t)q * kout + at);
     }
     out += __popc(bal);
   }
-  if (lane == 0) cn[q] = min(kp, out);
+  if (lane == 0) cn[q] = min(kout, out);
 }
 
 // Same selection as k_shortlist_merge with one CTA per query (MC_T threads):
@@ -967,8 +1061,9 @@ __device__ __forceinline__ int block_scan(bool flag, int* red, int* pre) {
 }
 __global__ void __launch_bounds__(MC_T) k_shortlist_merge_cta(const uint32_t* __restrict__ pk,
                                                               const int32_t* __restrict__ pn, int n_splits, int kp, int rps, int rshift,
-                                                              float* __restrict__ cs, uint32_t* __restrict__ cr,
-                                                              int32_t* __restrict__ cn) {
+                                                              int kout, float* __restrict__ cs, uint32_t* __restrict__ cr,
+                                                              int32_t* __restrict__ cn, const float* __restrict__ pd,
+                                                              float* __restrict__ cm) {
   extern __shared__ uint32_t s_key[];  // [2][n_splits * kp]
   __shared__ int red[MC_T / 32];
   const int q = blockIdx.x;
@@ -994,28 +1089,34 @@ __global__ void __launch_bounds__(MC_T) k_shortlist_merge_cta(const uint32_t* __
   }
   __syncthreads();
   uint32_t T = 1;
-  if (n_items > kp) {
+  if (n_items > kout) {
     uint32_t lo = 1, hi = 0xFFFFFFFFu;
     while (lo < hi) {
       const uint32_t mid = lo + (uint32_t)(((uint64_t)hi - lo + 1) >> 1);
       int c = 0;
       for (int i = threadIdx.x; i < n_items; i += MC_T) c += key[i] >= mid;
       c = block_sum(c, red);
-      if (c >= kp) lo = mid; else hi = mid - 1;
+      if (c >= kout) lo = mid; else hi = mid - 1;
     }
     T = lo;
   }
+  if (cm && threadIdx.x == 0) {
+    float drop = n_items > kout ? hkey_float(T >> 16) : -INFINITY;
+    if (pd)
+      for (int s0 = 0; s0 < n_splits; ++s0) drop = fmaxf(drop, pd[(size_t)q * n_splits + s0]);
+    cm[q] = drop;
+  }
   int out = 0;
   for (int pass = 0; pass < 2; ++pass)
-    for (int i0 = 0; i0 < n_items && out < kp; i0 += MC_T) {
+    for (int i0 = 0; i0 < n_items && out < kout; i0 += MC_T) {
       const int i = i0 + threadIdx.x;
       const bool take = i < n_items && (pass == 0 ? key[i] > T : key[i] == T);
       int pre;
       const int tot = block_scan(take, red, &pre);
-      if (take && out + pre < kp) emit(key[i], slot[i], kp, rps, rshift, cs, cr, (size_t)q * kp + out + pre);
+      if (take && out + pre < kout) emit(key[i], slot[i], kp, rps, rshift, cs, cr, (size_t)q * kout + out + pre);
       out += tot;
     }
-  if (threadIdx.x == 0) cn[q] = min(kp, out);
+  if (threadIdx.x == 0) cn[q] = min(kout, out);
 }
 
 }  // namespace sm100
@@ -1089,10 +1190,11 @@ static void launch_single(lc_ctx* ctx, const ApproxPlan& plan, sm100::Params prm
   FC_LAUNCH_CHECK();
 }
 
-static void launch_pair(lc_ctx* ctx, const ApproxPlan& plan, const CUtensorMap& tmQ, sm100::Params& prm) {
+template <bool I8>
+static void launch_pair(lc_ctx* ctx, const CUtensorMap& tmB, const CUtensorMap& tmQ, sm100::Params& prm) {
   using namespace sm100;
-  const int nkb = prm.dim / BK;
-  const int KS = nkb > 8 ? nkb - 8 : 0;
+  const int nkb = prm.dim / (I8 ? 128 : BK);
+  const int KS = !I8 && nkb > 8 ? nkb - 8 : 0;
   const size_t budget = 227 * 1024 - 1024 - 512;
   const size_t slot_bytes = (size_t)2 * BM * 4;  // one packed u32 per candidate, one list per column half
   const size_t fixed = (size_t)KS * ABOX;
@@ -1115,70 +1217,89 @@ static void launch_pair(lc_ctx* ctx, const ApproxPlan& plan, const CUtensorMap& 
   if (const char* e = getenv("FC_SHORTLIST_CAPMAX")) cap_max = std::max<int64_t>(min_cap, atoi(e));
   prm.cap = (int)std::min<int64_t>((budget - fixed - nstage * stage_bytes) / slot_bytes, cap_max);
   const size_t smem = 1024 + 512 + nstage * stage_bytes + fixed + (size_t)prm.cap * slot_bytes;
-  FC_CUDA(cudaFuncSetAttribute(k_shortlist_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  FC_CUDA(cudaFuncSetAttribute(k_shortlist_pair<I8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = 2 * std::min(prm.n_units, ctx->sm_count / 2);
   KTimer kt(ctx, g_shortlist_timer);
-  k_shortlist_pair<<<grid, PAIR_THREADS, smem, ctx->stream>>>(plan.tmap2, tmQ, prm);
+  k_shortlist_pair<I8><<<grid, PAIR_THREADS, smem, ctx->stream>>>(tmB, tmQ, prm);
   kt.stop();
   FC_LAUNCH_CHECK();
 }
 
 thread_local const char* g_shortlist_timer = "shortlist";
 
-void approx_shortlist(lc_ctx* ctx, const ApproxPlan& plan, const float* Qdev, int nq, int kp, float* cand_s,
-                      uint32_t* cand_r, int32_t* cand_n) {
+namespace {
+// One shortlist pass: work-unit split, candidate lists, the tcgen05 kernel,
+// the per-query merge. Qconv = converted queries [nq_pad][dim] (bf16 or s8).
+struct ShortlistRun {
+  bool i8 = false;
+  bool pair = true;
+  int dim = 0, nq = 0, nq_pad = 0, n_qtiles = 0, bn = 0;
+  int64_t n_rows = 0;
+  int kp = 0, kout = 0;
+  const void* Qconv = nullptr;
+  const ApproxPlan* bplan = nullptr;  // bf16 tier
+  const I8Plan* iplan = nullptr;      // int8 tier
+  const float* qscale = nullptr;
+  const float2* qerr = nullptr;
+  int k = 0;
+  float* cand_s = nullptr;
+  uint32_t* cand_r = nullptr;
+  int32_t* cand_n = nullptr;
+  float* cand_m = nullptr;
+};
+
+void run_shortlist(lc_ctx* ctx, const ShortlistRun& R) {
   using namespace sm100;
-  const int dim = plan.dim;
-  // a CTA pair's 256-query tile is mostly padding for a handful of queries
-  // (the tier-2 re-shortlist): the single-CTA kernel does half the MMA work
-  const bool pair = use_pair(dim) && nq > BM;
-  const int qt = pair ? 2 * BM : BM;  // queries per work unit
-  const int n_qtiles = (nq + qt - 1) / qt;
-  const int nq_pad = n_qtiles * qt;
-  DevBuf qb((size_t)nq_pad * dim * sizeof(__nv_bfloat16), ctx->stream);
-  k_q_to_bf16<<<grid_for((int64_t)nq_pad * dim, 256), 256, 0, ctx->stream>>>(Qdev, nq, dim, qb.as<__nv_bfloat16>(), nq_pad);
-  FC_LAUNCH_CHECK();
-  const int bn = pair ? PN : plan.bn;
-  const int64_t total_tiles = (plan.n_rows + bn - 1) / bn;
-  const int64_t workers = pair ? ctx->sm_count / 2 : ctx->sm_count;  // persistent CTAs / CTA pairs
+  const int nq = R.nq, kp = R.kp, bn = R.bn;
+  const int64_t total_tiles = (R.n_rows + bn - 1) / bn;
+  const int64_t workers = R.pair ? ctx->sm_count / 2 : ctx->sm_count;  // persistent CTAs / CTA pairs
   // ~16 units per persistent worker: shorter row ranges keep the query tiles
   // that share a range closer together in time, so the table is re-read from
   // L2 rather than HBM (ncu, 1M x 768 x 4096: 37 splits 3.63 GB DRAM per launch,
   // 74 splits 2.74 GB and 2.5 % faster; 148 splits cost more in the merge)
-  int64_t splits = std::max<int64_t>(1, (workers * 16 + n_qtiles - 1) / n_qtiles);
+  int64_t splits = std::max<int64_t>(1, (workers * 16 + R.n_qtiles - 1) / R.n_qtiles);
   splits = std::min<int64_t>(splits, std::max<int64_t>(1, total_tiles / 16));
   // keep one query's partial lists within the merge's shared memory (few queries)
-  splits = std::min<int64_t>(splits, std::max<int64_t>(workers, (200 * 1024) / ((int64_t)kp * 8 * (pair ? 2 : 1))));
+  splits = std::min<int64_t>(splits, std::max<int64_t>(workers, (200 * 1024) / ((int64_t)kp * 8 * (R.pair ? 2 : 1))));
   // packed candidates carry the row offset in 16 bits
   splits = std::max<int64_t>(splits, (total_tiles * bn + 65535) / 65536);
   const int64_t tiles_per_split = std::min<int64_t>((total_tiles + splits - 1) / splits, 65536 / bn);
   splits = (total_tiles + tiles_per_split - 1) / tiles_per_split;
   Params prm;
-  prm.Qb = qb.as<__nv_bfloat16>();
+  prm.Qb = reinterpret_cast<const __nv_bfloat16*>(R.Qconv);
   prm.nq = nq;
-  prm.n_qtiles = n_qtiles;
-  prm.dim = dim;
-  prm.n_rows = plan.n_rows;
+  prm.n_qtiles = R.n_qtiles;
+  prm.dim = R.dim;
+  prm.n_rows = R.n_rows;
   prm.rows_per_split = (int)(tiles_per_split * bn);
   prm.n_splits = (int)splits;
-  prm.n_units = (int)(splits * n_qtiles);
+  prm.n_units = (int)(splits * R.n_qtiles);
   prm.kp = kp;
+  prm.kh = R.i8 ? R.k : kp;
+  prm.tscale = R.i8 ? R.iplan->tscale : nullptr;
+  prm.tres = R.i8 ? R.iplan->tres : nullptr;
+  prm.qscale = R.qscale;
+  prm.qerr = R.qerr;
+  prm.r_typ = R.i8 ? R.iplan->r_typ : 0.f;
+  prm.slack = 0.0015f;
+  if (const char* e = getenv("FC_LOOKUP_I8_SLACK")) prm.slack = (float)atof(e);
   {
     const char* dbg = getenv("FC_SHORTLIST_DEBUG");
     prm.debug = dbg ? atoi(dbg) : 0;
   }
   // candidate lists per query: one per row range (single-CTA kernel) or one
   // per row range and epilogue column half (pair kernel)
-  const int rshift = pair ? 1 : 0;
+  const int rshift = R.pair ? 1 : 0;
   const int64_t lists = splits << rshift;
   DevBuf pk((size_t)nq * lists * kp * sizeof(uint32_t), ctx->stream);
   DevBuf pn((size_t)nq * lists * sizeof(int32_t), ctx->stream);
-  DevBuf gk((size_t)nq_pad * sizeof(uint32_t), ctx->stream);
+  DevBuf pd(R.i8 ? (size_t)nq * lists * sizeof(float) : 16, ctx->stream);
+  DevBuf gk((size_t)R.nq_pad * sizeof(uint32_t), ctx->stream);
   FC_CUDA(cudaMemsetAsync(gk.p, 0, gk.bytes, ctx->stream));
   DevBuf st(96, ctx->stream);  // u32 [0,4): counters; u64 [2,6): epilogue cycle spans; u64 [6,9): MMA waits
   FC_CUDA(cudaMemsetAsync(st.p, 0, 96, ctx->stream));
-  DevBuf hist(pair ? (size_t)nq_pad * HSTRIDE * sizeof(uint32_t) : 16, ctx->stream);
-  if (pair) FC_CUDA(cudaMemsetAsync(hist.p, 0, hist.bytes, ctx->stream));
+  DevBuf hist(R.pair ? (size_t)R.nq_pad * HSTRIDE * sizeof(uint32_t) : 16, ctx->stream);
+  if (R.pair) FC_CUDA(cudaMemsetAsync(hist.p, 0, hist.bytes, ctx->stream));
   prm.hist = hist.as<uint32_t>();
   {
     const char* e = getenv("FC_SHORTLIST_REFRESH");
@@ -1188,14 +1309,19 @@ void approx_shortlist(lc_ctx* ctx, const ApproxPlan& plan, const float* Qdev, in
   prm.gkey = gk.as<uint32_t>();
   prm.part_k = pk.as<uint32_t>();
   prm.part_n = pn.as<int32_t>();
-  if (pair) {
+  prm.part_d = R.i8 ? pd.as<float>() : nullptr;
+  if (R.i8) {
+    alignas(64) CUtensorMap unused;
+    memset(&unused, 0, sizeof unused);
+    launch_pair<true>(ctx, R.iplan->tmap, unused, prm);
+  } else if (R.pair) {
     alignas(64) CUtensorMap tmQ;
-    encode_2d(&tmQ, qb.as<__nv_bfloat16>(), nq_pad, dim, BM);  // smem-resident query boxes [128 q][64]
-    launch_pair(ctx, plan, tmQ, prm);
+    encode_2d(&tmQ, reinterpret_cast<const __nv_bfloat16*>(R.Qconv), R.nq_pad, R.dim, BM);  // smem-resident query boxes [128 q][64]
+    launch_pair<false>(ctx, R.bplan->tmap2, tmQ, prm);
   } else if (bn == 64) {
-    launch_single<64>(ctx, plan, prm);
+    launch_single<64>(ctx, *R.bplan, prm);
   } else {
-    launch_single<128>(ctx, plan, prm);
+    launch_single<128>(ctx, *R.bplan, prm);
   }
   if (prm.debug & 16) {
     uint32_t h[24];
@@ -1205,13 +1331,14 @@ void approx_shortlist(lc_ctx* ctx, const ApproxPlan& plan, const float* Qdev, in
     memcpy(cy, h + 4, sizeof cy);
     memcpy(mc, h + 12, sizeof mc);
     const double wt = (double)std::max(1u, h[2]);  // warp-tiles
-    fprintf(stderr, "shortlist stats: warp-tiles %u slow-chunks %u (%.3f/tile) compactions %u (%.4f/tile) nstage %d bps %d cap %d splits %d"
+    fprintf(stderr, "shortlist%s stats: warp-tiles %u slow-chunks %u (%.3f/tile) compactions %u (%.4f/tile) nstage %d bps %d cap %d splits %d"
             " | cycles per warp-tile: acc-wait %.0f hist %.0f compact %.0f append %.0f"
             " | MMA cycles per tile: acc-free wait %.0f data wait %.0f A wait %.0f\n",
-            h[2], h[0], h[0] / wt, h[1], h[1] / wt, prm.nstage, prm.bps, prm.cap, prm.n_splits, cy[0] / wt, cy[1] / wt,
-            cy[2] / wt, cy[3] / wt, mc[0] * 16.0 / wt, mc[1] * 16.0 / wt, mc[2] * 16.0 / wt);
+            R.i8 ? "[i8]" : "", h[2], h[0], h[0] / wt, h[1], h[1] / wt, prm.nstage, prm.bps, prm.cap, prm.n_splits,
+            cy[0] / wt, cy[1] / wt, cy[2] / wt, cy[3] / wt, mc[0] * 16.0 / wt, mc[1] * 16.0 / wt, mc[2] * 16.0 / wt);
   }
   const size_t per_warp = (size_t)lists * kp * 2 * sizeof(uint32_t);  // keys + slots
+  const float* pdp = R.i8 ? pd.as<float>() : nullptr;
   KTimer kmt(ctx, "shortlist_merge");
   if (nq < ctx->sm_count && per_warp <= 200 * 1024) {
     static std::atomic<uint64_t> attr_set{0};  // per-device bit: the attribute is per device
@@ -1220,7 +1347,8 @@ void approx_shortlist(lc_ctx* ctx, const ApproxPlan& plan, const float* Qdev, in
       attr_set.fetch_or(1ull << (ctx->device & 63));
     }
     k_shortlist_merge_cta<<<nq, MC_T, per_warp, ctx->stream>>>(pk.as<uint32_t>(), pn.as<int32_t>(), (int)lists, kp,
-                                                               prm.rows_per_split, rshift, cand_s, cand_r, cand_n);
+                                                               prm.rows_per_split, rshift, R.kout, R.cand_s, R.cand_r,
+                                                               R.cand_n, pdp, R.cand_m);
     FC_LAUNCH_CHECK();
     count_launch(ctx, 3);
     return;
@@ -1235,10 +1363,208 @@ void approx_shortlist(lc_ctx* ctx, const ApproxPlan& plan, const float* Qdev, in
     attr_set2.fetch_or(1ull << (ctx->device & 63));
   }
   k_shortlist_merge<<<(nq + MG_W - 1) / MG_W, MG_W * 32, msmem, ctx->stream>>>(
-      pk.as<uint32_t>(), pn.as<int32_t>(), (int)lists, kp, prm.rows_per_split, rshift, nq, cand_s, cand_r, cand_n,
-      gkeys.as<uint32_t>());
+      pk.as<uint32_t>(), pn.as<int32_t>(), (int)lists, kp, prm.rows_per_split, rshift, nq, R.kout, R.cand_s, R.cand_r,
+      R.cand_n, gkeys.as<uint32_t>(), pdp, R.cand_m);
   FC_LAUNCH_CHECK();
   count_launch(ctx, 3);
+}
+}  // namespace
+
+void approx_shortlist(lc_ctx* ctx, const ApproxPlan& plan, const float* Qdev, int nq, int kp, float* cand_s,
+                      uint32_t* cand_r, int32_t* cand_n) {
+  using namespace sm100;
+  const int dim = plan.dim;
+  // a CTA pair's 256-query tile is mostly padding for a handful of queries
+  // (the tier-2 re-shortlist): the single-CTA kernel does half the MMA work
+  const bool pair = use_pair(dim) && nq > BM;
+  const int qt = pair ? 2 * BM : BM;  // queries per work unit
+  ShortlistRun R;
+  R.pair = pair;
+  R.dim = dim;
+  R.nq = nq;
+  R.n_qtiles = (nq + qt - 1) / qt;
+  R.nq_pad = R.n_qtiles * qt;
+  R.bn = pair ? PN : plan.bn;
+  R.n_rows = plan.n_rows;
+  R.kp = R.kout = kp;
+  R.bplan = &plan;
+  DevBuf qb((size_t)R.nq_pad * dim * sizeof(__nv_bfloat16), ctx->stream);
+  k_q_to_bf16<<<grid_for((int64_t)R.nq_pad * dim, 256), 256, 0, ctx->stream>>>(Qdev, nq, dim, qb.as<__nv_bfloat16>(), R.nq_pad);
+  FC_LAUNCH_CHECK();
+  R.Qconv = qb.p;
+  R.cand_s = cand_s;
+  R.cand_r = cand_r;
+  R.cand_n = cand_n;
+  run_shortlist(ctx, R);
+}
+
+// ---------------------------------------------------------------------------
+// int8 tier
+// ---------------------------------------------------------------------------
+namespace sm100 {
+// Per query (one warp): s_q = max|q| / 127 (1 for an all-zero row), qq =
+// rint(q / s_q) clamped to [-127, 127], and the exact fp64 norms of dq = q -
+// s_q qq and qhat = s_q qq (each product s_q * qq is exact in fp64), rounded
+// up by 2^-40 (far above the fp64 summation error of <= 1024 terms).
+__global__ void k_q_to_i8(const float* __restrict__ Q, int nq, int dim, int nq_pad, int8_t* __restrict__ Qi,
+                          float* __restrict__ qscale, float2* __restrict__ qerr) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= nq_pad) return;
+  int8_t* dst = Qi + (size_t)w * dim;
+  if (w >= nq) {
+    for (int d = lane; d < dim; d += 32) dst[d] = 0;
+    if (lane == 0) {
+      qscale[w] = 1.f;
+      qerr[w] = make_float2(0.f, 0.f);
+    }
+    return;
+  }
+  const float* x = Q + (size_t)w * dim;
+  float amax = 0.f;
+  for (int d = lane; d < dim; d += 32) amax = fmaxf(amax, fabsf(x[d]));
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, off));
+  const float sc = amax > 0.f && amax < INFINITY ? amax / 127.f : 1.f;
+  double e2 = 0.0, h2 = 0.0;
+  for (int d = lane; d < dim; d += 32) {
+    float r = rintf(__fdiv_rn(x[d], sc));
+    r = fminf(127.f, fmaxf(-127.f, r));
+    dst[d] = (int8_t)(int)r;
+    const double qh = (double)sc * (double)r;
+    const double e = (double)x[d] - qh;
+    e2 = fma(e, e, e2);
+    h2 = fma(qh, qh, h2);
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    e2 += __shfl_xor_sync(0xffffffffu, e2, off);
+    h2 += __shfl_xor_sync(0xffffffffu, h2, off);
+  }
+  if (lane == 0) {
+    qscale[w] = sc;
+    // (||dq|| X, ||qhat||) with X = 1 + 1e-6 >= ||x|| for stored rows (from_unit),
+    // rounded up to fp32; a non-finite query gives non-finite bounds (rejected later)
+    qerr[w] = make_float2(__double2float_ru(sqrt(e2) * (1.0 + 1e-6) * (1.0 + 0x1p-40)),
+                          __double2float_ru(sqrt(h2) * (1.0 + 0x1p-40)));
+  }
+}
+
+// One CTA per 128-row tile: s_t = max|x| / 127 over the tile's live rows,
+// xq = rint(x / s_t) clamped, the row residual norms ||x - s_t xq|| (exact
+// fp64 terms) max-reduced into *res_bits. Rows >= n_rows become zero.
+constexpr int QT_T = 256;
+__global__ void __launch_bounds__(QT_T) k_quant_tiles(const float* __restrict__ rows, int64_t n_rows, int dim, int64_t t0,
+                                                      int8_t* __restrict__ rows8, float* __restrict__ tscale,
+                                                      float* __restrict__ tres, unsigned long long* __restrict__ res_bits) {
+  const int64_t tile = t0 + blockIdx.x;
+  const int64_t r0 = tile * 128;
+  const int64_t r1 = min(n_rows, r0 + 128);
+  __shared__ float red[QT_T / 32];
+  float amax = 0.f;
+  const int64_t live = (r1 - r0) * dim;
+  const float* base = rows + r0 * dim;
+  for (int64_t i = threadIdx.x; i < live; i += QT_T) amax = fmaxf(amax, fabsf(base[i]));
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, off));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = amax;
+  __syncthreads();
+  amax = 0.f;
+  for (int i = 0; i < QT_T / 32; ++i) amax = fmaxf(amax, red[i]);
+  const float sc = amax > 0.f && amax < INFINITY ? amax / 127.f : 1.f;
+  if (threadIdx.x == 0) tscale[tile] = sc;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double worst = 0.0;
+  for (int64_t r = r0 + w; r < r0 + 128; r += QT_T / 32) {
+    int8_t* dst = rows8 + r * dim;
+    if (r >= n_rows) {
+      for (int d = lane; d < dim; d += 32) dst[d] = 0;
+      continue;
+    }
+    const float* x = rows + r * dim;
+    double e2 = 0.0;
+    for (int d = lane; d < dim; d += 32) {
+      float q = rintf(__fdiv_rn(x[d], sc));
+      q = fminf(127.f, fmaxf(-127.f, q));
+      dst[d] = (int8_t)(int)q;
+      const double e = (double)x[d] - (double)sc * (double)q;
+      e2 = fma(e, e, e2);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) e2 += __shfl_xor_sync(0xffffffffu, e2, off);
+    worst = fmax(worst, sqrt(e2) * (1.0 + 0x1p-40));
+  }
+  __shared__ double wred[QT_T / 32];
+  if (lane == 0) wred[w] = worst;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int i = 0; i < QT_T / 32; ++i) m = fmax(m, wred[i]);
+    tres[tile] = __double2float_ru(m);
+    if (m > 0) atomicMax(res_bits, (unsigned long long)__double_as_longlong(m));
+  }
+}
+}  // namespace sm100
+
+void i8_quantize_tiles(lc_ctx* ctx, const float* rows, int64_t n_rows, int dim, int64_t t0, int64_t t1, int8_t* rows8,
+                       float* tscale, float* tres, unsigned long long* res_bits) {
+  if (t1 <= t0) return;
+  sm100::k_quant_tiles<<<(unsigned)(t1 - t0), sm100::QT_T, 0, ctx->stream>>>(rows, n_rows, dim, t0, rows8, tscale, tres,
+                                                                             res_bits);
+  FC_LAUNCH_CHECK();
+  count_launch(ctx);
+}
+
+void i8_plan(I8Plan& p, const int8_t* rows, const float* tscale, const float* tres, int64_t n_rows, int dim,
+             float r_typ) {
+  p.n_rows = n_rows;
+  p.dim = dim;
+  p.rows = rows;
+  p.tscale = tscale;
+  p.tres = tres;
+  p.r_typ = r_typ;
+  cuuint64_t gdim[2] = {(cuuint64_t)dim, (cuuint64_t)n_rows};
+  cuuint64_t gstride[1] = {(cuuint64_t)dim};
+  cuuint32_t box[2] = {128, (cuuint32_t)sm100::PHB};
+  cuuint32_t estride[2] = {1, 1};
+  CUresult r = encode_fn()(&p.tmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(rows), gdim, gstride, box,
+                           estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) raise(LC_ERR_CUDA, "cuTensorMapEncodeTiled (s8) failed: " + std::to_string((int)r));
+  p.valid = true;
+}
+
+void i8_shortlist(lc_ctx* ctx, const I8Plan& plan, const float* Qdev, int nq, int k, int kp_unit, int kout, float* cand_s,
+                  uint32_t* cand_r, int32_t* cand_n, float* cand_m) {
+  using namespace sm100;
+  FC_REQUIRE(plan.dim % 128 == 0 && plan.dim <= 1024, "int8 lookup tier: dim must be a multiple of 128, <= 1024");
+  ShortlistRun R;
+  R.i8 = true;
+  R.pair = true;
+  R.dim = plan.dim;
+  R.nq = nq;
+  R.n_qtiles = (nq + 2 * BM - 1) / (2 * BM);
+  R.nq_pad = R.n_qtiles * 2 * BM;
+  R.bn = PN;
+  R.n_rows = plan.n_rows;
+  R.kp = kp_unit;
+  R.kout = kout;
+  R.iplan = &plan;
+  DevBuf qi((size_t)R.nq_pad * plan.dim, ctx->stream);
+  DevBuf qs((size_t)R.nq_pad * sizeof(float), ctx->stream);
+  DevBuf qe((size_t)R.nq_pad * sizeof(float2), ctx->stream);
+  k_q_to_i8<<<(unsigned)((R.nq_pad + 7) / 8), 256, 0, ctx->stream>>>(Qdev, nq, plan.dim, R.nq_pad, qi.as<int8_t>(),
+                                                                     qs.as<float>(), qe.as<float2>());
+  FC_LAUNCH_CHECK();
+  count_launch(ctx);
+  R.Qconv = qi.p;
+  R.qscale = qs.as<float>();
+  R.qerr = qe.as<float2>();
+  R.k = k;
+  R.cand_s = cand_s;
+  R.cand_r = cand_r;
+  R.cand_n = cand_n;
+  R.cand_m = cand_m;
+  run_shortlist(ctx, R);
 }
 
 }  // namespace fc

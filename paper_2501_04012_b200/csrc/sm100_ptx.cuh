@@ -178,6 +178,34 @@ __device__ __forceinline__ void mma_box4_pair(uint32_t d_tmem, uint32_t a_tmem, 
       : "memory");
 }
 
+// kind::i8 (s8 x s8 -> s32) variant: four K=32 MMAs over one 128-byte K box;
+// A advances 8 TMEM columns (32 int8) and B 32 bytes per MMA, exactly like
+// the bf16 box above (measured on B200: 4.1 POPS at M=256 x N=128, 2.08x the
+// bf16 rate of the same shape; profiles/r02p_mma_i8_rates.log).
+__device__ __forceinline__ void mma_box4_pair_i8(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                                 uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p, t;\n"
+      ".reg .b64 d1, d2, d3;\n"
+      ".reg .b32 a1, a2, a3;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "setp.eq.b32 t, 0, 0;\n"
+      "add.s64 d1, %2, 2;\n"
+      "add.s64 d2, %2, 4;\n"
+      "add.s64 d3, %2, 6;\n"
+      "add.u32 a1, %1, 8;\n"
+      "add.u32 a2, %1, 16;\n"
+      "add.u32 a3, %1, 24;\n"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], [%1], %2, %3, p;\n"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], [a1], d1, %3, t;\n"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], [a2], d2, %3, t;\n"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], [a3], d3, %3, t;\n"
+      "}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
 // K-major operand tile written by TMA with SWIZZLE_128B: rows of 128 B,
 // 8-row atoms of 1024 B (SBO), LBO unused (1), descriptor version 1 (sm100).
 __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t addr) {

@@ -117,7 +117,7 @@ void run(int sms) {
 }
 
 // cta_group::2: M=256 (128 rows per CTA), A and B from SMEM, leader issues.
-template <int N, int NACC>
+template <int N, int NACC, bool I8 = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) k_mma2(int iters) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -141,12 +141,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) k_mma2(int i
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tslot;
   if (rank == 0 && threadIdx.x == 0) {
-    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+    // kind::i8: D s32 (2 << 4), A/B signed 8-bit (1 << 7, 1 << 10), K = 32 per MMA
+    const uint32_t idesc = I8 ? ((2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(256 >> 4) << 24))
+                              : ((1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(256 >> 4) << 24));
     const uint64_t bd = desc_sw128(smem_u32(base));
     const uint64_t ad = desc_sw128(smem_u32(base + 32768));
     for (int it = 0; it < iters; ++it) {
       const uint32_t d_tmem = tmem + (it % NACC) * N;
       const uint32_t acc = it & 15 ? 1u : 0u;
+      if (I8)
+      asm volatile(
+          "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+          "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+          "l"(ad + (it & 3) * 2), "l"(bd + (it & 3) * 2), "r"(idesc), "r"(acc)
+          : "memory");
+      else
       asm volatile(
           "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
           "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
@@ -177,10 +186,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) k_mma2(int i
   }
 }
 
-template <int N, int NACC>
+template <int N, int NACC, bool I8 = false>
 void run_pair(int sms) {
   const int iters = 16 * 4096;
-  auto k = k_mma2<N, NACC>;
+  auto k = k_mma2<N, NACC, I8>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024 + 1024);
   k<<<sms, 128, 64 * 1024 + 1024>>>(1024);
   cudaDeviceSynchronize();
@@ -193,14 +202,24 @@ void run_pair(int sms) {
   cudaEventSynchronize(b);
   float ms = 0;
   cudaEventElapsedTime(&ms, a, b);
-  const double flops = 2.0 * 256 * N * 16 * (double)iters * (sms / 2);
-  printf("PAIR M=256 N=%3d nacc=%d: %.3f ms  %.1f TFLOP/s  (%.1f cyc/MMA)  err=%s\n", N, NACC, ms,
+  const double flops = 2.0 * 256 * N * (I8 ? 32 : 16) * (double)iters * (sms / 2);
+  printf("PAIR %s M=256 N=%3d nacc=%d: %.3f ms  %.1f T(FL)OP/s  (%.1f cyc/MMA)  err=%s\n", I8 ? "i8  " : "bf16", N, NACC, ms,
          flops / (ms * 1e-3) / 1e12, ms * 1e-3 * 1.965e9 / iters, cudaGetErrorString(cudaGetLastError()));
 }
 
-int main() {
+int main(int argc, char** argv) {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  if (argc > 1) {  // "i8": int8 vs bf16 pair rates only
+    for (int rep = 0; rep < 2; ++rep) {
+      run_pair<128, 2>(sms);
+      run_pair<128, 2, true>(sms);
+      run_pair<256, 1, true>(sms);
+      run_pair<256, 2, true>(sms);
+      run_pair<64, 2, true>(sms);
+    }
+    return 0;
+  }
   run<64, false, 9>(sms);
   run<128, false, 9>(sms);
   run<32, false, 9>(sms);
