@@ -1679,16 +1679,9 @@ void launch_decompress(lc_ctx* ctx, const std::vector<const EntryData*>& ents, c
   if (groups) {
     std::vector<DecJob> jobs((size_t)ents.size() * F);  // pageable: the async copy stages it before returning
     size_t nj = 0;
-    for (size_t i = 0; i < ents.size(); ++i) {
-      const std::vector<int32_t>& mp = ents[i]->maps[sidx[i]];
-      for (int m = 0; m < F; ++m) {
-        if (mp[m] != m) continue;
-        DecJob jb{(int32_t)i, m, {0, 0, 0, 0}};
-        for (int j = m; j < F; ++j)
-          if (mp[j] == m) jb.mask[j >> 6] |= 1ull << (j & 63);
-        jobs[nj++] = jb;
-      }
-    }
+    for (size_t i = 0; i < ents.size(); ++i)  // per-entry key groups are cached (EntryData::key_groups)
+      for (const EntryData::KeyGroup& kg : ents[i]->key_groups(sidx[i]))
+        jobs[nj++] = DecJob{(int32_t)i, kg.key, {kg.mask[0], kg.mask[1], kg.mask[2], kg.mask[3]}};
     DevBuf dj(nj * sizeof(DecJob), ctx->stream);
     FC_CUDA(cudaMemcpyAsync(dj.p, jobs.data(), dj.bytes, cudaMemcpyHostToDevice, ctx->stream));
     KTimer kt(ctx, "decompress");

@@ -12,6 +12,7 @@
 #pragma once
 #include <atomic>
 #include <memory>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -54,6 +55,40 @@ struct EntryData {
   uint8_t* dev = nullptr;
   size_t dev_bytes = 0;
   std::shared_ptr<DevArena> arena;  // set when dev lives in a batch allocation
+  // grouped-decompress jobs per step (key frame + the frames mapped to it),
+  // built on first use: decompress calls then only concatenate them
+  struct KeyGroup {
+    int32_t key;
+    uint64_t mask[4];
+  };
+  mutable std::mutex groups_mu;
+  mutable std::vector<std::vector<KeyGroup>> groups;
+  const std::vector<KeyGroup>& key_groups(int si) const {
+    std::lock_guard<std::mutex> lk(groups_mu);
+    if (groups.size() != steps.size()) groups.assign(steps.size(), {});
+    std::vector<KeyGroup>& g = groups[si];
+    if (g.empty()) {
+      const std::vector<int32_t>& mp = maps[si];
+      std::vector<int> slot(F, -1);
+      for (int j = 0; j < F; ++j) {
+        // frames mapped to a key frame (mp[m] == m) share the key's recipe;
+        // any other frame (only an imported map can do that) stands alone
+        // with its own recipe, exactly as the per-frame kernel would serve it
+        const int m = mp[mp[j]] == mp[j] ? mp[j] : j;
+        if (m == j && mp[j] != j) {
+          g.push_back(KeyGroup{j, {0, 0, 0, 0}});
+          g.back().mask[j >> 6] |= 1ull << (j & 63);
+          continue;
+        }
+        if (slot[m] < 0) {
+          slot[m] = (int)g.size();
+          g.push_back(KeyGroup{m, {0, 0, 0, 0}});
+        }
+        g[slot[m]].mask[j >> 6] |= 1ull << (j & 63);
+      }
+    }
+    return g;
+  }
   ~EntryData();
 
   const float* fbase() const { return reinterpret_cast<const float*>(dev); }

@@ -510,7 +510,7 @@ __device__ __forceinline__ uint32_t fkey(float f) {
 __global__ void __launch_bounds__(RI_WARPS * 32)
     k_rescore_i8(const float* __restrict__ Q, int nq, int dim, const float* __restrict__ rows,
                  const __nv_bfloat16* __restrict__ rowsb, const uint64_t* __restrict__ ids,
-                 const uint32_t* __restrict__ cand_r, const int32_t* __restrict__ cand_n,
+                 const float* __restrict__ cand_s, const uint32_t* __restrict__ cand_r, const int32_t* __restrict__ cand_n,
                  const float* __restrict__ cand_m, int kout, int64_t n_rows, int k, double dres, double eps_floor,
                  uint64_t* __restrict__ out_ids, double* __restrict__ out_sc, int32_t* __restrict__ out_cnt,
                  int32_t* __restrict__ fail_list, int32_t* __restrict__ fail_n,
@@ -520,8 +520,8 @@ __global__ void __launch_bounds__(RI_WARPS * 32)
   const int q = blockIdx.x * RI_WARPS + warp;
   if (q >= nq) return;
   extern __shared__ uint8_t s_raw[];
-  // per warp: fp32 query [dim] | bf16 query [dim] | sort keys [KI_MAX]
-  const size_t per_warp = (size_t)dim * 6 + KI_MAX * 8;
+  // per warp: fp32 query [dim] | bf16 query [dim] | sort keys [KI_MAX] | b [KI_MAX]
+  const size_t per_warp = (size_t)dim * 6 + KI_MAX * 12;
   uint8_t* wbase = s_raw + (size_t)warp * per_warp;
   float* sq = reinterpret_cast<float*>(wbase);
   __nv_bfloat16* sb = reinterpret_cast<__nv_bfloat16*>(wbase + (size_t)dim * 4);
@@ -555,25 +555,90 @@ __global__ void __launch_bounds__(RI_WARPS * 32)
   eps = fmax(eps * (1.0 + 0x1p-20), eps_floor * fmax(1.0, qn));
   // the reference's fp64 sequential dot vs the real dot: <= dim 2^-53 ||q|| ||x||
   const double margin = 1e-12 * (1.0 + qn);
-  const int cn = min(cand_n[q], KI_MAX);
-  // (1) bf16 pre-score, 4 candidates per iteration (loads of all 4 in flight)
+  const int cn_all = min(cand_n[q], KI_MAX);
+  // warp bitonic sort of skey[0, n) descending (n padded to a power of two with 0 keys)
+  auto sort_desc = [&](int n) {
+    int np2 = 32;
+    while (np2 < n) np2 <<= 1;
+    for (int i = n + lane; i < np2; i += 32) skey[i] = 0;
+    __syncwarp();
+    for (int kk = 2; kk <= np2; kk <<= 1)
+      for (int j = kk >> 1; j > 0; j >>= 1) {
+        for (int i = lane; i < np2; i += 32) {
+          const int p = i ^ j;
+          if (p > i) {
+            const uint64_t x = skey[i], y = skey[p];
+            const bool desc = (i & kk) == 0;
+            if (desc ? x < y : x > y) {
+              skey[i] = y;
+              skey[p] = x;
+            }
+          }
+        }
+        __syncwarp();
+      }
+  };
+  // (0) candidates in descending order of U (an upper bound of the exact score)
+  for (int i = lane; i < cn_all; i += 32) {
+    const float u = cand_s[(int64_t)q * kout + i];
+    skey[i] = ((uint64_t)fkey(u) << 32) | (uint32_t)i;
+  }
+  sort_desc(cn_all);
+  // (1) bf16 pre-score in that order, 4 candidates per iteration: every lane
+  // issues all its 16-byte chunks of the 4 rows (<= 4 each, dim <= 1024)
+  // before any math, so one memory round trip serves 4 candidates. After the
+  // first 32, T_lo = (k-th best b among them) - eps <= T_k; a candidate with
+  // U < T_lo has exact <= U < T_k and neither it nor any later one (smaller U)
+  // can reach the top k: the pass stops there.
   const uint4* sb4 = reinterpret_cast<const uint4*>(sb);
   const int n16 = dim / 8;  // 16-byte chunks per bf16 row
-  for (int i0 = 0; i0 < cn; i0 += 4) {
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  constexpr int CPL = 4;    // chunks per lane (dim <= 1024)
+  uint4 qa[CPL];
+#pragma unroll
+  for (int u = 0; u < CPL; ++u) qa[u] = lane + 32 * u < n16 ? sb4[lane + 32 * u] : make_uint4(0, 0, 0, 0);
+  float* sbv = reinterpret_cast<float*>(skey + KI_MAX);  // [KI_MAX] b by U-sorted position
+  double t_lo = -INFINITY;
+  int cn = cn_all;  // candidates pre-scored (a prefix of the U order)
+  for (int i0 = 0; i0 < cn_all; i0 += 4) {
+    if (i0 == 32 && cn_all > 32) {
+      // k-th best b among the first 32 (rank counting across the lanes)
+      const float mine = sbv[lane];
+      int rank = 0;
+      for (int j = 0; j < 32; ++j) {
+        const float o = __shfl_sync(0xffffffffu, mine, j);
+        rank += (o > mine) | ((o == mine) & (j < lane));
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, rank == k - 1);
+      t_lo = (double)__shfl_sync(0xffffffffu, mine, __ffs(bal) - 1) - eps;
+    }
+    {
+      const uint32_t uk = (uint32_t)(skey[i0] >> 32);
+      const float u0 = __uint_as_float((uk & 0x80000000u) ? (uk & 0x7FFFFFFFu) : ~uk);
+      if ((double)u0 < t_lo) {
+        cn = i0;
+        break;
+      }
+    }
     uint32_t rr[4];
 #pragma unroll
-    for (int g = 0; g < 4; ++g) rr[g] = i0 + g < cn ? cand_r[(int64_t)q * kout + i0 + g] : 0u;
-    for (int c = lane; c < n16; c += 32) {
-      const uint4 qa = sb4[c];
-      uint4 xa[4];
+    for (int g = 0; g < 4; ++g)
+      rr[g] = i0 + g < cn_all ? cand_r[(int64_t)q * kout + (uint32_t)skey[i0 + g]] : 0u;
+    uint4 xa[4][CPL];
 #pragma unroll
-      for (int g = 0; g < 4; ++g)
-        xa[g] = i0 + g < cn ? __ldg(reinterpret_cast<const uint4*>(rowsb + (int64_t)rr[g] * dim) + c) : make_uint4(0, 0, 0, 0);
+    for (int g = 0; g < 4; ++g)
 #pragma unroll
-      for (int g = 0; g < 4; ++g) {
-        const __nv_bfloat162* x2 = reinterpret_cast<const __nv_bfloat162*>(&xa[g]);
-        const __nv_bfloat162* q2 = reinterpret_cast<const __nv_bfloat162*>(&qa);
+      for (int u = 0; u < CPL; ++u) {
+        const int c = lane + 32 * u;
+        xa[g][u] = (i0 + g < cn_all && c < n16) ? __ldg(reinterpret_cast<const uint4*>(rowsb + (int64_t)rr[g] * dim) + c)
+                                                 : make_uint4(0, 0, 0, 0);
+      }
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int g = 0; g < 4; ++g)
+#pragma unroll
+      for (int u = 0; u < CPL; ++u) {
+        const __nv_bfloat162* x2 = reinterpret_cast<const __nv_bfloat162*>(&xa[g][u]);
+        const __nv_bfloat162* q2 = reinterpret_cast<const __nv_bfloat162*>(&qa[u]);
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
           const float2 xf = __bfloat1622float2(x2[h]), qf = __bfloat1622float2(q2[h]);
@@ -581,37 +646,18 @@ __global__ void __launch_bounds__(RI_WARPS * 32)
           acc[g] = fmaf(qf.y, xf.y, acc[g]);
         }
       }
-    }
 #pragma unroll
     for (int g = 0; g < 4; ++g) {
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) acc[g] += __shfl_xor_sync(0xffffffffu, acc[g], off);
     }
-    if (lane < 4 && i0 + lane < cn) {
-      const float bsc = lane == 0 ? acc[0] : lane == 1 ? acc[1] : lane == 2 ? acc[2] : acc[3];
-      skey[i0 + lane] = ((uint64_t)fkey(bsc) << 32) | (uint32_t)(i0 + lane);
-    }
+    if (lane < 4 && i0 + lane < cn_all) sbv[i0 + lane] = lane == 0 ? acc[0] : lane == 1 ? acc[1] : lane == 2 ? acc[2] : acc[3];
+    __syncwarp();
   }
-  // (2) sort by b, descending
-  int np2 = 32;
-  while (np2 < cn) np2 <<= 1;
-  for (int i = cn + lane; i < np2; i += 32) skey[i] = 0;
+  // (2) the pre-scored prefix by b, descending (list index kept in the low bits)
+  for (int i = lane; i < cn; i += 32) skey[i] = ((uint64_t)fkey(sbv[i]) << 32) | (uint32_t)skey[i];
   __syncwarp();
-  for (int kk = 2; kk <= np2; kk <<= 1)
-    for (int j = kk >> 1; j > 0; j >>= 1) {
-      for (int i = lane; i < np2; i += 32) {
-        const int p = i ^ j;
-        if (p > i) {
-          const uint64_t a = skey[i], b = skey[p];
-          const bool desc = (i & kk) == 0;
-          if (desc ? a < b : a > b) {
-            skey[i] = b;
-            skey[p] = a;
-          }
-        }
-      }
-      __syncwarp();
-    }
+  sort_desc(cn);
   auto key_b = [](uint64_t key) {
     const uint32_t ok = (uint32_t)(key >> 32);
     return __uint_as_float((ok & 0x80000000u) ? (ok & 0x7FFFFFFFu) : ~ok);
@@ -683,7 +729,8 @@ __global__ void __launch_bounds__(RI_WARPS * 32)
   if (lane == 0) {
     if (local_err > 0) atomicMax(max_err_bits, (unsigned long long)__double_as_longlong(local_err));
     atomicAdd(gathered, (unsigned long long)n_gath);
-    atomicAdd(gathered + 1, (unsigned long long)cn);
+    atomicAdd(gathered + 1, (unsigned long long)cn_all);
+    atomicAdd(gathered + 2, (unsigned long long)cn);
   }
   const int got = min(n_have, k);
   if (lane < k) {
@@ -694,7 +741,7 @@ __global__ void __launch_bounds__(RI_WARPS * 32)
     out_cnt[q] = got;
     bool ok;
     if (q_uncertifiable) ok = false;
-    else if (cn >= n_rows) ok = true;  // every row is in the list
+    else if (cn_all >= n_rows) ok = true;  // every row is in the list
     else ok = got >= k && (double)cand_m[q] + margin < tk;
     if (!ok) fail_list[atomicAdd(fail_n, 1)] = q;
   }
@@ -893,12 +940,12 @@ void query_dev(lc_index* ix, int kind, const float* Qdev, int nq, int k, uint64_
   // Tier 1: the int8 tensor-core shortlist (2x the bf16 tensor rate) for
   // batches that fill CTA pairs, else the bf16 shortlist with K' = kprime.
   const bool tier1_i8 = i8_ok;
-  int64_t gathered = -1, cands = -1;
+  int64_t gathered = -1, cands = -1, prescored = -1;
   if (tier1_i8) {
     const int kout = ix->i8_kout;
     DevBuf cs((size_t)nq * kout * sizeof(float), ctx->stream), cr((size_t)nq * kout * sizeof(uint32_t), ctx->stream);
     DevBuf cn((size_t)nq * sizeof(int32_t), ctx->stream), cm((size_t)nq * sizeof(float), ctx->stream);
-    DevBuf gb(2 * sizeof(unsigned long long), ctx->stream);
+    DevBuf gb(3 * sizeof(unsigned long long), ctx->stream);
     FC_CUDA(cudaMemsetAsync(gb.p, 0, gb.bytes, ctx->stream));
     {
       std::lock_guard<std::mutex> pl(ix->plan_mu);
@@ -914,26 +961,27 @@ void query_dev(lc_index* ix, int kind, const float* Qdev, int nq, int k, uint64_
     }
     i8_shortlist(ctx, ix->iplan[kind], Qdev, nq, k, ix->i8_kunit, kout, cs.as<float>(), cr.as<uint32_t>(),
                  cn.as<int32_t>(), cm.as<float>());
-    const size_t ri_smem = (size_t)RI_WARPS * ((size_t)dim * 6 + KI_MAX * 8);
+    const size_t ri_smem = (size_t)RI_WARPS * ((size_t)dim * 6 + KI_MAX * 12);
     static std::atomic<uint64_t> attr_set{0};
     if (!(attr_set.load() >> (ctx->device & 63) & 1)) {
       FC_CUDA(cudaFuncSetAttribute(k_rescore_i8, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)(RI_WARPS * (1024 * 6 + KI_MAX * 8))));
+                                   (int)(RI_WARPS * (1024 * 6 + KI_MAX * 12))));
       attr_set.fetch_or(1ull << (ctx->device & 63));
     }
     KTimer kt(ctx, "rescore");
     k_rescore_i8<<<(unsigned)((nq + RI_WARPS - 1) / RI_WARPS), RI_WARPS * 32, ri_smem, ctx->stream>>>(
-        Qdev, nq, dim, ix->rows[kind], ix->rowsb[kind], ix->ids_dev, cr.as<uint32_t>(), cn.as<int32_t>(),
+        Qdev, nq, dim, ix->rows[kind], ix->rowsb[kind], ix->ids_dev, cs.as<float>(), cr.as<uint32_t>(), cn.as<int32_t>(),
         cm.as<float>(), kout, ix->n, k, ix->dres[kind], ix->eps_floor, oid, osc, ocnt, fl.as<int32_t>(), fail_n,
         err_bits, bad_q, gb.as<unsigned long long>());
     kt.stop();
     FC_LAUNCH_CHECK();
     count_launch(ctx);
-    unsigned long long hg[2] = {0, 0};
+    unsigned long long hg[3] = {0, 0, 0};
     FC_CUDA(cudaMemcpyAsync(hg, gb.p, sizeof hg, cudaMemcpyDeviceToHost, ctx->stream));
     sync(ctx);
     gathered = (int64_t)hg[0];
     cands = (int64_t)hg[1];
+    prescored = (int64_t)hg[2];
   } else {
     DevBuf cs((size_t)nq * kp * sizeof(float), ctx->stream);
     DevBuf cr((size_t)nq * kp * sizeof(uint32_t), ctx->stream);
@@ -979,6 +1027,7 @@ void query_dev(lc_index* ix, int kind, const float* Qdev, int nq, int k, uint64_
       ix->stats.i8_batches += 1;
       ix->stats.i8_rescored += gathered;
       ix->stats.i8_candidates += cands;
+      ix->stats.i8_prescored += prescored;
     }
   }
   // FC_LOOKUP_DIAG=1 (kernel-timing diagnostics with FC_SHORTLIST_DEBUG only): skip the

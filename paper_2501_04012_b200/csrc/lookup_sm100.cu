@@ -266,7 +266,32 @@ struct Params {
   float r_typ;               // typical tile residual (median of tres): threshold offset
   float slack;               // threshold offset slack (actual vs bounded error, bucket width)
   float* part_d;             // [nq][lists] drop level: every row the unit rejected or dropped has U <= it
+  // int8 pilot pass: row tiles are every tile_stride-th physical tile (rows
+  // [row * tile_stride, +128) for logical row `row`); each thread publishes the
+  // max U of its query over the sampled tiles to gkey (order key) and keeps no
+  // lists. The main pass starts every query's threshold at that max - offset:
+  // over a 1/16 sample the max is about the table's 16th best, just below the
+  // k-th best, so the filter is tight from the first tile instead of after a
+  // warm-up (which cost ~5k accepted entries and ~20k list compactions per
+  // 4096-query batch at 1M rows).
+  int pilot;
+  int tile_stride;
+  int64_t n_rows_phys;
+  float* pilot_out;          // [nq][lists][PILOT_R] each list's best U values (descending)
+  // int8 main pass output: every unit appends its entries to its query's
+  // contiguous buffer (one atomic per (query, unit)), so the merge reads one
+  // segment per query instead of 2 * splits scattered lists
+  uint64_t* qbuf;            // [nq][qcap] (fp16 U key << 48) | absolute row
+  uint32_t* qcnt;            // [nq] entries appended (may exceed qcap)
+  uint32_t* qdrop;           // [nq] order key of the max drop level (0 = none)
+  int qcap;
 };
+// The pilot keeps each query's PILOT_R best U over the sample and the main
+// pass starts at the R-th best over the whole sample: over a 1/16 sample that
+// is about the table's 16R-th best, and it exceeds the k-th best (k = 8) only
+// when >= R of the top 8 fall in the sample (C(8,6) 16^-6 ~ 2e-6 for R = 6).
+// (The sample max instead failed certification for 32 % of the queries.)
+constexpr int PILOT_R = 6;
 
 constexpr int MAX_STAGE = 24;
 
@@ -646,7 +671,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
               if (leader) mbar_expect_tx(smem_u32(&full[stage]), 2 * STAGE_BYTES);
               for (int bx = 0; bx < BPS; ++bx)
                 tma_load_2d_pair(smem_u32(stages + stage * STAGE_BYTES + bx * PBOX), &tmB, smem_u32(&full[stage]),
-                                 (sg * BPS + bx) * BKE, (int)(row + rank * PHB));
+                                 (sg * BPS + bx) * BKE, (int)(row * p.tile_stride + rank * PHB));
             }
             if (++stage == NSTAGE) {
               stage = 0;
@@ -779,14 +804,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
       const float qsc = I8 ? __ldg(p.qscale + q) : 1.f;
       const float2 qe = I8 ? __ldg(p.qerr + q) : make_float2(0.f, 0.f);
       const float hoff = I8 ? __fmaf_ru(qe.y, p.r_typ, qe.x) + p.slack : 0.f;
-      hist_refresh(hq, p.kh, tau, hoff);
+      float ut[PILOT_R];  // pilot: best U over the sampled tiles, descending
+#pragma unroll
+      for (int i = 0; i < PILOT_R; ++i) ut[i] = -INFINITY;
+      if (!p.pilot) hist_refresh(hq, p.kh, tau, hoff);
+      if (I8 && !p.pilot) {  // the pilot's max U of this query
+        uint32_t pk;
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(pk) : "l"(p.gkey + q));
+        if (pk) tau = fmaxf(tau, key_float(pk) - hoff);
+      }
+      // int8: the tile's scale and residual bound are loaded one tile ahead
+      // (a dependent L2 round trip per tile otherwise sits on the critical path)
+      float nx_sc = 1.f, nx_res = 0.f;
+      if (I8) {
+        nx_sc = __ldg(p.tscale + ((r0 * p.tile_stride) >> 7));
+        nx_res = __ldg(p.tres + ((r0 * p.tile_stride) >> 7));
+      }
       // FC_SHORTLIST_DEBUG & 16: per-warp clock64 spans [accumulator wait, histogram, compaction, appends]
       long long cyc[4] = {0, 0, 0, 0}, c_t0 = 0;
       const bool prof = p.debug & 16;
       for (int64_t row = r0; row < r1; row += PN, ++tile) {
         const uint32_t b = tile & 1;
         const uint32_t use = tile >> 1;
-        if ((tile & p.refresh_mask) == 0) {
+        if ((tile & p.refresh_mask) == 0 && !p.pilot) {
           if (prof) c_t0 = clock64();
           hist_publish(hq, lk, t, pub, cnt);
           pub = cnt;
@@ -795,16 +835,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
         }
         // int8: this tile's scale product, error bound and integer threshold
         // (reject a <= tau - eps_t, i.e. U <= tau)
-        const float sqt = I8 ? qsc * __ldg(p.tscale + (row >> 7)) : 1.f;
-        const float eps_t = I8 ? __fmaf_ru(qe.y, __ldg(p.tres + (row >> 7)), qe.x) : 0.f;
+        const float sqt = I8 ? qsc * nx_sc : 1.f;
+        const float eps_t = I8 ? __fmaf_ru(qe.y, nx_res, qe.x) : 0.f;
         int thr = I8 ? i8_thr(__fsub_rd(tau, eps_t), sqt) : 0;
+        if (I8 && row + PN < r1) {
+          nx_sc = __ldg(p.tscale + (((row + PN) * p.tile_stride) >> 7));
+          nx_res = __ldg(p.tres + (((row + PN) * p.tile_stride) >> 7));
+        }
         if (prof) c_t0 = clock64();
         mbar_wait(smem_u32(&accf[b]), use & 1);
         tc_fence_after();
         if (prof) cyc[0] += clock64() - c_t0;
         if ((p.debug & 16) && lane == 0) atomicAdd(p.stats + 2, 1u);
         // columns [64 half, +64) of the tile; lim = valid rows of this half
-        const int lim_all = (int)max((int64_t)0, min((int64_t)EPI_HALF_COLS, r1 - row - half * EPI_HALF_COLS));
+        const int lim_all = (int)max((int64_t)0, min((int64_t)EPI_HALF_COLS,
+                                                     (p.pilot ? p.n_rows_phys - row * p.tile_stride : r1 - row) -
+                                                         half * EPI_HALF_COLS));
         const uint32_t off_base = (uint32_t)(row - r0) + half * EPI_HALF_COLS;
         // 32 accumulator columns per step (a rolled loop: the unrolled
         // 128-column body overflowed the instruction cache, ncu "no_inst";
@@ -822,6 +868,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_remote(smem_u32(&acce[b]), 0);
+        if (I8 && p.pilot) {  // fold the tile half's valid dots into the best-R U list
+          const int pthr = i8_thr(__fsub_rd(ut[PILOT_R - 1], eps_t), sqt);
+#pragma unroll
+          for (int c0 = 0; c0 < EPI_HALF_COLS; c0 += 16) {
+            int m = INT_MIN;
+#pragma unroll
+            for (int c = c0; c < c0 + 16; c += 2)
+              m = __vimax3_s32(m, c < lim_all ? (int)rv[c] : INT_MIN, c + 1 < lim_all ? (int)rv[c + 1] : INT_MIN);
+            if (!__any_sync(0xffffffffu, m > pthr)) continue;
+#pragma unroll
+            for (int c = c0; c < c0 + 16; ++c) {
+              if (c < lim_all && (int)rv[c] > pthr) {
+                float u = __fadd_ru(i8_score_up((int)rv[c], sqt), eps_t);
+#pragma unroll
+                for (int i = 0; i < PILOT_R; ++i) {  // insertion into the descending list
+                  const float hi = fmaxf(ut[i], u);
+                  u = fminf(ut[i], u);
+                  ut[i] = hi;
+                }
+              }
+            }
+          }
+          continue;
+        }
         if (!(p.debug & 4)) {
 #pragma unroll
           for (int hh = 0; hh < EPI_HALF_COLS / 16; ++hh) {
@@ -862,25 +932,51 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
             const uint32_t off0 = off_base + (uint32_t)c0;
 #pragma unroll
             for (int jj = 0; jj < 16; ++jj) {
-              bool acc;
-              float v;
               if constexpr (I8) {
                 const int d = (int)rv[c0 + jj];
-                acc = (c0 + jj < lim_all) & (d > thr);
-                v = __fadd_ru(i8_score_up(d, sqt), eps_t);
+                const bool acc = (c0 + jj < lim_all) & (d > thr);
+                if (acc) lk[cnt * BM + t] = (hkey_ru(__fadd_ru(i8_score_up(d, sqt), eps_t)) << 16) | (off0 + jj);
+                cnt += acc;
               } else {
-                v = __uint_as_float(rv[c0 + jj]);
-                acc = (c0 + jj < lim_all) & (v > tau);
+                const float v = __uint_as_float(rv[c0 + jj]);
+                const bool acc = (c0 + jj < lim_all) & (v > tau);
+                if (acc) lk[cnt * BM + t] = (hkey_ru(v) << 16) | (off0 + jj);
+                cnt += acc;
               }
-              if (acc) lk[cnt * BM + t] = (hkey_ru(v) << 16) | (off0 + jj);
-              cnt += acc;
             }
             if (prof) cyc[3] += clock64() - c_t0;
           }
         }
       }
+      if (I8 && p.pilot) {
+        if (q < p.nq) {
+          float* o = p.pilot_out + (((size_t)q * 2 * p.n_splits) + 2 * split + half) * PILOT_R;
+#pragma unroll
+          for (int i = 0; i < PILOT_R; ++i) o[i] = ut[i];
+        }
+        continue;
+      }
       if (prof) c_t0 = clock64();
       hist_publish(hq, lk, t, pub, cnt);
+      if (I8) {
+        // append the unit's entries to the query's buffer; what does not fit
+        // is dropped into the drop level, as is everything the unit rejected
+        // (U <= tau) or compacted away (stored U <= the raised tau)
+        if (q < p.nq) {
+          const uint32_t pos = cnt ? atomicAdd(p.qcnt + q, (uint32_t)cnt) : 0u;
+          float dmax = tau;
+          for (int i = 0; i < cnt; ++i) {
+            const uint32_t key = lk[i * BM + t];
+            if (pos + (uint32_t)i < (uint32_t)p.qcap)
+              p.qbuf[(size_t)q * p.qcap + pos + i] = ((uint64_t)(key >> 16) << 48) | (uint64_t)(r0 + (key & 0xFFFFu));
+            else
+              dmax = fmaxf(dmax, hkey_float(key >> 16));
+          }
+          if (dmax > -INFINITY) atomicMax(p.qdrop + q, okey(dmax));
+        }
+        if (prof) cyc[2] += clock64() - c_t0;
+        continue;
+      }
       compact_keys(lk, t, cnt, p.kp, tau, true);  // exact: the unit's list holds at most kp entries
       if (prof) {
         cyc[2] += clock64() - c_t0;
@@ -905,6 +1001,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
+}
+
+// Per query (one warp): the PILOT_R-th best U over all pilot lists -> gkey
+// (order key; 0 = none, the main pass then starts from its histogram only).
+__global__ void k_pilot_kth(const float* __restrict__ po, int lists, int nq, uint32_t* __restrict__ gkey) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= nq) return;
+  const float* v = po + (size_t)w * lists * PILOT_R;
+  const int n = lists * PILOT_R;
+  float best[PILOT_R];
+#pragma unroll
+  for (int i = 0; i < PILOT_R; ++i) best[i] = -INFINITY;
+  for (int j = lane; j < n; j += 32) {
+    float u = v[j];
+#pragma unroll
+    for (int i = 0; i < PILOT_R; ++i) {
+      const float hi = fmaxf(best[i], u);
+      u = fminf(best[i], u);
+      best[i] = hi;
+    }
+  }
+  // warp merge: PILOT_R rounds of warp max over the lanes' list heads
+  int ptr = 0;
+  float kth = -INFINITY;
+  for (int r = 0; r < PILOT_R; ++r) {
+    float h = ptr < PILOT_R ? best[0] : -INFINITY;
+    float m = h;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+    const unsigned own = __ballot_sync(0xffffffffu, h == m && ptr < PILOT_R);
+    if (own && lane == __ffs(own) - 1) {  // pop the head
+#pragma unroll
+      for (int i = 0; i < PILOT_R - 1; ++i) best[i] = best[i + 1];
+      best[PILOT_R - 1] = -INFINITY;
+      ++ptr;
+    }
+    kth = m;
+  }
+  if (lane == 0) gkey[w] = kth > -INFINITY ? okey(kth) : 0u;
 }
 
 __global__ void k_q_to_bf16(const float* __restrict__ Q, int nq, int dim, __nv_bfloat16* __restrict__ Qb, int nq_pad) {
@@ -1026,6 +1161,69 @@ __global__ void __launch_bounds__(MG_W * 32) k_shortlist_merge(const uint32_t* _
     out += __popc(bal);
   }
   if (lane == 0) cn[q] = min(kout, out);
+}
+
+// int8 tier merge: per query (one warp) the kout best of its contiguous
+// buffer by (U key, row); cm[q] = max(drop level, U at the cut).
+constexpr int QM_W = 4;
+constexpr int QCAP = 1024;
+__global__ void __launch_bounds__(QM_W * 32) k_i8_merge(const uint64_t* __restrict__ qbuf, const uint32_t* __restrict__ qcnt,
+                                                       const uint32_t* __restrict__ qdrop, int nq, int kout,
+                                                       float* __restrict__ cs, uint32_t* __restrict__ cr,
+                                                       int32_t* __restrict__ cn, float* __restrict__ cm) {
+  __shared__ uint64_t s_k[QM_W][QCAP];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q = blockIdx.x * QM_W + w;
+  if (q >= nq) return;
+  const int n = (int)min(qcnt[q], (uint32_t)QCAP);
+  const uint32_t dk = qdrop[q];
+  float drop = dk ? key_float(dk) : -INFINITY;
+  uint64_t* key = s_k[w];
+  for (int i = lane; i < n; i += 32) key[i] = qbuf[(size_t)q * QCAP + i];
+  __syncwarp();
+  uint64_t T = 0;  // keep everything
+  if (n > kout) {
+    uint64_t lo = 0, hi = ~0ull;
+    while (lo < hi) {  // max T with count(key >= T) >= kout
+      const uint64_t mid = lo + ((hi - lo) >> 1) + 1;
+      int c = 0;
+      for (int i = lane; i < n; i += 32) c += key[i] >= mid;
+      c = __reduce_add_sync(0xffffffffu, c);
+      if (c >= kout) lo = mid; else hi = mid - 1;
+    }
+    T = lo;
+    drop = fmaxf(drop, hkey_float((uint32_t)(T >> 48)));  // cut entries have stored U <= that of T
+  }
+  int out = 0;
+  for (int i0 = 0; i0 < n; i0 += 32) {
+    const int i = i0 + lane;
+    const bool take = i < n && key[i] >= T && (n <= kout || key[i] > T);
+    const unsigned bal = __ballot_sync(0xffffffffu, take);
+    if (take) {
+      const int at = out + __popc(bal & ((1u << lane) - 1));
+      cs[(size_t)q * kout + at] = hkey_float((uint32_t)(key[i] >> 48));
+      cr[(size_t)q * kout + at] = (uint32_t)(key[i] & 0xFFFFFFFFFFFFull);
+    }
+    out += __popc(bal);
+  }
+  if (n > kout)  // keys are unique (distinct rows): exactly one entry equals T
+    for (int i0 = 0; i0 < n && out < kout; i0 += 32) {
+      const int i = i0 + lane;
+      const bool take = i < n && key[i] == T;
+      const unsigned bal = __ballot_sync(0xffffffffu, take);
+      if (take) {
+        const int at = out + __popc(bal & ((1u << lane) - 1));
+        if (at < kout) {
+          cs[(size_t)q * kout + at] = hkey_float((uint32_t)(key[i] >> 48));
+          cr[(size_t)q * kout + at] = (uint32_t)(key[i] & 0xFFFFFFFFFFFFull);
+        }
+      }
+      out += __popc(bal);
+    }
+  if (lane == 0) {
+    cn[q] = min(out, kout);
+    cm[q] = drop;
+  }
 }
 
 // Same selection as k_shortlist_merge with one CTA per query (MC_T threads):
@@ -1251,21 +1449,29 @@ struct ShortlistRun {
 void run_shortlist(lc_ctx* ctx, const ShortlistRun& R) {
   using namespace sm100;
   const int nq = R.nq, kp = R.kp, bn = R.bn;
-  const int64_t total_tiles = (R.n_rows + bn - 1) / bn;
   const int64_t workers = R.pair ? ctx->sm_count / 2 : ctx->sm_count;  // persistent CTAs / CTA pairs
-  // ~16 units per persistent worker: shorter row ranges keep the query tiles
-  // that share a range closer together in time, so the table is re-read from
-  // L2 rather than HBM (ncu, 1M x 768 x 4096: 37 splits 3.63 GB DRAM per launch,
-  // 74 splits 2.74 GB and 2.5 % faster; 148 splits cost more in the merge)
-  int64_t splits = std::max<int64_t>(1, (workers * 16 + R.n_qtiles - 1) / R.n_qtiles);
-  splits = std::min<int64_t>(splits, std::max<int64_t>(1, total_tiles / 16));
-  // keep one query's partial lists within the merge's shared memory (few queries)
-  splits = std::min<int64_t>(splits, std::max<int64_t>(workers, (200 * 1024) / ((int64_t)kp * 8 * (R.pair ? 2 : 1))));
-  // packed candidates carry the row offset in 16 bits
-  splits = std::max<int64_t>(splits, (total_tiles * bn + 65535) / 65536);
-  const int64_t tiles_per_split = std::min<int64_t>((total_tiles + splits - 1) / splits, 65536 / bn);
-  splits = (total_tiles + tiles_per_split - 1) / tiles_per_split;
+  // work units over `tiles` row tiles: (splits, tiles per split)
+  auto split_rows = [&](int64_t tiles, int64_t& splits, int64_t& tiles_per_split) {
+    // ~16 units per persistent worker: shorter row ranges keep the query tiles
+    // that share a range closer together in time, so the table is re-read from
+    // L2 rather than HBM (ncu, 1M x 768 x 4096: 37 splits 3.63 GB DRAM per launch,
+    // 74 splits 2.74 GB and 2.5 % faster; 148 splits cost more in the merge)
+    splits = std::max<int64_t>(1, (workers * 16 + R.n_qtiles - 1) / R.n_qtiles);
+    splits = std::min<int64_t>(splits, std::max<int64_t>(1, tiles / 16));
+    // keep one query's partial lists within the merge's shared memory (few queries)
+    splits = std::min<int64_t>(splits, std::max<int64_t>(workers, (200 * 1024) / ((int64_t)kp * 8 * (R.pair ? 2 : 1))));
+    // packed candidates carry the row offset in 16 bits
+    splits = std::max<int64_t>(splits, (tiles * bn + 65535) / 65536);
+    tiles_per_split = std::min<int64_t>((tiles + splits - 1) / splits, 65536 / bn);
+    splits = (tiles + tiles_per_split - 1) / tiles_per_split;
+  };
+  const int64_t total_tiles = (R.n_rows + bn - 1) / bn;
+  int64_t splits = 0, tiles_per_split = 0;
+  split_rows(total_tiles, splits, tiles_per_split);
   Params prm;
+  prm.pilot = 0;
+  prm.tile_stride = 1;
+  prm.n_rows_phys = R.n_rows;
   prm.Qb = reinterpret_cast<const __nv_bfloat16*>(R.Qconv);
   prm.nq = nq;
   prm.n_qtiles = R.n_qtiles;
@@ -1281,7 +1487,7 @@ void run_shortlist(lc_ctx* ctx, const ShortlistRun& R) {
   prm.qscale = R.qscale;
   prm.qerr = R.qerr;
   prm.r_typ = R.i8 ? R.iplan->r_typ : 0.f;
-  prm.slack = 0.0015f;
+  prm.slack = 0.003f;
   if (const char* e = getenv("FC_LOOKUP_I8_SLACK")) prm.slack = (float)atof(e);
   {
     const char* dbg = getenv("FC_SHORTLIST_DEBUG");
@@ -1310,9 +1516,42 @@ void run_shortlist(lc_ctx* ctx, const ShortlistRun& R) {
   prm.part_k = pk.as<uint32_t>();
   prm.part_n = pn.as<int32_t>();
   prm.part_d = R.i8 ? pd.as<float>() : nullptr;
+  DevBuf qb(R.i8 ? (size_t)nq * QCAP * sizeof(uint64_t) : 16, ctx->stream);
+  DevBuf qc(R.i8 ? (size_t)nq * 2 * sizeof(uint32_t) : 16, ctx->stream);
+  prm.qbuf = qb.as<uint64_t>();
+  prm.qcnt = qc.as<uint32_t>();
+  prm.qdrop = qc.as<uint32_t>() + nq;
+  prm.qcap = QCAP;
+  if (R.i8) FC_CUDA(cudaMemsetAsync(qc.p, 0, qc.bytes, ctx->stream));
   if (R.i8) {
     alignas(64) CUtensorMap unused;
     memset(&unused, 0, sizeof unused);
+    // pilot over every 16th row tile (tables of >= 256 tiles): per-query max U
+    // into gkey, the main pass's starting threshold
+    constexpr int PILOT_STRIDE = 16;
+    static const bool no_pilot = getenv("FC_LOOKUP_I8_PILOT") && atoi(getenv("FC_LOOKUP_I8_PILOT")) == 0;
+    if (!no_pilot && total_tiles >= 256) {
+      Params pp = prm;
+      pp.pilot = 1;
+      pp.tile_stride = PILOT_STRIDE;
+      const int64_t ptiles = (total_tiles + PILOT_STRIDE - 1) / PILOT_STRIDE;
+      // ~2 long units per CTA pair (short units pay the query load into TMEM
+      // and the per-thread best-R warm-up each time)
+      int64_t ps = std::max<int64_t>(1, std::min<int64_t>(ptiles / 16, (2 * workers + R.n_qtiles / 2) / R.n_qtiles));
+      int64_t ptps = (ptiles + ps - 1) / ps;
+      ps = (ptiles + ptps - 1) / ptps;
+      pp.n_rows = ptiles * bn;
+      pp.rows_per_split = (int)(ptps * bn);
+      pp.n_splits = (int)ps;
+      pp.n_units = (int)(ps * R.n_qtiles);
+      DevBuf po((size_t)nq * 2 * ps * PILOT_R * sizeof(float), ctx->stream);
+      pp.pilot_out = po.as<float>();
+      ShortlistTimerName tn("shortlist_pilot");
+      launch_pair<true>(ctx, R.iplan->tmap, unused, pp);
+      k_pilot_kth<<<(unsigned)((nq + 7) / 8), 256, 0, ctx->stream>>>(po.as<float>(), (int)(2 * ps), nq, gk.as<uint32_t>());
+      FC_LAUNCH_CHECK();
+      count_launch(ctx, 2);
+    }
     launch_pair<true>(ctx, R.iplan->tmap, unused, prm);
   } else if (R.pair) {
     alignas(64) CUtensorMap tmQ;
@@ -1340,6 +1579,13 @@ void run_shortlist(lc_ctx* ctx, const ShortlistRun& R) {
   const size_t per_warp = (size_t)lists * kp * 2 * sizeof(uint32_t);  // keys + slots
   const float* pdp = R.i8 ? pd.as<float>() : nullptr;
   KTimer kmt(ctx, "shortlist_merge");
+  if (R.i8) {
+    k_i8_merge<<<(nq + QM_W - 1) / QM_W, QM_W * 32, 0, ctx->stream>>>(prm.qbuf, prm.qcnt, prm.qdrop, nq, R.kout,
+                                                                      R.cand_s, R.cand_r, R.cand_n, R.cand_m);
+    FC_LAUNCH_CHECK();
+    count_launch(ctx, 2);
+    return;
+  }
   if (nq < ctx->sm_count && per_warp <= 200 * 1024) {
     static std::atomic<uint64_t> attr_set{0};  // per-device bit: the attribute is per device
     if (!(attr_set.load() >> (ctx->device & 63) & 1)) {

@@ -29,8 +29,8 @@ sl = tot.value / n_.value
 tf = 2 * nb * rows * dim / (sl / 1e3) / 1e12
 st = ix.stats()
 parts = []
-for name in (b"shortlist_merge", b"rescore", b"shortlist_tier2", b"rescore_tier2", b"scan"):
+for name in (b"shortlist_pilot", b"shortlist_merge", b"rescore", b"shortlist_tier2", b"rescore_tier2", b"scan"):
     fc.lib.lc_ctx_kernel_time(ctx.h, name, C.byref(n_), C.byref(tot), 1)
     parts.append(f"{name.decode()} {tot.value / 6:.3f}")
 print(f"rows={rows} dim={dim} kp={kp} nq={nb}: step {e0.elapsed_time(e1)/6:.2f} ms, shortlist {sl:.3f} ms = {tf:.0f} T(FL)OP/s, "
-      f"fallback {st.fallback} i8 batches {st.i8_batches} cands/query {st.i8_candidates / max(1, 8 * nb):.1f} exact/query {st.i8_rescored / max(1, 8 * nb):.1f} | per step ms: " + ", ".join(parts), flush=True)
+      f"fallback {st.fallback} i8 batches {st.i8_batches} cands/query {st.i8_candidates / max(1, 8 * nb):.1f} bf16/query {st.i8_prescored / max(1, 8 * nb):.1f} exact/query {st.i8_rescored / max(1, 8 * nb):.1f} | per step ms: " + ", ".join(parts), flush=True)

@@ -145,12 +145,14 @@ def test_priority_functions(fc):
 
 
 @pytest.mark.parametrize("policy", [0, 1, 2, 3])
-@pytest.mark.parametrize("sort_path", ["0", "1"])
+@pytest.mark.parametrize("sort_path", ["0", "1", "2"])
 def test_eviction_burst_both_scoring_paths(fc, orc, synth, policy, sort_path):
     """600 evict_one at one `now` over ~1500 live steps: crosses the 256-entry
     scored head twice (re-scoring), LRBU sibling re-keys, and the radix-select
-    fast path (FC_SCORE_SORT=0) vs the segmented-sort path (=1)."""
-    os.environ["FC_SCORE_SORT"] = sort_path
+    fast path as one cooperative kernel (FC_SCORE_SORT=0, default) or as 7
+    launches ("2": FC_SCORE_FUSED=0) vs the segmented-sort path (=1)."""
+    os.environ["FC_SCORE_SORT"] = "1" if sort_path == "1" else "0"
+    os.environ["FC_SCORE_FUSED"] = "0" if sort_path == "2" else "1"
     try:
         ents = _tiny_entries(fc, synth, 300, policy)
         st = fc.CacheStore(1 << 40, fc.Policy(policy))
@@ -174,6 +176,7 @@ def test_eviction_burst_both_scoring_paths(fc, orc, synth, policy, sort_path):
         assert st.used() == ot.used() == st.recompute_used()
     finally:
         del os.environ["FC_SCORE_SORT"]
+        del os.environ["FC_SCORE_FUSED"]
 
 
 def _gpu_store_worker(rank, world, port, policy, seed, out_dir):
