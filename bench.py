@@ -65,6 +65,8 @@ def parse():
     ap.add_argument("--codec-prompts", type=int, default=256)
     ap.add_argument("--codec-frames", type=int, default=64)
     ap.add_argument("--no-codec", action="store_true")
+    ap.add_argument("--no-large", action="store_true", help="skip the config[4] large-latent section")
+    ap.add_argument("--large-prompts", type=int, default=32)
     ap.add_argument("--no-scoring", action="store_true")
     ap.add_argument("--score-prompts", type=int, default=100_000)
     ap.add_argument("--score-evictions", type=int, default=2000)
@@ -416,7 +418,7 @@ def main():
         step(qs[s])
     ix.stats(reset=True)
     fc.lib.lc_ctx_profile(ctx.h, 1)
-    for name in ("shortlist", "rescore", "scan", "shortlist_tier2", "rescore_tier2", "shortlist_merge"):
+    for name in ("shortlist", "shortlist_pilot", "rescore", "scan", "shortlist_tier2", "rescore_tier2", "shortlist_merge"):
         fc.lib.lc_ctx_kernel_time(ctx.h, name.encode(), None, None, 1)
     launches0 = ctx.launches
     if world > 1:
@@ -447,28 +449,44 @@ def main():
     value = args.steps * B / (ms / 1000.0)
     st = ix.stats()
     kt = {}
-    for name in ("shortlist", "rescore", "scan", "shortlist_tier2", "rescore_tier2", "shortlist_merge"):
+    for name in ("shortlist", "shortlist_pilot", "rescore", "scan", "shortlist_tier2", "rescore_tier2", "shortlist_merge"):
         n_, tot = C.c_uint64(), C.c_double()
         fc.lib.lc_ctx_kernel_time(ctx.h, name.encode(), C.byref(n_), C.byref(tot), 1)
         kt[name] = (n_.value, tot.value)
 
-    # roofline of the dominant kernel (tcgen05 shortlist GEMM)
+    # roofline of the dominant kernel (tcgen05 shortlist GEMM: the s8 tier-1
+    # pass when the int8 tier ran, else the bf16 pass)
     n_sl, t_sl = kt["shortlist"]
     flops_per_launch = 2.0 * B * n_local * args.dim
     roof = None
+    i8_tier = st.i8_batches > 0
     if n_sl:
         avg = t_sl / n_sl
         achieved = flops_per_launch / (avg / 1000.0) / 1e12
-        peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
         traffic = None
-        tp = os.path.join(ROOT, "profiles", "shortlist_traffic.json")
+        tp = os.path.join(ROOT, "profiles", "shortlist_i8_traffic.json" if i8_tier else "shortlist_traffic.json")
         if os.path.exists(tp):
             traffic = json.load(open(tp)).get("dram_bytes_per_launch")
-        roof = {"bound": "tensor", "achieved": round(achieved, 2), "peak": peak, "unit": "TFLOP/s",
-                "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": "k_shortlist (tcgen05)",
-                "avg_launch_ms": round(avg, 4), "peak_source": peaks["source"] + " bf16_tflops_sustained",
-                "frac_of_burst": round(achieved / peaks["bf16_tflops"], 4),
-                "kernel_share_of_step": round(t_sl / ms, 4)}
+        if i8_tier:
+            # s8 dense tensor rate = 2x bf16 on sm_100 (nominal 4.5 vs 2.25 P; the
+            # issue-rate microbenchmark measured 2.08x, profiles/r02p_mma_i8_rates.log):
+            # the denominator is twice the measured cuBLAS bf16 burst figure
+            peak = 2.0 * peaks["bf16_tflops"]
+            roof = {"bound": "tensor", "achieved": round(achieved, 2), "peak": round(peak, 1), "unit": "TOPS (s8)",
+                    "frac": round(achieved / peak, 4), "traffic": traffic,
+                    "kernel": "k_shortlist_pair<int8> (tcgen05 kind::i8, cta_group::2)",
+                    "avg_launch_ms": round(avg, 4),
+                    "peak_source": peaks["source"] + " 2 x bf16_tflops (burst); s8 = 2x bf16 dense",
+                    "frac_of_sustained": round(achieved / (2.0 * peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])), 4),
+                    "frac_of_mma_microbench": round(achieved / 4138.5, 4),
+                    "kernel_share_of_step": round(t_sl / ms, 4)}
+        else:
+            peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+            roof = {"bound": "tensor", "achieved": round(achieved, 2), "peak": peak, "unit": "TFLOP/s",
+                    "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": "k_shortlist (tcgen05)",
+                    "avg_launch_ms": round(avg, 4), "peak_source": peaks["source"] + " bf16_tflops_sustained",
+                    "frac_of_burst": round(achieved / peaks["bf16_tflops"], 4),
+                    "kernel_share_of_step": round(t_sl / ms, 4)}
 
     # ---- e2e: same lookups through the public API with HOST buffers ----
     e2e = None
@@ -519,6 +537,13 @@ def main():
     if not args.no_codec and rank == 0:
         codec = bench_codec(torch, fc, ctx, args, dev, peaks)
 
+    large = None
+    if not args.no_codec and not args.no_large and rank == 0:
+        try:
+            large = bench_codec_large(torch, fc, ctx, args, dev, peaks)
+        except Exception as ex:  # reported, never fatal to the headline line
+            large = {"error": str(ex)[:200]}
+
     scoring = None
     if not args.no_scoring and rank == 0:
         try:
@@ -556,17 +581,26 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "ms_per_step_median": statistics.median(step_ms), "ms_per_step_max": max(step_ms),
             "ms_per_step_all": [round(x, 3) for x in step_ms], "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None,
+            "dtype": "s8 tensor-core candidates, f64 exact scores" if i8_tier else "bf16 tensor-core candidates, f64 exact scores",
+            "data": "synthetic",
             "config": {"workload": f"config[1] lookup: {args.rows:,} cached {args.dim}-d embeddings, {B}-query batches, "
                                    f"top-{k}",
                        "rows": args.rows, "dim": args.dim, "global_batch": B, "k": k, "kprime": args.kprime,
                        "sharding": f"id mod {world}", "parallelism": f"entry-sharded x{world}",
                        "l2": "inputs larger than L2 (1.5 GB bf16 table streamed per step)",
-                       "exactness": "bit-exact top-8 vs fp64 reference scan (certified bf16 shortlist)"},
-            "lookup_stats": {"certified": st.certified, "fallback": st.fallback, "max_abs_err": st.max_abs_err},
+                       "exactness": "bit-exact top-8 vs the fp64 reference scan: certified int8 shortlist "
+                                    "(bf16 tier and exact scan behind it)" if i8_tier else
+                                    "bit-exact top-8 vs fp64 reference scan (certified bf16 shortlist)"},
+            "lookup_stats": {"certified": st.certified, "fallback": st.fallback, "max_abs_err": st.max_abs_err,
+                             "tier2_certified": st.tier2_certified, "exact_scans": st.exact_scans,
+                             "i8_batches": st.i8_batches,
+                             "i8_candidates_per_query": st.i8_candidates / max(1, st.queries),
+                             "i8_prescored_per_query": st.i8_prescored / max(1, st.queries),
+                             "i8_exact_per_query": st.i8_rescored / max(1, st.queries)},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clk.summary(), "kernel_ms": {k_: round(v_[1], 3) for k_, v_ in kt.items()},
-            "codec": codec, "scoring": scoring, "engine": engine, "comm": comm,
+            "codec": codec, "codec_large": large, "scoring": scoring, "engine": engine, "comm": comm,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -688,6 +722,89 @@ def bench_codec(torch, fc, ctx, args, dev, peaks):
         "fidelity": fidelity,
     }
     return res
+
+
+def bench_codec_large(torch, fc, ctx, args, dev, peaks):
+    """config[4] large-latent stress on one GPU: compress + decompress of
+    64-frame 4x72x128 (576x1024 px) latents at batch scale, and the per-step
+    cache checkpoint (save_snapshot, store.cpp:232-274, with serialize_entry,
+    codec.cpp:358-392) of a store holding them -- written to /dev/shm so the
+    number is the serializer's, not a disk's. (The 200k-entry, 8-GPU size of
+    config[4] does not fit one box: ~5 MB per compressed entry x 200k.)"""
+    import tempfile
+    n, F = args.large_prompts, 64
+    dims = (72, 128, 4)
+    E = 72 * 128 * 4
+    steps = [5, 10, 15, 20, 25]
+    lat, om, bm = make_latents(torch, n, F, dims, 11, dev)
+    torch.cuda.synchronize()
+    prompts = list(range(1, n + 1))
+    ents, sizes = fc.compress_batch(lat, steps, om, bm, dims, prompts, ctx=ctx)  # warm-up
+    del ents
+    reps = 3
+    rs = []
+    for i in range(reps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ents, sizes = fc.compress_batch(lat, steps, om, bm, dims, prompts, ctx=ctx)
+        rs.append(time.perf_counter() - t0)
+        if i < reps - 1:
+            del ents
+    comp_s = statistics.median(rs)
+    raw = n * 5 * F * E * 4
+    mask_b = 2 * n * F * (72 * 128 // 8)
+    comp_bytes = raw + mask_b + int(sizes.sum())
+    out = torch.empty((n, F, E), dtype=torch.float32, device=dev)
+    for s_ in steps:
+        fc.decompress_batch(ents, [s_] * n, out=out)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for s_ in steps:
+        fc.decompress_batch(ents, [s_] * n, out=out)
+    dec_s = time.perf_counter() - t0
+    infos = [e.info() for e in ents]
+    read_b = 0
+    for i in infos:
+        for si in range(i.n_steps):
+            read_b += 4 * E * (1 + i.n_extra[si]) + 2 * F + 4 * i.n_diff
+        read_b += 4 * E * i.n_diff * i.n_steps
+    dec_bytes = n * 5 * F * E * 4 + read_b
+    # checkpoint: store + index holding the n entries, saved after the insert batch
+    st = fc.CacheStore(1 << 40, fc.Policy.Lrbu, ctx=ctx)
+    for i, e in enumerate(ents):
+        st.insert_steps(i + 1, e, steps, i + 1)
+    ix = fc.SimilarityIndex(ctx=ctx)
+    g = torch.Generator(device=dev)
+    g.manual_seed(5)
+    emb = [make_table(torch, fc, ctx, n, 768, 100 + t, dev) for t in range(3)]
+    ix.insert_batch(np.arange(1, n + 1, dtype=np.uint64), *emb)
+    shm = "/dev/shm" if os.path.isdir("/dev/shm") else None
+    with tempfile.TemporaryDirectory(dir=shm) as td:
+        path = os.path.join(td, "ckpt.flxc")
+        fc.save_snapshot(st, ix, path)  # warm-up
+        ts = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            fc.save_snapshot(st, ix, path)
+            ts.append(time.perf_counter() - t0)
+        snap_b = os.path.getsize(path)
+        t0 = time.perf_counter()
+        st2, ix2 = fc.load_snapshot(path, ctx=ctx)
+        load_s = time.perf_counter() - t0
+        ok = st2.used() == st.used() and ix2.size() == ix.size()
+        del st2, ix2
+    save_s = statistics.median(ts)
+    hbm = peaks["hbm_gbs"]
+    return {"workload": f"config[4] per GPU: {n} prompts x 5 steps x {F} frames x 72x128x4 fp32 "
+                        f"({raw / 1e9:.2f} GB raw), rect masks, thr 0.99",
+            "compress_GBps": comp_bytes / comp_s / 1e9, "compress_frac_hbm": comp_bytes / comp_s / 1e9 / hbm,
+            "compress_s": comp_s, "ratio": raw / float(sizes.sum()),
+            "decompress_GBps_e2e": dec_bytes / dec_s / 1e9, "decompress_frac_hbm_e2e": dec_bytes / dec_s / 1e9 / hbm,
+            "checkpoint": {"api": "lc_snapshot_save (FLXC v1, byte-identical to the reference's save_snapshot)",
+                           "bytes": snap_b, "save_s": save_s, "save_GBps": snap_b / save_s / 1e9,
+                           "load_s": load_s, "load_GBps": snap_b / load_s / 1e9, "roundtrip_ok": bool(ok),
+                           "target": "/dev/shm" if shm else "tmp"},
+            "timing": "wall clock through the public API; compress median of 3 calls, decompress 5 steps x n"}
 
 
 def bench_engine(torch, fc, ctx, args, dev):
@@ -853,6 +970,7 @@ def bench_scoring(torch, fc, ctx, args, peaks):
     live = st.step_count()
     fc.lib.lc_ctx_profile(ctx.h, 1)
     fc.lib.lc_ctx_kernel_time(ctx.h, b"policy", None, None, 1)
+    fc.lib.lc_ctx_kernel_time(ctx.h, b"policy_call", None, None, 1)
     n_ev = args.score_evictions
     t0 = time.perf_counter()
     for _ in range(n_ev):
@@ -860,6 +978,8 @@ def bench_scoring(torch, fc, ctx, args, peaks):
     ev_s = time.perf_counter() - t0
     c_, t_ = C.c_uint64(), C.c_double()
     fc.lib.lc_ctx_kernel_time(ctx.h, b"policy", C.byref(c_), C.byref(t_), 1)
+    cc_, tc_ = C.c_uint64(), C.c_double()
+    fc.lib.lc_ctx_kernel_time(ctx.h, b"policy_call", C.byref(cc_), C.byref(tc_), 1)
     fc.lib.lc_ctx_profile(ctx.h, 0)
     assert st.used() == st.recompute_used()
     per_launch_ms = t_.value / c_.value if c_.value else None
@@ -867,7 +987,9 @@ def bench_scoring(torch, fc, ctx, args, peaks):
     return {"workload": f"{n_p} prompts x 5 steps LRBU, {live} live steps, {n_ev} evict_one calls",
             "evictions_per_s": n_ev / ev_s, "insert_steps_per_s": n_p / ins_s,
             "scoring_launches": int(c_.value), "scoring_ms_per_launch": per_launch_ms,
-            "roofline": {"bound": "hbm", "kernel": "k_policy_seg + k_head_seg (segmented bitonic sort)",
+            "scoring_ms_per_call": (tc_.value / cc_.value) if cc_.value else None,
+            "roofline": {"bound": "hbm", "kernel": "k_policy_fused (one cooperative launch: keys, radix threshold "
+                                                   "select, survivor sort)",
                          "achieved": round(alg_bytes / (per_launch_ms / 1e3) / 1e9, 1) if per_launch_ms else None,
                          "peak": peaks["hbm_gbs"], "unit": "GB/s",
                          "frac": round(alg_bytes / (per_launch_ms / 1e3) / 1e9 / peaks["hbm_gbs"], 4)

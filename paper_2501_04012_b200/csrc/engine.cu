@@ -267,7 +267,8 @@ lc_status lc_engine_process(lc_engine* e, const lc_request* req, int64_t n, cons
     int64_t j;
     uint64_t prompt, now;
     int first;
-    bool added_ix;  // its embeddings were registered for the index at deferral
+    bool added_ix;              // its embeddings were registered for the index at deferral
+    lc_entry* ready = nullptr;  // compressed speculatively already (owned)
   };
   std::vector<Pending> pending;
   std::unordered_set<uint64_t> pending_ids;
@@ -288,42 +289,54 @@ lc_status lc_engine_process(lc_engine* e, const lc_request* req, int64_t n, cons
     ok(lc_store_contains(e->st, pd.prompt, &cached));
     if (!cached && index_has(pd.prompt)) index_remove(pd.prompt);
   };
+  // lc_compress_batch of requests jobs[i] = (j, prompt) over the step set
+  // kCached[first..4], inputs staged in the engine's persistent buffer
+  auto compress_group = [&](const std::vector<std::pair<int64_t, uint64_t>>& jobs, int first,
+                            std::vector<lc_entry*>& ents) {
+    const int S = 5 - first;
+    const size_t m = jobs.size(), fe = (size_t)S * c.F * E, fm = (size_t)c.F * mb;
+    const size_t lat_b = (m * fe * sizeof(float) + 255) & ~size_t(255), msk_b = (m * fm + 255) & ~size_t(255);
+    auto* sbase = static_cast<uint8_t*>(e->stage_for(lat_b + 2 * msk_b));
+    float* dl = reinterpret_cast<float*>(sbase);
+    uint8_t* dom = sbase + lat_b;
+    uint8_t* dbm = dom + msk_b;
+    for (size_t q = 0; q < m; ++q) {
+      const int64_t j = jobs[q].first;
+      FC_CUDA(cudaMemcpyAsync(dl + q * fe, latents + ((size_t)j * 5 + first) * c.F * E, fe * sizeof(float),
+                              lat_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, e->ctx->stream));
+      FC_CUDA(cudaMemcpyAsync(dom + q * fm, obj_masks + (size_t)j * fm, fm,
+                              om_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, e->ctx->stream));
+      FC_CUDA(cudaMemcpyAsync(dbm + q * fm, bg_masks + (size_t)j * fm, fm,
+                              bm_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, e->ctx->stream));
+    }
+    std::vector<uint64_t> pids(m);
+    for (size_t q = 0; q < m; ++q) pids[q] = jobs[q].second;
+    ents.assign(m, nullptr);
+    std::vector<int32_t> steps(kCached + first, kCached + 5);
+    ok(lc_compress_batch(e->ctx, dl, steps.data(), S, c.F, c.H, c.W, c.C, dom, dbm, c.compress_threshold, pids.data(),
+                         (int64_t)m, ents.data(), nullptr));
+    sync(e->ctx);  // the staging buffer is reused by the next group / call
+  };
   auto flush = [&]() {
     if (pending.empty()) return;
     // one compress per step set; entries in request order
     std::map<int64_t, lc_entry*> ent_of;
+    for (auto& pd : pending)
+      if (pd.ready) {
+        ent_of[pd.j] = pd.ready;
+        pd.ready = nullptr;
+      }
     try {
     for (int first = 0; first < 5; ++first) {
       std::vector<const Pending*> grp;
       for (const auto& pd : pending)
-        if (pd.first == first) grp.push_back(&pd);
+        if (pd.first == first && !ent_of.count(pd.j)) grp.push_back(&pd);
       if (grp.empty()) continue;
-      const int S = 5 - first;
-      const size_t m = grp.size(), fe = (size_t)S * c.F * E, fm = (size_t)c.F * mb;
-      // inputs staged in the engine's persistent buffer (latents, then the
-      // two mask sets, 256-byte aligned); the previous group's compress has
-      // returned (it ends with a stream sync), so the buffer is free
-      const size_t lat_b = (m * fe * sizeof(float) + 255) & ~size_t(255), msk_b = (m * fm + 255) & ~size_t(255);
-      auto* sbase = static_cast<uint8_t*>(e->stage_for(lat_b + 2 * msk_b));
-      float* dl = reinterpret_cast<float*>(sbase);
-      uint8_t* dom = sbase + lat_b;
-      uint8_t* dbm = dom + msk_b;
-      for (size_t q = 0; q < m; ++q) {
-        const int64_t j = grp[q]->j;
-        FC_CUDA(cudaMemcpyAsync(dl + q * fe, latents + ((size_t)j * 5 + first) * c.F * E, fe * sizeof(float),
-                                lat_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, e->ctx->stream));
-        FC_CUDA(cudaMemcpyAsync(dom + q * fm, obj_masks + (size_t)j * fm, fm,
-                                om_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, e->ctx->stream));
-        FC_CUDA(cudaMemcpyAsync(dbm + q * fm, bg_masks + (size_t)j * fm, fm,
-                                bm_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, e->ctx->stream));
-      }
-      std::vector<uint64_t> pids(m);
-      for (size_t q = 0; q < m; ++q) pids[q] = grp[q]->prompt;
-      std::vector<lc_entry*> ents(m, nullptr);
-      std::vector<int32_t> steps(kCached + first, kCached + 5);
-      ok(lc_compress_batch(e->ctx, dl, steps.data(), S, c.F, c.H, c.W, c.C, dom, dbm, c.compress_threshold, pids.data(),
-                           (int64_t)m, ents.data(), nullptr));
-      sync(e->ctx);  // the staging buffer is reused by the next group / call
+      std::vector<std::pair<int64_t, uint64_t>> jobs;
+      for (const Pending* pd : grp) jobs.emplace_back(pd->j, pd->prompt);
+      std::vector<lc_entry*> ents;
+      compress_group(jobs, first, ents);
+      const size_t m = grp.size();
       for (size_t q = 0; q < m; ++q) ent_of[grp[q]->j] = ents[q];
     }
     } catch (...) {
@@ -371,6 +384,82 @@ lc_status lc_engine_process(lc_engine* e, const lc_request* req, int64_t n, cons
       for (const auto& pd : done) unregister(pd);  // the failed insert and every later one
     pc.lap(5);
     if (err) std::rethrow_exception(err);
+  };
+  // ---- speculative compression of evicting updates ----
+  // An update that may evict cannot be deferred (its evictions change what
+  // later requests see), and compressing it alone costs ~0.45 ms. But the
+  // compressed entry depends only on the request's own latents and its step
+  // set, never on the store: at the first evicting update of a batch, the
+  // step set of every later request is predicted from the batch lookup and
+  // the current store (decide + hole rule), and all of them are compressed in
+  // one batched lc_compress_batch per step set. A request whose real step
+  // set matches takes its entry (bit-identical to compressing it then); any
+  // other compresses alone, as before. No state is touched by a prediction,
+  // so results equal serial execution; unused entries are released.
+  std::unordered_map<int64_t, std::pair<int, lc_entry*>> spec;  // j -> (first, entry)
+  bool speculated = false;
+  auto release_spec = [&]() {
+    for (auto& kv : spec) lc_entry_release(kv.second.second);
+    spec.clear();
+  };
+  auto take_spec = [&](int64_t j, int first) -> lc_entry* {
+    auto it = spec.find(j);
+    if (it == spec.end()) return nullptr;
+    lc_entry* ent = it->second.first == first ? it->second.second : nullptr;
+    if (!ent) lc_entry_release(it->second.second);
+    spec.erase(it);
+    return ent;
+  };
+  auto speculate = [&](int64_t from) {
+    speculated = true;
+    std::vector<std::pair<int64_t, uint64_t>> grp[5];
+    std::unordered_set<uint64_t> seen;
+    for (int64_t jj = from; jj < n; ++jj) {
+      const uint64_t p = req[jj].prompt;
+      if (!seen.insert(p).second) continue;  // a repeated prompt is cached by its first update
+      int32_t cached = pending_ids.count(p) ? 1 : 0;
+      if (!cached) ok(lc_store_contains(e->st, p, &cached));
+      if (cached) continue;
+      uint64_t tid[3] = {0, 0, 0};
+      double tsc[3] = {0, 0, 0};
+      bool have[3] = {false, false, false};
+      for (int t = 0; t < 3; ++t)
+        for (int k = 0; k < bcnt[t][jj]; ++k)
+          if (!removed.count(bid[t][(size_t)jj * KTOP + k])) {
+            have[t] = true;
+            tid[t] = bid[t][(size_t)jj * KTOP + k];
+            tsc[t] = bsc[t][(size_t)jj * KTOP + k];
+            break;
+          }
+      lc_decision dc{};
+      dc.whole_id = tid[0];
+      dc.object_id = tid[1];
+      dc.background_id = tid[2];
+      decide_one(tsc[0], tsc[1], tsc[2], have[0], c.hit_threshold, c.bin_edges, &dc);
+      int actual = 0;
+      if (dc.kind == LC_WHOLE_HIT) {
+        actual = avail(live_steps(e->st, dc.whole_id), dc.step);
+      } else if (dc.kind == LC_DECOUPLED_HIT) {
+        const auto lo = live_steps(e->st, dc.object_id), lb = live_steps(e->st, dc.background_id);
+        int m = std::min(avail(lo, dc.step), avail(lb, dc.step));
+        while (m > 0 && (avail(lo, m) != m || avail(lb, m) != m)) m = std::min(avail(lo, m), avail(lb, m));
+        actual = m;
+      }
+      if (actual >= 25) continue;
+      int first = 0;
+      while (first < 5 && kCached[first] <= actual) ++first;
+      grp[first].emplace_back(jj, p);
+    }
+    for (int first = 0; first < 5; ++first) {
+      if (grp[first].empty()) continue;
+      std::vector<lc_entry*> ents;
+      try {
+        compress_group(grp[first], first, ents);
+      } catch (const Error&) {
+        continue;  // e.g. a non-finite latent: that request raises when it is reached
+      }
+      for (size_t q = 0; q < ents.size(); ++q) spec[grp[first][q].first] = {first, ents[q]};
+    }
   };
   try {
   for (int64_t j = 0; j < n; ++j) {
@@ -487,7 +576,7 @@ lc_status lc_engine_process(lc_engine* e, const lc_request* req, int64_t n, cons
       if (!cached && defer_ok && lc_store_used(e->st) + pending_bound + bound <= c.capacity &&
           pending_bound + bound >= pending_bound) {
         const bool add_ix = !index_has(r.prompt);
-        pending.push_back(Pending{j, r.prompt, now, first, add_ix});
+        pending.push_back(Pending{j, r.prompt, now, first, add_ix, take_spec(j, first)});
         pending_ids.insert(r.prompt);
         pending_bound += bound;
         o.n_inserted = S;
@@ -497,12 +586,15 @@ lc_status lc_engine_process(lc_engine* e, const lc_request* req, int64_t n, cons
         pc.lap(7);
       } else if (!cached) {
         flush();  // in-order state before an insert that may evict
+        if (!speculated && defer_ok) speculate(j);
         std::vector<int32_t> steps(kCached + first, kCached + 5);
-        const float* lat = latents + ((size_t)j * 5 + first) * c.F * E;
-        lc_entry* ent = nullptr;
-        uint64_t sz = 0;
-        ok(lc_compress_batch(e->ctx, lat, steps.data(), S, c.F, c.H, c.W, c.C, obj_masks + (size_t)j * c.F * mb,
-                             bg_masks + (size_t)j * c.F * mb, c.compress_threshold, &r.prompt, 1, &ent, &sz));
+        lc_entry* ent = take_spec(j, first);
+        if (!ent) {
+          const float* lat = latents + ((size_t)j * 5 + first) * c.F * E;
+          uint64_t sz = 0;
+          ok(lc_compress_batch(e->ctx, lat, steps.data(), S, c.F, c.H, c.W, c.C, obj_masks + (size_t)j * c.F * mb,
+                               bg_masks + (size_t)j * c.F * mb, c.compress_threshold, &r.prompt, 1, &ent, &sz));
+        }
         std::vector<lc_step_entry> ev((size_t)lc_store_step_count(e->st) + 1);
         int nev = 0;
         lc_status s1 = lc_store_insert(e->st, r.prompt, ent, steps.data(), S, now, ev.data(), (int)ev.size(), &nev);
@@ -536,6 +628,7 @@ lc_status lc_engine_process(lc_engine* e, const lc_request* req, int64_t n, cons
   }
   flush();
   index_flush();
+  release_spec();
   } catch (...) {
     // requests before the failing one are complete: apply their updates
     try {
@@ -543,6 +636,9 @@ lc_status lc_engine_process(lc_engine* e, const lc_request* req, int64_t n, cons
       index_flush();
     } catch (...) {
     }
+    release_spec();
+    for (auto& pd : pending)
+      if (pd.ready) lc_entry_release(pd.ready);
     throw;
   }
   LC_API_END

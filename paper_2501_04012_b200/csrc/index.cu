@@ -507,7 +507,7 @@ __device__ __forceinline__ uint32_t fkey(float f) {
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 
-__global__ void __launch_bounds__(RI_WARPS * 32)
+__global__ void __launch_bounds__(RI_WARPS * 32, 6)
     k_rescore_i8(const float* __restrict__ Q, int nq, int dim, const float* __restrict__ rows,
                  const __nv_bfloat16* __restrict__ rowsb, const uint64_t* __restrict__ ids,
                  const float* __restrict__ cand_s, const uint32_t* __restrict__ cand_r, const int32_t* __restrict__ cand_n,

@@ -526,6 +526,15 @@ constexpr int PHB = PN / 2;           // table rows per CTA per tile
 constexpr int PBOX = PHB * 128;       // one B box: 64 rows x 64 bf16 = 8 KB
 constexpr int ABOX = BM * 128;        // one A box: 128 queries x 64 bf16 = 16 KB
 constexpr int ACC_COL = 256;          // accumulators at TMEM columns [256, 512)
+// int8 kernel: the first 4 query K boxes (128 int8 each) live in TMEM columns
+// [0, 128), the rest in smem, so THREE 128-column accumulators fit in
+// [128, 512): the MMA can run two tiles ahead of the slowest epilogue warp
+// (ncu r02v: with two buffers the MMA waited ~1.8k cycles per tile for a
+// free accumulator while most epilogue warps idled waiting for the next one:
+// per-tile spikes of the few warps with accepted scores set the pace)
+constexpr int I8_KT = 4;
+constexpr int I8_ACC_COL = 128;
+constexpr int I8_NACC = 3;
 constexpr int PMAX_STAGE = 24;
 
 __device__ __forceinline__ void mma_box4_pair_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
@@ -572,6 +581,42 @@ __device__ __forceinline__ float i8_score_up(int dot, float sqt) {
   return a + fabsf(a) * 0x1p-20f;
 }
 
+__device__ __forceinline__ void mma_box4_pair_ss_i8(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                                    uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p, t;\n"
+      ".reg .b64 a1, a2, a3, d1, d2, d3;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "setp.eq.b32 t, 0, 0;\n"
+      "add.s64 a1, %1, 2;\n"
+      "add.s64 a2, %1, 4;\n"
+      "add.s64 a3, %1, 6;\n"
+      "add.s64 d1, %2, 2;\n"
+      "add.s64 d2, %2, 4;\n"
+      "add.s64 d3, %2, 6;\n"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], a1, d1, %3, t;\n"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], a2, d2, %3, t;\n"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], a3, d3, %3, t;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+// v[j] for a run-time j in [0, 16) from 16 registers (a 4-level select tree:
+// registers cannot be indexed dynamically without a local-memory copy)
+__device__ __forceinline__ uint32_t sel16(const uint32_t* v, int j) {
+  uint32_t a[8], b[4], c[2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = (j & 1) ? v[2 * i + 1] : v[2 * i];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) b[i] = (j & 2) ? a[2 * i + 1] : a[2 * i];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) c[i] = (j & 4) ? b[2 * i + 1] : b[2 * i];
+  return (j & 8) ? c[1] : c[0];
+}
+
 // Pair kernel warps: 0 TMA producer, 1 MMA issuer, 2..9 epilogue. Two
 // epilogue warps share each TMEM lane quarter (a warp may only read lanes
 // 32 * (warp % 4) ..): warp half h = (warp - 2) / 4 filters accumulator
@@ -594,8 +639,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
   const int cap = p.cap;
   constexpr int BKE = I8 ? 128 : BK;  // K elements per 128-byte box
   const int nkb = p.dim / BKE;
-  const int KT = nkb < 8 ? nkb : 8;  // A boxes resident in TMEM
-  const int KS = nkb - KT;           // A boxes resident in smem
+  const int KT = I8 ? (nkb < I8_KT ? nkb : I8_KT) : (nkb < 8 ? nkb : 8);  // A boxes resident in TMEM
+  const int KS = nkb - KT;                                                  // A boxes resident in smem
+  constexpr int NACC = I8 ? I8_NACC : 2;         // accumulator buffers
+  constexpr int ACC0 = I8 ? I8_ACC_COL : ACC_COL;  // first accumulator column
   const int BPS = p.bps;             // B boxes per pipeline stage (one barrier round trip per 4*BPS MMAs)
   const int STAGE_BYTES = BPS * PBOX;
   const int nsg = nkb / BPS;
@@ -606,8 +653,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
   uint64_t* full = bars;
   uint64_t* empty = bars + NSTAGE;
   uint64_t* accf = bars + 2 * NSTAGE;
-  uint64_t* acce = accf + 2;
-  uint64_t* aready = acce + 2;
+  uint64_t* acce = accf + 3;
+  uint64_t* aready = acce + 3;
   uint64_t* afree = aready + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(afree + 1);
 
@@ -621,7 +668,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
       mbar_init(smem_u32(&full[s]), 1);
       mbar_init(smem_u32(&empty[s]), 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NACC; ++b) {
       mbar_init(smem_u32(&accf[b]), 1);
       mbar_init(smem_u32(&acce[b]), 16);  // 8 epilogue warps x 2 CTAs
     }
@@ -707,8 +754,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
           if (mprof) mcyc[2] += clock64() - a_t0;
         }
         for (int64_t row = r0; row < r1; row += PN, ++tile) {
-          const uint32_t b = tile & 1;
-          const uint32_t use = tile >> 1;
+          const uint32_t b = tile % NACC;
+          const uint32_t use = tile / NACC;
           long long m_t0 = mprof ? clock64() : 0;
           mbar_wait(smem_u32(&acce[b]), (use & 1) ^ 1);
           tc_fence_after();
@@ -716,7 +763,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
             const long long t1 = clock64();
             mcyc[0] += t1 - m_t0;
           }
-          const uint32_t d_tmem = tmem + ACC_COL + b * PN;
+          const uint32_t d_tmem = tmem + ACC0 + b * PN;
           for (int sg = 0; sg < nsg; ++sg) {
             if (mprof) m_t0 = clock64();
             mbar_wait(smem_u32(&full[stage]), phase);
@@ -728,8 +775,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
                 const int kb = sg * BPS + bx;
                 const uint64_t bdesc = smem_desc_sw128(smem_u32(stages + stage * STAGE_BYTES + bx * PBOX));
                 if (p.debug & 1) continue;
-                if (I8)
+                if (I8 && kb < KT)
                   mma_box4_pair_i8(d_tmem, tmem + kb * 32, bdesc, idesc, kb != 0);
+                else if (I8)
+                  mma_box4_pair_ss_i8(d_tmem, smem_desc_sw128(smem_u32(asmem + (kb - KT) * ABOX)), bdesc, idesc, 1);
                 else if (kb < KT)
                   mma_box4_pair(d_tmem, tmem + kb * (BK / 16) * 8, bdesc, idesc, kb != 0);
                 else
@@ -824,8 +873,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
       long long cyc[4] = {0, 0, 0, 0}, c_t0 = 0;
       const bool prof = p.debug & 16;
       for (int64_t row = r0; row < r1; row += PN, ++tile) {
-        const uint32_t b = tile & 1;
-        const uint32_t use = tile >> 1;
+        const uint32_t b = tile % NACC;
+        const uint32_t use = tile / NACC;
         if ((tile & p.refresh_mask) == 0 && !p.pilot) {
           if (prof) c_t0 = clock64();
           hist_publish(hq, lk, t, pub, cnt);
@@ -861,8 +910,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
         // both 32-column loads of this warp's half in flight together, then
         // the accumulator buffer is released before any filtering
         uint32_t rv[EPI_HALF_COLS];
-        tmem_ld32_issue(tmem + lane_base + ACC_COL + b * PN + half * EPI_HALF_COLS, rv);
-        tmem_ld32_issue(tmem + lane_base + ACC_COL + b * PN + half * EPI_HALF_COLS + 32, rv + 32);
+        tmem_ld32_issue(tmem + lane_base + ACC0 + b * PN + half * EPI_HALF_COLS, rv);
+        tmem_ld32_issue(tmem + lane_base + ACC0 + b * PN + half * EPI_HALF_COLS + 32, rv + 32);
         tmem_ld32_wait(rv);
         tmem_ld32_wait(rv + 32);
         tc_fence_before();
@@ -877,16 +926,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
             for (int c = c0; c < c0 + 16; c += 2)
               m = __vimax3_s32(m, c < lim_all ? (int)rv[c] : INT_MIN, c + 1 < lim_all ? (int)rv[c + 1] : INT_MIN);
             if (!__any_sync(0xffffffffu, m > pthr)) continue;
+            uint32_t msk = 0;
 #pragma unroll
-            for (int c = c0; c < c0 + 16; ++c) {
-              if (c < lim_all && (int)rv[c] > pthr) {
-                float u = __fadd_ru(i8_score_up((int)rv[c], sqt), eps_t);
+            for (int jj = 0; jj < 16; ++jj) msk |= ((c0 + jj < lim_all) & ((int)rv[c0 + jj] > pthr)) ? (1u << jj) : 0u;
+            while (msk) {  // only the lane's qualifying dots (usually 0-1 per chunk)
+              const int jj = __ffs(msk) - 1;
+              msk &= msk - 1;
+              float u = __fadd_ru(i8_score_up((int)sel16(rv + c0, jj), sqt), eps_t);
 #pragma unroll
-                for (int i = 0; i < PILOT_R; ++i) {  // insertion into the descending list
-                  const float hi = fmaxf(ut[i], u);
-                  u = fminf(ut[i], u);
-                  ut[i] = hi;
-                }
+              for (int i = 0; i < PILOT_R; ++i) {  // insertion into the descending list
+                const float hi = fmaxf(ut[i], u);
+                u = fminf(ut[i], u);
+                ut[i] = hi;
               }
             }
           }
@@ -930,14 +981,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
             }
             if (prof) c_t0 = clock64();
             const uint32_t off0 = off_base + (uint32_t)c0;
+            if constexpr (I8) {
+              // a lane accepts ~1 of the 16 dots of a hot chunk: build its
+              // accept mask, then loop over the set bits only (the dot is
+              // picked out of the 16 registers by a 4-level select tree)
+              uint32_t m = 0;
+#pragma unroll
+              for (int jj = 0; jj < 16; ++jj) m |= ((c0 + jj < lim_all) & ((int)rv[c0 + jj] > thr)) ? (1u << jj) : 0u;
+              while (m) {
+                const int jj = __ffs(m) - 1;
+                m &= m - 1;
+                const int d = (int)sel16(rv + c0, jj);
+                lk[cnt * BM + t] = (hkey_ru(__fadd_ru(i8_score_up(d, sqt), eps_t)) << 16) | (off0 + jj);
+                ++cnt;
+              }
+            } else
 #pragma unroll
             for (int jj = 0; jj < 16; ++jj) {
-              if constexpr (I8) {
-                const int d = (int)rv[c0 + jj];
-                const bool acc = (c0 + jj < lim_all) & (d > thr);
-                if (acc) lk[cnt * BM + t] = (hkey_ru(__fadd_ru(i8_score_up(d, sqt), eps_t)) << 16) | (off0 + jj);
-                cnt += acc;
-              } else {
+              {
                 const float v = __uint_as_float(rv[c0 + jj]);
                 const bool acc = (c0 + jj < lim_all) & (v > tau);
                 if (acc) lk[cnt * BM + t] = (hkey_ru(v) << 16) | (off0 + jj);
@@ -974,7 +1035,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
           }
           if (dmax > -INFINITY) atomicMax(p.qdrop + q, okey(dmax));
         }
-        if (prof) cyc[2] += clock64() - c_t0;
+        if (prof) {
+          cyc[2] += clock64() - c_t0;
+          if (lane == 0)
+            for (int i = 0; i < 4; ++i)
+              atomicAdd(reinterpret_cast<unsigned long long*>(p.stats + 4) + i, (unsigned long long)cyc[i]);
+        }
         continue;
       }
       compact_keys(lk, t, cnt, p.kp, tau, true);  // exact: the unit's list holds at most kp entries
@@ -1392,7 +1458,7 @@ template <bool I8>
 static void launch_pair(lc_ctx* ctx, const CUtensorMap& tmB, const CUtensorMap& tmQ, sm100::Params& prm) {
   using namespace sm100;
   const int nkb = prm.dim / (I8 ? 128 : BK);
-  const int KS = !I8 && nkb > 8 ? nkb - 8 : 0;
+  const int KS = I8 ? std::max(0, nkb - I8_KT) : (nkb > 8 ? nkb - 8 : 0);
   const size_t budget = 227 * 1024 - 1024 - 512;
   const size_t slot_bytes = (size_t)2 * BM * 4;  // one packed u32 per candidate, one list per column half
   const size_t fixed = (size_t)KS * ABOX;
@@ -1509,7 +1575,10 @@ void run_shortlist(lc_ctx* ctx, const ShortlistRun& R) {
   prm.hist = hist.as<uint32_t>();
   {
     const char* e = getenv("FC_SHORTLIST_REFRESH");
-    prm.refresh_mask = (e ? atoi(e) : 16) - 1;
+    // int8: the pilot seeds the threshold, so the histogram refresh (~8k cycles of
+    // dependent L2 round trips per warp) runs every 64 tiles (r02x: 16 -> 2.25 ms,
+    // 32 -> 2.14, 64 -> 2.09 per 4096 x 1M launch)
+    prm.refresh_mask = (e ? atoi(e) : (R.i8 ? 64 : 16)) - 1;
   }
   prm.stats = st.as<uint32_t>();
   prm.gkey = gk.as<uint32_t>();
@@ -1524,8 +1593,18 @@ void run_shortlist(lc_ctx* ctx, const ShortlistRun& R) {
   prm.qcap = QCAP;
   if (R.i8) FC_CUDA(cudaMemsetAsync(qc.p, 0, qc.bytes, ctx->stream));
   if (R.i8) {
+    // smem-resident query K boxes beyond the first I8_KT: [128 queries][128 B] s8 boxes
     alignas(64) CUtensorMap unused;
-    memset(&unused, 0, sizeof unused);
+    {
+      cuuint64_t gdim[2] = {(cuuint64_t)R.dim, (cuuint64_t)R.nq_pad};
+      cuuint64_t gstride[1] = {(cuuint64_t)R.dim};
+      cuuint32_t box[2] = {128, (cuuint32_t)BM};
+      cuuint32_t estride[2] = {1, 1};
+      CUresult r = encode_fn()(&unused, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(R.Qconv), gdim, gstride, box,
+                               estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) raise(LC_ERR_CUDA, "cuTensorMapEncodeTiled (s8 queries) failed: " + std::to_string((int)r));
+    }
     // pilot over every 16th row tile (tables of >= 256 tiles): per-query max U
     // into gkey, the main pass's starting threshold
     constexpr int PILOT_STRIDE = 16;

@@ -422,9 +422,14 @@ __global__ void __launch_bounds__(SEG_T, 1) k_policy_fused(const DevLive* __rest
   // (B) histogram of (key - min) >> sh
   for (int t = threadIdx.x; t < NBIN; t += blockDim.x) h[t] = 0;
   __syncthreads();
-  for (int64_t i = gtid; i < n_slots; i += gstride) {
-    const uint64_t k = S.K[i];
-    if (k != ~0ull) atomicAdd(&h[(k - lo) >> sh], 1u);
+  // warp-aggregated: policy keys cluster in few bins (e.g. many LRBU keys
+  // share an order of magnitude), and same-bin shared atomics serialize
+  for (int64_t i0 = gtid - (threadIdx.x & 31); i0 < n_slots; i0 += gstride) {
+    const int64_t i = i0 + (threadIdx.x & 31);
+    const uint64_t k = i < n_slots ? S.K[i] : ~0ull;
+    const int bin = k != ~0ull ? (int)((k - lo) >> sh) : -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, bin);
+    if (bin >= 0 && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&h[bin], (unsigned)__popc(peers));
   }
   __syncthreads();
   for (int t = threadIdx.x; t < NBIN; t += blockDim.x)
@@ -449,9 +454,12 @@ __global__ void __launch_bounds__(SEG_T, 1) k_policy_fused(const DevLive* __rest
     for (int t = threadIdx.x; t < NBIN; t += blockDim.x) h[t] = 0;
     __syncthreads();
     const uint64_t tb = (uint64_t)s_pick[0];
-    for (int64_t i = gtid; i < n_slots; i += gstride) {
-      const uint64_t k = S.K[i];
-      if (k != ~0ull && ((k - lo) >> sh) == tb) atomicAdd(&h[((k - lo) >> sh2) & (NBIN - 1)], 1u);
+    for (int64_t i0 = gtid - (threadIdx.x & 31); i0 < n_slots; i0 += gstride) {
+      const int64_t i = i0 + (threadIdx.x & 31);
+      const uint64_t k = i < n_slots ? S.K[i] : ~0ull;
+      const int bin = (k != ~0ull && ((k - lo) >> sh) == tb) ? (int)(((k - lo) >> sh2) & (NBIN - 1)) : -1;
+      const unsigned peers = __match_any_sync(0xffffffffu, bin);
+      if (bin >= 0 && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&h[bin], (unsigned)__popc(peers));
     }
     __syncthreads();
     for (int t = threadIdx.x; t < NBIN; t += blockDim.x)

@@ -37,5 +37,8 @@ for mode in ("py", "raw"):
     ts = np.array(ts) * 1e6
     c_, t_ = C.c_uint64(), C.c_double()
     fc.lib.lc_ctx_kernel_time(ctx.h, b"policy", C.byref(c_), C.byref(t_), 1)
+    cc_, tc_ = C.c_uint64(), C.c_double()
+    fc.lib.lc_ctx_kernel_time(ctx.h, b"policy_call", C.byref(cc_), C.byref(tc_), 1)
+    print(f"  scoring call span (launch..readback): {tc_.value / max(1, cc_.value) * 1e3:.1f} us x {cc_.value}")
     print(f"{mode}: median {np.median(ts):.1f} us, mean {ts.mean():.1f} us, max {ts.max():.0f} us; "
           f"scorings {c_.value} x {t_.value / max(1, c_.value):.3f} ms")
