@@ -73,7 +73,7 @@ def parse():
     ap.add_argument("--no-engine", action="store_true")
     ap.add_argument("--engine-cached", type=int, default=10_000)
     ap.add_argument("--engine-requests", type=int, default=1000)
-    ap.add_argument("--mixed-requests", type=int, default=4096)
+    ap.add_argument("--mixed-requests", type=int, default=16384)
     ap.add_argument("--mixed-capacity-gb", type=float, default=4.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-queries", type=int, default=0, help="reference sample size (0 = auto)")

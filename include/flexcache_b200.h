@@ -171,6 +171,7 @@ typedef struct lc_lookup_stats {
   uint64_t i8_rescored;   /* rows exact-scored by the int8 tier's rescore  */
   uint64_t i8_candidates; /* rows in the int8 tier's merged shortlists     */
   uint64_t i8_prescored;  /* of those, bf16 pre-scored by the rescore       */
+  uint64_t threshold_certified; /* fallbacks certified by the fixed-threshold int8 tier */
 } lc_lookup_stats;
 lc_status lc_index_stats(lc_index* ix, lc_lookup_stats* out, int reset);
 /* mode: 0 auto (tensor-core path when size >= 8192), 1 force exact scan,

@@ -78,7 +78,7 @@ class LatentSpec(C.Structure):
 class LookupStats(C.Structure):
     _fields_ = [("queries", u64), ("certified", u64), ("fallback", u64), ("exact_scans", u64),
                 ("max_abs_err", f64), ("tier2_certified", u64), ("i8_batches", u64), ("i8_rescored", u64),
-                ("i8_candidates", u64), ("i8_prescored", u64)]
+                ("i8_candidates", u64), ("i8_prescored", u64), ("threshold_certified", u64)]
 
 
 class CodecStats(C.Structure):

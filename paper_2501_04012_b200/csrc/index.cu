@@ -24,6 +24,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <exception>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -234,6 +235,29 @@ __global__ void k_scatter_topk(const uint64_t* __restrict__ ids, const double* _
   osc[q * k + t] = sc[i];
   if (t == 0) ocnt[q] = cnt[r];
 }
+// Threshold tier input: for failed query i (original index list[i]) the k-th
+// best EXACT score its last tier found (a lower bound of T_k: those are real
+// rows) minus twice the reference-dot rounding margin, rounded down; -inf
+// when fewer than k rows were found. One warp per query.
+__global__ void k_tau_fix(const float* __restrict__ Q, const int32_t* __restrict__ list, int n, int dim,
+                          const double* __restrict__ osc, const int32_t* __restrict__ ocnt, int k,
+                          float* __restrict__ tau) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= n) return;
+  const int q = list[w];
+  double qsq = 0.0;
+  for (int d = lane; d < dim; d += 32) {
+    const double v = Q[(int64_t)q * dim + d];
+    qsq = fma(v, v, qsq);
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) qsq += __shfl_xor_sync(0xffffffffu, qsq, off);
+  if (lane == 0) {
+    const double margin = 1e-12 * (1.0 + sqrt(qsq) * (1.0 + 0x1p-40));
+    tau[w] = ocnt[q] >= k ? __double2float_rd(osc[(int64_t)q * k + k - 1] - 2.0 * margin) : -INFINITY;
+  }
+}
+
 __global__ void k_map_list(const int32_t* __restrict__ sub, const int32_t* __restrict__ list, int n,
                            int32_t* __restrict__ out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -507,7 +531,7 @@ __device__ __forceinline__ uint32_t fkey(float f) {
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 
-__global__ void __launch_bounds__(RI_WARPS * 32, 6)
+__global__ void __launch_bounds__(RI_WARPS * 32)
     k_rescore_i8(const float* __restrict__ Q, int nq, int dim, const float* __restrict__ rows,
                  const __nv_bfloat16* __restrict__ rowsb, const uint64_t* __restrict__ ids,
                  const float* __restrict__ cand_s, const uint32_t* __restrict__ cand_r, const int32_t* __restrict__ cand_n,
@@ -515,7 +539,15 @@ __global__ void __launch_bounds__(RI_WARPS * 32, 6)
                  uint64_t* __restrict__ out_ids, double* __restrict__ out_sc, int32_t* __restrict__ out_cnt,
                  int32_t* __restrict__ fail_list, int32_t* __restrict__ fail_n,
                  unsigned long long* __restrict__ max_err_bits, int32_t* __restrict__ bad_query,
-                 unsigned long long* __restrict__ gathered) {
+                 unsigned long long* __restrict__ gathered, float* __restrict__ tlo_out,
+                 const float* __restrict__ t_glob) {
+  // tlo_out (sharded lookup, first pass): only write a lower bound of this
+  // rank's k-th exact score ((k-th best b of the 32 best candidates by U) -
+  // eps, rounded down) and return. t_glob (second pass): the max of those
+  // bounds over the ranks, a lower bound T of the GLOBAL k-th score: rows
+  // below it cannot be in the merged top-k, so this rank pre-scores only
+  // candidates with U >= T, exact-scores only those with b >= T - eps, and its
+  // list is certified when every row outside it is below T (cm + margin < T).
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = blockIdx.x * RI_WARPS + warp;
   if (q >= nq) return;
@@ -597,19 +629,28 @@ __global__ void __launch_bounds__(RI_WARPS * 32, 6)
 #pragma unroll
   for (int u = 0; u < CPL; ++u) qa[u] = lane + 32 * u < n16 ? sb4[lane + 32 * u] : make_uint4(0, 0, 0, 0);
   float* sbv = reinterpret_cast<float*>(skey + KI_MAX);  // [KI_MAX] b by U-sorted position
-  double t_lo = -INFINITY;
+  // (k-th best b among the first m <= 32 pre-scored) - eps, -inf if m < k
+  auto local_lo = [&](int m) -> double {
+    const float mine = lane < m ? sbv[lane] : -INFINITY;
+    int rank = 0;
+    for (int j = 0; j < 32; ++j) {
+      const float o = __shfl_sync(0xffffffffu, mine, j);
+      rank += (o > mine) | ((o == mine) & (j < lane));
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, rank == k - 1 && lane < m);
+    return bal ? (double)__shfl_sync(0xffffffffu, mine, __ffs(bal) - 1) - eps : -INFINITY;
+  };
+  const bool global_mode = t_glob != nullptr;
+  double t_lo = global_mode ? (double)t_glob[q] : -INFINITY;
   int cn = cn_all;  // candidates pre-scored (a prefix of the U order)
   for (int i0 = 0; i0 < cn_all; i0 += 4) {
     if (i0 == 32 && cn_all > 32) {
-      // k-th best b among the first 32 (rank counting across the lanes)
-      const float mine = sbv[lane];
-      int rank = 0;
-      for (int j = 0; j < 32; ++j) {
-        const float o = __shfl_sync(0xffffffffu, mine, j);
-        rank += (o > mine) | ((o == mine) & (j < lane));
+      const double lo = local_lo(32);
+      if (tlo_out) {
+        if (lane == 0) tlo_out[q] = __double2float_rd(lo);
+        return;
       }
-      const unsigned bal = __ballot_sync(0xffffffffu, rank == k - 1);
-      t_lo = (double)__shfl_sync(0xffffffffu, mine, __ffs(bal) - 1) - eps;
+      t_lo = fmax(t_lo, lo);
     }
     {
       const uint32_t uk = (uint32_t)(skey[i0] >> 32);
@@ -654,6 +695,11 @@ __global__ void __launch_bounds__(RI_WARPS * 32, 6)
     if (lane < 4 && i0 + lane < cn_all) sbv[i0 + lane] = lane == 0 ? acc[0] : lane == 1 ? acc[1] : lane == 2 ? acc[2] : acc[3];
     __syncwarp();
   }
+  if (tlo_out) {  // <= 32 candidates: all pre-scored
+    const double lo = local_lo(min(cn, 32));
+    if (lane == 0) tlo_out[q] = __double2float_rd(lo);
+    return;
+  }
   // (2) the pre-scored prefix by b, descending (list index kept in the low bits)
   for (int i = lane; i < cn; i += 32) skey[i] = ((uint64_t)fkey(sbv[i]) << 32) | (uint32_t)skey[i];
   __syncwarp();
@@ -665,7 +711,8 @@ __global__ void __launch_bounds__(RI_WARPS * 32, 6)
   // exact-score the prefix with b >= b_k - 2 eps (the whole list when it
   // holds <= k candidates)
   const float bk = cn > k ? key_b(skey[k - 1]) : -INFINITY;
-  const double need_b = (double)bk - 2.0 * eps;
+  // global mode: a candidate with b < T - eps has exact < T and is not needed either
+  const double need_b = global_mode ? fmax((double)bk - 2.0 * eps, t_lo - eps) : (double)bk - 2.0 * eps;
   Cand best;
   best.s = -INFINITY;
   best.id = ~0ull;
@@ -742,6 +789,7 @@ __global__ void __launch_bounds__(RI_WARPS * 32, 6)
     bool ok;
     if (q_uncertifiable) ok = false;
     else if (cn_all >= n_rows) ok = true;  // every row is in the list
+    else if (global_mode) ok = (double)cand_m[q] + margin < t_lo;  // every row outside is below T
     else ok = got >= k && (double)cand_m[q] + margin < tk;
     if (!ok) fail_list[atomicAdd(fail_n, 1)] = q;
   }
@@ -893,8 +941,32 @@ void exact_scan(lc_index* ix, int kind, const float* Qdev, const int32_t* qlist_
 }
 
 // Device-resident top-k (no host sync unless a fallback is needed).
-void query_dev(lc_index* ix, int kind, const float* Qdev, int nq, int k, uint64_t* oid, double* osc, int32_t* ocnt) {
+__global__ void k_fill_f32(float* p, int n, float v) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
+// The bound exchange is a collective: every rank must take part exactly once
+// per sharded query batch, whichever tier its own shard used (shards differ in
+// size, so one may scan exactly while another runs the int8 tier). A rank that
+// did not exchange contributes -inf bounds on the way out.
+struct ExchangeOnce {
+  const BoundExchange* x;
+  lc_ctx* ctx;
+  int n;
+  bool done = false;
+  ~ExchangeOnce() {
+    if (!x || done || std::uncaught_exceptions() > 0) return;
+    DevBuf d((size_t)std::max(n, 1) * sizeof(float), ctx->stream);
+    k_fill_f32<<<grid_for(std::max(n, 1), 256), 256, 0, ctx->stream>>>(d.as<float>(), n, -INFINITY);
+    (*x)(d.as<float>(), n);
+  }
+};
+
+void query_dev(lc_index* ix, int kind, const float* Qdev, int nq, int k, uint64_t* oid, double* osc, int32_t* ocnt,
+               const BoundExchange* xchg = nullptr) {
   lc_ctx* ctx = ix->ctx;
+  ExchangeOnce xonce{xchg, ix->ctx, nq};
   {
     std::lock_guard<std::mutex> sl(ix->stats_mu);
     ix->stats.queries += nq;
@@ -969,10 +1041,22 @@ void query_dev(lc_index* ix, int kind, const float* Qdev, int nq, int k, uint64_
       attr_set.fetch_or(1ull << (ctx->device & 63));
     }
     KTimer kt(ctx, "rescore");
+    DevBuf tlo(xchg ? (size_t)nq * sizeof(float) : 16, ctx->stream);
+    if (xchg) {
+      // sharded: each rank's lower bound of its k-th score, max over the ranks
+      k_rescore_i8<<<(unsigned)((nq + RI_WARPS - 1) / RI_WARPS), RI_WARPS * 32, ri_smem, ctx->stream>>>(
+          Qdev, nq, dim, ix->rows[kind], ix->rowsb[kind], ix->ids_dev, cs.as<float>(), cr.as<uint32_t>(),
+          cn.as<int32_t>(), cm.as<float>(), kout, ix->n, k, ix->dres[kind], ix->eps_floor, oid, osc, ocnt,
+          fl.as<int32_t>(), fail_n, err_bits, bad_q, gb.as<unsigned long long>(), tlo.as<float>(), nullptr);
+      FC_LAUNCH_CHECK();
+      count_launch(ctx);
+      (*xchg)(tlo.as<float>(), nq);
+      xonce.done = true;
+    }
     k_rescore_i8<<<(unsigned)((nq + RI_WARPS - 1) / RI_WARPS), RI_WARPS * 32, ri_smem, ctx->stream>>>(
         Qdev, nq, dim, ix->rows[kind], ix->rowsb[kind], ix->ids_dev, cs.as<float>(), cr.as<uint32_t>(), cn.as<int32_t>(),
         cm.as<float>(), kout, ix->n, k, ix->dres[kind], ix->eps_floor, oid, osc, ocnt, fl.as<int32_t>(), fail_n,
-        err_bits, bad_q, gb.as<unsigned long long>());
+        err_bits, bad_q, gb.as<unsigned long long>(), nullptr, xchg ? tlo.as<float>() : nullptr);
     kt.stop();
     FC_LAUNCH_CHECK();
     count_launch(ctx);
@@ -1121,6 +1205,78 @@ void query_dev(lc_index* ix, int kind, const float* Qdev, int nq, int k, uint64_
     if (level < 0 && nf2 > 8 && nf2 * 16 > nq) tier2_off = true;
     n_left = nf2;
   }
+  // Threshold tier (int8 tables, k <= 32): near-tied clusters (many rows
+  // within the tensor-core error of the k-th score) defeat every K'-based
+  // shortlist; instead collect EVERY row whose int8 upper bound U exceeds a
+  // known lower bound of T_k (the k-th best exact score found so far) with one
+  // fixed-threshold int8 pass, then rescore/certify as the int8 tier does.
+  // One streaming pass of the 768 MB s8 table for the few queries left
+  // instead of an fp64 scan of the whole fp32 table (~170 ms at 1M rows).
+  static const bool thr_off = getenv("FC_LOOKUP_THRESHOLD_TIER") && atoi(getenv("FC_LOOKUP_THRESHOLD_TIER")) == 0;
+  if (n_left > 0 && ix->i8 && k <= 32 && !thr_off) {
+    DevBuf q2((size_t)n_left * dim * sizeof(float), ctx->stream), tau((size_t)n_left * sizeof(float), ctx->stream);
+    k_gather_queries<<<grid_for((int64_t)n_left * dim, 256), 256, 0, ctx->stream>>>(Qdev, list_buf.as<int32_t>(), n_left,
+                                                                                   dim, q2.as<float>());
+    k_tau_fix<<<(unsigned)((n_left + 7) / 8), 256, 0, ctx->stream>>>(Qdev, list_buf.as<int32_t>(), n_left, dim, osc, ocnt,
+                                                                     k, tau.as<float>());
+    FC_LAUNCH_CHECK();
+    count_launch(ctx, 2);
+    {
+      std::lock_guard<std::mutex> pl(ix->plan_mu);
+      if (!ix->iplan[kind].valid || ix->iplan[kind].n_rows != ix->n) {
+        const int64_t nt = (ix->n + 127) / 128;
+        std::vector<float> tr(nt);
+        FC_CUDA(cudaMemcpyAsync(tr.data(), ix->tres[kind], nt * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+        sync(ctx);
+        std::nth_element(tr.begin(), tr.begin() + nt / 2, tr.end());
+        i8_plan(ix->iplan[kind], ix->rows8[kind], ix->tscale[kind], ix->tres[kind], ix->n, dim, tr[nt / 2]);
+      }
+    }
+    const int kout = KI_MAX;
+    DevBuf cs2((size_t)n_left * kout * sizeof(float), ctx->stream), cr2((size_t)n_left * kout * sizeof(uint32_t), ctx->stream);
+    DevBuf cn2((size_t)n_left * sizeof(int32_t), ctx->stream), cm2((size_t)n_left * sizeof(float), ctx->stream);
+    {
+      ShortlistTimerName tn("shortlist_threshold");
+      i8_shortlist(ctx, ix->iplan[kind], q2.as<float>(), n_left, k, ix->i8_kunit, kout, cs2.as<float>(),
+                   cr2.as<uint32_t>(), cn2.as<int32_t>(), cm2.as<float>(), tau.as<float>());
+    }
+    DevBuf id2((size_t)n_left * k * sizeof(uint64_t), ctx->stream), sc2((size_t)n_left * k * sizeof(double), ctx->stream);
+    DevBuf ct2((size_t)n_left * sizeof(int32_t), ctx->stream), fl2((size_t)n_left * sizeof(int32_t), ctx->stream);
+    DevBuf fn2(16, ctx->stream), gb2(3 * sizeof(unsigned long long), ctx->stream);
+    FC_CUDA(cudaMemsetAsync(fn2.p, 0, 16, ctx->stream));
+    FC_CUDA(cudaMemsetAsync(gb2.p, 0, gb2.bytes, ctx->stream));
+    {
+      KTimer kt3(ctx, "rescore_threshold");
+      const size_t ri_smem = (size_t)RI_WARPS * ((size_t)dim * 6 + KI_MAX * 12);
+      k_rescore_i8<<<(unsigned)((n_left + RI_WARPS - 1) / RI_WARPS), RI_WARPS * 32, ri_smem, ctx->stream>>>(
+          q2.as<float>(), n_left, dim, ix->rows[kind], ix->rowsb[kind], ix->ids_dev, cs2.as<float>(), cr2.as<uint32_t>(),
+          cn2.as<int32_t>(), cm2.as<float>(), kout, ix->n, k, ix->dres[kind], ix->eps_floor, id2.as<uint64_t>(),
+          sc2.as<double>(), ct2.as<int32_t>(), fl2.as<int32_t>(), fn2.as<int32_t>(),
+          reinterpret_cast<unsigned long long*>(fn2.as<char>() + 8), fn2.as<int32_t>() + 1,
+          gb2.as<unsigned long long>(), nullptr, nullptr);
+    }
+    k_scatter_topk<<<grid_for((int64_t)n_left * k, 256), 256, 0, ctx->stream>>>(
+        id2.as<uint64_t>(), sc2.as<double>(), ct2.as<int32_t>(), list_buf.as<int32_t>(), n_left, k, oid, osc, ocnt);
+    FC_LAUNCH_CHECK();
+    count_launch(ctx, 2);
+    int32_t hf3[4] = {0, 0, 0, 0};
+    FC_CUDA(cudaMemcpyAsync(hf3, fn2.p, 16, cudaMemcpyDeviceToHost, ctx->stream));
+    sync(ctx);
+    const int nf3 = hf3[0];
+    {
+      std::lock_guard<std::mutex> sl(ix->stats_mu);
+      ix->stats.threshold_certified += n_left - nf3;
+    }
+    if (nf3 > 0) {
+      DevBuf nl((size_t)nf3 * sizeof(int32_t), ctx->stream);
+      k_map_list<<<grid_for(nf3, 128), 128, 0, ctx->stream>>>(fl2.as<int32_t>(), list_buf.as<int32_t>(), nf3,
+                                                              nl.as<int32_t>());
+      FC_LAUNCH_CHECK();
+      count_launch(ctx);
+      FC_CUDA(cudaMemcpyAsync(list_buf.p, nl.p, (size_t)nf3 * sizeof(int32_t), cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    n_left = nf3;
+  }
   if (n_left > 0) {
     exact_scan(ix, kind, Qdev, list_buf.as<int32_t>(), n_left, k, oid, osc, ocnt);
     std::lock_guard<std::mutex> sl(ix->stats_mu);
@@ -1136,17 +1292,19 @@ namespace fc {
 // an empty table yields counts 0. Takes the index's reader lock.
 lc_ctx* index_ctx(lc_index* ix) { return ix->ctx; }
 int index_dim(lc_index* ix) { return ix->dim; }
-void index_topk_dev(lc_index* ix, int kind, const float* Qdev, int nq, int k, uint64_t* oid, double* osc, int32_t* ocnt) {
+void index_topk_dev(lc_index* ix, int kind, const float* Qdev, int nq, int k, uint64_t* oid, double* osc, int32_t* ocnt,
+                    const BoundExchange* xchg) {
   std::shared_lock lock(ix->mu);
   lc_ctx* ctx = ix->ctx;
   if (nq <= 0) return;
   if (ix->n == 0) {
+    ExchangeOnce xonce{xchg, ctx, nq};  // an empty shard still takes part in the collective
     FC_CUDA(cudaMemsetAsync(oid, 0, (size_t)nq * k * sizeof(uint64_t), ctx->stream));
     FC_CUDA(cudaMemsetAsync(osc, 0, (size_t)nq * k * sizeof(double), ctx->stream));
     FC_CUDA(cudaMemsetAsync(ocnt, 0, (size_t)nq * sizeof(int32_t), ctx->stream));
     return;
   }
-  query_dev(ix, kind, Qdev, nq, k, oid, osc, ocnt);
+  query_dev(ix, kind, Qdev, nq, k, oid, osc, ocnt, xchg);
 }
 }  // namespace fc
 

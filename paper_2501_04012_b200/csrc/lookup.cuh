@@ -18,6 +18,8 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include <functional>
+
 #include "common.cuh"
 
 namespace fc {
@@ -67,8 +69,15 @@ void i8_quantize_tiles(lc_ctx* ctx, const float* rows, int64_t n_rows, int dim, 
 // Each unit keeps <= kp_unit rows, the merge the kout best U. cand_m[q] = an
 // upper bound of U for EVERY row outside the output list (the max drop level
 // of the units and the merge cut): rows outside have exact <= cand_m[q].
+// tau_fix (device, per query; threshold tier): fixed U thresholds instead of
+// the pilot/histogram heuristic -- every row with U > tau_fix[q] is kept
+// (up to the query buffer), so cand_m[q] = tau_fix[q] unless it overflowed.
 void i8_shortlist(lc_ctx* ctx, const I8Plan& p, const float* Qdev, int nq, int k, int kp_unit, int kout, float* cand_s,
-                  uint32_t* cand_r, int32_t* cand_n, float* cand_m);
+                  uint32_t* cand_r, int32_t* cand_n, float* cand_m, const float* tau_fix = nullptr);
+
+// Sharded lookup: all-gathers per-query float bounds (device, n of them) and
+// replaces each by its max over the ranks, on the context's stream.
+using BoundExchange = std::function<void(float* bounds_dev, int n)>;
 
 bool approx_available();
 void approx_plan(ApproxPlan& p, const __nv_bfloat16* rows_bf16, int64_t n_rows, int dim, int sm_count);

@@ -285,6 +285,11 @@ struct Params {
   uint32_t* qcnt;            // [nq] entries appended (may exceed qcap)
   uint32_t* qdrop;           // [nq] order key of the max drop level (0 = none)
   int qcap;
+  // threshold tier (null otherwise): per-query fixed threshold in U space,
+  // never raised (no pilot, no histogram, full unit lists flushed to the
+  // query buffer instead of compacted), so every row with U > tau_fix[q]
+  // reaches the merge unless the query buffer overflows
+  const float* tau_fix;
 };
 // The pilot keeps each query's PILOT_R best U over the sample and the main
 // pass starts at the R-th best over the whole sample: over a 1/16 sample that
@@ -604,6 +609,23 @@ __device__ __forceinline__ void mma_box4_pair_ss_i8(uint32_t d_tmem, uint64_t a_
       : "memory");
 }
 
+// Append a unit list (cnt packed keys of query q, rows r0 + offset) to the
+// query's contiguous buffer; entries past its capacity and everything the
+// unit rejected (U <= tau) raise the query's drop level.
+__device__ __forceinline__ void i8_append(const Params& p, int q, const uint32_t* lk, int t, int cnt, int64_t r0,
+                                          float tau) {
+  const uint32_t pos = cnt ? atomicAdd(p.qcnt + q, (uint32_t)cnt) : 0u;
+  float dmax = tau;
+  for (int i = 0; i < cnt; ++i) {
+    const uint32_t key = lk[i * BM + t];
+    if (pos + (uint32_t)i < (uint32_t)p.qcap)
+      p.qbuf[(size_t)q * p.qcap + pos + i] = ((uint64_t)(key >> 16) << 48) | (uint64_t)(r0 + (key & 0xFFFFu));
+    else
+      dmax = fmaxf(dmax, hkey_float(key >> 16));
+  }
+  if (dmax > -INFINITY) atomicMax(p.qdrop + q, okey(dmax));
+}
+
 // v[j] for a run-time j in [0, 16) from 16 registers (a 4-level select tree:
 // registers cannot be indexed dynamically without a local-memory copy)
 __device__ __forceinline__ uint32_t sel16(const uint32_t* v, int j) {
@@ -856,8 +878,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
       float ut[PILOT_R];  // pilot: best U over the sampled tiles, descending
 #pragma unroll
       for (int i = 0; i < PILOT_R; ++i) ut[i] = -INFINITY;
-      if (!p.pilot) hist_refresh(hq, p.kh, tau, hoff);
-      if (I8 && !p.pilot) {  // the pilot's max U of this query
+      const bool fixed_tau = I8 && p.tau_fix != nullptr;
+      if (fixed_tau) tau = __ldg(p.tau_fix + q);
+      if (!p.pilot && !fixed_tau) hist_refresh(hq, p.kh, tau, hoff);
+      if (I8 && !p.pilot && !fixed_tau) {  // the pilot's max U of this query
         uint32_t pk;
         asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(pk) : "l"(p.gkey + q));
         if (pk) tau = fmaxf(tau, key_float(pk) - hoff);
@@ -875,7 +899,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
       for (int64_t row = r0; row < r1; row += PN, ++tile) {
         const uint32_t b = tile % NACC;
         const uint32_t use = tile / NACC;
-        if ((tile & p.refresh_mask) == 0 && !p.pilot) {
+        if ((tile & p.refresh_mask) == 0 && !p.pilot && !fixed_tau) {
           if (prof) c_t0 = clock64();
           hist_publish(hq, lk, t, pub, cnt);
           pub = cnt;
@@ -970,6 +994,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
             if (!__any_sync(0xffffffffu, hot | (lim_all < EPI_HALF_COLS))) continue;
             if (p.debug & 32) continue;  // diagnostic: fast path only
             if ((p.debug & 16) && lane == 0) atomicAdd(p.stats + 0, 1u);
+            if (I8 && fixed_tau && __any_sync(0xffffffffu, cnt + 16 > cap)) {
+              // threshold tier: flush the list to the query buffer (tau stays)
+              if (q < p.nq) i8_append(p, q, lk, t, cnt, r0, tau);
+              cnt = 0;
+              pub = 0;
+            }
             if (__any_sync(0xffffffffu, cnt + 16 > cap)) {
               if ((p.debug & 16) && lane == 0) atomicAdd(p.stats + 1, 1u);
               if (prof) c_t0 = clock64();
@@ -1023,18 +1053,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
         // append the unit's entries to the query's buffer; what does not fit
         // is dropped into the drop level, as is everything the unit rejected
         // (U <= tau) or compacted away (stored U <= the raised tau)
-        if (q < p.nq) {
-          const uint32_t pos = cnt ? atomicAdd(p.qcnt + q, (uint32_t)cnt) : 0u;
-          float dmax = tau;
-          for (int i = 0; i < cnt; ++i) {
-            const uint32_t key = lk[i * BM + t];
-            if (pos + (uint32_t)i < (uint32_t)p.qcap)
-              p.qbuf[(size_t)q * p.qcap + pos + i] = ((uint64_t)(key >> 16) << 48) | (uint64_t)(r0 + (key & 0xFFFFu));
-            else
-              dmax = fmaxf(dmax, hkey_float(key >> 16));
-          }
-          if (dmax > -INFINITY) atomicMax(p.qdrop + q, okey(dmax));
-        }
+        if (q < p.nq) i8_append(p, q, lk, t, cnt, r0, tau);
         if (prof) {
           cyc[2] += clock64() - c_t0;
           if (lane == 0)
@@ -1505,6 +1524,7 @@ struct ShortlistRun {
   const I8Plan* iplan = nullptr;      // int8 tier
   const float* qscale = nullptr;
   const float2* qerr = nullptr;
+  const float* tau_fix = nullptr;
   int k = 0;
   float* cand_s = nullptr;
   uint32_t* cand_r = nullptr;
@@ -1522,7 +1542,8 @@ void run_shortlist(lc_ctx* ctx, const ShortlistRun& R) {
     // that share a range closer together in time, so the table is re-read from
     // L2 rather than HBM (ncu, 1M x 768 x 4096: 37 splits 3.63 GB DRAM per launch,
     // 74 splits 2.74 GB and 2.5 % faster; 148 splits cost more in the merge)
-    splits = std::max<int64_t>(1, (workers * 16 + R.n_qtiles - 1) / R.n_qtiles);
+    static const int upw = getenv("FC_SHORTLIST_UPW") ? std::max(1, atoi(getenv("FC_SHORTLIST_UPW"))) : 16;
+    splits = std::max<int64_t>(1, (workers * upw + R.n_qtiles - 1) / R.n_qtiles);
     splits = std::min<int64_t>(splits, std::max<int64_t>(1, tiles / 16));
     // keep one query's partial lists within the merge's shared memory (few queries)
     splits = std::min<int64_t>(splits, std::max<int64_t>(workers, (200 * 1024) / ((int64_t)kp * 8 * (R.pair ? 2 : 1))));
@@ -1538,6 +1559,7 @@ void run_shortlist(lc_ctx* ctx, const ShortlistRun& R) {
   prm.pilot = 0;
   prm.tile_stride = 1;
   prm.n_rows_phys = R.n_rows;
+  prm.tau_fix = R.tau_fix;
   prm.Qb = reinterpret_cast<const __nv_bfloat16*>(R.Qconv);
   prm.nq = nq;
   prm.n_qtiles = R.n_qtiles;
@@ -1609,7 +1631,7 @@ void run_shortlist(lc_ctx* ctx, const ShortlistRun& R) {
     // into gkey, the main pass's starting threshold
     constexpr int PILOT_STRIDE = 16;
     static const bool no_pilot = getenv("FC_LOOKUP_I8_PILOT") && atoi(getenv("FC_LOOKUP_I8_PILOT")) == 0;
-    if (!no_pilot && total_tiles >= 256) {
+    if (!no_pilot && !R.tau_fix && total_tiles >= 256) {
       Params pp = prm;
       pp.pilot = 1;
       pp.tile_stride = PILOT_STRIDE;
@@ -1859,7 +1881,7 @@ void i8_plan(I8Plan& p, const int8_t* rows, const float* tscale, const float* tr
 }
 
 void i8_shortlist(lc_ctx* ctx, const I8Plan& plan, const float* Qdev, int nq, int k, int kp_unit, int kout, float* cand_s,
-                  uint32_t* cand_r, int32_t* cand_n, float* cand_m) {
+                  uint32_t* cand_r, int32_t* cand_n, float* cand_m, const float* tau_fix) {
   using namespace sm100;
   FC_REQUIRE(plan.dim % 128 == 0 && plan.dim <= 1024, "int8 lookup tier: dim must be a multiple of 128, <= 1024");
   ShortlistRun R;
@@ -1885,6 +1907,7 @@ void i8_shortlist(lc_ctx* ctx, const I8Plan& plan, const float* Qdev, int nq, in
   R.qscale = qs.as<float>();
   R.qerr = qe.as<float2>();
   R.k = k;
+  R.tau_fix = tau_fix;
   R.cand_s = cand_s;
   R.cand_r = cand_r;
   R.cand_n = cand_n;

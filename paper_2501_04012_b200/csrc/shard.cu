@@ -43,7 +43,7 @@ __global__ void k_topk_merge(const uint64_t* __restrict__ ids, const double* __r
 lc_ctx* index_ctx(lc_index* ix);
 int index_dim(lc_index* ix);
 void index_topk_dev(lc_index* ix, int kind, const float* Qdev, int nq, int k, uint64_t* oid, double* osc,
-                    int32_t* ocnt);
+                    int32_t* ocnt, const BoundExchange* xchg);
 }  // namespace fc
 
 using namespace fc;
@@ -190,14 +190,39 @@ struct ShardLists {
   DevBuf ids, sc, cnt, gids, gsc, gcnt;
 };
 
-void local_lists(lc_index* ix, int kind, const float* qdev, int64_t n, int k, int G, ShardLists& L, cudaStream_t st) {
+__global__ void k_bound_max(const float* __restrict__ all, int G, int n, float* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float m = all[i];
+  for (int g = 1; g < G; ++g) m = fmaxf(m, all[(size_t)g * n + i]);
+  out[i] = m;
+}
+
+// Rank-local lists for the merge. With G > 1 the int8 tier runs two-phase:
+// after its candidate pass each rank's per-query lower bound of its k-th score
+// is all-gathered and max-reduced, a lower bound of the GLOBAL k-th score, so
+// each rank rescores only the candidates that can reach the merged top-k
+// (~1/G of them) instead of its whole local top-k.
+void local_lists(lc_ctx* ctx, Comm& cm, lc_index* ix, int kind, const float* qdev, int64_t n, int k, ShardLists& L) {
+  const cudaStream_t st = ctx->stream;
+  const int G = cm.nranks;
   L.ids = DevBuf((size_t)n * k * 8, st);
   L.sc = DevBuf((size_t)n * k * 8, st);
   L.cnt = DevBuf((size_t)n * 4, st);
   L.gids = DevBuf((size_t)G * n * k * 8, st);
   L.gsc = DevBuf((size_t)G * n * k * 8, st);
   L.gcnt = DevBuf((size_t)G * n * 4, st);
-  index_topk_dev(ix, kind, qdev, (int)n, k, L.ids.as<uint64_t>(), L.sc.as<double>(), L.cnt.as<int32_t>());
+  static const bool two_phase = !(getenv("FC_SHARD_TWO_PHASE") && atoi(getenv("FC_SHARD_TWO_PHASE")) == 0);
+  BoundExchange ex = [&](float* b, int nb) {
+    DevBuf all((size_t)G * nb * sizeof(float), st);
+    std::vector<Comm::Part> parts{{b, all.p, (size_t)nb * sizeof(float)}};
+    cm.allgather_dev(ctx, parts);
+    k_bound_max<<<grid_for(nb, 256), 256, 0, st>>>(all.as<float>(), G, nb, b);
+    FC_LAUNCH_CHECK();
+    count_launch(ctx);
+  };
+  index_topk_dev(ix, kind, qdev, (int)n, k, L.ids.as<uint64_t>(), L.sc.as<double>(), L.cnt.as<int32_t>(),
+                 (G > 1 && two_phase) ? &ex : nullptr);
 }
 
 void add_parts(std::vector<Comm::Part>& parts, ShardLists& L, int64_t n, int k) {
@@ -411,7 +436,7 @@ lc_status lc_sharded_query_topk(lc_index* ix, int kind, const float* q, int64_t 
   OutArg<double> os(ctx, out_scores, (size_t)n * k);
   OutArg<int32_t> oc(ctx, out_counts, (size_t)n);
   ShardLists L;
-  local_lists(ix, kind, qa.dev, n, k, cm.nranks, L, ctx->stream);
+  local_lists(ctx, cm, ix, kind, qa.dev, n, k, L);
   std::vector<Comm::Part> parts;
   add_parts(parts, L, n, k);
   cm.allgather_dev(ctx, parts);
@@ -441,7 +466,7 @@ lc_status lc_sharded_lookup_decide(lc_index* ix, const float* qw, const float* q
   std::vector<Comm::Part> parts;
   for (int t = 0; t < 3; ++t) {
     InArg<float> qa(ctx, qs[t], (size_t)n * dim);
-    local_lists(ix, t, qa.dev, n, 1, cm.nranks, L[t], ctx->stream);
+    local_lists(ctx, cm, ix, t, qa.dev, n, 1, L[t]);
     add_parts(parts, L[t], n, 1);
   }
   cm.allgather_dev(ctx, parts);

@@ -153,3 +153,101 @@ def test_i8_matches_bf16_tier_on_large_table(fc, synth):
     s = a.stats()
     assert s.i8_batches == 1 and s.certified >= 0.97 * 1024, (s.certified, s.fallback)
     print("i8 candidates / exact-scored per query", s.i8_candidates / 1024, s.i8_rescored / 1024)
+
+
+def _clusters(n, dim, nq, csize, spread, seed):
+    rng = np.random.default_rng(seed)
+    base = rng.standard_normal((n, dim)).astype(np.float32)
+    q = rng.standard_normal((nq, dim)).astype(np.float32)
+    for j in range(nq):  # csize near-copies of each query: near-tied top-k
+        base[j * csize:(j + 1) * csize] = q[j] + spread * rng.standard_normal((csize, dim)).astype(np.float32)
+    perm = rng.permutation(n)
+    return base[perm], q
+
+
+@pytest.mark.parametrize("nq,csize", [(6, 200), (300, 150)])
+def test_threshold_tier_certifies_clusters(fc, orc, nq, csize):
+    """Clusters of 150-200 near-copies around each query. 6 queries (bf16
+    tier first): every bf16 K' (up to 128) is inside the error bound of the
+    k-th score, so they fail and the fixed-threshold int8 pass (every row with
+    U above a known lower bound of T_k) certifies them. 300 queries: the int8
+    tier's 256-candidate merge already holds a 150-row cluster. No fp64 scan
+    either way; bit-exact with the oracle."""
+    base, q = _clusters(nq * csize + 20000, 256, nq, csize, 0.01, 5 + nq)
+    tab = orc.normalize_rows(base)
+    qn = orc.normalize_rows(q)
+    ids = (np.arange(tab.shape[0], dtype=np.uint64) * 11 + 7)
+    ix = fc.SimilarityIndex()
+    ix.insert_batch(ids, tab, tab, tab)
+    ix.set_lookup(2, 32)
+    ix.stats(reset=True)
+    _check(fc, orc, ix, tab, ids, qn, 8)
+    s = ix.stats()
+    assert s.exact_scans == 0, s.exact_scans
+    if nq <= 128:
+        assert s.fallback == nq and s.threshold_certified == nq, (s.fallback, s.threshold_certified)
+    else:
+        assert s.i8_batches == 1 and s.certified >= 0.9 * nq, (s.certified, s.fallback)
+
+
+def test_threshold_tier_off_uses_exact_scan(fc, orc):
+    import subprocess
+    import sys
+    code = ("import numpy as np, sys; sys.path.insert(0, '.'); sys.path.insert(0, 'oracle');"
+            "import paper_2501_04012_b200 as fc; from oracle import Checker;"
+            "sys.path.insert(0, 'tests'); from test_gpu_lookup_i8 import _clusters;"
+            "orc = Checker('orc'); base, q = _clusters(30000, 256, 6, 200, 0.01, 11);"
+            "tab = orc.normalize_rows(base); qn = orc.normalize_rows(q);"
+            "ids = np.arange(30000, dtype=np.uint64) * 3 + 1; ix = fc.SimilarityIndex();"
+            "ix.insert_batch(ids, tab, tab, tab); ix.set_lookup(2, 32);"
+            "gi, gs, gc = ix.query_topk(fc.EmbeddingKind.Whole, qn, 8); oi, os_, oc = orc.topk_flat(tab, ids, qn, 8);"
+            "assert (gi.astype(np.uint64) == oi).all() and (gs == os_).all();"
+            "s = ix.stats(); assert s.threshold_certified == 0 and s.exact_scans == 6, (s.threshold_certified, s.exact_scans)")
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, FC_LOOKUP_THRESHOLD_TIER="0")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+
+
+def test_clustered_1m_table_time_and_exactness(fc, synth):
+    """1M x 768 with 64 queries each surrounded by a 150-row near-tied cluster:
+    bit-exact with the product's exact fp64 scan (the reference's
+    sequential dot, itself pinned to the oracle), and the batch takes at most
+    3x a plain (unclustered) batch of the same size -- the exact-scan
+    fallback alone costs ~170 ms at this size."""
+    import time
+    import torch
+    n, dim, nq = 1_000_000, 768, 256
+    tab = synth.gaussian_embeddings(n, dim, 3)
+    rng = np.random.default_rng(4)
+    qc = synth.gaussian_embeddings(64, dim, 9)
+    for j in range(64):
+        rows = rng.choice(n, 150, replace=False)
+        tab[rows] = synth.normalize_rows(qc[j] + 0.01 * rng.standard_normal((150, dim)).astype(np.float32))
+    ids = np.arange(n, dtype=np.uint64)
+    ix = fc.SimilarityIndex()
+    ix.insert_batch(ids, tab, tab, tab)
+    qp, _ = synth.perturbed_queries(tab, nq, 7)
+    qcl = qp.copy()
+    qcl[:64] = qc
+    for qq in (qp, qcl):  # warm-up
+        ix.query_topk(fc.EmbeddingKind.Whole, qq, 8)
+    ts = {}
+    for name, qq in (("plain", qp), ("clustered", qcl)):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = ix.query_topk(fc.EmbeddingKind.Whole, qq, 8)
+        torch.cuda.synchronize()
+        ts[name] = time.perf_counter() - t0
+        if name == "clustered":
+            got = res
+    ex = fc.SimilarityIndex()
+    ex.insert_batch(ids, tab, tab, tab)
+    ex.set_lookup(1, 32)
+    ei, es, ec = ex.query_topk(fc.EmbeddingKind.Whole, qcl, 8)
+    assert (got[0] == ei).all() and (bits(got[1]) == bits(es)).all() and (got[2] == ec).all()
+    s = ix.stats()
+    print("clustered vs plain", ts, "threshold_certified", s.threshold_certified, "exact_scans", s.exact_scans)
+    assert s.exact_scans == 0
+    assert ts["clustered"] <= 3 * ts["plain"] + 0.005, ts

@@ -40,22 +40,24 @@ def _init(rank, world, port):
     return dist, fc, sharded, ctx
 
 
-def _lookup_worker(rank, world, port, out_dir):
+def _lookup_worker(rank, world, port, out_dir, n, d, nq, mode, skew):
     dist, fc, sharded, ctx = _init(rank, world, port)
     from oracle import Checker
     from paper_2501_04012_b200 import synth
     orc = Checker("orc")
-    n, d, nq = 20000, 256, 96
     tabs = [synth.gaussian_embeddings(n, d, 70 + t) for t in range(3)]
     tabs[0][n - 1] = tabs[0][5]  # exact duplicates across shards: ties -> smaller id
     ids = (np.arange(n, dtype=np.uint64) * 7 + 3)
+    if skew:  # rank 1 (odd ids) gets only 4,000 rows: below the tensor-core size, it scans exactly
+        ids = np.arange(n, dtype=np.uint64) * 2
+        ids[::n // 4000] += np.uint64(1)
     ids[:50] += np.uint64(2 ** 63)  # u64 ids above 2^63
     q = [synth.perturbed_queries(tabs[t], nq, 80 + t)[0] for t in range(3)]
     q[0][0] = tabs[0][5]
     ix = fc.SimilarityIndex(ctx=ctx)
     sh = sharded.CommShardedIndex(ix, d)
     assert sh.insert_batch(ids, *tabs) > 0
-    ix.set_lookup(2, 32)  # tensor-core path on each shard
+    ix.set_lookup(mode, 32)  # 2: tensor-core path on each shard; 0: by shard size
     gi, gs, gc = sh.query_topk(0, q[0], 8)
     dec = sh.lookup_decide(q[0], q[1], q[2])
     info = sharded.comm_info(ctx)
@@ -77,9 +79,15 @@ def _lookup_worker(rank, world, port, out_dir):
     dist.destroy_process_group()
 
 
-def test_capi_sharded_lookup_two_ranks(tmp_path):
+@pytest.mark.parametrize("n,d,nq,mode,skew", [
+    (20000, 256, 96, 2, False),   # bf16 tier per shard (batch too small for the int8 tier)
+    (30000, 768, 300, 2, False),  # int8 tier, two-phase: shared lower bound of the global k-th score
+    (30000, 768, 300, 0, True),   # one shard scans exactly, the other runs two-phase: the bound
+                                  # exchange is still one collective per rank
+])
+def test_capi_sharded_lookup_two_ranks(tmp_path, n, d, nq, mode, skew):
     import torch.multiprocessing as mp
-    mp.spawn(_lookup_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    mp.spawn(_lookup_worker, args=(2, _free_port(), str(tmp_path), n, d, nq, mode, skew), nprocs=2, join=True)
     r0 = pickle.load(open(tmp_path / "l0.pkl", "rb"))
     r1 = pickle.load(open(tmp_path / "l1.pkl", "rb"))
     oi, os_, oc, ref_dec = r0["ref"]
