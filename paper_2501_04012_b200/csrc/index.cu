@@ -530,6 +530,27 @@ __device__ __forceinline__ uint32_t fkey(float f) {
   const uint32_t u = __float_as_uint(f);
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
+__device__ __forceinline__ float fkey_inv(uint32_t k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k);
+}
+// The k-th largest of the warp's keys (8 per lane, 0 = no key), exact: an
+// MSB-first bisection over the 32 key bits, one warp count per bit. Needs at
+// least k nonzero keys.
+__device__ __forceinline__ uint32_t warp_kth_key(const uint32_t (&key)[8], int k) {
+  uint32_t t = 0;
+#pragma unroll 1
+  for (int bit = 31; bit >= 0; --bit) {
+    const uint32_t c = t | (1u << bit);
+    uint32_t n = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) n += key[j] >= c;
+    if ((int)__reduce_add_sync(0xffffffffu, n) >= k) t = c;
+  }
+  return t;
+}
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
 
 __global__ void __launch_bounds__(RI_WARPS * 32)
     k_rescore_i8(const float* __restrict__ Q, int nq, int dim, const float* __restrict__ rows,
@@ -548,22 +569,42 @@ __global__ void __launch_bounds__(RI_WARPS * 32)
   // below it cannot be in the merged top-k, so this rank pre-scores only
   // candidates with U >= T, exact-scores only those with b >= T - eps, and its
   // list is certified when every row outside it is below T (cm + margin < T).
+  //
+  // No sorting: every stage is a set defined by a threshold (the k-th / 32nd
+  // largest key, found by bisection in registers), compacted into a position
+  // list and processed in any order; the exact top-k merge is order-free.
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = blockIdx.x * RI_WARPS + warp;
   if (q >= nq) return;
-  extern __shared__ uint8_t s_raw[];
-  // per warp: fp32 query [dim] | bf16 query [dim] | sort keys [KI_MAX] | b [KI_MAX]
-  const size_t per_warp = (size_t)dim * 6 + KI_MAX * 12;
+  extern __shared__ __align__(16) uint8_t s_raw[];
+  // per warp: fp64 query [dim] | bf16 query [dim] | position list [KI_MAX] |
+  // b by position [KI_MAX] | table row by position [KI_MAX]
+  const size_t per_warp = (size_t)dim * 10 + KI_MAX * 12;
   uint8_t* wbase = s_raw + (size_t)warp * per_warp;
-  float* sq = reinterpret_cast<float*>(wbase);
-  __nv_bfloat16* sb = reinterpret_cast<__nv_bfloat16*>(wbase + (size_t)dim * 4);
-  uint64_t* skey = reinterpret_cast<uint64_t*>(wbase + (size_t)dim * 6);
+  double* sqd = reinterpret_cast<double*>(wbase);
+  __nv_bfloat16* sb = reinterpret_cast<__nv_bfloat16*>(wbase + (size_t)dim * 8);
+  int32_t* list = reinterpret_cast<int32_t*>(wbase + (size_t)dim * 10);
+  float* sbv = reinterpret_cast<float*>(list + KI_MAX);
+  uint32_t* srow = reinterpret_cast<uint32_t*>(sbv + KI_MAX);
   const float* qv = Q + (int64_t)q * dim;
+  const int64_t cbase = (int64_t)q * kout;
+  const int cn_all = min(cand_n[q], KI_MAX);
+  // candidates: position lane + 32 j, U key in registers, row in smem
+  uint32_t uk[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int i = lane + 32 * j;
+    uk[j] = 0;
+    if (i < cn_all) {
+      uk[j] = fkey(cand_s[cbase + i]);
+      srow[i] = cand_r[cbase + i];
+    }
+  }
   double qsq = 0.0, dsq = 0.0;
   bool qfin = true;
   for (int d = lane; d < dim; d += 32) {
     const float v = qv[d];
-    sq[d] = v;
+    sqd[d] = (double)v;
     const __nv_bfloat16 bv = __float2bfloat16_rn(v);
     sb[d] = bv;
     qfin &= isfinite(v);
@@ -587,155 +628,131 @@ __global__ void __launch_bounds__(RI_WARPS * 32)
   eps = fmax(eps * (1.0 + 0x1p-20), eps_floor * fmax(1.0, qn));
   // the reference's fp64 sequential dot vs the real dot: <= dim 2^-53 ||q|| ||x||
   const double margin = 1e-12 * (1.0 + qn);
-  const int cn_all = min(cand_n[q], KI_MAX);
-  // warp bitonic sort of skey[0, n) descending (n padded to a power of two with 0 keys)
-  auto sort_desc = [&](int n) {
-    int np2 = 32;
-    while (np2 < n) np2 <<= 1;
-    for (int i = n + lane; i < np2; i += 32) skey[i] = 0;
+  const bool global_mode = t_glob != nullptr;
+  double t_lo = global_mode ? (double)t_glob[q] : -INFINITY;
+  // positions with pred(j) into list[0, n), ascending
+  auto compact = [&](auto pred) -> int {
+    int n = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const bool f = pred(j);
+      const unsigned bal = __ballot_sync(0xffffffffu, f);
+      if (f) list[n + __popc(bal & ((1u << lane) - 1u))] = lane + 32 * j;
+      n += __popc(bal);
+    }
     __syncwarp();
-    for (int kk = 2; kk <= np2; kk <<= 1)
-      for (int j = kk >> 1; j > 0; j >>= 1) {
-        for (int i = lane; i < np2; i += 32) {
-          const int p = i ^ j;
-          if (p > i) {
-            const uint64_t x = skey[i], y = skey[p];
-            const bool desc = (i & kk) == 0;
-            if (desc ? x < y : x > y) {
-              skey[i] = y;
-              skey[p] = x;
-            }
-          }
-        }
-        __syncwarp();
-      }
+    return n;
   };
-  // (0) candidates in descending order of U (an upper bound of the exact score)
-  for (int i = lane; i < cn_all; i += 32) {
-    const float u = cand_s[(int64_t)q * kout + i];
-    skey[i] = ((uint64_t)fkey(u) << 32) | (uint32_t)i;
-  }
-  sort_desc(cn_all);
-  // (1) bf16 pre-score in that order, 4 candidates per iteration: every lane
-  // issues all its 16-byte chunks of the 4 rows (<= 4 each, dim <= 1024)
-  // before any math, so one memory round trip serves 4 candidates. After the
-  // first 32, T_lo = (k-th best b among them) - eps <= T_k; a candidate with
-  // U < T_lo has exact <= U < T_k and neither it nor any later one (smaller U)
-  // can reach the top k: the pass stops there.
+  // bf16 pre-score b of list[0, n) into sbv[position], 4 rows per iteration:
+  // every lane issues all its 16-byte chunks of the 4 rows (<= 4 each, dim <=
+  // 1024) before any math, and the bulk engine keeps the next PW rows on
+  // their way into L2
   const uint4* sb4 = reinterpret_cast<const uint4*>(sb);
   const int n16 = dim / 8;  // 16-byte chunks per bf16 row
   constexpr int CPL = 4;    // chunks per lane (dim <= 1024)
+  constexpr int PW = 16;    // rows prefetched ahead
   uint4 qa[CPL];
 #pragma unroll
   for (int u = 0; u < CPL; ++u) qa[u] = lane + 32 * u < n16 ? sb4[lane + 32 * u] : make_uint4(0, 0, 0, 0);
-  float* sbv = reinterpret_cast<float*>(skey + KI_MAX);  // [KI_MAX] b by U-sorted position
-  // (k-th best b among the first m <= 32 pre-scored) - eps, -inf if m < k
-  auto local_lo = [&](int m) -> double {
-    const float mine = lane < m ? sbv[lane] : -INFINITY;
-    int rank = 0;
-    for (int j = 0; j < 32; ++j) {
-      const float o = __shfl_sync(0xffffffffu, mine, j);
-      rank += (o > mine) | ((o == mine) & (j < lane));
-    }
-    const unsigned bal = __ballot_sync(0xffffffffu, rank == k - 1 && lane < m);
-    return bal ? (double)__shfl_sync(0xffffffffu, mine, __ffs(bal) - 1) - eps : -INFINITY;
-  };
-  const bool global_mode = t_glob != nullptr;
-  double t_lo = global_mode ? (double)t_glob[q] : -INFINITY;
-  int cn = cn_all;  // candidates pre-scored (a prefix of the U order)
-  for (int i0 = 0; i0 < cn_all; i0 += 4) {
-    if (i0 == 32 && cn_all > 32) {
-      const double lo = local_lo(32);
-      if (tlo_out) {
-        if (lane == 0) tlo_out[q] = __double2float_rd(lo);
-        return;
-      }
-      t_lo = fmax(t_lo, lo);
-    }
-    {
-      const uint32_t uk = (uint32_t)(skey[i0] >> 32);
-      const float u0 = __uint_as_float((uk & 0x80000000u) ? (uk & 0x7FFFFFFFu) : ~uk);
-      if ((double)u0 < t_lo) {
-        cn = i0;
-        break;
-      }
-    }
-    uint32_t rr[4];
+  auto prescore = [&](int n) {
+    if (lane < PW && lane < n) prefetch_l2_bulk(rowsb + (int64_t)srow[list[lane]] * dim, (uint32_t)dim * 2);
+    for (int i0 = 0; i0 < n; i0 += 4) {
+      if (lane < 4 && i0 + PW + lane < n)
+        prefetch_l2_bulk(rowsb + (int64_t)srow[list[i0 + PW + lane]] * dim, (uint32_t)dim * 2);
+      uint32_t rr[4];
 #pragma unroll
-    for (int g = 0; g < 4; ++g)
-      rr[g] = i0 + g < cn_all ? cand_r[(int64_t)q * kout + (uint32_t)skey[i0 + g]] : 0u;
-    uint4 xa[4][CPL];
+      for (int g = 0; g < 4; ++g) rr[g] = i0 + g < n ? srow[list[i0 + g]] : 0u;
+      uint4 xa[4][CPL];
 #pragma unroll
-    for (int g = 0; g < 4; ++g)
+      for (int g = 0; g < 4; ++g)
 #pragma unroll
-      for (int u = 0; u < CPL; ++u) {
-        const int c = lane + 32 * u;
-        xa[g][u] = (i0 + g < cn_all && c < n16) ? __ldg(reinterpret_cast<const uint4*>(rowsb + (int64_t)rr[g] * dim) + c)
-                                                 : make_uint4(0, 0, 0, 0);
-      }
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-    for (int g = 0; g < 4; ++g)
-#pragma unroll
-      for (int u = 0; u < CPL; ++u) {
-        const __nv_bfloat162* x2 = reinterpret_cast<const __nv_bfloat162*>(&xa[g][u]);
-        const __nv_bfloat162* q2 = reinterpret_cast<const __nv_bfloat162*>(&qa[u]);
-#pragma unroll
-        for (int h = 0; h < 4; ++h) {
-          const float2 xf = __bfloat1622float2(x2[h]), qf = __bfloat1622float2(q2[h]);
-          acc[g] = fmaf(qf.x, xf.x, acc[g]);
-          acc[g] = fmaf(qf.y, xf.y, acc[g]);
+        for (int u = 0; u < CPL; ++u) {
+          const int c = lane + 32 * u;
+          xa[g][u] = (i0 + g < n && c < n16) ? __ldg(reinterpret_cast<const uint4*>(rowsb + (int64_t)rr[g] * dim) + c)
+                                             : make_uint4(0, 0, 0, 0);
         }
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int g = 0; g < 4; ++g)
+#pragma unroll
+        for (int u = 0; u < CPL; ++u) {
+          const __nv_bfloat162* x2 = reinterpret_cast<const __nv_bfloat162*>(&xa[g][u]);
+          const __nv_bfloat162* q2 = reinterpret_cast<const __nv_bfloat162*>(&qa[u]);
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            const float2 xf = __bfloat1622float2(x2[h]), qf = __bfloat1622float2(q2[h]);
+            acc[g] = fmaf(qf.x, xf.x, acc[g]);
+            acc[g] = fmaf(qf.y, xf.y, acc[g]);
+          }
+        }
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) acc[g] += __shfl_xor_sync(0xffffffffu, acc[g], off);
       }
-#pragma unroll
-    for (int g = 0; g < 4; ++g) {
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) acc[g] += __shfl_xor_sync(0xffffffffu, acc[g], off);
+      if (lane < 4 && i0 + lane < n) sbv[list[i0 + lane]] = lane == 0 ? acc[0] : lane == 1 ? acc[1] : lane == 2 ? acc[2] : acc[3];
     }
-    if (lane < 4 && i0 + lane < cn_all) sbv[i0 + lane] = lane == 0 ? acc[0] : lane == 1 ? acc[1] : lane == 2 ? acc[2] : acc[3];
     __syncwarp();
-  }
-  if (tlo_out) {  // <= 32 candidates: all pre-scored
-    const double lo = local_lo(min(cn, 32));
+  };
+  // (1) set A: the 32 best candidates by U (ties at the 32nd included), in
+  // global mode without those below T; T_lo = (k-th best b in A) - eps <= T_k
+  const uint32_t tauA = cn_all > 32 ? warp_kth_key(uk, 32) : 1u;
+  auto inA = [&](int j) {
+    return uk[j] >= tauA && uk[j] != 0 && !(global_mode && (double)fkey_inv(uk[j]) < t_lo);
+  };
+  const int nA = compact(inA);
+  prescore(nA);
+  uint32_t bkey[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) bkey[j] = inA(j) ? fkey(sbv[lane + 32 * j]) : 0u;
+  const double lo = nA >= k ? (double)fkey_inv(warp_kth_key(bkey, k)) - eps : -INFINITY;
+  if (tlo_out) {
     if (lane == 0) tlo_out[q] = __double2float_rd(lo);
     return;
   }
-  // (2) the pre-scored prefix by b, descending (list index kept in the low bits)
-  for (int i = lane; i < cn; i += 32) skey[i] = ((uint64_t)fkey(sbv[i]) << 32) | (uint32_t)skey[i];
-  __syncwarp();
-  sort_desc(cn);
-  auto key_b = [](uint64_t key) {
-    const uint32_t ok = (uint32_t)(key >> 32);
-    return __uint_as_float((ok & 0x80000000u) ? (ok & 0x7FFFFFFFu) : ~ok);
-  };
-  // exact-score the prefix with b >= b_k - 2 eps (the whole list when it
-  // holds <= k candidates)
-  const float bk = cn > k ? key_b(skey[k - 1]) : -INFINITY;
+  t_lo = fmax(t_lo, lo);
+  // (2) set B: the rest of the candidates with U >= T_lo (a candidate with
+  // U < T_lo has exact <= U < T_k and cannot reach the top k)
+  bool pre[8];
+  auto inB = [&](int j) { return uk[j] != 0 && !inA(j) && !((double)fkey_inv(uk[j]) < t_lo); };
+  const int nB = compact(inB);
+  prescore(nB);
+  int cn = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    pre[j] = uk[j] != 0 && (inA(j) || !((double)fkey_inv(uk[j]) < t_lo));
+    bkey[j] = pre[j] ? fkey(sbv[lane + 32 * j]) : 0u;
+    cn += pre[j];
+  }
+  cn = (int)__reduce_add_sync(0xffffffffu, (uint32_t)cn);
+  // (3) exact-score the pre-scored candidates with b >= b_k - 2 eps (b_k =
+  // k-th best b; all of them when <= k)
+  const float bk = cn > k ? fkey_inv(warp_kth_key(bkey, k)) : -INFINITY;
   // global mode: a candidate with b < T - eps has exact < T and is not needed either
   const double need_b = global_mode ? fmax((double)bk - 2.0 * eps, t_lo - eps) : (double)bk - 2.0 * eps;
+  const int nC = compact([&](int j) { return pre[j] && (double)fkey_inv(bkey[j]) >= need_b; });
+  for (int c = lane; c < nC; c += 32) prefetch_l2_bulk(rows + (int64_t)srow[list[c]] * dim, (uint32_t)dim * 4);
   Cand best;
   best.s = -INFINITY;
   best.id = ~0ull;
   best.slot = -1;
   int n_have = 0, n_gath = 0;
   double local_err = 0.0;
-  for (int base = 0; base < cn; base += 32) {
-    if ((double)key_b(skey[base]) < need_b) break;
+  for (int base = 0; base < nC; base += 32) {
     Cand c;
     c.s = -INFINITY;
     c.id = ~0ull;
     c.slot = -1;
-    const int i = base + lane;
-    if (i < cn && (double)key_b(skey[i]) >= need_b) {
-      const int li = (int)(uint32_t)skey[i];
-      const uint32_t r = cand_r[(int64_t)q * kout + li];
+    if (base + lane < nC) {
+      const int pos = list[base + lane];
+      const uint32_t r = srow[pos];
       const float* x = rows + (int64_t)r * dim;
       double acc = 0.0;
       {
         // sequential fp64 in d order (vindex.cpp:67), 32 elements in flight
-        // (dim % 128 == 0 on the int8 tier)
+        // (dim % 128 == 0 on the int8 tier); the query is fp64 in smem
         const float4* x4 = reinterpret_cast<const float4*>(x);
-        const float4* q4 = reinterpret_cast<const float4*>(sq);
+        const double2* q2 = reinterpret_cast<const double2*>(sqd);
         float4 nx[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) nx[u] = __ldg(x4 + u);
@@ -749,15 +766,15 @@ __global__ void __launch_bounds__(RI_WARPS * 32)
           }
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
-            const float4 qq = q4[d4 + u];
-            acc = fma((double)qq.x, (double)cx[u].x, acc);
-            acc = fma((double)qq.y, (double)cx[u].y, acc);
-            acc = fma((double)qq.z, (double)cx[u].z, acc);
-            acc = fma((double)qq.w, (double)cx[u].w, acc);
+            const double2 qa2 = q2[2 * (d4 + u)], qb2 = q2[2 * (d4 + u) + 1];
+            acc = fma(qa2.x, (double)cx[u].x, acc);
+            acc = fma(qa2.y, (double)cx[u].y, acc);
+            acc = fma(qb2.x, (double)cx[u].z, acc);
+            acc = fma(qb2.y, (double)cx[u].w, acc);
           }
         }
       }
-      local_err = fmax(local_err, fabs(acc - (double)key_b(skey[i])));
+      local_err = fmax(local_err, fabs(acc - (double)sbv[pos]));
       c.s = acc;
       c.id = ids[r];
       c.slot = r;
@@ -807,6 +824,17 @@ namespace {
 bool i8_wanted(int dim) {
   static const bool off = getenv("FC_LOOKUP_I8") && atoi(getenv("FC_LOOKUP_I8")) == 0;
   return !off && dim % 128 == 0 && dim <= 1024;
+}
+
+// k_rescore_i8 takes up to RI_WARPS * (10 dim + 12 KI_MAX) bytes of smem
+// (53 KB at dim 1024): opt in once per device
+void rescore_i8_attr(lc_ctx* ctx) {
+  static std::atomic<uint64_t> attr_set{0};
+  if (!(attr_set.load() >> (ctx->device & 63) & 1)) {
+    FC_CUDA(cudaFuncSetAttribute(k_rescore_i8, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(RI_WARPS * (1024 * 10 + KI_MAX * 12))));
+    attr_set.fetch_or(1ull << (ctx->device & 63));
+  }
 }
 
 void ensure_capacity(lc_index* ix, int64_t need) {
@@ -1033,13 +1061,8 @@ void query_dev(lc_index* ix, int kind, const float* Qdev, int nq, int k, uint64_
     }
     i8_shortlist(ctx, ix->iplan[kind], Qdev, nq, k, ix->i8_kunit, kout, cs.as<float>(), cr.as<uint32_t>(),
                  cn.as<int32_t>(), cm.as<float>());
-    const size_t ri_smem = (size_t)RI_WARPS * ((size_t)dim * 6 + KI_MAX * 12);
-    static std::atomic<uint64_t> attr_set{0};
-    if (!(attr_set.load() >> (ctx->device & 63) & 1)) {
-      FC_CUDA(cudaFuncSetAttribute(k_rescore_i8, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)(RI_WARPS * (1024 * 6 + KI_MAX * 12))));
-      attr_set.fetch_or(1ull << (ctx->device & 63));
-    }
+    const size_t ri_smem = (size_t)RI_WARPS * ((size_t)dim * 10 + KI_MAX * 12);
+    rescore_i8_attr(ctx);
     KTimer kt(ctx, "rescore");
     DevBuf tlo(xchg ? (size_t)nq * sizeof(float) : 16, ctx->stream);
     if (xchg) {
@@ -1247,7 +1270,8 @@ void query_dev(lc_index* ix, int kind, const float* Qdev, int nq, int k, uint64_
     FC_CUDA(cudaMemsetAsync(gb2.p, 0, gb2.bytes, ctx->stream));
     {
       KTimer kt3(ctx, "rescore_threshold");
-      const size_t ri_smem = (size_t)RI_WARPS * ((size_t)dim * 6 + KI_MAX * 12);
+      rescore_i8_attr(ctx);
+      const size_t ri_smem = (size_t)RI_WARPS * ((size_t)dim * 10 + KI_MAX * 12);
       k_rescore_i8<<<(unsigned)((n_left + RI_WARPS - 1) / RI_WARPS), RI_WARPS * 32, ri_smem, ctx->stream>>>(
           q2.as<float>(), n_left, dim, ix->rows[kind], ix->rowsb[kind], ix->ids_dev, cs2.as<float>(), cr2.as<uint32_t>(),
           cn2.as<int32_t>(), cm2.as<float>(), kout, ix->n, k, ix->dres[kind], ix->eps_floor, id2.as<uint64_t>(),
