@@ -246,7 +246,10 @@ typedef struct lc_entry_info {
 } lc_entry_info;
 lc_status lc_entry_get_info(lc_entry* e, lc_entry_info* out);
 /* decompress_step (codec.cpp:263-301) for n (entry, step) pairs into
- * out_dev [n][F][E] (device). Bit-exact. Unknown step => LC_ERR_STEP_NOT_CACHED. */
+ * out_dev [n][F][E] (device). Bit-exact. Unknown step => LC_ERR_STEP_NOT_CACHED.
+ * Stream-ordered: returns after launching on ctx's stream (no host sync);
+ * synchronize that stream (lc_ctx_synchronize) before reading out_dev from
+ * another stream or the host. Same for lc_decompress_stitch_batch. */
 lc_status lc_decompress_batch(lc_ctx* ctx, lc_entry* const* entries, const int32_t* steps,
                               int64_t n, float* out_dev);
 /* Decoupled hit: decompress the object source and the background source at

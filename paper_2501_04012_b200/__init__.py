@@ -408,6 +408,7 @@ class CompressedEntry:
 
     def __init__(self, h, ctx: Context, owned=True):
         self.h = h
+        self.hv = h.value if isinstance(h, C.c_void_p) else int(h)  # handle as int (batch calls)
         self.ctx = ctx
         self.owned = owned
 
@@ -545,6 +546,24 @@ def inter_compress(latent_steps, maps, steps, obj_masks, bg_masks, dims, prompt,
     return CompressedEntry(h, ctx)
 
 
+def _handles(entries):
+    """lc_entry* array of a list of CompressedEntry (uintp numpy array)."""
+    return np.fromiter((e.hv for e in entries), dtype=np.uintp, count=len(entries))
+
+
+def _torch_after(ctx):
+    """The decompress calls are stream-ordered on ctx's stream: order torch's
+    current stream after it (no host sync) when the two differ."""
+    import torch
+    cur = torch.cuda.current_stream(ctx.device)
+    cs = ctx.stream
+    if cs in (0, 1) and cur.cuda_stream == 0 or cs == cur.cuda_stream:
+        return
+    ev = torch.cuda.Event()
+    ev.record(torch.cuda.ExternalStream(cs, device=ctx.device))
+    cur.wait_event(ev)
+
+
 def _torch_out(shape, ctx):
     import torch
     return torch.empty(shape, dtype=torch.float32, device=f"cuda:{ctx.device}")
@@ -559,9 +578,10 @@ def decompress_batch(entries, steps, out=None):
     E = info.H * info.W * info.C
     if out is None:
         out = _torch_out((n, info.F, E), ctx)
-    hs = (C.c_void_p * n)(*[e.h.value if isinstance(e.h, C.c_void_p) else e.h for e in entries])
+    hs = _handles(entries)
     st_ = np.ascontiguousarray(steps, np.int32)
-    _check(lib.lc_decompress_batch(ctx.h, hs, _ptr(st_), n, _ptr(out)))
+    _check(lib.lc_decompress_batch(ctx.h, _ptr(hs), _ptr(st_), n, _ptr(out)))
+    _torch_after(ctx)
     return out
 
 
@@ -578,10 +598,11 @@ def decompress_stitch(obj_entries, bg_entries, steps, out=None):
     E = info.H * info.W * info.C
     if out is None:
         out = _torch_out((n, info.F, E), ctx)
-    ho = (C.c_void_p * n)(*[e.h.value if isinstance(e.h, C.c_void_p) else e.h for e in obj_entries])
-    hb = (C.c_void_p * n)(*[e.h.value if isinstance(e.h, C.c_void_p) else e.h for e in bg_entries])
+    ho = _handles(obj_entries)
+    hb = _handles(bg_entries)
     st_ = np.ascontiguousarray(steps, np.int32)
-    _check(lib.lc_decompress_stitch_batch(ctx.h, ho, hb, _ptr(st_), n, _ptr(out)))
+    _check(lib.lc_decompress_stitch_batch(ctx.h, _ptr(ho), _ptr(hb), _ptr(st_), n, _ptr(out)))
+    _torch_after(ctx)
     return out
 
 

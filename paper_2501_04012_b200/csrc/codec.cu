@@ -1669,30 +1669,35 @@ void launch_decompress(lc_ctx* ctx, const std::vector<const EntryData*>& ents, c
   const EntryData* d0 = ents[0];
   const int F = d0->F;
   const int64_t E = d0->E;
-  std::vector<DecItem> items(ents.size());
-  for (size_t i = 0; i < ents.size(); ++i)
-    items[i] = DecItem{ents[i]->fbase(), ents[i]->recipes(sidx[i]), out + (int64_t)i * F * E};
-  DevBuf di(items.size() * sizeof(DecItem), ctx->stream);
-  FC_CUDA(cudaMemcpyAsync(di.p, items.data(), di.bytes, cudaMemcpyHostToDevice, ctx->stream));
   const char* ge = getenv("FC_DEC_GROUPS");
   const bool groups = (E & 3) == 0 && F <= 256 && !(ge && atoi(ge) == 0);
+  // items and (grouped path) jobs travel in ONE host->device copy; the
+  // pageable source is staged by the driver before cudaMemcpyAsync returns,
+  // so nothing here has to outlive the call
+  size_t nj = 0;
+  if (groups)
+    for (size_t i = 0; i < ents.size(); ++i) nj += ents[i]->key_groups(sidx[i]).size();  // cached per entry step
+  const size_t items_b = (ents.size() * sizeof(DecItem) + 15) & ~size_t(15);
+  std::vector<uint8_t> stage(items_b + nj * sizeof(DecJob));
+  DecItem* items = reinterpret_cast<DecItem*>(stage.data());
+  for (size_t i = 0; i < ents.size(); ++i)
+    items[i] = DecItem{ents[i]->fbase(), ents[i]->recipes(sidx[i]), out + (int64_t)i * F * E};
   if (groups) {
-    std::vector<DecJob> jobs((size_t)ents.size() * F);  // pageable: the async copy stages it before returning
-    size_t nj = 0;
-    for (size_t i = 0; i < ents.size(); ++i)  // per-entry key groups are cached (EntryData::key_groups)
+    DecJob* jobs = reinterpret_cast<DecJob*>(stage.data() + items_b);
+    size_t j = 0;
+    for (size_t i = 0; i < ents.size(); ++i)
       for (const EntryData::KeyGroup& kg : ents[i]->key_groups(sidx[i]))
-        jobs[nj++] = DecJob{(int32_t)i, kg.key, {kg.mask[0], kg.mask[1], kg.mask[2], kg.mask[3]}};
-    DevBuf dj(nj * sizeof(DecJob), ctx->stream);
-    FC_CUDA(cudaMemcpyAsync(dj.p, jobs.data(), dj.bytes, cudaMemcpyHostToDevice, ctx->stream));
-    KTimer kt(ctx, "decompress");
-    k_decompress_groups<<<(unsigned)nj, DEC_T, 0, ctx->stream>>>(di.as<DecItem>(), dj.as<DecJob>(), F, E);
-    kt.stop();
-    FC_LAUNCH_CHECK();
-    count_launch(ctx);
-    return;
+        jobs[j++] = DecJob{(int32_t)i, kg.key, {kg.mask[0], kg.mask[1], kg.mask[2], kg.mask[3]}};
   }
+  DevBuf dv(stage.size(), ctx->stream);
+  FC_CUDA(cudaMemcpyAsync(dv.p, stage.data(), stage.size(), cudaMemcpyHostToDevice, ctx->stream));
+  const DecItem* di = dv.as<DecItem>();
   KTimer kt(ctx, "decompress");
-  k_decompress<<<(unsigned)(items.size() * F), DEC_T, 0, ctx->stream>>>(di.as<DecItem>(), F, E);
+  if (groups)
+    k_decompress_groups<<<(unsigned)nj, DEC_T, 0, ctx->stream>>>(
+        di, reinterpret_cast<const DecJob*>(dv.as<uint8_t>() + items_b), F, E);
+  else
+    k_decompress<<<(unsigned)(ents.size() * F), DEC_T, 0, ctx->stream>>>(di, F, E);
   kt.stop();
   FC_LAUNCH_CHECK();
   count_launch(ctx);
@@ -2202,8 +2207,8 @@ lc_status lc_decompress_batch(lc_ctx* ctx, lc_entry* const* entries, const int32
     ents[i] = e->d.get();
     sidx[i] = si;
   }
+  // stream-ordered (no host sync): out_dev is complete in ctx's stream order
   launch_decompress(ctx, ents, sidx, out_dev);
-  sync(ctx);
   LC_API_END
 }
 
@@ -2239,7 +2244,7 @@ lc_status lc_decompress_stitch_batch(lc_ctx* ctx, lc_entry* const* oe, lc_entry*
                                                                                      d0->C, d0->mb);
   FC_LAUNCH_CHECK();
   count_launch(ctx);
-  sync(ctx);
+  // stream-ordered (no host sync), as lc_decompress_batch
   LC_API_END
 }
 

@@ -430,6 +430,7 @@ int cmd_codec(lc_ctx* ctx, const Args& a) {
   for (int s = 0; s < 5; ++s) {
     std::vector<int32_t> st(n, steps[s]);
     ok(lc_decompress_batch(ctx, ents.data(), st.data(), n, dec));
+    ok(lc_ctx_synchronize(ctx));  // stream-ordered output; cudaMemcpy below is on the legacy stream
     for (int i = 0; i < n; ++i)
       cudaMemcpy(orig.data() + (size_t)i * F * E, lat + ((size_t)i * 5 + s) * F * E, (size_t)F * E * 4,
                  cudaMemcpyDeviceToHost);
