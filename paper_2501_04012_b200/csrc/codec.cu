@@ -38,7 +38,8 @@ namespace fc {
 
 // gram_sm100.cu
 bool gram_tc_supported(int F, int64_t E, const float* lat);
-void gram_tc(lc_ctx* ctx, const float* lat, int n_items, int F, int64_t E, double* G, double* nrm, int* bad);
+void gram_tc(lc_ctx* ctx, const float* lat, int n_items, int F, int64_t E, double* G, float* GT, double* nrm,
+             uint32_t* fmx, int* bad);
 
 DevArena::~DevArena() {
   if (p) {
@@ -206,29 +207,46 @@ __global__ void k_exact_norms(const float* __restrict__ lat, const int32_t* __re
 // dot (core.cpp:104-110 order) of every candidate pair, one lane per pair,
 // and applies the reference rule to the exact values. delta = 0 (exact
 // Gram) takes the exact values directly. One warp per (prompt, step) item.
-__global__ void __launch_bounds__(128) k_select_cert(const double* __restrict__ G, const double* __restrict__ nrm,
-                                                     const float* __restrict__ lat, int n_items, int F, int64_t E,
-                                                     double thr, double delta, int32_t* __restrict__ maps,
-                                                     int* __restrict__ bad, unsigned* __restrict__ n_exact) {
+__global__ void __launch_bounds__(128) k_select_cert(const double* __restrict__ G, const float* __restrict__ GT,
+                                                     const double* __restrict__ nrm,
+                                                     const uint32_t* __restrict__ fmx, const float* __restrict__ lat,
+                                                     int n_items, int F, int64_t E, double thr, double delta,
+                                                     int32_t* __restrict__ maps, int* __restrict__ bad,
+                                                     unsigned* __restrict__ n_exact) {
   __shared__ int s_keys[4][256];
   __shared__ double s_sim[4][256];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int item = blockIdx.x * 4 + w;
   if (item >= n_items) return;
   const double* g = G + (int64_t)item * F * F;
+  const float* gt = GT ? GT + (int64_t)item * F * F : nullptr;
   const double* nr = nrm + (int64_t)item * F;
   const float* X = lat + (int64_t)item * F * E;
   int32_t* map = maps + (int64_t)item * F;
   int* keys = s_keys[w];
   double* sim = s_sim[w];
+  // fmx (tensor-core Gram): exact zero-frame test from max |x|, and items
+  // with a frame outside the error model's range [2^-40, 2^56] take the
+  // exact path for every pair (delta = inf, a = 0: every key a candidate)
+  bool unsafe = false;
   if (F >= 2) {
     bool z = false;
-    for (int j = lane; j < F; j += 32) z |= nr[j] == 0.0;
+    for (int j = lane; j < F; j += 32) {
+      if (fmx) {
+        const uint32_t m = fmx[(int64_t)item * F + j];
+        z |= m == 0u;
+        unsafe |= m > 0x5B800000u || m < 0x2B800000u;
+      } else {
+        z |= nr[j] == 0.0;
+      }
+    }
     if (__any_sync(0xffffffffu, z)) {  // cosine_similarity throws on a zero-norm operand (core.cpp:111-112)
       if (lane == 0) atomicExch(bad, 1);
       return;
     }
+    unsafe = __any_sync(0xffffffffu, unsafe);
   }
+  if (unsafe) delta = INFINITY;
   int nk = 1;
   if (lane == 0) {
     keys[0] = 0;
@@ -243,7 +261,8 @@ __global__ void __launch_bounds__(128) k_select_cert(const double* __restrict__ 
     int ncand = 0;
     for (int t = lane; t < nk; t += 32) {
       const int k = keys[t];
-      const double a = g[(int64_t)j * F + k] / (sj * sqrt(nr[k]));
+      const double gjk = g[(int64_t)j * F + k] + (GT ? (double)gt[(int64_t)k * F + j] : 0.0);
+      const double a = unsafe ? 0.0 : gjk / (sj * sqrt(nr[k]));
       sim[t] = a;
       if (a >= thr - delta) {
         ++ncand;
@@ -523,7 +542,7 @@ __global__ void __launch_bounds__(ICT, 2) k_inter_cert(const float* __restrict__
                                                       InterCert* __restrict__ cert, int force_replay) {
   constexpr int NA = S * (S + 1) / 2;  // A[s<=b] = sum d_s d_b
   constexpr int NP = S * (S - 1);      // P[s!=b] = sum d_b k_s ; Q[s!=b] = sum f_s d_b
-  constexpr int NV = NA + 2 * NP + S;  // + FK[s] = sum f_s k_s
+  constexpr int NV = NA + 2 * NP + 3 * S;  // + FK[s] = sum f_s k_s, FF[s] = |f_s|^2, KK[s] = |k_s|^2
   constexpr int NW = ICT / 32;
   __shared__ double s_red[NW][NV];
   __shared__ float s_max[NW][2 * S];
@@ -595,6 +614,10 @@ __global__ void __launch_bounds__(ICT, 2) k_inter_cert(const float* __restrict__
           }
 #pragma unroll
       for (int s = 0; s < S; ++s, ++a) acc[a] = fma(fd[s], kd[s], acc[a]);
+#pragma unroll
+      for (int s = 0; s < S; ++s, ++a) acc[a] = fma(fd[s], fd[s], acc[a]);
+#pragma unroll
+      for (int s = 0; s < S; ++s, ++a) acc[a] = fma(kd[s], kd[s], acc[a]);
     }
   }
   // block reduction (fixed order)
@@ -740,8 +763,8 @@ __global__ void __launch_bounds__(ICT, 2) k_inter_cert(const float* __restrict__
       const double a = (double)alpha;
       // r must stay finite (else the reference throws; the exact path reports it)
       if ((double)s_max[0][s] + fabs(a) * (double)s_max[0][S + b] >= 1.0e38) ok = false, why = 3;
-      const double ff = nrm[((int64_t)it.entry * S + perm[s]) * F + 0];  // |f_s|^2 (Gram pass)
-      const double kk = nrm[((int64_t)it.entry * S + perm[s]) * F + m];  // |k_s|^2 (Gram pass)
+      const double ff = R[NA + 2 * NP + S + s];      // |f_s|^2 (this pass, reassociated)
+      const double kk = R[NA + 2 * NP + 2 * S + s];  // |k_s|^2 (this pass, reassociated)
       const double dot = R[NA + 2 * NP + s] + a * R[Pidx(s, b)];
       const double na = ff + 2.0 * a * R[Qidx(s, b)] + a * a * den;
       const double K = sqrt(kk);
@@ -1095,15 +1118,20 @@ void gram(lc_ctx* ctx, const float* lat, int n_items, const Geo& g, double* G) {
   count_launch(ctx);
 }
 
-// Frame Gram matrices + exact squared norms of n_items latents. Tensor-core
-// path (gram_sm100.cu) when the shape allows; returns the certified
-// similarity error bound delta for k_select_cert (0 = exact Gram).
-constexpr double GRAM_DELTA = 1e-4;
+// Frame Gram matrices + squared norms of n_items latents. Tensor-core path
+// (gram_sm100.cu) when the shape allows: G~ and nrm = diag(G~) within
+// GRAM_REL relative, fmx = per-frame max |x| bits; returns the certified
+// similarity error bound delta for k_select_cert (0 = exact Gram, exact
+// norms, fmx unused). With |G~ - dot| <= rho |x_j||x_k| and |n~ - n| <= rho n,
+// a = G~ / sqrt(n~_j n~_k) is within 2 rho / (1 - rho) of the cosine
+// (rho = GRAM_REL): 2.1e-4 covers it with the fp64 rounding.
+constexpr double GRAM_DELTA = 2.1e-4;
 // Also raises *bad if any element is non-finite (fused into the tensor-core
 // pass; a separate check pass otherwise).
-double grams_and_norms(lc_ctx* ctx, const float* lat, int n_items, const Geo& g, double* G, double* nrm, int* bad) {
-  if (gram_tc_supported(g.F, g.E, lat)) {
-    gram_tc(ctx, lat, n_items, g.F, g.E, G, nrm, bad);
+double grams_and_norms(lc_ctx* ctx, const float* lat, int n_items, const Geo& g, double* G, float* GT, double* nrm,
+                       uint32_t* fmx, int* bad) {
+  if (fmx && GT && gram_tc_supported(g.F, g.E, lat)) {
+    gram_tc(ctx, lat, n_items, g.F, g.E, G, GT, nrm, fmx, bad);
     return GRAM_DELTA;
   }
   const int64_t total = (int64_t)n_items * g.F * g.E;
@@ -1117,14 +1145,16 @@ double grams_and_norms(lc_ctx* ctx, const float* lat, int n_items, const Geo& g,
   return 0.0;
 }
 
-void select_cert(lc_ctx* ctx, const double* G, const double* nrm, const float* lat, int n_items, const Geo& g, double thr,
-                 double delta, int32_t* maps, int* bad) {
+void select_cert(lc_ctx* ctx, const double* G, const float* GT, const double* nrm, const uint32_t* fmx, const float* lat,
+                 int n_items, const Geo& g, double thr, double delta, int32_t* maps, int* bad) {
   DevBuf ne(sizeof(unsigned), ctx->stream);
   FC_CUDA(cudaMemsetAsync(ne.p, 0, sizeof(unsigned), ctx->stream));
   {
     KTimer kt(ctx, "select");
-    k_select_cert<<<(unsigned)((n_items + 3) / 4), 128, 0, ctx->stream>>>(G, nrm, lat, n_items, g.F, g.E, thr, delta,
-                                                                          maps, bad, ne.as<unsigned>());
+    k_select_cert<<<(unsigned)((n_items + 3) / 4), 128, 0, ctx->stream>>>(G, delta > 0.0 ? GT : nullptr, nrm,
+                                                                          delta > 0.0 ? fmx : nullptr, lat,
+                                                                          n_items, g.F, g.E, thr, delta, maps, bad,
+                                                                          ne.as<unsigned>());
   }
   FC_LAUNCH_CHECK();
   count_launch(ctx);
@@ -1784,10 +1814,12 @@ void compress_chunk(lc_ctx* ctx, const float* lat, const uint8_t* om, const uint
   DevBuf flags(2 * sizeof(int), ctx->stream);
   FC_CUDA(cudaMemsetAsync(flags.p, 0, 2 * sizeof(int), ctx->stream));
   DevBuf G((size_t)n * S * F * F * sizeof(double), ctx->stream), NR((size_t)n * S * F * sizeof(double), ctx->stream);
-  const double delta = grams_and_norms(ctx, lat, (int)(n * S), g, G.as<double>(), NR.as<double>(), flags.as<int>());
+  DevBuf FM((size_t)n * S * F * sizeof(uint32_t), ctx->stream), GT((size_t)n * S * F * F * sizeof(float), ctx->stream);
+  const double delta = grams_and_norms(ctx, lat, (int)(n * S), g, G.as<double>(), GT.as<float>(), NR.as<double>(),
+                                       FM.as<uint32_t>(), flags.as<int>());
   DevBuf maps((size_t)n * S * F * sizeof(int32_t), ctx->stream);
-  select_cert(ctx, G.as<double>(), NR.as<double>(), lat, (int)(n * S), g, thr, delta, maps.as<int32_t>(),
-              flags.as<int>() + 1);
+  select_cert(ctx, G.as<double>(), GT.as<float>(), NR.as<double>(), FM.as<uint32_t>(), lat, (int)(n * S), g, thr, delta,
+              maps.as<int32_t>(), flags.as<int>() + 1);
   // one round trip: maps, frame norms and both flags
   PinnedBuf<int32_t> maps_h((size_t)n * S * F);
   PinnedBuf<double> diag((size_t)n * S * F);
@@ -1967,10 +1999,13 @@ lc_status lc_select_keyframes(lc_ctx* ctx, const float* latents, int64_t n, int 
   DevBuf bad(sizeof(int), ctx->stream);
   FC_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), ctx->stream));
   DevBuf G((size_t)n * F * F * sizeof(double), ctx->stream), NR((size_t)n * F * sizeof(double), ctx->stream);
+  DevBuf FM((size_t)n * F * sizeof(uint32_t), ctx->stream), GT((size_t)n * F * F * sizeof(float), ctx->stream);
   Geo g{F, H, W, C, E, ((int64_t)H * W + 7) / 8};
-  const double delta = grams_and_norms(ctx, lat.dev, (int)n, g, G.as<double>(), NR.as<double>(), bad.as<int>());
+  const double delta = grams_and_norms(ctx, lat.dev, (int)n, g, G.as<double>(), GT.as<float>(), NR.as<double>(),
+                                       FM.as<uint32_t>(), bad.as<int>());
   if (check_flag(ctx, bad)) raise(LC_ERR_INVALID_ARGUMENT, "Frame: non-finite element");
-  select_cert(ctx, G.as<double>(), NR.as<double>(), lat.dev, (int)n, g, thr, delta, om.dev, bad.as<int>());
+  select_cert(ctx, G.as<double>(), GT.as<float>(), NR.as<double>(), FM.as<uint32_t>(), lat.dev, (int)n, g, thr, delta,
+              om.dev, bad.as<int>());
   om.finish(ctx);
   if (check_flag(ctx, bad)) raise(LC_ERR_INVALID_ARGUMENT, "cosine_similarity: zero-norm operand");
   LC_API_END
@@ -2095,7 +2130,9 @@ lc_status lc_inter_compress(lc_ctx* ctx, const float* latents, const int32_t* ma
   DevBuf G((size_t)S * F * F * sizeof(double), ctx->stream), NR((size_t)S * F * sizeof(double), ctx->stream);
   DevBuf bad(sizeof(int), ctx->stream);
   FC_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), ctx->stream));
-  const double delta = grams_and_norms(ctx, lat.dev, S, g, G.as<double>(), NR.as<double>(), bad.as<int>());
+  DevBuf FM((size_t)S * F * sizeof(uint32_t), ctx->stream), GT((size_t)S * F * F * sizeof(float), ctx->stream);
+  const double delta = grams_and_norms(ctx, lat.dev, S, g, G.as<double>(), GT.as<float>(), NR.as<double>(),
+                                       FM.as<uint32_t>(), bad.as<int>());
   PinnedBuf<double> diag((size_t)S * F);
   FC_CUDA(cudaMemcpyAsync(diag.data(), NR.p, NR.bytes, cudaMemcpyDeviceToHost, ctx->stream));
   if (check_flag(ctx, bad)) raise(LC_ERR_INVALID_ARGUMENT, "Frame: non-finite element");

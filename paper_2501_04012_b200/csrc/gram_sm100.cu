@@ -10,28 +10,40 @@
 // pairs whose decision the bound cannot settle. Outputs:
 //   G~[item][F][F]  fp64, |G~(j,k) - dot(j,k)| <= GRAM_REL * sum_i |x_ji x_ki|
 //                   <= GRAM_REL * ||x_j|| ||x_k||  (Cauchy-Schwarz)
-//   nrm[item][F]    fp64, sum_i x_ji^2 reassociated into 4 chains (each
-//                   product exact): |nrm - sequential| <= 2 gamma_E nrm.
-//                   Zero iff the frame is all zero. Consumers that need the
-//                   reference's exact sequential value (exact select pairs,
-//                   exact K7 fallback) recompute it (k_exact_norms, codec.cu).
-//
-// Error model (bf16x3): x = hi + lo + r with hi = RN_bf16(x), lo =
-// RN_bf16(x - hi), |r| <= 2^-16 |x|; the MMAs form hi*hi' + hi*lo' + lo*hi'
+//   nrm[item][F]    fp64, G~(j,j): the same approximation of sum_i x_ji^2,
+//                   |nrm - ||x_j||^2| <= GRAM_REL ||x_j||^2. Consumers that
+//                   need the reference's exact sequential value (exact
+//                   select pairs, exact K7 fallback) recompute it
+//                   (k_exact_norms, codec.cu); the certified K7 sums its own.
+//   fmx[item][F]    u32, max_i |x_ji| as fp32 bits: exact zero-frame and
+//                   non-finite detection (>= 0x7F800000) and the range guard
+//                   of the error model below (select takes the exact path for
+//                   an item whose frames leave [2^-40, 2^56]).
+// Error model (bf16x3): x = hi + lo + r with hi = x rounded to bf16 (round
+// half away from zero, done on the integer bits: (u + 0x8000) & 0xFFFF0000),
+// lo = x - hi exact in fp32 (|lo| <= 2^-8 |x|), lo rounded to nearest bf16
+// (|r| <= 2^-8 |lo| <= 2^-16 |x|); the MMAs form hi*hi' + hi*lo' + lo*hi'
 // (each product exact in fp32), dropping lo*lo' and the r terms:
-// <= 3.1 * 2^-16 |x x'|. Accumulation: fp32 in TMEM over chunks of 256
-// elements (<= 256 * 2^-23 relative to the chunk's sum |x x'|, truncating
-// adders assumed), chunk totals added in fp64. GRAM_REL = 1e-4 covers both
-// (7.8e-5).
+// <= 3.1 * 2^-16 |x x'|. The operand is the Gram of one tile with itself, so
+// lo*hi' = (hi*lo')^T: two MMAs per K step (HH = hi hi', HL = hi lo') and
+// G~(j,k) = (HH + HL)(j,k) + HL(k,j), the transpose added by the consumer
+// (GT). Accumulation: fp32 in TMEM over chunks of 256 elements (<= 256 *
+// 2^-23 relative to the chunk's sum |x x'|, truncating adders assumed),
+// HH chunk totals added in fp64, HL chunk totals in fp32 (|HL| <= 2^-8
+// sum|x x'|, so <= nchunks 2^-32 relative, negligible). Products that underflow fp32
+// add <= 3 E 2^-126 in all, < 2^-17 of the bound when every frame's max |x|
+// is >= 2^-40; max |x| <= 2^56 keeps chunk sums finite. GRAM_REL = 1e-4
+// covers the sum (8.6e-5). Per element the split is integer/FADD work plus
+// half a bf16x2 pack: no fp64.
 //
 // Tiles: two items (2 x F <= 128 frames) form the M = N = 128 operand; the
 // cross-item blocks of the 128x128 product are unused (tensor throughput is
 // not the limit: the kernel streams each latent once, HBM-bound).
 // Warp roles (320 threads): 0 TMA producer (fp32 boxes of 32 elements),
 // 1 MMA issuer (elected lane), 2-9 workers: thread = half a frame row of
-// each K unit (norm partials + hi/lo split into SWIZZLE_128B bf16 tiles),
-// and the TMEM -> fp64 chunk accumulation of 32 Gram columns of that row
-// one chunk behind.
+// each K unit (max |x| + hi/lo split into SWIZZLE_128B bf16 tiles), and the
+// TMEM -> fp64 chunk accumulation of 32 Gram columns of that row one chunk
+// behind.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cudaTypedefs.h>
@@ -59,7 +71,9 @@ struct Params {
   int64_t E;
   int n_units;          // E / KU
   double* G;            // [n_items][F][F]
-  double* nrm;          // [n_items][F]
+  float* GT;            // [n_items][F][F] HL; G~(j,k) = G(j,k) + GT(k,j)
+  double* nrm;          // [n_items][F] G~(j,j)
+  uint32_t* fmx;        // [n_items][F] max |x| bits
   int* bad;             // set to 1 if any element is non-finite (Frame ctor rule, core.cpp:11-25)
 };
 
@@ -80,6 +94,22 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
 // 16-byte chunk c of row r in a 128-B-row SWIZZLE_128B tile
 __device__ __forceinline__ uint32_t sw128(int r, int c) { return (uint32_t)(r * 128 + ((c ^ (r & 7)) << 4)); }
 
+__device__ __forceinline__ void lds128(uint32_t a, uint32_t (&v)[4]) {
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]) : "r"(a));
+}
+__device__ __forceinline__ void sts128(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
+}
+// bf16 pair (x0 low, x1 high) of the round-half-away hi parts and of the
+// rounded remainders; exact lo = x - hi in between
+__device__ __forceinline__ void split2(uint32_t u0, uint32_t u1, uint32_t& hi2, uint32_t& lo2) {
+  const uint32_t h0 = (u0 + 0x8000u) & 0xFFFF0000u, h1 = (u1 + 0x8000u) & 0xFFFF0000u;
+  const float l0 = __uint_as_float(u0) - __uint_as_float(h0), l1 = __uint_as_float(u1) - __uint_as_float(h1);
+  hi2 = __byte_perm(h0, h1, 0x7632);
+  const __nv_bfloat162 l2 = __floats2bfloat162_rn(l0, l1);  // one F2FP (RN) for the pair
+  lo2 = *reinterpret_cast<const uint32_t*>(&l2);
+}
+
 __global__ void __launch_bounds__(GT, 1) k_gram_tc(const __grid_constant__ CUtensorMap tmX, Params p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -93,7 +123,7 @@ __global__ void __launch_bounds__(GT, 1) k_gram_tc(const __grid_constant__ CUten
   uint64_t* afull = bempty + NB;
   uint64_t* aempty = afull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + 2);
-  __shared__ double s_nrm[2][128];
+  __shared__ uint32_t s_mx[2][128];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int F = p.F;
@@ -117,7 +147,7 @@ __global__ void __launch_bounds__(GT, 1) k_gram_tc(const __grid_constant__ CUten
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // zero-fill visible to TMA / MMA
@@ -175,7 +205,7 @@ __global__ void __launch_bounds__(GT, 1) k_gram_tc(const __grid_constant__ CUten
         const uint32_t ab = ch & 1;
         mbar_wait(smem_u32(&aempty[ab]), ((ch >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t d = tmem + ab * 128;
+        const uint32_t d = tmem + ab * 256;  // HH at +0, HL at +128
         const int k1 = min(nu, (c + 1) * CHUNK);
         for (int k = c * CHUNK; k < k1; ++k, ++u) {
           const int s = u % NB;
@@ -187,9 +217,10 @@ __global__ void __launch_bounds__(GT, 1) k_gram_tc(const __grid_constant__ CUten
 #pragma unroll
             for (int t = 0; t < 4; ++t) {  // K = 16 per MMA; +32 B per step inside the swizzled row
               const uint64_t o = 2 * t;
-              mma_ss(d, dh + o, dh + o, idesc, (k != c * CHUNK || t != 0) ? 1u : 0u);
-              mma_ss(d, dh + o, dl + o, idesc, 1u);
-              mma_ss(d, dl + o, dh + o, idesc, 1u);
+              const uint32_t acc = (k != c * CHUNK || t != 0) ? 1u : 0u;
+              mma_ss(d, dh + o, dh + o, idesc, acc);        // HH = hi hi'
+              mma_ss(d + 128, dh + o, dl + o, idesc, acc);  // HL = hi lo'; lo hi' = HL^T
+
             }
           }
           if (issuer) tc_commit(smem_u32(&bempty[s]));
@@ -216,52 +247,48 @@ __global__ void __launch_bounds__(GT, 1) k_gram_tc(const __grid_constant__ CUten
       const int item = 2 * tile + (r >> 6);
       const int row = r & 63;
       const bool real = row < F && item < p.n_items;
-      double nrm[4];  // 4 independent chains (the sequential one is latency-bound)
+      uint32_t mx = 0;  // max |x| bits of this half row
+      double acc[32];  // sum over chunks of HH(row, col), fp64
+      float acc2[32];  // sum over chunks of HL(row, col), fp32 (|HL| <= 2^-8 sum|x x'|)
 #pragma unroll
-      for (int c = 0; c < 4; ++c) nrm[c] = 0.0;
-      double acc[32];
-#pragma unroll
-      for (int i = 0; i < 32; ++i) acc[i] = 0.0;
+      for (int i = 0; i < 32; ++i) acc[i] = 0.0, acc2[i] = 0.f;
       auto epilogue = [&](uint32_t gch) {
         const uint32_t ab = gch & 1;
         mbar_wait(smem_u32(&afull[ab]), (gch >> 1) & 1);
         tc_fence_after();
         float v[32];
-        tmem_ld32(tmem + lane_base + ab * 128 + colb, v);
+        tmem_ld32(tmem + lane_base + ab * 256 + colb, v);  // HH
+#pragma unroll
+        for (int i = 0; i < 32; ++i) acc[i] += (double)v[i];
+        tmem_ld32(tmem + lane_base + ab * 256 + 128 + colb, v);  // HL
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&aempty[ab]));
 #pragma unroll
-        for (int i = 0; i < 32; ++i) acc[i] += (double)v[i];
+        for (int i = 0; i < 32; ++i) acc2[i] += v[i];
       };
       const uint32_t ch0 = ch;
       for (int k = 0; k < nu; ++k, ++u) {
         const int sx = u % NX, sb = u % NB;
         mbar_wait(smem_u32(&xfull[sx]), (u / NX) & 1);
         mbar_wait(smem_u32(&bempty[sb]), ((u / NB) & 1) ^ 1);
-        const uint8_t* xb = xst + sx * XSTAGE + h * XBOX;
-        uint8_t* hi = bst + sb * BSTAGE;
-        uint8_t* lo = hi + BTILE;
+        const uint32_t xb = smem_u32(xst) + sx * XSTAGE + h * XBOX;
+        const uint32_t hi = smem_u32(bst) + sb * BSTAGE;
+        const uint32_t lo = hi + BTILE;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {  // bf16 chunk 4h+c = elements 8c..8c+7 of this box
-          const float4 v0 = *reinterpret_cast<const float4*>(xb + sw128(r, 2 * c));
-          const float4 v1 = *reinterpret_cast<const float4*>(xb + sw128(r, 2 * c + 1));
-          const float x[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-          uint32_t h2[4], l2[4];
+          uint32_t x0[4], x1[4];
+          lds128(xb + sw128(r, 2 * c), x0);
+          lds128(xb + sw128(r, 2 * c + 1), x1);
 #pragma unroll
-          for (int e = 0; e < 8; e += 2) {
-            // a non-finite element makes its norm non-finite (x^2 of a finite
-            // float cannot overflow fp64): checked once per row below
-            nrm[c] = fma((double)x[e], (double)x[e], nrm[c]);
-            nrm[c] = fma((double)x[e + 1], (double)x[e + 1], nrm[c]);
-            const __nv_bfloat162 hh = __floats2bfloat162_rn(x[e], x[e + 1]);
-            const float2 hf = __bfloat1622float2(hh);
-            const __nv_bfloat162 ll = __floats2bfloat162_rn(x[e] - hf.x, x[e + 1] - hf.y);
-            h2[e / 2] = *reinterpret_cast<const uint32_t*>(&hh);
-            l2[e / 2] = *reinterpret_cast<const uint32_t*>(&ll);
-          }
-          *reinterpret_cast<uint4*>(hi + sw128(r, 4 * h + c)) = make_uint4(h2[0], h2[1], h2[2], h2[3]);
-          *reinterpret_cast<uint4*>(lo + sw128(r, 4 * h + c)) = make_uint4(l2[0], l2[1], l2[2], l2[3]);
+          for (int e = 0; e < 4; ++e) mx = max(mx, max(x0[e] & 0x7FFFFFFFu, x1[e] & 0x7FFFFFFFu));
+          uint32_t h2[4], l2[4];
+          split2(x0[0], x0[1], h2[0], l2[0]);
+          split2(x0[2], x0[3], h2[1], l2[1]);
+          split2(x1[0], x1[1], h2[2], l2[2]);
+          split2(x1[2], x1[3], h2[3], l2[3]);
+          sts128(hi + sw128(r, 4 * h + c), h2[0], h2[1], h2[2], h2[3]);
+          sts128(lo + sw128(r, 4 * h + c), l2[0], l2[1], l2[2], l2[3]);
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> tensor-core reads
         __syncwarp();
@@ -272,20 +299,27 @@ __global__ void __launch_bounds__(GT, 1) k_gram_tc(const __grid_constant__ CUten
         if ((k + 1) % CHUNK == 0 && k + 1 > CHUNK) epilogue(ch++);  // chunk k/CHUNK - 1
       }
       while (ch < ch0 + (uint32_t)nchunk) epilogue(ch++);
-      // row norm = box-0 half + box-1 half (smem, double-buffered by tile parity)
-      const double t = (nrm[0] + nrm[1]) + (nrm[2] + nrm[3]);
-      if (h == 1) s_nrm[par][r] = t;
+      // row max |x| = max of the two halves (smem, double-buffered by tile parity)
+      if (h == 1) s_mx[par][r] = mx;
       asm volatile("bar.sync 1, 256;" ::: "memory");
       if (real) {
         if (h == 0) {
-          const double tot = t + s_nrm[par][r];
-          p.nrm[(int64_t)item * F + row] = tot;
-          if (!isfinite(tot)) atomicExch(p.bad, 1);
+          const uint32_t m = max(mx, s_mx[par][r]);
+          p.fmx[(int64_t)item * F + row] = m;
+          if (m >= 0x7F800000u) atomicExch(p.bad, 1);  // inf / NaN element
+        }
+        if (h == (row >> 5)) {  // this thread holds column `row`: the diagonal HH + 2 HL
+          double dg = 0.0;
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (i == (row & 31)) dg = acc[i] + 2.0 * (double)acc2[i];
+          p.nrm[(int64_t)item * F + row] = dg;
         }
         double* g = p.G + ((int64_t)item * F + row) * F + h * 32;
+        float* gt = p.GT + ((int64_t)item * F + row) * F + h * 32;
 #pragma unroll
         for (int i = 0; i < 32; ++i)
-          if (h * 32 + i < F) g[i] = acc[i];
+          if (h * 32 + i < F) g[i] = acc[i] + (double)acc2[i], gt[i] = acc2[i];
       }
     }
   }
@@ -293,7 +327,7 @@ __global__ void __launch_bounds__(GT, 1) k_gram_tc(const __grid_constant__ CUten
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
 }
 
@@ -320,7 +354,8 @@ bool gram_tc_supported(int F, int64_t E, const float* lat) {
          (reinterpret_cast<uintptr_t>(lat) & 15) == 0;
 }
 
-void gram_tc(lc_ctx* ctx, const float* lat, int n_items, int F, int64_t E, double* G, double* nrm, int* bad) {
+void gram_tc(lc_ctx* ctx, const float* lat, int n_items, int F, int64_t E, double* G, float* Gt, double* nrm,
+             uint32_t* fmx, int* bad) {
   using namespace gram;
   alignas(64) CUtensorMap tm;
   cuuint64_t gdim[3] = {(cuuint64_t)E, (cuuint64_t)F, (cuuint64_t)n_items};
@@ -338,7 +373,9 @@ void gram_tc(lc_ctx* ctx, const float* lat, int n_items, int F, int64_t E, doubl
   p.E = E;
   p.n_units = (int)(E / KU);
   p.G = G;
+  p.GT = Gt;
   p.nrm = nrm;
+  p.fmx = fmx;
   p.bad = bad;
   const size_t smem = 1024 + NX * XSTAGE + NB * BSTAGE + 256;
   FC_CUDA(cudaFuncSetAttribute(k_gram_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
