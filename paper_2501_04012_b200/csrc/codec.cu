@@ -535,11 +535,18 @@ constexpr int ICT_CHUNK = 1024;  // products staged per step of an exact chain r
 
 __device__ __forceinline__ float f4c(const float4& v, int c) { return c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w; }
 
+// Split over blocks (nsplit > 1, few items, long frames): block (item, sp)
+// sums elements [sp, sp + 1) * E / nsplit, writes its block totals to
+// part_*, and the last block of the item to finish (ticket) adds the nsplit
+// partials in split order -- another reassociation of the same sums, inside
+// the same bounds -- and runs the certification.
 template <int S>
 __global__ void __launch_bounds__(ICT, 2) k_inter_cert(const float* __restrict__ lat, const InterItem* __restrict__ items,
                                                       const int* __restrict__ perm, int F, int64_t E,
-                                                      const double* __restrict__ nrm, InterRes* __restrict__ out,
-                                                      InterCert* __restrict__ cert, int force_replay) {
+                                                      InterRes* __restrict__ out, InterCert* __restrict__ cert,
+                                                      int force_replay, int nsplit, double* __restrict__ part_red,
+                                                      float* __restrict__ part_max, unsigned* __restrict__ part_flag,
+                                                      unsigned* __restrict__ ticket) {
   constexpr int NA = S * (S + 1) / 2;  // A[s<=b] = sum d_s d_b
   constexpr int NP = S * (S - 1);      // P[s!=b] = sum d_b k_s ; Q[s!=b] = sum f_s d_b
   constexpr int NV = NA + 2 * NP + 3 * S;  // + FK[s] = sum f_s k_s, FF[s] = |f_s|^2, KK[s] = |k_s|^2
@@ -551,7 +558,8 @@ __global__ void __launch_bounds__(ICT, 2) k_inter_cert(const float* __restrict__
   __shared__ float s_alpha[S * S];
   __shared__ int s_amb[S * S];
   __shared__ double s_pn[ICT_CHUNK], s_pd[ICT_CHUNK], s_chain;
-  const InterItem it = items[blockIdx.x];
+  const int item = blockIdx.x / nsplit, sp = blockIdx.x - item * nsplit;
+  const InterItem it = items[item];
   const int m = it.m;
   const float* base = lat + (int64_t)it.entry * S * F * E;
   const float4* kp[S];
@@ -569,7 +577,17 @@ __global__ void __launch_bounds__(ICT, 2) k_inter_cert(const float* __restrict__
 #pragma unroll
   for (int s = 0; s < S; ++s) mxf[s] = mxd[s] = 0.f;
   const int64_t n4 = E >> 2;
-  for (int64_t v = threadIdx.x; v < n4; v += ICT) {
+  const int64_t v0 = n4 * sp / nsplit, v1 = n4 * (sp + 1) / nsplit;
+  // the block's 2S frame ranges stream into L2 through the bulk engine first:
+  // with ~250 registers per thread only a few loads per thread are in flight,
+  // so the loop below would otherwise pay full HBM latency per iteration
+  if (threadIdx.x < 2 * S) {
+    const float4* src = threadIdx.x < S ? kp[threadIdx.x] : fp[threadIdx.x - S];
+    for (int64_t c0 = v0; c0 < v1; c0 += 4096)  // <= 64 KB per bulk prefetch
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + c0), "r"((uint32_t)(min(v1 - c0, (int64_t)4096) * 16))
+                   : "memory");
+  }
+  for (int64_t v = v0 + threadIdx.x; v < v1; v += ICT) {
     float4 k4[S], f4[S];
 #pragma unroll
     for (int s = 0; s < S; ++s) {
@@ -673,9 +691,43 @@ __global__ void __launch_bounds__(ICT, 2) k_inter_cert(const float* __restrict__
     s_flag[0][1] = e;
   }
   __syncthreads();
+  if (nsplit > 1) {
+    __shared__ int s_last;
+    const int64_t slot = (int64_t)item * nsplit + sp;
+    if (threadIdx.x < NV) part_red[slot * NV + threadIdx.x] = s_red[0][threadIdx.x];
+    if (threadIdx.x < 2 * S) part_max[slot * 2 * S + threadIdx.x] = s_max[0][threadIdx.x];
+    if (threadIdx.x < 2) part_flag[slot * 2 + threadIdx.x] = s_flag[0][threadIdx.x];
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(&ticket[item], 1u) == (unsigned)(nsplit - 1);
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const int64_t s0 = (int64_t)item * nsplit;
+    if (threadIdx.x < NV) {
+      double x = 0.0;
+      for (int q = 0; q < nsplit; ++q) x += __ldcg(part_red + (s0 + q) * NV + threadIdx.x);
+      s_red[0][threadIdx.x] = x;
+    }
+    if (threadIdx.x < 2 * S) {
+      float x = 0.f;
+      for (int q = 0; q < nsplit; ++q) x = fmaxf(x, __ldcg(part_max + (s0 + q) * 2 * S + threadIdx.x));
+      s_max[0][threadIdx.x] = x;
+    }
+    if (threadIdx.x == 0) {
+      unsigned o = 0, e = (1u << S) - 1;
+      for (int q = 0; q < nsplit; ++q) {
+        o |= __ldcg(part_flag + (s0 + q) * 2);
+        e &= __ldcg(part_flag + (s0 + q) * 2 + 1);
+      }
+      s_flag[0][0] = o;
+      s_flag[0][1] = e;
+    }
+    __syncthreads();
+  }
   // ---- per (s, b) pair: certified alpha ----
-  InterRes* o = out + blockIdx.x;
-  InterCert* oc = cert + blockIdx.x;
+  InterRes* o = out + item;
+  InterCert* oc = cert + item;
   const unsigned NZ = s_flag[0][0], EX = s_flag[0][1];
   const double* R = s_red[0];
   auto Aidx = [](int s, int b) { return s * S - s * (s - 1) / 2 + (b - s); };  // s <= b
@@ -1344,12 +1396,25 @@ void assemble(lc_ctx* ctx, const float* lat, const uint8_t* om, const uint8_t* b
     FC_CUDA(cudaMemcpyAsync(di.p, items_h.data(), di.bytes, cudaMemcpyHostToDevice, ctx->stream));
     // FC_INTER_REPLAY=1 (tests): treat every alpha as ambiguous -> exact chain replay
     const int force_replay = getenv("FC_INTER_REPLAY") && atoi(getenv("FC_INTER_REPLAY")) == 1;
+    // few items on long frames (config[4]: 192 items of 36,864 floats) leave
+    // SMs idle: split each item's elements over blocks (>= 2 waves of the 2
+    // resident blocks per SM, >= 1024 float4 per block)
+    const int64_t want_blocks = 4LL * ctx->sm_count;
+    int nsplit = (int)std::min<int64_t>(std::max<int64_t>(1, (want_blocks + (int64_t)items.size() - 1) / (int64_t)items.size()),
+                                        std::max<int64_t>(1, (E / 4) / 1024));
+    nsplit = std::min(nsplit, 16);
+    DevBuf pred(nsplit > 1 ? items.size() * nsplit * 80 * sizeof(double) : 16, ctx->stream);
+    DevBuf pmax(nsplit > 1 ? items.size() * nsplit * 2 * MAXS * sizeof(float) : 16, ctx->stream);
+    DevBuf pflag(nsplit > 1 ? items.size() * nsplit * 2 * sizeof(unsigned) : 16, ctx->stream);
+    DevBuf tick(items.size() * sizeof(unsigned), ctx->stream);
+    FC_CUDA(cudaMemsetAsync(tick.p, 0, tick.bytes, ctx->stream));
     {
       KTimer kt(ctx, "inter");
-      const unsigned nb = (unsigned)items.size();
+      const unsigned nb = (unsigned)(items.size() * nsplit);
       auto args = [&](auto kern) {
-        kern<<<nb, ICT, 0, ctx->stream>>>(lat, di.as<InterItem>(), dp.as<int>(), F, E, nrm_dev, dr.as<InterRes>(),
-                                          dc.as<InterCert>(), force_replay);
+        kern<<<nb, ICT, 0, ctx->stream>>>(lat, di.as<InterItem>(), dp.as<int>(), F, E, dr.as<InterRes>(),
+                                          dc.as<InterCert>(), force_replay, nsplit, pred.as<double>(), pmax.as<float>(),
+                                          pflag.as<unsigned>(), tick.as<unsigned>());
       };
       switch (S) {
         case 1: args(k_inter_cert<1>); break;

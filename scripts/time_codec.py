@@ -7,7 +7,8 @@ import paper_2501_04012_b200 as fc
 import bench
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 256
 F = int(sys.argv[2]) if len(sys.argv) > 2 else 64
-dims = (40, 64, 4); E = 40 * 64 * 4
+dims = tuple(int(x) for x in sys.argv[3].split('x')) if len(sys.argv) > 3 else (40, 64, 4)  # e.g. 72x128x4 (config[4])
+E = dims[0] * dims[1] * dims[2]
 dev = torch.device('cuda', 0)
 stream = torch.cuda.Stream(); torch.cuda.set_stream(stream)
 ctx = fc.Context(0, stream=stream.cuda_stream)
@@ -45,5 +46,5 @@ half = n // 2
 out2 = torch.empty((half, F, E), dtype=torch.float32, device=dev)
 fc.decompress_stitch(ents[:half], ents[half:2 * half], [15] * half, out=out2); kt()
 fc.decompress_stitch(ents[:half], ents[half:2 * half], [15] * half, out=out2); k = kt()
-sb = half * F * E * 4 * 2 + 2 * half * F * (40 * 64 // 8)
+sb = half * F * E * 4 * 2 + 2 * half * F * (dims[0] * dims[1] // 8)
 print(f"decompress_stitch: {k.get('decompress_stitch')} ms = {sb / (k['decompress_stitch'] / 1e3) / 1e9:.0f} GB/s")
