@@ -735,7 +735,9 @@ def bench_codec_large(torch, fc, ctx, args, dev, peaks):
     cache checkpoint (save_snapshot, store.cpp:232-274, with serialize_entry,
     codec.cpp:358-392) of a store holding them -- written to /dev/shm so the
     number is the serializer's, not a disk's. (The 200k-entry, 8-GPU size of
-    config[4] does not fit one box: ~5 MB per compressed entry x 200k.)"""
+    config[4] is 25k entries per GPU: scripts/config3_scale.py --dims 72x128x4
+    runs that share through the engine with periodic whole-cache checkpoints,
+    profiles/r02bf_config4_25k.json.)"""
     import tempfile
     n, F = args.large_prompts, 64
     dims = (72, 128, 4)

@@ -1906,6 +1906,42 @@ void compress_chunk(lc_ctx* ctx, const float* lat, const uint8_t* om, const uint
 }  // namespace
 
 namespace fc {
+
+// serialize_entry (codec.cpp:358-392) of the entry view e from a host copy
+// `img` of its device image (d.dev_bytes bytes) into out[0, cap); returns the
+// bytes written (= entry_compressed_size(e)).
+uint64_t serialize_entry_image(const lc_entry* e, const uint8_t* img, uint8_t* out, uint64_t cap) {
+  const EntryData& d = *e->d;
+  const float* fb = reinterpret_cast<const float*>(img);
+  Writer w{out, cap};
+  w.u64(d.prompt);
+  w.u8((uint8_t)d.base_step);
+  w.u8((uint8_t)e->sel.size());
+  w.u16((uint16_t)d.n_diff());
+  w.u16((uint16_t)d.F);
+  w.u16((uint16_t)d.H);
+  w.u16((uint16_t)d.W);
+  w.u16((uint16_t)d.C);
+  for (int si : e->sel) {
+    w.u8((uint8_t)d.steps[si]);
+    w.f32s(fb + d.first_off[si], d.E);
+    for (int j = 0; j < d.F; ++j) w.u16((uint16_t)d.maps[si][j]);
+    if (d.steps[si] != d.base_step) w.f32s(d.alphas[si].data(), (int64_t)d.alphas[si].size());
+    w.u16((uint16_t)d.extra_idx[si].size());
+    for (size_t x = 0; x < d.extra_idx[si].size(); ++x) {
+      w.u16((uint16_t)d.extra_idx[si][x]);
+      w.f32s(fb + d.extra_off[si][x], d.E);
+    }
+  }
+  for (int t = 0; t < d.n_diff(); ++t) {
+    w.u16((uint16_t)d.diff_idx[t]);
+    w.f32s(fb + d.diff_off[t], d.E);
+  }
+  w.put(img + d.mask_off, 2ull * d.F * d.mb);
+  if (w.n != entry_compressed_size(e)) raise(LC_ERR_INTERNAL, "serialize_entry: size accounting mismatch");
+  return w.n;
+}
+
 // deserialize_entry (codec.cpp:395-473) from the front of bytes[0, len):
 // parses one entry, reports the bytes it used, uploads it to HBM. Errors as
 // the reference (SnapshotError offsets relative to the entry start).
@@ -2245,33 +2281,7 @@ lc_status lc_entry_export(lc_entry* e, uint8_t* bytes, uint64_t cap, uint64_t* l
   std::vector<uint8_t> img(d.dev_bytes);
   FC_CUDA(cudaMemcpyAsync(img.data(), d.dev, d.dev_bytes, cudaMemcpyDeviceToHost, d.ctx->stream));
   sync(d.ctx);
-  const float* fb = reinterpret_cast<const float*>(img.data());
-  Writer w{bytes, cap};
-  w.u64(d.prompt);
-  w.u8((uint8_t)d.base_step);
-  w.u8((uint8_t)e->sel.size());
-  w.u16((uint16_t)d.n_diff());
-  w.u16((uint16_t)d.F);
-  w.u16((uint16_t)d.H);
-  w.u16((uint16_t)d.W);
-  w.u16((uint16_t)d.C);
-  for (int si : e->sel) {
-    w.u8((uint8_t)d.steps[si]);
-    w.f32s(fb + d.first_off[si], d.E);
-    for (int j = 0; j < d.F; ++j) w.u16((uint16_t)d.maps[si][j]);
-    if (d.steps[si] != d.base_step) w.f32s(d.alphas[si].data(), (int64_t)d.alphas[si].size());
-    w.u16((uint16_t)d.extra_idx[si].size());
-    for (size_t x = 0; x < d.extra_idx[si].size(); ++x) {
-      w.u16((uint16_t)d.extra_idx[si][x]);
-      w.f32s(fb + d.extra_off[si][x], d.E);
-    }
-  }
-  for (int t = 0; t < d.n_diff(); ++t) {
-    w.u16((uint16_t)d.diff_idx[t]);
-    w.f32s(fb + d.diff_off[t], d.E);
-  }
-  w.put(img.data() + d.mask_off, 2ull * d.F * d.mb);
-  if (w.n != total) raise(LC_ERR_INTERNAL, "lc_entry_export: size accounting mismatch");
+  serialize_entry_image(e, img.data(), bytes, cap);
   LC_API_END
 }
 

@@ -629,6 +629,7 @@ lc_status lc_engine_process(lc_engine* e, const lc_request* req, int64_t n, cons
   flush();
   index_flush();
   release_spec();
+  if (served_dev) sync(e->ctx);  // decoupled hits are stitched stream-ordered (lc_decompress_stitch_batch)
   } catch (...) {
     // requests before the failing one are complete: apply their updates
     try {

@@ -124,6 +124,8 @@ struct lc_entry {
 namespace fc {
 lc_entry* make_entry_view(const std::shared_ptr<EntryData>& d, std::vector<int> sel);
 uint64_t entry_compressed_size(const lc_entry* e);
+// serialize_entry of e from a host copy of its device image (codec.cu)
+uint64_t serialize_entry_image(const lc_entry* e, const uint8_t* img, uint8_t* out, uint64_t cap);
 // deserialize_entry from the front of bytes[0, len) (codec.cu); *consumed = bytes used
 lc_entry* import_entry(lc_ctx* ctx, const uint8_t* bytes, uint64_t len, uint64_t* consumed);
 // Decompress n (entry, step-index) pairs into out [n][F][E] on the ctx stream.

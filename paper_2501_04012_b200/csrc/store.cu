@@ -28,6 +28,10 @@
 #include <queue>
 #include <unordered_map>
 #include <unordered_set>
+#include <fcntl.h>
+#include <unistd.h>
+#include <mutex>
+#include <cstring>
 
 #include "entry.hpp"
 #include "topk.cuh"
@@ -1468,49 +1472,93 @@ lc_status lc_snapshot_save(lc_store* s, lc_index* ix, const char* path) {
     }
   }
   w.u32((uint32_t)s->prompts.size());
-  // records: entry images pulled from HBM in prompt order, then the live
-  // records appended and the per-record CRC32s computed in parallel
-  std::vector<std::vector<uint8_t>> bodies(s->prompts.size());
-  std::vector<uint32_t> crcs(bodies.size());
-  {
-    size_t i = 0;
-    for (const auto& kv : s->prompts) {  // ascending prompt id (std::map)
-      const lc_store::Rec& r = kv.second;
-      const uint64_t elen = entry_compressed_size(r.view);
-      std::vector<uint8_t>& body = bodies[i++];
-      body.resize(elen + 1 + r.live.size() * 33);
-      uint64_t got = 0;
-      check_status(lc_entry_export(r.view, body.data(), elen, &got));
-      body.resize(got);
-      BW lb;
-      lb.u8((uint8_t)r.live.size());
-      for (const auto& l : r.live) {  // ascending step
-        lb.u8((uint8_t)l.step);
-        lb.u64(l.f);
-        lb.u64(l.last);
-        lb.u64(l.inserted_at);
-        lb.u64(l.seq);
-      }
-      body.insert(body.end(), lb.b.begin(), lb.b.end());
+  // Records, in ascending prompt id (std::map): u32 len | entry image |
+  // live records | u32 CRC32(body). Every record's size and file offset is
+  // known from the host metadata, so up to 16 host threads each pull an entry
+  // image from HBM (own stream, pinned staging), serialize it, checksum it
+  // and pwrite it at its offset: no whole-file buffer, no serial copy.
+  struct Job {
+    const lc_store::Rec* r;
+    uint64_t elen, off;
+  };
+  std::vector<Job> jobs;
+  jobs.reserve(s->prompts.size());
+  uint64_t off = w.b.size(), max_img = 0, max_rec = 0;
+  for (const auto& kv : s->prompts) {
+    const lc_store::Rec& r = kv.second;
+    const uint64_t elen = entry_compressed_size(r.view);
+    const uint64_t rec = 4 + elen + 1 + 33ull * r.live.size() + 4;
+    jobs.push_back(Job{&r, elen, off});
+    off += rec;
+    max_rec = std::max(max_rec, rec);
+    max_img = std::max<uint64_t>(max_img, r.view->d->dev_bytes);
+  }
+  sync(s->ctx);  // entry images complete on the store's stream
+  const int fd = open(path, O_WRONLY | O_CREAT | O_TRUNC, 0644);
+  if (fd < 0) raise(LC_ERR_IO, std::string("cannot open snapshot for writing: ") + path);
+  auto pwrite_all = [&](const uint8_t* p, uint64_t n, uint64_t at) {
+    while (n > 0) {
+      const ssize_t k = pwrite(fd, p, n, (off_t)at);
+      if (k <= 0) return false;
+      p += k, n -= (uint64_t)k, at += (uint64_t)k;
     }
-  }
-  par_for(bodies.size(), [&](size_t i) { crcs[i] = crc32_of(bodies[i].data(), bodies[i].size()); });
+    return true;
+  };
+  std::atomic<bool> io_ok{pwrite_all(w.b.data(), w.b.size(), 0)};
+  std::exception_ptr err = nullptr;
+  std::mutex err_mu;
+  std::atomic<size_t> next{0};
+  const int dev = s->ctx->device;
+  const int nt = (int)std::min<size_t>(jobs.size(), std::min(16u, std::max(1u, std::thread::hardware_concurrency())));
+  auto worker = [&] {
+    try {
+      DeviceGuard g2(dev);
+      cudaStream_t st = nullptr;
+      FC_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+      struct StreamGuard {
+        cudaStream_t s;
+        ~StreamGuard() { cudaStreamDestroy(s); }
+      } sg{st};
+      PinnedBuf<uint8_t> img(max_img);
+      std::vector<uint8_t> rec(max_rec);
+      for (size_t i; (i = next.fetch_add(1)) < jobs.size() && io_ok.load();) {
+        const Job& j = jobs[i];
+        const lc_entry* view = j.r->view;
+        const EntryData& d = *view->d;
+        FC_CUDA(cudaMemcpyAsync(img.data(), d.dev, d.dev_bytes, cudaMemcpyDeviceToHost, st));
+        FC_CUDA(cudaStreamSynchronize(st));
+        uint8_t* body = rec.data() + 4;
+        serialize_entry_image(view, img.data(), body, j.elen);
+        uint8_t* q = body + j.elen;
+        *q++ = (uint8_t)j.r->live.size();
+        for (const auto& l : j.r->live) {  // ascending step
+          *q++ = (uint8_t)l.step;
+          memcpy(q, &l.f, 8), q += 8;
+          memcpy(q, &l.last, 8), q += 8;
+          memcpy(q, &l.inserted_at, 8), q += 8;
+          memcpy(q, &l.seq, 8), q += 8;
+        }
+        const uint32_t blen = (uint32_t)(q - body);
+        memcpy(rec.data(), &blen, 4);
+        const uint32_t crc = crc32_of(body, blen);
+        memcpy(q, &crc, 4);
+        if (!pwrite_all(rec.data(), (uint64_t)blen + 8, j.off)) io_ok = false;
+      }
+    } catch (...) {
+      std::lock_guard<std::mutex> lk(err_mu);
+      if (!err) err = std::current_exception();
+      io_ok = false;
+    }
+  };
   {
-    size_t total = w.b.size();
-    for (const auto& b : bodies) total += b.size() + 8;
-    w.b.reserve(total);
+    std::vector<std::thread> th;
+    for (int t = 1; t < nt; ++t) th.emplace_back(worker);
+    if (nt >= 1) worker();
+    for (auto& t : th) t.join();
   }
-  for (size_t i = 0; i < bodies.size(); ++i) {
-    w.u32((uint32_t)bodies[i].size());
-    w.raw(bodies[i].data(), bodies[i].size());
-    w.u32(crcs[i]);
-    std::vector<uint8_t>().swap(bodies[i]);
-  }
-  FILE* f = fopen(path, "wb");
-  if (!f) raise(LC_ERR_IO, std::string("cannot open snapshot for writing: ") + path);
-  const size_t wr = fwrite(w.b.data(), 1, w.b.size(), f);
-  const int cl = fclose(f);
-  if (wr != w.b.size() || cl != 0) raise(LC_ERR_IO, std::string("snapshot write failed: ") + path);
+  const int cl = close(fd);
+  if (err) std::rethrow_exception(err);
+  if (!io_ok.load() || cl != 0) raise(LC_ERR_IO, std::string("snapshot write failed: ") + path);
   LC_API_END
 }
 
@@ -1520,12 +1568,23 @@ lc_status lc_snapshot_load(lc_ctx* ctx, const char* path, lc_store** store_out, 
   DeviceGuard g(ctx->device);
   std::vector<uint8_t> raw;
   {
-    FILE* f = fopen(path, "rb");
-    if (!f) raise(LC_ERR_IO, std::string("cannot open snapshot: ") + path);
-    uint8_t buf[1 << 16];
-    size_t k;
-    while ((k = fread(buf, 1, sizeof buf, f)) > 0) raw.insert(raw.end(), buf, buf + k);
-    fclose(f);
+    // one sized read (the file can be tens of GB: no chunked vector growth)
+    const int fd = open(path, O_RDONLY);
+    if (fd < 0) raise(LC_ERR_IO, std::string("cannot open snapshot: ") + path);
+    const off_t sz = lseek(fd, 0, SEEK_END);
+    bool ok = sz >= 0;
+    if (ok) {
+      raw.resize((size_t)sz);
+      uint64_t got = 0;
+      while (got < (uint64_t)sz) {
+        const ssize_t k = pread(fd, raw.data() + got, (size_t)sz - got, (off_t)got);
+        if (k <= 0) break;
+        got += (uint64_t)k;
+      }
+      ok = got == (uint64_t)sz;
+    }
+    close(fd);
+    if (!ok) raise(LC_ERR_IO, std::string("cannot read snapshot: ") + path);
   }
   BR r{raw.data(), raw.size()};
   const uint8_t* magic = r.bytes(4);

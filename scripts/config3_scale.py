@@ -1,4 +1,5 @@
-"""config[3] at its stated size on one B200 (diagnostic run, not the bench):
+"""config[3] (and config[4] per GPU) at stated size on one B200 (diagnostic
+run, not the bench):
 a cold engine serves R requests (default 100,000 = 100k entries offered to the
 cache) of 64-frame 4x40x64 latents with Zipf(1.0) prompt reuse over 20,000
 templates (popularity reshuffled every R/4 requests) under a fixed
@@ -13,7 +14,12 @@ metrics and the final store contents must be identical (bitwise).
 
   python scripts/config3_scale.py [--requests 100000] [--capacity-gb 16]
                                   [--prefix 400] [--prefix-capacity-gb 0.25]
-Prints one JSON object (throughput + parity verdict).
+config[4] per GPU (200k entries over 8 B200 = 25k offered per GPU; large
+latents; per-step cache checkpoints = lc_snapshot_save of the whole store +
+index every --checkpoint-every requests, timed apart from the serving):
+  python scripts/config3_scale.py --dims 72x128x4 --batch 64 --requests 25000 \
+      --capacity-gb 16 --checkpoint-every 5000 --prefix 96 --prefix-capacity-gb 1
+Prints one JSON object (throughput + checkpoints + parity verdict).
 """
 import argparse
 import ctypes as C
@@ -31,7 +37,8 @@ sys.path.insert(0, os.path.join(ROOT, "oracle"))
 import paper_2501_04012_b200 as fc  # noqa: E402
 import bench  # noqa: E402
 
-F, DIMS, D = 64, (40, 64, 4), 768
+F, D = 64, 768
+DIMS = (40, 64, 4)
 N_T = 20000
 B = 256
 
@@ -65,13 +72,13 @@ class Trace:
         return qs, lat, om, bm
 
 
-def run_product(ctx, dev, n_r, cap, keep=0):
+def run_product(ctx, dev, n_r, cap, keep=0, ckpt_every=0, ckpt_dir="/dev/shm"):
     """Serve n_r requests; returns (requests/s, outcomes of the first `keep`,
-    inputs of the first `keep` (host), engine)."""
+    inputs of the first `keep` (host), engine, evicted steps, checkpoints)."""
     cfg = fc.engine_config(dim=D, F=F, H=DIMS[0], W=DIMS[1], C=DIMS[2], policy=int(fc.Policy.Lrbu), capacity=cap)
     eng = fc.Engine(cfg, ctx=ctx)
     tr = Trace(ctx, dev, n_r)
-    dt, outs, inputs, ev = 0.0, [], [], 0
+    dt, outs, inputs, ev, ckpts = 0.0, [], [], 0, []
     for j0 in range(0, n_r, B):
         m = min(B, n_r - j0)
         qs, lat, om, bm = tr.batch(j0, m)
@@ -88,7 +95,16 @@ def run_product(ctx, dev, n_r, cap, keep=0):
             inputs.append((prompts[:k], [q[:k] for q in qs], lat[:k].cpu().numpy(), om[:k].cpu().numpy(),
                            bm[:k].cpu().numpy()))
         del lat, om, bm
-    return n_r / dt, outs, inputs, eng, ev
+        done = j0 + m
+        if ckpt_every and (done % ckpt_every < B or done == n_r) and done >= ckpt_every:
+            path = os.path.join(ckpt_dir, f"flexcache_ckpt_{os.getpid()}.flxc")
+            t0 = time.perf_counter()
+            eng.save_snapshot(path)
+            sv = time.perf_counter() - t0
+            sz = os.path.getsize(path)
+            os.remove(path)
+            ckpts.append({"after_requests": done, "bytes": sz, "save_s": round(sv, 3), "GBps": round(sz / sv / 1e9, 3)})
+    return n_r / dt, outs, inputs, eng, ev, ckpts
 
 
 def cmp(a, b, j):
@@ -113,20 +129,32 @@ def main():
     ap.add_argument("--capacity-gb", type=float, default=16.0)
     ap.add_argument("--prefix", type=int, default=400)
     ap.add_argument("--prefix-capacity-gb", type=float, default=0.25)
+    ap.add_argument("--dims", default="40x64x4")
+    ap.add_argument("--batch", type=int, default=256)
+    ap.add_argument("--checkpoint-every", type=int, default=0)
+    ap.add_argument("--snapshot-dir", default="/dev/shm")
     args = ap.parse_args()
+    global DIMS, B
+    DIMS = tuple(int(x) for x in args.dims.split("x"))
+    B = args.batch
     dev = torch.device("cuda", 0)
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     ctx = fc.Context(0, stream=stream.cuda_stream)
-    res = {"workload": f"config[3]: {args.requests} requests (entries offered), 64 x 40x64x4 fp32 latents, "
+    res = {"workload": f"{args.requests} requests (entries offered), 64 x {args.dims} fp32 latents, "
                        f"768-d embeddings, Zipf(1.0) over {N_T} templates with popularity reshuffles, LRBU, "
                        f"capacity {args.capacity_gb} GiB, batches of {B}"}
-    rps, _, _, eng, ev = run_product(ctx, dev, args.requests, int(args.capacity_gb * (1 << 30)))
+    rps, _, _, eng, ev, ckpts = run_product(ctx, dev, args.requests, int(args.capacity_gb * (1 << 30)),
+                                            ckpt_every=args.checkpoint_every, ckpt_dir=args.snapshot_dir)
     m = eng.metrics()
     res.update({"requests_per_s": rps, "evicted_steps": ev, "store_used_bytes": eng.store.used(),
                 "live_prompts": len({e.as_tuple()[0] for e in eng.store.entries_snapshot()}),
                 "whole_hits": m["whole_hits"], "decoupled_hits": m["decoupled_hits"], "misses": m["misses"],
                 "computation_savings": m["computation_savings"]})
+    if ckpts:
+        res["checkpoints"] = {"api": "Engine.save_snapshot = lc_snapshot_save (FLXC v1, byte-identical to the "
+                                     "reference's save_snapshot, store.cpp:232-274), whole store + index",
+                              "target": args.snapshot_dir, "runs": ckpts}
     del eng
     # ---- parity on the prefix (same trace, small capacity so evictions start early) ----
     if args.prefix > 0:
@@ -134,7 +162,7 @@ def main():
         from engine import OracleEngine
         orc = Checker("orc")
         cap = int(args.prefix_capacity_gb * (1 << 30))
-        _, outs, inputs, eng, ev = run_product(ctx, dev, args.prefix, cap, keep=args.prefix)
+        _, outs, inputs, eng, ev, _ = run_product(ctx, dev, args.prefix, cap, keep=args.prefix)
         oe = OracleEngine(orc, D, F, *DIMS, capacity=cap, policy=int(fc.Policy.Lrbu))
         t0 = time.perf_counter()
         exp, j, bad = [], 0, None

@@ -316,3 +316,27 @@ def test_large_latent_shape_config4(fc, orc, synth):
     db = orc.decompress(ents[1].serialize(), 20, F, E_)
     exp = orc.stitch(da, om[0], bm[0], db, om[1], bm[1], dims)
     assert (bits(fused) == bits(exp)).all()
+
+
+def test_gram_range_guard_and_denormals(fc, orc, synth):
+    """The tensor-core Gram's error model holds for frames whose max |x| lies in
+    [2^-40, 2^56] (gram_sm100.cu); items with a frame outside (tiny or huge
+    scales, all-denormal frames) must take select's exact path, and denormal
+    elements must not be mistaken for zeros (zero-norm rule, core.cpp:111-112).
+    Wire bytes equal the restatement's in every case."""
+    dims = (8, 8, 4)
+    F = 16
+    n = 4
+    lat = np.stack([synth.latents(300 + i, F=F, dims=dims) for i in range(n)]).astype(np.float32)
+    lat[0, 1] *= np.float32(1e-13)             # a whole step below 2^-40
+    lat[1, 2, 5] *= np.float32(1e17)           # one frame above 2^56
+    lat[2, 3, 7, :5] = np.float32(1e-40)       # denormal elements in a normal frame
+    lat[3, 4, 3] = (lat[3, 4, 3] * np.float32(1e-41)).astype(np.float32)  # an all-denormal (nonzero) frame
+    assert np.all(lat[3, 4, 3][lat[3, 4, 3] != 0] < 1.2e-38)
+    masks = [synth.rect_masks(F, dims[0], dims[1], 300 + i) for i in range(n)]
+    om = np.stack([m[0] for m in masks])
+    bm = np.stack([m[1] for m in masks])
+    prompts = [40 + i for i in range(n)]
+    ents, _ = fc.compress_batch(lat, synth.CACHED_STEPS, om, bm, dims, prompts)
+    for i in range(n):
+        assert ents[i].serialize() == orc.compress(lat[i], synth.CACHED_STEPS, om[i], bm[i], dims, prompts[i]), i
