@@ -702,6 +702,10 @@ def bench_codec(torch, fc, ctx, args, dev, peaks):
     dk_bytes = dec_bytes / 5 if dk_n else 0
     dk_gbs = (dec_bytes * dec_reps) / (dk_t / 1000) / 1e9 if dk_t else None
     stitch_bytes = half * F * E * 4 * 2 + 2 * half * F * (40 * 64 // 8)  # out + selected source reads + masks
+    dec_traffic = None  # ncu dram read + write per launch (profiles/, one --set full capture), if present
+    tpath = os.path.join(ROOT, "profiles", "decompress_traffic.json")
+    if os.path.exists(tpath) and n == 256 and F == 64:
+        dec_traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
     cpu = None
     if not args.no_cpu:
         try:
@@ -720,7 +724,7 @@ def bench_codec(torch, fc, ctx, args, dev, peaks):
         "compress_timing": "median of 5 calls, wall clock, inputs device-resident",
         "decompress_GBps_e2e": dec_bytes / dec_s / 1e9, "decompress_frac_hbm_e2e": dec_bytes / dec_s / 1e9 / hbm,
         "roofline": {"bound": "hbm", "achieved": round(dk_gbs, 1) if dk_gbs else None, "peak": hbm, "unit": "GB/s",
-                     "frac": round(dk_gbs / hbm, 4) if dk_gbs else None, "traffic": None,
+                     "frac": round(dk_gbs / hbm, 4) if dk_gbs else None, "traffic": dec_traffic,
                      "kernel": "k_decompress_groups", "bytes_per_launch": int(dk_bytes),
                      "avg_launch_ms": round(dk_t / dk_n, 4) if dk_n else None},
         "decompress_stitch_GBps": (stitch_bytes / (t_.value / 1000) / 1e9) if t_.value else None,
