@@ -115,6 +115,12 @@ struct KTimer {
     t->prof[name].emplace_back(a, b);
     a = nullptr;
   }
+  void cancel() {  // drop the interval (the caller times a narrower one)
+    if (!a) return;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    a = b = nullptr;
+  }
   ~KTimer() { stop(); }
 };
 }  // namespace fc

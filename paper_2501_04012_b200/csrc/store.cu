@@ -384,6 +384,11 @@ struct FusedScratch {
   int* rep;                    // [8] report: pick[5], n_out, bad (follows head)
 };
 
+// REG: the store fits KR keys per thread of the grid, so each thread keeps
+// its slots' key images in registers across the phases (no K[] round trips
+// through memory) and issues all its slot loads before the prompt gathers.
+constexpr int KR = 8;
+template <bool REG>
 __global__ void __launch_bounds__(SEG_T, 1) k_policy_fused(const DevLive* __restrict__ live, int64_t n_slots,
                                                            const DevPrompt* __restrict__ prompts, int policy,
                                                            uint64_t now, FusedScratch S) {
@@ -393,20 +398,50 @@ __global__ void __launch_bounds__(SEG_T, 1) k_policy_fused(const DevLive* __rest
   __shared__ int s_pick[5];
   const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+  uint64_t kr[REG ? KR : 1];
   // (A) key image of every slot, min/max
   {
     uint64_t lo = ~0ull, hi = 0;
     int b = 0;
-    for (int64_t i = gtid; i < n_slots; i += gstride) {
-      const DevLive l = live[i];
-      uint64_t k = ~0ull;
-      if (l.step != 0) {
-        uint64_t cap;
-        k = key_bits(pkey(policy, l, prompts[l.pslot], now, &cap, &b));
-        lo = k < lo ? k : lo;
-        hi = k > hi ? k : hi;
+    if constexpr (REG) {
+      constexpr int G = 4;  // slots loaded together (registers: 4 x (40 + 16) bytes in flight)
+#pragma unroll
+      for (int j0 = 0; j0 < KR; j0 += G) {
+        DevLive lv[G];
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+          const int64_t i = gtid + (j0 + j) * gstride;
+          if (i < n_slots) lv[j] = live[i];
+          else lv[j].step = 0;
+        }
+        DevPrompt pv[G];
+#pragma unroll
+        for (int j = 0; j < G; ++j)
+          if (lv[j].step != 0) pv[j] = prompts[lv[j].pslot];
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+          uint64_t k = ~0ull;
+          if (lv[j].step != 0) {
+            uint64_t cap;
+            k = key_bits(pkey(policy, lv[j], pv[j], now, &cap, &b));
+            lo = k < lo ? k : lo;
+            hi = k > hi ? k : hi;
+          }
+          kr[j0 + j] = k;
+        }
       }
-      S.K[i] = k;
+    } else {
+      for (int64_t i = gtid; i < n_slots; i += gstride) {
+        const DevLive l = live[i];
+        uint64_t k = ~0ull;
+        if (l.step != 0) {
+          uint64_t cap;
+          k = key_bits(pkey(policy, l, prompts[l.pslot], now, &cap, &b));
+          lo = k < lo ? k : lo;
+          hi = k > hi ? k : hi;
+        }
+        S.K[i] = k;
+      }
     }
     if (b) atomicExch(&S.n_acc[1], 1);
 #pragma unroll
@@ -425,18 +460,29 @@ __global__ void __launch_bounds__(SEG_T, 1) k_policy_fused(const DevLive* __rest
   const int sh = bin_shift(lo, hi);
   const int sh2 = sh > 12 ? sh - 12 : 0;
   unsigned* h = reinterpret_cast<unsigned*>(sm);  // [NBIN] block histogram
+  // every slot of this thread in lockstep across the warp (gstride % 32 == 0):
+  // f(key, slot) with key ~0 for dead / out-of-range slots
+  auto each = [&](auto f) {
+    if constexpr (REG) {
+#pragma unroll
+      for (int j = 0; j < KR; ++j) f(kr[j], gtid + j * gstride);
+    } else {
+      for (int64_t i0 = gtid - (threadIdx.x & 31); i0 < n_slots; i0 += gstride) {
+        const int64_t i = i0 + (threadIdx.x & 31);
+        f(i < n_slots ? S.K[i] : ~0ull, i);
+      }
+    }
+  };
   // (B) histogram of (key - min) >> sh
   for (int t = threadIdx.x; t < NBIN; t += blockDim.x) h[t] = 0;
   __syncthreads();
   // warp-aggregated: policy keys cluster in few bins (e.g. many LRBU keys
   // share an order of magnitude), and same-bin shared atomics serialize
-  for (int64_t i0 = gtid - (threadIdx.x & 31); i0 < n_slots; i0 += gstride) {
-    const int64_t i = i0 + (threadIdx.x & 31);
-    const uint64_t k = i < n_slots ? S.K[i] : ~0ull;
+  each([&](uint64_t k, int64_t) {
     const int bin = k != ~0ull ? (int)((k - lo) >> sh) : -1;
     const unsigned peers = __match_any_sync(0xffffffffu, bin);
     if (bin >= 0 && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&h[bin], (unsigned)__popc(peers));
-  }
+  });
   __syncthreads();
   for (int t = threadIdx.x; t < NBIN; t += blockDim.x)
     if (h[t]) atomicAdd(&S.hist[t], h[t]);
@@ -460,13 +506,11 @@ __global__ void __launch_bounds__(SEG_T, 1) k_policy_fused(const DevLive* __rest
     for (int t = threadIdx.x; t < NBIN; t += blockDim.x) h[t] = 0;
     __syncthreads();
     const uint64_t tb = (uint64_t)s_pick[0];
-    for (int64_t i0 = gtid - (threadIdx.x & 31); i0 < n_slots; i0 += gstride) {
-      const int64_t i = i0 + (threadIdx.x & 31);
-      const uint64_t k = i < n_slots ? S.K[i] : ~0ull;
+    each([&](uint64_t k, int64_t) {
       const int bin = (k != ~0ull && ((k - lo) >> sh) == tb) ? (int)(((k - lo) >> sh2) & (NBIN - 1)) : -1;
       const unsigned peers = __match_any_sync(0xffffffffu, bin);
       if (bin >= 0 && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&h[bin], (unsigned)__popc(peers));
-    }
+    });
     __syncthreads();
     for (int t = threadIdx.x; t < NBIN; t += blockDim.x)
       if (h[t]) atomicAdd(&S.hist2[t], h[t]);
@@ -483,15 +527,14 @@ __global__ void __launch_bounds__(SEG_T, 1) k_policy_fused(const DevLive* __rest
   // (E) collect the survivors
   if (s_pick[4] <= CAP) {
     const uint64_t tb = (uint64_t)s_pick[0], tb2 = (uint64_t)s_pick[3];
-    for (int64_t i = gtid; i < n_slots; i += gstride) {
-      const uint64_t k = S.K[i];
-      if (k == ~0ull) continue;
+    each([&](uint64_t k, int64_t i) {
+      if (k == ~0ull) return;
       const uint64_t b = (k - lo) >> sh;
       if (b < tb || (b == tb && (((k - lo) >> sh2) & (NBIN - 1)) <= tb2)) {
         const int at = atomicAdd(&S.n_acc[0], 1);
         if (at < CAP) S.items[at] = ScoreItem{k, live[i].seq, i};
       }
-    }
+    });
   }
   grid.sync();
   if (blockIdx.x != 0) return;
@@ -739,6 +782,7 @@ struct lc_store {
     DevBuf cur;
     const bool fused = !(getenv("FC_SCORE_FUSED") && atoi(getenv("FC_SCORE_FUSED")) == 0);
     if (fast && fused) {
+      kt.cancel();  // the kernel alone is timed below (host set-up between two events would count as GPU time)
       KTimer kcall(ctx, "policy_call");  // launch through the report readback (one scoring as the host sees it)
       size_t rep_off = 0, rep_bytes = 0;
       const int64_t had = fs_slots;
@@ -750,22 +794,29 @@ struct lc_store {
       static std::atomic<uint64_t> fattr{0};
       static int blocks_per_sm = 0;
       if (!(fattr.load() & (1ull << (ctx->device & 63)))) {
-        FC_CUDA(cudaFuncSetAttribute(k_policy_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        FC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_policy_fused, SEG_T, smem));
+        FC_CUDA(cudaFuncSetAttribute(k_policy_fused<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        FC_CUDA(cudaFuncSetAttribute(k_policy_fused<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int b1 = 0, b2 = 0;
+        FC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k_policy_fused<true>, SEG_T, smem));
+        FC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k_policy_fused<false>, SEG_T, smem));
+        blocks_per_sm = std::min(b1, b2);
         fattr.fetch_or(1ull << (ctx->device & 63));
       }
       if (blocks_per_sm < 1) raise(LC_ERR_CUDA, "fused scoring kernel cannot be resident");
       const int grid = (int)std::min<int64_t>(ctx->sm_count, std::max<int64_t>(1, (n_slots + SEG_T - 1) / SEG_T));
+      const bool reg = n_slots <= (int64_t)KR * grid * SEG_T && !(getenv("FC_SCORE_REG") && atoi(getenv("FC_SCORE_REG")) == 0);
       const DevLive* a0 = dl;
       const DevPrompt* a2 = dp;
       int a3 = policy;
       uint64_t a4 = now;
       int64_t a1 = n_slots;
       void* args[] = {(void*)&a0, (void*)&a1, (void*)&a2, (void*)&a3, (void*)&a4, (void*)&S};
-      FC_CUDA(cudaLaunchCooperativeKernel((const void*)k_policy_fused, dim3(grid), dim3(SEG_T), args, smem, ctx->stream));
+      KTimer kk(ctx, "policy");
+      FC_CUDA(cudaLaunchCooperativeKernel(reg ? (const void*)k_policy_fused<true> : (const void*)k_policy_fused<false>,
+                                          dim3(grid), dim3(SEG_T), args, smem, ctx->stream));
       FC_LAUNCH_CHECK();
       count_launch(ctx, 1);
-      kt.stop();
+      kk.stop();
       FC_CUDA(cudaMemcpyAsync(fs_host, fs + rep_off, rep_bytes, cudaMemcpyDeviceToHost, ctx->stream));
       kcall.stop();
       sync(ctx);
