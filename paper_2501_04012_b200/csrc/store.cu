@@ -1680,14 +1680,82 @@ lc_status lc_snapshot_load(lc_ctx* ctx, const char* path, lc_store** store_out, 
   lc_store* s = st.get();
   s->next_seq = next_seq;
   const uint32_t n_prompts = r.u32();
-  for (uint32_t i = 0; i < n_prompts; ++i) {
-    const uint64_t record_pos = r.pos;
-    const uint32_t body_len = r.u32();
-    const uint8_t* body = r.bytes(body_len);
-    const uint32_t crc = r.u32();
-    if (crc32_of(body, body_len) != crc) raise_snap("checksum mismatch in prompt record", record_pos);
-    uint64_t used_e = 0;
-    lc_entry* view = import_entry(ctx, body, body_len, &used_e);
+  // (1) framing: record positions up to the first framing error (raised only
+  // after every record before it, as the reference's sequential loop would)
+  struct Rc {
+    uint64_t pos;
+    const uint8_t* body;
+    uint32_t len, crc;
+  };
+  std::vector<Rc> recs;
+  recs.reserve(n_prompts);
+  std::exception_ptr frame_err = nullptr;
+  try {
+    for (uint32_t i = 0; i < n_prompts; ++i) {
+      Rc c;
+      c.pos = r.pos;
+      c.len = r.u32();
+      c.body = r.bytes(c.len);
+      c.crc = r.u32();
+      recs.push_back(c);
+    }
+  } catch (...) {
+    frame_err = std::current_exception();
+  }
+  // (2) per record, in parallel: CRC32 and the entry import (parse + upload
+  // on a child stream per thread); errors kept per record
+  const size_t nr = recs.size();
+  std::vector<lc_entry*> imported(nr, nullptr);
+  std::vector<uint64_t> used_of(nr, 0);
+  std::vector<std::exception_ptr> rec_err(nr, nullptr);
+  std::vector<char> crc_bad(nr, 0);
+  struct Release {
+    std::vector<lc_entry*>& v;
+    ~Release() {
+      for (lc_entry* e : v)
+        if (e) lc_entry_release(e);
+    }
+  } release_left{imported};
+  {
+    std::atomic<size_t> next{0};
+    const int nt = (int)std::min<size_t>(nr, std::min(16u, std::max(1u, std::thread::hardware_concurrency())));
+    auto worker = [&](int t) {
+      lc_ctx* c = nullptr;
+      try {
+        c = aux_ctx(ctx, t);
+      } catch (...) {
+        c = ctx;
+      }
+      DeviceGuard g2(ctx->device);
+      for (size_t i; (i = next.fetch_add(1)) < nr;) {
+        if (crc32_of(recs[i].body, recs[i].len) != recs[i].crc) {
+          crc_bad[i] = 1;
+          continue;
+        }
+        try {
+          imported[i] = import_entry(c, recs[i].body, recs[i].len, &used_of[i]);
+          imported[i]->d->ctx = ctx;  // uploaded and synced on the child stream; owned by the caller's context
+        } catch (...) {
+          rec_err[i] = std::current_exception();
+        }
+      }
+    };
+    std::vector<std::thread> th;
+    for (int t = 1; t < nt; ++t) th.emplace_back(worker, t);
+    if (nt >= 1) worker(0);
+    for (auto& x : th) x.join();
+  }
+  // (3) in file order: the first error wins, then the live records and the
+  // store state exactly as the sequential loop (store.cpp:323-360)
+  for (size_t i = 0; i < nr; ++i) {
+    const uint64_t record_pos = recs[i].pos;
+    const uint8_t* body = recs[i].body;
+    const uint32_t body_len = recs[i].len;
+    if (crc_bad[i]) raise_snap("checksum mismatch in prompt record", record_pos);
+    if (rec_err[i]) std::rethrow_exception(rec_err[i]);
+    const uint64_t used_e = used_of[i];
+    lc_entry* view = imported[i];
+    imported[i] = nullptr;
     std::unique_ptr<lc_entry, lc_status (*)(lc_entry*)> vh(view, lc_entry_release);
     const EntryData& d = *view->d;
     BR br{body, body_len, used_e};
@@ -1733,6 +1801,7 @@ lc_status lc_snapshot_load(lc_ctx* ctx, const char* path, lc_store** store_out, 
     }
     s->write_prompt(it->second);
   }
+  if (frame_err) std::rethrow_exception(frame_err);
   if (r.pos != r.n) raise_snap("trailing bytes after last record", r.pos);
   *store_out = st.release();
   *index_out = ix.release();

@@ -145,14 +145,17 @@ def test_priority_functions(fc):
 
 
 @pytest.mark.parametrize("policy", [0, 1, 2, 3])
-@pytest.mark.parametrize("sort_path", ["0", "1", "2"])
+@pytest.mark.parametrize("sort_path", ["0", "1", "2", "3"])
 def test_eviction_burst_both_scoring_paths(fc, orc, synth, policy, sort_path):
     """600 evict_one at one `now` over ~1500 live steps: crosses the 256-entry
     scored head twice (re-scoring), LRBU sibling re-keys, and the radix-select
-    fast path as one cooperative kernel (FC_SCORE_SORT=0, default) or as 7
-    launches ("2": FC_SCORE_FUSED=0) vs the segmented-sort path (=1)."""
+    fast path as one cooperative kernel (FC_SCORE_SORT=0, default; keys in
+    registers, or "3": FC_SCORE_REG=0, keys through memory as for stores too
+    large for the registers) or as 7 launches ("2": FC_SCORE_FUSED=0) vs the
+    segmented-sort path (=1)."""
     os.environ["FC_SCORE_SORT"] = "1" if sort_path == "1" else "0"
     os.environ["FC_SCORE_FUSED"] = "0" if sort_path == "2" else "1"
+    os.environ["FC_SCORE_REG"] = "0" if sort_path == "3" else "1"
     try:
         ents = _tiny_entries(fc, synth, 300, policy)
         st = fc.CacheStore(1 << 40, fc.Policy(policy))
@@ -177,6 +180,7 @@ def test_eviction_burst_both_scoring_paths(fc, orc, synth, policy, sort_path):
     finally:
         del os.environ["FC_SCORE_SORT"]
         del os.environ["FC_SCORE_FUSED"]
+        del os.environ["FC_SCORE_REG"]
 
 
 def _gpu_store_worker(rank, world, port, policy, seed, out_dir):
