@@ -77,6 +77,9 @@ def codec_case(orc, rng):
         lat[:, :, F // 2] = lat[:, :, 0]
     if rng.random() < 0.2:
         lat[:, :, -1] = 0.0
+    if rng.random() < 0.2:  # frames outside the tensor-core Gram's range guard [2^-40, 2^56] / denormals
+        sc = float(rng.choice([1e-13, 1e-20, 1e17, 1e-41]))
+        lat[int(rng.integers(0, n)), int(rng.integers(0, S)), int(rng.integers(0, F))] *= np.float32(sc)
     masks = [synth.rect_masks(F, dims[0], dims[1], seed + i) for i in range(n)]
     om = np.stack([m[0] for m in masks])
     bm = np.stack([m[1] for m in masks])
