@@ -187,3 +187,54 @@ def test_capi_sharded_store_global_budget(tmp_path, policy, id_base, batch):
     if batch > 1:  # batched rounds: fewer collective rounds than evictions
         ev = r0["stats"]["local_evictions"] + r1["stats"]["local_evictions"]
         assert r0["stats"]["rounds"] <= ev
+
+
+def _nccl_worker(port, out_dir):
+    """world 1: the library's own NCCL communicator (ncclCommInitRank on
+    cuda:0, dlopen'ed libnccl) drives lc_sharded_query_topk / lookup_decide,
+    i.e. the collective code path the N-GPU bench uses."""
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    import paper_2501_04012_b200 as fc
+    from paper_2501_04012_b200 import sharded, synth
+    ctx = fc.Context(0)
+    sharded.attach_comm(ctx, transport="nccl")
+    nr, rk, be, _ = sharded.comm_info(ctx)
+    n, d, nq, k = 20000, 256, 300, 8
+    tabs = [synth.gaussian_embeddings(n, d, 90 + t) for t in range(3)]
+    ids = np.arange(n, dtype=np.uint64) * 5 + 1
+    q = [synth.perturbed_queries(tabs[t], nq, 95 + t)[0] for t in range(3)]
+    ix = fc.SimilarityIndex(ctx=ctx)
+    sh = sharded.CommShardedIndex(ix, d)
+    assert sh.insert_batch(ids, *tabs) == n
+    ix.set_lookup(2, 32)
+    got = sh.query_topk(fc.EmbeddingKind.Whole, q[0], k)
+    ref = ix.query_topk(fc.EmbeddingKind.Whole, q[0], k)
+    dec = sh.lookup_decide(q[0], q[1], q[2])
+    dref = fc.lookup_decide(ix, q[0], q[1], q[2])
+    with open(os.path.join(out_dir, "nccl.pkl"), "wb") as f:
+        pickle.dump({"comm": (nr, rk, be), "ids": (np.asarray(got[0]).view(np.uint64), np.asarray(ref[0]).view(np.uint64)),
+                     "sc": (np.asarray(got[1]), np.asarray(ref[1])), "cnt": (np.asarray(got[2]), np.asarray(ref[2])),
+                     "dec": ([(x.kind, x.step, x.object_id, x.background_id, x.score) for x in dec],
+                             [(x.kind, x.step, x.object_id, x.background_id, x.score) for x in dref])}, f)
+    dist.destroy_process_group()
+
+
+def test_nccl_communicator_single_rank(tmp_path):
+    import multiprocessing as mp
+    ctxm = mp.get_context("spawn")
+    p = ctxm.Process(target=_nccl_worker, args=(_free_port(), str(tmp_path)))
+    p.start()
+    p.join(600)
+    assert p.exitcode == 0
+    with open(tmp_path / "nccl.pkl", "rb") as f:
+        r = pickle.load(f)
+    assert r["comm"] == (1, 0, 1)  # one rank, backend NCCL
+    for key in ("ids", "sc", "cnt"):
+        a, b = r[key]
+        assert (np.asarray(a) == np.asarray(b)).all(), key
+    assert r["dec"][0] == r["dec"][1]
