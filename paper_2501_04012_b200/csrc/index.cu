@@ -1041,6 +1041,8 @@ void query_dev(lc_index* ix, int kind, const float* Qdev, int nq, int k, uint64_
   // batches that fill CTA pairs, else the bf16 shortlist with K' = kprime.
   const bool tier1_i8 = i8_ok;
   int64_t gathered = -1, cands = -1, prescored = -1;
+  PinnedBuf<unsigned long long> hpin(5);  // [0,3) candidate counters | [3,5) the 16 B of failure counters
+  bool hg_pending = false;
   if (tier1_i8) {
     const int kout = ix->i8_kout;
     DevBuf cs((size_t)nq * kout * sizeof(float), ctx->stream), cr((size_t)nq * kout * sizeof(uint32_t), ctx->stream);
@@ -1083,12 +1085,9 @@ void query_dev(lc_index* ix, int kind, const float* Qdev, int nq, int k, uint64_
     kt.stop();
     FC_LAUNCH_CHECK();
     count_launch(ctx);
-    unsigned long long hg[3] = {0, 0, 0};
-    FC_CUDA(cudaMemcpyAsync(hg, gb.p, sizeof hg, cudaMemcpyDeviceToHost, ctx->stream));
-    sync(ctx);
-    gathered = (int64_t)hg[0];
-    cands = (int64_t)hg[1];
-    prescored = (int64_t)hg[2];
+    // the candidate counters come back with the failure counters below (one sync)
+    FC_CUDA(cudaMemcpyAsync(hpin.data(), gb.p, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+    hg_pending = true;
   } else {
     DevBuf cs((size_t)nq * kp * sizeof(float), ctx->stream);
     DevBuf cr((size_t)nq * kp * sizeof(uint32_t), ctx->stream);
@@ -1118,8 +1117,14 @@ void query_dev(lc_index* ix, int kind, const float* Qdev, int nq, int k, uint64_
     count_launch(ctx);
   }
   int32_t hf[4] = {0, 0, 0, 0};
-  FC_CUDA(cudaMemcpyAsync(hf, fn.p, 16, cudaMemcpyDeviceToHost, ctx->stream));
+  FC_CUDA(cudaMemcpyAsync(hpin.data() + 3, fn.p, 16, cudaMemcpyDeviceToHost, ctx->stream));  // pinned: async
   sync(ctx);
+  memcpy(hf, hpin.data() + 3, 16);
+  if (hg_pending) {
+    gathered = (int64_t)hpin[0];
+    cands = (int64_t)hpin[1];
+    prescored = (int64_t)hpin[2];
+  }
   double err = 0.0;
   uint64_t eb = (uint64_t)(uint32_t)hf[2] | ((uint64_t)(uint32_t)hf[3] << 32);
   memcpy(&err, &eb, 8);
