@@ -1629,7 +1629,8 @@ void run_shortlist(lc_ctx* ctx, const ShortlistRun& R) {
     }
     // pilot over every 16th row tile (tables of >= 256 tiles): per-query max U
     // into gkey, the main pass's starting threshold
-    constexpr int PILOT_STRIDE = 16;
+    static const int PILOT_STRIDE =
+        getenv("FC_LOOKUP_I8_PILOT_STRIDE") ? std::max(1, atoi(getenv("FC_LOOKUP_I8_PILOT_STRIDE"))) : 16;
     static const bool no_pilot = getenv("FC_LOOKUP_I8_PILOT") && atoi(getenv("FC_LOOKUP_I8_PILOT")) == 0;
     if (!no_pilot && !R.tau_fix && total_tiles >= 256) {
       Params pp = prm;
