@@ -46,6 +46,39 @@ std::vector<float> to_host(const float* p, size_t n) {
   return h;
 }
 
+// Exact dots among the batch's own queries, per table: D[t][j][i] =
+// sum_d (double)q_j[d] * (double)q_i[d] in d order (vindex.cpp:67; the
+// product of two floats is exact in fp64, so fma == the reference's mul+add)
+// for i < j. Rows inserted during the batch are earlier requests' query rows,
+// so the per-request fix-up reads these instead of scoring on the host.
+// Block = 16 x 16 (j, i) pairs, the two 16-row query slices staged in smem
+// 64 dims at a time; blocks above the diagonal exit.
+constexpr int BD_T = 16, BD_K = 64;
+__global__ void __launch_bounds__(BD_T * BD_T) k_batch_dots(const float* __restrict__ q0, const float* __restrict__ q1,
+                                                          const float* __restrict__ q2, int n, int d,
+                                                          double* __restrict__ D) {
+  const int t = blockIdx.z;
+  const float* q = t == 0 ? q0 : t == 1 ? q1 : q2;
+  const int j0 = blockIdx.y * BD_T, i0 = blockIdx.x * BD_T;
+  if (i0 > j0 + BD_T - 1) return;  // every pair of the block has i > j
+  __shared__ float sj[BD_T][BD_K + 1], si[BD_T][BD_K + 1];
+  const int tj = threadIdx.x / BD_T, ti = threadIdx.x % BD_T;
+  const int j = j0 + tj, i = i0 + ti;
+  double acc = 0.0;
+  for (int k0 = 0; k0 < d; k0 += BD_K) {
+    const int kn = min(BD_K, d - k0);
+    for (int x = threadIdx.x; x < BD_T * BD_K; x += BD_T * BD_T) {
+      const int r = x / BD_K, c = x % BD_K;
+      sj[r][c] = (j0 + r < n && c < kn) ? q[(size_t)(j0 + r) * d + k0 + c] : 0.f;
+      si[r][c] = (i0 + r < n && c < kn) ? q[(size_t)(i0 + r) * d + k0 + c] : 0.f;
+    }
+    __syncthreads();
+    for (int c = 0; c < kn; ++c) acc = fma((double)sj[tj][c], (double)si[ti][c], acc);
+    __syncthreads();
+  }
+  if (j < n && i < j) D[((size_t)t * n + j) * n + i] = acc;
+}
+
 // FC_TRACE=1: accumulated host time per engine phase, printed per call
 struct PhaseClock {
   bool on = getenv("FC_TRACE") && atoi(getenv("FC_TRACE")) == 1;
@@ -216,6 +249,28 @@ lc_status lc_engine_process(lc_engine* e, const lc_request* req, int64_t n, cons
     bcnt[t].assign((size_t)n, 0);
     if (size0 > 0)
       ok(lc_index_query_topk(e->ix, t, qh[t].data(), n, KTOP, bid[t].data(), bsc[t].data(), bcnt[t].data()));
+  }
+  // exact dots among the batch's queries (the rows this batch may insert)
+  std::vector<double> bdots;
+  if (n >= 2 && n <= 1024) {
+    DevBuf dq(3 * (size_t)n * d * sizeof(float), e->ctx->stream), dD(3 * (size_t)n * n * sizeof(double), e->ctx->stream);
+    const float* qd[3];
+    for (int t = 0; t < 3; ++t) {
+      if (is_device_ptr(qs[t])) {
+        qd[t] = qs[t];
+      } else {
+        float* dst = dq.as<float>() + (size_t)t * n * d;
+        FC_CUDA(cudaMemcpyAsync(dst, qh[t].data(), (size_t)n * d * sizeof(float), cudaMemcpyHostToDevice, e->ctx->stream));
+        qd[t] = dst;
+      }
+    }
+    const unsigned nb = (unsigned)((n + BD_T - 1) / BD_T);
+    k_batch_dots<<<dim3(nb, nb, 3), BD_T * BD_T, 0, e->ctx->stream>>>(qd[0], qd[1], qd[2], (int)n, d, dD.as<double>());
+    FC_LAUNCH_CHECK();
+    count_launch(e->ctx);
+    bdots.resize(3 * (size_t)n * n);
+    FC_CUDA(cudaMemcpyAsync(bdots.data(), dD.p, dD.bytes, cudaMemcpyDeviceToHost, e->ctx->stream));
+    sync(e->ctx);
   }
   pc.lap(0);
   // index changes since the batch lookup
@@ -495,17 +550,32 @@ lc_status lc_engine_process(lc_engine* e, const lc_request* req, int64_t n, cons
         tsc[t] = s1;
         continue;
       }
-      // exact scores of the rows added since the lookup, four independent
-      // sequential chains at a time (each in vindex.cpp:67 element order)
+      // exact scores of the rows added since the lookup: earlier query rows
+      // of this batch come from the device dot table; anything else is
+      // scored here, four independent sequential chains at a time (each in
+      // vindex.cpp:67 element order)
       auto it = added.begin();
       while (it != added.end()) {
         const float* x[4];
         uint64_t id[4];
         int m = 0;
-        for (; m < 4 && it != added.end(); ++m, ++it) {
-          x[m] = it->second[t];
+        for (; m < 4 && it != added.end(); ++it) {
+          const float* row = it->second[t];
+          const ptrdiff_t off = row - qh[t].data();
+          if (!bdots.empty() && off >= 0 && off % d == 0 && off / d < j) {
+            const double s = bdots[((size_t)t * n + j) * n + off / d];
+            if (!have[t] || better(s, it->first, tsc[t], tid[t])) {
+              have[t] = true;
+              tid[t] = it->first;
+              tsc[t] = s;
+            }
+            continue;
+          }
+          x[m] = row;
           id[m] = it->first;
+          ++m;
         }
+        if (m == 0) continue;
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
         for (int i = 0; i < d; ++i) {
           const double qi = (double)q[i];
