@@ -943,12 +943,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
         if (lane == 0) mbar_arrive_remote(smem_u32(&acce[b]), 0);
         if (I8 && p.pilot) {  // fold the tile half's valid dots into the best-R U list
           const int pthr = i8_thr(__fsub_rd(ut[PILOT_R - 1], eps_t), sqt);
+          const bool full = lim_all >= EPI_HALF_COLS;  // warp-uniform: every tile but the last
 #pragma unroll
           for (int c0 = 0; c0 < EPI_HALF_COLS; c0 += 16) {
             int m = INT_MIN;
+            if (full) {  // unguarded 3-input max tree (ncu r02ca: the guarded chain kept the ALU pipe 72 % busy)
+              const int* vi = reinterpret_cast<const int*>(rv + c0);
+              int m0 = __vimax3_s32(vi[0], vi[1], vi[2]), m1 = __vimax3_s32(vi[3], vi[4], vi[5]);
+              int m2 = __vimax3_s32(vi[6], vi[7], vi[8]), m3 = __vimax3_s32(vi[9], vi[10], vi[11]);
+              int m4 = __vimax3_s32(vi[12], vi[13], vi[14]);
+              m0 = __vimax3_s32(m0, m1, m2);
+              m3 = __vimax3_s32(m3, m4, vi[15]);
+              m = max(m0, m3);
+            } else {
 #pragma unroll
-            for (int c = c0; c < c0 + 16; c += 2)
-              m = __vimax3_s32(m, c < lim_all ? (int)rv[c] : INT_MIN, c + 1 < lim_all ? (int)rv[c + 1] : INT_MIN);
+              for (int c = c0; c < c0 + 16; c += 2)
+                m = __vimax3_s32(m, c < lim_all ? (int)rv[c] : INT_MIN, c + 1 < lim_all ? (int)rv[c + 1] : INT_MIN);
+            }
             if (!__any_sync(0xffffffffu, m > pthr)) continue;
             uint32_t msk = 0;
 #pragma unroll
