@@ -1610,8 +1610,12 @@ void run_shortlist(lc_ctx* ctx, const ShortlistRun& R) {
     const char* e = getenv("FC_SHORTLIST_REFRESH");
     // int8: the pilot seeds the threshold, so the histogram refresh (~8k cycles of
     // dependent L2 round trips per warp) runs every 64 tiles (r02x: 16 -> 2.25 ms,
-    // 32 -> 2.14, 64 -> 2.09 per 4096 x 1M launch)
-    prm.refresh_mask = (e ? atoi(e) : (R.i8 ? 64 : 16)) - 1;
+    // 32 -> 2.14, 64 -> 2.09 per 4096 x 1M launch); tables large enough for the
+    // pilot (>= 256 tiles) refresh every 512 (r02cd: 64 -> 2.156 ms, 256 -> 2.12,
+    // 512 -> 2.11 once the pilot's epilogue was fixed)
+    const int64_t tiles = (R.n_rows + PN - 1) / PN;
+    const bool pilot = tiles >= 256 && !R.tau_fix && !(getenv("FC_LOOKUP_I8_PILOT") && atoi(getenv("FC_LOOKUP_I8_PILOT")) == 0);
+    prm.refresh_mask = (e ? atoi(e) : (R.i8 ? (pilot ? 512 : 64) : 16)) - 1;
   }
   prm.stats = st.as<uint32_t>();
   prm.gkey = gk.as<uint32_t>();
