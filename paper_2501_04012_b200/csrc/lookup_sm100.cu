@@ -1494,7 +1494,8 @@ static void launch_pair(lc_ctx* ctx, const CUtensorMap& tmB, const CUtensorMap& 
   const size_t fixed = (size_t)KS * ABOX;
   // candidate buffer: kp + 32 slots minimum (compactions stay rare once the
   // shared threshold is warm); the rest of smem goes to the table ring
-  const int64_t min_cap = prm.kp + 32;
+  int64_t min_cap = prm.kp + 32;
+  if (const char* e = getenv("FC_SHORTLIST_MINCAP")) min_cap = std::max<int64_t>(prm.kp + 8, atoi(e));
   {
     const char* e = getenv("FC_SHORTLIST_BPS");
     int want = e ? atoi(e) : 2;
