@@ -942,7 +942,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive_remote(smem_u32(&acce[b]), 0);
         if (I8 && p.pilot) {  // fold the tile half's valid dots into the best-R U list
-          const int pthr = i8_thr(__fsub_rd(ut[PILOT_R - 1], eps_t), sqt);
+          int pthr = i8_thr(__fsub_rd(ut[PILOT_R - 1], eps_t), sqt);  // refreshed after insertions
           const bool full = lim_all >= EPI_HALF_COLS;  // warp-uniform: every tile but the last
 #pragma unroll
           for (int c0 = 0; c0 < EPI_HALF_COLS; c0 += 16) {
@@ -962,18 +962,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
             }
             if (!__any_sync(0xffffffffu, m > pthr)) continue;
             uint32_t msk = 0;
+            if (full) {
 #pragma unroll
-            for (int jj = 0; jj < 16; ++jj) msk |= ((c0 + jj < lim_all) & ((int)rv[c0 + jj] > pthr)) ? (1u << jj) : 0u;
-            while (msk) {  // only the lane's qualifying dots (usually 0-1 per chunk)
-              const int jj = __ffs(msk) - 1;
-              msk &= msk - 1;
-              float u = __fadd_ru(i8_score_up((int)sel16(rv + c0, jj), sqt), eps_t);
+              for (int jj = 0; jj < 16; ++jj) msk |= ((int)rv[c0 + jj] > pthr) ? (1u << jj) : 0u;
+            } else {
 #pragma unroll
-              for (int i = 0; i < PILOT_R; ++i) {  // insertion into the descending list
-                const float hi = fmaxf(ut[i], u);
-                u = fminf(ut[i], u);
-                ut[i] = hi;
-              }
+              for (int jj = 0; jj < 16; ++jj) msk |= ((c0 + jj < lim_all) & ((int)rv[c0 + jj] > pthr)) ? (1u << jj) : 0u;
+            }
+            if (msk) {
+              do {  // only the lane's qualifying dots (usually 0-1 per chunk)
+                const int jj = __ffs(msk) - 1;
+                msk &= msk - 1;
+                float u = __fadd_ru(i8_score_up((int)sel16(rv + c0, jj), sqt), eps_t);
+#pragma unroll
+                for (int i = 0; i < PILOT_R; ++i) {  // insertion into the descending list
+                  const float hi = fmaxf(ut[i], u);
+                  u = fminf(ut[i], u);
+                  ut[i] = hi;
+                }
+              } while (msk);
+              pthr = i8_thr(__fsub_rd(ut[PILOT_R - 1], eps_t), sqt);  // the tighter bound for the next chunks
             }
           }
           continue;
