@@ -552,8 +552,13 @@ __device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) 
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
-__global__ void __launch_bounds__(RI_WARPS * 32)
-    k_rescore_i8(const float* __restrict__ Q, int nq, int dim, const float* __restrict__ rows,
+// CPL: 16-byte bf16 chunks per lane of a pre-scored row (3 for dim <= 768, 4
+// for <= 1024): the CPL = 3 build drops the spills of the 128-register cap
+// (r02cl: 0.295 -> 0.282 ms per 4096 x 1M batch; 5 blocks/SM at 96 registers
+// spilled and was slower)
+template <int CPL, int MINB>
+__global__ void __launch_bounds__(RI_WARPS * 32, MINB)
+    k_rescore_i8_t(const float* __restrict__ Q, int nq, int dim, const float* __restrict__ rows,
                  const __nv_bfloat16* __restrict__ rowsb, const uint64_t* __restrict__ ids,
                  const float* __restrict__ cand_s, const uint32_t* __restrict__ cand_r, const int32_t* __restrict__ cand_n,
                  const float* __restrict__ cand_m, int kout, int64_t n_rows, int k, double dres, double eps_floor,
@@ -649,7 +654,6 @@ __global__ void __launch_bounds__(RI_WARPS * 32)
   // their way into L2
   const uint4* sb4 = reinterpret_cast<const uint4*>(sb);
   const int n16 = dim / 8;  // 16-byte chunks per bf16 row
-  constexpr int CPL = 4;    // chunks per lane (dim <= 1024)
   constexpr int PW = 16;    // rows prefetched ahead
   uint4 qa[CPL];
 #pragma unroll
@@ -812,6 +816,9 @@ __global__ void __launch_bounds__(RI_WARPS * 32)
   }
 }
 
+// the launch sites pick the build by dimension
+#define RESCORE_I8(dim_) ((dim_) <= 768 ? k_rescore_i8_t<3, 4> : k_rescore_i8_t<4, 4>)
+
 }  // namespace fc
 
 // ---------------------------------------------------------------------------
@@ -831,7 +838,9 @@ bool i8_wanted(int dim) {
 void rescore_i8_attr(lc_ctx* ctx) {
   static std::atomic<uint64_t> attr_set{0};
   if (!(attr_set.load() >> (ctx->device & 63) & 1)) {
-    FC_CUDA(cudaFuncSetAttribute(k_rescore_i8, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    FC_CUDA(cudaFuncSetAttribute(k_rescore_i8_t<3, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(RI_WARPS * (768 * 10 + KI_MAX * 12))));
+    FC_CUDA(cudaFuncSetAttribute(k_rescore_i8_t<4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)(RI_WARPS * (1024 * 10 + KI_MAX * 12))));
     attr_set.fetch_or(1ull << (ctx->device & 63));
   }
@@ -1069,7 +1078,7 @@ void query_dev(lc_index* ix, int kind, const float* Qdev, int nq, int k, uint64_
     DevBuf tlo(xchg ? (size_t)nq * sizeof(float) : 16, ctx->stream);
     if (xchg) {
       // sharded: each rank's lower bound of its k-th score, max over the ranks
-      k_rescore_i8<<<(unsigned)((nq + RI_WARPS - 1) / RI_WARPS), RI_WARPS * 32, ri_smem, ctx->stream>>>(
+      RESCORE_I8(dim)<<<(unsigned)((nq + RI_WARPS - 1) / RI_WARPS), RI_WARPS * 32, ri_smem, ctx->stream>>>(
           Qdev, nq, dim, ix->rows[kind], ix->rowsb[kind], ix->ids_dev, cs.as<float>(), cr.as<uint32_t>(),
           cn.as<int32_t>(), cm.as<float>(), kout, ix->n, k, ix->dres[kind], ix->eps_floor, oid, osc, ocnt,
           fl.as<int32_t>(), fail_n, err_bits, bad_q, gb.as<unsigned long long>(), tlo.as<float>(), nullptr);
@@ -1078,7 +1087,7 @@ void query_dev(lc_index* ix, int kind, const float* Qdev, int nq, int k, uint64_
       (*xchg)(tlo.as<float>(), nq);
       xonce.done = true;
     }
-    k_rescore_i8<<<(unsigned)((nq + RI_WARPS - 1) / RI_WARPS), RI_WARPS * 32, ri_smem, ctx->stream>>>(
+    RESCORE_I8(dim)<<<(unsigned)((nq + RI_WARPS - 1) / RI_WARPS), RI_WARPS * 32, ri_smem, ctx->stream>>>(
         Qdev, nq, dim, ix->rows[kind], ix->rowsb[kind], ix->ids_dev, cs.as<float>(), cr.as<uint32_t>(), cn.as<int32_t>(),
         cm.as<float>(), kout, ix->n, k, ix->dres[kind], ix->eps_floor, oid, osc, ocnt, fl.as<int32_t>(), fail_n,
         err_bits, bad_q, gb.as<unsigned long long>(), nullptr, xchg ? tlo.as<float>() : nullptr);
@@ -1277,7 +1286,7 @@ void query_dev(lc_index* ix, int kind, const float* Qdev, int nq, int k, uint64_
       KTimer kt3(ctx, "rescore_threshold");
       rescore_i8_attr(ctx);
       const size_t ri_smem = (size_t)RI_WARPS * ((size_t)dim * 10 + KI_MAX * 12);
-      k_rescore_i8<<<(unsigned)((n_left + RI_WARPS - 1) / RI_WARPS), RI_WARPS * 32, ri_smem, ctx->stream>>>(
+      RESCORE_I8(dim)<<<(unsigned)((n_left + RI_WARPS - 1) / RI_WARPS), RI_WARPS * 32, ri_smem, ctx->stream>>>(
           q2.as<float>(), n_left, dim, ix->rows[kind], ix->rowsb[kind], ix->ids_dev, cs2.as<float>(), cr2.as<uint32_t>(),
           cn2.as<int32_t>(), cm2.as<float>(), kout, ix->n, k, ix->dres[kind], ix->eps_floor, id2.as<uint64_t>(),
           sc2.as<double>(), ct2.as<int32_t>(), fl2.as<int32_t>(), fn2.as<int32_t>(),
