@@ -1287,13 +1287,50 @@ __global__ void __launch_bounds__(QM_W * 32) k_i8_merge(const uint64_t* __restri
   __syncwarp();
   uint64_t T = 0;  // keep everything
   if (n > kout) {
-    uint64_t lo = 0, hi = ~0ull;
-    while (lo < hi) {  // max T with count(key >= T) >= kout
+    // T = the kout-th largest key (keys are unique): bisection over the top
+    // 16 bits (the score bucket) on all n keys, then over the full key on the
+    // few keys of that bucket only, copied behind the list when they fit
+    uint32_t t16 = 0;
+#pragma unroll 1
+    for (int bit = 15; bit >= 0; --bit) {
+      const uint32_t c16 = t16 | (1u << bit);
+      int c = 0;
+      for (int i = lane; i < n; i += 32) c += (uint32_t)(key[i] >> 48) >= c16;
+      if ((int)__reduce_add_sync(0xffffffffu, (unsigned)c) >= kout) t16 = c16;
+    }
+    int above = 0;  // keys in higher buckets (< kout by the choice of t16)
+    for (int i = lane; i < n; i += 32) above += (uint32_t)(key[i] >> 48) > t16;
+    above = (int)__reduce_add_sync(0xffffffffu, (unsigned)above);
+    const int need = kout - above;  // >= 1 keys wanted from the t16 bucket
+    const uint64_t* tk = key;
+    int m = n;
+    {  // compact the bucket behind the list (n + m <= QCAP), else scan in place
+      int cnt = 0;
+      for (int i = lane; i < n; i += 32) cnt += (uint32_t)(key[i] >> 48) == t16;
+      cnt = (int)__reduce_add_sync(0xffffffffu, (unsigned)cnt);
+      if (n + cnt <= QCAP) {
+        int o = n;
+        for (int i0 = 0; i0 < n; i0 += 32) {
+          const int i = i0 + lane;
+          const bool in = i < n && (uint32_t)(key[i] >> 48) == t16;
+          const unsigned bal = __ballot_sync(0xffffffffu, in);
+          if (in) key[o + __popc(bal & ((1u << lane) - 1))] = key[i];
+          o += __popc(bal);
+        }
+        __syncwarp();
+        tk = key + n;
+        m = cnt;
+      }
+    }
+    // (scanning in place, the higher buckets count too: target kout)
+    const int target = tk == key ? kout : need;
+    uint64_t lo = (uint64_t)t16 << 48, hi = lo | 0xFFFFFFFFFFFFull;
+    while (lo < hi) {  // max T in the bucket with count(key >= T) >= target
       const uint64_t mid = lo + ((hi - lo) >> 1) + 1;
       int c = 0;
-      for (int i = lane; i < n; i += 32) c += key[i] >= mid;
+      for (int i = lane; i < m; i += 32) c += tk[i] >= mid;
       c = __reduce_add_sync(0xffffffffu, c);
-      if (c >= kout) lo = mid; else hi = mid - 1;
+      if (c >= target) lo = mid; else hi = mid - 1;
     }
     T = lo;
     drop = fmaxf(drop, hkey_float((uint32_t)(T >> 48)));  // cut entries have stored U <= that of T
