@@ -1002,7 +1002,9 @@ __global__ void __launch_bounds__(DEC_T) k_decompress_groups(const DecItem* __re
   const DecJob jb = jobs[blockIdx.x];
   const DecItem it = items[jb.item];
   const Recipe r = it.rec[jb.key];
-  const int64_t n4 = E >> 2;
+  // blockIdx.y: slice of the frame (few jobs on long frames fill the GPU)
+  const int64_t n4all = E >> 2;
+  const int64_t v0 = n4all * blockIdx.y / gridDim.y, n4 = n4all * (blockIdx.y + 1) / gridDim.y;
   const float4* a4 = reinterpret_cast<const float4*>(it.base + r.a);
   const float4* b4 = reinterpret_cast<const float4*>(it.base + r.b);
   const double al = r.alpha;
@@ -1016,7 +1018,7 @@ __global__ void __launch_bounds__(DEC_T) k_decompress_groups(const DecItem* __re
   }
   __syncthreads();
   const int nf = s_nf;
-  for (int64_t i0 = threadIdx.x; i0 < n4; i0 += (int64_t)DEC_T * DEC_U) {
+  for (int64_t i0 = v0 + threadIdx.x; i0 < n4; i0 += (int64_t)DEC_T * DEC_U) {
     float4 va[DEC_U], vb[DEC_U];
 #pragma unroll
     for (int u = 0; u < DEC_U; ++u) {
@@ -1788,9 +1790,14 @@ void launch_decompress(lc_ctx* ctx, const std::vector<const EntryData*>& ents, c
   FC_CUDA(cudaMemcpyAsync(dv.p, stage.data(), stage.size(), cudaMemcpyHostToDevice, ctx->stream));
   const DecItem* di = dv.as<DecItem>();
   KTimer kt(ctx, "decompress");
-  if (groups)
-    k_decompress_groups<<<(unsigned)nj, DEC_T, 0, ctx->stream>>>(
+  if (groups) {
+    // >= ~8 blocks per SM: split each job's frame when there are few jobs
+    const int64_t want = 8LL * ctx->sm_count;
+    const unsigned ys = (unsigned)std::max<int64_t>(
+        1, std::min<int64_t>((want + (int64_t)nj - 1) / (int64_t)nj, std::max<int64_t>(1, (E >> 2) / (DEC_T * DEC_U))));
+    k_decompress_groups<<<dim3((unsigned)nj, ys), DEC_T, 0, ctx->stream>>>(
         di, reinterpret_cast<const DecJob*>(dv.as<uint8_t>() + items_b), F, E);
+  }
   else
     k_decompress<<<(unsigned)(ents.size() * F), DEC_T, 0, ctx->stream>>>(di, F, E);
   kt.stop();
