@@ -236,9 +236,9 @@ def cpu_reference_lookup(table_np, queries_np, nthreads, n_q):
     build_s = time.perf_counter() - t0
     q = np.ascontiguousarray(queries_np[:n_q])
     t0 = time.perf_counter()
-    ix.query_top1(0, q, nthreads=nthreads)
+    rid, rsc, _ = ix.query_top1(0, q, nthreads=nthreads)
     dt = time.perf_counter() - t0
-    return kind, n_q / dt, build_s, dt
+    return kind, n_q / dt, build_s, dt, (rid, rsc)
 
 
 def _safe(fn):
@@ -568,10 +568,19 @@ def main():
             tab_np = full.cpu().numpy()
             q_np = qs[0][:n_q].cpu().numpy()
             del full
-            kind, v, build_s, dt = cpu_reference_lookup(tab_np, q_np, nthreads, n_q)
+            kind, v, build_s, dt, (rid, rsc) = cpu_reference_lookup(tab_np, q_np, nthreads, n_q)
             cpu = {"value": v, "unit": "lookups/s", "cores": nthreads, "kind": kind,
                    "sample": f"{n_q} queries x query_top1 over {args.rows} rows (whole table), {nthreads} "
                              f"concurrent readers; index build {build_s:.1f}s excluded; {dt:.1f}s timed"}
+            # the timed path's answers for the same queries (batch qs[0], re-run
+            # untimed through the int8 tier) against the reference's query_top1
+            step(qs[0])
+            torch.cuda.synchronize()
+            gid = o_ids[:n_q, 0].cpu().numpy().view(np.uint64)
+            gsc = o_sc[:n_q, 0].cpu().numpy()
+            same = (gid == rid) & (gsc.view(np.uint64) == rsc.view(np.uint64))
+            cpu["parity"] = {"queries": int(n_q), "top1_identical": int(same.sum()),
+                             "vs": f"{kind} query_top1 (ids and fp64 scores, bitwise)"}
         except Exception as ex:  # the baseline is reported, never the target
             cpu = {"value": None, "unit": "lookups/s", "cores": 0, "kind": "unavailable", "sample": str(ex)[:200]}
 
