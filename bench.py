@@ -257,12 +257,24 @@ def cpu_reference_codec(lat_np, om_np, bm_np, nthreads):
     chk = Checker("ref" if kind == "reference" else "orc")
     n = lat_np.shape[0]
     t0 = time.perf_counter()
-    sizes = chk.compress_batch_sizes(lat_np, [5, 10, 15, 20, 25], om_np, bm_np, (40, 64, 4), list(range(1, n + 1)),
-                                     nthreads=nthreads)
+    hashes = None
+    if kind == "reference":  # sizes + a weighted byte sum of each entry's wire bytes (checked below)
+        sizes, hashes = chk.compress_batch_hash(lat_np, [5, 10, 15, 20, 25], om_np, bm_np, (40, 64, 4),
+                                                list(range(1, n + 1)), nthreads=nthreads)
+    else:
+        sizes = chk.compress_batch_sizes(lat_np, [5, 10, 15, 20, 25], om_np, bm_np, (40, 64, 4),
+                                         list(range(1, n + 1)), nthreads=nthreads)
     dt = time.perf_counter() - t0
     byt = lat_np.nbytes + om_np.nbytes + bm_np.nbytes + int(sizes.sum())
     return {"value": byt / dt / 1e9, "unit": "GB/s (compress)", "cores": nthreads, "kind": kind,
-            "sample": f"{n} config[2] prompts (5 x 64 x 40x64x4), {dt:.1f}s"}
+            "sample": f"{n} config[2] prompts (5 x 64 x 40x64x4), {dt:.1f}s"}, sizes, hashes
+
+
+def wire_sum(b):
+    """The weighted byte sum the reference's compress_batch_hash reports (oracle/ref_shim.cpp)."""
+    b = np.frombuffer(b, np.uint8).astype(np.uint64)
+    w = (np.arange(b.size, dtype=np.uint64) * np.uint64(0x9E3779B1) + np.uint64(1)) & np.uint64(0xFFFFFFFF)
+    return int((b * w).sum(dtype=np.uint64))
 
 
 def cpu_reference_evict(n_prompts=100_000, n_ev=16):
@@ -719,8 +731,13 @@ def bench_codec(torch, fc, ctx, args, dev, peaks):
     if not args.no_cpu:
         try:
             m = min(n, 32)
-            cpu = cpu_reference_codec(lat[:m].cpu().numpy(), om[:m].cpu().numpy(), bm[:m].cpu().numpy(),
-                                      os.cpu_count() or 1)
+            cpu, rsz, rh = cpu_reference_codec(lat[:m].cpu().numpy(), om[:m].cpu().numpy(), bm[:m].cpu().numpy(),
+                                               os.cpu_count() or 1)
+            # the timed compress's entries for the same prompts against the reference's
+            same = [int(sizes[i]) == int(rsz[i]) and (rh is None or wire_sum(ents[i].serialize()) == int(rh[i]))
+                    for i in range(m)]
+            cpu["parity"] = {"prompts": m, "entries_identical": int(sum(same)),
+                             "vs": f"{cpu['kind']} compress (sizes" + (" + wire-byte sums)" if rh is not None else ")")}
         except Exception as ex:  # reported, never the target
             cpu = {"value": None, "kind": "unavailable", "sample": str(ex)[:200]}
     res = {
