@@ -1595,11 +1595,11 @@ void run_shortlist(lc_ctx* ctx, const ShortlistRun& R) {
   const int64_t workers = R.pair ? ctx->sm_count / 2 : ctx->sm_count;  // persistent CTAs / CTA pairs
   // work units over `tiles` row tiles: (splits, tiles per split)
   auto split_rows = [&](int64_t tiles, int64_t& splits, int64_t& tiles_per_split) {
-    // ~16 units per persistent worker: shorter row ranges keep the query tiles
-    // that share a range closer together in time, so the table is re-read from
-    // L2 rather than HBM (ncu, 1M x 768 x 4096: 37 splits 3.63 GB DRAM per launch,
-    // 74 splits 2.74 GB and 2.5 % faster; 148 splits cost more in the merge)
-    static const int upw = getenv("FC_SHORTLIST_UPW") ? std::max(1, atoi(getenv("FC_SHORTLIST_UPW"))) : 16;
+    // ~8 units per persistent worker (round 1, bf16 tier: 16 -- 74 splits moved
+    // 2.74 GB of DRAM per 1M x 768 x 4096 launch against 3.63 GB with 37; the
+    // int8 tier with its pilot-seeded thresholds prefers longer units, r02cv:
+    // 1M 2.70 -> 2.68 ms, 250k 1.27 -> 1.15 ms, 125k 0.87 -> 0.84 ms per step)
+    static const int upw = getenv("FC_SHORTLIST_UPW") ? std::max(1, atoi(getenv("FC_SHORTLIST_UPW"))) : 8;
     splits = std::max<int64_t>(1, (workers * upw + R.n_qtiles - 1) / R.n_qtiles);
     splits = std::min<int64_t>(splits, std::max<int64_t>(1, tiles / 16));
     // keep one query's partial lists within the merge's shared memory (few queries)
