@@ -1545,6 +1545,10 @@ void assemble(lc_ctx* ctx, const float* lat, const uint8_t* om, const uint8_t* b
         nwhy[std::min<int>(cres[c].why, 4)]++;
       }
       for (int64_t e = 0; e < n; ++e) nprompt += need[e];
+      int nexact = 0, nall = 0;  // (item, step) pairs whose fp32 differences are exact (k = f + d)
+      for (size_t c = 0; c < items.size(); ++c)
+        for (int si = 0; si < S; ++si) nexact += res[c].exact[si], ++nall;
+      fprintf(stderr, "[compress] K7 exact-difference steps: %d/%d\n", nexact, nall);
       fprintf(stderr, "[compress] K7 cert: %d/%zu items certified (why: ovf %d nr %d), %d/%lld prompts exact\n",
               ncert, items.size(), nwhy[3], nwhy[4], nprompt, (long long)n);
     }
