@@ -1000,6 +1000,12 @@ struct ExchangeOnce {
   }
 };
 
+// Sharded int8 lookups exchange the pilot's per-query keys once per batch;
+// whether a batch does depends only on rank-uniform inputs (table config,
+// batch size, k), so every rank joins the same collectives in the same order
+// (pilot keys, then the bound exchange), whatever its shard holds.
+bool pilot_exchange_expected(const lc_index* ix, int nq, int k) { return ix->i8 && k <= 32 && nq > 128; }
+
 void query_dev(lc_index* ix, int kind, const float* Qdev, int nq, int k, uint64_t* oid, double* osc, int32_t* ocnt,
                const BoundExchange* xchg = nullptr) {
   lc_ctx* ctx = ix->ctx;
@@ -1027,6 +1033,7 @@ void query_dev(lc_index* ix, int kind, const float* Qdev, int nq, int k, uint64_
       sync(ctx);
       if (hb) raise(LC_ERR_INVALID_ARGUMENT, "Embedding: non-finite element");
     }
+    if (xchg && pilot_exchange_expected(ix, nq, k)) dummy_pilot_exchange(ctx, *xchg, nq);  // small shard: no pilot here
     exact_scan(ix, kind, Qdev, nullptr, nq, k, oid, osc, ocnt);
     std::lock_guard<std::mutex> sl(ix->stats_mu);
     ix->stats.exact_scans += nq;
@@ -1071,7 +1078,7 @@ void query_dev(lc_index* ix, int kind, const float* Qdev, int nq, int k, uint64_
       }
     }
     i8_shortlist(ctx, ix->iplan[kind], Qdev, nq, k, ix->i8_kunit, kout, cs.as<float>(), cr.as<uint32_t>(),
-                 cn.as<int32_t>(), cm.as<float>());
+                 cn.as<int32_t>(), cm.as<float>(), nullptr, xchg);
     const size_t ri_smem = (size_t)RI_WARPS * ((size_t)dim * 10 + KI_MAX * 12);
     rescore_i8_attr(ctx);
     KTimer kt(ctx, "rescore");
@@ -1336,7 +1343,8 @@ void index_topk_dev(lc_index* ix, int kind, const float* Qdev, int nq, int k, ui
   lc_ctx* ctx = ix->ctx;
   if (nq <= 0) return;
   if (ix->n == 0) {
-    ExchangeOnce xonce{xchg, ctx, nq};  // an empty shard still takes part in the collective
+    ExchangeOnce xonce{xchg, ctx, nq};  // an empty shard still takes part in the collectives
+    if (xchg && pilot_exchange_expected(ix, nq, k)) dummy_pilot_exchange(ctx, *xchg, nq);
     FC_CUDA(cudaMemsetAsync(oid, 0, (size_t)nq * k * sizeof(uint64_t), ctx->stream));
     FC_CUDA(cudaMemsetAsync(osc, 0, (size_t)nq * k * sizeof(double), ctx->stream));
     FC_CUDA(cudaMemsetAsync(ocnt, 0, (size_t)nq * sizeof(int32_t), ctx->stream));

@@ -73,7 +73,12 @@ void i8_quantize_tiles(lc_ctx* ctx, const float* rows, int64_t n_rows, int dim, 
 // the pilot/histogram heuristic -- every row with U > tau_fix[q] is kept
 // (up to the query buffer), so cand_m[q] = tau_fix[q] unless it overflowed.
 void i8_shortlist(lc_ctx* ctx, const I8Plan& p, const float* Qdev, int nq, int k, int kp_unit, int kout, float* cand_s,
-                  uint32_t* cand_r, int32_t* cand_n, float* cand_m, const float* tau_fix = nullptr);
+                  uint32_t* cand_r, int32_t* cand_n, float* cand_m, const float* tau_fix = nullptr,
+                  const std::function<void(float*, int)>* pilot_xchg = nullptr);
+// Sharded int8 lookup: the pilot's per-query threshold key, exchanged across
+// ranks (max) between the pilot and the main pass; a rank that runs no pilot
+// (empty or small shard) takes part with -inf (dummy_pilot_exchange).
+void dummy_pilot_exchange(lc_ctx* ctx, const std::function<void(float*, int)>& x, int nq);
 
 // Sharded lookup: all-gathers per-query float bounds (device, n of them) and
 // replaces each by its max over the ranks, on the context's stream.

@@ -1582,12 +1582,27 @@ struct ShortlistRun {
   const float* qscale = nullptr;
   const float2* qerr = nullptr;
   const float* tau_fix = nullptr;
+  const std::function<void(float*, int)>* pilot_xchg = nullptr;
   int k = 0;
   float* cand_s = nullptr;
   uint32_t* cand_r = nullptr;
   int32_t* cand_n = nullptr;
   float* cand_m = nullptr;
 };
+
+__global__ void k_gkey_to_f32(const uint32_t* __restrict__ gk, int n, float* __restrict__ f) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) f[i] = gk[i] ? sm100::key_float(gk[i]) : -INFINITY;
+}
+__global__ void k_f32_to_gkey(const float* __restrict__ f, int n, uint32_t* __restrict__ gk) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) gk[i] = f[i] > -INFINITY ? sm100::okey(f[i]) : 0u;
+}
+
+__global__ void k_fill_ninf(float* __restrict__ f, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) f[i] = -INFINITY;
+}
 
 void run_shortlist(lc_ctx* ctx, const ShortlistRun& R) {
   using namespace sm100;
@@ -1715,6 +1730,17 @@ void run_shortlist(lc_ctx* ctx, const ShortlistRun& R) {
       FC_LAUNCH_CHECK();
       count_launch(ctx, 2);
     }
+    if (R.pilot_xchg) {
+      // sharded: every rank filters with the max over the ranks of the
+      // pilots' per-query keys (a G x larger sample; a rank without a pilot
+      // contributes -inf and still receives the others')
+      DevBuf pf((size_t)std::max(nq, 1) * sizeof(float), ctx->stream);
+      k_gkey_to_f32<<<grid_for(std::max(nq, 1), 256), 256, 0, ctx->stream>>>(gk.as<uint32_t>(), nq, pf.as<float>());
+      (*R.pilot_xchg)(pf.as<float>(), nq);
+      k_f32_to_gkey<<<grid_for(std::max(nq, 1), 256), 256, 0, ctx->stream>>>(pf.as<float>(), nq, gk.as<uint32_t>());
+      FC_LAUNCH_CHECK();
+      count_launch(ctx, 2);
+    }
     launch_pair<true>(ctx, R.iplan->tmap, unused, prm);
   } else if (R.pair) {
     alignas(64) CUtensorMap tmQ;
@@ -1778,6 +1804,14 @@ void run_shortlist(lc_ctx* ctx, const ShortlistRun& R) {
   count_launch(ctx, 3);
 }
 }  // namespace
+
+void dummy_pilot_exchange(lc_ctx* ctx, const std::function<void(float*, int)>& x, int nq) {
+  DevBuf pf((size_t)std::max(nq, 1) * sizeof(float), ctx->stream);
+  k_fill_ninf<<<grid_for(std::max(nq, 1), 256), 256, 0, ctx->stream>>>(pf.as<float>(), nq);
+  FC_LAUNCH_CHECK();
+  count_launch(ctx);
+  x(pf.as<float>(), nq);
+}
 
 void approx_shortlist(lc_ctx* ctx, const ApproxPlan& plan, const float* Qdev, int nq, int kp, float* cand_s,
                       uint32_t* cand_r, int32_t* cand_n) {
@@ -1943,7 +1977,8 @@ void i8_plan(I8Plan& p, const int8_t* rows, const float* tscale, const float* tr
 }
 
 void i8_shortlist(lc_ctx* ctx, const I8Plan& plan, const float* Qdev, int nq, int k, int kp_unit, int kout, float* cand_s,
-                  uint32_t* cand_r, int32_t* cand_n, float* cand_m, const float* tau_fix) {
+                  uint32_t* cand_r, int32_t* cand_n, float* cand_m, const float* tau_fix,
+                  const std::function<void(float*, int)>* pilot_xchg) {
   using namespace sm100;
   FC_REQUIRE(plan.dim % 128 == 0 && plan.dim <= 1024, "int8 lookup tier: dim must be a multiple of 128, <= 1024");
   ShortlistRun R;
@@ -1970,6 +2005,7 @@ void i8_shortlist(lc_ctx* ctx, const I8Plan& plan, const float* Qdev, int nq, in
   R.qerr = qe.as<float2>();
   R.k = k;
   R.tau_fix = tau_fix;
+  R.pilot_xchg = tau_fix ? nullptr : pilot_xchg;
   R.cand_s = cand_s;
   R.cand_r = cand_r;
   R.cand_n = cand_n;

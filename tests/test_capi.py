@@ -27,7 +27,8 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_library_loads_and_reports_version():
-    lib = C.CDLL(LIB)
+    # RTLD_NOW: every undefined symbol must resolve at load time, not at first call on the GPU box
+    lib = C.CDLL(LIB, mode=os.RTLD_NOW)
     lib.lc_version.restype = C.c_char_p
     assert b"sm_100a" in lib.lc_version()
 

@@ -61,7 +61,8 @@ def _lookup_worker(rank, world, port, out_dir, n, d, nq, mode, skew):
     gi, gs, gc = sh.query_topk(0, q[0], 8)
     dec = sh.lookup_decide(q[0], q[1], q[2])
     info = sharded.comm_info(ctx)
-    res = {"ids": gi, "sc": gs, "cnt": gc, "dec": [(x.kind, x.step, x.whole_id, x.object_id, x.background_id,
+    st = ix.stats()
+    res = {"fallback": st.fallback, "i8_batches": st.i8_batches, "ids": gi, "sc": gs, "cnt": gc, "dec": [(x.kind, x.step, x.whole_id, x.object_id, x.background_id,
                                                      x.score) for x in dec], "info": info}
     if rank == 0:
         oi, os_, oc = orc.topk_flat(tabs[0], ids, q[0], 8)
@@ -84,6 +85,10 @@ def _lookup_worker(rank, world, port, out_dir, n, d, nq, mode, skew):
     (30000, 768, 300, 2, False),  # int8 tier, two-phase: shared lower bound of the global k-th score
     (30000, 768, 300, 0, True),   # one shard scans exactly, the other runs two-phase: the bound
                                   # exchange is still one collective per rank
+    (72000, 768, 160, 2, False),  # shards of >= 256 row tiles: both run the pilot and filter with
+                                  # the max over the ranks of the pilots' per-query keys
+    (72000, 768, 160, 0, True),   # only rank 0 runs a pilot; the exact-scanning rank joins the
+                                  # pilot-key exchange with -inf
 ])
 def test_capi_sharded_lookup_two_ranks(tmp_path, n, d, nq, mode, skew):
     import torch.multiprocessing as mp
@@ -98,6 +103,8 @@ def test_capi_sharded_lookup_two_ranks(tmp_path, n, d, nq, mode, skew):
         assert [x[:5] for x in r["dec"]] == [x[:5] for x in ref_dec]
         assert [x[5] for x in r["dec"]] == [x[5] for x in ref_dec]
     assert r0["info"][:3] == (2, 0, 2) and r1["info"][:3] == (2, 1, 2)
+    if n >= 72000 and not skew:  # the exchanged pilot keys leave every query certified
+        assert min(r0["i8_batches"], r1["i8_batches"]) >= 1 and r0["fallback"] == r1["fallback"] == 0
 
 
 def _store_worker(rank, world, port, policy, id_base, batch, out_dir):
