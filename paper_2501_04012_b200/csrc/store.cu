@@ -178,6 +178,7 @@ __global__ void __launch_bounds__(SEG_T) k_head_seg(const ScoreItem* __restrict_
 constexpr int NBIN = 4096;
 constexpr int CAP = SEG;
 constexpr int REFINE = 2 * SCORE_H;  // refine the threshold bin above this many survivors (smaller final sort)
+constexpr int RANK_MAX = 2048;       // fused kernel: survivors ranked by counting across the grid (phase F)
 
 __global__ void k_policy_keys(const DevLive* __restrict__ live, int64_t n_slots, const DevPrompt* __restrict__ prompts,
                               int policy, uint64_t now, uint64_t* __restrict__ K, unsigned long long* __restrict__ mm,
@@ -235,38 +236,60 @@ __global__ void k_policy_hist(const uint64_t* __restrict__ K, int64_t n_slots, c
 // below it.
 template <int NT = 1024>
 __device__ void block_pick(const unsigned* __restrict__ hist, unsigned need, int* bin, unsigned* at, unsigned* below) {
-  __shared__ unsigned c[NBIN];
-  __shared__ unsigned tot[NT];
+  // PER consecutive bins per thread (16-byte loads), warp-shuffle scans: three
+  // block barriers instead of a Hillis-Steele scan's 2 log2(NT)
+  constexpr int PER = NBIN / NT, NW = NT / 32;
+  static_assert(PER % 4 == 0, "block_pick: 16-byte bin loads");
+  __shared__ unsigned wtot[NW];
   __shared__ int s_bin;
-  constexpr int PER = NBIN / NT;
+  __shared__ unsigned s_at, s_below;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   unsigned loc[PER], run = 0;
+  const uint4* h4 = reinterpret_cast<const uint4*>(hist) + threadIdx.x * (PER / 4);
 #pragma unroll
-  for (int q = 0; q < PER; ++q) run += (loc[q] = hist[threadIdx.x * PER + q]);
-  tot[threadIdx.x] = run;
-  if (threadIdx.x == 0) s_bin = NBIN - 1;
-  __syncthreads();
-  for (int o = 1; o < NT; o <<= 1) {  // inclusive scan of the per-thread totals
-    const unsigned v = threadIdx.x >= o ? tot[threadIdx.x - o] : 0;
-    __syncthreads();
-    tot[threadIdx.x] += v;
-    __syncthreads();
+  for (int q = 0; q < PER / 4; ++q) {
+    const uint4 v = h4[q];
+    loc[4 * q] = v.x, loc[4 * q + 1] = v.y, loc[4 * q + 2] = v.z, loc[4 * q + 3] = v.w;
   }
-  unsigned acc = tot[threadIdx.x] - run;
 #pragma unroll
-  for (int q = 0; q < PER; ++q) {
-    acc += loc[q];
-    c[threadIdx.x * PER + q] = acc;
+  for (int q = 0; q < PER; ++q) run += loc[q];
+  unsigned inc = run;  // inclusive scan over the warp
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned v = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += v;
+  }
+  if (lane == 31) wtot[warp] = inc;
+  if (threadIdx.x == 0) {
+    s_bin = NBIN - 1;
+    s_at = 0;
+    s_below = 0;
   }
   __syncthreads();
+  unsigned wbase = 0;
+  for (int w = 0; w < warp; ++w) wbase += wtot[w];
+  if (threadIdx.x == NT - 1) {  // no bin reaches `need`: the last bin, everything below it
+    const unsigned all = wbase + inc;
+    s_at = all;
+    s_below = all - loc[PER - 1];
+  }
+  __syncthreads();
+  unsigned acc = wbase + inc - run;  // exclusive prefix of this thread's first bin
+  if (acc < need && acc + run >= need) {
 #pragma unroll
-  for (int q = 0; q < PER; ++q) {
-    const int b = threadIdx.x * PER + q;
-    if (c[b] >= need && (b == 0 || c[b - 1] < need)) s_bin = b;
+    for (int q = 0; q < PER; ++q) {
+      if (acc < need && acc + loc[q] >= need) {
+        s_bin = threadIdx.x * PER + q;
+        s_at = acc + loc[q];
+        s_below = acc;
+      }
+      acc += loc[q];
+    }
   }
   __syncthreads();
   *bin = s_bin;
-  *at = c[s_bin];
-  *below = s_bin > 0 ? c[s_bin - 1] : 0;
+  *at = s_at;
+  *below = s_below;
 }
 
 // pick[0] = threshold bin, pick[1] = survivors (cum count), pick[2] = below it
@@ -382,6 +405,7 @@ struct FusedScratch {
   ScoreItem* items;            // [CAP]
   ScoreItem* head;             // [SCORE_H] report
   int* rep;                    // [8] report: pick[5], n_out, bad (follows head)
+  unsigned long long* ts;      // [8] phase timestamps of CTA 0 (FC_SCORE_PHASES=1), else null
 };
 
 // REG: the store fits KR keys per thread of the grid, so each thread keeps
@@ -396,6 +420,16 @@ __global__ void __launch_bounds__(SEG_T, 1) k_policy_fused(const DevLive* __rest
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) uint8_t sm[];
   __shared__ int s_pick[5];
+  auto stamp = [&](int p) {
+    if (S.ts && blockIdx.x == 0 && threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      S.ts[p] = t;
+    }
+  };
+  stamp(0);
+  // survivor counter: first used in phase (E), after two grid barriers
+  if (blockIdx.x == 0 && threadIdx.x == 0) S.n_acc[0] = 0;
   const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
   uint64_t kr[REG ? KR : 1];
@@ -456,6 +490,7 @@ __global__ void __launch_bounds__(SEG_T, 1) k_policy_fused(const DevLive* __rest
     }
   }
   grid.sync();
+  stamp(1);
   const uint64_t lo = S.mm[0], hi = S.mm[1];
   const int sh = bin_shift(lo, hi);
   const int sh2 = sh > 12 ? sh - 12 : 0;
@@ -487,6 +522,7 @@ __global__ void __launch_bounds__(SEG_T, 1) k_policy_fused(const DevLive* __rest
   for (int t = threadIdx.x; t < NBIN; t += blockDim.x)
     if (h[t]) atomicAdd(&S.hist[t], h[t]);
   grid.sync();
+  stamp(2);
   // (C) pick: every CTA computes the same pick from the global histogram
   {
     int bin;
@@ -501,8 +537,10 @@ __global__ void __launch_bounds__(SEG_T, 1) k_policy_fused(const DevLive* __rest
     }
     __syncthreads();
   }
-  // (D) refine inside the threshold bin when it leaves too many survivors
-  if (s_pick[1] > REFINE) {
+  stamp(3);
+  // (D) refine inside the threshold bin when it leaves more survivors than
+  // the rank pass (F) takes (a refine costs a histogram pass and a grid barrier)
+  if (s_pick[1] > RANK_MAX) {
     for (int t = threadIdx.x; t < NBIN; t += blockDim.x) h[t] = 0;
     __syncthreads();
     const uint64_t tb = (uint64_t)s_pick[0];
@@ -524,6 +562,7 @@ __global__ void __launch_bounds__(SEG_T, 1) k_policy_fused(const DevLive* __rest
     }
     __syncthreads();
   }
+  stamp(4);
   // (E) collect the survivors
   if (s_pick[4] <= CAP) {
     const uint64_t tb = (uint64_t)s_pick[0], tb2 = (uint64_t)s_pick[3];
@@ -537,10 +576,39 @@ __global__ void __launch_bounds__(SEG_T, 1) k_policy_fused(const DevLive* __rest
     });
   }
   grid.sync();
-  if (blockIdx.x != 0) return;
-  // (F) CTA 0: sort the survivors, report, reset the scratch for the next call
+  stamp(5);
+  // (F) the head: a survivor's rank = how many survivors precede it in
+  // (key, seq, slot) order, a total order, so the ranks are a permutation.
+  // One warp per survivor over all the CTAs (up to RANK_MAX survivors, which
+  // is why (D) rarely runs), each written straight to its place: no
+  // single-CTA sort on the tail. More survivors (dense ties): CTA 0 sorts.
   const int n = min(S.n_acc[0], CAP);
-  if (s_pick[4] <= CAP) {
+  if (s_pick[4] <= CAP && n <= RANK_MAX) {
+    // survivor i: CTA i % grid, warp (i / grid) % warps; each CTA with work
+    // stages the whole survivor list in shared memory once
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int NWARP = SEG_T / 32;
+    if ((int)blockIdx.x < n) {
+      ScoreItem* si = reinterpret_cast<ScoreItem*>(sm);
+      for (int t = threadIdx.x; t < n; t += SEG_T) si[t] = S.items[t];
+      __syncthreads();
+      for (int i = blockIdx.x + gridDim.x * warp; i < n; i += gridDim.x * NWARP) {
+        const ScoreItem me = si[i];
+        int r = 0;
+#pragma unroll 4
+        for (int j = lane; j < n; j += 32) {
+          const ScoreItem o = si[j];
+          r += o.kb < me.kb || (o.kb == me.kb && (o.seq < me.seq || (o.seq == me.seq && o.slot < me.slot)));
+        }
+#pragma unroll
+        for (int off = 16; off; off >>= 1) r += __shfl_xor_sync(0xffffffffu, r, off);
+        if (lane == 0 && r < SCORE_H) S.head[r] = me;
+      }
+    }
+    for (int64_t t = n + gtid; t < SCORE_H; t += gstride) S.head[t] = ScoreItem{~0ull, ~0ull, -1};
+  }
+  if (blockIdx.x != 0) return;
+  if (s_pick[4] <= CAP && n > RANK_MAX) {
     uint64_t* kb = reinterpret_cast<uint64_t*>(sm);
     uint64_t* sq = kb + SEG;
     int64_t* sl = reinterpret_cast<int64_t*>(sq + SEG);
@@ -557,13 +625,13 @@ __global__ void __launch_bounds__(SEG_T, 1) k_policy_fused(const DevLive* __rest
     seg_sort(kb, sq, sl, n2);
     for (int t = threadIdx.x; t < SCORE_H; t += SEG_T) S.head[t] = ScoreItem{kb[t], sq[t], sl[t]};
   }
+  stamp(6);
   if (threadIdx.x < 5) S.rep[threadIdx.x] = s_pick[threadIdx.x];
   __syncthreads();
   if (threadIdx.x == 0) {
-    S.rep[5] = S.n_acc[0];
+    S.rep[5] = n;
     S.rep[6] = S.n_acc[1];
-    S.n_acc[0] = 0;
-    S.n_acc[1] = 0;
+    S.n_acc[1] = 0;  // n_acc[0] is read by every CTA after the last barrier: reset in phase (A) of the next call
     S.mm[0] = ~0ull;
     S.mm[1] = 0;
   }
@@ -681,6 +749,12 @@ struct lc_store {
     S.items = reinterpret_cast<ScoreItem*>(fs + kz + z_b);
     S.head = reinterpret_cast<ScoreItem*>(fs + kz + z_b + i_b);
     S.rep = reinterpret_cast<int*>(S.head + SCORE_H);
+    S.ts = nullptr;
+    if (getenv("FC_SCORE_PHASES") && atoi(getenv("FC_SCORE_PHASES")) == 1) {
+      static unsigned long long* ts_dev = nullptr;  // diagnostic only
+      if (!ts_dev) FC_CUDA(cudaMalloc(&ts_dev, 8 * sizeof(unsigned long long)));
+      S.ts = ts_dev;
+    }
     *rep_off = kz + z_b + i_b;
     *rep_bytes = h_b;
     (void)z_off;
@@ -822,6 +896,17 @@ struct lc_store {
       sync(ctx);
       const int* rp = reinterpret_cast<const int*>(fs_host + (size_t)SCORE_H * sizeof(ScoreItem));
       if (rp[6]) raise(LC_ERR_INVALID_ARGUMENT, "lrbu_priority: now precedes last access");
+      if (S.ts) {  // FC_SCORE_PHASES=1: mean CTA-0 phase times over the calls so far, every 4 calls
+        static double acc[6] = {0, 0, 0, 0, 0, 0};
+        static long calls = 0;
+        unsigned long long t[8];
+        FC_CUDA(cudaMemcpy(t, S.ts, sizeof(t), cudaMemcpyDeviceToHost));
+        for (int i = 0; i < 6; ++i) acc[i] += (double)(t[i + 1] - t[i]);
+        if (++calls % 4 == 0)
+          fprintf(stderr, "[score phases] %ld calls, mean ns: keys+sync %.0f | hist+sync %.0f | pick %.0f | refine %.0f | "
+                  "collect+sync %.0f | head (CTA 0) %.0f\n", calls, acc[0] / calls, acc[1] / calls,
+                  acc[2] / calls, acc[3] / calls, acc[4] / calls, acc[5] / calls);
+      }
       if (getenv("FC_TRACE") && atoi(getenv("FC_TRACE")) == 1)
         fprintf(stderr, "[score fused] slots %lld: bin %d, survivors %d (below %d), sub-bin %d -> %d%s\n",
                 (long long)n_slots, rp[0], rp[1], rp[2], rp[3], rp[4], rp[4] <= CAP ? "" : " => segmented sort");
