@@ -406,6 +406,7 @@ struct FusedScratch {
   ScoreItem* head;             // [SCORE_H] report
   int* rep;                    // [8] report: pick[5], n_out, bad (follows head)
   unsigned long long* ts;      // [8] phase timestamps of CTA 0 (FC_SCORE_PHASES=1), else null
+  int rank_max;                // survivors ranked across the grid (F) up to this; refine (D) above it
 };
 
 // REG: the store fits KR keys per thread of the grid, so each thread keeps
@@ -540,7 +541,7 @@ __global__ void __launch_bounds__(SEG_T, 1) k_policy_fused(const DevLive* __rest
   stamp(3);
   // (D) refine inside the threshold bin when it leaves more survivors than
   // the rank pass (F) takes (a refine costs a histogram pass and a grid barrier)
-  if (s_pick[1] > RANK_MAX) {
+  if (s_pick[1] > S.rank_max) {
     for (int t = threadIdx.x; t < NBIN; t += blockDim.x) h[t] = 0;
     __syncthreads();
     const uint64_t tb = (uint64_t)s_pick[0];
@@ -583,7 +584,7 @@ __global__ void __launch_bounds__(SEG_T, 1) k_policy_fused(const DevLive* __rest
   // is why (D) rarely runs), each written straight to its place: no
   // single-CTA sort on the tail. More survivors (dense ties): CTA 0 sorts.
   const int n = min(S.n_acc[0], CAP);
-  if (s_pick[4] <= CAP && n <= RANK_MAX) {
+  if (s_pick[4] <= CAP && n <= S.rank_max) {
     // survivor i: CTA i % grid, warp (i / grid) % warps; each CTA with work
     // stages the whole survivor list in shared memory once
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -608,7 +609,7 @@ __global__ void __launch_bounds__(SEG_T, 1) k_policy_fused(const DevLive* __rest
     for (int64_t t = n + gtid; t < SCORE_H; t += gstride) S.head[t] = ScoreItem{~0ull, ~0ull, -1};
   }
   if (blockIdx.x != 0) return;
-  if (s_pick[4] <= CAP && n > RANK_MAX) {
+  if (s_pick[4] <= CAP && n > S.rank_max) {
     uint64_t* kb = reinterpret_cast<uint64_t*>(sm);
     uint64_t* sq = kb + SEG;
     int64_t* sl = reinterpret_cast<int64_t*>(sq + SEG);
@@ -750,6 +751,9 @@ struct lc_store {
     S.head = reinterpret_cast<ScoreItem*>(fs + kz + z_b + i_b);
     S.rep = reinterpret_cast<int*>(S.head + SCORE_H);
     S.ts = nullptr;
+    // FC_SCORE_RANK_MAX (tests): lower it to take the refine pass and CTA 0's bitonic sort
+    const char* rm = getenv("FC_SCORE_RANK_MAX");
+    S.rank_max = rm ? std::max(0, std::min(RANK_MAX, atoi(rm))) : RANK_MAX;
     if (getenv("FC_SCORE_PHASES") && atoi(getenv("FC_SCORE_PHASES")) == 1) {
       static unsigned long long* ts_dev = nullptr;  // diagnostic only
       if (!ts_dev) FC_CUDA(cudaMalloc(&ts_dev, 8 * sizeof(unsigned long long)));

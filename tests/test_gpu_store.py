@@ -145,17 +145,20 @@ def test_priority_functions(fc):
 
 
 @pytest.mark.parametrize("policy", [0, 1, 2, 3])
-@pytest.mark.parametrize("sort_path", ["0", "1", "2", "3"])
+@pytest.mark.parametrize("sort_path", ["0", "1", "2", "3", "4", "5"])
 def test_eviction_burst_both_scoring_paths(fc, orc, synth, policy, sort_path):
     """600 evict_one at one `now` over ~1500 live steps: crosses the 256-entry
     scored head twice (re-scoring), LRBU sibling re-keys, and the radix-select
     fast path as one cooperative kernel (FC_SCORE_SORT=0, default; keys in
     registers, or "3": FC_SCORE_REG=0, keys through memory as for stores too
     large for the registers) or as 7 launches ("2": FC_SCORE_FUSED=0) vs the
-    segmented-sort path (=1)."""
+    segmented-sort path (=1). The fused kernel ranks up to 2048 survivors
+    across the grid; "4" (FC_SCORE_RANK_MAX=0) forces its refine pass and
+    CTA 0's bitonic sort, "5" (=300) mixes the two."""
     os.environ["FC_SCORE_SORT"] = "1" if sort_path == "1" else "0"
     os.environ["FC_SCORE_FUSED"] = "0" if sort_path == "2" else "1"
     os.environ["FC_SCORE_REG"] = "0" if sort_path == "3" else "1"
+    os.environ["FC_SCORE_RANK_MAX"] = {"4": "0", "5": "300"}.get(sort_path, "2048")
     try:
         ents = _tiny_entries(fc, synth, 300, policy)
         st = fc.CacheStore(1 << 40, fc.Policy(policy))
@@ -181,6 +184,7 @@ def test_eviction_burst_both_scoring_paths(fc, orc, synth, policy, sort_path):
         del os.environ["FC_SCORE_SORT"]
         del os.environ["FC_SCORE_FUSED"]
         del os.environ["FC_SCORE_REG"]
+        del os.environ["FC_SCORE_RANK_MAX"]
 
 
 def _gpu_store_worker(rank, world, port, policy, seed, out_dir):
@@ -275,3 +279,33 @@ def test_peek_matches_evict_one(fc, synth):
     for _ in range(60):
         e, k = st.peek(100)
         assert e.as_tuple() == st.evict_one(100).as_tuple()
+
+
+@pytest.mark.parametrize("policy", [1, 3])
+def test_large_store_fused_scoring_matches_segmented_sort(fc, policy):
+    """100k live steps (the bench's access pattern at 1/5 size): the first 300
+    evictions of the fused scoring kernel (grid-wide rank head; LRBU leaves
+    ~1/450 of the steps in the lowest bin, so the rank pass takes them without
+    a refine) equal those of the independent segmented-sort path."""
+    n_p, steps = 20000, [5, 10, 15, 20, 25]
+    rng = np.random.default_rng(3 + policy)
+    lat = rng.standard_normal((n_p, 5, 1, 64)).astype(np.float32)
+    om = np.zeros((n_p, 1, 8), np.uint8)
+    ents, sizes = fc.compress_batch(lat, steps, om, om, (8, 8, 1), list(range(1, n_p + 1)))
+    logs = []
+    for sort in ("0", "1"):
+        os.environ["FC_SCORE_SORT"] = sort
+        try:
+            st = fc.CacheStore(int(sizes.sum()) * 2, fc.Policy(policy))
+            for i, e in enumerate(ents):
+                st.insert_steps(i + 1, e, steps, i + 1)
+            now = n_p + 1
+            for pid in np.random.default_rng(5).integers(1, n_p + 1, n_p // 2):
+                st.get_step(int(pid), 25, now, want_latent=False)
+                now += 1
+            logs.append([tup(st.evict_one(now)) for _ in range(300)])
+            assert st.used() == st.recompute_used()
+        finally:
+            del os.environ["FC_SCORE_SORT"]
+        del st
+    assert logs[0] == logs[1]
