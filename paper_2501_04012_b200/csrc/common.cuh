@@ -216,15 +216,22 @@ struct InArg {
   }
 };
 
+void* pinned_acquire(size_t bytes);
+void pinned_release(void* p);
+
 // Output argument that may live on host or device; finish() copies back.
+// stage = true: a pageable host destination is reached through a pooled
+// pinned buffer (an async DMA instead of the driver's staged pageable copy);
+// the caller calls deliver() after its stream sync.
 template <class T>
 struct OutArg {
   T* user = nullptr;
   T* dev = nullptr;
   size_t count = 0;
   bool host = false;
+  T* pin = nullptr;
   DevBuf tmp;
-  OutArg(lc_ctx* ctx, T* p, size_t n) : user(p), count(n) {
+  OutArg(lc_ctx* ctx, T* p, size_t n, bool stage = false) : user(p), count(n) {
     if (!p || n == 0) return;
     if (is_device_ptr(p)) {
       dev = p;
@@ -232,10 +239,20 @@ struct OutArg {
       host = true;
       tmp = DevBuf(n * sizeof(T), ctx->stream);
       dev = tmp.as<T>();
+      if (stage) pin = static_cast<T*>(pinned_acquire(n * sizeof(T)));
     }
   }
+  OutArg(const OutArg&) = delete;
+  OutArg& operator=(const OutArg&) = delete;
+  ~OutArg() {
+    if (pin) pinned_release(pin);
+  }
   void finish(lc_ctx* ctx) {
-    if (host && count) FC_CUDA(cudaMemcpyAsync(user, dev, count * sizeof(T), cudaMemcpyDeviceToHost, ctx->stream));
+    if (host && count)
+      FC_CUDA(cudaMemcpyAsync(pin ? pin : user, dev, count * sizeof(T), cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  void deliver() {  // after the stream sync
+    if (pin) memcpy(user, pin, count * sizeof(T));
   }
 };
 

@@ -1557,9 +1557,9 @@ lc_status lc_index_query_topk(lc_index* ix, int kind, const float* q, int64_t n,
   lc_ctx* ctx = ix->ctx;
   DeviceGuard g(ctx->device);
   if (n == 0) return LC_OK;
-  OutArg<uint64_t> oi(ctx, out_ids, (size_t)n * k);
-  OutArg<double> os(ctx, out_scores, (size_t)n * k);
-  OutArg<int32_t> oc(ctx, out_counts, (size_t)n);
+  OutArg<uint64_t> oi(ctx, out_ids, (size_t)n * k, true);
+  OutArg<double> os(ctx, out_scores, (size_t)n * k, true);
+  OutArg<int32_t> oc(ctx, out_counts, (size_t)n, true);
   if (ix->n == 0) {  // empty table => nullopt (vindex.cpp:54)
     FC_CUDA(cudaMemsetAsync(oi.dev, 0, (size_t)n * k * sizeof(uint64_t), ctx->stream));
     FC_CUDA(cudaMemsetAsync(os.dev, 0, (size_t)n * k * sizeof(double), ctx->stream));
@@ -1572,6 +1572,9 @@ lc_status lc_index_query_topk(lc_index* ix, int kind, const float* q, int64_t n,
   os.finish(ctx);
   oc.finish(ctx);
   sync(ctx);
+  oi.deliver();
+  os.deliver();
+  oc.deliver();
   LC_API_END
 }
 
@@ -1587,7 +1590,7 @@ lc_status lc_lookup_decide(lc_index* ix, const float* qw, const float* qo, const
   const double* e = edges4 ? edges4 : def;
   DevBuf ids(3 * (size_t)n * sizeof(uint64_t), ctx->stream), sc(3 * (size_t)n * sizeof(double), ctx->stream),
       cnt(3 * (size_t)n * sizeof(int32_t), ctx->stream);
-  OutArg<lc_decision> o(ctx, out, (size_t)n);
+  OutArg<lc_decision> o(ctx, out, (size_t)n, true);
   if (ix->n == 0) {
     FC_CUDA(cudaMemsetAsync(ids.p, 0, ids.bytes, ctx->stream));
     FC_CUDA(cudaMemsetAsync(sc.p, 0, sc.bytes, ctx->stream));
@@ -1607,6 +1610,7 @@ lc_status lc_lookup_decide(lc_index* ix, const float* qw, const float* qo, const
   count_launch(ctx);
   o.finish(ctx);
   sync(ctx);
+  o.deliver();
   LC_API_END
 }
 
