@@ -1026,6 +1026,9 @@ def bench_scoring(torch, fc, ctx, args, peaks):
             "evictions_per_s": n_ev / ev_s, "insert_steps_per_s": n_p / ins_s,
             "scoring_launches": int(c_.value), "scoring_ms_per_launch": per_launch_ms,
             "scoring_ms_per_call": (tc_.value / cc_.value) if cc_.value else None,
+            "scoring_call_note": "call = device span from an event recorded before the host builds and issues the "
+                                 "cooperative launch to the end of the report readback; it includes host launch "
+                                 "latency (and any host stall in between), the kernel alone is scoring_ms_per_launch",
             "roofline": {"bound": "hbm", "kernel": "k_policy_fused (one cooperative launch: keys, radix threshold "
                                                    "select, survivor sort)",
                          "achieved": round(alg_bytes / (per_launch_ms / 1e3) / 1e9, 1) if per_launch_ms else None,
